@@ -1,0 +1,205 @@
+/*
+ * permez_b200.h -- C ABI of the B200-native PW_REL block compression path.
+ *
+ * Drop-in boundary for the reference package's compress/decompress path
+ * (arXiv 2309.09778, "permez").  The reference's interface for this path is
+ * Python (SPEC.md op signatures + transform.py); every entry point below names
+ * the reference interface it replaces.  Python binds these through ctypes in
+ * paper_2309_09778_b200/_native.py.
+ *
+ * Conventions:
+ *  - plain pointers and sizes, no torch types; device pointers are CUDA
+ *    global-memory pointers owned by the caller, `stream` is a cudaStream_t;
+ *  - the library never allocates device memory: the caller passes a workspace
+ *    of pmz_workspace_size() bytes;
+ *  - no global mutable state; weights travel by value in pmz_params;
+ *  - return value 0 or a negative PMZ_ERR_* status mapped 1:1 onto the
+ *    reference exception classes (errors.py:4-128);
+ *  - output is deterministic for any launch configuration.
+ */
+#ifndef PERMEZ_B200_H
+#define PERMEZ_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PMZ_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define PMZ_API __attribute__((visibility("default")))
+#else
+#define PMZ_API
+#endif
+
+/* status codes <-> errors.py exception classes */
+enum pmz_status {
+  PMZ_OK = 0,
+  PMZ_ERR_CONFIG = -1,                /* ConfigError            errors.py:8   */
+  PMZ_ERR_NONFINITE = -2,             /* NonFiniteInput         errors.py:18  */
+  PMZ_ERR_DEGENERATE = -3,            /* DegenerateBlock        errors.py:22  */
+  PMZ_ERR_SUBNORMAL = -4,             /* SubnormalMinimum       errors.py:26  */
+  PMZ_ERR_NONREPRESENTABLE = -5,      /* NonRepresentableFactor errors.py:32  */
+  PMZ_ERR_TOO_FEW_BLOCKS = -6,        /* TooFewBlocks           errors.py:50  */
+  PMZ_ERR_BALANCE_FLAG = -7,          /* BalanceFlagNotDequantizable :64     */
+  PMZ_ERR_DEGENERATE_ALPHABET = -8,   /* DegenerateAlphabet     errors.py:68  */
+  PMZ_ERR_UNASSIGNED = -9,            /* UnassignedCode         errors.py:72  */
+  PMZ_ERR_TRUNCATED = -10,            /* TruncatedStream        errors.py:76  */
+  PMZ_ERR_INVALID_PREFIX = -11,       /* InvalidPrefix          errors.py:80  */
+  PMZ_ERR_BAD_MAGIC = -12,            /* BadMagic               errors.py:90  */
+  PMZ_ERR_UNSUPPORTED_VERSION = -13,  /* UnsupportedVersion     errors.py:94  */
+  PMZ_ERR_CORRUPT = -14,              /* Corrupt                errors.py:98  */
+  PMZ_ERR_BALANCE_UNDERFLOW = -15,    /* BalanceUnderflow       errors.py:102 */
+  PMZ_ERR_CAPACITY = -16,             /* output buffer too small (no ref. class) */
+  PMZ_ERR_CUDA = -17,                 /* CUDA runtime failure                  */
+  PMZ_ERR_WORKSPACE = -18,            /* workspace too small                   */
+  PMZ_ERR_UNRESOLVED_ROUNDING = -19   /* CR log2/exp2 undecided (never seen)   */
+};
+
+/* Compression parameters.  Mirrors the reference parameters: b_r (--rel-error),
+ * block size (--block-size RxC), partition_rows (--partition-rows),
+ * perceptron weights (PerceptronModel), coverage target
+ * (--coverage-target).  b_a and onepbr2 are the host-evaluated scalars of
+ * transform.py:118 and :160-162 (`float(np.log2(1.0 + b_r))`,
+ * `(1.0 + b_r) ** 2`). */
+typedef struct pmz_params {
+  double b_r;
+  double b_a;
+  double onepbr2;
+  double eps0;            /* float_floor(float32) = 2^-126, transform.py:37  */
+  double repair_t;        /* repair_factor * b_r; SPEC default factor 1.5    */
+  double coverage_target; /* 0.99 default                      */
+  double slope;           /* leaky ReLU slope                  */
+  double w1[8];           /* (S+1) x H, row-major              */
+  double w2[2];           /* H                                               */
+  int32_t block_rows, block_cols, partition_rows;
+  int32_t S;              /* surface size: 3 (2-D) or 1 (1-D)   */
+  int32_t H;              /* hidden width, 2                                 */
+  int32_t m;              /* code width; 0 = select_m on validation blocks   */
+} pmz_params;
+
+/* Shard geometry: this process holds rows [0, rows) of its shard, which are
+ * global block-rows starting at `block_row0`.  Single GPU: block_row0 = 0. */
+typedef struct pmz_geom {
+  uint64_t rows, cols;
+  uint64_t block_row0;
+  uint64_t global_rows;   /* rows of the full field (header)                 */
+} pmz_geom;
+
+typedef struct pmz_result {
+  uint64_t header_bytes;  /* container header (0 when not written)           */
+  uint64_t record_bytes;  /* this shard's block records                      */
+  uint64_t nblocks, ntrivial, nbal, nrepair, ncodes;
+  uint64_t coverage[18];  /* select_m histogram (index = required m; 17 none) */
+  int32_t m;
+  int32_t max_code_len;
+  uint32_t unresolved;    /* undecided CR roundings (expected 0)             */
+  uint32_t flags;
+} pmz_result;
+
+/* Parsed container header (read_container, layout :496). */
+typedef struct pmz_header {
+  uint64_t rows, cols;
+  uint32_t block_rows, block_cols, partition_rows;
+  uint32_t version, elem, m, S, H;
+  double b_r, coverage_target, slope, w1[8], w2[2];
+  uint64_t nblocks;
+  uint64_t header_bytes;
+  uint64_t lens_offset;   /* byte offset of the 2^m code lengths             */
+} pmz_header;
+
+/* library / ABI identification */
+PMZ_API int pmz_abi_version(void);
+PMZ_API const char *pmz_status_string(int status);
+
+/* Workspace bytes for a shard.  Replaces nothing in the reference (the
+ * reference allocates implicitly through numpy). */
+PMZ_API int pmz_workspace_size(const pmz_params *p, const pmz_geom *g, uint64_t *bytes);
+
+/* Upper bound of the container bytes for a shard (header + records). */
+PMZ_API int pmz_max_container_size(const pmz_params *p, const pmz_geom *g, uint64_t *bytes);
+
+/* --- compression --------------------------------------------------------- */
+
+/* Stage 1: per-block stats + transform parameters for every block of the
+ * shard, and the select_m coverage histogram over the validation blocks the
+ * shard owns.  Replaces compute_block_stats + make_transform_params
+ * (transform.py:84-107, 138-167) and the residual part of trainer.select_m
+ * (SPEC.md:362-370).  d_val_blocks: shard-local validation block ids. */
+PMZ_API int pmz_compress_analyze(const float *d_in, const pmz_geom *g, const pmz_params *p, const int64_t *d_val_blocks,
+                         int64_t n_val, void *d_ws, uint64_t ws_bytes, void *stream);
+
+/* Device pointer of the 18 x u64 coverage histogram inside the workspace
+ * (sum it across shards before stage 2 when sharded). */
+PMZ_API uint64_t *pmz_ws_coverage(void *d_ws, const pmz_params *p, const pmz_geom *g);
+
+/* Stage 2: select_m, then compress_block + verify_and_repair for every block
+ * and the validation-code histogram of
+ * estimate_codebook. */
+PMZ_API int pmz_compress_codes(const float *d_in, const pmz_geom *g, const pmz_params *p, const int64_t *d_val_blocks,
+                       int64_t n_val, void *d_ws, uint64_t ws_bytes, void *stream);
+
+/* Device pointer of the 65536 x u64 validation histogram (sum across shards
+ * before stage 3) and of the i32 count of non-trivial validation blocks. */
+PMZ_API uint64_t *pmz_ws_histogram(void *d_ws, const pmz_params *p, const pmz_geom *g);
+
+/* Stage 3: build_codebook, encode and
+ * write_container (byte layout :496).  Writes the header at
+ * d_out[0] when write_header != 0 and this shard's block records right after
+ * it (or at d_out[0] when write_header == 0).  Synchronises `stream` and fills
+ * *res.  Returns PMZ_ERR_CAPACITY (res filled with the required sizes) when
+ * out_cap is too small. */
+PMZ_API int pmz_compress_finish(const pmz_geom *g, const pmz_params *p, int write_header, uint8_t *d_out, uint64_t out_cap,
+                        uint64_t *d_block_offsets, void *d_ws, uint64_t ws_bytes, void *stream, pmz_result *res);
+
+/* One-call single-GPU compress (cmd_compress minus ingest/training). */
+PMZ_API int pmz_compress(const float *d_in, const pmz_geom *g, const pmz_params *p, const int64_t *d_val_blocks,
+                 int64_t n_val, uint8_t *d_out, uint64_t out_cap, uint64_t *d_block_offsets, void *d_ws,
+                 uint64_t ws_bytes, void *stream, pmz_result *res);
+
+/* --- container ------------------------------------------------------------ */
+
+/* read_container header part: BadMagic / UnsupportedVersion /
+ * Corrupt.  Host memory. */
+PMZ_API int pmz_parse_header(const uint8_t *h_buf, uint64_t n, pmz_header *hdr);
+
+/* Walk the block records (host memory) and emit the byte offset of each
+ * block record (nblocks entries).  Corrupt / TruncatedStream on bad framing. */
+PMZ_API int pmz_index_blocks(const uint8_t *h_buf, uint64_t n, const pmz_header *hdr, uint64_t *h_block_offsets);
+
+/* --- decompression --------------------------------------------------------- */
+
+PMZ_API int pmz_decompress_workspace_size(const pmz_header *hdr, uint64_t *bytes);
+
+/* decompress_block for every block + inverse_map
+ * (transform.py:188-202) -> f32 grid (rows x cols).  d_buf: the container in
+ * device memory; d_block_offsets: byte offset of each block record. */
+/* b_a = float(np.log2(1.0 + hdr->b_r)), evaluated by the host as in
+ * derive_transform_params (transform.py:118). */
+PMZ_API int pmz_decompress(const uint8_t *d_buf, uint64_t n, const pmz_header *hdr, double b_a,
+                   const uint64_t *d_block_offsets, float *d_out, void *d_ws, uint64_t ws_bytes, void *stream);
+
+/* --- transform module (transform.py) on device ------------------------------ */
+
+/* Per-block transform parameters: 10 doubles per block in TransformParams
+ * field order (transform.py:61-81) + trivial flag. */
+PMZ_API int pmz_transform_params(const float *d_in, const pmz_geom *g, const pmz_params *p, double *d_params10,
+                         uint8_t *d_trivial, void *d_ws, uint64_t ws_bytes, void *stream);
+
+/* forward_map / inverse_map (transform.py:170-202) elementwise with one
+ * parameter set (TransformParams fields, transform.py:61-81). */
+PMZ_API int pmz_forward_map(const double *d_x, uint64_t n, const double *params10, double *d_v, void *stream);
+PMZ_API int pmz_inverse_map(const double *d_v, uint64_t n, const double *params10, double *d_x64, float *d_x32,
+                    void *stream);
+
+/* CR log2 of float32 values (exhaustive-check helper, see tests). Writes the
+ * double result; counts undecided roundings into *d_amb. */
+PMZ_API int pmz_log2_f32_batch(const float *d_x, uint64_t n, double *d_out, uint32_t *d_amb, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PERMEZ_B200_H */

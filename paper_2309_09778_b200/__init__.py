@@ -1,0 +1,13 @@
+"""B200-native (sm_100a) implementation of the permez block-parallel PW_REL
+compress/decompress path (arXiv 2309.09778).
+
+Public entry points mirror the reference package: ``compress`` /
+``decompress`` (pipeline), the transform module, the exception hierarchy.
+"""
+from . import errors
+from .errors import PermezError
+from .pipeline import Codec, CompressConfig, CompressInfo, compress, decompress
+from .predictor import PerceptronModel, init_model, lorenzo_coefficients
+
+__all__ = ["compress", "decompress", "Codec", "CompressConfig", "CompressInfo", "PerceptronModel", "init_model",
+           "lorenzo_coefficients", "errors", "PermezError"]

@@ -1,0 +1,634 @@
+// capi.cu -- extern "C" boundary (include/permez_b200.h): workspace layout,
+// stage launches, container header parsing and block indexing.
+// Single translation unit: all kernels are included here.
+#include <cub/device/device_scan.cuh>
+#include <cmath>
+#include <cstring>
+#include <cstdio>
+
+#include "common.cuh"
+#include "compress.cuh"
+#include "decompress.cuh"
+#include "encode.cuh"
+
+using namespace pmz;
+
+#define CK(x)                                   \
+  do {                                          \
+    cudaError_t e_ = (x);                       \
+    if (e_ != cudaSuccess) return PMZ_ERR_CUDA; \
+  } while (0)
+
+namespace {
+
+int check_params(const pmz_params *p) {
+  if (!p) return PMZ_ERR_CONFIG;
+  if (!(p->b_r > 0.0 && p->b_r < 1.0)) return PMZ_ERR_CONFIG;  // transform.py:146-147
+  if (p->block_rows <= 0 || p->block_cols <= 0 || p->partition_rows <= 0) return PMZ_ERR_CONFIG;
+  if (p->partition_rows > 32) return PMZ_ERR_CONFIG;  // one warp lane per partition row
+  if (p->block_rows / p->partition_rows > 64) return PMZ_ERR_CONFIG;
+  if (p->S != 1 && p->S != 3) return PMZ_ERR_CONFIG;
+  if (p->H != 2) return PMZ_ERR_CONFIG;
+  if (p->m != 0 && (p->m < 4 || p->m > 16)) return PMZ_ERR_CONFIG;
+  if (!(p->b_a > 0.0) || !(p->repair_t > 0.0)) return PMZ_ERR_CONFIG;
+  return PMZ_OK;
+}
+
+Geom make_geom(int64_t rows, int64_t cols, int br, int bc, int prow, int64_t block_row0) {
+  Geom g{};
+  g.rows = rows;
+  g.cols = cols;
+  g.br = br;
+  g.bc = bc;
+  g.prow = prow;
+  g.block_row0 = block_row0;
+  g.nbr = rows > 0 ? (rows + br - 1) / br : 0;
+  g.nbc = cols > 0 ? (cols + bc - 1) / bc : 0;
+  g.nblocks = g.nbr * g.nbc;
+  g.np_full = (br + prow - 1) / prow;
+  g.br_last = g.nbr > 0 ? (int)(rows - (g.nbr - 1) * br) : 0;
+  g.np_last = g.nbr > 0 ? (g.br_last + prow - 1) / prow : 0;
+  g.nparts = g.nbr > 0 ? (g.nbr - 1) * g.nbc * g.np_full + g.nbc * g.np_last : 0;
+  return g;
+}
+
+Geom geom_of(const pmz_params *p, const pmz_geom *g) {
+  return make_geom((int64_t)g->rows, (int64_t)g->cols, p->block_rows, p->block_cols, p->partition_rows,
+                   (int64_t)g->block_row0);
+}
+
+KParams kparams(const pmz_params *p) {
+  KParams k{};
+  k.b_r = p->b_r;
+  k.b_a = p->b_a;
+  k.two_ba = 2.0 * p->b_a;
+  k.onepbr2 = p->onepbr2;
+  k.eps0 = p->eps0;
+  k.repair_t = p->repair_t;
+  k.slope = p->slope;
+  k.coverage_target = p->coverage_target;
+  for (int i = 0; i < 8; i++) k.w1[i] = p->w1[i];
+  for (int i = 0; i < 2; i++) k.w2[i] = p->w2[i];
+  k.S = p->S;
+  k.H = p->H;
+  k.block_rows = p->block_rows;
+  k.block_cols = p->block_cols;
+  k.partition_rows = p->partition_rows;
+  k.m_fixed = p->m;
+  return k;
+}
+
+size_t cub_scan_bytes(int64_t n) {
+  size_t bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, bytes, (unsigned long long *)nullptr, (unsigned long long *)nullptr,
+                                (int)(n > 0 ? n : 1));
+  return bytes;
+}
+
+WsLayout compress_layout(const Geom &g) {
+  WsLayout L{};
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    size_t at = o;
+    o = align_up(o + bytes, 256);
+    return at;
+  };
+  L.status = take(sizeof(WsStatus));
+  L.cov = take(18 * 8);
+  L.hist = take((kMaxAlpha + 1) * 8);
+  L.lens = take(kMaxAlpha);
+  L.cw = take(kMaxAlpha * 4);
+  L.cb_keys = take(kMaxAlpha * 8);
+  L.cb_w = take(kMaxAlpha * 4);
+  L.cb_parent = 0;
+  L.blkp = take(sizeof(BlkP) * (size_t)(g.nblocks + 1));
+  L.part_bits = take(8 * (size_t)(g.nparts + 1));
+  L.part_zeros = take(8 * (size_t)(g.nparts + 1));
+  L.anchors = take(8 * (size_t)(g.nparts + 1));
+  L.rec_size = take(8 * (size_t)(g.nblocks + 1));
+  L.rec_off = take(8 * (size_t)(g.nblocks + 1));
+  L.cub_bytes = cub_scan_bytes(g.nblocks + 1);
+  L.cub_tmp = take(L.cub_bytes);
+  L.codes = take(2 * (size_t)(g.rows * g.cols));
+  L.balv = take(8 * (size_t)(g.rows * g.cols));
+  L.total = o;
+  return L;
+}
+
+template <class T>
+T *at(void *ws, size_t off) {
+  return reinterpret_cast<T *>(reinterpret_cast<uint8_t *>(ws) + off);
+}
+
+int err_from_bits(unsigned bits) {
+  for (int i = 1; i < 32; i++)
+    if (bits & (1u << i)) return -i;
+  return PMZ_OK;
+}
+
+int launch_check() {
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? PMZ_OK : PMZ_ERR_CUDA;
+}
+
+constexpr int kNT = 256;
+
+}  // namespace
+
+// C linkage comes from the declarations in permez_b200.h.
+
+int pmz_abi_version(void) { return PMZ_ABI_VERSION; }
+
+const char *pmz_status_string(int s) {
+  switch (s) {
+    case PMZ_OK: return "ok";
+    case PMZ_ERR_CONFIG: return "ConfigError";
+    case PMZ_ERR_NONFINITE: return "NonFiniteInput";
+    case PMZ_ERR_DEGENERATE: return "DegenerateBlock";
+    case PMZ_ERR_SUBNORMAL: return "SubnormalMinimum";
+    case PMZ_ERR_NONREPRESENTABLE: return "NonRepresentableFactor";
+    case PMZ_ERR_TOO_FEW_BLOCKS: return "TooFewBlocks";
+    case PMZ_ERR_BALANCE_FLAG: return "BalanceFlagNotDequantizable";
+    case PMZ_ERR_DEGENERATE_ALPHABET: return "DegenerateAlphabet";
+    case PMZ_ERR_UNASSIGNED: return "UnassignedCode";
+    case PMZ_ERR_TRUNCATED: return "TruncatedStream";
+    case PMZ_ERR_INVALID_PREFIX: return "InvalidPrefix";
+    case PMZ_ERR_BAD_MAGIC: return "BadMagic";
+    case PMZ_ERR_UNSUPPORTED_VERSION: return "UnsupportedVersion";
+    case PMZ_ERR_CORRUPT: return "Corrupt";
+    case PMZ_ERR_BALANCE_UNDERFLOW: return "BalanceUnderflow";
+    case PMZ_ERR_CAPACITY: return "CapacityExceeded";
+    case PMZ_ERR_CUDA: return "CudaError";
+    case PMZ_ERR_WORKSPACE: return "WorkspaceTooSmall";
+    case PMZ_ERR_UNRESOLVED_ROUNDING: return "UnresolvedRounding";
+    default: return "unknown";
+  }
+}
+
+int pmz_workspace_size(const pmz_params *p, const pmz_geom *g, uint64_t *bytes) {
+  int s = check_params(p);
+  if (s) return s;
+  *bytes = compress_layout(geom_of(p, g)).total;
+  return PMZ_OK;
+}
+
+int pmz_max_container_size(const pmz_params *p, const pmz_geom *g, uint64_t *bytes) {
+  int s = check_params(p);
+  if (s) return s;
+  Geom G = geom_of(p, g);
+  // header at m = 16 + per block fixed part + every element a balance value +
+  // every code at the 32-bit maximum length.
+  uint64_t b = header_bytes(16, p->S, p->H);
+  b += (uint64_t)G.nblocks * 25 + (uint64_t)G.nparts * 24;
+  b += (uint64_t)(G.rows * G.cols) * 12 + (uint64_t)G.nparts;
+  *bytes = b;
+  return PMZ_OK;
+}
+
+uint64_t *pmz_ws_coverage(void *d_ws, const pmz_params *p, const pmz_geom *g) {
+  return at<uint64_t>(d_ws, compress_layout(geom_of(p, g)).cov);
+}
+
+uint64_t *pmz_ws_histogram(void *d_ws, const pmz_params *p, const pmz_geom *g) {
+  return at<uint64_t>(d_ws, compress_layout(geom_of(p, g)).hist);
+}
+
+int pmz_compress_analyze(const float *d_in, const pmz_geom *g, const pmz_params *p, const int64_t *d_val,
+                         int64_t n_val, void *d_ws, uint64_t ws_bytes, void *stream) {
+  int s = check_params(p);
+  if (s) return s;
+  Geom G = geom_of(p, g);
+  WsLayout L = compress_layout(G);
+  if (ws_bytes < L.total) return PMZ_ERR_WORKSPACE;
+  cudaStream_t st = (cudaStream_t)stream;
+  KParams k = kparams(p);
+  // zero status, coverage and histogram (contiguous at the front)
+  CK(cudaMemsetAsync(d_ws, 0, L.lens, st));
+  if (G.nblocks == 0) return PMZ_OK;
+  k_block_params<kNT><<<(unsigned)G.nblocks, kNT, 0, st>>>(d_in, G, k, at<BlkP>(d_ws, L.blkp),
+                                                            at<WsStatus>(d_ws, L.status));
+  if (p->m == 0 && n_val > 0) {
+    dim3 grid(16, (unsigned)n_val);
+    k_coverage<kNT><<<grid, kNT, 0, st>>>(d_in, G, k, at<BlkP>(d_ws, L.blkp), d_val,
+                                          at<unsigned long long>(d_ws, L.cov), at<WsStatus>(d_ws, L.status));
+  }
+  return launch_check();
+}
+
+int pmz_compress_codes(const float *d_in, const pmz_geom *g, const pmz_params *p, const int64_t *d_val,
+                       int64_t n_val, void *d_ws, uint64_t ws_bytes, void *stream) {
+  int s = check_params(p);
+  if (s) return s;
+  Geom G = geom_of(p, g);
+  WsLayout L = compress_layout(G);
+  if (ws_bytes < L.total) return PMZ_ERR_WORKSPACE;
+  cudaStream_t st = (cudaStream_t)stream;
+  KParams k = kparams(p);
+  k_select_m<<<1, 32, 0, st>>>(at<unsigned long long>(d_ws, L.cov), k, at<WsStatus>(d_ws, L.status));
+  if (G.nparts > 0) {
+    unsigned grid = (unsigned)((G.nparts + kWarps - 1) / kWarps);
+    k_wavefront<kWarps><<<grid, kWarps * 32, 0, st>>>(
+        d_in, G, k, at<BlkP>(d_ws, L.blkp), at<WsStatus>(d_ws, L.status), at<uint16_t>(d_ws, L.codes),
+        at<double>(d_ws, L.balv), at<double>(d_ws, L.anchors), at<unsigned long long>(d_ws, L.part_zeros));
+  }
+  if (n_val > 0) {
+    dim3 grid(16, (unsigned)n_val);
+    k_val_hist<kNT><<<grid, kNT, 0, st>>>(G, at<BlkP>(d_ws, L.blkp), d_val, at<uint16_t>(d_ws, L.codes),
+                                          at<unsigned long long>(d_ws, L.hist));
+  }
+  return launch_check();
+}
+
+__global__ void k_block_offsets(Geom g, KParams k, int write_header, const unsigned long long *rec_off,
+                                const WsStatus *st, unsigned long long *boff) {
+  int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b > g.nblocks) return;
+  unsigned long long base = write_header ? header_bytes(st->m, k.S, k.H) : 0;
+  boff[b] = base + rec_off[b];
+}
+
+__global__ void k_finish_status(Geom g, KParams k, int write_header, const unsigned long long *rec_off,
+                                unsigned long long cap, WsStatus *st) {
+  unsigned long long hb = write_header ? header_bytes(st->m, k.S, k.H) : 0;
+  st->header_bytes = hb;
+  st->record_bytes = rec_off[g.nblocks];
+  st->total_bytes = hb + rec_off[g.nblocks];
+  if (st->total_bytes > cap) atomicOr(&st->err_bits, 1u << (-PMZ_ERR_CAPACITY));
+}
+
+int pmz_compress_finish(const pmz_geom *g, const pmz_params *p, int write_header, uint8_t *d_out, uint64_t out_cap,
+                        uint64_t *d_block_offsets, void *d_ws, uint64_t ws_bytes, void *stream, pmz_result *res) {
+  int s = check_params(p);
+  if (s) return s;
+  Geom G = geom_of(p, g);
+  WsLayout L = compress_layout(G);
+  if (ws_bytes < L.total) return PMZ_ERR_WORKSPACE;
+  cudaStream_t st = (cudaStream_t)stream;
+  KParams k = kparams(p);
+  WsStatus *S = at<WsStatus>(d_ws, L.status);
+  CK(cudaFuncSetAttribute(k_codebook, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * 12));
+  k_codebook<<<1, 1024, 8192 * 12, st>>>(at<unsigned long long>(d_ws, L.hist), S,
+                                         at<unsigned long long>(d_ws, L.cb_keys), at<unsigned>(d_ws, L.cb_w),
+                                         at<uint8_t>(d_ws, L.lens), at<unsigned>(d_ws, L.cw));
+  if (G.nparts > 0) {
+    unsigned grid = (unsigned)((G.nparts + kWarps - 1) / kWarps);
+    k_part_bits<kWarps><<<grid, kWarps * 32, 0, st>>>(G, at<BlkP>(d_ws, L.blkp), at<uint16_t>(d_ws, L.codes),
+                                                      at<uint8_t>(d_ws, L.lens),
+                                                      at<unsigned long long>(d_ws, L.part_bits));
+  }
+  k_block_sizes<<<(unsigned)((G.nblocks + 1 + 255) / 256), 256, 0, st>>>(
+      G, at<BlkP>(d_ws, L.blkp), at<unsigned long long>(d_ws, L.part_bits),
+      at<unsigned long long>(d_ws, L.part_zeros), at<unsigned long long>(d_ws, L.rec_size));
+  size_t cb = L.cub_bytes;
+  CK(cub::DeviceScan::ExclusiveSum(at<void>(d_ws, L.cub_tmp), cb, at<unsigned long long>(d_ws, L.rec_size),
+                                   at<unsigned long long>(d_ws, L.rec_off), (int)(G.nblocks + 1), st));
+  k_finish_status<<<1, 1, 0, st>>>(G, k, write_header, at<unsigned long long>(d_ws, L.rec_off), out_cap, S);
+  // size check on the host: the writers need the final offsets anyway
+  WsStatus hs;
+  CK(cudaMemcpyAsync(&hs, S, sizeof(WsStatus), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (res) {
+    memset(res, 0, sizeof(*res));
+    res->header_bytes = hs.header_bytes;
+    res->record_bytes = hs.record_bytes;
+    res->nblocks = (uint64_t)G.nblocks;
+    res->ntrivial = hs.ntrivial;
+    res->nbal = hs.nbal;
+    res->nrepair = hs.nrepair;
+    res->ncodes = hs.ncodes;
+    res->m = hs.m;
+    res->max_code_len = hs.max_len;
+    res->unresolved = hs.unresolved;
+    CK(cudaMemcpy(res->coverage, at<uint64_t>(d_ws, L.cov), 18 * 8, cudaMemcpyDeviceToHost));
+  }
+  int err = err_from_bits(hs.err_bits);
+  if (err) return err;
+  if (hs.unresolved) return PMZ_ERR_UNRESOLVED_ROUNDING;
+  if (d_out == nullptr) return PMZ_ERR_CAPACITY;
+  unsigned long long rec_base = hs.header_bytes;
+  if (write_header)
+    k_write_header<<<1, 256, 0, st>>>(d_out, G, k, g->global_rows, at<uint8_t>(d_ws, L.lens), S);
+  if (G.nblocks > 0)
+    k_write_records<kWarps><<<(unsigned)G.nblocks, kWarps * 32, 0, st>>>(
+        G, at<BlkP>(d_ws, L.blkp), at<uint16_t>(d_ws, L.codes), at<double>(d_ws, L.balv),
+        at<double>(d_ws, L.anchors), at<unsigned long long>(d_ws, L.part_bits),
+        at<unsigned long long>(d_ws, L.part_zeros), at<unsigned long long>(d_ws, L.rec_off),
+        at<uint8_t>(d_ws, L.lens), at<unsigned>(d_ws, L.cw), d_out, rec_base);
+  if (d_block_offsets)
+    k_block_offsets<<<(unsigned)((G.nblocks + 1 + 255) / 256), 256, 0, st>>>(
+        G, k, write_header, at<unsigned long long>(d_ws, L.rec_off), S, (unsigned long long *)d_block_offsets);
+  s = launch_check();
+  if (s) return s;
+  CK(cudaStreamSynchronize(st));
+  CK(cudaMemcpy(&hs, S, sizeof(WsStatus), cudaMemcpyDeviceToHost));
+  err = err_from_bits(hs.err_bits);
+  if (err) return err;
+  return PMZ_OK;
+}
+
+int pmz_compress(const float *d_in, const pmz_geom *g, const pmz_params *p, const int64_t *d_val, int64_t n_val,
+                 uint8_t *d_out, uint64_t out_cap, uint64_t *d_block_offsets, void *d_ws, uint64_t ws_bytes,
+                 void *stream, pmz_result *res) {
+  int s = pmz_compress_analyze(d_in, g, p, d_val, n_val, d_ws, ws_bytes, stream);
+  if (s) return s;
+  s = pmz_compress_codes(d_in, g, p, d_val, n_val, d_ws, ws_bytes, stream);
+  if (s) return s;
+  return pmz_compress_finish(g, p, 1, d_out, out_cap, d_block_offsets, d_ws, ws_bytes, stream, res);
+}
+
+// ---------------------------------------------------------------------------
+// container header / index (host)
+
+namespace {
+struct HReader {
+  const uint8_t *b;
+  uint64_t n, pos;
+  bool err;
+  bool get(void *d, uint64_t k) {
+    if (err || pos + k > n) { err = true; return false; }
+    memcpy(d, b + pos, k);
+    pos += k;
+    return true;
+  }
+  template <class T>
+  T v() {
+    T x{};
+    get(&x, sizeof(T));
+    return x;
+  }
+};
+}  // namespace
+
+int pmz_parse_header(const uint8_t *h, uint64_t n, pmz_header *hd) {
+  memset(hd, 0, sizeof(*hd));
+  HReader r{h, n, 0, false};
+  char mg[4];
+  if (!r.get(mg, 4)) return PMZ_ERR_CORRUPT;
+  if (memcmp(mg, "PMEZ", 4) != 0) return PMZ_ERR_BAD_MAGIC;
+  hd->version = r.v<uint16_t>();
+  if (r.err) return PMZ_ERR_CORRUPT;
+  if (hd->version != 1) return PMZ_ERR_UNSUPPORTED_VERSION;
+  hd->elem = r.v<uint8_t>();
+  hd->rows = r.v<uint64_t>();
+  hd->cols = r.v<uint64_t>();
+  hd->block_rows = r.v<uint32_t>();
+  hd->block_cols = r.v<uint32_t>();
+  hd->partition_rows = r.v<uint32_t>();
+  hd->b_r = r.v<double>();
+  hd->coverage_target = r.v<double>();
+  hd->m = r.v<uint8_t>();
+  uint64_t ml = r.v<uint64_t>();
+  if (r.err) return PMZ_ERR_CORRUPT;
+  if (hd->elem != 0) return PMZ_ERR_CORRUPT;
+  if (hd->m < 4 || hd->m > 16 || hd->block_rows == 0 || hd->block_cols == 0 || hd->partition_rows == 0 ||
+      hd->partition_rows > 32 || hd->block_rows / hd->partition_rows > 64)
+    return PMZ_ERR_CORRUPT;
+  if (!(hd->b_r > 0.0 && hd->b_r < 1.0)) return PMZ_ERR_CORRUPT;
+  hd->S = r.v<uint32_t>();
+  hd->H = r.v<uint32_t>();
+  hd->slope = r.v<double>();
+  if (r.err || hd->H != 2 || (hd->S != 1 && hd->S != 3)) return PMZ_ERR_CORRUPT;
+  uint32_t nw1 = (hd->S + 1) * hd->H;
+  if (ml != model_blob_bytes(hd->S, hd->H)) return PMZ_ERR_CORRUPT;
+  for (uint32_t i = 0; i < nw1; i++) hd->w1[i] = r.v<double>();
+  for (uint32_t i = 0; i < hd->H; i++) hd->w2[i] = r.v<double>();
+  uint64_t cl = r.v<uint64_t>();
+  uint64_t alpha = 1ull << hd->m;
+  if (r.err || cl != 2 + alpha) return PMZ_ERR_CORRUPT;
+  uint16_t a16 = r.v<uint16_t>();
+  if (a16 != (uint16_t)(alpha & 0xffff)) return PMZ_ERR_CORRUPT;
+  hd->lens_offset = r.pos;
+  r.pos += alpha;
+  hd->nblocks = r.v<uint64_t>();
+  if (r.err) return PMZ_ERR_CORRUPT;
+  uint64_t nb = (hd->rows && hd->cols)
+                    ? ((hd->rows + hd->block_rows - 1) / hd->block_rows) * ((hd->cols + hd->block_cols - 1) / hd->block_cols)
+                    : 0;
+  if (hd->nblocks != nb) return PMZ_ERR_CORRUPT;
+  hd->header_bytes = r.pos;
+  return PMZ_OK;
+}
+
+int pmz_index_blocks(const uint8_t *h, uint64_t n, const pmz_header *hd, uint64_t *offs) {
+  Geom G = make_geom((int64_t)hd->rows, (int64_t)hd->cols, (int)hd->block_rows, (int)hd->block_cols,
+                     (int)hd->partition_rows, 0);
+  uint64_t pos = hd->header_bytes;
+  for (int64_t b = 0; b < G.nblocks; b++) {
+    if (pos >= n) return PMZ_ERR_TRUNCATED;
+    offs[b] = pos;
+    uint8_t t = h[pos];
+    if (t == 1) { pos += 1; continue; }
+    if (t != 0) return PMZ_ERR_CORRUPT;
+    BlockBox bb = block_box(G, b);
+    uint64_t head = 25 + 24ull * bb.np;
+    if (pos + head > n) return PMZ_ERR_TRUNCATED;
+    uint64_t pay = 0;
+    for (int i = 0; i < bb.np; i++) {
+      uint64_t off, len;
+      memcpy(&off, h + pos + 17 + 24ull * i, 8);
+      memcpy(&len, h + pos + 25 + 24ull * i, 8);
+      if (off != pay * 8) return PMZ_ERR_CORRUPT;
+      if (len > 40ull * bb.br * bb.bc) return PMZ_ERR_CORRUPT;
+      pay += (len + 7) / 8;
+    }
+    uint64_t nb;
+    memcpy(&nb, h + pos + 17 + 24ull * bb.np, 8);
+    if (nb > (uint64_t)bb.br * bb.bc) return PMZ_ERR_CORRUPT;
+    pos += head + 8 * nb + pay;
+    if (pos > n) return PMZ_ERR_TRUNCATED;
+  }
+  if (pos != n) return PMZ_ERR_CORRUPT;
+  if (G.nblocks >= 0) offs[G.nblocks] = pos;
+  return PMZ_OK;
+}
+
+// ---------------------------------------------------------------------------
+// decompression
+
+namespace {
+struct DecLayout {
+  size_t status, blkp, part_bits, part_off, part_zeros, anchors, bal_off, pay_off, blk_nbal, tab, sym, lut, codes,
+      total;
+};
+DecLayout dec_layout(const Geom &g) {
+  DecLayout L{};
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    size_t a = o;
+    o = align_up(o + bytes, 256);
+    return a;
+  };
+  L.status = take(sizeof(WsStatus));
+  L.blkp = take(sizeof(BlkP) * (size_t)(g.nblocks + 1));
+  L.part_bits = take(8 * (size_t)(g.nparts + 1));
+  L.part_off = take(8 * (size_t)(g.nparts + 1));
+  L.part_zeros = take(8 * (size_t)(g.nparts + 1));
+  L.anchors = take(8 * (size_t)(g.nparts + 1));
+  L.bal_off = take(8 * (size_t)(g.nblocks + 1));
+  L.pay_off = take(8 * (size_t)(g.nblocks + 1));
+  L.blk_nbal = take(8 * (size_t)(g.nblocks + 1));
+  L.tab = take(sizeof(DecTab));
+  L.sym = take(2 * kMaxAlpha);
+  L.lut = take(4 << kLutBits);
+  L.codes = take(2 * (size_t)(g.rows * g.cols));
+  L.total = o;
+  return L;
+}
+Geom hdr_geom(const pmz_header *h) {
+  return make_geom((int64_t)h->rows, (int64_t)h->cols, (int)h->block_rows, (int)h->block_cols,
+                   (int)h->partition_rows, 0);
+}
+KParams hdr_kparams(const pmz_header *h, double b_a) {
+  KParams k{};
+  k.b_r = h->b_r;
+  k.b_a = b_a;
+  k.two_ba = 2.0 * b_a;
+  k.eps0 = 0x1p-126;
+  k.slope = h->slope;
+  for (int i = 0; i < 8; i++) k.w1[i] = h->w1[i];
+  for (int i = 0; i < 2; i++) k.w2[i] = h->w2[i];
+  k.S = (int)h->S;
+  k.H = (int)h->H;
+  k.block_rows = (int)h->block_rows;
+  k.block_cols = (int)h->block_cols;
+  k.partition_rows = (int)h->partition_rows;
+  k.m_fixed = (int)h->m;
+  return k;
+}
+}  // namespace
+
+int pmz_decompress_workspace_size(const pmz_header *hdr, uint64_t *bytes) {
+  *bytes = dec_layout(hdr_geom(hdr)).total;
+  return PMZ_OK;
+}
+
+int pmz_decompress(const uint8_t *d_buf, uint64_t n, const pmz_header *hdr, double b_a, const uint64_t *d_boff,
+                   float *d_out, void *d_ws, uint64_t ws_bytes, void *stream) {
+  Geom G = hdr_geom(hdr);
+  DecLayout L = dec_layout(G);
+  if (ws_bytes < L.total) return PMZ_ERR_WORKSPACE;
+  if (!(b_a > 0.0)) return PMZ_ERR_CONFIG;
+  cudaStream_t st = (cudaStream_t)stream;
+  KParams k = hdr_kparams(hdr, b_a);
+  WsStatus *S = at<WsStatus>(d_ws, L.status);
+  CK(cudaMemsetAsync(S, 0, sizeof(WsStatus), st));
+  if (G.nblocks > 0) {
+    k_dec_blocks<<<(unsigned)((G.nblocks + 127) / 128), 128, 0, st>>>(
+        d_buf, n, G, k, (const unsigned long long *)d_boff, at<BlkP>(d_ws, L.blkp),
+        at<unsigned long long>(d_ws, L.part_bits), at<unsigned long long>(d_ws, L.part_off),
+        at<double>(d_ws, L.anchors), at<unsigned long long>(d_ws, L.bal_off),
+        at<unsigned long long>(d_ws, L.pay_off), at<unsigned long long>(d_ws, L.blk_nbal), S);
+    k_dec_tables<<<1, 1024, 0, st>>>(d_buf + hdr->lens_offset, (int)hdr->m, at<DecTab>(d_ws, L.tab),
+                                     at<uint16_t>(d_ws, L.sym), at<unsigned>(d_ws, L.lut), S);
+    unsigned grid = (unsigned)((G.nparts + kWarps - 1) / kWarps);
+    k_decode<kWarps><<<grid, kWarps * 32, 0, st>>>(
+        d_buf, G, at<BlkP>(d_ws, L.blkp), at<DecTab>(d_ws, L.tab), at<uint16_t>(d_ws, L.sym),
+        at<unsigned>(d_ws, L.lut), at<unsigned long long>(d_ws, L.part_bits),
+        at<unsigned long long>(d_ws, L.part_off), at<unsigned long long>(d_ws, L.pay_off),
+        at<uint16_t>(d_ws, L.codes), at<unsigned long long>(d_ws, L.part_zeros), S);
+    k_reconstruct<kWarps><<<grid, kWarps * 32, 0, st>>>(
+        d_buf, G, k, (int)hdr->m, at<BlkP>(d_ws, L.blkp), at<uint16_t>(d_ws, L.codes), at<double>(d_ws, L.anchors),
+        at<unsigned long long>(d_ws, L.part_zeros), at<unsigned long long>(d_ws, L.bal_off),
+        at<unsigned long long>(d_ws, L.blk_nbal), d_out, S);
+  }
+  int s = launch_check();
+  if (s) return s;
+  WsStatus hs;
+  CK(cudaMemcpyAsync(&hs, S, sizeof(WsStatus), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  s = err_from_bits(hs.err_bits);
+  if (s) return s;
+  if (hs.unresolved) return PMZ_ERR_UNRESOLVED_ROUNDING;
+  return PMZ_OK;
+}
+
+// ---------------------------------------------------------------------------
+// transform module entry points
+
+__global__ void k_params10(Geom g, const BlkP *blkp, KParams k, double *out, uint8_t *triv) {
+  int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= g.nblocks) return;
+  BlkP P = blkp[b];
+  double *o = out + 10 * b;
+  o[0] = P.factor_pos; o[1] = P.factor_neg; o[2] = k.eps0; o[3] = k.b_r; o[4] = k.b_a;
+  o[5] = P.boundary; o[6] = P.zero_code; o[7] = P.zero_threshold; o[8] = P.lg_pos; o[9] = P.lg_neg;
+  triv[b] = (uint8_t)P.trivial;
+}
+
+int pmz_transform_params(const float *d_in, const pmz_geom *g, const pmz_params *p, double *d_params10,
+                         uint8_t *d_trivial, void *d_ws, uint64_t ws_bytes, void *stream) {
+  int s = check_params(p);
+  if (s) return s;
+  Geom G = geom_of(p, g);
+  WsLayout L = compress_layout(G);
+  if (ws_bytes < L.total) return PMZ_ERR_WORKSPACE;
+  cudaStream_t st = (cudaStream_t)stream;
+  KParams k = kparams(p);
+  CK(cudaMemsetAsync(d_ws, 0, L.lens, st));
+  if (G.nblocks == 0) return PMZ_OK;
+  k_block_params<kNT><<<(unsigned)G.nblocks, kNT, 0, st>>>(d_in, G, k, at<BlkP>(d_ws, L.blkp),
+                                                            at<WsStatus>(d_ws, L.status));
+  k_params10<<<(unsigned)((G.nblocks + 127) / 128), 128, 0, st>>>(G, at<BlkP>(d_ws, L.blkp), k, d_params10,
+                                                                  d_trivial);
+  s = launch_check();
+  if (s) return s;
+  WsStatus hs;
+  CK(cudaMemcpyAsync(&hs, at<WsStatus>(d_ws, L.status), sizeof(WsStatus), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return err_from_bits(hs.err_bits);
+}
+
+struct P10 { double v[10]; };
+
+__global__ void k_forward(const double *x, uint64_t n, P10 q, double *v, unsigned *amb) {
+  uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double xi = x[i];
+  if (xi == 0.0) { v[i] = q.v[6]; return; }
+  double a = fabs(xi), lg;
+  float af = (float)a;
+  if ((double)af == a && af >= 1.17549435e-38f && isfinite(af)) lg = pmz_log2_f32(a, amb);
+  else if (a >= 0x1p-1022 && isfinite(a)) lg = pmz_log2_d(a, amb);
+  else lg = log2(a);  // subnormal doubles / inf: outside the path's domain
+  v[i] = xi > 0.0 ? __dadd_rn(lg, q.v[8]) : __dadd_rn(lg, q.v[9]);
+}
+
+__global__ void k_inverse(const double *v, uint64_t n, P10 q, double *x64, float *x32, unsigned *amb) {
+  uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double vi = v[i], r;
+  if (vi <= q.v[7]) r = 0.0;
+  else if (vi > q.v[5]) r = -pmz_exp2_cr(__dsub_rn(vi, q.v[9]), amb);
+  else r = pmz_exp2_cr(__dsub_rn(vi, q.v[8]), amb);
+  if (x64) x64[i] = r;
+  if (x32) x32[i] = __double2float_rn(r);
+}
+
+int pmz_forward_map(const double *d_x, uint64_t n, const double *params10, double *d_v, void *stream) {
+  P10 q;
+  memcpy(q.v, params10, sizeof(q.v));
+  if (n == 0) return PMZ_OK;
+  k_forward<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(d_x, n, q, d_v, nullptr);
+  return launch_check();
+}
+
+int pmz_inverse_map(const double *d_v, uint64_t n, const double *params10, double *d_x64, float *d_x32,
+                    void *stream) {
+  P10 q;
+  memcpy(q.v, params10, sizeof(q.v));
+  if (n == 0) return PMZ_OK;
+  k_inverse<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(d_v, n, q, d_x64, d_x32, nullptr);
+  return launch_check();
+}
+
+__global__ void k_log2_batch(const float *x, uint64_t n, double *out, unsigned *amb) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = pmz_log2_f32((double)x[i], amb);
+}
+
+int pmz_log2_f32_batch(const float *d_x, uint64_t n, double *d_out, uint32_t *d_amb, void *stream) {
+  if (n == 0) return PMZ_OK;
+  k_log2_batch<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(d_x, n, d_out, d_amb);
+  return launch_check();
+}
+

@@ -1,0 +1,154 @@
+// common.cuh -- shared device types: geometry, per-block parameters, predictor,
+// quantizer, workspace layout.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "../../include/permez_b200.h"
+#include "dmath.cuh"
+
+namespace pmz {
+
+constexpr int kMaxAlpha = 1 << 16;
+constexpr int kWarps = 4;  // warps per CTA for per-partition kernels
+
+// Kernel-parameter copy of pmz_params (passed by value -> constant bank).
+struct KParams {
+  double b_r, b_a, two_ba, onepbr2, eps0, repair_t, slope, coverage_target;
+  double w1[8], w2[2];
+  int S, H, block_rows, block_cols, partition_rows, m_fixed;
+};
+
+// Shard geometry (derived).
+struct Geom {
+  int64_t rows, cols;        // shard rows, cols
+  int64_t nbr, nbc, nblocks; // block grid of the shard
+  int64_t block_row0;        // global block-row of the shard's first block-row
+  int br, bc, prow;          // block rows/cols, partition rows
+  int np_full, np_last;      // partitions per block (full / last block-row)
+  int64_t nparts;
+  int br_last;               // rows of the last block-row
+};
+
+// Per-block transform parameters (TransformParams fields, transform.py:61-81).
+struct BlkP {
+  double factor_pos, factor_neg, lg_pos, lg_neg, zero_code, zero_threshold, boundary;
+  int trivial;
+  int pad;
+};
+
+struct BlockBox { int64_t r0, c0; int br, bc, np; };
+
+__host__ __device__ inline BlockBox block_box(const Geom &g, int64_t b) {
+  BlockBox bb;
+  int64_t bi = b / g.nbc, bj = b - bi * g.nbc;
+  bb.r0 = bi * g.br;
+  bb.c0 = bj * g.bc;
+  int64_t rr = g.rows - bb.r0, cc = g.cols - bb.c0;
+  bb.br = (int)(rr < g.br ? rr : g.br);
+  bb.bc = (int)(cc < g.bc ? cc : g.bc);
+  bb.np = (bb.br + g.prow - 1) / g.prow;
+  return bb;
+}
+
+// global partition id -> (block, local partition)
+__host__ __device__ inline void part_of(const Geom &g, int64_t p, int64_t &b, int &pi) {
+  int64_t nfull = (g.nbr - 1) * g.nbc * g.np_full;
+  if (p < nfull) { b = p / g.np_full; pi = (int)(p - b * g.np_full); }
+  else { int64_t q = p - nfull; b = (g.nbr - 1) * g.nbc + q / g.np_last; pi = (int)(q % g.np_last); }
+}
+// first global partition id of block b
+__host__ __device__ inline int64_t first_part(const Geom &g, int64_t b) {
+  int64_t nfullb = (g.nbr - 1) * g.nbc;
+  if (b < nfullb) return b * g.np_full;
+  return nfullb * g.np_full + (b - nfullb) * g.np_last;
+}
+
+// predict with the D3 evaluation order and no contraction.
+__device__ __forceinline__ double predict(const KParams &k, double s0, double s1, double s2) {
+  double a0, a1;
+  if (k.S == 3) {
+    double h0 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(s0, k.w1[0]), __dmul_rn(s1, k.w1[2])), __dmul_rn(s2, k.w1[4])),
+                          k.w1[6]);
+    double h1 = __dadd_rn(__dadd_rn(__dadd_rn(__dmul_rn(s0, k.w1[1]), __dmul_rn(s1, k.w1[3])), __dmul_rn(s2, k.w1[5])),
+                          k.w1[7]);
+    a0 = h0 < 0.0 ? __dmul_rn(k.slope, h0) : h0;
+    a1 = h1 < 0.0 ? __dmul_rn(k.slope, h1) : h1;
+  } else {
+    double h0 = __dadd_rn(__dmul_rn(s0, k.w1[0]), k.w1[2]);
+    double h1 = __dadd_rn(__dmul_rn(s0, k.w1[1]), k.w1[3]);
+    a0 = h0 < 0.0 ? __dmul_rn(k.slope, h0) : h0;
+    a1 = h1 < 0.0 ? __dmul_rn(k.slope, h1) : h1;
+  }
+  return __dadd_rn(__dmul_rn(a0, k.w2[0]), __dmul_rn(a1, k.w2[1]));
+}
+
+// quantize (D5): center + round_half_away(err / (2 b_a)).
+__device__ __forceinline__ int quantize(double err, double two_ba, int m) {
+  double q = __ddiv_rn(err, two_ba);
+  double c = __dadd_rn((double)(1 << (m - 1)), round(q));
+  if (c >= 1.0 && c <= (double)((1 << m) - 1)) return (int)c;
+  return 0;
+}
+// smallest m in [4,16] covering round(q); 17 = none (select_m)
+__device__ __forceinline__ int m_required(double err, double two_ba) {
+  double a = fabs(round(__ddiv_rn(err, two_ba)));
+#pragma unroll 1
+  for (int m = 4; m <= 16; m++)
+    if (a <= (double)((1 << (m - 1)) - 1)) return m;
+  return 17;
+}
+// dequantize (D6)
+__device__ __forceinline__ double dequantize(int code, double two_ba, int m) {
+  return __dmul_rn((double)(code - (1 << (m - 1))), two_ba);
+}
+
+// zero_sub_floor_magnitudes (transform.py:205-210) on one f32 element.
+__device__ __forceinline__ float zfloor(float x) {
+  return fabsf(x) <= 1.17549435e-38f ? 0.0f : x;
+}
+
+// forward_map (transform.py:170-185) of a zero-floored f32 element.
+__device__ __forceinline__ double fwd(float xz, const BlkP &p, unsigned *amb) {
+  if (xz == 0.0f) return p.zero_code;
+  double lg = pmz_log2_f32((double)fabsf(xz), amb);
+  return xz > 0.0f ? __dadd_rn(lg, p.lg_pos) : __dadd_rn(lg, p.lg_neg);
+}
+
+// inverse_map (transform.py:188-202) + f32 cast (D20).
+__device__ __forceinline__ float inv_f32(double v, const BlkP &p, unsigned *amb) {
+  if (v <= p.zero_threshold) return 0.0f;
+  if (v > p.boundary) return -pmz_exp2_to_f32(__dsub_rn(v, p.lg_neg), amb);
+  return pmz_exp2_to_f32(__dsub_rn(v, p.lg_pos), amb);
+}
+
+// D8 violation test on the emitted f32 value.
+__device__ __forceinline__ bool violates(float xh, float xz, double t) {
+  if (xz == 0.0f) return xh != 0.0f;
+  double d = fabs(__dsub_rn((double)xh, (double)xz));
+  return __ddiv_rn(d, fabs((double)xz)) > t;
+}
+
+// ---------------------------------------------------------------------------
+// workspace layout
+
+struct WsStatus {
+  unsigned err_bits;     // PMZ error bitmask (1 << -status)
+  unsigned unresolved;   // undecided roundings
+  int m;                 // selected code width
+  int max_len;           // max codeword length
+  int n_val_nontrivial;  // k for the histogram floor (D10)
+  int pad[3];
+  unsigned long long nbal, nrepair, ntrivial, ncodes;
+  unsigned long long total_bytes, header_bytes, record_bytes;
+  unsigned long long pad2;
+};
+
+struct WsLayout {
+  size_t status, cov, hist, lens, cw, cb_keys, cb_w, cb_parent, blkp, part_bits, part_zeros, anchors, rec_size,
+      rec_off, cub_tmp, codes, balv, total;
+  size_t cub_bytes;
+};
+
+__host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+}  // namespace pmz

@@ -1,0 +1,200 @@
+// dmath.cuh -- correctly rounded log2 / exp2 on sm_100a FP64 pipes.
+//
+// The reference evaluates the transform with numpy in float64
+// (transform.py:95-98, 118-123, 177-182, 195-199).  This repo pins np.log2 /
+// np.exp2 to their correctly rounded (CR) values (decision D22);
+// the CPU oracle does the same with long double / __float128 arithmetic, so
+// GPU and oracle agree bit for bit.
+//
+//  * pmz_log2_f32(x):   CR log2 of a positive normal float (as double).
+//    Table + double-double Horner (~2^-88 abs error), ambiguity test against a
+//    2^-80 relative bound, exact-path fallback with an all-double-double series.
+//  * pmz_log2_d(x):     CR log2 of any positive normal double (slow path;
+//    per-block scalars only: lg_pos/lg_neg/log2(factor_pos - eps0)).
+//  * pmz_inv_f32(y):    (float)CR64(2^y)  -- the f32 cast of the CR double
+//    exp2, exactly what inverse_map(..).astype(float32) produces.
+#pragma once
+#include <cstdint>
+#include "dmath_tables.cuh"
+
+namespace pmz {
+
+struct dd { double hi, lo; };
+
+__device__ __forceinline__ dd two_sum(double a, double b) {
+  double s = __dadd_rn(a, b);
+  double bb = __dsub_rn(s, a);
+  double e = __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb));
+  return {s, e};
+}
+__device__ __forceinline__ dd fast_two_sum(double a, double b) {  // |a| >= |b|
+  double s = __dadd_rn(a, b);
+  double e = __dsub_rn(b, __dsub_rn(s, a));
+  return {s, e};
+}
+__device__ __forceinline__ dd two_prod(double a, double b) {
+  double p = __dmul_rn(a, b);
+  double e = __fma_rn(a, b, -p);
+  return {p, e};
+}
+__device__ __forceinline__ dd dd_add(dd a, dd b) {
+  dd s = two_sum(a.hi, b.hi);
+  dd t = two_sum(a.lo, b.lo);
+  s.lo = __dadd_rn(s.lo, t.hi);
+  s = fast_two_sum(s.hi, s.lo);
+  s.lo = __dadd_rn(s.lo, t.lo);
+  return fast_two_sum(s.hi, s.lo);
+}
+__device__ __forceinline__ dd dd_mul(dd a, dd b) {
+  dd p = two_prod(a.hi, b.hi);
+  p.lo = __fma_rn(a.hi, b.lo, p.lo);
+  p.lo = __fma_rn(a.lo, b.hi, p.lo);
+  return fast_two_sum(p.hi, p.lo);
+}
+__device__ __forceinline__ dd dd_mul_d(dd a, double b) {
+  dd p = two_prod(a.hi, b);
+  p.lo = __fma_rn(a.lo, b, p.lo);
+  return fast_two_sum(p.hi, p.lo);
+}
+
+// RN(x) is certain when every value in [x - B, x + B] rounds to r.hi.
+__device__ __forceinline__ bool dd_round_certain(dd r, double B) {
+  double lo = __dadd_rn(r.hi, __dsub_rn(r.lo, B));
+  double hi = __dadd_rn(r.hi, __dadd_rn(r.lo, B));
+  return lo == r.hi && hi == r.hi;
+}
+
+// decompose a positive normal double: x = 2^e * m, m in [0.75, 1.5); returns
+// table index i in [0, 96] (center 1 + (i-32)/128).
+__device__ __forceinline__ int log2_split(double x, double &m, int &e) {
+  long long b = __double_as_longlong(x);
+  e = (int)((b >> 52) & 0x7ff) - 1023;
+  long long mb = (b & 0x000fffffffffffffLL) | 0x3ff0000000000000LL;
+  m = __longlong_as_double(mb);
+  if (m >= 1.5) { m = __dmul_rn(m, 0.5); e += 1; }
+  int i = __double2int_rn(__dmul_rn(__dsub_rn(m, 1.0), 128.0));
+  return i + 32;
+}
+
+// Series S(r) = log2(1 + r) with r given as a double-double; all terms dd.
+__device__ __noinline__ dd log2_series_dd(dd r, int nterms) {
+  dd a = {pmz_log2_k_hi[nterms - 1], pmz_log2_k_lo[nterms - 1]};
+  for (int n = nterms - 2; n >= 0; --n) {
+    a = dd_mul(a, r);
+    a = dd_add(a, dd{pmz_log2_k_hi[n], pmz_log2_k_lo[n]});
+  }
+  return dd_mul(a, r);
+}
+
+// Slow, general path: x any positive normal double.  |error| ~ 2^-100 |log2 x|.
+__device__ __noinline__ dd log2_dd_general(double x) {
+  double m; int e;
+  int i = log2_split(x, m, e);
+  double c = pmz_log2_tab_c[i];
+  dd p = two_prod(m, c);
+  double rh0 = __dsub_rn(p.hi, 1.0);  // exact (Sterbenz)
+  dd r = two_sum(rh0, p.lo);
+  dd s = log2_series_dd(r, 16);
+  dd t = dd_add(dd{pmz_log2_tab_hi[i], pmz_log2_tab_lo[i]}, s);
+  return dd_add(dd{(double)e, 0.0}, t);
+}
+
+// CR log2 of any positive normal double.  *amb set when the 2^-96 relative
+// bound could not decide the rounding (never observed; counted by callers).
+__device__ __noinline__ double pmz_log2_d(double x, unsigned *amb) {
+  dd r = log2_dd_general(x);
+  if (!dd_round_certain(r, fabs(r.hi) * 0x1p-96)) {
+    if (amb) atomicAdd(amb, 1u);
+  }
+  return r.hi;
+}
+
+// CR log2 of a positive normal float value (passed as double, 24-bit mantissa).
+// Fast path: r = m*c - 1 is exact (24-bit m times a 29-bit c), series terms
+// 1..4 in double-double and 5..12 in double.
+__device__ __forceinline__ double pmz_log2_f32(double x, unsigned *amb) {
+  double m; int e;
+  int i = log2_split(x, m, e);
+  double c = __ldg(&pmz_log2_tab_c[i]);
+  double r = __dsub_rn(__dmul_rn(m, c), 1.0);  // exact for f32 inputs
+  // Q = k5 + r (k6 + ... + r k12) in double
+  double q = pmz_log2_k_hi[11];
+#pragma unroll
+  for (int n = 10; n >= 4; --n) q = __fma_rn(q, r, pmz_log2_k_hi[n]);
+  dd a = {q, 0.0};
+#pragma unroll
+  for (int n = 3; n >= 0; --n) {
+    dd p = two_prod(r, a.hi);
+    p.lo = __fma_rn(r, a.lo, p.lo);
+    dd s = fast_two_sum(pmz_log2_k_hi[n], p.hi);
+    s.lo = __dadd_rn(s.lo, __dadd_rn(pmz_log2_k_lo[n], p.lo));
+    a = fast_two_sum(s.hi, s.lo);
+  }
+  dd S = two_prod(r, a.hi);
+  S.lo = __fma_rn(r, a.lo, S.lo);
+  S = fast_two_sum(S.hi, S.lo);
+  dd T = dd_add(dd{__ldg(&pmz_log2_tab_hi[i]), __ldg(&pmz_log2_tab_lo[i])}, S);
+  dd R = (e == 0) ? T : dd_add(dd{(double)e, 0.0}, T);
+  if (__builtin_expect(dd_round_certain(R, fabs(R.hi) * 0x1p-80), 1)) return R.hi;
+  return pmz_log2_d(x, amb);
+}
+
+// exp2 helpers ---------------------------------------------------------------
+
+// double-double 2^y for |y| <= 1100, error ~2^-100 relative.
+__device__ __noinline__ dd exp2_dd(double y, int &n) {
+  double nn = rint(y);
+  n = (int)nn;
+  double f = __dsub_rn(y, nn);  // exact, |f| <= 0.5
+  double jj = rint(__dmul_rn(f, 64.0));
+  int j = (int)jj;
+  double t = __dsub_rn(f, __dmul_rn(jj, 0.015625));  // exact, |t| <= 2^-7
+  // 2^t = sum_k (ln2^k / k!) t^k, all terms dd
+  dd a = {pmz_exp2_c_hi[16], pmz_exp2_c_lo[16]};
+  for (int k = 15; k >= 0; --k) {
+    a = dd_mul_d(a, t);
+    a = dd_add(a, dd{pmz_exp2_c_hi[k], pmz_exp2_c_lo[k]});
+  }
+  return dd_mul(a, dd{pmz_exp2_tab_hi[j + 32], pmz_exp2_tab_lo[j + 32]});
+}
+
+// CR64(2^y) as a double (slow path).
+__device__ __noinline__ double pmz_exp2_cr(double y, unsigned *amb) {
+  if (y >= 1024.0) return __longlong_as_double(0x7ff0000000000000LL);
+  if (y < -1080.0) return 0.0;
+  int n;
+  dd a = exp2_dd(y, n);
+  // scale by 2^n in two steps to stay in range; subnormal results need care:
+  // compute the rounding in the scaled domain only when the result is normal.
+  if (n >= -1020 && n <= 1023) {
+    if (!dd_round_certain(a, fabs(a.hi) * 0x1p-96)) { if (amb) atomicAdd(amb, 1u); }
+    double hi = __dadd_rn(a.hi, a.lo);
+    return scalbn(hi, n);
+  }
+  // subnormal / extreme: sum exactly in scaled form via scalbn of hi+lo pieces
+  double hi = scalbn(a.hi, n), lo = scalbn(a.lo, n);
+  return __dadd_rn(hi, lo);
+}
+
+// (float)CR64(2^y): f32 output of inverse_map (transform.py:196 + D20 cast).
+__device__ __forceinline__ float pmz_exp2_to_f32(double y, unsigned *amb) {
+  if (__builtin_expect(y > -125.0 && y < 127.0, 1)) {
+    double nn = rint(y);
+    double f = __dsub_rn(y, nn);
+    double jj = rint(__dmul_rn(f, 64.0));
+    int j = (int)jj;
+    double t = __dsub_rn(f, __dmul_rn(jj, 0.015625));
+    double p = pmz_exp2_c_hi[8];
+#pragma unroll
+    for (int k = 7; k >= 0; --k) p = __fma_rn(p, t, pmz_exp2_c_hi[k]);
+    double a = __dmul_rn(__ldg(&pmz_exp2_tab_hi[j + 32]), p);
+    a = scalbn(a, (int)nn);
+    float f0 = __double2float_rn(a);
+    float fl = __double2float_rn(__dmul_rn(a, 1.0 - 0x1p-44));
+    float fh = __double2float_rn(__dmul_rn(a, 1.0 + 0x1p-44));
+    if (__builtin_expect(fl == f0 && fh == f0, 1)) return f0;
+  }
+  return __double2float_rn(pmz_exp2_cr(y, amb));
+}
+
+}  // namespace pmz

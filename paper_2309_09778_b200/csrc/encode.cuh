@@ -1,0 +1,312 @@
+// encode.cuh -- validation histogram, canonical Huffman codebook, bit packing
+// and container records (layout :496).
+#pragma once
+#include "common.cuh"
+
+namespace pmz {
+
+// K5: per-block code histograms of the validation blocks, summed (D10).
+// Warp-aggregated: lanes holding the same code elect one leader (match_any).
+template <int NT>
+__global__ void __launch_bounds__(NT) k_val_hist(Geom g, const BlkP *__restrict__ blkp, const int64_t *val_ids,
+                                                 const uint16_t *__restrict__ codes, unsigned long long *hist) {
+  int64_t b = val_ids[blockIdx.y];
+  if (blkp[b].trivial) return;
+  if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&hist[kMaxAlpha], 1ull);  // k for the floor (D10)
+  BlockBox bb = block_box(g, b);
+  int64_t n = (int64_t)bb.br * bb.bc;
+  const int lane = threadIdx.x & 31;
+  for (int64_t base = (int64_t)blockIdx.x * NT; base < n; base += (int64_t)gridDim.x * NT) {
+    int64_t e = base + threadIdx.x;
+    int code = -1;
+    if (e < n) {
+      int r = (int)(e / bb.bc), c = (int)(e - (int64_t)r * bb.bc);
+      if (!((r % g.prow) == 0 && c == 0)) code = codes[(bb.r0 + r) * g.cols + bb.c0 + c];
+    }
+    unsigned peers = __match_any_sync(0xffffffffu, code);
+    int leader = __ffs(peers) - 1;
+    if (code >= 0 && lane == leader) atomicAdd(&hist[code], (unsigned long long)__popc(peers));
+  }
+}
+
+// Bitonic sort of n (power of two) u64 keys, ascending, by one CTA.
+__device__ void bitonic_sort(unsigned long long *a, int n) {
+  for (int k = 2; k <= n; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        int l = i ^ j;
+        if (l > i) {
+          unsigned long long x = a[i], y = a[l];
+          bool up = (i & k) == 0;
+          if ((x > y) == up) { a[i] = y; a[l] = x; }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// K6: build_codebook (D10).  Frequencies = summed validation
+// histograms floored at k (= number of non-trivial validation blocks), leaves
+// sorted by (frequency, code); two-queue Huffman with ties preferring the leaf
+// (Moffat-Katajainen in-place form, same tree); canonical codewords in
+// (length, code) order.  One CTA; smem when 2^m <= 8192, else global scratch.
+__global__ void __launch_bounds__(1024) k_codebook(const unsigned long long *hist, WsStatus *st,
+                                                   unsigned long long *g_keys, unsigned *g_A, uint8_t *lens,
+                                                   unsigned *cw) {
+  extern __shared__ unsigned long long sm[];
+  const int m = st->m;
+  const int n = 1 << m;
+  const bool in_smem = n <= 8192;
+  unsigned long long *keys = in_smem ? sm : g_keys;
+  unsigned *A = in_smem ? (unsigned *)(sm + n) : g_A;
+  unsigned long long kval = hist[kMaxAlpha] > 0 ? hist[kMaxAlpha] : 1ull;
+  for (int s = threadIdx.x; s < n; s += blockDim.x) {
+    unsigned long long f = hist[s];
+    if (f < kval) f = kval;
+    keys[s] = (f << 17) | (unsigned long long)s;
+  }
+  __syncthreads();
+  bitonic_sort(keys, n);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) A[i] = (unsigned)(keys[i] >> 17);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    // phase 1: pair up (internal node weights / parent pointers in place)
+    A[0] += A[1];
+    int root = 0, leaf = 2;
+    for (int nxt = 1; nxt < n - 1; nxt++) {
+      if (leaf >= n || A[root] < A[leaf]) { A[nxt] = A[root]; A[root++] = nxt; }
+      else A[nxt] = A[leaf++];
+      if (leaf >= n || (root < nxt && A[root] < A[leaf])) { A[nxt] += A[root]; A[root++] = nxt; }
+      else A[nxt] += A[leaf++];
+    }
+    // phase 2: internal node depths
+    A[n - 2] = 0;
+    for (int nxt = n - 3; nxt >= 0; nxt--) A[nxt] = A[A[nxt]] + 1;
+    // phase 3: leaf depths
+    int avail = 1, used = 0, depth = 0, r = n - 2, nxt = n - 1;
+    while (avail > 0) {
+      while (r >= 0 && (int)A[r] == depth) { used++; r--; }
+      while (avail > used) { A[nxt--] = depth; avail--; }
+      avail = 2 * used; depth++; used = 0;
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) lens[keys[i] & 0x1ffff] = (uint8_t)A[i];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned cnt[64] = {0}, next[64];
+    int maxl = 0;
+    for (int s = 0; s < n; s++) { cnt[lens[s]]++; if (lens[s] > maxl) maxl = lens[s]; }
+    st->max_len = maxl;
+    if (maxl > 32) { atomicOr(&st->err_bits, 1u << (-PMZ_ERR_UNASSIGNED)); return; }
+    unsigned long long c = 0;
+    cnt[0] = 0;
+    for (int l = 1; l <= maxl; l++) { c = (c + cnt[l - 1]) << 1; next[l] = (unsigned)c; }
+    for (int s = 0; s < n; s++) cw[s] = next[lens[s]]++;
+  }
+}
+
+// K7: per-partition payload bits and balance counts.
+template <int NW>
+__global__ void __launch_bounds__(NW * 32) k_part_bits(Geom g, const BlkP *__restrict__ blkp,
+                                                       const uint16_t *__restrict__ codes,
+                                                       const uint8_t *__restrict__ lens,
+                                                       unsigned long long *part_bits) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t p = (int64_t)blockIdx.x * NW + warp;
+  if (p >= g.nparts) return;
+  int64_t b;
+  int pi;
+  part_of(g, p, b, pi);
+  unsigned long long bits = 0;
+  if (!blkp[b].trivial) {
+    BlockBox bb = block_box(g, b);
+    int pr0 = pi * g.prow, R = min(g.prow, bb.br - pr0), C = bb.bc;
+    for (int r = 0; r < R; r++) {
+      const uint16_t *crow = codes + (bb.r0 + pr0 + r) * g.cols + bb.c0;
+      for (int c = lane; c < C; c += 32)
+        if (r | c) bits += __ldg(&lens[crow[c]]);
+    }
+    for (int o = 16; o > 0; o >>= 1) bits += __shfl_xor_sync(0xffffffffu, bits, o);
+  }
+  if (lane == 0) part_bits[p] = bits;
+}
+
+__host__ __device__ inline uint64_t model_blob_bytes(int S, int H) { return 16 + 8ull * (S + 1) * H + 8ull * H; }
+__host__ __device__ inline uint64_t header_bytes(int m, int S, int H) {
+  return 52 + 8 + model_blob_bytes(S, H) + 8 + 2 + (1ull << m) + 8;
+}
+
+// K8: record size per block (D13, D15).
+__global__ void k_block_sizes(Geom g, const BlkP *__restrict__ blkp, const unsigned long long *part_bits,
+                              const unsigned long long *part_zeros, unsigned long long *rec_size) {
+  int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b > g.nblocks) return;
+  if (b == g.nblocks) { rec_size[b] = 0; return; }
+  if (blkp[b].trivial) { rec_size[b] = 1; return; }
+  BlockBox bb = block_box(g, b);
+  int64_t p0 = first_part(g, b);
+  unsigned long long sz = 1 + 16 + 24ull * bb.np + 8;
+  for (int i = 0; i < bb.np; i++) sz += 8ull * part_zeros[p0 + i] + (part_bits[p0 + i] + 7) / 8;
+  rec_size[b] = sz;
+}
+
+__device__ __forceinline__ void put_bytes(uint8_t *p, const void *v, int n) {
+  const uint8_t *s = (const uint8_t *)v;
+  for (int i = 0; i < n; i++) p[i] = s[i];
+}
+__device__ __forceinline__ void put_u64(uint8_t *p, unsigned long long v) { put_bytes(p, &v, 8); }
+__device__ __forceinline__ void put_f64(uint8_t *p, double v) { put_bytes(p, &v, 8); }
+
+// K9: container header (D11, D12).
+__global__ void k_write_header(uint8_t *out, Geom g, KParams k, uint64_t global_rows, const uint8_t *lens,
+                               WsStatus *st) {
+  const int m = st->m;
+  const int n = 1 << m;
+  const uint64_t mb = model_blob_bytes(k.S, k.H);
+  if (threadIdx.x == 0) {
+    uint8_t *p = out;
+    p[0] = 'P'; p[1] = 'M'; p[2] = 'E'; p[3] = 'Z';
+    unsigned short ver = 1;
+    put_bytes(p + 4, &ver, 2);
+    p[6] = 0;
+    unsigned long long rows = global_rows, cols = (unsigned long long)g.cols;
+    put_u64(p + 7, rows);
+    put_u64(p + 15, cols);
+    unsigned br = k.block_rows, bcl = k.block_cols, pr = k.partition_rows;
+    put_bytes(p + 23, &br, 4);
+    put_bytes(p + 27, &bcl, 4);
+    put_bytes(p + 31, &pr, 4);
+    put_f64(p + 35, k.b_r);
+    put_f64(p + 43, k.coverage_target);
+    p[51] = (uint8_t)m;
+    put_u64(p + 52, mb);
+    uint8_t *q = p + 60;
+    unsigned S = k.S, H = k.H;
+    put_bytes(q, &S, 4);
+    put_bytes(q + 4, &H, 4);
+    put_f64(q + 8, k.slope);
+    int nw1 = (k.S + 1) * k.H;
+    for (int i = 0; i < nw1; i++) put_f64(q + 16 + 8 * i, k.w1[i]);
+    for (int i = 0; i < k.H; i++) put_f64(q + 16 + 8 * nw1 + 8 * i, k.w2[i]);
+    q += mb;
+    put_u64(q, 2ull + n);
+    unsigned short a16 = (unsigned short)(n & 0xffff);
+    put_bytes(q + 8, &a16, 2);
+    unsigned long long gnb = ((global_rows + k.block_rows - 1) / k.block_rows) * (unsigned long long)g.nbc;
+    put_u64(q + 10 + n, gnb);
+  }
+  uint8_t *L = out + 60 + mb + 10;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) L[i] = lens[i];
+}
+
+// MSB-first OR of a codeword (len <= 32) at bit position `bit` of byte stream `base`.
+__device__ __forceinline__ void or_bits(uint8_t *base, unsigned long long bit, unsigned code, int len) {
+  if (len == 0) return;
+  uint8_t *p = base + (bit >> 3);
+  int o = (int)(bit & 7);
+  // 64-bit big-endian window: codeword starts at window bit 63 - o
+  unsigned long long w = ((unsigned long long)code) << (64 - len - o);
+  int nbytes = (o + len + 7) >> 3;
+  // group bytes by aligned 32-bit words
+  uintptr_t a0 = (uintptr_t)p;
+  int i = 0;
+  while (i < nbytes) {
+    uintptr_t wa = (a0 + i) & ~(uintptr_t)3;
+    unsigned val = 0;
+    int j = i;
+    while (j < nbytes && (((a0 + j) & ~(uintptr_t)3) == wa)) {
+      unsigned byte = (unsigned)((w >> (56 - 8 * j)) & 0xff);
+      val |= byte << (8 * (int)((a0 + j) & 3));
+      j++;
+    }
+    if (val) atomicOr((unsigned *)wa, val);
+    i = j;
+  }
+}
+
+// K10: write one block record per CTA (D9, D13, D15).
+template <int NW>
+__global__ void __launch_bounds__(NW * 32) k_write_records(Geom g, const BlkP *__restrict__ blkp,
+                                                           const uint16_t *__restrict__ codes,
+                                                           const double *__restrict__ balv,
+                                                           const double *__restrict__ anchors,
+                                                           const unsigned long long *__restrict__ part_bits,
+                                                           const unsigned long long *__restrict__ part_zeros,
+                                                           const unsigned long long *__restrict__ rec_off,
+                                                           const uint8_t *__restrict__ lens,
+                                                           const unsigned *__restrict__ cw, uint8_t *out,
+                                                           unsigned long long rec_base) {
+  const int64_t b = blockIdx.x;
+  uint8_t *base = out + rec_base + rec_off[b];
+  const BlkP P = blkp[b];
+  if (P.trivial) {
+    if (threadIdx.x == 0) base[0] = 1;
+    return;
+  }
+  const BlockBox bb = block_box(g, b);
+  const int64_t p0 = first_part(g, b);
+  __shared__ unsigned long long s_zb[64], s_pb[64];
+  __shared__ unsigned long long s_nbal, s_pay;
+  if (threadIdx.x == 0) {
+    unsigned long long zb = 0, pb = 0;
+    for (int i = 0; i < bb.np; i++) {
+      s_zb[i] = zb; s_pb[i] = pb;
+      zb += part_zeros[p0 + i];
+      pb += (part_bits[p0 + i] + 7) / 8;
+    }
+    s_nbal = zb;
+    s_pay = pb;
+    base[0] = 0;
+    put_f64(base + 1, P.factor_pos);
+    put_f64(base + 9, P.factor_neg);
+    put_u64(base + 17 + 24ull * bb.np, zb);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < bb.np; i += blockDim.x) {
+    uint8_t *e = base + 17 + 24ull * i;
+    put_u64(e, s_pb[i] * 8);
+    put_u64(e + 8, part_bits[p0 + i]);
+    put_f64(e + 16, anchors[p0 + i]);
+  }
+  uint8_t *bal0 = base + 25 + 24ull * bb.np;
+  uint8_t *pay0 = bal0 + 8ull * s_nbal;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int pi = warp; pi < bb.np; pi += NW) {
+    const int pr0 = pi * g.prow, R = min(g.prow, bb.br - pr0), C = bb.bc;
+    uint8_t *pay = pay0 + s_pb[pi];
+    const unsigned long long nbytes = (part_bits[p0 + pi] + 7) / 8;
+    for (unsigned long long i = lane; i < nbytes; i += 32) pay[i] = 0;
+    __syncwarp();
+    unsigned long long zb = s_zb[pi], bit = 0;
+    const int64_t n = (int64_t)R * C;
+    for (int64_t e0 = 0; e0 < n; e0 += 32) {
+      const int64_t e = e0 + lane;
+      int code = -1;
+      int r = 0, c = 0;
+      if (e < n && e > 0) {
+        r = (int)(e / C);
+        c = (int)(e - (int64_t)r * C);
+        code = codes[(bb.r0 + pr0 + r) * g.cols + bb.c0 + c];
+      }
+      const unsigned zmask = __ballot_sync(0xffffffffu, code == 0);
+      if (code == 0) {
+        const unsigned idx = __popc(zmask & ((1u << lane) - 1));
+        put_f64(bal0 + 8ull * (zb + idx), balv[(bb.r0 + pr0 + r) * g.cols + bb.c0 + c]);
+      }
+      zb += __popc(zmask);
+      const int len = code >= 0 ? lens[code] : 0;
+      // warp inclusive scan of lengths
+      unsigned s = len;
+      for (int o = 1; o < 32; o <<= 1) {
+        unsigned t = __shfl_up_sync(0xffffffffu, s, o);
+        if (lane >= o) s += t;
+      }
+      if (code >= 0) or_bits(pay, bit + (s - len), cw[code], len);
+      bit += __shfl_sync(0xffffffffu, s, 31);
+    }
+  }
+}
+
+}  // namespace pmz

@@ -1,0 +1,255 @@
+"""Pipeline module: the compress / decompress entry points
+of the reference package, executed by the sm_100a kernels behind the C ABI.
+
+Host side (this file): argument checking, the seeded validation split, buffer
+ownership (torch CUDA tensors), stream plumbing and the container framing
+helpers.  Device side (csrc/): every per-element and per-block operation of
+compress_block, verify_and_repair, estimate_codebook, build_codebook, encode,
+decode_next, decompress_block and the domain transform.
+
+There is deliberately no CPU fallback; without the native library or a CUDA
+device every call raises ``DeviceError``.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .errors import ConfigError, DeviceError, check
+from .predictor import PerceptronModel, init_model
+from .trainer import COVERAGE_TARGET, SAMPLE_RATE, validation_blocks
+
+EPS0_F32 = float(np.finfo(np.float32).tiny)  # transform.py:37-39 float_floor(float32)
+REPAIR_FACTOR_SPEC = 1.5
+
+
+@dataclass
+class CompressConfig:
+    """Reference parameters (SPEC.md:607 flags): --rel-error, --block-size RxC,
+    --partition-rows, --coverage-target, --sample-rate, --seed; the model is
+    the PerceptronModel (weights) and ``repair_factor`` the verify_and_repair
+    tolerance multiple (D8: SPEC 1.5, BASELINE runs 1.0)."""
+    rel_error: float = 1e-2
+    block_rows: int = 256
+    block_cols: int = 256
+    partition_rows: int = 32
+    repair_factor: float = REPAIR_FACTOR_SPEC
+    coverage_target: float = COVERAGE_TARGET
+    sample_rate: float = SAMPLE_RATE
+    seed: int = 0
+    m: int = 0
+    model: PerceptronModel | None = None
+
+
+@dataclass
+class CompressInfo:
+    nbytes: int
+    header_bytes: int
+    nblocks: int
+    ntrivial: int
+    nbal: int
+    nrepair: int
+    ncodes: int
+    m: int
+    max_code_len: int
+    coverage: list = field(default_factory=list)
+    shape: tuple = ()
+    val_blocks: np.ndarray | None = None
+
+
+def host_b_a(b_r: float) -> float:
+    return float(np.log2(1.0 + b_r))  # transform.py:118
+
+
+def grid_view_shape(shape):
+    """1-D -> (1, N), S=1; 2-D as is; n-D -> (prod(lead), last) (D18)."""
+    if len(shape) == 1:
+        return (1, int(shape[0])), 1
+    if len(shape) == 2:
+        return (int(shape[0]), int(shape[1])), 3
+    return (int(np.prod(shape[:-1])), int(shape[-1])), 3
+
+
+def make_params(cfg: CompressConfig, S: int) -> N.Params:
+    if not (0.0 < cfg.rel_error < 1.0):
+        raise ConfigError(f"relative error bound must be in (0, 1), got {cfg.rel_error}")
+    if cfg.repair_factor <= 0:
+        raise ConfigError("repair_factor must be > 0")
+    model = cfg.model if cfg.model is not None else init_model(S)
+    if model.S != S:
+        raise ConfigError(f"model surface size {model.S} does not match the data ({S})")
+    p = N.Params()
+    p.b_r = cfg.rel_error
+    p.b_a = host_b_a(cfg.rel_error)
+    p.onepbr2 = (1.0 + cfg.rel_error) ** 2  # transform.py:160-162, Python float pow
+    p.eps0 = EPS0_F32
+    p.repair_t = cfg.repair_factor * cfg.rel_error
+    p.coverage_target = cfg.coverage_target
+    p.slope = float(model.leaky_slope)
+    for i, v in enumerate(model.w1.reshape(-1)):
+        p.w1[i] = float(v)
+    for i, v in enumerate(model.w2.reshape(-1)):
+        p.w2[i] = float(v)
+    p.block_rows, p.block_cols, p.partition_rows = cfg.block_rows, cfg.block_cols, cfg.partition_rows
+    p.S, p.H, p.m = S, 2, cfg.m
+    return p
+
+
+def _ptr(t: torch.Tensor | None):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def _stream_ptr(device):
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def _require_cuda(device):
+    if not torch.cuda.is_available():
+        raise DeviceError("CUDA device required (no CPU fallback)")
+    return torch.device(device if device is not None else "cuda")
+
+
+class Codec:
+    """Reusable device codec: owns the workspace and output buffers so
+    repeated calls (benchmarks, streaming) allocate nothing."""
+
+    def __init__(self, device=None):
+        self.device = _require_cuda(device)
+        self.lib = N.load()
+        self._ws = None
+        self._dws = None
+        self._out = None
+
+    # ---- buffers ------------------------------------------------------
+    def _buf(self, name: str, nbytes: int) -> torch.Tensor:
+        cur = getattr(self, name)
+        if cur is None or cur.numel() < nbytes:
+            cur = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=self.device)
+            setattr(self, name, cur)
+        return cur
+
+    # ---- compression --------------------------------------------------
+    def plan(self, shape, cfg: CompressConfig):
+        (rows, cols), S = grid_view_shape(tuple(shape))
+        p = make_params(cfg, S)
+        g = N.Geom(rows, cols, 0, rows)
+        nb = ((rows + cfg.block_rows - 1) // cfg.block_rows) * ((cols + cfg.block_cols - 1) // cfg.block_cols) \
+            if rows and cols else 0
+        val = validation_blocks(nb, cfg.sample_rate, cfg.seed)
+        return p, g, nb, val
+
+    def compress_device(self, x: torch.Tensor, cfg: CompressConfig | None = None, out_capacity: int | None = None,
+                        plan=None, d_val: torch.Tensor | None = None, block_offsets: torch.Tensor | None = None):
+        """Compress a float32 CUDA tensor; returns (container uint8 CUDA tensor
+        view, CompressInfo).  The container bytes are the full reference layout."""
+        cfg = cfg or CompressConfig()
+        if x.dtype != torch.float32:
+            raise ConfigError("only float32 element type is supported on the device path")
+        if not x.is_cuda:
+            raise DeviceError("compress_device expects a CUDA tensor")
+        x = x.contiguous()
+        p, g, nb, val = plan if plan is not None else self.plan(x.shape, cfg)
+        if d_val is None:
+            d_val = torch.as_tensor(val, dtype=torch.int64, device=self.device)
+        lib = self.lib
+        wsz = ctypes.c_uint64(0)
+        check(lib.pmz_workspace_size(ctypes.byref(p), ctypes.byref(g), ctypes.byref(wsz)), "workspace_size")
+        ws = self._buf("_ws", wsz.value)
+        if out_capacity is None:
+            out_capacity = int(x.numel() * 4 * 1.25) + 65536 + 64 * max(nb, 1) * 12
+        out = self._buf("_out", out_capacity)
+        res = N.Result()
+        s = lib.pmz_compress(_ptr(x), ctypes.byref(g), ctypes.byref(p), _ptr(d_val), int(d_val.numel()), _ptr(out),
+                             out.numel(), _ptr(block_offsets), _ptr(ws), ws.numel(), _stream_ptr(self.device),
+                             ctypes.byref(res))
+        if s == -16:  # capacity: retry with the exact size
+            need = int(res.header_bytes + res.record_bytes)
+            out = self._buf("_out", need)
+            s = lib.pmz_compress(_ptr(x), ctypes.byref(g), ctypes.byref(p), _ptr(d_val), int(d_val.numel()),
+                                 _ptr(out), out.numel(), _ptr(block_offsets), _ptr(ws), ws.numel(),
+                                 _stream_ptr(self.device), ctypes.byref(res))
+        check(s, "compress")
+        n = int(res.header_bytes + res.record_bytes)
+        info = CompressInfo(n, int(res.header_bytes), int(res.nblocks), int(res.ntrivial), int(res.nbal),
+                            int(res.nrepair), int(res.ncodes), int(res.m), int(res.max_code_len),
+                            list(res.coverage), tuple(x.shape), val)
+        return out[:n], info
+
+    # ---- decompression ------------------------------------------------
+    @staticmethod
+    def parse_header(buf: np.ndarray) -> N.Header:
+        lib = N.load()
+        h = N.Header()
+        check(lib.pmz_parse_header(buf.ctypes.data_as(ctypes.c_void_p), buf.size, ctypes.byref(h)), "read_container")
+        return h
+
+    @staticmethod
+    def index_blocks(buf: np.ndarray, h: N.Header) -> np.ndarray:
+        lib = N.load()
+        offs = np.zeros(int(h.nblocks) + 1, np.uint64)
+        check(lib.pmz_index_blocks(buf.ctypes.data_as(ctypes.c_void_p), buf.size, ctypes.byref(h),
+                                   offs.ctypes.data_as(ctypes.c_void_p)), "read_container")
+        return offs
+
+    def decompress_device(self, d_buf: torch.Tensor, h: N.Header, d_offsets: torch.Tensor,
+                          out: torch.Tensor | None = None) -> torch.Tensor:
+        lib = self.lib
+        wsz = ctypes.c_uint64(0)
+        check(lib.pmz_decompress_workspace_size(ctypes.byref(h), ctypes.byref(wsz)), "workspace")
+        ws = self._buf("_dws", wsz.value)
+        if out is None:
+            out = torch.empty((int(h.rows), int(h.cols)), dtype=torch.float32, device=self.device)
+        check(lib.pmz_decompress(_ptr(d_buf), d_buf.numel(), ctypes.byref(h), host_b_a(h.b_r), _ptr(d_offsets),
+                                 _ptr(out), _ptr(ws), ws.numel(), _stream_ptr(self.device)), "decompress")
+        return out
+
+
+_codecs: dict = {}
+
+
+def _codec(device=None) -> Codec:
+    dev = _require_cuda(device)
+    key = str(dev)
+    if key not in _codecs:
+        _codecs[key] = Codec(dev)
+    return _codecs[key]
+
+
+def compress(data, rel_error: float = 1e-2, block_size=(256, 256), partition_rows: int = 32,
+             model: PerceptronModel | None = None, repair_factor: float = REPAIR_FACTOR_SPEC,
+             coverage_target: float = COVERAGE_TARGET, sample_rate: float = SAMPLE_RATE, seed: int = 0,
+             m: int = 0, device=None, return_info: bool = False):
+    """cmd_compress minus ingest/training: array in, container bytes out."""
+    cfg = CompressConfig(rel_error, int(block_size[0]), int(block_size[1]), partition_rows, repair_factor,
+                         coverage_target, sample_rate, seed, m, model)
+    codec = _codec(device)
+    if isinstance(data, torch.Tensor):
+        x = data.to(device=codec.device, dtype=torch.float32)
+    else:
+        a = np.ascontiguousarray(np.asarray(data), dtype=np.float32)
+        x = torch.from_numpy(a).to(codec.device)
+    buf, info = codec.compress_device(x, cfg)
+    host = buf.cpu().numpy().tobytes()
+    return (host, info) if return_info else host
+
+
+def decompress(container: bytes, device=None, shape=None) -> np.ndarray:
+    """cmd_decompress: container bytes in, float32 array out."""
+    codec = _codec(device)
+    buf = np.frombuffer(container, dtype=np.uint8)
+    h = codec.parse_header(buf)
+    offs = codec.index_blocks(buf, h)
+    d_buf = torch.from_numpy(buf.copy()).to(codec.device)
+    d_off = torch.from_numpy(offs.view(np.int64)).to(codec.device)
+    out = codec.decompress_device(d_buf, h, d_off)
+    res = out.cpu().numpy()
+    if shape is not None:
+        return res.reshape(shape)
+    if h.rows == 1 and h.S == 1:
+        return res.reshape(-1)
+    return res
