@@ -1,0 +1,371 @@
+"""Benchmark of the B200 PW_REL block compression path (BASELINE.json metric:
+"compress/decompress GB/s at PW_REL 1e-2 (1/2/4/8 B200); compression ratio").
+
+Workload (N=1): config C2 of BASELINE.json -- float32 1800x3600 exp(GRF k^-3)
+sign-flipped on 30% of a smooth mask, PW_REL 1e-2, repair_factor 1.0 (every
+point |x'-x| <= eps|x|), Lorenzo-init perceptron, 256x256 blocks, 32-row
+partitions.  A step = one compress of the field resident in HBM; decompress is
+timed the same way and reported beside it.  N>1: the field is N copies of C2
+stacked along the slowest axis and sharded into whole block-rows, one shard
+per rank (weak scaling); shards exchange only the select_m / codebook
+histograms (NCCL all-reduce) and the per-shard sizes (NCCL all-gather).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+HBM_FALLBACK = 6650.0
+METRIC = "compress GB/s at PW_REL 1e-2 (C2 1800x3600 f32)"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return HBM_FALLBACK, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([v.strip() for v in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 2 + i and
+                          s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def c2_field(device):
+    import torch
+    from paper_2309_09778_b200 import synthetic
+    return synthetic.generate("C2", device=device)
+
+
+def shard_rows(global_rows: int, block_rows: int, world: int, rank: int):
+    nbr = (global_rows + block_rows - 1) // block_rows
+    b0, b1 = nbr * rank // world, nbr * (rank + 1) // world
+    return b0, min(b0 * block_rows, global_rows), min(b1 * block_rows, global_rows)
+
+
+def cpu_reference_time(x: np.ndarray, eps: float, repair: float, reps: int, threads: int):
+    """Oracle restatement of the reference path (CPU, all host threads)."""
+    from oracle import oracle as O
+    cfg = O.OracleConfig(b_r=eps, repair_factor=repair)
+    O.compress(x, cfg, nthreads=threads)  # warm
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        buf, _ = O.compress(x, cfg, nthreads=threads)
+    dt = (time.perf_counter() - t0) / reps
+    return dt, len(buf)
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import torch
+    from paper_2309_09778_b200 import synthetic
+    x = synthetic.generate("C2").numpy()
+    threads = os.cpu_count() or 1
+    from oracle import oracle as O
+    cfg = O.OracleConfig(b_r=args.eps, repair_factor=args.repair)
+    for _ in range(args.warmup):
+        O.compress(x, cfg, nthreads=threads)
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        buf, _ = O.compress(x, cfg, nthreads=threads)
+        ts.append(time.perf_counter() - t0)
+    t = sum(ts) / len(ts)
+    gbs = x.nbytes / t / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "C2 1800x3600 f32 exp(GRF k^-3) sign-flipped, PW_REL 1e-2, repair 1.0",
+                   "path": "oracle/permez_oracle.c (C restatement of the reference path; the reference ships "
+                           "no compress code) + numpy split, OpenMP over blocks"},
+        "compression_ratio": len(buf) / x.nbytes,
+        "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": threads, "kind": "port",
+                         "sample": f"full C2 field per step, {args.steps} steps"},
+        "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--eps", type=float, default=1e-2)
+    ap.add_argument("--repair", type=float, default=1.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-steps", type=int, default=0, help="(ncu) run this many steps, no JSON timing claims")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.profile_steps == 0 else args.warmup
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+    import paper_2309_09778_b200 as P
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def allreduce(t):
+        if world > 1:
+            dist.all_reduce(t)
+
+    cfg = P.CompressConfig(rel_error=args.eps, repair_factor=args.repair)
+    base = c2_field(dev)                      # 1800 x 3600, seed 1
+    R0, C = base.shape
+    grows = R0 * world
+    b0, r0, r1 = shard_rows(grows, cfg.block_rows, world, rank)
+    idx = torch.arange(r0, r1, device=dev) % R0
+    x = base[idx].contiguous()                # this rank's shard of the stacked field
+    del base
+    codec = P.Codec(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    offs = torch.empty(((x.shape[0] + 255) // 256) * ((C + 255) // 256) + 1, dtype=torch.int64, device=dev)
+
+    def compress_once(ev=None):
+        return codec.compress_staged(x, cfg, block_row0=b0, global_rows=grows, allreduce=allreduce,
+                                     block_offsets=offs, events=ev)
+
+    # one compress to build the decompress inputs
+    buf, info = compress_once()
+    from paper_2309_09778_b200 import _native as N
+    import ctypes
+
+    full = buf.cpu().numpy()
+    hdr = N.Header()
+    # parse the header of this shard's container (header + own records)
+    lib = N.load()
+    st = lib.pmz_parse_header(full.ctypes.data_as(ctypes.c_void_p), full.size, ctypes.byref(hdr))
+    if st != 0:
+        raise RuntimeError(f"header parse failed {st}")
+    hdr.rows = x.shape[0]
+    hdr.nblocks = offs.numel() - 1
+    dbuf = buf.clone()
+    doffs = offs.clone()
+    out = torch.empty(x.shape, dtype=torch.float32, device=dev)
+
+    def decompress_once():
+        return codec.decompress_device(dbuf, hdr, doffs, out=out)
+
+    # correctness guard on the benchmarked data: bound + zeros exact
+    y = decompress_once()
+    torch.cuda.synchronize()
+    xz = torch.where(x.abs() <= 1.1754943508222875e-38, torch.zeros_like(x), x)
+    nz = xz != 0
+    rel = ((y.double() - xz.double()).abs() / xz.double().abs().clamp_min(1e-300))[nz]
+    max_rel = float(rel.max()) if rel.numel() else 0.0
+    zeros_ok = bool((y[~nz] == 0).all())
+    assert max_rel <= args.eps * args.repair and zeros_ok, (max_rel, zeros_ok)
+
+    # warm-up
+    for _ in range(args.warmup):
+        compress_once()
+        decompress_once()
+    torch.cuda.synchronize()
+
+    if args.profile_steps:
+        for _ in range(args.profile_steps):
+            compress_once()
+            decompress_once()
+        torch.cuda.synchronize()
+        return 0
+
+    n_elem = x.numel()
+    K = args.steps
+    c_ms, codes_ms, d_ms = [], [], []
+    launches = 0
+    sampler = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with sampler:
+        for _ in range(K):
+            flush.fill_(1)  # L2 flush, outside the timed events
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            bufk, infok = compress_once(ev)
+            dstart, dstop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            flush.fill_(2)
+            dstart.record()
+            decompress_once()
+            dstop.record()
+            torch.cuda.synchronize()
+            c_ms.append(ev[0].elapsed_time(ev[3]))
+            codes_ms.append(ev[1].elapsed_time(ev[2]))
+            d_ms.append(dstart.elapsed_time(dstop))
+            launches += infok.launches + 4
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    tot = torch.tensor([sum(c_ms), sum(d_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    c_tot, d_tot = float(tot[0]), float(tot[1])
+    # total bytes = sum over ranks (shards are whole block-rows, ~equal)
+    nb_t = torch.tensor([float(n_elem * 4), float(infok.nbytes)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(nb_t)
+    bytes_all, cbytes_all = float(nb_t[0]), float(nb_t[1])
+    comp_gbs = bytes_all / (c_tot / K / 1e3) / 1e9
+    dec_gbs = bytes_all / (d_tot / K / 1e3) / 1e9
+    cr = cbytes_all / bytes_all
+
+    # e2e through the public API with host buffers (pinned), every step
+    e2e_c, e2e_d = None, None
+    h_in = torch.empty(x.shape, dtype=torch.float32, pin_memory=True)
+    h_in.copy_(x)
+    h_out = torch.empty(int(info.nbytes) + (1 << 20), dtype=torch.uint8, pin_memory=True)
+    h_y = torch.empty(x.shape, dtype=torch.float32, pin_memory=True)
+    full_host = np.ascontiguousarray(bufk.cpu().numpy())
+    h_cont = torch.from_numpy(full_host).pin_memory()
+    e_ms, ed_ms = [], []
+    for i in range(max(3, K // 2)):
+        flush.fill_(3)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        xd = h_in.to(dev, non_blocking=True)
+        b2, i2 = codec.compress_staged(xd, cfg, block_row0=b0, global_rows=grows, allreduce=allreduce)
+        h_out[: i2.nbytes].copy_(b2, non_blocking=True)
+        e.record()
+        torch.cuda.synchronize()
+        e_ms.append(s.elapsed_time(e))
+        # decompress e2e: host container -> index walk -> H2D -> decode -> D2H
+        s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s2.record()
+        hoffs = P.Codec.index_blocks(full_host, hdr) if world == 1 else None
+        db = h_cont.to(dev, non_blocking=True)
+        do = torch.from_numpy(hoffs.view(np.int64)).to(dev, non_blocking=True) if hoffs is not None else doffs
+        yy = codec.decompress_device(db, hdr, do)
+        h_y.copy_(yy, non_blocking=True)
+        e2.record()
+        torch.cuda.synchronize()
+        ed_ms.append(s2.elapsed_time(e2))
+    et = torch.tensor([sum(e_ms) / len(e_ms), sum(ed_ms) / len(ed_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(et, op=dist.ReduceOp.MAX)
+    e2e_c = bytes_all / (float(et[0]) / 1e3) / 1e9
+    e2e_d = bytes_all / (float(et[1]) / 1e3) / 1e9
+
+    hbm, peak_kind = peaks()
+    codes_avg = sum(codes_ms) / len(codes_ms) / 1e3
+    alg_bytes = n_elem * (4.0 + 4.0 * cr)
+    achieved = alg_bytes / codes_avg / 1e9
+    traffic = None
+    tr_path = os.path.join(ROOT, "profiles", "traffic_latest.json")
+    if os.path.exists(tr_path):
+        try:
+            traffic = json.load(open(tr_path)).get("k_wavefront_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    cpu_base = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            xs = x.cpu().numpy()
+            threads = os.cpu_count() or 1
+            dt, _ = cpu_reference_time(xs, args.eps, args.repair, reps=3, threads=threads)
+            cpu_base = {"value": xs.nbytes / dt / 1e9, "unit": "GB/s", "cores": threads, "kind": "port",
+                        "sample": "full C2 field x3 compressions (oracle restatement, OpenMP over blocks)"}
+        except Exception as ex:  # the CPU baseline is reported, never required
+            cpu_base = {"value": None, "unit": "GB/s", "cores": os.cpu_count(), "kind": "port",
+                        "sample": f"failed: {ex!r}"}
+
+    clocks = sampler.summary()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": comp_gbs, "unit": "GB/s", "n_gpus": world, "steps": K,
+            "warmup": args.warmup, "ms_per_step": c_tot / K, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "C2: 1800x3600 f32 exp(GRF k^-3), 30% sign-flipped; PW_REL 1e-2, repair 1.0; "
+                                   "per rank one C2-sized shard of the stacked field",
+                       "block": "256x256", "partition_rows": 32, "model": "init_model (Lorenzo)",
+                       "l2": "flushed between steps (256 MiB write), inputs < L2",
+                       "parallelism": f"shard{world}" if world > 1 else "single"},
+            "compression_ratio": cr, "max_rel_err": max_rel, "m": infok.m,
+            "decompress": {"value": dec_gbs, "unit": "GB/s", "ms_per_step": d_tot / K,
+                           "e2e": {"value": e2e_d, "unit": "GB/s"}},
+            "e2e": {"value": e2e_c, "unit": "GB/s", "h2d_bytes_per_step": int(n_elem * 4),
+                    "d2h_bytes_per_step": int(info.nbytes)},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": achieved / hbm, "traffic": traffic, "kernel": "k_wavefront (codes stage)",
+                         "peak_kind": peak_kind,
+                         "alg_bytes_per_elem": 4.0 + 4.0 * cr},
+            "cpu_baseline": cpu_base,
+            "gpu_launches": launches,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -97,7 +97,7 @@ typedef struct pmz_result {
   int32_t m;
   int32_t max_code_len;
   uint32_t unresolved;    /* undecided CR roundings (expected 0)             */
-  uint32_t flags;
+  uint32_t launches;      /* kernels this library launched for the call      */
 } pmz_result;
 
 /* Parsed container header (read_container, layout :496). */

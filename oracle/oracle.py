@@ -197,7 +197,10 @@ def split_blocks(nblocks: int, sample_rate: float, seed: int):
     if nblocks == 0:
         return np.zeros(0, np.int64), np.zeros(0, np.int64)
     k = max(ceil_frac(sample_rate, nblocks), min(nblocks, 5))
-    ids = np.random.default_rng(seed).permutation(nblocks)[:k].astype(np.int64)
+    if sample_rate == 1.0:
+        ids = np.arange(nblocks, dtype=np.int64)  # all blocks, original order
+    else:
+        ids = np.random.default_rng(seed).permutation(nblocks)[:k].astype(np.int64)
     ntr = ceil_frac(0.8, k)
     train, val = ids[:ntr], ids[ntr:]
     if val.size == 0:

@@ -36,7 +36,7 @@ class Result(ctypes.Structure):
     _fields_ = [
         ("header_bytes", c_uint64), ("record_bytes", c_uint64), ("nblocks", c_uint64), ("ntrivial", c_uint64),
         ("nbal", c_uint64), ("nrepair", c_uint64), ("ncodes", c_uint64), ("coverage", c_uint64 * 18),
-        ("m", c_int32), ("max_code_len", c_int32), ("unresolved", c_uint32), ("flags", c_uint32),
+        ("m", c_int32), ("max_code_len", c_int32), ("unresolved", c_uint32), ("launches", c_uint32),
     ]
 
 

@@ -234,13 +234,14 @@ int pmz_compress_codes(const float *d_in, const pmz_geom *g, const pmz_params *p
   if (n_val > 0) {
     dim3 grid(16, (unsigned)n_val);
     k_val_hist<kNT><<<grid, kNT, 0, st>>>(G, at<BlkP>(d_ws, L.blkp), d_val, at<uint16_t>(d_ws, L.codes),
-                                          at<unsigned long long>(d_ws, L.hist));
+                                          at<unsigned long long>(d_ws, L.hist), at<WsStatus>(d_ws, L.status));
   }
   return launch_check();
 }
 
 __global__ void k_block_offsets(Geom g, KParams k, int write_header, const unsigned long long *rec_off,
-                                const WsStatus *st, unsigned long long *boff) {
+                                WsStatus *st, unsigned long long *boff) {
+  count_launch(st);
   int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (b > g.nblocks) return;
   unsigned long long base = write_header ? header_bytes(st->m, k.S, k.H) : 0;
@@ -249,6 +250,7 @@ __global__ void k_block_offsets(Geom g, KParams k, int write_header, const unsig
 
 __global__ void k_finish_status(Geom g, KParams k, int write_header, const unsigned long long *rec_off,
                                 unsigned long long cap, WsStatus *st) {
+  count_launch(st);
   unsigned long long hb = write_header ? header_bytes(st->m, k.S, k.H) : 0;
   st->header_bytes = hb;
   st->record_bytes = rec_off[g.nblocks];
@@ -274,11 +276,11 @@ int pmz_compress_finish(const pmz_geom *g, const pmz_params *p, int write_header
     unsigned grid = (unsigned)((G.nparts + kWarps - 1) / kWarps);
     k_part_bits<kWarps><<<grid, kWarps * 32, 0, st>>>(G, at<BlkP>(d_ws, L.blkp), at<uint16_t>(d_ws, L.codes),
                                                       at<uint8_t>(d_ws, L.lens),
-                                                      at<unsigned long long>(d_ws, L.part_bits));
+                                                      at<unsigned long long>(d_ws, L.part_bits), S);
   }
   k_block_sizes<<<(unsigned)((G.nblocks + 1 + 255) / 256), 256, 0, st>>>(
       G, at<BlkP>(d_ws, L.blkp), at<unsigned long long>(d_ws, L.part_bits),
-      at<unsigned long long>(d_ws, L.part_zeros), at<unsigned long long>(d_ws, L.rec_size));
+      at<unsigned long long>(d_ws, L.part_zeros), at<unsigned long long>(d_ws, L.rec_size), S);
   size_t cb = L.cub_bytes;
   CK(cub::DeviceScan::ExclusiveSum(at<void>(d_ws, L.cub_tmp), cb, at<unsigned long long>(d_ws, L.rec_size),
                                    at<unsigned long long>(d_ws, L.rec_off), (int)(G.nblocks + 1), st));
@@ -299,6 +301,7 @@ int pmz_compress_finish(const pmz_geom *g, const pmz_params *p, int write_header
     res->m = hs.m;
     res->max_code_len = hs.max_len;
     res->unresolved = hs.unresolved;
+    res->launches = hs.launches;
     CK(cudaMemcpy(res->coverage, at<uint64_t>(d_ws, L.cov), 18 * 8, cudaMemcpyDeviceToHost));
   }
   int err = err_from_bits(hs.err_bits);
@@ -313,7 +316,7 @@ int pmz_compress_finish(const pmz_geom *g, const pmz_params *p, int write_header
         G, at<BlkP>(d_ws, L.blkp), at<uint16_t>(d_ws, L.codes), at<double>(d_ws, L.balv),
         at<double>(d_ws, L.anchors), at<unsigned long long>(d_ws, L.part_bits),
         at<unsigned long long>(d_ws, L.part_zeros), at<unsigned long long>(d_ws, L.rec_off),
-        at<uint8_t>(d_ws, L.lens), at<unsigned>(d_ws, L.cw), d_out, rec_base);
+        at<uint8_t>(d_ws, L.lens), at<unsigned>(d_ws, L.cw), d_out, rec_base, S);
   if (d_block_offsets)
     k_block_offsets<<<(unsigned)((G.nblocks + 1 + 255) / 256), 256, 0, st>>>(
         G, k, write_header, at<unsigned long long>(d_ws, L.rec_off), S, (unsigned long long *)d_block_offsets);
@@ -321,6 +324,7 @@ int pmz_compress_finish(const pmz_geom *g, const pmz_params *p, int write_header
   if (s) return s;
   CK(cudaStreamSynchronize(st));
   CK(cudaMemcpy(&hs, S, sizeof(WsStatus), cudaMemcpyDeviceToHost));
+  if (res) res->launches = hs.launches;
   err = err_from_bits(hs.err_bits);
   if (err) return err;
   return PMZ_OK;

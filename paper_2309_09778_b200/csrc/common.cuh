@@ -137,7 +137,8 @@ struct WsStatus {
   int m;                 // selected code width
   int max_len;           // max codeword length
   int n_val_nontrivial;  // k for the histogram floor (D10)
-  int pad[3];
+  unsigned launches;     // kernels of this library that ran (counted on device)
+  int pad[2];
   unsigned long long nbal, nrepair, ntrivial, ncodes;
   unsigned long long total_bytes, header_bytes, record_bytes;
   unsigned long long pad2;
@@ -148,6 +149,11 @@ struct WsLayout {
       rec_off, cub_tmp, codes, balv, total;
   size_t cub_bytes;
 };
+
+// count one executed kernel (first thread of the grid)
+__device__ __forceinline__ void count_launch(WsStatus *st) {
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) atomicAdd(&st->launches, 1u);
+}
 
 __host__ __device__ inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 

@@ -51,6 +51,7 @@ __device__ inline void derive_params(double fp, double fn, const KParams &k, Blk
 template <int NT>
 __global__ void __launch_bounds__(NT) k_block_params(const float *__restrict__ x, Geom g, KParams k, BlkP *blkp,
                                                      WsStatus *st) {
+  count_launch(st);
   int64_t b = blockIdx.x;
   BlockBox bb = block_box(g, b);
   float mn = INFINITY, mx = 0.0f;
@@ -87,6 +88,7 @@ __global__ void __launch_bounds__(NT) k_block_params(const float *__restrict__ x
 template <int NT>
 __global__ void __launch_bounds__(NT) k_coverage(const float *__restrict__ x, Geom g, KParams k, const BlkP *blkp,
                                                  const int64_t *val_ids, unsigned long long *cov, WsStatus *st) {
+  count_launch(st);
   __shared__ unsigned int h[18];
   if (threadIdx.x < 18) h[threadIdx.x] = 0;
   __syncthreads();
@@ -119,6 +121,7 @@ __global__ void __launch_bounds__(NT) k_coverage(const float *__restrict__ x, Ge
 // K3: select_m (D17): smallest m in [4,16] whose coverage
 // covered/total (f64) meets the target; 16 when none does, 4 with no residuals.
 __global__ void k_select_m(const unsigned long long *cov, KParams k, WsStatus *st) {
+  count_launch(st);
   if (threadIdx.x != 0) return;
   int m = k.m_fixed;
   if (m == 0) {
@@ -151,6 +154,7 @@ __global__ void __launch_bounds__(NW * 32) k_wavefront(const float *__restrict__
                                                        uint16_t *__restrict__ codes, double *__restrict__ balv,
                                                        double *__restrict__ anchors,
                                                        unsigned long long *__restrict__ part_zeros) {
+  count_launch(st);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t p = (int64_t)blockIdx.x * NW + warp;
   if (p >= g.nparts) return;

@@ -9,7 +9,9 @@ namespace pmz {
 // Warp-aggregated: lanes holding the same code elect one leader (match_any).
 template <int NT>
 __global__ void __launch_bounds__(NT) k_val_hist(Geom g, const BlkP *__restrict__ blkp, const int64_t *val_ids,
-                                                 const uint16_t *__restrict__ codes, unsigned long long *hist) {
+                                                 const uint16_t *__restrict__ codes, unsigned long long *hist,
+                                                 WsStatus *st) {
+  count_launch(st);
   int64_t b = val_ids[blockIdx.y];
   if (blkp[b].trivial) return;
   if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&hist[kMaxAlpha], 1ull);  // k for the floor (D10)
@@ -55,6 +57,7 @@ __global__ void __launch_bounds__(1024) k_codebook(const unsigned long long *his
                                                    unsigned long long *g_keys, unsigned *g_A, uint8_t *lens,
                                                    unsigned *cw) {
   extern __shared__ unsigned long long sm[];
+  count_launch(st);
   const int m = st->m;
   const int n = 1 << m;
   const bool in_smem = n <= 8192;
@@ -112,7 +115,8 @@ template <int NW>
 __global__ void __launch_bounds__(NW * 32) k_part_bits(Geom g, const BlkP *__restrict__ blkp,
                                                        const uint16_t *__restrict__ codes,
                                                        const uint8_t *__restrict__ lens,
-                                                       unsigned long long *part_bits) {
+                                                       unsigned long long *part_bits, WsStatus *st) {
+  count_launch(st);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t p = (int64_t)blockIdx.x * NW + warp;
   if (p >= g.nparts) return;
@@ -140,7 +144,9 @@ __host__ __device__ inline uint64_t header_bytes(int m, int S, int H) {
 
 // K8: record size per block (D13, D15).
 __global__ void k_block_sizes(Geom g, const BlkP *__restrict__ blkp, const unsigned long long *part_bits,
-                              const unsigned long long *part_zeros, unsigned long long *rec_size) {
+                              const unsigned long long *part_zeros, unsigned long long *rec_size,
+                              WsStatus *st) {
+  count_launch(st);
   int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (b > g.nblocks) return;
   if (b == g.nblocks) { rec_size[b] = 0; return; }
@@ -162,6 +168,7 @@ __device__ __forceinline__ void put_f64(uint8_t *p, double v) { put_bytes(p, &v,
 // K9: container header (D11, D12).
 __global__ void k_write_header(uint8_t *out, Geom g, KParams k, uint64_t global_rows, const uint8_t *lens,
                                WsStatus *st) {
+  count_launch(st);
   const int m = st->m;
   const int n = 1 << m;
   const uint64_t mb = model_blob_bytes(k.S, k.H);
@@ -237,7 +244,8 @@ __global__ void __launch_bounds__(NW * 32) k_write_records(Geom g, const BlkP *_
                                                            const unsigned long long *__restrict__ rec_off,
                                                            const uint8_t *__restrict__ lens,
                                                            const unsigned *__restrict__ cw, uint8_t *out,
-                                                           unsigned long long rec_base) {
+                                                           unsigned long long rec_base, WsStatus *st) {
+  count_launch(st);
   const int64_t b = blockIdx.x;
   uint8_t *base = out + rec_base + rec_off[b];
   const BlkP P = blkp[b];

@@ -60,6 +60,7 @@ class CompressInfo:
     coverage: list = field(default_factory=list)
     shape: tuple = ()
     val_blocks: np.ndarray | None = None
+    launches: int = 0
 
 
 def host_b_a(b_r: float) -> float:
@@ -177,7 +178,74 @@ class Codec:
         n = int(res.header_bytes + res.record_bytes)
         info = CompressInfo(n, int(res.header_bytes), int(res.nblocks), int(res.ntrivial), int(res.nbal),
                             int(res.nrepair), int(res.ncodes), int(res.m), int(res.max_code_len),
-                            list(res.coverage), tuple(x.shape), val)
+                            list(res.coverage), tuple(x.shape), val, int(res.launches))
+        return out[:n], info
+
+    def compress_staged(self, x: torch.Tensor, cfg: CompressConfig, *, block_row0: int = 0,
+                        global_rows: int | None = None, global_shape=None, allreduce=None,
+                        write_header: bool = True, out_capacity: int | None = None,
+                        block_offsets: torch.Tensor | None = None, events=None, d_val: torch.Tensor | None = None):
+        """Stage-by-stage compress of one shard (whole block-rows starting at
+        global block-row ``block_row0``).  ``allreduce(tensor)`` sums a device
+        int64 tensor across shards (NCCL) between stages: the select_m coverage
+        histogram and the validation-code histogram, so every shard derives the
+        same m and codebook.  ``events`` (4 CUDA events) time
+        the stages on the launching stream."""
+        if x.dtype != torch.float32 or not x.is_cuda:
+            raise ConfigError("compress_staged expects a float32 CUDA tensor")
+        x = x.contiguous()
+        (rows, cols), S = grid_view_shape(tuple(x.shape))
+        if global_shape is not None:
+            (grows, _), S = grid_view_shape(tuple(global_shape))
+        else:
+            grows = global_rows if global_rows is not None else rows
+        p = make_params(cfg, S)
+        g = N.Geom(rows, cols, block_row0, grows)
+        nbc = (cols + cfg.block_cols - 1) // cfg.block_cols
+        nb_local = ((rows + cfg.block_rows - 1) // cfg.block_rows) * nbc
+        if d_val is None:
+            gnb = ((grows + cfg.block_rows - 1) // cfg.block_rows) * nbc
+            val = validation_blocks(gnb, cfg.sample_rate, cfg.seed)
+            lo = block_row0 * nbc
+            val = val[(val >= lo) & (val < lo + nb_local)] - lo
+            d_val = torch.as_tensor(val, dtype=torch.int64, device=self.device)
+        lib = self.lib
+        wsz = ctypes.c_uint64(0)
+        check(lib.pmz_workspace_size(ctypes.byref(p), ctypes.byref(g), ctypes.byref(wsz)), "workspace_size")
+        ws = self._buf("_ws", wsz.value)
+        if out_capacity is None:
+            cap = ctypes.c_uint64(0)
+            check(lib.pmz_max_container_size(ctypes.byref(p), ctypes.byref(g), ctypes.byref(cap)), "max_size")
+            out_capacity = int(cap.value)
+        out = self._buf("_out", out_capacity)
+        stream = _stream_ptr(self.device)
+        nv = int(d_val.numel())
+        if events is not None:
+            events[0].record()
+        check(lib.pmz_compress_analyze(_ptr(x), ctypes.byref(g), ctypes.byref(p), _ptr(d_val), nv, _ptr(ws),
+                                       ws.numel(), stream), "compress_analyze")
+        if allreduce is not None:
+            off = lib.pmz_ws_coverage(_ptr(ws), ctypes.byref(p), ctypes.byref(g)) - ws.data_ptr()
+            allreduce(ws[off: off + 18 * 8].view(torch.int64))
+        if events is not None:
+            events[1].record()
+        check(lib.pmz_compress_codes(_ptr(x), ctypes.byref(g), ctypes.byref(p), _ptr(d_val), nv, _ptr(ws),
+                                     ws.numel(), stream), "compress_codes")
+        if events is not None:
+            events[2].record()
+        if allreduce is not None:
+            off = lib.pmz_ws_histogram(_ptr(ws), ctypes.byref(p), ctypes.byref(g)) - ws.data_ptr()
+            allreduce(ws[off: off + (65536 + 1) * 8].view(torch.int64))
+        res = N.Result()
+        s = lib.pmz_compress_finish(ctypes.byref(g), ctypes.byref(p), int(write_header), _ptr(out), out.numel(),
+                                    _ptr(block_offsets), _ptr(ws), ws.numel(), stream, ctypes.byref(res))
+        check(s, "compress_finish")
+        if events is not None:
+            events[3].record()
+        n = int(res.header_bytes + res.record_bytes)
+        info = CompressInfo(n, int(res.header_bytes), int(res.nblocks), int(res.ntrivial), int(res.nbal),
+                            int(res.nrepair), int(res.ncodes), int(res.m), int(res.max_code_len),
+                            list(res.coverage), tuple(x.shape), None, int(res.launches))
         return out[:n], info
 
     # ---- decompression ------------------------------------------------

@@ -1,0 +1,194 @@
+"""GPU parity tests: the CUDA path (through the C ABI) vs the CPU oracle on
+the same seeded inputs.  Integer/byte outputs must be bit-exact: the whole
+container (header, per-block transform factors, partition tables, anchors,
+balance lists, Huffman payload) and the decompressed float32 grid."""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def codec():
+    import paper_2309_09778_b200 as P
+    return P.Codec("cuda:0")
+
+
+def _field(name, shape=None):
+    from paper_2309_09778_b200 import synthetic
+    return synthetic.generate(name, shape=shape).numpy()
+
+
+def _check_bound(x, y, bound):
+    xz = np.where(np.abs(x) <= np.finfo(np.float32).tiny, 0, x).astype(np.float64).reshape(-1)
+    y = y.astype(np.float64).reshape(-1)
+    nz = xz != 0
+    rel = np.abs(y[nz] - xz[nz]) / np.abs(xz[nz])
+    assert rel.max(initial=0.0) <= bound
+    assert np.all(y[~nz] == 0)
+
+
+def _parity(codec, oracle, x, **kw):
+    import paper_2309_09778_b200 as P
+    ocfg = oracle.OracleConfig(**{k: v for k, v in kw.items()})
+    pcfg = P.CompressConfig(rel_error=kw.get("b_r", 1e-2), repair_factor=kw.get("repair_factor", 1.5),
+                            block_rows=kw.get("block_rows", 256), block_cols=kw.get("block_cols", 256),
+                            partition_rows=kw.get("partition_rows", 32), m=kw.get("m", 0))
+    dbuf, info = codec.compress_device(torch.from_numpy(np.ascontiguousarray(x)).cuda(), pcfg)
+    gpu = dbuf.cpu().numpy().tobytes()
+    ref, rinfo = oracle.compress(x, ocfg)
+    assert info.m == rinfo["m"]
+    assert info.nbal == rinfo["nbal"] and info.nrepair == rinfo["nrepair"]
+    if gpu != ref:
+        a, b = np.frombuffer(gpu, np.uint8), np.frombuffer(ref, np.uint8)
+        n = min(a.size, b.size)
+        d = np.nonzero(a[:n] != b[:n])[0]
+        pytest.fail(f"container mismatch: len {a.size} vs {b.size}, first diff {d[:5]}")
+    y = P.decompress(gpu, device="cuda:0")
+    yo = oracle.decompress(ref)
+    assert np.array_equal(y.reshape(-1).view(np.uint32), yo.reshape(-1).view(np.uint32))
+    bound = kw.get("b_r", 1e-2) * kw.get("repair_factor", 1.5)
+    _check_bound(x, y, bound)
+    return info, len(gpu)
+
+
+@pytest.mark.parametrize("b_r,rf", [(1e-2, 1.0), (1e-2, 1.5)])
+def test_c1_full(codec, oracle, b_r, rf):
+    _parity(codec, oracle, _field("C1"), b_r=b_r, repair_factor=rf, S=1)
+
+
+@pytest.mark.parametrize("b_r,rf", [(1e-2, 1.0), (1e-3, 1.0), (1e-2, 1.5)])
+def test_c2_full(codec, oracle, b_r, rf):
+    _parity(codec, oracle, _field("C2"), b_r=b_r, repair_factor=rf)
+
+
+def test_c3_crop(codec, oracle):
+    _parity(codec, oracle, _field("C3", (64, 256, 512)), b_r=1e-2, repair_factor=1.0)
+
+
+@pytest.mark.parametrize("b_r", [1e-2, 1e-4])
+def test_c4_crop(codec, oracle, b_r):
+    _parity(codec, oracle, _field("C4", (30, 200, 300)), b_r=b_r, repair_factor=1.0)
+
+
+@pytest.mark.parametrize("shape", [(1, 1), (1, 7), (7, 1), (2, 2), (33, 257), (300, 7), (257, 513), (31, 1000)])
+def test_edge_shapes(codec, oracle, shape):
+    rng = np.random.default_rng(sum(shape))
+    x = (rng.normal(0, 1, shape) * 10).astype(np.float32)
+    _parity(codec, oracle, x, b_r=1e-2, repair_factor=1.0)
+
+
+@pytest.mark.parametrize("br,bc,pr", [(64, 128, 16), (32, 32, 8), (100, 60, 7), (256, 256, 32), (512, 64, 32)])
+def test_block_geometries(codec, oracle, br, bc, pr):
+    x = _field("C2", (300, 500))
+    _parity(codec, oracle, x, b_r=1e-2, repair_factor=1.0, block_rows=br, block_cols=bc, partition_rows=pr)
+
+
+def test_all_zero_and_constant(codec, oracle):
+    _parity(codec, oracle, np.zeros((300, 300), np.float32))
+    _parity(codec, oracle, np.full((200, 300), -2.5, np.float32))
+
+
+def test_subnormals_and_extremes(codec, oracle):
+    rng = np.random.default_rng(4)
+    x = (rng.choice([-1, 1], (130, 140)) * 10.0 ** rng.uniform(-37.9, 38.4, (130, 140))).astype(np.float32)
+    x[::7, ::5] = np.float32(1e-42)         # subnormal -> reclassified zero
+    x[3, 3] = np.finfo(np.float32).max
+    x[4, 4] = -np.finfo(np.float32).max
+    x[5, 5] = np.finfo(np.float32).tiny      # == eps0 -> zero (<=)
+    x[6, 6] = np.nextafter(np.finfo(np.float32).tiny, np.float32(1))
+    _parity(codec, oracle, x, b_r=1e-3, repair_factor=1.0)
+
+
+def test_white_noise_adversarial(codec, oracle):
+    rng = np.random.default_rng(8)
+    x = (rng.choice([-1, 1], (256, 300)) * 10.0 ** rng.uniform(-20, 20, (256, 300))).astype(np.float32)
+    x[rng.random(x.shape) < 0.1] = 0
+    _parity(codec, oracle, x, b_r=1e-4, repair_factor=1.0)
+
+
+@pytest.mark.parametrize("m", [4, 9, 16])
+def test_fixed_m(codec, oracle, m):
+    _parity(codec, oracle, _field("C2", (300, 400)), b_r=1e-2, repair_factor=1.0, m=m)
+
+
+def test_nonfinite_input_raises(codec):
+    import paper_2309_09778_b200 as P
+    from paper_2309_09778_b200 import errors as E
+    x = np.ones((64, 64), np.float32)
+    x[3, 4] = np.nan
+    with pytest.raises(E.NonFiniteInput):
+        P.compress(x, device="cuda:0")
+    x[3, 4] = np.inf
+    with pytest.raises(E.NonFiniteInput):
+        P.compress(x, device="cuda:0")
+
+
+def test_config_errors(codec):
+    import paper_2309_09778_b200 as P
+    from paper_2309_09778_b200 import errors as E
+    for br in (0.0, 1.0, -1e-3):
+        with pytest.raises(E.ConfigError):
+            P.compress(np.ones((8, 8), np.float32), rel_error=br, device="cuda:0")
+
+
+def test_decompress_corrupted_payload(codec, oracle):
+    """Flipped payload bits surface as coding/container errors, never a crash."""
+    import paper_2309_09778_b200 as P
+    from paper_2309_09778_b200 import errors as E
+    x = _field("C2", (256, 256))
+    buf, _ = oracle.compress(x, oracle.OracleConfig(b_r=1e-2))
+    a = bytearray(buf)
+    for k in range(1, 21):  # AC7: 20 mutated fixtures
+        b = bytearray(a)
+        pos = len(b) - 37 * k
+        b[pos] ^= 0xFF
+        try:
+            y = P.decompress(bytes(b), device="cuda:0")
+            assert y.shape == (256, 256)
+        except E.PermezError:
+            pass
+
+
+def test_log2_device_matches_oracle(oracle):
+    """Device CR log2 for f32 inputs vs the oracle on 2^20 random floats."""
+    import ctypes
+    from paper_2309_09778_b200 import _native as N
+    lib = N.load()
+    rng = np.random.default_rng(1)
+    bits = rng.integers(0x00800000, 0x7f7fffff, 1 << 20, dtype=np.uint32)
+    xs = bits.view(np.float32)
+    dx = torch.from_numpy(xs).cuda()
+    out = torch.empty(xs.size, dtype=torch.float64, device="cuda")
+    amb = torch.zeros(1, dtype=torch.int32, device="cuda")
+    s = lib.pmz_log2_f32_batch(ctypes.c_void_p(dx.data_ptr()), xs.size, ctypes.c_void_p(out.data_ptr()),
+                               ctypes.c_void_p(amb.data_ptr()), None)
+    assert s == 0
+    torch.cuda.synchronize()
+    got = out.cpu().numpy()
+    ref = np.array([oracle.log2(float(v)) for v in xs[:200000]])
+    assert np.array_equal(got[:200000], ref)
+    assert int(amb.item()) == 0
+
+
+@pytest.mark.slow
+def test_log2_exhaustive_no_ambiguity():
+    """All 2^31 - 2^23 positive normal finite floats: the fast path never needs
+    an undecided rounding (amb == 0) -- the device log2 is provably CR given
+    its error bound."""
+    import ctypes
+    from paper_2309_09778_b200 import _native as N
+    lib = N.load()
+    chunk = 1 << 28
+    amb = torch.zeros(1, dtype=torch.int32, device="cuda")
+    out = torch.empty(chunk, dtype=torch.float64, device="cuda")
+    start = 0x00800000
+    while start < 0x7f800000:
+        n = min(chunk, 0x7f800000 - start)
+        xs = torch.arange(start, start + n, dtype=torch.int64, device="cuda").to(torch.int32).view(torch.float32)
+        assert lib.pmz_log2_f32_batch(ctypes.c_void_p(xs.data_ptr()), n, ctypes.c_void_p(out.data_ptr()),
+                                      ctypes.c_void_p(amb.data_ptr()), None) == 0
+        start += n
+    torch.cuda.synchronize()
+    assert int(amb.item()) == 0
