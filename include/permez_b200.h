@@ -197,7 +197,8 @@ PMZ_API int pmz_inverse_map(const double *d_v, uint64_t n, const double *params1
 
 /* CR log2 of float32 values (exhaustive-check helper, see tests). Writes the
  * double result; counts undecided roundings into *d_amb. */
-PMZ_API int pmz_log2_f32_batch(const float *d_x, uint64_t n, double *d_out, uint32_t *d_amb, void *stream);
+PMZ_API int pmz_log2_f32_batch(const float *d_x, uint64_t n, double *d_out, uint32_t *d_amb, int variant,
+                               void *stream);
 
 #ifdef __cplusplus
 }

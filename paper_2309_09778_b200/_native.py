@@ -72,7 +72,7 @@ _SIGS = {
     "pmz_transform_params": (c_int32, [VP, ctypes.POINTER(Geom), ctypes.POINTER(Params), VP, VP, VP, c_uint64, VP]),
     "pmz_forward_map": (c_int32, [VP, c_uint64, VP, VP, VP]),
     "pmz_inverse_map": (c_int32, [VP, c_uint64, VP, VP, VP, VP]),
-    "pmz_log2_f32_batch": (c_int32, [VP, c_uint64, VP, VP, VP]),
+    "pmz_log2_f32_batch": (c_int32, [VP, c_uint64, VP, VP, c_int32, VP]),
 }
 
 EXPORTS = tuple(_SIGS)

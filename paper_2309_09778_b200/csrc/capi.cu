@@ -8,6 +8,9 @@
 
 #include "common.cuh"
 #include "compress.cuh"
+#include "blockc.cuh"
+#include "wsc.cuh"
+#include "dsc.cuh"
 #include "decompress.cuh"
 #include "encode.cuh"
 
@@ -57,6 +60,17 @@ Geom geom_of(const pmz_params *p, const pmz_geom *g) {
                    (int64_t)g->block_row0);
 }
 
+// weights equal init_model(S) -> constant-folded predictor
+int is_init_model(int S, const double *w1, const double *w2) {
+  if (w2[0] != 0.5 || w2[1] != 0.5) return 0;
+  static const double i3[8] = {1, 1, 1, 1, -1, -1, 0, 0}, i1[4] = {1, 1, 0, 0};
+  const double *ref = S == 3 ? i3 : i1;
+  int n = S == 3 ? 8 : 4;
+  for (int i = 0; i < n; i++)
+    if (w1[i] != ref[i] || std::signbit(w1[i]) != std::signbit(ref[i])) return 0;
+  return S;
+}
+
 KParams kparams(const pmz_params *p) {
   KParams k{};
   k.b_r = p->b_r;
@@ -75,6 +89,10 @@ KParams kparams(const pmz_params *p) {
   k.block_cols = p->block_cols;
   k.partition_rows = p->partition_rows;
   k.m_fixed = p->m;
+  k.inv_two_ba = 1.0 / (2.0 * p->b_a);
+  k.dpos = std::log2(1.0 + p->repair_t);
+  k.dneg = std::log2(1.0 - p->repair_t);
+  k.init_model = is_init_model(p->S, p->w1, p->w2);
   return k;
 }
 
@@ -132,6 +150,37 @@ int launch_check() {
 }
 
 constexpr int kNT = 256;
+
+template <int PK>
+int launch_ws(const KParams &k, unsigned grid, cudaStream_t st, const float *x, const Geom &G, void *d_ws,
+              const WsLayout &L) {
+  CK(cudaFuncSetAttribute(k_compress_ws<PK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWscSmem));
+  k_compress_ws<PK><<<grid, kPPC * 64, kWscSmem, st>>>(x, G, k, at<BlkP>(d_ws, L.blkp), at<WsStatus>(d_ws, L.status),
+                                                       at<uint16_t>(d_ws, L.codes), at<double>(d_ws, L.balv),
+                                                       at<double>(d_ws, L.anchors),
+                                                       at<unsigned long long>(d_ws, L.part_zeros));
+  return PMZ_OK;
+}
+
+template <int MODE, int PK>
+int launch_blocks_pk(const KParams &k, unsigned grid, cudaStream_t st, const float *x, const Geom &G,
+                     const int64_t *ids, BlkP *blkp, WsStatus *S, uint16_t *codes, double *balv, double *anchors,
+                     unsigned long long *pz, unsigned long long *cov) {
+  CK(cudaFuncSetAttribute(k_compress_blocks<MODE, PK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)kBlockSmem));
+  k_compress_blocks<MODE, PK><<<grid, kBW * 32, kBlockSmem, st>>>(x, G, k, ids, blkp, S, codes, balv, anchors, pz,
+                                                                   cov);
+  return PMZ_OK;
+}
+
+template <int MODE>
+int launch_blocks(const KParams &k, unsigned grid, cudaStream_t st, const float *x, const Geom &G,
+                  const int64_t *ids, BlkP *blkp, WsStatus *S, uint16_t *codes, double *balv, double *anchors,
+                  unsigned long long *pz, unsigned long long *cov) {
+  if (k.init_model == 3) return launch_blocks_pk<MODE, 3>(k, grid, st, x, G, ids, blkp, S, codes, balv, anchors, pz, cov);
+  if (k.init_model == 1) return launch_blocks_pk<MODE, 1>(k, grid, st, x, G, ids, blkp, S, codes, balv, anchors, pz, cov);
+  return launch_blocks_pk<MODE, 0>(k, grid, st, x, G, ids, blkp, S, codes, balv, anchors, pz, cov);
+}
 
 }  // namespace
 
@@ -205,10 +254,9 @@ int pmz_compress_analyze(const float *d_in, const pmz_geom *g, const pmz_params 
   // zero status, coverage and histogram (contiguous at the front)
   CK(cudaMemsetAsync(d_ws, 0, L.lens, st));
   if (G.nblocks == 0) return PMZ_OK;
-  k_block_params<kNT><<<(unsigned)G.nblocks, kNT, 0, st>>>(d_in, G, k, at<BlkP>(d_ws, L.blkp),
-                                                            at<WsStatus>(d_ws, L.status));
+  k_stats<<<(unsigned)G.nblocks, kBW * 32, 0, st>>>(d_in, G, k, at<BlkP>(d_ws, L.blkp), at<WsStatus>(d_ws, L.status));
   if (p->m == 0 && n_val > 0) {
-    dim3 grid(16, (unsigned)n_val);
+    dim3 grid(128, (unsigned)n_val);
     k_coverage<kNT><<<grid, kNT, 0, st>>>(d_in, G, k, at<BlkP>(d_ws, L.blkp), d_val,
                                           at<unsigned long long>(d_ws, L.cov), at<WsStatus>(d_ws, L.status));
   }
@@ -226,10 +274,11 @@ int pmz_compress_codes(const float *d_in, const pmz_geom *g, const pmz_params *p
   KParams k = kparams(p);
   k_select_m<<<1, 32, 0, st>>>(at<unsigned long long>(d_ws, L.cov), k, at<WsStatus>(d_ws, L.status));
   if (G.nparts > 0) {
-    unsigned grid = (unsigned)((G.nparts + kWarps - 1) / kWarps);
-    k_wavefront<kWarps><<<grid, kWarps * 32, 0, st>>>(
-        d_in, G, k, at<BlkP>(d_ws, L.blkp), at<WsStatus>(d_ws, L.status), at<uint16_t>(d_ws, L.codes),
-        at<double>(d_ws, L.balv), at<double>(d_ws, L.anchors), at<unsigned long long>(d_ws, L.part_zeros));
+    const unsigned grid = (unsigned)((G.nparts + kPPC - 1) / kPPC);
+    if (k.init_model == 3) s = launch_ws<3>(k, grid, st, d_in, G, d_ws, L);
+    else if (k.init_model == 1) s = launch_ws<1>(k, grid, st, d_in, G, d_ws, L);
+    else s = launch_ws<0>(k, grid, st, d_in, G, d_ws, L);
+    if (s) return s;
   }
   if (n_val > 0) {
     dim3 grid(16, (unsigned)n_val);
@@ -312,7 +361,7 @@ int pmz_compress_finish(const pmz_geom *g, const pmz_params *p, int write_header
   if (write_header)
     k_write_header<<<1, 256, 0, st>>>(d_out, G, k, g->global_rows, at<uint8_t>(d_ws, L.lens), S);
   if (G.nblocks > 0)
-    k_write_records<kWarps><<<(unsigned)G.nblocks, kWarps * 32, 0, st>>>(
+    k_write_records<8><<<(unsigned)G.nblocks, 8 * 32, 0, st>>>(
         G, at<BlkP>(d_ws, L.blkp), at<uint16_t>(d_ws, L.codes), at<double>(d_ws, L.balv),
         at<double>(d_ws, L.anchors), at<unsigned long long>(d_ws, L.part_bits),
         at<unsigned long long>(d_ws, L.part_zeros), at<unsigned long long>(d_ws, L.rec_off),
@@ -452,7 +501,7 @@ int pmz_index_blocks(const uint8_t *h, uint64_t n, const pmz_header *hd, uint64_
 namespace {
 struct DecLayout {
   size_t status, blkp, part_bits, part_off, part_zeros, anchors, bal_off, pay_off, blk_nbal, tab, sym, lut, codes,
-      total;
+      large, total;
 };
 DecLayout dec_layout(const Geom &g) {
   DecLayout L{};
@@ -475,9 +524,21 @@ DecLayout dec_layout(const Geom &g) {
   L.sym = take(2 * kMaxAlpha);
   L.lut = take(4 << kLutBits);
   L.codes = take(2 * (size_t)(g.rows * g.cols));
+  L.large = take(4 * (size_t)(g.nparts + 1));
   L.total = o;
   return L;
 }
+template <int PK>
+int launch_recon(const KParams &k, unsigned grid, cudaStream_t st, const uint8_t *d_buf, const Geom &G, int m,
+                 void *d_ws, const DecLayout &L, float *d_out) {
+  CK(cudaFuncSetAttribute(k_reconstruct_ws<PK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDscSmem));
+  k_reconstruct_ws<PK><<<grid, kPPC * 64, kDscSmem, st>>>(
+      d_buf, G, k, m, at<BlkP>(d_ws, L.blkp), at<uint16_t>(d_ws, L.codes), at<double>(d_ws, L.anchors),
+      at<unsigned long long>(d_ws, L.part_zeros), at<unsigned long long>(d_ws, L.bal_off),
+      at<unsigned long long>(d_ws, L.blk_nbal), d_out, at<WsStatus>(d_ws, L.status));
+  return PMZ_OK;
+}
+
 Geom hdr_geom(const pmz_header *h) {
   return make_geom((int64_t)h->rows, (int64_t)h->cols, (int)h->block_rows, (int)h->block_cols,
                    (int)h->partition_rows, 0);
@@ -497,6 +558,8 @@ KParams hdr_kparams(const pmz_header *h, double b_a) {
   k.block_cols = (int)h->block_cols;
   k.partition_rows = (int)h->partition_rows;
   k.m_fixed = (int)h->m;
+  k.inv_two_ba = 1.0 / (2.0 * b_a);
+  k.init_model = is_init_model(k.S, k.w1, k.w2);
   return k;
 }
 }  // namespace
@@ -525,15 +588,27 @@ int pmz_decompress(const uint8_t *d_buf, uint64_t n, const pmz_header *hdr, doub
     k_dec_tables<<<1, 1024, 0, st>>>(d_buf + hdr->lens_offset, (int)hdr->m, at<DecTab>(d_ws, L.tab),
                                      at<uint16_t>(d_ws, L.sym), at<unsigned>(d_ws, L.lut), S);
     unsigned grid = (unsigned)((G.nparts + kWarps - 1) / kWarps);
-    k_decode<kWarps><<<grid, kWarps * 32, 0, st>>>(
+    using Small = DecCfg<2, false>;
+    using Large = DecCfg<1, true>;
+    CK(cudaMemsetAsync(at<unsigned>(d_ws, L.large), 0, 4, st));
+    CK(cudaFuncSetAttribute(k_decode<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Small::kSmem));
+    CK(cudaFuncSetAttribute(k_decode<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Large::kSmem));
+    k_decode<2, false><<<(unsigned)((G.nparts + 1) / 2), 64, Small::kSmem, st>>>(
         d_buf, G, at<BlkP>(d_ws, L.blkp), at<DecTab>(d_ws, L.tab), at<uint16_t>(d_ws, L.sym),
         at<unsigned>(d_ws, L.lut), at<unsigned long long>(d_ws, L.part_bits),
         at<unsigned long long>(d_ws, L.part_off), at<unsigned long long>(d_ws, L.pay_off),
-        at<uint16_t>(d_ws, L.codes), at<unsigned long long>(d_ws, L.part_zeros), S);
-    k_reconstruct<kWarps><<<grid, kWarps * 32, 0, st>>>(
-        d_buf, G, k, (int)hdr->m, at<BlkP>(d_ws, L.blkp), at<uint16_t>(d_ws, L.codes), at<double>(d_ws, L.anchors),
-        at<unsigned long long>(d_ws, L.part_zeros), at<unsigned long long>(d_ws, L.bal_off),
-        at<unsigned long long>(d_ws, L.blk_nbal), d_out, S);
+        at<uint16_t>(d_ws, L.codes), at<unsigned long long>(d_ws, L.part_zeros), at<unsigned>(d_ws, L.large), S);
+    k_decode<1, true><<<296, 32, Large::kSmem, st>>>(
+        d_buf, G, at<BlkP>(d_ws, L.blkp), at<DecTab>(d_ws, L.tab), at<uint16_t>(d_ws, L.sym),
+        at<unsigned>(d_ws, L.lut), at<unsigned long long>(d_ws, L.part_bits),
+        at<unsigned long long>(d_ws, L.part_off), at<unsigned long long>(d_ws, L.pay_off),
+        at<uint16_t>(d_ws, L.codes), at<unsigned long long>(d_ws, L.part_zeros), at<unsigned>(d_ws, L.large), S);
+    const unsigned rgrid = (unsigned)((G.nparts + kPPC - 1) / kPPC);
+    int s2;
+    if (k.init_model == 3) s2 = launch_recon<3>(k, rgrid, st, d_buf, G, (int)hdr->m, d_ws, L, d_out);
+    else if (k.init_model == 1) s2 = launch_recon<1>(k, rgrid, st, d_buf, G, (int)hdr->m, d_ws, L, d_out);
+    else s2 = launch_recon<0>(k, rgrid, st, d_buf, G, (int)hdr->m, d_ws, L, d_out);
+    if (s2) return s2;
   }
   int s = launch_check();
   if (s) return s;
@@ -591,7 +666,7 @@ __global__ void k_forward(const double *x, uint64_t n, P10 q, double *v, unsigne
   if (xi == 0.0) { v[i] = q.v[6]; return; }
   double a = fabs(xi), lg;
   float af = (float)a;
-  if ((double)af == a && af >= 1.17549435e-38f && isfinite(af)) lg = pmz_log2_f32(a, amb);
+  if ((double)af == a && af >= 1.17549435e-38f && isfinite(af)) lg = pmz_log2_f32_fast(a, amb);
   else if (a >= 0x1p-1022 && isfinite(a)) lg = pmz_log2_d(a, amb);
   else lg = log2(a);  // subnormal doubles / inf: outside the path's domain
   v[i] = xi > 0.0 ? __dadd_rn(lg, q.v[8]) : __dadd_rn(lg, q.v[9]);
@@ -625,14 +700,16 @@ int pmz_inverse_map(const double *d_v, uint64_t n, const double *params10, doubl
   return launch_check();
 }
 
-__global__ void k_log2_batch(const float *x, uint64_t n, double *out, unsigned *amb) {
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
-    out[i] = pmz_log2_f32((double)x[i], amb);
+__global__ void k_log2_batch(const float *x, uint64_t n, double *out, unsigned *amb, int variant) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const double a = (double)x[i];
+    out[i] = variant == 0 ? pmz_log2_f32_fast(a, amb) : (variant == 1 ? pmz_log2_f32(a, amb) : pmz_log2_d(a, amb));
+  }
 }
 
-int pmz_log2_f32_batch(const float *d_x, uint64_t n, double *d_out, uint32_t *d_amb, void *stream) {
+int pmz_log2_f32_batch(const float *d_x, uint64_t n, double *d_out, uint32_t *d_amb, int variant, void *stream) {
   if (n == 0) return PMZ_OK;
-  k_log2_batch<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(d_x, n, d_out, d_amb);
+  k_log2_batch<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(d_x, n, d_out, d_amb, variant);
   return launch_check();
 }
 

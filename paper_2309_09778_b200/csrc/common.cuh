@@ -14,6 +14,9 @@ constexpr int kWarps = 4;  // warps per CTA for per-partition kernels
 // Kernel-parameter copy of pmz_params (passed by value -> constant bank).
 struct KParams {
   double b_r, b_a, two_ba, onepbr2, eps0, repair_t, slope, coverage_target;
+  double inv_two_ba;       // RN(1 / (2 b_a)) for the filtered quantizer
+  double dpos, dneg;       // log2(1 + t), log2(1 - t): violation thresholds in the log domain
+  int init_model;          // weights equal init_model: constant-folded predictor
   double w1[8], w2[2];
   int S, H, block_rows, block_cols, partition_rows, m_fixed;
 };
@@ -82,6 +85,26 @@ __device__ __forceinline__ double predict(const KParams &k, double s0, double s1
   return __dadd_rn(__dmul_rn(a0, k.w2[0]), __dmul_rn(a1, k.w2[1]));
 }
 
+// predict with compile-time init_model weights: the same D3
+// expression with constant weights, which the compiler folds (x*1 -> x,
+// x*-1 -> -x; the +0.0 bias is kept, so even the sign of zero is identical).
+template <int S>
+__device__ __forceinline__ double predict_init(double slope, double s0, double s1, double s2) {
+  double h;
+  if (S == 3) h = __dadd_rn(__dadd_rn(__dadd_rn(s0, s1), -s2), 0.0);
+  else h = __dadd_rn(s0, 0.0);
+  const double a = h < 0.0 ? __dmul_rn(slope, h) : h;
+  const double a2 = __dmul_rn(a, 0.5);
+  return __dadd_rn(a2, a2);
+}
+
+template <int PK>  // 0: general weights, 3 / 1: init_model with S = 3 / 1
+__device__ __forceinline__ double predict_k(const KParams &k, double s0, double s1, double s2) {
+  if (PK == 3) return predict_init<3>(k.slope, s0, s1, s2);
+  if (PK == 1) return predict_init<1>(k.slope, s0, s1, s2);
+  return predict(k, s0, s1, s2);
+}
+
 // quantize (D5): center + round_half_away(err / (2 b_a)).
 __device__ __forceinline__ int quantize(double err, double two_ba, int m) {
   double q = __ddiv_rn(err, two_ba);
@@ -89,6 +112,20 @@ __device__ __forceinline__ int quantize(double err, double two_ba, int m) {
   if (c >= 1.0 && c <= (double)((1 << m) - 1)) return (int)c;
   return 0;
 }
+// Same result as quantize() without the IEEE division: q' = err * RN(1/(2 b_a))
+// differs from RN(err / (2 b_a)) by < 2^-51 |q|, so round(q') is exact unless q'
+// sits within 2^-48 |q| of a half-integer, where the division decides.
+__device__ __forceinline__ int quantize_fast(double err, const KParams &k, int m) {
+  const double q = __dmul_rn(err, k.inv_two_ba);
+  const double aq = fabs(q);
+  if (aq >= 65536.0) return 0;  // out of range for every m <= 16
+  const double f = __dsub_rn(aq, trunc(aq));
+  if (__builtin_expect(fabs(__dsub_rn(f, 0.5)) <= aq * 0x1p-48, 0)) return quantize(err, k.two_ba, m);
+  const double c = __dadd_rn((double)(1 << (m - 1)), round(q));
+  if (c >= 1.0 && c <= (double)((1 << m) - 1)) return (int)c;
+  return 0;
+}
+
 // smallest m in [4,16] covering round(q); 17 = none (select_m)
 __device__ __forceinline__ int m_required(double err, double two_ba) {
   double a = fabs(round(__ddiv_rn(err, two_ba)));
@@ -110,7 +147,7 @@ __device__ __forceinline__ float zfloor(float x) {
 // forward_map (transform.py:170-185) of a zero-floored f32 element.
 __device__ __forceinline__ double fwd(float xz, const BlkP &p, unsigned *amb) {
   if (xz == 0.0f) return p.zero_code;
-  double lg = pmz_log2_f32((double)fabsf(xz), amb);
+  double lg = pmz_log2_f32_fast((double)fabsf(xz), amb);
   return xz > 0.0f ? __dadd_rn(lg, p.lg_pos) : __dadd_rn(lg, p.lg_neg);
 }
 
@@ -126,6 +163,31 @@ __device__ __forceinline__ bool violates(float xh, float xz, double t) {
   if (xz == 0.0f) return xh != 0.0f;
   double d = fabs(__dsub_rn((double)xh, (double)xz));
   return __ddiv_rn(d, fabs((double)xz)) > t;
+}
+
+// verify_and_repair bound check (D8) without exp2 / division in the common
+// case.  With d = vhat - v, log2(xhat/x) = d + e where |e| <= 2^-24/ln2 + 2^-43
+// (f32 rounding of xhat plus the rounding of v, vhat and their difference),
+// so xhat is within the bound when dneg + mu < d < dpos - mu and out of it when
+// d > dpos + mu or d < dneg - mu (mu = 2^-20).  Sign crossings, the zero
+// threshold, zeros and f32 range extremes always take the exact path.
+// Returns 1 = violation, 0 = fine.
+__device__ __forceinline__ int check_filtered(double vhat, double v, float xz, const BlkP &P, const KParams &k,
+                                              unsigned *amb) {
+  const float ax = fabsf(xz);
+  if (__builtin_expect(ax > 0.0f, 1)) {
+    const bool pos = xz > 0.0f;
+    const bool side_ok = pos ? (vhat <= P.boundary) : (vhat > P.boundary);
+    if (side_ok && vhat > P.zero_threshold && ax < 1.7e38f && ax > 4.7e-38f) {
+      const double d = __dsub_rn(vhat, v);
+      const double mu = 0x1p-20;
+      if (d < __dsub_rn(k.dpos, mu) && d > __dadd_rn(k.dneg, mu)) return 0;
+      if (d > __dadd_rn(k.dpos, mu) || d < __dsub_rn(k.dneg, mu)) return 1;
+    }
+  } else if (vhat <= P.zero_threshold) {
+    return 0;  // x = 0 decodes to exactly 0
+  }
+  return violates(inv_f32(vhat, P, amb), xz, k.repair_t) ? 1 : 0;
 }
 
 // ---------------------------------------------------------------------------

@@ -97,16 +97,66 @@ __global__ void __launch_bounds__(1024) k_codebook(const unsigned long long *his
   __syncthreads();
   for (int i = threadIdx.x; i < n; i += blockDim.x) lens[keys[i] & 0x1ffff] = (uint8_t)A[i];
   __syncthreads();
+  __shared__ unsigned s_cnt[64], s_next[64];
+  __shared__ int s_maxl;
+  if (threadIdx.x < 64) s_cnt[threadIdx.x] = 0;
+  if (threadIdx.x == 0) s_maxl = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    atomicAdd(&s_cnt[lens[i]], 1u);
+    atomicMax(&s_maxl, (int)lens[i]);
+  }
+  __syncthreads();
+  const int maxl = s_maxl;
   if (threadIdx.x == 0) {
-    unsigned cnt[64] = {0}, next[64];
-    int maxl = 0;
-    for (int s = 0; s < n; s++) { cnt[lens[s]]++; if (lens[s] > maxl) maxl = lens[s]; }
     st->max_len = maxl;
-    if (maxl > 32) { atomicOr(&st->err_bits, 1u << (-PMZ_ERR_UNASSIGNED)); return; }
     unsigned long long c = 0;
-    cnt[0] = 0;
-    for (int l = 1; l <= maxl; l++) { c = (c + cnt[l - 1]) << 1; next[l] = (unsigned)c; }
-    for (int s = 0; s < n; s++) cw[s] = next[lens[s]]++;
+    s_cnt[0] = 0;
+    for (int l = 1; l <= maxl && l < 64; l++) { c = (c + s_cnt[l - 1]) << 1; s_next[l] = (unsigned)c; }
+  }
+  __syncthreads();
+  if (maxl > 32) {
+    if (threadIdx.x == 0) atomicOr(&st->err_bits, 1u << (-PMZ_ERR_UNASSIGNED));
+    return;
+  }
+  // canonical codewords in (length, code) order: code = first[len] + rank of the
+  // symbol among equal-length symbols; ranks via the sorted order (keys hold the
+  // symbol; the leaf order by (freq, sym) is not the code order, so count
+  // per length with a block-wide scan over symbols in index order).
+  __shared__ unsigned s_wsum[32][33];
+  const int nt = blockDim.x, tid = threadIdx.x;
+  const int per = (n + nt - 1) / nt;
+  const int lo = tid * per, hi = min(n, lo + per);
+  // each thread counts lengths in its contiguous symbol range (lengths <= 32)
+  unsigned myc[33];
+#pragma unroll
+  for (int l = 0; l <= 32; l++) myc[l] = 0;
+  for (int i = lo; i < hi; i++) myc[lens[i]]++;
+  // exclusive prefix over threads, per length: warp scans then warp totals
+  const int wid = tid >> 5, ln = tid & 31;
+  unsigned mypre[33];
+#pragma unroll
+  for (int l = 1; l <= 32; l++) {
+    unsigned v = myc[l], incl = v;
+    for (int d = 1; d < 32; d <<= 1) {
+      const unsigned t = __shfl_up_sync(0xffffffffu, incl, d);
+      if (ln >= d) incl += t;
+    }
+    mypre[l] = incl - v;
+    if (ln == 31) s_wsum[wid][l] = incl;
+  }
+  __syncthreads();
+  if (tid < 33 && tid >= 1) {
+    unsigned acc = 0;
+    for (int w = 0; w < nt / 32; w++) { const unsigned t = s_wsum[w][tid]; s_wsum[w][tid] = acc; acc += t; }
+  }
+  __syncthreads();
+  unsigned nxt[33];
+#pragma unroll
+  for (int l = 1; l <= 32; l++) nxt[l] = s_next[l] + s_wsum[wid][l] + mypre[l];
+  for (int i = lo; i < hi; i++) {
+    const int l = lens[i];
+    cw[i] = l ? nxt[l]++ : 0;
   }
 }
 
@@ -127,10 +177,38 @@ __global__ void __launch_bounds__(NW * 32) k_part_bits(Geom g, const BlkP *__res
   if (!blkp[b].trivial) {
     BlockBox bb = block_box(g, b);
     int pr0 = pi * g.prow, R = min(g.prow, bb.br - pr0), C = bb.bc;
-    for (int r = 0; r < R; r++) {
-      const uint16_t *crow = codes + (bb.r0 + pr0 + r) * g.cols + bb.c0;
-      for (int c = lane; c < C; c += 32)
-        if (r | c) bits += __ldg(&lens[crow[c]]);
+    const uint16_t *cp = codes + (bb.r0 + pr0) * g.cols + bb.c0;
+    if ((g.cols & 7) == 0 && (C & 7) == 0) {
+      const int vpr = C >> 3, nv = R * vpr;  // 8 codes per 16-byte vector
+      for (int i0 = lane; i0 < nv; i0 += 128) {
+        uint4 q[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          const int i = i0 + 32 * u;
+          if (i < nv) {
+            const int r = i / vpr, c = (i - r * vpr) << 3;
+            q[u] = __ldg(reinterpret_cast<const uint4 *>(cp + (int64_t)r * g.cols + c));
+          } else {
+            q[u] = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);  // anchor marker -> len 0 below
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          const unsigned w[4] = {q[u].x, q[u].y, q[u].z, q[u].w};
+#pragma unroll
+          for (int h = 0; h < 4; h++) {
+            const unsigned a = w[h] & 0xffff, c2 = w[h] >> 16;
+            if (a != 0xffff) bits += __ldg(&lens[a]);
+            if (c2 != 0xffff) bits += __ldg(&lens[c2]);
+          }
+        }
+      }
+    } else {
+      for (int r = 0; r < R; r++) {
+        const uint16_t *crow = cp + (int64_t)r * g.cols;
+        for (int c = lane; c < C; c += 32)
+          if (r | c) bits += __ldg(&lens[crow[c]]);
+      }
     }
     for (int o = 16; o > 0; o >>= 1) bits += __shfl_xor_sync(0xffffffffu, bits, o);
   }
@@ -208,32 +286,32 @@ __global__ void k_write_header(uint8_t *out, Geom g, KParams k, uint64_t global_
   for (int i = threadIdx.x; i < n; i += blockDim.x) L[i] = lens[i];
 }
 
-// MSB-first OR of a codeword (len <= 32) at bit position `bit` of byte stream `base`.
-__device__ __forceinline__ void or_bits(uint8_t *base, unsigned long long bit, unsigned code, int len) {
+// MSB-first OR of a codeword (len <= 32) into a little-endian u32 smem window
+// at window bit position `bit` (bit i of the stream = bit 7 - i%8 of byte i/8).
+__device__ __forceinline__ void or_bits_smem(unsigned *win, unsigned bit, unsigned code, int len) {
   if (len == 0) return;
-  uint8_t *p = base + (bit >> 3);
-  int o = (int)(bit & 7);
-  // 64-bit big-endian window: codeword starts at window bit 63 - o
-  unsigned long long w = ((unsigned long long)code) << (64 - len - o);
-  int nbytes = (o + len + 7) >> 3;
-  // group bytes by aligned 32-bit words
-  uintptr_t a0 = (uintptr_t)p;
-  int i = 0;
-  while (i < nbytes) {
-    uintptr_t wa = (a0 + i) & ~(uintptr_t)3;
-    unsigned val = 0;
-    int j = i;
-    while (j < nbytes && (((a0 + j) & ~(uintptr_t)3) == wa)) {
-      unsigned byte = (unsigned)((w >> (56 - 8 * j)) & 0xff);
-      val |= byte << (8 * (int)((a0 + j) & 3));
-      j++;
+  const unsigned o = bit & 7;
+  const unsigned long long w = ((unsigned long long)code) << (64 - len - o);  // big-endian window
+  const int nbytes = (int)((o + len + 7) >> 3);
+  const unsigned byte0 = bit >> 3;
+#pragma unroll
+  for (int i = 0; i < 5; i++) {
+    if (i < nbytes) {
+      const unsigned by = (unsigned)((w >> (56 - 8 * i)) & 0xff);
+      if (by) {
+        const unsigned bi = byte0 + i;
+        atomicOr(&win[bi >> 2], by << (8 * (bi & 3)));
+      }
     }
-    if (val) atomicOr((unsigned *)wa, val);
-    i = j;
   }
 }
 
-// K10: write one block record per CTA (D9, D13, D15).
+constexpr int kWinWords = 1024;  // 4 KB bit-packing window per warp
+
+// K10: write one block record per CTA (D9, D13, D15).  Each warp
+// packs a partition's codewords into a shared-memory window (warp prefix sum
+// of code lengths -> bit offsets, smem atomics) and flushes finished bytes to
+// the (byte-aligned, unaligned-to-word) output with coalesced byte stores.
 template <int NW>
 __global__ void __launch_bounds__(NW * 32) k_write_records(Geom g, const BlkP *__restrict__ blkp,
                                                            const uint16_t *__restrict__ codes,
@@ -245,6 +323,9 @@ __global__ void __launch_bounds__(NW * 32) k_write_records(Geom g, const BlkP *_
                                                            const uint8_t *__restrict__ lens,
                                                            const unsigned *__restrict__ cw, uint8_t *out,
                                                            unsigned long long rec_base, WsStatus *st) {
+  __shared__ unsigned s_win[NW][kWinWords];
+  __shared__ unsigned long long s_zb[64], s_pb[64];
+  __shared__ unsigned long long s_nbal;
   count_launch(st);
   const int64_t b = blockIdx.x;
   uint8_t *base = out + rec_base + rec_off[b];
@@ -255,65 +336,105 @@ __global__ void __launch_bounds__(NW * 32) k_write_records(Geom g, const BlkP *_
   }
   const BlockBox bb = block_box(g, b);
   const int64_t p0 = first_part(g, b);
-  __shared__ unsigned long long s_zb[64], s_pb[64];
-  __shared__ unsigned long long s_nbal, s_pay;
   if (threadIdx.x == 0) {
     unsigned long long zb = 0, pb = 0;
     for (int i = 0; i < bb.np; i++) {
-      s_zb[i] = zb; s_pb[i] = pb;
+      s_zb[i] = zb;
+      s_pb[i] = pb;
       zb += part_zeros[p0 + i];
       pb += (part_bits[p0 + i] + 7) / 8;
     }
     s_nbal = zb;
-    s_pay = pb;
-    base[0] = 0;
-    put_f64(base + 1, P.factor_pos);
-    put_f64(base + 9, P.factor_neg);
-    put_u64(base + 17 + 24ull * bb.np, zb);
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < bb.np; i += blockDim.x) {
-    uint8_t *e = base + 17 + 24ull * i;
-    put_u64(e, s_pb[i] * 8);
-    put_u64(e + 8, part_bits[p0 + i]);
-    put_f64(e + 16, anchors[p0 + i]);
+  // fixed head: trivial flag, factors, partition table, balance count (coalesced bytes)
+  const unsigned head = 25 + 24u * bb.np;
+  for (unsigned i = threadIdx.x; i < head; i += blockDim.x) {
+    unsigned long long word;
+    unsigned byte;
+    if (i == 0) { base[0] = 0; continue; }
+    if (i < 17) {
+      word = __double_as_longlong(i < 9 ? P.factor_pos : P.factor_neg);
+      byte = (i - 1) & 7;
+    } else if (i < 17 + 24u * bb.np) {
+      const unsigned q = i - 17, pi = q / 24, f = (q % 24) / 8;
+      word = f == 0 ? s_pb[pi] * 8 : (f == 1 ? part_bits[p0 + pi] : __double_as_longlong(anchors[p0 + pi]));
+      byte = q & 7;
+    } else {
+      word = s_nbal;
+      byte = (i - 17 - 24u * bb.np) & 7;
+    }
+    base[i] = (uint8_t)(word >> (8 * byte));
   }
-  uint8_t *bal0 = base + 25 + 24ull * bb.np;
+  uint8_t *bal0 = base + head;
   uint8_t *pay0 = bal0 + 8ull * s_nbal;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  unsigned *win = s_win[warp];
   for (int pi = warp; pi < bb.np; pi += NW) {
     const int pr0 = pi * g.prow, R = min(g.prow, bb.br - pr0), C = bb.bc;
     uint8_t *pay = pay0 + s_pb[pi];
-    const unsigned long long nbytes = (part_bits[p0 + pi] + 7) / 8;
-    for (unsigned long long i = lane; i < nbytes; i += 32) pay[i] = 0;
+    for (int i = lane; i < kWinWords; i += 32) win[i] = 0;
     __syncwarp();
-    unsigned long long zb = s_zb[pi], bit = 0;
-    const int64_t n = (int64_t)R * C;
-    for (int64_t e0 = 0; e0 < n; e0 += 32) {
-      const int64_t e = e0 + lane;
-      int code = -1;
-      int r = 0, c = 0;
+    unsigned long long zb = s_zb[pi];
+    unsigned long long bit = 0, wbase = 0;  // partition bit position, window base (bits, multiple of 32)
+    const int n = R * C;
+    const uint16_t *cbase = codes + (bb.r0 + pr0) * g.cols + bb.c0;
+    const double *bbase = balv + (bb.r0 + pr0) * g.cols + bb.c0;
+    auto load_code = [&](int e, int &r, int &c) -> int {
+      r = 0;
+      c = 0;
       if (e < n && e > 0) {
-        r = (int)(e / C);
-        c = (int)(e - (int64_t)r * C);
-        code = codes[(bb.r0 + pr0 + r) * g.cols + bb.c0 + c];
+        r = (int)((unsigned)e / (unsigned)C);
+        c = e - r * C;
+        return __ldg(&cbase[(int64_t)r * g.cols + c]);
       }
+      return -1;
+    };
+    int nr, nc;
+    int ncode = load_code(lane, nr, nc);
+    for (int e0 = 0; e0 < n; e0 += 32) {
+      const int code = ncode, r = nr, c = nc;
+      ncode = load_code(e0 + 32 + lane, nr, nc);  // prefetch the next 32 codes
       const unsigned zmask = __ballot_sync(0xffffffffu, code == 0);
       if (code == 0) {
         const unsigned idx = __popc(zmask & ((1u << lane) - 1));
-        put_f64(bal0 + 8ull * (zb + idx), balv[(bb.r0 + pr0 + r) * g.cols + bb.c0 + c]);
+        const unsigned long long v = __double_as_longlong(bbase[(int64_t)r * g.cols + c]);
+        uint8_t *d = bal0 + 8ull * (zb + idx);
+#pragma unroll
+        for (int q = 0; q < 8; q++) d[q] = (uint8_t)(v >> (8 * q));
       }
       zb += __popc(zmask);
-      const int len = code >= 0 ? lens[code] : 0;
-      // warp inclusive scan of lengths
+      const int len = code >= 0 ? __ldg(&lens[code]) : 0;
       unsigned s = len;
       for (int o = 1; o < 32; o <<= 1) {
-        unsigned t = __shfl_up_sync(0xffffffffu, s, o);
+        const unsigned t = __shfl_up_sync(0xffffffffu, s, o);
         if (lane >= o) s += t;
       }
-      if (code >= 0) or_bits(pay, bit + (s - len), cw[code], len);
+      if (code >= 0) or_bits_smem(win, (unsigned)(bit + (s - len) - wbase), __ldg(&cw[code]), len);
       bit += __shfl_sync(0xffffffffu, s, 31);
+      __syncwarp();
+      if (bit - wbase > (unsigned long long)(kWinWords - 64) * 32) {
+        // flush the whole words below the current position
+        const unsigned nw = (unsigned)((bit - wbase) >> 5);
+        uint8_t *dst = pay + (wbase >> 3);
+        const uint8_t *wb = reinterpret_cast<const uint8_t *>(win);
+        for (unsigned i = lane; i < nw * 4; i += 32) dst[i] = wb[i];
+        __syncwarp();
+        const unsigned keep = win[nw];
+        __syncwarp();
+        for (int i = lane; i < kWinWords; i += 32) win[i] = 0;
+        __syncwarp();
+        if (lane == 0) win[0] = keep;
+        __syncwarp();
+        wbase += (unsigned long long)nw * 32;
+      }
     }
+    // final flush, zero-padded to the byte boundary (D15)
+    const unsigned nbytes = (unsigned)(((bit + 7) >> 3) - (wbase >> 3));
+    uint8_t *dst = pay + (wbase >> 3);
+    const uint8_t *wb = reinterpret_cast<const uint8_t *>(win);
+    for (unsigned i = lane; i < nbytes; i += 32) dst[i] = wb[i];
+    __syncwarp();
   }
 }
 
