@@ -175,6 +175,67 @@ __device__ __forceinline__ double pmz_log2_f32_fast(double x, unsigned *amb) {
   return pmz_log2_f32(x, amb);
 }
 
+// N-wide interleaved version of pmz_log2_f32_fast (same arithmetic per lane of
+// the batch): independent chains are issued together so the FP64 pipe sees N
+// operations in flight instead of one long dependent chain.
+template <int N>
+__device__ __forceinline__ void pmz_log2_f32_fast_n(const double (&x)[N], double (&out)[N], unsigned *amb) {
+  double m[N], r[N], Th[N], Tl[N];
+  int e[N];
+#pragma unroll
+  for (int u = 0; u < N; u++) {
+    const long long b = __double_as_longlong(x[u]);
+    e[u] = (int)((b >> 52) & 0x7ff) - 1023;
+    m[u] = __longlong_as_double((b & 0x000fffffffffffffLL) | 0x3ff0000000000000LL);
+    if (m[u] >= 1.4142135623730951) {
+      m[u] = __dmul_rn(m[u], 0.5);
+      e[u] += 1;
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < N; u++) {
+    const int i = __double2int_rn(__dmul_rn(__dsub_rn(m[u], 1.0), 1024.0));
+    const double2 *tp = reinterpret_cast<const double2 *>(&pmz_l2t3[i + PMZ_L2T3_OFF]);
+    const double2 T0 = __ldg(tp), T1 = __ldg(tp + 1);
+    r[u] = __fma_rn(m[u], T0.x, -1.0);
+    Th[u] = T0.y;
+    Tl[u] = T1.x;
+  }
+  double q[N];
+#pragma unroll
+  for (int u = 0; u < N; u++) q[u] = __fma_rn(r[u], pmz_log2_k_hi[6], pmz_log2_k_hi[5]);
+#pragma unroll
+  for (int u = 0; u < N; u++) q[u] = __fma_rn(r[u], q[u], pmz_log2_k_hi[4]);
+#pragma unroll
+  for (int u = 0; u < N; u++) q[u] = __fma_rn(r[u], q[u], pmz_log2_k_hi[3]);
+#pragma unroll
+  for (int u = 0; u < N; u++) q[u] = __fma_rn(r[u], q[u], pmz_log2_k_hi[2]);
+#pragma unroll
+  for (int u = 0; u < N; u++) q[u] = __fma_rn(r[u], q[u], pmz_log2_k_hi[1]);
+  bool ok = true;
+#pragma unroll
+  for (int u = 0; u < N; u++) {
+    const dd P = two_prod(r[u], pmz_log2_k_hi[0]);
+    const double slo = __dadd_rn(P.lo, __fma_rn(r[u], pmz_log2_k_lo[0], __dmul_rn(__dmul_rn(r[u], r[u]), q[u])));
+    const dd A = two_sum(Th[u], P.hi);
+    dd C = A;
+    if (e[u] != 0) C = fast_two_sum((double)e[u], A.hi);
+    else C.lo = 0.0;
+    const double lo = __dadd_rn(__dadd_rn(A.lo, C.lo), __dadd_rn(Tl[u], slo));
+    const dd R = fast_two_sum(C.hi, lo);
+    out[u] = R.hi;
+    if (!dd_round_certain(R, __fma_rn(fabs(R.hi), 0x1p-64, 0x1p-72))) {
+      ok = false;
+      out[u] = -INFINITY;  // marker: recompute on the precise path
+    }
+  }
+  if (__builtin_expect(!ok, 0)) {
+#pragma unroll
+    for (int u = 0; u < N; u++)
+      if (out[u] == -INFINITY) out[u] = pmz_log2_f32(x[u], amb);
+  }
+}
+
 // exp2 helpers ---------------------------------------------------------------
 
 // double-double 2^y for |y| <= 1100, error ~2^-100 relative.

@@ -48,6 +48,8 @@ __device__ __forceinline__ uint8_t xclass(float xz) {
 __device__ __forceinline__ int check_cls(double vhat, double v, int cls, const BlkP &P, const KParams &k) {
   if (cls == 1 || cls == 2) {
     const bool side_ok = cls == 1 ? (vhat <= P.boundary) : (vhat > P.boundary);
+    // wrong sign or snapped to zero: relative error >= 1 > t (when t < 1)
+    if ((!side_ok || vhat <= P.zero_threshold) && k.repair_t < 1.0) return 1;
     if (side_ok && vhat > P.zero_threshold) {
       const double d = __dsub_rn(vhat, v);
       const double mu = 0x1p-20;
@@ -59,6 +61,11 @@ __device__ __forceinline__ int check_cls(double vhat, double v, int cls, const B
   }
   return -1;  // undecided: exact path
 }
+
+#ifdef PMZ_CMP_PROFILE
+__device__ long long g_cmp_prof[65536][2][4];  // [partition][role][start, end, wait cycles, phase cycles]
+__device__ long long g_cmp_ph[65536][4];
+#endif
 
 template <int PK>
 __global__ void __launch_bounds__(kPPC * 64) k_compress_ws(const float *__restrict__ x, Geom g, KParams k,
@@ -92,6 +99,12 @@ __global__ void __launch_bounds__(kPPC * 64) k_compress_ws(const float *__restri
   const float *xp = x + (bb.r0 + pr0) * g.cols + bb.c0;
   unsigned *amb = &st->unresolved;
 
+#ifdef PMZ_CMP_PROFILE
+  long long t_start = clock64(), t_wait = 0, t_fwd = 0, t_code = 0, t_flush = 0, t_mark;
+#define TIMED_SYNC(id) { long long t0_ = clock64(); bar_sync_n(id, 64); t_wait += clock64() - t0_; }
+#else
+#define TIMED_SYNC(id) bar_sync_n(id, 64);
+#endif
   if (role == 0) {
     // ------------------------------ producer ------------------------------
     uint16_t *cpart = codes + (bb.r0 + pr0) * g.cols + bb.c0;
@@ -109,54 +122,100 @@ __global__ void __launch_bounds__(kPPC * 64) k_compress_ws(const float *__restri
     for (int kc = 0; kc < nch; kc++) {
       const int s = kc % kSlots;
       if (kc >= kSlots) {
-        bar_sync_n(bar0 + kSlots + s, 64);  // consumer done with chunk kc-3
+        TIMED_SYNC(bar0 + kSlots + s)  // consumer done with chunk kc-3
+#ifdef PMZ_CMP_PROFILE
+        t_mark = clock64();
+#endif
         flush(kc - kSlots);
         __syncwarp();
+#ifdef PMZ_CMP_PROFILE
+        t_flush += clock64() - t_mark;
+#endif
       }
+#ifdef PMZ_CMP_PROFILE
+      t_mark = clock64();
+#endif
       const int col = kc * 32 + lane;
       const bool inb = col < C;
+#if defined(PMZ_CMP_ISOLATE) && PMZ_CMP_ISOLATE == 2
+      if (kc >= 0) { __syncwarp(); bar_arrive_n(bar0 + s, 64); continue; }
+#endif
       for (int rb = 0; rb < R; rb += 8) {
         float xr[8];
 #pragma unroll
         for (int q = 0; q < 8; q++) xr[q] = (inb && rb + q < R) ? __ldg(xp + (rb + q) * g.cols + col) : 0.0f;
+        // forward_map of 8 rows with interleaved log2 chains (transform.py:170-185)
+        double ax[8], lg[8];
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+          const float xz = zfloor(xr[q]);
+          ax[q] = xz != 0.0f ? (double)fabsf(xz) : 1.0;
+        }
+        pmz_log2_f32_fast_n<8>(ax, lg, amb);
 #pragma unroll
         for (int q = 0; q < 8; q++) {
           if (rb + q < R) {
             const float xz = zfloor(xr[q]);
-            W.v[s][rb + q][lane] = inb ? fwd(xz, P, amb) : 0.0;
+            double v = P.zero_code;
+            if (xz > 0.0f) v = __dadd_rn(lg[q], P.lg_pos);
+            else if (xz < 0.0f) v = __dadd_rn(lg[q], P.lg_neg);
+            W.v[s][rb + q][lane] = inb ? v : 0.0;
             W.cls[s][rb + q][lane] = xclass(xz);
           }
         }
       }
       __syncwarp();
+#ifdef PMZ_CMP_PROFILE
+      t_fwd += clock64() - t_mark;
+      t_mark = clock64();
+#endif
       if (inb) {
         const int ps = (kc + kSlots - 1) % kSlots;
-#pragma unroll 2
-        for (int r = 0; r < R; r++) {
-          const double v = W.v[s][r][lane];
-          double w = 0.0, n = 0.0, nw = 0.0;
-          if (col > 0) w = lane > 0 ? W.v[s][r][lane - 1] : W.v[ps][r][31];
-          if (r > 0) {
-            n = W.v[s][r - 1][lane];
-            if (col > 0) nw = lane > 0 ? W.v[s][r - 1][lane - 1] : W.v[ps][r - 1][31];
+        // TRUE-surface residuals and codes, 4 rows per batch (independent chains)
+        for (int rb = 0; rb < R; rb += 4) {
+          double err[4];
+#pragma unroll
+          for (int q = 0; q < 4; q++) {
+            const int r = min(rb + q, R - 1);
+            const double v = W.v[s][r][lane];
+            double w = 0.0, n = 0.0, nw = 0.0;
+            if (col > 0) w = lane > 0 ? W.v[s][r][lane - 1] : W.v[ps][r][31];
+            if (r > 0) {
+              n = W.v[s][r - 1][lane];
+              if (col > 0) nw = lane > 0 ? W.v[s][r - 1][lane - 1] : W.v[ps][r - 1][31];
+            }
+            err[q] = __dsub_rn(v, predict_k<PK>(k, w, n, nw));
           }
-          uint16_t cd;
-          if (r == 0 && col == 0) {
-            cd = kAnc;
-            anchors[p] = v;  // forced anchor, D1
-          } else {
-            cd = (uint16_t)quantize_fast(__dsub_rn(v, predict_k<PK>(k, w, n, nw)), k, m);
+#pragma unroll
+          for (int q = 0; q < 4; q++) {
+            const int r = rb + q;
+            if (r < R) {
+              uint16_t cd;
+              if (r == 0 && col == 0) {
+                cd = kAnc;
+                anchors[p] = W.v[s][0][0];  // forced anchor, D1
+              } else {
+                cd = (uint16_t)quantize_fast(err[q], k, m);
+              }
+              W.code[s][r][lane] = cd;
+            }
           }
-          W.code[s][r][lane] = cd;
         }
       }
       __syncwarp();
+#ifdef PMZ_CMP_PROFILE
+      t_code += clock64() - t_mark;
+#endif
       bar_arrive_n(bar0 + s, 64);  // full[s]
     }
     for (int kc = max(0, nch - kSlots); kc < nch; kc++) {
-      bar_sync_n(bar0 + kSlots + kc % kSlots, 64);
+      TIMED_SYNC(bar0 + kSlots + kc % kSlots)
       flush(kc);
     }
+#ifdef PMZ_CMP_PROFILE
+    if (lane == 0 && p < 65536) { g_cmp_prof[p][0][0] = t_start; g_cmp_prof[p][0][1] = clock64(); g_cmp_prof[p][0][2] = t_wait;
+      g_cmp_ph[p][0] = t_fwd; g_cmp_ph[p][1] = t_code; g_cmp_ph[p][2] = t_flush; }
+#endif
   } else {
     // ------------------------------ consumer ------------------------------
     const int nsteps = C + R - 1;
@@ -164,9 +223,13 @@ __global__ void __launch_bounds__(kPPC * 64) k_compress_ws(const float *__restri
     double hl = 0.0, hp = 0.0;
     unsigned zeros = 0, repairs = 0;
     for (int kg = 0; kg < ngroups; kg++) {
-      if (kg < nch) bar_sync_n(bar0 + kg % kSlots, 64);  // full: chunk kg ready
+      if (kg < nch) TIMED_SYNC(bar0 + kg % kSlots)  // full: chunk kg ready
       const int t1 = min(nsteps, (kg + 1) * 32);
+#if defined(PMZ_CMP_ISOLATE) && PMZ_CMP_ISOLATE == 1
+      for (int t = t1; t < t1; t++) {
+#else
       for (int t = kg * 32; t < t1; t++) {
+#endif
         const double nhl = __shfl_up_sync(0xffffffffu, hl, 1), nhp = __shfl_up_sync(0xffffffffu, hp, 1);
         const int c = t - lane;
         if (lane < R && c >= 0 && c < C) {
@@ -210,6 +273,9 @@ __global__ void __launch_bounds__(kPPC * 64) k_compress_ws(const float *__restri
       zeros += __shfl_xor_sync(0xffffffffu, zeros, o);
       repairs += __shfl_xor_sync(0xffffffffu, repairs, o);
     }
+#ifdef PMZ_CMP_PROFILE
+    if (lane == 0 && p < 65536) { g_cmp_prof[p][1][0] = t_start; g_cmp_prof[p][1][1] = clock64(); g_cmp_prof[p][1][2] = t_wait; }
+#endif
     if (lane == 0) {
       part_zeros[p] = zeros;
       atomicAdd(&st->nbal, (unsigned long long)zeros);

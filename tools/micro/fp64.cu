@@ -1,6 +1,7 @@
 // FP64 throughput / latency microbenchmark + log2 variants throughput.
 #include <cstdio>
 #include <cuda_runtime.h>
+#include <vector>
 #include "../../paper_2309_09778_b200/csrc/dmath.cuh"
 using namespace pmz;
 
@@ -51,7 +52,10 @@ __global__ void ddiv_tput(double *out, int iters) {
   for (int i = 0; i < iters; i++) { s += __ddiv_rn(a, 1.0 + i * 1e-9); a += 1e-12; }
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
-int main() {
+int main1();
+int main2();
+int main() { main2(); return main1(); }
+int main1() {
   double *d; float *f; long long *cyc;
   cudaMalloc(&d, 1 << 28); cudaMalloc(&f, 1 << 28); cudaMalloc(&cyc, 8);
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
@@ -93,5 +97,45 @@ int main() {
     printf("log2 variant %d: %.2f G/s  (%.1f cycles/elem/SM)\n", v, n / ms / 1e6, 148 * 1.965e9 / (n / (ms * 1e-3)));
   }
   printf("err %s\n", cudaGetErrorString(cudaGetLastError()));
+  return 0;
+}
+// ---- single-warp latency of the batched log2
+__global__ void lat_log2n(const float *x, double *out, long long *cyc, int iters) {
+  unsigned amb = 0;
+  double acc = 0;
+  long long t0 = clock64();
+  for (int it = 0; it < iters; it++) {
+    double ax[8], lg[8];
+#pragma unroll
+    for (int q = 0; q < 8; q++) ax[q] = (double)x[(it * 8 + q) * 32 + threadIdx.x];
+    pmz_log2_f32_fast_n<8>(ax, lg, &amb);
+#pragma unroll
+    for (int q = 0; q < 8; q++) acc += lg[q];
+  }
+  long long t1 = clock64();
+  out[threadIdx.x] = acc;
+  if (threadIdx.x == 0) *cyc = t1 - t0;
+}
+__global__ void lat_log2_1(const float *x, double *out, long long *cyc, int iters) {
+  unsigned amb = 0;
+  double acc = 0;
+  long long t0 = clock64();
+  for (int it = 0; it < iters * 8; it++) acc += pmz_log2_f32_fast((double)x[it * 32 + threadIdx.x], &amb);
+  long long t1 = clock64();
+  out[threadIdx.x] = acc;
+  if (threadIdx.x == 0) *cyc = t1 - t0;
+}
+int main2() {
+  int iters = 64;
+  float *x; double *o; long long *c;
+  cudaMalloc(&x, 4 * 32 * 8 * iters); cudaMalloc(&o, 8 * 32); cudaMalloc(&c, 8);
+  std::vector<float> h(32 * 8 * iters);
+  for (size_t i = 0; i < h.size(); i++) h[i] = 1.0f + 0.37f * (float)i;
+  cudaMemcpy(x, h.data(), 4 * h.size(), cudaMemcpyHostToDevice);
+  long long hc;
+  for (int r = 0; r < 2; r++) { lat_log2n<<<1, 32>>>(x, o, c, iters); cudaMemcpy(&hc, c, 8, cudaMemcpyDeviceToHost); }
+  printf("log2 x8 interleaved: %.1f cycles per batch of 8 (%.1f per value)\n", (double)hc / iters, (double)hc / iters / 8);
+  for (int r = 0; r < 2; r++) { lat_log2_1<<<1, 32>>>(x, o, c, iters); cudaMemcpy(&hc, c, 8, cudaMemcpyDeviceToHost); }
+  printf("log2 scalar: %.1f cycles per value\n", (double)hc / iters / 8);
   return 0;
 }
