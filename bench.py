@@ -94,12 +94,6 @@ def c2_field(device):
     return synthetic.generate("C2", device=device)
 
 
-def shard_rows(global_rows: int, block_rows: int, world: int, rank: int):
-    nbr = (global_rows + block_rows - 1) // block_rows
-    b0, b1 = nbr * rank // world, nbr * (rank + 1) // world
-    return b0, min(b0 * block_rows, global_rows), min(b1 * block_rows, global_rows)
-
-
 def cpu_reference_time(x: np.ndarray, eps: float, repair: float, reps: int, threads: int):
     """Oracle restatement of the reference path (CPU, all host threads)."""
     from oracle import oracle as O
@@ -178,11 +172,14 @@ def main():
         if world > 1:
             dist.all_reduce(t)
 
+    from paper_2309_09778_b200.sharding import exchange_record_sizes, local_validation_blocks, plan_shard
     cfg = P.CompressConfig(rel_error=args.eps, repair_factor=args.repair)
     base = c2_field(dev)                      # 1800 x 3600, seed 1
     R0, C = base.shape
     grows = R0 * world
-    b0, r0, r1 = shard_rows(grows, cfg.block_rows, world, rank)
+    plan = plan_shard(grows, C, cfg.block_rows, cfg.block_cols, world, rank)
+    b0, r0, r1 = plan.block_row0, plan.row0, plan.row1
+    d_val = torch.as_tensor(local_validation_blocks(plan, cfg.sample_rate, cfg.seed), dtype=torch.int64, device=dev)
     idx = torch.arange(r0, r1, device=dev) % R0
     x = base[idx].contiguous()                # this rank's shard of the stacked field
     del base
@@ -191,8 +188,11 @@ def main():
     offs = torch.empty(((x.shape[0] + 255) // 256) * ((C + 255) // 256) + 1, dtype=torch.int64, device=dev)
 
     def compress_once(ev=None):
-        return codec.compress_staged(x, cfg, block_row0=b0, global_rows=grows, allreduce=allreduce,
-                                     block_offsets=offs, events=ev)
+        out = codec.compress_staged(x, cfg, block_row0=b0, global_rows=grows, allreduce=allreduce,
+                                    block_offsets=offs, events=ev, d_val=d_val)
+        if world > 1:  # the final NCCL gather of per-shard sizes -> container offsets
+            exchange_record_sizes(out[1].nbytes - out[1].header_bytes, device=dev)
+        return out
 
     # one compress to build the decompress inputs
     buf, info = compress_once()
@@ -291,7 +291,9 @@ def main():
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record()
         xd = h_in.to(dev, non_blocking=True)
-        b2, i2 = codec.compress_staged(xd, cfg, block_row0=b0, global_rows=grows, allreduce=allreduce)
+        b2, i2 = codec.compress_staged(xd, cfg, block_row0=b0, global_rows=grows, allreduce=allreduce, d_val=d_val)
+        if world > 1:
+            exchange_record_sizes(i2.nbytes - i2.header_bytes, device=dev)
         h_out[: i2.nbytes].copy_(b2, non_blocking=True)
         e.record()
         torch.cuda.synchronize()
