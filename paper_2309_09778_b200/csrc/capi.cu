@@ -129,6 +129,7 @@ WsLayout compress_layout(const Geom &g) {
   L.cub_tmp = take(L.cub_bytes);
   L.codes = take(2 * (size_t)(g.rows * g.cols));
   L.balv = take(8 * (size_t)(g.rows * g.cols));
+  L.zrow = take(2 * 32 * (size_t)(g.nparts + 1));
   L.total = o;
   return L;
 }
@@ -158,7 +159,8 @@ int launch_ws(const KParams &k, unsigned grid, cudaStream_t st, const float *x, 
   k_compress_ws<PK><<<grid, kPPC * 64, kWscSmem, st>>>(x, G, k, at<BlkP>(d_ws, L.blkp), at<WsStatus>(d_ws, L.status),
                                                        at<uint16_t>(d_ws, L.codes), at<double>(d_ws, L.balv),
                                                        at<double>(d_ws, L.anchors),
-                                                       at<unsigned long long>(d_ws, L.part_zeros));
+                                                       at<unsigned long long>(d_ws, L.part_zeros),
+                                                       at<uint16_t>(d_ws, L.zrow));
   return PMZ_OK;
 }
 
@@ -360,12 +362,15 @@ int pmz_compress_finish(const pmz_geom *g, const pmz_params *p, int write_header
   unsigned long long rec_base = hs.header_bytes;
   if (write_header)
     k_write_header<<<1, 256, 0, st>>>(d_out, G, k, g->global_rows, at<uint8_t>(d_ws, L.lens), S);
-  if (G.nblocks > 0)
-    k_write_records<8><<<(unsigned)G.nblocks, 8 * 32, 0, st>>>(
+  if (G.nparts > 0) {
+    const size_t wsm = 4ull * 2 * ((size_t)G.prow * (size_t)G.bc + 160 + 2 * kPackWords + 4);
+    CK(cudaFuncSetAttribute(k_write_records2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm));
+    k_write_records2<4><<<(unsigned)((G.nparts + 3) / 4), 128, wsm, st>>>(
         G, at<BlkP>(d_ws, L.blkp), at<uint16_t>(d_ws, L.codes), at<double>(d_ws, L.balv),
         at<double>(d_ws, L.anchors), at<unsigned long long>(d_ws, L.part_bits),
         at<unsigned long long>(d_ws, L.part_zeros), at<unsigned long long>(d_ws, L.rec_off),
-        at<uint8_t>(d_ws, L.lens), at<unsigned>(d_ws, L.cw), d_out, rec_base, S);
+        at<uint8_t>(d_ws, L.lens), at<unsigned>(d_ws, L.cw), hs.m, d_out, rec_base, at<uint16_t>(d_ws, L.zrow), S);
+  }
   if (d_block_offsets)
     k_block_offsets<<<(unsigned)((G.nblocks + 1 + 255) / 256), 256, 0, st>>>(
         G, k, write_header, at<unsigned long long>(d_ws, L.rec_off), S, (unsigned long long *)d_block_offsets);

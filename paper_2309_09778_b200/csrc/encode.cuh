@@ -438,4 +438,266 @@ __global__ void __launch_bounds__(NW * 32) k_write_records(Geom g, const BlkP *_
   }
 }
 
+// Store 8 little-endian bytes at an arbitrary byte address with at most four
+// naturally aligned stores.
+__device__ __forceinline__ void put8_unaligned(uint8_t *p, unsigned long long v) {
+  const unsigned a = (unsigned)(reinterpret_cast<uintptr_t>(p) & 7);
+  if (a == 0) { *reinterpret_cast<unsigned long long *>(p) = v; return; }
+  if ((a & 3) == 0) {
+    reinterpret_cast<unsigned *>(p)[0] = (unsigned)v;
+    reinterpret_cast<unsigned *>(p)[1] = (unsigned)(v >> 32);
+    return;
+  }
+  if ((a & 1) == 0) {  // a = 2 or 6
+    *reinterpret_cast<uint16_t *>(p) = (uint16_t)v;
+    *reinterpret_cast<unsigned *>(p + 2) = (unsigned)(v >> 16);
+    *reinterpret_cast<uint16_t *>(p + 6) = (uint16_t)(v >> 48);
+    return;
+  }
+  if ((a & 3) == 1) {  // a = 1 or 5
+    p[0] = (uint8_t)v;
+    *reinterpret_cast<uint16_t *>(p + 1) = (uint16_t)(v >> 8);
+    *reinterpret_cast<unsigned *>(p + 3) = (unsigned)(v >> 24);
+    p[7] = (uint8_t)(v >> 56);
+    return;
+  }
+  // a = 3 or 7
+  p[0] = (uint8_t)v;
+  *reinterpret_cast<unsigned *>(p + 1) = (unsigned)(v >> 8);
+  *reinterpret_cast<uint16_t *>(p + 5) = (uint16_t)(v >> 40);
+  p[7] = (uint8_t)(v >> 56);
+}
+
+// OR one byte into global memory (the containing aligned word, atomically).
+__device__ __forceinline__ void or_byte(uint8_t *p, unsigned v) {
+  if (!v) return;
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  atomicOr(reinterpret_cast<unsigned *>(a & ~(uintptr_t)3), v << (8 * (unsigned)(a & 3)));
+}
+
+// K10 (v2): one warp per partition.  The partition's codes are staged in
+// shared memory (coalesced), lane j owns a contiguous run of them in raster
+// order (the anchor excluded, D1): pass 1 sums code lengths, a warp scan gives
+// each lane its bit offset, pass 2 packs the codewords MSB-first in a 64-bit
+// register and stores whole bytes (the <= 2 bytes a lane shares with its
+// neighbours are zeroed first and OR-ed atomically).  The balance list is
+// written by a lane-parallel ballot pass.  The warp of partition 0 also writes
+// the block's record head (D9, D13, D15).
+#ifdef PMZ_CMP_PROFILE
+__device__ long long g_wr_prof[65536][6];
+#define WR_STAMP(i) if (lane == 0 && p < 65536) g_wr_prof[p][i] = clock64();
+#else
+#define WR_STAMP(i)
+#endif
+constexpr unsigned kPackWords = 2048;  // 8 KB packed payload per warp in smem (else direct global path)
+
+template <int NW>
+__global__ void __launch_bounds__(NW * 32) k_write_records2(Geom g, const BlkP *__restrict__ blkp,
+                                                            const uint16_t *__restrict__ codes,
+                                                            const double *__restrict__ balv,
+                                                            const double *__restrict__ anchors,
+                                                            const unsigned long long *__restrict__ part_bits,
+                                                            const unsigned long long *__restrict__ part_zeros,
+                                                            const unsigned long long *__restrict__ rec_off,
+                                                            const uint8_t *__restrict__ lens,
+                                                            const unsigned *__restrict__ cw, int m, uint8_t *out,
+                                                            unsigned long long rec_base,
+                                                            const uint16_t *__restrict__ zrow, WsStatus *st) {
+  __shared__ uint8_t s_len[4096];
+  __shared__ unsigned s_cw[4096];
+  extern __shared__ __align__(16) uint16_t s_codes_all[];
+  count_launch(st);
+  const bool small_tab = m <= 12;
+  if (small_tab) {
+    for (int i = threadIdx.x; i < (1 << m); i += blockDim.x) {
+      s_len[i] = lens[i];
+      s_cw[i] = cw[i];
+    }
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t p = (int64_t)blockIdx.x * NW + warp;
+  if (p >= g.nparts) return;
+  int64_t b;
+  int pi;
+  part_of(g, p, b, pi);
+  uint8_t *base = out + rec_base + rec_off[b];
+  const BlkP P = blkp[b];
+  if (P.trivial) {
+    if (pi == 0 && lane == 0) base[0] = 1;
+    return;
+  }
+  WR_STAMP(0)
+  const BlockBox bb = block_box(g, b);
+  const int64_t p0 = first_part(g, b);
+  unsigned long long zb = 0, pb = 0, nbal = 0;
+  for (int i = 0; i < bb.np; i++) {
+    const unsigned long long z = part_zeros[p0 + i], by = (part_bits[p0 + i] + 7) / 8;
+    if (i < pi) { zb += z; pb += by; }
+    nbal += z;
+  }
+  const unsigned head = 25 + 24u * bb.np;
+  if (pi == 0) {
+    // record head: trivial flag, factors, partition table, balance count
+    for (unsigned i = lane; i < head; i += 32) {
+      unsigned long long word;
+      unsigned byte;
+      if (i == 0) { base[0] = 0; continue; }
+      if (i < 17) {
+        word = __double_as_longlong(i < 9 ? P.factor_pos : P.factor_neg);
+        byte = (i - 1) & 7;
+      } else if (i < 17 + 24u * bb.np) {
+        const unsigned q = i - 17, pq = q / 24, f = (q % 24) / 8;
+        if (f == 0) {
+          unsigned long long off = 0;
+          for (unsigned t = 0; t < pq; t++) off += (part_bits[p0 + t] + 7) / 8;
+          word = off * 8;
+        } else {
+          word = f == 1 ? part_bits[p0 + pq] : __double_as_longlong(anchors[p0 + pq]);
+        }
+        byte = q & 7;
+      } else {
+        word = nbal;
+        byte = (i - 17 - 24u * bb.np) & 7;
+      }
+      base[i] = (uint8_t)(word >> (8 * byte));
+    }
+  }
+  uint8_t *bal = base + head + 8ull * zb;
+  uint8_t *pay = base + head + 8ull * nbal + pb;
+  const int pr0 = pi * g.prow, R = min(g.prow, bb.br - pr0), C = bb.bc;
+  const uint16_t *cp = codes + (bb.r0 + pr0) * g.cols + bb.c0;
+  uint16_t *sc = s_codes_all + (size_t)warp * ((size_t)g.prow * g.bc + 160 + 2 * kPackWords + 4);
+  const unsigned n = (unsigned)(R * C - 1);  // codes at raster indices 1..n
+  // lane j packs codes [1 + j RUN, 1 + (j+1) RUN); they are staged at
+  // sc[j STRIDE + i] with STRIDE/2 odd so the 32 lanes hit 32 different banks
+  const unsigned RUN = (n + 31) / 32;
+  unsigned STRIDE = RUN + 1;
+  while ((STRIDE & 1) || !((STRIDE >> 1) & 1)) STRIDE++;
+  const unsigned rrun = RUN > 1 ? (unsigned)(0x100000000ull / RUN) + 1u : 0u;  // floor(x/RUN) = umulhi(x, rrun)
+  auto spos = [&](unsigned e) -> unsigned {  // e >= 1
+    const unsigned x = e - 1, j = RUN > 1 ? __umulhi(x, rrun) : x;
+    return j * STRIDE + (x - j * RUN);
+  };
+  // stage the partition's codes (coalesced global reads)
+  for (int r = 0; r < R; r++)
+    for (int c = lane; c < C; c += 32) {
+      const unsigned e = (unsigned)(r * C + c);
+      if (e) sc[spos(e)] = __ldg(&cp[(int64_t)r * g.cols + c]);
+    }
+  __syncwarp();
+  WR_STAMP(1)
+  // balance list: the compress kernel left each row's balance values
+  // compacted at the start of the row segment (zrow = counts): contiguous,
+  // coalesced copies at row offsets from a warp scan of the counts
+  {
+    const double *bp = balv + (bb.r0 + pr0) * g.cols + bb.c0;
+    const unsigned zc = lane < R ? zrow[p * 32 + lane] : 0u;
+    unsigned zi = zc;
+    for (int d = 1; d < 32; d <<= 1) {
+      const unsigned t = __shfl_up_sync(0xffffffffu, zi, d);
+      if (lane >= d) zi += t;
+    }
+    zi -= zc;  // exclusive
+    // flattened over the partition's whole list: element i belongs to the
+    // last row whose exclusive prefix is <= i (5-step search over the lanes'
+    // prefixes); 4 independent loads in flight per lane
+    const unsigned T = __shfl_sync(0xffffffffu, zi + zc, 31);
+    for (unsigned i0 = 0; i0 < T; i0 += 128) {
+      unsigned long long v[4];
+      unsigned ii[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const unsigned i = i0 + u * 32 + lane;
+        int r = 0;
+#pragma unroll
+        for (int d = 16; d >= 1; d >>= 1) {
+          const unsigned zr = __shfl_sync(0xffffffffu, zi, r + d);
+          if (r + d < R && zr <= i) r += d;
+        }
+        const unsigned rb = __shfl_sync(0xffffffffu, zi, r);
+        ii[u] = i;
+        v[u] = i < T ? __double_as_longlong(__ldg(&bp[(int64_t)r * g.cols + (i - rb)])) : 0ull;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; u++)
+        if (ii[u] < T) put8_unaligned(bal + 8ull * ii[u], v[u]);
+    }
+  }
+  WR_STAMP(2)
+  auto len_of = [&](unsigned c) -> unsigned { return small_tab ? s_len[c] : __ldg(&lens[c]); };
+  auto cw_of = [&](unsigned c) -> unsigned { return small_tab ? s_cw[c] : __ldg(&cw[c]); };
+  const unsigned e0 = min(n + 1, 1 + lane * RUN), e1 = min(n + 1, 1 + (lane + 1) * RUN);
+  const uint16_t *myc = sc + lane * STRIDE;
+  unsigned bits = 0;
+#pragma unroll 8
+  for (unsigned e = e0; e < e1; e++) bits += len_of(myc[e - e0]);
+  unsigned ib = bits;
+  for (int d = 1; d < 32; d <<= 1) {
+    const unsigned t = __shfl_up_sync(0xffffffffu, ib, d);
+    if (lane >= d) ib += t;
+  }
+  const unsigned B = ib - bits;
+  const unsigned total_bits = __shfl_sync(0xffffffffu, ib, 31);
+  const unsigned nwords = (total_bits + 31) >> 5;
+  unsigned *sw = reinterpret_cast<unsigned *>(sc + 32 * STRIDE + 2);  // payload words after the codes
+  if (nwords <= kPackWords) {
+    // MSB-first words in shared memory: interior words stored, the two words a
+    // lane may share with its neighbours OR-ed (zeroed first)
+    sw = reinterpret_cast<unsigned *>((reinterpret_cast<uintptr_t>(sw) + 3) & ~(uintptr_t)3);
+    const unsigned fw = B >> 5, lw = bits ? (B + bits - 1) >> 5 : fw;
+    if (bits) { sw[fw] = 0; sw[lw] = 0; }
+    __syncwarp();
+    WR_STAMP(3)
+    unsigned long long acc = 0;
+    int nacc = (int)(B & 31);
+    unsigned ow = fw;
+#pragma unroll 4
+    for (unsigned e = e0; e < e1; e++) {
+      const unsigned cd = myc[e - e0];
+      const int l = (int)len_of(cd);
+      acc = (acc << l) | cw_of(cd);
+      nacc += l;
+      if (nacc >= 32) {
+        const unsigned w = (unsigned)(acc >> (nacc - 32));
+        if (ow == fw || ow == lw) atomicOr(&sw[ow], w);
+        else sw[ow] = w;
+        ow++;
+        nacc -= 32;
+      }
+    }
+    if (nacc > 0) atomicOr(&sw[ow], (unsigned)(acc << (32 - nacc)));
+    __syncwarp();
+    // coalesced byte copy to the (byte-aligned) payload
+    const unsigned nbytes = (total_bits + 7) >> 3;
+    for (unsigned i = lane; i < nbytes; i += 32) pay[i] = (uint8_t)(sw[i >> 2] >> (24 - 8 * (i & 3)));
+  } else {
+    const unsigned fbyte = B >> 3, lbyte = bits ? (B + bits - 1) >> 3 : fbyte;
+    if (bits) {
+      pay[fbyte] = 0;
+      pay[lbyte] = 0;
+    }
+    __syncwarp();
+    unsigned long long acc = 0;
+    int nacc = (int)(B & 7);  // leading bits owned by the previous lane
+    unsigned outb = fbyte;
+    for (unsigned e = e0; e < e1; e++) {
+      const unsigned cd = myc[e - e0];
+      const int l = (int)len_of(cd);
+      acc = (acc << l) | cw_of(cd);
+      nacc += l;
+      while (nacc >= 8) {
+        const unsigned byte = (unsigned)(acc >> (nacc - 8)) & 0xffu;
+        if (outb == fbyte || outb == lbyte) or_byte(pay + outb, byte);
+        else pay[outb] = (uint8_t)byte;
+        outb++;
+        nacc -= 8;
+      }
+    }
+    if (nacc > 0) or_byte(pay + outb, (unsigned)(acc << (8 - nacc)) & 0xffu);
+  }
+  __syncwarp();
+  WR_STAMP(4)
+}
+
 }  // namespace pmz

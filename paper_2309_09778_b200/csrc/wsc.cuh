@@ -72,7 +72,8 @@ __global__ void __launch_bounds__(kPPC * 64) k_compress_ws(const float *__restri
                                                            const BlkP *__restrict__ blkp, WsStatus *st,
                                                            uint16_t *__restrict__ codes, double *__restrict__ balv,
                                                            double *__restrict__ anchors,
-                                                           unsigned long long *__restrict__ part_zeros) {
+                                                           unsigned long long *__restrict__ part_zeros,
+                                                           uint16_t *__restrict__ zrow) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   count_launch(st);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -109,14 +110,18 @@ __global__ void __launch_bounds__(kPPC * 64) k_compress_ws(const float *__restri
     // ------------------------------ producer ------------------------------
     uint16_t *cpart = codes + (bb.r0 + pr0) * g.cols + bb.c0;
     double *bpart = balv + (bb.r0 + pr0) * g.cols + bb.c0;
+    // balance values are appended per row (row-compacted: row r's list starts
+    // at column 0 of its block-row segment), counts per row in zrow
+    unsigned rowcnt = 0;  // lane r's count for row r (lane = row here)
     auto flush = [&](int chunk) {
       const int s = chunk % kSlots, col = chunk * 32 + lane;
-      if (col < C) {
-        for (int r = 0; r < R; r++) {
-          const uint16_t cd = W.code[s][r][lane];
-          cpart[r * g.cols + col] = cd;
-          if (cd == 0) bpart[r * g.cols + col] = W.v[s][r][lane];
-        }
+      for (int r = 0; r < R; r++) {
+        const uint16_t cd = col < C ? W.code[s][r][lane] : (uint16_t)1;
+        if (col < C) cpart[r * g.cols + col] = cd;
+        const unsigned zm = __ballot_sync(0xffffffffu, cd == 0);
+        const unsigned base = __shfl_sync(0xffffffffu, rowcnt, r);
+        if (cd == 0) bpart[r * g.cols + base + __popc(zm & ((1u << lane) - 1))] = W.v[s][r][lane];
+        if (lane == r) rowcnt += __popc(zm);
       }
     };
     for (int kc = 0; kc < nch; kc++) {
@@ -212,6 +217,7 @@ __global__ void __launch_bounds__(kPPC * 64) k_compress_ws(const float *__restri
       TIMED_SYNC(bar0 + kSlots + kc % kSlots)
       flush(kc);
     }
+    if (lane < R) zrow[p * 32 + lane] = (uint16_t)rowcnt;
 #ifdef PMZ_CMP_PROFILE
     if (lane == 0 && p < 65536) { g_cmp_prof[p][0][0] = t_start; g_cmp_prof[p][0][1] = clock64(); g_cmp_prof[p][0][2] = t_wait;
       g_cmp_ph[p][0] = t_fwd; g_cmp_ph[p][1] = t_code; g_cmp_ph[p][2] = t_flush; }

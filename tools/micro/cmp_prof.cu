@@ -34,6 +34,13 @@ int main(int argc, char **argv) {
   double a = 0, b2 = 0, c2 = 0;
   for (int i = 0; i < G.nparts; i++) { a += ph[i * 4]; b2 += ph[i * 4 + 1]; c2 += ph[i * 4 + 2]; }
   printf("producer phases: loads+fwd %.0f  codes %.0f  flush %.0f\n", a / G.nparts, b2 / G.nparts, c2 / G.nparts);
+  {
+    std::vector<long long> w(65536 * 6);
+    cudaMemcpyFromSymbol(w.data(), g_wr_prof, 8 * 65536 * 6);
+    double ph[4] = {0};
+    for (int i = 0; i < G.nparts; i++) for (int j = 0; j < 4; j++) ph[j] += (double)(w[i * 6 + j + 1] - w[i * 6 + j]);
+    printf("write_records: stage %.0f  balance %.0f  pass1 %.0f  pack %.0f\n", ph[0] / G.nparts, ph[1] / G.nparts, ph[2] / G.nparts, ph[3] / G.nparts);
+  }
   printf("producer: avg %.0f cycles, waiting %.0f\nconsumer: avg %.0f cycles, waiting %.0f\n", pd / n, pw / n, cd / n, cw / n);
   return 0;
 }
