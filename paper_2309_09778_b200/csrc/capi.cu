@@ -13,6 +13,7 @@
 #include "dsc.cuh"
 #include "decompress.cuh"
 #include "encode.cuh"
+#include "fwdq.cuh"
 
 using namespace pmz;
 
@@ -114,6 +115,7 @@ WsLayout compress_layout(const Geom &g) {
   L.status = take(sizeof(WsStatus));
   L.cov = take(18 * 8);
   L.hist = take((kMaxAlpha + 1) * 8);
+  L.vflag = take((size_t)g.nblocks + 1);  // zeroed with status / cov / hist
   L.lens = take(kMaxAlpha);
   L.cw = take(kMaxAlpha * 4);
   L.cb_keys = take(kMaxAlpha * 8);
@@ -130,6 +132,9 @@ WsLayout compress_layout(const Geom &g) {
   L.codes = take(2 * (size_t)(g.rows * g.cols));
   L.balv = take(8 * (size_t)(g.rows * g.cols));
   L.zrow = take(2 * 32 * (size_t)(g.nparts + 1));
+  L.vbuf = take(8 * (size_t)(g.rows * g.cols));
+  L.rqbuf = take(2 * (size_t)(g.rows * g.cols));
+  L.clsbuf = take((size_t)(g.rows * g.cols));
   L.total = o;
   return L;
 }
@@ -160,8 +165,18 @@ int launch_ws(const KParams &k, unsigned grid, cudaStream_t st, const float *x, 
                                                        at<uint16_t>(d_ws, L.codes), at<double>(d_ws, L.balv),
                                                        at<double>(d_ws, L.anchors),
                                                        at<unsigned long long>(d_ws, L.part_zeros),
-                                                       at<uint16_t>(d_ws, L.zrow));
+                                                       at<uint16_t>(d_ws, L.zrow), at<double>(d_ws, L.vbuf),
+                                                       at<int16_t>(d_ws, L.rqbuf), at<uint8_t>(d_ws, L.clsbuf));
   return PMZ_OK;
+}
+
+template <int PK>
+void launch_fwdq(const KParams &k, cudaStream_t st, const float *x, const Geom &G, void *d_ws, const WsLayout &L) {
+  cudaFuncSetAttribute(k_fwdq<PK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFqSmem);
+  k_fwdq<PK><<<(unsigned)G.nparts, kFqW * 32, kFqSmem, st>>>(
+      x, G, k, at<BlkP>(d_ws, L.blkp), at<uint8_t>(d_ws, L.vflag), at<WsStatus>(d_ws, L.status),
+      at<double>(d_ws, L.vbuf), at<int16_t>(d_ws, L.rqbuf), at<uint8_t>(d_ws, L.clsbuf),
+      at<unsigned long long>(d_ws, L.cov));
 }
 
 template <int MODE, int PK>
@@ -257,10 +272,15 @@ int pmz_compress_analyze(const float *d_in, const pmz_geom *g, const pmz_params 
   CK(cudaMemsetAsync(d_ws, 0, L.lens, st));
   if (G.nblocks == 0) return PMZ_OK;
   k_stats<<<(unsigned)G.nblocks, kBW * 32, 0, st>>>(d_in, G, k, at<BlkP>(d_ws, L.blkp), at<WsStatus>(d_ws, L.status));
-  if (p->m == 0 && n_val > 0) {
-    dim3 grid(128, (unsigned)n_val);
-    k_coverage<kNT><<<grid, kNT, 0, st>>>(d_in, G, k, at<BlkP>(d_ws, L.blkp), d_val,
-                                          at<unsigned long long>(d_ws, L.cov), at<WsStatus>(d_ws, L.status));
+  if (p->m == 0 && n_val > 0)
+    k_mark_val<<<(unsigned)((n_val + 255) / 256), 256, 0, st>>>(d_val, n_val, at<uint8_t>(d_ws, L.vflag),
+                                                               at<WsStatus>(d_ws, L.status));
+  // forward map + m-independent TRUE-surface quantization of every element,
+  // coverage of the validation blocks in the same pass
+  if (G.nparts > 0) {
+    if (k.init_model == 3) launch_fwdq<3>(k, st, d_in, G, d_ws, L);
+    else if (k.init_model == 1) launch_fwdq<1>(k, st, d_in, G, d_ws, L);
+    else launch_fwdq<0>(k, st, d_in, G, d_ws, L);
   }
   return launch_check();
 }
@@ -363,9 +383,7 @@ int pmz_compress_finish(const pmz_geom *g, const pmz_params *p, int write_header
   if (write_header)
     k_write_header<<<1, 256, 0, st>>>(d_out, G, k, g->global_rows, at<uint8_t>(d_ws, L.lens), S);
   if (G.nparts > 0) {
-    const size_t wsm = 4ull * 2 * ((size_t)G.prow * (size_t)G.bc + 160 + 2 * kPackWords + 4);
-    CK(cudaFuncSetAttribute(k_write_records2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm));
-    k_write_records2<4><<<(unsigned)((G.nparts + 3) / 4), 128, wsm, st>>>(
+    k_write_part<<<(unsigned)G.nparts, kWT, 0, st>>>(
         G, at<BlkP>(d_ws, L.blkp), at<uint16_t>(d_ws, L.codes), at<double>(d_ws, L.balv),
         at<double>(d_ws, L.anchors), at<unsigned long long>(d_ws, L.part_bits),
         at<unsigned long long>(d_ws, L.part_zeros), at<unsigned long long>(d_ws, L.rec_off),

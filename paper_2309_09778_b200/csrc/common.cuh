@@ -126,6 +126,30 @@ __device__ __forceinline__ int quantize_fast(double err, const KParams &k, int m
   return 0;
 }
 
+constexpr int16_t kRqOut = (int16_t)-32768;  // |round(q)| > 32767: code 0 for every m
+// round_half_away(err / (2 b_a)) with the same exactness argument as
+// quantize_fast (reciprocal multiply, IEEE division only near a tie).
+__device__ __forceinline__ int quantize_rq(double err, const KParams &k) {
+  const double q = __dmul_rn(err, k.inv_two_ba);
+  const double aq = fabs(q);
+  if (!(aq < 32768.0)) return kRqOut;
+  const double f = __dsub_rn(aq, trunc(aq));
+  double r;
+  if (__builtin_expect(fabs(__dsub_rn(f, 0.5)) <= aq * 0x1p-48, 0)) r = round(__ddiv_rn(err, k.two_ba));
+  else r = round(q);
+  return fabs(r) <= 32767.0 ? (int)r : (int)kRqOut;
+}
+
+__device__ __forceinline__ int code_of_rq(int rq, int center) {
+  return (rq != kRqOut && abs(rq) < center) ? center + rq : 0;
+}
+
+__device__ __forceinline__ int m_of_rq(int rq) {
+  if (rq == kRqOut) return 17;
+  const int bl = 32 - __clz(abs(rq));
+  return max(4, bl + 1);
+}
+
 // smallest m in [4,16] covering round(q); 17 = none (select_m)
 __device__ __forceinline__ int m_required(double err, double two_ba) {
   double a = fabs(round(__ddiv_rn(err, two_ba)));
@@ -208,7 +232,7 @@ struct WsStatus {
 
 struct WsLayout {
   size_t status, cov, hist, lens, cw, cb_keys, cb_w, cb_parent, blkp, part_bits, part_zeros, anchors, rec_size,
-      rec_off, cub_tmp, codes, balv, zrow, total;
+      rec_off, cub_tmp, codes, balv, zrow, vflag, vbuf, rqbuf, clsbuf, total;
   size_t cub_bytes;
 };
 

@@ -700,4 +700,207 @@ __global__ void __launch_bounds__(NW * 32) k_write_records2(Geom g, const BlkP *
   WR_STAMP(4)
 }
 
+// One block record's share written by ONE CTA per partition (kWT threads):
+// the record head (partition 0 only), the partition's slice of the block
+// balance list, and its Huffman substream.  Thread t
+// encodes the raster run [t RUN, (t+1) RUN) of the partition (raster index 0
+// = the anchor, not coded, D1); bit offsets come from a CTA-wide scan of the
+// runs' bit counts; words are assembled MSB-first in shared memory and copied
+// out coalesced.
+constexpr int kWT = 256;
+constexpr unsigned kPartWords = 4096;  // 16 KB payload staging (else direct byte writes)
+
+__global__ void __launch_bounds__(kWT) k_write_part(Geom g, const BlkP *__restrict__ blkp,
+                                                    const uint16_t *__restrict__ codes,
+                                                    const double *__restrict__ balv,
+                                                    const double *__restrict__ anchors,
+                                                    const unsigned long long *__restrict__ part_bits,
+                                                    const unsigned long long *__restrict__ part_zeros,
+                                                    const unsigned long long *__restrict__ rec_off,
+                                                    const uint8_t *__restrict__ lens,
+                                                    const unsigned *__restrict__ cw, int m, uint8_t *out,
+                                                    unsigned long long rec_base,
+                                                    const uint16_t *__restrict__ zrow, WsStatus *st) {
+  __shared__ uint8_t s_len[4096];
+  __shared__ unsigned s_cw[4096];
+  __shared__ unsigned sw[kPartWords];
+  __shared__ unsigned s_wsum[kWT / 32], s_zi[33];
+  count_launch(st);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t p = blockIdx.x;
+  int64_t b;
+  int pi;
+  part_of(g, p, b, pi);
+  uint8_t *base = out + rec_base + rec_off[b];
+  const BlkP P = blkp[b];
+  if (P.trivial) {
+    if (pi == 0 && tid == 0) base[0] = 1;
+    return;
+  }
+  const bool small_tab = m <= 12;
+  if (small_tab) {
+    for (int i = tid; i < (1 << m); i += kWT) {
+      s_len[i] = lens[i];
+      s_cw[i] = cw[i];
+    }
+  }
+  const BlockBox bb = block_box(g, b);
+  const int64_t p0 = first_part(g, b);
+  unsigned long long zb = 0, pb = 0, nbal = 0;
+  for (int i = 0; i < bb.np; i++) {
+    const unsigned long long z = part_zeros[p0 + i], by = (part_bits[p0 + i] + 7) / 8;
+    if (i < pi) { zb += z; pb += by; }
+    nbal += z;
+  }
+  const unsigned head = 25 + 24u * bb.np;
+  if (pi == 0) {
+    // record head: trivial flag, factors, partition table, balance count
+    for (unsigned i = tid; i < head; i += kWT) {
+      unsigned long long word;
+      unsigned byte;
+      if (i == 0) { base[0] = 0; continue; }
+      if (i < 17) {
+        word = __double_as_longlong(i < 9 ? P.factor_pos : P.factor_neg);
+        byte = (i - 1) & 7;
+      } else if (i < 17 + 24u * bb.np) {
+        const unsigned q = i - 17, pq = q / 24, f = (q % 24) / 8;
+        if (f == 0) {
+          unsigned long long off = 0;
+          for (unsigned t = 0; t < pq; t++) off += (part_bits[p0 + t] + 7) / 8;
+          word = off * 8;
+        } else {
+          word = f == 1 ? part_bits[p0 + pq] : __double_as_longlong(anchors[p0 + pq]);
+        }
+        byte = q & 7;
+      } else {
+        word = nbal;
+        byte = (i - 17 - 24u * bb.np) & 7;
+      }
+      base[i] = (uint8_t)(word >> (8 * byte));
+    }
+  }
+  uint8_t *bal = base + head + 8ull * zb;
+  uint8_t *pay = base + head + 8ull * nbal + pb;
+  const int pr0 = pi * g.prow, R = min(g.prow, bb.br - pr0), C = bb.bc;
+  const uint16_t *cp = codes + (bb.r0 + pr0) * g.cols + bb.c0;
+
+  // ---- balance list: row-compacted by the compress kernel (zrow = counts) ----
+  if (warp == 0) {
+    const unsigned zc = lane < R ? zrow[p * 32 + lane] : 0u;
+    unsigned zi = zc;
+    for (int d = 1; d < 32; d <<= 1) {
+      const unsigned t = __shfl_up_sync(0xffffffffu, zi, d);
+      if (lane >= d) zi += t;
+    }
+    s_zi[lane] = zi - zc;
+    if (lane == 31) s_zi[32] = zi;
+  }
+  __syncthreads();  // also publishes s_len / s_cw
+  {
+    const double *bp = balv + (bb.r0 + pr0) * g.cols + bb.c0;
+    const unsigned T = s_zi[32];
+    for (unsigned i = tid; i < T; i += kWT) {
+      int r = 0;
+#pragma unroll
+      for (int d = 16; d >= 1; d >>= 1)
+        if (r + d < R && s_zi[r + d] <= i) r += d;
+      put8_unaligned(bal + 8ull * i, __double_as_longlong(__ldg(&bp[(int64_t)r * g.cols + (i - s_zi[r])])));
+    }
+  }
+
+  // ---- Huffman substream ----
+  auto len_of = [&](unsigned c) -> unsigned { return small_tab ? s_len[c] : __ldg(&lens[c]); };
+  auto cw_of = [&](unsigned c) -> unsigned { return small_tab ? s_cw[c] : __ldg(&cw[c]); };
+  const unsigned ne = (unsigned)(R * C);
+  const unsigned RUN = (ne + kWT - 1) / kWT;
+  const unsigned e0 = min(ne, tid * RUN), e1 = min(ne, e0 + RUN);
+  // element e -> (e / C, e % C): walk the run with a (row, col) cursor
+  const int r0 = (int)(e0 / (unsigned)C), c0 = (int)(e0 - (unsigned)r0 * C);
+  unsigned bits = 0;
+  {
+    int r = r0, c = c0;
+#pragma unroll 8
+    for (unsigned e = e0; e < e1; e++) {
+      if (e) bits += len_of(__ldg(&cp[(int64_t)r * g.cols + c]));
+      if (++c == C) { c = 0; r++; }
+    }
+  }
+  // CTA exclusive scan of the runs' bit counts
+  unsigned ib = bits;
+  for (int d = 1; d < 32; d <<= 1) {
+    const unsigned t = __shfl_up_sync(0xffffffffu, ib, d);
+    if (lane >= d) ib += t;
+  }
+  if (lane == 31) s_wsum[warp] = ib;
+  __syncthreads();
+  unsigned wofs = 0, total_bits = 0;
+#pragma unroll
+  for (int w = 0; w < kWT / 32; w++) {
+    const unsigned v = s_wsum[w];
+    if (w < warp) wofs += v;
+    total_bits += v;
+  }
+  const unsigned B = wofs + ib - bits;
+  const unsigned nwords = (total_bits + 31) >> 5;
+  if (nwords <= kPartWords) {
+    for (unsigned i = tid; i < nwords; i += kWT) sw[i] = 0;
+    __syncthreads();
+    const unsigned fw = B >> 5, lw = bits ? (B + bits - 1) >> 5 : fw;
+    unsigned long long acc = 0;
+    int nacc = (int)(B & 31);
+    unsigned ow = fw;
+    int r = r0, c = c0;
+#pragma unroll 4
+    for (unsigned e = e0; e < e1; e++) {
+      if (e) {
+        const unsigned cd = __ldg(&cp[(int64_t)r * g.cols + c]);
+        const int l = (int)len_of(cd);
+        acc = (acc << l) | cw_of(cd);
+        nacc += l;
+        if (nacc >= 32) {
+          const unsigned w = (unsigned)(acc >> (nacc - 32));
+          if (ow == fw || ow == lw) atomicOr(&sw[ow], w);
+          else sw[ow] = w;
+          ow++;
+          nacc -= 32;
+        }
+      }
+      if (++c == C) { c = 0; r++; }
+    }
+    if (nacc > 0) atomicOr(&sw[ow], (unsigned)(acc << (32 - nacc)));
+    __syncthreads();
+    const unsigned nbytes = (total_bits + 7) >> 3;
+    for (unsigned i = tid; i < nbytes; i += kWT) pay[i] = (uint8_t)(sw[i >> 2] >> (24 - 8 * (i & 3)));
+  } else {
+    // oversized substream: bytes straight to global, boundary bytes OR-ed
+    const unsigned fbyte = B >> 3, lbyte = bits ? (B + bits - 1) >> 3 : fbyte;
+    if (bits) {
+      pay[fbyte] = 0;
+      pay[lbyte] = 0;
+    }
+    __syncthreads();
+    unsigned long long acc = 0;
+    int nacc = (int)(B & 7);
+    unsigned outb = fbyte;
+    int r = r0, c = c0;
+    for (unsigned e = e0; e < e1; e++) {
+      if (e) {
+        const unsigned cd = __ldg(&cp[(int64_t)r * g.cols + c]);
+        const int l = (int)len_of(cd);
+        acc = (acc << l) | cw_of(cd);
+        nacc += l;
+        while (nacc >= 8) {
+          const unsigned byte = (unsigned)(acc >> (nacc - 8)) & 0xffu;
+          if (outb == fbyte || outb == lbyte) or_byte(pay + outb, byte);
+          else pay[outb] = (uint8_t)byte;
+          outb++;
+          nacc -= 8;
+        }
+      }
+      if (++c == C) { c = 0; r++; }
+    }
+    if (nacc > 0) or_byte(pay + outb, (unsigned)(acc << (8 - nacc)) & 0xffu);
+  }
+}
+
 }  // namespace pmz

@@ -73,7 +73,10 @@ __global__ void __launch_bounds__(kPPC * 64) k_compress_ws(const float *__restri
                                                            uint16_t *__restrict__ codes, double *__restrict__ balv,
                                                            double *__restrict__ anchors,
                                                            unsigned long long *__restrict__ part_zeros,
-                                                           uint16_t *__restrict__ zrow) {
+                                                           uint16_t *__restrict__ zrow,
+                                                           const double *__restrict__ vbuf,
+                                                           const int16_t *__restrict__ rqbuf,
+                                                           const uint8_t *__restrict__ clsbuf) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   count_launch(st);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -98,6 +101,9 @@ __global__ void __launch_bounds__(kPPC * 64) k_compress_ws(const float *__restri
   const int center = 1 << (m - 1);
   const int bar0 = 1 + pair * 2 * kSlots;  // full[s] = bar0 + s, empty[s] = bar0 + kSlots + s
   const float *xp = x + (bb.r0 + pr0) * g.cols + bb.c0;
+  const double *vp = vbuf + (bb.r0 + pr0) * g.cols + bb.c0;
+  const int16_t *rqp = rqbuf + (bb.r0 + pr0) * g.cols + bb.c0;
+  const uint8_t *clp = clsbuf + (bb.r0 + pr0) * g.cols + bb.c0;
   unsigned *amb = &st->unresolved;
 
 #ifdef PMZ_CMP_PROFILE
@@ -145,67 +151,32 @@ __global__ void __launch_bounds__(kPPC * 64) k_compress_ws(const float *__restri
 #if defined(PMZ_CMP_ISOLATE) && PMZ_CMP_ISOLATE == 2
       if (kc >= 0) { __syncwarp(); bar_arrive_n(bar0 + s, 64); continue; }
 #endif
+      // ring fill from the k_fwdq results (L2-resident): TRUE value, class,
+      // and the code for this m
       for (int rb = 0; rb < R; rb += 8) {
-        float xr[8];
-#pragma unroll
-        for (int q = 0; q < 8; q++) xr[q] = (inb && rb + q < R) ? __ldg(xp + (rb + q) * g.cols + col) : 0.0f;
-        // forward_map of 8 rows with interleaved log2 chains (transform.py:170-185)
-        double ax[8], lg[8];
+        double vv[8];
+        int rq[8];
+        uint8_t cl[8];
 #pragma unroll
         for (int q = 0; q < 8; q++) {
-          const float xz = zfloor(xr[q]);
-          ax[q] = xz != 0.0f ? (double)fabsf(xz) : 1.0;
+          const bool ok = inb && rb + q < R;
+          const int64_t e = (int64_t)(rb + q) * g.cols + col;
+          vv[q] = ok ? __ldg(vp + e) : 0.0;
+          rq[q] = ok ? __ldg(rqp + e) : 0;
+          cl[q] = ok ? __ldg(clp + e) : (uint8_t)0;
         }
-        pmz_log2_f32_fast_n<8>(ax, lg, amb);
 #pragma unroll
         for (int q = 0; q < 8; q++) {
           if (rb + q < R) {
-            const float xz = zfloor(xr[q]);
-            double v = P.zero_code;
-            if (xz > 0.0f) v = __dadd_rn(lg[q], P.lg_pos);
-            else if (xz < 0.0f) v = __dadd_rn(lg[q], P.lg_neg);
-            W.v[s][rb + q][lane] = inb ? v : 0.0;
-            W.cls[s][rb + q][lane] = xclass(xz);
+            W.v[s][rb + q][lane] = vv[q];
+            W.cls[s][rb + q][lane] = cl[q];
+            W.code[s][rb + q][lane] = (uint16_t)code_of_rq(rq[q], center);
           }
         }
       }
-      __syncwarp();
-#ifdef PMZ_CMP_PROFILE
-      t_fwd += clock64() - t_mark;
-      t_mark = clock64();
-#endif
-      if (inb) {
-        const int ps = (kc + kSlots - 1) % kSlots;
-        // TRUE-surface residuals and codes, 4 rows per batch (independent chains)
-        for (int rb = 0; rb < R; rb += 4) {
-          double err[4];
-#pragma unroll
-          for (int q = 0; q < 4; q++) {
-            const int r = min(rb + q, R - 1);
-            const double v = W.v[s][r][lane];
-            double w = 0.0, n = 0.0, nw = 0.0;
-            if (col > 0) w = lane > 0 ? W.v[s][r][lane - 1] : W.v[ps][r][31];
-            if (r > 0) {
-              n = W.v[s][r - 1][lane];
-              if (col > 0) nw = lane > 0 ? W.v[s][r - 1][lane - 1] : W.v[ps][r - 1][31];
-            }
-            err[q] = __dsub_rn(v, predict_k<PK>(k, w, n, nw));
-          }
-#pragma unroll
-          for (int q = 0; q < 4; q++) {
-            const int r = rb + q;
-            if (r < R) {
-              uint16_t cd;
-              if (r == 0 && col == 0) {
-                cd = kAnc;
-                anchors[p] = W.v[s][0][0];  // forced anchor, D1
-              } else {
-                cd = (uint16_t)quantize_fast(err[q], k, m);
-              }
-              W.code[s][r][lane] = cd;
-            }
-          }
-        }
+      if (kc == 0 && lane == 0) {
+        W.code[s][0][0] = kAnc;
+        anchors[p] = W.v[s][0][0];  // forced anchor, D1
       }
       __syncwarp();
 #ifdef PMZ_CMP_PROFILE
