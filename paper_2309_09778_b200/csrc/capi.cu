@@ -119,8 +119,8 @@ WsLayout compress_layout(const Geom &g) {
   L.lens = take(kMaxAlpha);
   L.cw = take(kMaxAlpha * 4);
   L.cb_keys = take(kMaxAlpha * 8);
-  L.cb_w = take(kMaxAlpha * 4);
-  L.cb_parent = 0;
+  L.cb_w = take(kMaxAlpha * 8);       // internal weights (u64), reused as depth / jump arrays
+  L.cb_parent = take(kMaxAlpha * 4);  // parent of every internal node
   L.blkp = take(sizeof(BlkP) * (size_t)(g.nblocks + 1));
   L.part_bits = take(8 * (size_t)(g.nparts + 1));
   L.part_zeros = take(8 * (size_t)(g.nparts + 1));
@@ -179,25 +179,6 @@ void launch_fwdq(const KParams &k, cudaStream_t st, const float *x, const Geom &
       at<unsigned long long>(d_ws, L.cov));
 }
 
-template <int MODE, int PK>
-int launch_blocks_pk(const KParams &k, unsigned grid, cudaStream_t st, const float *x, const Geom &G,
-                     const int64_t *ids, BlkP *blkp, WsStatus *S, uint16_t *codes, double *balv, double *anchors,
-                     unsigned long long *pz, unsigned long long *cov) {
-  CK(cudaFuncSetAttribute(k_compress_blocks<MODE, PK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)kBlockSmem));
-  k_compress_blocks<MODE, PK><<<grid, kBW * 32, kBlockSmem, st>>>(x, G, k, ids, blkp, S, codes, balv, anchors, pz,
-                                                                   cov);
-  return PMZ_OK;
-}
-
-template <int MODE>
-int launch_blocks(const KParams &k, unsigned grid, cudaStream_t st, const float *x, const Geom &G,
-                  const int64_t *ids, BlkP *blkp, WsStatus *S, uint16_t *codes, double *balv, double *anchors,
-                  unsigned long long *pz, unsigned long long *cov) {
-  if (k.init_model == 3) return launch_blocks_pk<MODE, 3>(k, grid, st, x, G, ids, blkp, S, codes, balv, anchors, pz, cov);
-  if (k.init_model == 1) return launch_blocks_pk<MODE, 1>(k, grid, st, x, G, ids, blkp, S, codes, balv, anchors, pz, cov);
-  return launch_blocks_pk<MODE, 0>(k, grid, st, x, G, ids, blkp, S, codes, balv, anchors, pz, cov);
-}
 
 }  // namespace
 
@@ -339,10 +320,11 @@ int pmz_compress_finish(const pmz_geom *g, const pmz_params *p, int write_header
   cudaStream_t st = (cudaStream_t)stream;
   KParams k = kparams(p);
   WsStatus *S = at<WsStatus>(d_ws, L.status);
-  CK(cudaFuncSetAttribute(k_codebook, cudaFuncAttributeMaxDynamicSharedMemorySize, 8192 * 12));
-  k_codebook<<<1, 1024, 8192 * 12, st>>>(at<unsigned long long>(d_ws, L.hist), S,
-                                         at<unsigned long long>(d_ws, L.cb_keys), at<unsigned>(d_ws, L.cb_w),
-                                         at<uint8_t>(d_ws, L.lens), at<unsigned>(d_ws, L.cw));
+  CK(cudaFuncSetAttribute(k_codebook, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCbSmem));
+  k_codebook<<<1, 1024, kCbSmem, st>>>(at<unsigned long long>(d_ws, L.hist), S,
+                                       at<unsigned long long>(d_ws, L.cb_keys), at<unsigned long long>(d_ws, L.cb_w),
+                                       at<unsigned>(d_ws, L.cb_parent), at<uint8_t>(d_ws, L.lens),
+                                       at<unsigned>(d_ws, L.cw));
   if (G.nparts > 0) {
     unsigned grid = (unsigned)((G.nparts + kWarps - 1) / kWarps);
     k_part_bits<kWarps><<<grid, kWarps * 32, 0, st>>>(G, at<BlkP>(d_ws, L.blkp), at<uint16_t>(d_ws, L.codes),

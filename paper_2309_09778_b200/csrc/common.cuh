@@ -105,6 +105,27 @@ __device__ __forceinline__ double predict_k(const KParams &k, double s0, double 
   return predict(k, s0, s1, s2);
 }
 
+// predict_k with a shorter dependency chain, same value as far as any
+// consumer can tell (used by the verify/reconstruct recurrences, whose only
+// use of the prediction is vhat = pred + dq):
+//  * the "+ 0.0" of the init model only turns -0 into +0, and
+//    -0 + dq == +0 + dq for every dq (dq = +0 when code == center);
+//  * a2 + a2 with a2 = a * 0.5 equals a whenever |a| >= 2^-1021 (the halving
+//    is exact), so the two trailing ops are only evaluated for tiny |a|.
+template <int PK>
+__device__ __forceinline__ double predict_chain(const KParams &k, double s0, double s1, double s2) {
+  if (PK == 3 || PK == 1) {
+    const double h = PK == 3 ? __dsub_rn(__dadd_rn(s0, s1), s2) : s0;
+    const double a = h < 0.0 ? __dmul_rn(k.slope, h) : h;
+    if (__builtin_expect(fabs(a) < 0x1p-1020, 0)) {
+      const double a2 = __dmul_rn(a, 0.5);
+      return __dadd_rn(a2, a2);
+    }
+    return a;
+  }
+  return predict(k, s0, s1, s2);
+}
+
 // quantize (D5): center + round_half_away(err / (2 b_a)).
 __device__ __forceinline__ int quantize(double err, double two_ba, int m) {
   double q = __ddiv_rn(err, two_ba);

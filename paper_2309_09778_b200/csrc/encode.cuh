@@ -50,114 +50,196 @@ __device__ void bitonic_sort(unsigned long long *a, int n) {
 
 // K6: build_codebook (D10).  Frequencies = summed validation
 // histograms floored at k (= number of non-trivial validation blocks), leaves
-// sorted by (frequency, code); two-queue Huffman with ties preferring the leaf
-// (Moffat-Katajainen in-place form, same tree); canonical codewords in
-// (length, code) order.  One CTA; smem when 2^m <= 8192, else global scratch.
+// sorted by (frequency, code); two-queue Huffman with ties preferring the leaf;
+// canonical codewords in (length, code) order.  One CTA:
+//   1. bitonic sort of (freq << 17 | sym) keys;
+//   2. two-queue merge by ONE thread with the four queue heads cached in
+//      registers (the only sequential part; internal weights u64, parent of
+//      every internal node recorded);
+//   3. internal-node depths by pointer jumping (parallel);
+//   4. leaf depths from the per-depth internal counts (leaves at depth d =
+//      2 I(d-1) - I(d), shallowest to the heaviest leaves -- the
+//      Moffat-Katajainen leaf-depth assignment), parallel;
+//   5. canonical codes: rank among equal-length symbols by match_any within
+//      a warp + a per-(warp, length) scan, 1024 symbols per round.
+// Scratch in smem when 2^m <= 8192 (20 B / symbol), else in the workspace.
+#ifdef PMZ_CMP_PROFILE
+__device__ long long g_cb_prof[8];
+#define CB_STAMP(i) if (threadIdx.x == 0) g_cb_prof[i] = clock64();
+#else
+#define CB_STAMP(i)
+#endif
+// Two-queue Huffman merge over sorted leaves keys[0..n) (weight = key >> 17):
+// internal node k gets weight I[k]; P[c] = parent of internal node c.  The
+// queue heads live in registers, refilled 3-4 picks ahead of their use.
+__device__ __forceinline__ void huff_merge(const unsigned long long *__restrict__ keys,
+                                           unsigned long long *__restrict__ I, unsigned *__restrict__ P, int n) {
+  const unsigned long long INF = ~0ull;
+  auto leafw = [&](int i) -> unsigned long long { return i < n ? keys[i] >> 17 : INF; };
+  int li = 0, ii = 0;
+  unsigned long long l0 = leafw(0), l1 = leafw(1), l2 = leafw(2), l3 = leafw(3);
+  unsigned long long i0 = INF, i1 = INF, i2 = INF;
+  for (int k = 0; k < n - 1; k++) {
+    unsigned long long w = 0;
+#pragma unroll
+    for (int pick = 0; pick < 2; pick++) {
+      // internal only when strictly lighter (ties prefer the leaf); an
+      // exhausted internal queue reads INF
+      if (l0 <= i0) {
+        w += l0;
+        l0 = l1; l1 = l2; l2 = l3; l3 = leafw(li + 4); li++;
+      } else {
+        w += i0;
+        P[ii] = k;
+        i0 = i1; i1 = i2; i2 = (ii + 3 < k) ? I[ii + 3] : INF; ii++;
+      }
+    }
+    I[k] = w;
+    if (ii == k) i0 = w;
+    else if (ii + 1 == k) i1 = w;
+    else if (ii + 2 == k) i2 = w;
+  }
+  P[n - 2] = n - 2;  // root
+}
+
+constexpr int kCbSmemSyms = 8192;
+constexpr size_t kCbSmem = (size_t)kCbSmemSyms * 20;
+
 __global__ void __launch_bounds__(1024) k_codebook(const unsigned long long *hist, WsStatus *st,
-                                                   unsigned long long *g_keys, unsigned *g_A, uint8_t *lens,
-                                                   unsigned *cw) {
+                                                   unsigned long long *g_keys, unsigned long long *g_I,
+                                                   unsigned *g_P, uint8_t *lens, unsigned *cw) {
   extern __shared__ unsigned long long sm[];
+  __shared__ unsigned s_cntI[64], s_first[64], s_lcum[65];
+  __shared__ unsigned s_wl[32][33];
+  __shared__ int s_maxl;
   count_launch(st);
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5;
   const int m = st->m;
   const int n = 1 << m;
-  const bool in_smem = n <= 8192;
+  const bool in_smem = n <= kCbSmemSyms;
   unsigned long long *keys = in_smem ? sm : g_keys;
-  unsigned *A = in_smem ? (unsigned *)(sm + n) : g_A;
-  unsigned long long kval = hist[kMaxAlpha] > 0 ? hist[kMaxAlpha] : 1ull;
-  for (int s = threadIdx.x; s < n; s += blockDim.x) {
+  unsigned long long *I = in_smem ? sm + n : g_I;
+  unsigned *P = in_smem ? reinterpret_cast<unsigned *>(sm + 2 * n) : g_P;
+  CB_STAMP(0)
+  const unsigned long long kval = hist[kMaxAlpha] > 0 ? hist[kMaxAlpha] : 1ull;
+  for (int s = tid; s < n; s += nt) {
     unsigned long long f = hist[s];
     if (f < kval) f = kval;
     keys[s] = (f << 17) | (unsigned long long)s;
   }
+  if (tid < 64) s_cntI[tid] = 0;
   __syncthreads();
+  CB_STAMP(1)
   bitonic_sort(keys, n);
-  for (int i = threadIdx.x; i < n; i += blockDim.x) A[i] = (unsigned)(keys[i] >> 17);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    // phase 1: pair up (internal node weights / parent pointers in place)
-    A[0] += A[1];
-    int root = 0, leaf = 2;
-    for (int nxt = 1; nxt < n - 1; nxt++) {
-      if (leaf >= n || A[root] < A[leaf]) { A[nxt] = A[root]; A[root++] = nxt; }
-      else A[nxt] = A[leaf++];
-      if (leaf >= n || (root < nxt && A[root] < A[leaf])) { A[nxt] += A[root]; A[root++] = nxt; }
-      else A[nxt] += A[leaf++];
-    }
-    // phase 2: internal node depths
-    A[n - 2] = 0;
-    for (int nxt = n - 3; nxt >= 0; nxt--) A[nxt] = A[A[nxt]] + 1;
-    // phase 3: leaf depths
-    int avail = 1, used = 0, depth = 0, r = n - 2, nxt = n - 1;
-    while (avail > 0) {
-      while (r >= 0 && (int)A[r] == depth) { used++; r--; }
-      while (avail > used) { A[nxt--] = depth; avail--; }
-      avail = 2 * used; depth++; used = 0;
-    }
+  CB_STAMP(2)
+  // ---- 2. two-queue merge (thread 0) ----
+  if (tid == 0) {
+    if (in_smem) huff_merge(sm, sm + n, reinterpret_cast<unsigned *>(sm + 2 * n), n);
+    else huff_merge(g_keys, g_I, g_P, n);
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < n; i += blockDim.x) lens[keys[i] & 0x1ffff] = (uint8_t)A[i];
+  CB_STAMP(3)
+  // ---- 3. depths of the n-1 internal nodes: pointer jumping ----
+  // D, Q overlay I (no longer needed): D[k] = distance to the root so far
+  unsigned *D = reinterpret_cast<unsigned *>(I), *Q = D + n;
+  const int ni = n - 1;
+  for (int k = tid; k < ni; k += nt) {
+    D[k] = k == ni - 1 ? 0u : 1u;
+    Q[k] = P[k];
+  }
   __syncthreads();
-  __shared__ unsigned s_cnt[64], s_next[64];
-  __shared__ int s_maxl;
-  if (threadIdx.x < 64) s_cnt[threadIdx.x] = 0;
-  if (threadIdx.x == 0) s_maxl = 0;
+  for (int span = 1; span < ni; span <<= 1) {
+    unsigned dn[8], qn[8];
+    // ni <= 65535, nt = 1024: <= 64 nodes per thread, 8 per batch
+    for (int k0 = 0; k0 < ni; k0 += 8 * nt) {
+#pragma unroll
+      for (int u = 0; u < 8; u++) {
+        const int k = k0 + u * nt + tid;
+        if (k < ni) {
+          const unsigned q = Q[k];
+          dn[u] = D[k] + D[q];
+          qn[u] = Q[q];
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int u = 0; u < 8; u++) {
+        const int k = k0 + u * nt + tid;
+        if (k < ni) { D[k] = dn[u]; Q[k] = qn[u]; }
+      }
+      __syncthreads();
+    }
+  }
+  for (int k = tid; k < ni; k += nt) atomicAdd(&s_cntI[min(D[k], 63u)], 1u);
   __syncthreads();
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    atomicAdd(&s_cnt[lens[i]], 1u);
-    atomicMax(&s_maxl, (int)lens[i]);
+  // ---- 4. leaf depths ----
+  if (tid == 0) {
+    // leaves at depth d: 2 I(d-1) - I(d) (I(-1) = 1/2: the root level holds
+    // no leaf when n >= 2); cumulative from the shallowest level
+    unsigned cum = 0, prev = 0;
+    int maxl = 0;
+    s_lcum[0] = 0;
+    for (int d = 1; d < 64; d++) {
+      prev = s_cntI[d - 1];
+      const unsigned leaves = 2 * prev - s_cntI[d];
+      cum += leaves;
+      s_lcum[d] = cum;
+      if (leaves) maxl = d;
+    }
+    s_lcum[64] = cum;
+    s_maxl = maxl;
   }
   __syncthreads();
   const int maxl = s_maxl;
-  if (threadIdx.x == 0) {
-    st->max_len = maxl;
-    unsigned long long c = 0;
-    s_cnt[0] = 0;
-    for (int l = 1; l <= maxl && l < 64; l++) { c = (c + s_cnt[l - 1]) << 1; s_next[l] = (unsigned)c; }
+  for (int j = tid; j < n; j += nt) {
+    // the t-th heaviest leaf (t = n-1-j) sits at the first depth d with t < lcum[d]
+    const unsigned t = (unsigned)(n - 1 - j);
+    int d = 1;
+    while (d < 64 && t >= s_lcum[d]) d++;
+    lens[keys[j] & 0x1ffff] = (uint8_t)d;
   }
   __syncthreads();
+  CB_STAMP(4)
+  if (tid == 0) st->max_len = maxl;
   if (maxl > 32) {
-    if (threadIdx.x == 0) atomicOr(&st->err_bits, 1u << (-PMZ_ERR_UNASSIGNED));
+    if (tid == 0) atomicOr(&st->err_bits, 1u << (-PMZ_ERR_UNASSIGNED));
     return;
   }
-  // canonical codewords in (length, code) order: code = first[len] + rank of the
-  // symbol among equal-length symbols; ranks via the sorted order (keys hold the
-  // symbol; the leaf order by (freq, sym) is not the code order, so count
-  // per length with a block-wide scan over symbols in index order).
-  __shared__ unsigned s_wsum[32][33];
-  const int nt = blockDim.x, tid = threadIdx.x;
-  const int per = (n + nt - 1) / nt;
-  const int lo = tid * per, hi = min(n, lo + per);
-  // each thread counts lengths in its contiguous symbol range (lengths <= 32)
-  unsigned myc[33];
-#pragma unroll
-  for (int l = 0; l <= 32; l++) myc[l] = 0;
-  for (int i = lo; i < hi; i++) myc[lens[i]]++;
-  // exclusive prefix over threads, per length: warp scans then warp totals
-  const int wid = tid >> 5, ln = tid & 31;
-  unsigned mypre[33];
-#pragma unroll
-  for (int l = 1; l <= 32; l++) {
-    unsigned v = myc[l], incl = v;
-    for (int d = 1; d < 32; d <<= 1) {
-      const unsigned t = __shfl_up_sync(0xffffffffu, incl, d);
-      if (ln >= d) incl += t;
+  // ---- 5. canonical codes: first code per length ----
+  if (tid == 0) {
+    unsigned cnt[34];
+    for (int l = 0; l <= 33; l++) cnt[l] = 0;
+    for (int d = 1; d <= maxl; d++) cnt[d] = s_lcum[d] - s_lcum[d - 1];
+    unsigned long long c = 0;
+    s_first[0] = 0;
+    for (int l = 1; l <= 32; l++) { c = (c + cnt[l - 1]) << 1; s_first[l] = (unsigned)c; }
+  }
+  __syncthreads();
+  // running per-length base: ranks handed out in earlier rounds
+  __shared__ unsigned s_base[33];
+  if (tid < 33) s_base[tid] = 0;
+  __syncthreads();
+  for (int r0 = 0; r0 < n; r0 += nt) {
+    const int i = r0 + tid;
+    const int l = i < n ? lens[i] : 0;
+    const unsigned peers = __match_any_sync(0xffffffffu, l);
+    const unsigned rank = __popc(peers & ((1u << lane) - 1));
+    // per-warp counts per length
+    for (int q = lane; q < 33; q += 32) s_wl[wid][q] = 0;
+    __syncwarp();
+    if (i < n && rank == 0) s_wl[wid][l] = __popc(peers);
+    __syncthreads();
+    // exclusive scan over warps, per length (thread = length)
+    if (tid < 33) {
+      unsigned acc = s_base[tid];
+      for (int w = 0; w < nt / 32; w++) { const unsigned t = s_wl[w][tid]; s_wl[w][tid] = acc; acc += t; }
+      s_base[tid] = acc;
     }
-    mypre[l] = incl - v;
-    if (ln == 31) s_wsum[wid][l] = incl;
+    __syncthreads();
+    if (i < n) cw[i] = l ? s_first[l] + s_wl[wid][l] + rank : 0u;
+    __syncthreads();
   }
-  __syncthreads();
-  if (tid < 33 && tid >= 1) {
-    unsigned acc = 0;
-    for (int w = 0; w < nt / 32; w++) { const unsigned t = s_wsum[w][tid]; s_wsum[w][tid] = acc; acc += t; }
-  }
-  __syncthreads();
-  unsigned nxt[33];
-#pragma unroll
-  for (int l = 1; l <= 32; l++) nxt[l] = s_next[l] + s_wsum[wid][l] + mypre[l];
-  for (int i = lo; i < hi; i++) {
-    const int l = lens[i];
-    cw[i] = l ? nxt[l]++ : 0;
-  }
+  CB_STAMP(5)
 }
 
 // K7: per-partition payload bits and balance counts.
@@ -286,158 +368,6 @@ __global__ void k_write_header(uint8_t *out, Geom g, KParams k, uint64_t global_
   for (int i = threadIdx.x; i < n; i += blockDim.x) L[i] = lens[i];
 }
 
-// MSB-first OR of a codeword (len <= 32) into a little-endian u32 smem window
-// at window bit position `bit` (bit i of the stream = bit 7 - i%8 of byte i/8).
-__device__ __forceinline__ void or_bits_smem(unsigned *win, unsigned bit, unsigned code, int len) {
-  if (len == 0) return;
-  const unsigned o = bit & 7;
-  const unsigned long long w = ((unsigned long long)code) << (64 - len - o);  // big-endian window
-  const int nbytes = (int)((o + len + 7) >> 3);
-  const unsigned byte0 = bit >> 3;
-#pragma unroll
-  for (int i = 0; i < 5; i++) {
-    if (i < nbytes) {
-      const unsigned by = (unsigned)((w >> (56 - 8 * i)) & 0xff);
-      if (by) {
-        const unsigned bi = byte0 + i;
-        atomicOr(&win[bi >> 2], by << (8 * (bi & 3)));
-      }
-    }
-  }
-}
-
-constexpr int kWinWords = 1024;  // 4 KB bit-packing window per warp
-
-// K10: write one block record per CTA (D9, D13, D15).  Each warp
-// packs a partition's codewords into a shared-memory window (warp prefix sum
-// of code lengths -> bit offsets, smem atomics) and flushes finished bytes to
-// the (byte-aligned, unaligned-to-word) output with coalesced byte stores.
-template <int NW>
-__global__ void __launch_bounds__(NW * 32) k_write_records(Geom g, const BlkP *__restrict__ blkp,
-                                                           const uint16_t *__restrict__ codes,
-                                                           const double *__restrict__ balv,
-                                                           const double *__restrict__ anchors,
-                                                           const unsigned long long *__restrict__ part_bits,
-                                                           const unsigned long long *__restrict__ part_zeros,
-                                                           const unsigned long long *__restrict__ rec_off,
-                                                           const uint8_t *__restrict__ lens,
-                                                           const unsigned *__restrict__ cw, uint8_t *out,
-                                                           unsigned long long rec_base, WsStatus *st) {
-  __shared__ unsigned s_win[NW][kWinWords];
-  __shared__ unsigned long long s_zb[64], s_pb[64];
-  __shared__ unsigned long long s_nbal;
-  count_launch(st);
-  const int64_t b = blockIdx.x;
-  uint8_t *base = out + rec_base + rec_off[b];
-  const BlkP P = blkp[b];
-  if (P.trivial) {
-    if (threadIdx.x == 0) base[0] = 1;
-    return;
-  }
-  const BlockBox bb = block_box(g, b);
-  const int64_t p0 = first_part(g, b);
-  if (threadIdx.x == 0) {
-    unsigned long long zb = 0, pb = 0;
-    for (int i = 0; i < bb.np; i++) {
-      s_zb[i] = zb;
-      s_pb[i] = pb;
-      zb += part_zeros[p0 + i];
-      pb += (part_bits[p0 + i] + 7) / 8;
-    }
-    s_nbal = zb;
-  }
-  __syncthreads();
-  // fixed head: trivial flag, factors, partition table, balance count (coalesced bytes)
-  const unsigned head = 25 + 24u * bb.np;
-  for (unsigned i = threadIdx.x; i < head; i += blockDim.x) {
-    unsigned long long word;
-    unsigned byte;
-    if (i == 0) { base[0] = 0; continue; }
-    if (i < 17) {
-      word = __double_as_longlong(i < 9 ? P.factor_pos : P.factor_neg);
-      byte = (i - 1) & 7;
-    } else if (i < 17 + 24u * bb.np) {
-      const unsigned q = i - 17, pi = q / 24, f = (q % 24) / 8;
-      word = f == 0 ? s_pb[pi] * 8 : (f == 1 ? part_bits[p0 + pi] : __double_as_longlong(anchors[p0 + pi]));
-      byte = q & 7;
-    } else {
-      word = s_nbal;
-      byte = (i - 17 - 24u * bb.np) & 7;
-    }
-    base[i] = (uint8_t)(word >> (8 * byte));
-  }
-  uint8_t *bal0 = base + head;
-  uint8_t *pay0 = bal0 + 8ull * s_nbal;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  unsigned *win = s_win[warp];
-  for (int pi = warp; pi < bb.np; pi += NW) {
-    const int pr0 = pi * g.prow, R = min(g.prow, bb.br - pr0), C = bb.bc;
-    uint8_t *pay = pay0 + s_pb[pi];
-    for (int i = lane; i < kWinWords; i += 32) win[i] = 0;
-    __syncwarp();
-    unsigned long long zb = s_zb[pi];
-    unsigned long long bit = 0, wbase = 0;  // partition bit position, window base (bits, multiple of 32)
-    const int n = R * C;
-    const uint16_t *cbase = codes + (bb.r0 + pr0) * g.cols + bb.c0;
-    const double *bbase = balv + (bb.r0 + pr0) * g.cols + bb.c0;
-    auto load_code = [&](int e, int &r, int &c) -> int {
-      r = 0;
-      c = 0;
-      if (e < n && e > 0) {
-        r = (int)((unsigned)e / (unsigned)C);
-        c = e - r * C;
-        return __ldg(&cbase[(int64_t)r * g.cols + c]);
-      }
-      return -1;
-    };
-    int nr, nc;
-    int ncode = load_code(lane, nr, nc);
-    for (int e0 = 0; e0 < n; e0 += 32) {
-      const int code = ncode, r = nr, c = nc;
-      ncode = load_code(e0 + 32 + lane, nr, nc);  // prefetch the next 32 codes
-      const unsigned zmask = __ballot_sync(0xffffffffu, code == 0);
-      if (code == 0) {
-        const unsigned idx = __popc(zmask & ((1u << lane) - 1));
-        const unsigned long long v = __double_as_longlong(bbase[(int64_t)r * g.cols + c]);
-        uint8_t *d = bal0 + 8ull * (zb + idx);
-#pragma unroll
-        for (int q = 0; q < 8; q++) d[q] = (uint8_t)(v >> (8 * q));
-      }
-      zb += __popc(zmask);
-      const int len = code >= 0 ? __ldg(&lens[code]) : 0;
-      unsigned s = len;
-      for (int o = 1; o < 32; o <<= 1) {
-        const unsigned t = __shfl_up_sync(0xffffffffu, s, o);
-        if (lane >= o) s += t;
-      }
-      if (code >= 0) or_bits_smem(win, (unsigned)(bit + (s - len) - wbase), __ldg(&cw[code]), len);
-      bit += __shfl_sync(0xffffffffu, s, 31);
-      __syncwarp();
-      if (bit - wbase > (unsigned long long)(kWinWords - 64) * 32) {
-        // flush the whole words below the current position
-        const unsigned nw = (unsigned)((bit - wbase) >> 5);
-        uint8_t *dst = pay + (wbase >> 3);
-        const uint8_t *wb = reinterpret_cast<const uint8_t *>(win);
-        for (unsigned i = lane; i < nw * 4; i += 32) dst[i] = wb[i];
-        __syncwarp();
-        const unsigned keep = win[nw];
-        __syncwarp();
-        for (int i = lane; i < kWinWords; i += 32) win[i] = 0;
-        __syncwarp();
-        if (lane == 0) win[0] = keep;
-        __syncwarp();
-        wbase += (unsigned long long)nw * 32;
-      }
-    }
-    // final flush, zero-padded to the byte boundary (D15)
-    const unsigned nbytes = (unsigned)(((bit + 7) >> 3) - (wbase >> 3));
-    uint8_t *dst = pay + (wbase >> 3);
-    const uint8_t *wb = reinterpret_cast<const uint8_t *>(win);
-    for (unsigned i = lane; i < nbytes; i += 32) dst[i] = wb[i];
-    __syncwarp();
-  }
-}
-
 // Store 8 little-endian bytes at an arbitrary byte address with at most four
 // naturally aligned stores.
 __device__ __forceinline__ void put8_unaligned(uint8_t *p, unsigned long long v) {
@@ -473,231 +403,6 @@ __device__ __forceinline__ void or_byte(uint8_t *p, unsigned v) {
   if (!v) return;
   const uintptr_t a = reinterpret_cast<uintptr_t>(p);
   atomicOr(reinterpret_cast<unsigned *>(a & ~(uintptr_t)3), v << (8 * (unsigned)(a & 3)));
-}
-
-// K10 (v2): one warp per partition.  The partition's codes are staged in
-// shared memory (coalesced), lane j owns a contiguous run of them in raster
-// order (the anchor excluded, D1): pass 1 sums code lengths, a warp scan gives
-// each lane its bit offset, pass 2 packs the codewords MSB-first in a 64-bit
-// register and stores whole bytes (the <= 2 bytes a lane shares with its
-// neighbours are zeroed first and OR-ed atomically).  The balance list is
-// written by a lane-parallel ballot pass.  The warp of partition 0 also writes
-// the block's record head (D9, D13, D15).
-#ifdef PMZ_CMP_PROFILE
-__device__ long long g_wr_prof[65536][6];
-#define WR_STAMP(i) if (lane == 0 && p < 65536) g_wr_prof[p][i] = clock64();
-#else
-#define WR_STAMP(i)
-#endif
-constexpr unsigned kPackWords = 2048;  // 8 KB packed payload per warp in smem (else direct global path)
-
-template <int NW>
-__global__ void __launch_bounds__(NW * 32) k_write_records2(Geom g, const BlkP *__restrict__ blkp,
-                                                            const uint16_t *__restrict__ codes,
-                                                            const double *__restrict__ balv,
-                                                            const double *__restrict__ anchors,
-                                                            const unsigned long long *__restrict__ part_bits,
-                                                            const unsigned long long *__restrict__ part_zeros,
-                                                            const unsigned long long *__restrict__ rec_off,
-                                                            const uint8_t *__restrict__ lens,
-                                                            const unsigned *__restrict__ cw, int m, uint8_t *out,
-                                                            unsigned long long rec_base,
-                                                            const uint16_t *__restrict__ zrow, WsStatus *st) {
-  __shared__ uint8_t s_len[4096];
-  __shared__ unsigned s_cw[4096];
-  extern __shared__ __align__(16) uint16_t s_codes_all[];
-  count_launch(st);
-  const bool small_tab = m <= 12;
-  if (small_tab) {
-    for (int i = threadIdx.x; i < (1 << m); i += blockDim.x) {
-      s_len[i] = lens[i];
-      s_cw[i] = cw[i];
-    }
-  }
-  __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t p = (int64_t)blockIdx.x * NW + warp;
-  if (p >= g.nparts) return;
-  int64_t b;
-  int pi;
-  part_of(g, p, b, pi);
-  uint8_t *base = out + rec_base + rec_off[b];
-  const BlkP P = blkp[b];
-  if (P.trivial) {
-    if (pi == 0 && lane == 0) base[0] = 1;
-    return;
-  }
-  WR_STAMP(0)
-  const BlockBox bb = block_box(g, b);
-  const int64_t p0 = first_part(g, b);
-  unsigned long long zb = 0, pb = 0, nbal = 0;
-  for (int i = 0; i < bb.np; i++) {
-    const unsigned long long z = part_zeros[p0 + i], by = (part_bits[p0 + i] + 7) / 8;
-    if (i < pi) { zb += z; pb += by; }
-    nbal += z;
-  }
-  const unsigned head = 25 + 24u * bb.np;
-  if (pi == 0) {
-    // record head: trivial flag, factors, partition table, balance count
-    for (unsigned i = lane; i < head; i += 32) {
-      unsigned long long word;
-      unsigned byte;
-      if (i == 0) { base[0] = 0; continue; }
-      if (i < 17) {
-        word = __double_as_longlong(i < 9 ? P.factor_pos : P.factor_neg);
-        byte = (i - 1) & 7;
-      } else if (i < 17 + 24u * bb.np) {
-        const unsigned q = i - 17, pq = q / 24, f = (q % 24) / 8;
-        if (f == 0) {
-          unsigned long long off = 0;
-          for (unsigned t = 0; t < pq; t++) off += (part_bits[p0 + t] + 7) / 8;
-          word = off * 8;
-        } else {
-          word = f == 1 ? part_bits[p0 + pq] : __double_as_longlong(anchors[p0 + pq]);
-        }
-        byte = q & 7;
-      } else {
-        word = nbal;
-        byte = (i - 17 - 24u * bb.np) & 7;
-      }
-      base[i] = (uint8_t)(word >> (8 * byte));
-    }
-  }
-  uint8_t *bal = base + head + 8ull * zb;
-  uint8_t *pay = base + head + 8ull * nbal + pb;
-  const int pr0 = pi * g.prow, R = min(g.prow, bb.br - pr0), C = bb.bc;
-  const uint16_t *cp = codes + (bb.r0 + pr0) * g.cols + bb.c0;
-  uint16_t *sc = s_codes_all + (size_t)warp * ((size_t)g.prow * g.bc + 160 + 2 * kPackWords + 4);
-  const unsigned n = (unsigned)(R * C - 1);  // codes at raster indices 1..n
-  // lane j packs codes [1 + j RUN, 1 + (j+1) RUN); they are staged at
-  // sc[j STRIDE + i] with STRIDE/2 odd so the 32 lanes hit 32 different banks
-  const unsigned RUN = (n + 31) / 32;
-  unsigned STRIDE = RUN + 1;
-  while ((STRIDE & 1) || !((STRIDE >> 1) & 1)) STRIDE++;
-  const unsigned rrun = RUN > 1 ? (unsigned)(0x100000000ull / RUN) + 1u : 0u;  // floor(x/RUN) = umulhi(x, rrun)
-  auto spos = [&](unsigned e) -> unsigned {  // e >= 1
-    const unsigned x = e - 1, j = RUN > 1 ? __umulhi(x, rrun) : x;
-    return j * STRIDE + (x - j * RUN);
-  };
-  // stage the partition's codes (coalesced global reads)
-  for (int r = 0; r < R; r++)
-    for (int c = lane; c < C; c += 32) {
-      const unsigned e = (unsigned)(r * C + c);
-      if (e) sc[spos(e)] = __ldg(&cp[(int64_t)r * g.cols + c]);
-    }
-  __syncwarp();
-  WR_STAMP(1)
-  // balance list: the compress kernel left each row's balance values
-  // compacted at the start of the row segment (zrow = counts): contiguous,
-  // coalesced copies at row offsets from a warp scan of the counts
-  {
-    const double *bp = balv + (bb.r0 + pr0) * g.cols + bb.c0;
-    const unsigned zc = lane < R ? zrow[p * 32 + lane] : 0u;
-    unsigned zi = zc;
-    for (int d = 1; d < 32; d <<= 1) {
-      const unsigned t = __shfl_up_sync(0xffffffffu, zi, d);
-      if (lane >= d) zi += t;
-    }
-    zi -= zc;  // exclusive
-    // flattened over the partition's whole list: element i belongs to the
-    // last row whose exclusive prefix is <= i (5-step search over the lanes'
-    // prefixes); 4 independent loads in flight per lane
-    const unsigned T = __shfl_sync(0xffffffffu, zi + zc, 31);
-    for (unsigned i0 = 0; i0 < T; i0 += 128) {
-      unsigned long long v[4];
-      unsigned ii[4];
-#pragma unroll
-      for (int u = 0; u < 4; u++) {
-        const unsigned i = i0 + u * 32 + lane;
-        int r = 0;
-#pragma unroll
-        for (int d = 16; d >= 1; d >>= 1) {
-          const unsigned zr = __shfl_sync(0xffffffffu, zi, r + d);
-          if (r + d < R && zr <= i) r += d;
-        }
-        const unsigned rb = __shfl_sync(0xffffffffu, zi, r);
-        ii[u] = i;
-        v[u] = i < T ? __double_as_longlong(__ldg(&bp[(int64_t)r * g.cols + (i - rb)])) : 0ull;
-      }
-#pragma unroll
-      for (int u = 0; u < 4; u++)
-        if (ii[u] < T) put8_unaligned(bal + 8ull * ii[u], v[u]);
-    }
-  }
-  WR_STAMP(2)
-  auto len_of = [&](unsigned c) -> unsigned { return small_tab ? s_len[c] : __ldg(&lens[c]); };
-  auto cw_of = [&](unsigned c) -> unsigned { return small_tab ? s_cw[c] : __ldg(&cw[c]); };
-  const unsigned e0 = min(n + 1, 1 + lane * RUN), e1 = min(n + 1, 1 + (lane + 1) * RUN);
-  const uint16_t *myc = sc + lane * STRIDE;
-  unsigned bits = 0;
-#pragma unroll 8
-  for (unsigned e = e0; e < e1; e++) bits += len_of(myc[e - e0]);
-  unsigned ib = bits;
-  for (int d = 1; d < 32; d <<= 1) {
-    const unsigned t = __shfl_up_sync(0xffffffffu, ib, d);
-    if (lane >= d) ib += t;
-  }
-  const unsigned B = ib - bits;
-  const unsigned total_bits = __shfl_sync(0xffffffffu, ib, 31);
-  const unsigned nwords = (total_bits + 31) >> 5;
-  unsigned *sw = reinterpret_cast<unsigned *>(sc + 32 * STRIDE + 2);  // payload words after the codes
-  if (nwords <= kPackWords) {
-    // MSB-first words in shared memory: interior words stored, the two words a
-    // lane may share with its neighbours OR-ed (zeroed first)
-    sw = reinterpret_cast<unsigned *>((reinterpret_cast<uintptr_t>(sw) + 3) & ~(uintptr_t)3);
-    const unsigned fw = B >> 5, lw = bits ? (B + bits - 1) >> 5 : fw;
-    if (bits) { sw[fw] = 0; sw[lw] = 0; }
-    __syncwarp();
-    WR_STAMP(3)
-    unsigned long long acc = 0;
-    int nacc = (int)(B & 31);
-    unsigned ow = fw;
-#pragma unroll 4
-    for (unsigned e = e0; e < e1; e++) {
-      const unsigned cd = myc[e - e0];
-      const int l = (int)len_of(cd);
-      acc = (acc << l) | cw_of(cd);
-      nacc += l;
-      if (nacc >= 32) {
-        const unsigned w = (unsigned)(acc >> (nacc - 32));
-        if (ow == fw || ow == lw) atomicOr(&sw[ow], w);
-        else sw[ow] = w;
-        ow++;
-        nacc -= 32;
-      }
-    }
-    if (nacc > 0) atomicOr(&sw[ow], (unsigned)(acc << (32 - nacc)));
-    __syncwarp();
-    // coalesced byte copy to the (byte-aligned) payload
-    const unsigned nbytes = (total_bits + 7) >> 3;
-    for (unsigned i = lane; i < nbytes; i += 32) pay[i] = (uint8_t)(sw[i >> 2] >> (24 - 8 * (i & 3)));
-  } else {
-    const unsigned fbyte = B >> 3, lbyte = bits ? (B + bits - 1) >> 3 : fbyte;
-    if (bits) {
-      pay[fbyte] = 0;
-      pay[lbyte] = 0;
-    }
-    __syncwarp();
-    unsigned long long acc = 0;
-    int nacc = (int)(B & 7);  // leading bits owned by the previous lane
-    unsigned outb = fbyte;
-    for (unsigned e = e0; e < e1; e++) {
-      const unsigned cd = myc[e - e0];
-      const int l = (int)len_of(cd);
-      acc = (acc << l) | cw_of(cd);
-      nacc += l;
-      while (nacc >= 8) {
-        const unsigned byte = (unsigned)(acc >> (nacc - 8)) & 0xffu;
-        if (outb == fbyte || outb == lbyte) or_byte(pay + outb, byte);
-        else pay[outb] = (uint8_t)byte;
-        outb++;
-        nacc -= 8;
-      }
-    }
-    if (nacc > 0) or_byte(pay + outb, (unsigned)(acc << (8 - nacc)) & 0xffu);
-  }
-  __syncwarp();
-  WR_STAMP(4)
 }
 
 // One block record's share written by ONE CTA per partition (kWT threads):

@@ -199,6 +199,10 @@ __global__ void __launch_bounds__(kPPC * 64) k_compress_ws(const float *__restri
     const int ngroups = (nsteps + 31) >> 5;
     double hl = 0.0, hp = 0.0;
     unsigned zeros = 0, repairs = 0;
+    const double mu = 0x1p-20;
+    const double dpos_m = __dsub_rn(k.dpos, mu), dneg_m = __dadd_rn(k.dneg, mu);
+    const double dpos_p = __dadd_rn(k.dpos, mu), dneg_p = __dsub_rn(k.dneg, mu);
+    const bool tlt1 = k.repair_t < 1.0;
     for (int kg = 0; kg < ngroups; kg++) {
       if (kg < nch) TIMED_SYNC(bar0 + kg % kSlots)  // full: chunk kg ready
       const int t1 = min(nsteps, (kg + 1) * 32);
@@ -213,28 +217,31 @@ __global__ void __launch_bounds__(kPPC * 64) k_compress_ws(const float *__restri
           const int s = (c >> 5) % kSlots, j = c & 31;
           const double v = W.v[s][lane][j];
           const int code = W.code[s][lane][j];
-          double vh = v;
-          if (code == 0) {
-            zeros++;
-          } else if (code != kAnc) {
-            const bool hw = c > 0, hn = lane > 0;
-            const double vhat = __dadd_rn(predict_k<PK>(k, hw ? hl : 0.0, hn ? nhl : 0.0, (hw && hn) ? nhp : 0.0),
-                                          __dmul_rn((double)(code - center), k.two_ba));
-            int viol = check_cls(vhat, v, W.cls[s][lane][j], P, k);
-            if (viol < 0) {
-              const float xz = zfloor(__ldg(xp + lane * g.cols + c));
-              viol = violates(inv_f32(vhat, P, amb), xz, k.repair_t) ? 1 : 0;
-            }
-            if (viol) {
-              W.code[s][lane][j] = 0;
-              zeros++;
-              repairs++;
-            } else {
-              vh = vhat;
-            }
+          const int cls = W.cls[s][lane][j];
+          const double dq = __dmul_rn((double)(code - center), k.two_ba);  // off the chain
+          const bool hw = c > 0, hn = lane > 0;
+          const double vhat = __dadd_rn(predict_chain<PK>(k, hw ? hl : 0.0, hn ? nhl : 0.0, (hw && hn) ? nhp : 0.0), dq);
+          // check_cls, predicated (D8 log-domain filter)
+          const double d = __dsub_rn(vhat, v);
+          const bool side_ok = cls == 1 ? (vhat <= P.boundary) : (vhat > P.boundary);
+          const bool nz = vhat > P.zero_threshold;
+          const bool in12 = side_ok && nz;
+          const bool is12 = cls == 1 || cls == 2;
+          bool acc = is12 ? (in12 && d < dpos_m && d > dneg_m) : (cls == 0 && !nz);
+          bool vio = is12 && ((tlt1 && !in12) || (in12 && (d > dpos_p || d < dneg_p)));
+          const bool normal = code != 0 && code != kAnc;
+          if (__builtin_expect(normal && !acc && !vio, 0)) {
+            const float xz = zfloor(__ldg(xp + lane * g.cols + c));
+            vio = violates(inv_f32(vhat, P, amb), xz, k.repair_t);
           }
+          const bool keep = normal && !vio;
+          if (normal && !keep) {
+            W.code[s][lane][j] = 0;
+            repairs++;
+          }
+          zeros += (code == 0 || (normal && !keep)) ? 1u : 0u;
           hp = hl;
-          hl = vh;
+          hl = keep ? vhat : v;
         }
       }
       if (kg >= 1 && kg - 1 < nch) {

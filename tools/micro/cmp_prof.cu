@@ -41,6 +41,11 @@ int main(int argc, char **argv) {
     for (int i = 0; i < G.nparts; i++) for (int j = 0; j < 4; j++) ph[j] += (double)(w[i * 6 + j + 1] - w[i * 6 + j]);
     printf("write_records: stage %.0f  balance %.0f  pass1 %.0f  pack %.0f\n", ph[0] / G.nparts, ph[1] / G.nparts, ph[2] / G.nparts, ph[3] / G.nparts);
   }
+  {
+    long long cb[8];
+    cudaMemcpyFromSymbol(cb, g_cb_prof, 64);
+    printf("codebook: init %lld sort %lld mk %lld lens+cnt %lld canon %lld\n", cb[1] - cb[0], cb[2] - cb[1], cb[3] - cb[2], cb[4] - cb[3], cb[5] - cb[4]);
+  }
   printf("producer: avg %.0f cycles, waiting %.0f\nconsumer: avg %.0f cycles, waiting %.0f\n", pd / n, pw / n, cd / n, cw / n);
   return 0;
 }
