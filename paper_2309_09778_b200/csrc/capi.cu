@@ -53,6 +53,7 @@ Geom make_geom(int64_t rows, int64_t cols, int br, int bc, int prow, int64_t blo
   g.br_last = g.nbr > 0 ? (int)(rows - (g.nbr - 1) * br) : 0;
   g.np_last = g.nbr > 0 ? (g.br_last + prow - 1) / prow : 0;
   g.nparts = g.nbr > 0 ? (g.nbr - 1) * g.nbc * g.np_full + g.nbc * g.np_last : 0;
+  g.nct = (bc + 31) / 32;
   return g;
 }
 
@@ -93,6 +94,10 @@ KParams kparams(const pmz_params *p) {
   k.inv_two_ba = 1.0 / (2.0 * p->b_a);
   k.dpos = std::log2(1.0 + p->repair_t);
   k.dneg = std::log2(1.0 - p->repair_t);
+  k.dpos_m = k.dpos - 0x1p-20;
+  k.dneg_m = k.dneg + 0x1p-20;
+  k.dpos_p = k.dpos + 0x1p-20;
+  k.dneg_p = k.dneg - 0x1p-20;
   k.init_model = is_init_model(p->S, p->w1, p->w2);
   return k;
 }
@@ -129,12 +134,10 @@ WsLayout compress_layout(const Geom &g) {
   L.rec_off = take(8 * (size_t)(g.nblocks + 1));
   L.cub_bytes = cub_scan_bytes(g.nblocks + 1);
   L.cub_tmp = take(L.cub_bytes);
-  L.codes = take(2 * (size_t)(g.rows * g.cols));
-  L.balv = take(8 * (size_t)(g.rows * g.cols));
-  L.zrow = take(2 * 32 * (size_t)(g.nparts + 1));
-  L.vbuf = take(8 * (size_t)(g.rows * g.cols));
-  L.rqbuf = take(2 * (size_t)(g.rows * g.cols));
-  L.clsbuf = take((size_t)(g.rows * g.cols));
+  const size_t ntile = (size_t)g.nparts * (size_t)g.nct * kTile;  // partition-tiled elements
+  L.vbuf = take(8 * ntile);
+  L.rqbuf = take(2 * ntile);
+  L.clsbuf = take(ntile);
   L.total = o;
   return L;
 }
@@ -162,11 +165,9 @@ int launch_ws(const KParams &k, unsigned grid, cudaStream_t st, const float *x, 
               const WsLayout &L) {
   CK(cudaFuncSetAttribute(k_compress_ws<PK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWscSmem));
   k_compress_ws<PK><<<grid, kPPC * 64, kWscSmem, st>>>(x, G, k, at<BlkP>(d_ws, L.blkp), at<WsStatus>(d_ws, L.status),
-                                                       at<uint16_t>(d_ws, L.codes), at<double>(d_ws, L.balv),
-                                                       at<double>(d_ws, L.anchors),
-                                                       at<unsigned long long>(d_ws, L.part_zeros),
-                                                       at<uint16_t>(d_ws, L.zrow), at<double>(d_ws, L.vbuf),
-                                                       at<int16_t>(d_ws, L.rqbuf), at<uint8_t>(d_ws, L.clsbuf));
+                                                       at<double>(d_ws, L.vbuf), at<int16_t>(d_ws, L.rqbuf),
+                                                       at<uint8_t>(d_ws, L.clsbuf), at<double>(d_ws, L.anchors),
+                                                       at<unsigned long long>(d_ws, L.part_zeros));
   return PMZ_OK;
 }
 
@@ -285,7 +286,7 @@ int pmz_compress_codes(const float *d_in, const pmz_geom *g, const pmz_params *p
   }
   if (n_val > 0) {
     dim3 grid(16, (unsigned)n_val);
-    k_val_hist<kNT><<<grid, kNT, 0, st>>>(G, at<BlkP>(d_ws, L.blkp), d_val, at<uint16_t>(d_ws, L.codes),
+    k_val_hist<kNT><<<grid, kNT, 0, st>>>(G, at<BlkP>(d_ws, L.blkp), d_val, at<int16_t>(d_ws, L.rqbuf),
                                           at<unsigned long long>(d_ws, L.hist), at<WsStatus>(d_ws, L.status));
   }
   return launch_check();
@@ -327,7 +328,7 @@ int pmz_compress_finish(const pmz_geom *g, const pmz_params *p, int write_header
                                        at<unsigned>(d_ws, L.cw));
   if (G.nparts > 0) {
     unsigned grid = (unsigned)((G.nparts + kWarps - 1) / kWarps);
-    k_part_bits<kWarps><<<grid, kWarps * 32, 0, st>>>(G, at<BlkP>(d_ws, L.blkp), at<uint16_t>(d_ws, L.codes),
+    k_part_bits<kWarps><<<grid, kWarps * 32, 0, st>>>(G, at<BlkP>(d_ws, L.blkp), at<int16_t>(d_ws, L.rqbuf),
                                                       at<uint8_t>(d_ws, L.lens),
                                                       at<unsigned long long>(d_ws, L.part_bits), S);
   }
@@ -365,11 +366,11 @@ int pmz_compress_finish(const pmz_geom *g, const pmz_params *p, int write_header
   if (write_header)
     k_write_header<<<1, 256, 0, st>>>(d_out, G, k, g->global_rows, at<uint8_t>(d_ws, L.lens), S);
   if (G.nparts > 0) {
-    k_write_part<<<(unsigned)G.nparts, kWT, 0, st>>>(
-        G, at<BlkP>(d_ws, L.blkp), at<uint16_t>(d_ws, L.codes), at<double>(d_ws, L.balv),
+    k_write_part<<<(unsigned)G.nparts, kWT, write_part_smem(hs.m), st>>>(
+        G, at<BlkP>(d_ws, L.blkp), at<int16_t>(d_ws, L.rqbuf), at<double>(d_ws, L.vbuf),
         at<double>(d_ws, L.anchors), at<unsigned long long>(d_ws, L.part_bits),
         at<unsigned long long>(d_ws, L.part_zeros), at<unsigned long long>(d_ws, L.rec_off),
-        at<uint8_t>(d_ws, L.lens), at<unsigned>(d_ws, L.cw), hs.m, d_out, rec_base, at<uint16_t>(d_ws, L.zrow), S);
+        at<uint8_t>(d_ws, L.lens), at<unsigned>(d_ws, L.cw), hs.m, d_out, rec_base, S);
   }
   if (d_block_offsets)
     k_block_offsets<<<(unsigned)((G.nblocks + 1 + 255) / 256), 256, 0, st>>>(

@@ -16,6 +16,8 @@ struct KParams {
   double b_r, b_a, two_ba, onepbr2, eps0, repair_t, slope, coverage_target;
   double inv_two_ba;       // RN(1 / (2 b_a)) for the filtered quantizer
   double dpos, dneg;       // log2(1 + t), log2(1 - t): violation thresholds in the log domain
+  double dpos_m, dneg_m;   // dpos - mu, dneg + mu: inside -> certainly within the bound (mu = 2^-20)
+  double dpos_p, dneg_p;   // dpos + mu, dneg - mu: outside -> certainly a violation
   int init_model;          // weights equal init_model: constant-folded predictor
   double w1[8], w2[2];
   int S, H, block_rows, block_cols, partition_rows, m_fixed;
@@ -30,7 +32,20 @@ struct Geom {
   int np_full, np_last;      // partitions per block (full / last block-row)
   int64_t nparts;
   int br_last;               // rows of the last block-row
+  int nct;                   // 32x32 tiles per partition row-strip (ceil(bc / 32))
 };
+
+// Partition-tiled layout of the per-element compress arrays (v, rq, cls):
+// partition p, column chunk kc -> one contiguous 32x32 tile (row-major,
+// 1024 elements; rows >= R / columns >= C are padding).  A chunk is then one
+// bulk copy.
+constexpr int kTile = 1024;
+__host__ __device__ __forceinline__ int64_t tile_base(const Geom &g, int64_t p, int kc) {
+  return (p * g.nct + kc) * (int64_t)kTile;
+}
+__host__ __device__ __forceinline__ int64_t tile_elem(const Geom &g, int64_t p, int r, int c) {
+  return tile_base(g, p, c >> 5) + r * 32 + (c & 31);
+}
 
 // Per-block transform parameters (TransformParams fields, transform.py:61-81).
 struct BlkP {

@@ -6,28 +6,35 @@
 namespace pmz {
 
 // K5: per-block code histograms of the validation blocks, summed (D10).
+// Reads the final rq tiles (a block's partitions are consecutive, so its
+// tiles are one contiguous range); code = code_of_rq(rq, center).
 // Warp-aggregated: lanes holding the same code elect one leader (match_any).
 template <int NT>
 __global__ void __launch_bounds__(NT) k_val_hist(Geom g, const BlkP *__restrict__ blkp, const int64_t *val_ids,
-                                                 const uint16_t *__restrict__ codes, unsigned long long *hist,
+                                                 const int16_t *__restrict__ rqbuf, unsigned long long *hist,
                                                  WsStatus *st) {
   count_launch(st);
-  int64_t b = val_ids[blockIdx.y];
+  const int64_t b = val_ids[blockIdx.y];
   if (blkp[b].trivial) return;
   if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&hist[kMaxAlpha], 1ull);  // k for the floor (D10)
-  BlockBox bb = block_box(g, b);
-  int64_t n = (int64_t)bb.br * bb.bc;
+  const int center = 1 << (st->m - 1);
+  const BlockBox bb = block_box(g, b);
+  const int64_t p0 = first_part(g, b);
+  const int64_t n = (int64_t)bb.np * g.nct * kTile;
+  const int16_t *rp = rqbuf + tile_base(g, p0, 0);
   const int lane = threadIdx.x & 31;
   for (int64_t base = (int64_t)blockIdx.x * NT; base < n; base += (int64_t)gridDim.x * NT) {
-    int64_t e = base + threadIdx.x;
+    const int64_t i = base + threadIdx.x;
     int code = -1;
-    if (e < n) {
-      int r = (int)(e / bb.bc), c = (int)(e - (int64_t)r * bb.bc);
-      if (!((r % g.prow) == 0 && c == 0)) code = codes[(bb.r0 + r) * g.cols + bb.c0 + c];
+    if (i < n) {
+      const int t = (int)(i >> 10), off = (int)(i & (kTile - 1));
+      const int pi = t / g.nct, kc = t - pi * g.nct;
+      const int r = off >> 5, c = kc * 32 + (off & 31);
+      const int R = min(g.prow, bb.br - pi * g.prow);
+      if (r < R && c < bb.bc && (r | c)) code = code_of_rq(__ldg(rp + i), center);
     }
-    unsigned peers = __match_any_sync(0xffffffffu, code);
-    int leader = __ffs(peers) - 1;
-    if (code >= 0 && lane == leader) atomicAdd(&hist[code], (unsigned long long)__popc(peers));
+    const unsigned peers = __match_any_sync(0xffffffffu, code);
+    if (code >= 0 && lane == __ffs(peers) - 1) atomicAdd(&hist[code], (unsigned long long)__popc(peers));
   }
 }
 
@@ -242,10 +249,11 @@ __global__ void __launch_bounds__(1024) k_codebook(const unsigned long long *his
   CB_STAMP(5)
 }
 
-// K7: per-partition payload bits and balance counts.
+// K7: per-partition payload bits from the final rq tiles (one warp per
+// partition; 8 residuals per 16-byte load, the anchor excluded).
 template <int NW>
 __global__ void __launch_bounds__(NW * 32) k_part_bits(Geom g, const BlkP *__restrict__ blkp,
-                                                       const uint16_t *__restrict__ codes,
+                                                       const int16_t *__restrict__ rqbuf,
                                                        const uint8_t *__restrict__ lens,
                                                        unsigned long long *part_bits, WsStatus *st) {
   count_launch(st);
@@ -257,39 +265,26 @@ __global__ void __launch_bounds__(NW * 32) k_part_bits(Geom g, const BlkP *__res
   part_of(g, p, b, pi);
   unsigned long long bits = 0;
   if (!blkp[b].trivial) {
-    BlockBox bb = block_box(g, b);
-    int pr0 = pi * g.prow, R = min(g.prow, bb.br - pr0), C = bb.bc;
-    const uint16_t *cp = codes + (bb.r0 + pr0) * g.cols + bb.c0;
-    if ((g.cols & 7) == 0 && (C & 7) == 0) {
-      const int vpr = C >> 3, nv = R * vpr;  // 8 codes per 16-byte vector
-      for (int i0 = lane; i0 < nv; i0 += 128) {
-        uint4 q[4];
+    const int center = 1 << (st->m - 1);
+    const BlockBox bb = block_box(g, b);
+    const int R = min(g.prow, bb.br - pi * g.prow), C = bb.bc, nch = (C + 31) >> 5;
+    const uint4 *tp = reinterpret_cast<const uint4 *>(rqbuf + tile_base(g, p, 0));
+    // vector v of a tile: row v >> 2, columns 8 (v & 3) .. + 7
+    for (int kc = 0; kc < nch; kc++) {
+      uint4 q[4];
 #pragma unroll
-        for (int u = 0; u < 4; u++) {
-          const int i = i0 + 32 * u;
-          if (i < nv) {
-            const int r = i / vpr, c = (i - r * vpr) << 3;
-            q[u] = __ldg(reinterpret_cast<const uint4 *>(cp + (int64_t)r * g.cols + c));
-          } else {
-            q[u] = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);  // anchor marker -> len 0 below
-          }
+      for (int u = 0; u < 4; u++) q[u] = __ldg(tp + kc * (kTile / 8) + lane + 32 * u);
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const int vi = lane + 32 * u, r = vi >> 2, c0 = kc * 32 + (vi & 3) * 8;
+        if (r >= R) continue;
+        const unsigned w[4] = {q[u].x, q[u].y, q[u].z, q[u].w};
+#pragma unroll
+        for (int h = 0; h < 8; h++) {
+          const int c = c0 + h;
+          const int rq = (int)(int16_t)(w[h >> 1] >> (16 * (h & 1)));
+          if (c < C && (r | c)) bits += __ldg(&lens[code_of_rq(rq, center)]);
         }
-#pragma unroll
-        for (int u = 0; u < 4; u++) {
-          const unsigned w[4] = {q[u].x, q[u].y, q[u].z, q[u].w};
-#pragma unroll
-          for (int h = 0; h < 4; h++) {
-            const unsigned a = w[h] & 0xffff, c2 = w[h] >> 16;
-            if (a != 0xffff) bits += __ldg(&lens[a]);
-            if (c2 != 0xffff) bits += __ldg(&lens[c2]);
-          }
-        }
-      }
-    } else {
-      for (int r = 0; r < R; r++) {
-        const uint16_t *crow = cp + (int64_t)r * g.cols;
-        for (int c = lane; c < C; c += 32)
-          if (r | c) bits += __ldg(&lens[crow[c]]);
       }
     }
     for (int o = 16; o > 0; o >>= 1) bits += __shfl_xor_sync(0xffffffffu, bits, o);
@@ -405,31 +400,57 @@ __device__ __forceinline__ void or_byte(uint8_t *p, unsigned v) {
   atomicOr(reinterpret_cast<unsigned *>(a & ~(uintptr_t)3), v << (8 * (unsigned)(a & 3)));
 }
 
+// Copy n bytes from shared memory (word-aligned source) to an arbitrary
+// global byte address with aligned 32-bit stores (funnel-shifted source
+// words; at most 3 + 3 bytes at the ends go out as single bytes).  CTA-wide.
+__device__ __forceinline__ void copy_s2g_bytes(uint8_t *dst, const unsigned *src, unsigned n, int tid, int nt) {
+  if (n == 0) return;
+  const uint8_t *sb = reinterpret_cast<const uint8_t *>(src);
+  const unsigned head = (unsigned)((4 - ((uintptr_t)dst & 3)) & 3);
+  const unsigned hb = min(head, n);
+  for (unsigned i = tid; i < hb; i += nt) dst[i] = sb[i];
+  if (n <= hb) return;
+  const unsigned nw = (n - hb) >> 2, tail = (n - hb) & 3;
+  unsigned *dw = reinterpret_cast<unsigned *>(dst + hb);
+  // output word j = source bytes [hb + 4j, hb + 4j + 4): little-endian words
+  const unsigned sh = 8 * (hb & 3), wq = hb >> 2;
+  for (unsigned j = tid; j < nw; j += nt) {
+    const unsigned lo = src[wq + j];
+    dw[j] = sh ? __funnelshift_r(lo, src[wq + j + 1], sh) : lo;
+  }
+  for (unsigned i = tid; i < tail; i += nt) dst[hb + 4 * nw + i] = sb[hb + 4 * nw + i];
+}
+
 // One block record's share written by ONE CTA per partition (kWT threads):
 // the record head (partition 0 only), the partition's slice of the block
-// balance list, and its Huffman substream.  Thread t
-// encodes the raster run [t RUN, (t+1) RUN) of the partition (raster index 0
-// = the anchor, not coded, D1); bit offsets come from a CTA-wide scan of the
-// runs' bit counts; words are assembled MSB-first in shared memory and copied
-// out coalesced.
+// balance list, and its Huffman substream (D9).
+// A run is one 32-column tile-row segment of the partition (run q = row *
+// nch + chunk: raster order); thread t owns runs t, t + kWT, ...  Per round of
+// kWT runs: the 32 residuals come in four 16-byte loads, pass 1 counts bits
+// and balance points (code 0; raster index 0 = the anchor is neither, D1), a
+// CTA scan gives both offsets; balance values (TRUE surface, D9) are staged in
+// shared memory and copied out with aligned word stores; codewords are
+// assembled MSB-first into shared-memory words, copied out at the end.
 constexpr int kWT = 256;
 constexpr unsigned kPartWords = 4096;  // 16 KB payload staging (else direct byte writes)
+constexpr unsigned kBalStage = 1024;   // balance values per staging sub-round (8 KB)
+__host__ __device__ inline size_t write_part_smem(int m) { return m <= 12 ? (size_t)(1u << m) * 5 : 0; }
 
 __global__ void __launch_bounds__(kWT) k_write_part(Geom g, const BlkP *__restrict__ blkp,
-                                                    const uint16_t *__restrict__ codes,
-                                                    const double *__restrict__ balv,
+                                                    const int16_t *__restrict__ rqbuf,
+                                                    const double *__restrict__ vbuf,
                                                     const double *__restrict__ anchors,
                                                     const unsigned long long *__restrict__ part_bits,
                                                     const unsigned long long *__restrict__ part_zeros,
                                                     const unsigned long long *__restrict__ rec_off,
                                                     const uint8_t *__restrict__ lens,
                                                     const unsigned *__restrict__ cw, int m, uint8_t *out,
-                                                    unsigned long long rec_base,
-                                                    const uint16_t *__restrict__ zrow, WsStatus *st) {
-  __shared__ uint8_t s_len[4096];
-  __shared__ unsigned s_cw[4096];
+                                                    unsigned long long rec_base, WsStatus *st) {
+  extern __shared__ __align__(16) unsigned char wp_dyn[];
   __shared__ unsigned sw[kPartWords];
-  __shared__ unsigned s_wsum[kWT / 32], s_zi[33];
+  __shared__ unsigned long long sbal[kBalStage + 1];
+  __shared__ unsigned s_wsum[kWT / 32][2];
+  __shared__ unsigned s_carry[2];
   count_launch(st);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t p = blockIdx.x;
@@ -443,6 +464,8 @@ __global__ void __launch_bounds__(kWT) k_write_part(Geom g, const BlkP *__restri
     return;
   }
   const bool small_tab = m <= 12;
+  unsigned *s_cw = reinterpret_cast<unsigned *>(wp_dyn);
+  uint8_t *s_len = wp_dyn + (small_tab ? (4u << m) : 0u);
   if (small_tab) {
     for (int i = tid; i < (1 << m); i += kWT) {
       s_len[i] = lens[i];
@@ -486,111 +509,125 @@ __global__ void __launch_bounds__(kWT) k_write_part(Geom g, const BlkP *__restri
   }
   uint8_t *bal = base + head + 8ull * zb;
   uint8_t *pay = base + head + 8ull * nbal + pb;
-  const int pr0 = pi * g.prow, R = min(g.prow, bb.br - pr0), C = bb.bc;
-  const uint16_t *cp = codes + (bb.r0 + pr0) * g.cols + bb.c0;
+  const int R = min(g.prow, bb.br - pi * g.prow), C = bb.bc, nch = (C + 31) >> 5;
+  const int center = 1 << (m - 1);
+  const int16_t *rp = rqbuf + tile_base(g, p, 0);
+  const double *vp = vbuf + tile_base(g, p, 0);
+  const unsigned total_bits = (unsigned)part_bits[p];
+  const unsigned nwords = (total_bits + 31) >> 5;
+  const bool staged = nwords <= kPartWords;
+  for (unsigned i = tid; i < (staged ? nwords : 0u); i += kWT) sw[i] = 0;
+  if (tid < 2) s_carry[tid] = 0;
+  __syncthreads();  // tables, sw, carry
 
-  // ---- balance list: row-compacted by the compress kernel (zrow = counts) ----
-  if (warp == 0) {
-    const unsigned zc = lane < R ? zrow[p * 32 + lane] : 0u;
-    unsigned zi = zc;
-    for (int d = 1; d < 32; d <<= 1) {
-      const unsigned t = __shfl_up_sync(0xffffffffu, zi, d);
-      if (lane >= d) zi += t;
-    }
-    s_zi[lane] = zi - zc;
-    if (lane == 31) s_zi[32] = zi;
-  }
-  __syncthreads();  // also publishes s_len / s_cw
-  {
-    const double *bp = balv + (bb.r0 + pr0) * g.cols + bb.c0;
-    const unsigned T = s_zi[32];
-    for (unsigned i = tid; i < T; i += kWT) {
-      int r = 0;
-#pragma unroll
-      for (int d = 16; d >= 1; d >>= 1)
-        if (r + d < R && s_zi[r + d] <= i) r += d;
-      put8_unaligned(bal + 8ull * i, __double_as_longlong(__ldg(&bp[(int64_t)r * g.cols + (i - s_zi[r])])));
-    }
-  }
-
-  // ---- Huffman substream ----
   auto len_of = [&](unsigned c) -> unsigned { return small_tab ? s_len[c] : __ldg(&lens[c]); };
   auto cw_of = [&](unsigned c) -> unsigned { return small_tab ? s_cw[c] : __ldg(&cw[c]); };
-  const unsigned ne = (unsigned)(R * C);
-  const unsigned RUN = (ne + kWT - 1) / kWT;
-  const unsigned e0 = min(ne, tid * RUN), e1 = min(ne, e0 + RUN);
-  // element e -> (e / C, e % C): walk the run with a (row, col) cursor
-  const int r0 = (int)(e0 / (unsigned)C), c0 = (int)(e0 - (unsigned)r0 * C);
-  unsigned bits = 0;
-  {
-    int r = r0, c = c0;
-#pragma unroll 8
-    for (unsigned e = e0; e < e1; e++) {
-      if (e) bits += len_of(__ldg(&cp[(int64_t)r * g.cols + c]));
-      if (++c == C) { c = 0; r++; }
-    }
-  }
-  // CTA exclusive scan of the runs' bit counts
-  unsigned ib = bits;
-  for (int d = 1; d < 32; d <<= 1) {
-    const unsigned t = __shfl_up_sync(0xffffffffu, ib, d);
-    if (lane >= d) ib += t;
-  }
-  if (lane == 31) s_wsum[warp] = ib;
-  __syncthreads();
-  unsigned wofs = 0, total_bits = 0;
+  const int nrun = R * nch;
+  for (int q0 = 0; q0 < nrun; q0 += kWT) {
+    const int q = q0 + tid;
+    const bool valid = q < nrun;
+    const int r = valid ? q / nch : 0, kc = valid ? q - r * nch : 0;
+    const int ncol = valid ? min(32, C - 32 * kc) : 0;
+    // the run's 32 residuals (16-byte aligned tile row)
+    unsigned w[16];
+    if (valid) {
+      const uint4 *src = reinterpret_cast<const uint4 *>(rp + (int64_t)kc * kTile + r * 32);
 #pragma unroll
-  for (int w = 0; w < kWT / 32; w++) {
-    const unsigned v = s_wsum[w];
-    if (w < warp) wofs += v;
-    total_bits += v;
-  }
-  const unsigned B = wofs + ib - bits;
-  const unsigned nwords = (total_bits + 31) >> 5;
-  if (nwords <= kPartWords) {
-    for (unsigned i = tid; i < nwords; i += kWT) sw[i] = 0;
+      for (int u = 0; u < 4; u++) {
+        const uint4 x4 = __ldg(src + u);
+        w[4 * u] = x4.x; w[4 * u + 1] = x4.y; w[4 * u + 2] = x4.z; w[4 * u + 3] = x4.w;
+      }
+    }
+    auto code_at = [&](int i) -> unsigned {
+      return (unsigned)code_of_rq((int)(int16_t)(w[i >> 1] >> (16 * (i & 1))), center);
+    };
+    const int i0 = (r == 0 && kc == 0) ? 1 : 0;  // the anchor
+    unsigned bits = 0, zmask = 0;
+#pragma unroll
+    for (int i = 0; i < 32; i++) {
+      if (i >= i0 && i < ncol) {
+        const unsigned cd = code_at(i);
+        bits += len_of(cd);
+        zmask |= (cd == 0 ? 1u : 0u) << i;
+      }
+    }
+    const unsigned nz = __popc(zmask);
+    // CTA scan of (bits, nz) over this round's runs, plus the carry
+    unsigned ib = bits, iz = nz;
+    for (int d = 1; d < 32; d <<= 1) {
+      const unsigned t = __shfl_up_sync(0xffffffffu, ib, d), u = __shfl_up_sync(0xffffffffu, iz, d);
+      if (lane >= d) { ib += t; iz += u; }
+    }
+    if (lane == 31) { s_wsum[warp][0] = ib; s_wsum[warp][1] = iz; }
     __syncthreads();
-    const unsigned fw = B >> 5, lw = bits ? (B + bits - 1) >> 5 : fw;
-    unsigned long long acc = 0;
-    int nacc = (int)(B & 31);
-    unsigned ow = fw;
-    int r = r0, c = c0;
-#pragma unroll 4
-    for (unsigned e = e0; e < e1; e++) {
-      if (e) {
-        const unsigned cd = __ldg(&cp[(int64_t)r * g.cols + c]);
-        const int l = (int)len_of(cd);
-        acc = (acc << l) | cw_of(cd);
-        nacc += l;
-        if (nacc >= 32) {
-          const unsigned w = (unsigned)(acc >> (nacc - 32));
-          if (ow == fw || ow == lw) atomicOr(&sw[ow], w);
-          else sw[ow] = w;
-          ow++;
-          nacc -= 32;
+    unsigned wofs = s_carry[0], zofs = s_carry[1], rb = 0, rz = 0;
+#pragma unroll
+    for (int w2 = 0; w2 < kWT / 32; w2++) {
+      const unsigned a = s_wsum[w2][0], z = s_wsum[w2][1];
+      if (w2 < warp) { wofs += a; zofs += z; }
+      rb += a;
+      rz += z;
+    }
+    const unsigned B = wofs + ib - bits, Z = zofs + iz - nz;
+    const unsigned zr0 = s_carry[1];  // first balance index of the round
+    __syncthreads();
+    if (tid == 0) { s_carry[0] += rb; s_carry[1] += rz; }
+
+    // ---- balance values: staged sub-rounds of kBalStage values ----
+    for (unsigned s0 = zr0; s0 < zr0 + rz; s0 += kBalStage) {
+      const unsigned s1 = min(zr0 + rz, s0 + kBalStage);
+      if (nz && Z < s1 && Z + nz > s0) {
+        unsigned zm = zmask, k = Z;
+        const double *vrow = vp + (int64_t)kc * kTile + r * 32;
+        while (zm) {
+          const int i = __ffs(zm) - 1;
+          zm &= zm - 1;
+          if (k >= s0 && k < s1) sbal[k - s0] = __double_as_longlong(__ldg(vrow + i));
+          k++;
         }
       }
-      if (++c == C) { c = 0; r++; }
+      __syncthreads();
+      copy_s2g_bytes(bal + 8ull * s0, reinterpret_cast<const unsigned *>(sbal), 8 * (s1 - s0), tid, kWT);
+      __syncthreads();
     }
-    if (nacc > 0) atomicOr(&sw[ow], (unsigned)(acc << (32 - nacc)));
-    __syncthreads();
-    const unsigned nbytes = (total_bits + 7) >> 3;
-    for (unsigned i = tid; i < nbytes; i += kWT) pay[i] = (uint8_t)(sw[i >> 2] >> (24 - 8 * (i & 3)));
-  } else {
-    // oversized substream: bytes straight to global, boundary bytes OR-ed
-    const unsigned fbyte = B >> 3, lbyte = bits ? (B + bits - 1) >> 3 : fbyte;
-    if (bits) {
-      pay[fbyte] = 0;
-      pay[lbyte] = 0;
-    }
-    __syncthreads();
-    unsigned long long acc = 0;
-    int nacc = (int)(B & 7);
-    unsigned outb = fbyte;
-    int r = r0, c = c0;
-    for (unsigned e = e0; e < e1; e++) {
-      if (e) {
-        const unsigned cd = __ldg(&cp[(int64_t)r * g.cols + c]);
+
+    // ---- codewords of the run ----
+    if (staged) {
+      const unsigned fw = B >> 5, lw = bits ? (B + bits - 1) >> 5 : fw;
+      unsigned long long acc = 0;
+      int nacc = (int)(B & 31);
+      unsigned ow = fw;
+#pragma unroll
+      for (int i = 0; i < 32; i++) {
+        if (i >= i0 && i < ncol) {
+          const unsigned cd = code_at(i);
+          const int l = (int)len_of(cd);
+          acc = (acc << l) | cw_of(cd);
+          nacc += l;
+          if (nacc >= 32) {
+            const unsigned wv = (unsigned)(acc >> (nacc - 32));
+            if (ow == fw || ow == lw) atomicOr(&sw[ow], wv);
+            else sw[ow] = wv;
+            ow++;
+            nacc -= 32;
+          }
+        }
+      }
+      if (nacc > 0) atomicOr(&sw[ow], (unsigned)(acc << (32 - nacc)));
+    } else {
+      // oversized substream: bytes straight to global, boundary bytes OR-ed
+      const unsigned fbyte = B >> 3, lbyte = bits ? (B + bits - 1) >> 3 : fbyte;
+      if (bits) {
+        // a round's first run may share its first byte with the previous round
+        if ((B & 7) == 0 || q != q0) pay[fbyte] = 0;
+        pay[lbyte] = 0;
+      }
+      __syncthreads();
+      unsigned long long acc = 0;
+      int nacc = (int)(B & 7);
+      unsigned outb = fbyte;
+      for (int i = i0; i < ncol; i++) {
+        const unsigned cd = code_at(i);
         const int l = (int)len_of(cd);
         acc = (acc << l) | cw_of(cd);
         nacc += l;
@@ -602,9 +639,14 @@ __global__ void __launch_bounds__(kWT) k_write_part(Geom g, const BlkP *__restri
           nacc -= 8;
         }
       }
-      if (++c == C) { c = 0; r++; }
+      if (nacc > 0) or_byte(pay + outb, (unsigned)(acc << (8 - nacc)) & 0xffu);
+      __syncthreads();
     }
-    if (nacc > 0) or_byte(pay + outb, (unsigned)(acc << (8 - nacc)) & 0xffu);
+  }
+  if (staged) {
+    __syncthreads();
+    const unsigned nbytes = (total_bits + 7) >> 3;
+    for (unsigned i = tid; i < nbytes; i += kWT) pay[i] = (uint8_t)(sw[i >> 2] >> (24 - 8 * (i & 3)));
   }
 }
 

@@ -9,6 +9,7 @@
 // blocks falls out of the same pass: m_required(err) = max(4, bitlen|rq| + 1),
 // 17 for kRqOut.
 //
+// Outputs go to the partition-tiled layout (common.cuh: tile_base).
 // One CTA per 32-row partition, swept in 256-column strips: 8 warps forward-map
 // a strip (lane = column, 8 interleaved log2 chains per lane) into shared
 // memory, then compute the residuals from the shared tile (W / N / NW inside
@@ -80,9 +81,9 @@ __global__ void __launch_bounds__(kFqW * 32, 2) k_fwdq(const float *__restrict__
           if (xz > 0.0f) v = __dadd_rn(lg[q], P.lg_pos);
           else if (xz < 0.0f) v = __dadd_rn(lg[q], P.lg_neg);
           sv[rb + q][j] = v;
-          const int64_t e = (int64_t)(rb + q) * g.cols + col;
-          vbuf[off + e] = v;
-          clsbuf[off + e] = xclass(xz);
+          const int64_t e = tile_elem(g, p, rb + q, col);
+          vbuf[e] = v;
+          clsbuf[e] = xclass(xz);
         }
       }
     }
@@ -107,7 +108,7 @@ __global__ void __launch_bounds__(kFqW * 32, 2) k_fwdq(const float *__restrict__
         for (int q = 0; q < 4; q++) {
           const int r = rb + q;
           if (r < R) {
-            rqbuf[off + (int64_t)r * g.cols + col] = (int16_t)rq[q];
+            rqbuf[tile_elem(g, p, r, col)] = (int16_t)rq[q];
             if (val && !(r == 0 && col == 0)) {  // anchors excluded (D17)
               const int mm = m_of_rq(rq[q]);
               const unsigned grp = __match_any_sync(__activemask(), mm);

@@ -1,19 +1,19 @@
-// wsc.cuh -- warp-specialized compress_block + verify_and_repair
-// (SPEC.md:443-451, 461-469).
+// wsc.cuh -- compress_block's sequential half: verify_and_repair
+// as one streaming pass per 32-row partition.
 //
-// Each 32-row partition is owned by a warp PAIR:
-//   producer warp (lane = column): for each 32-column chunk, loads the float
-//     tile, forward-maps it (transform.py:170-185), classifies the sign/range
-//     of every element and quantizes the TRUE-surface residuals
-//      into slot k%3 of a 3-deep shared-memory ring; later it
-//     flushes the chunk's final codes and balance values to global memory.
-//     This is all independent, FP64-throughput work.
-//   consumer warp (lane = row): the decoder simulation of verify_and_repair,
-//     an anti-diagonal recurrence over the ring: predict from RECONSTRUCTED
-//     neighbours (shuffles), dequantize, bound check in the log domain,
-//     repair on violation.  Only this chain is sequential.
-// Producer and consumer hand slots over with named barriers
-// (full[s] / empty[s], 64 threads each), CUTLASS-style.
+// k_fwdq already produced, per element and in the partition-tiled layout, the
+// TRUE value v, its sign/range class and the m-independent quantized residual
+// rq (code = center + rq when |rq| < center, else 0).  What remains is the
+// decoder simulation, an anti-diagonal recurrence (lane = row): predict from
+// RECONSTRUCTED W / N / NW (N, NW by shuffle from lane - 1), dequantize, bound
+// check in the log domain, repair (rq := kRqOut, i.e. code 0 / balance point)
+// on violation.  Each partition is owned by a warp PAIR:
+//   producer warp: one elected lane streams the chunk tiles (v, rq, cls) into
+//     a 3-deep shared-memory ring with cp.async.bulk on an mbarrier, and
+//     bulk-stores each finished rq tile back in place (final codes);
+//   consumer warp: the recurrence; it releases a slot with a named barrier.
+// Steady-state steps (all 32 lanes inside the partition) run a guard-free
+// variant of the step.
 #pragma once
 #include "common.cuh"
 #include "compress.cuh"
@@ -25,16 +25,67 @@ constexpr int kPPC = 2;      // partitions (warp pairs) per CTA
 constexpr int kSlots = 3;    // ring depth
 constexpr uint16_t kAnc = 0xFFFF;
 
-struct PRing {
-  double v[kSlots][32][32];       // forward-mapped TRUE values
-  uint16_t code[kSlots][32][32];  // codes; the consumer zeroes repaired ones
-  uint8_t cls[kSlots][32][32];    // 0: x == 0, 1: x > 0, 2: x < 0 (normal range), 3: exact path only
+struct alignas(128) PRing {
+  double v[kSlots][kTile];         // TRUE values
+  int16_t rq[kSlots][kTile];       // quantized residuals; repaired -> kRqOut
+  uint8_t cls[kSlots][kTile];      // 0: x == 0, 1: x > 0, 2: x < 0 (normal range), 3: exact path only
+  unsigned long long full[kSlots]; // mbarriers: tile bytes landed
 };
 constexpr size_t kWscSmem = sizeof(PRing) * kPPC;
+constexpr unsigned kTileBytes = kTile * (8 + 2 + 1);
+#ifndef PMZ_WS_UNROLL
+#define PMZ_WS_UNROLL 2
+#endif
+constexpr int kWsUnroll = PMZ_WS_UNROLL;
 
 __device__ __forceinline__ void bar_sync_n(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void bar_arrive_n(int id, int n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// ---- mbarrier / bulk-copy helpers (sm_90+ PTX) ----
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long *b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_init_fence() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long *b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *b, unsigned parity) {
+  unsigned ok;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, unsigned long long *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void *dst, const void *src, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// Keep a loop-invariant value in a register (no rematerialisation from the
+// constant bank inside hot loops).
+__device__ __forceinline__ double pin(double x) {
+  asm volatile("" : "+d"(x));
+  return x;
+}
+__device__ __forceinline__ int pin(int x) {
+  asm volatile("" : "+r"(x));
+  return x;
 }
 
 __device__ __forceinline__ uint8_t xclass(float xz) {
@@ -44,44 +95,45 @@ __device__ __forceinline__ uint8_t xclass(float xz) {
   return 3;
 }
 
-// D8 bound check with the sign/range class precomputed by the producer.
-__device__ __forceinline__ int check_cls(double vhat, double v, int cls, const BlkP &P, const KParams &k) {
-  if (cls == 1 || cls == 2) {
-    const bool side_ok = cls == 1 ? (vhat <= P.boundary) : (vhat > P.boundary);
-    // wrong sign or snapped to zero: relative error >= 1 > t (when t < 1)
-    if ((!side_ok || vhat <= P.zero_threshold) && k.repair_t < 1.0) return 1;
-    if (side_ok && vhat > P.zero_threshold) {
-      const double d = __dsub_rn(vhat, v);
-      const double mu = 0x1p-20;
-      if (d < __dsub_rn(k.dpos, mu) && d > __dadd_rn(k.dneg, mu)) return 0;
-      if (d > __dadd_rn(k.dpos, mu) || d < __dsub_rn(k.dneg, mu)) return 1;
+// Prediction for a lane with all of W / N / NW inside the partition except
+// that lane 0 has no N / NW (they read 0): predict_chain semantics.
+template <int PK>
+__device__ __forceinline__ double predict_steady(const KParams &k, double w, double n, double nw, bool lane0) {
+  if (PK == 3) {
+    double h = __dsub_rn(__dadd_rn(w, n), nw);
+    h = lane0 ? w : h;  // (w + 0) - 0 up to the sign of a zero (see predict_chain)
+    const double a = h < 0.0 ? __dmul_rn(k.slope, h) : h;
+    if (__builtin_expect(fabs(a) < 0x1p-1020, 0)) {
+      const double a2 = __dmul_rn(a, 0.5);
+      return __dadd_rn(a2, a2);
     }
-  } else if (cls == 0 && vhat <= P.zero_threshold) {
-    return 0;
+    return a;
   }
-  return -1;  // undecided: exact path
+  if (PK == 1) return predict_chain<1>(k, w, 0.0, 0.0);
+  return predict(k, w, lane0 ? 0.0 : n, lane0 ? 0.0 : nw);
 }
 
 #ifdef PMZ_CMP_PROFILE
-__device__ long long g_cmp_prof[65536][2][4];  // [partition][role][start, end, wait cycles, phase cycles]
-__device__ long long g_cmp_ph[65536][4];
+__device__ long long g_cmp_prof[65536][2][4];  // [partition][role][start, end, wait, steady]
 #endif
 
 template <int PK>
 __global__ void __launch_bounds__(kPPC * 64) k_compress_ws(const float *__restrict__ x, Geom g, KParams k,
                                                            const BlkP *__restrict__ blkp, WsStatus *st,
-                                                           uint16_t *__restrict__ codes, double *__restrict__ balv,
+                                                           const double *__restrict__ vbuf, int16_t *rqbuf,
+                                                           const uint8_t *__restrict__ clsbuf,
                                                            double *__restrict__ anchors,
-                                                           unsigned long long *__restrict__ part_zeros,
-                                                           uint16_t *__restrict__ zrow,
-                                                           const double *__restrict__ vbuf,
-                                                           const int16_t *__restrict__ rqbuf,
-                                                           const uint8_t *__restrict__ clsbuf) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+                                                           unsigned long long *__restrict__ part_zeros) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   count_launch(st);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int pair = warp >> 1, role = warp & 1;  // role 0: producer, 1: consumer
   PRing &W = reinterpret_cast<PRing *>(smem_raw)[pair];
+  if (role == 0 && lane == 0) {
+    for (int s = 0; s < kSlots; s++) mbar_init(&W.full[s], 1);
+    mbar_init_fence();
+  }
+  __syncthreads();
   const int64_t p = (int64_t)blockIdx.x * kPPC + pair;
   if (p >= g.nparts) return;
   int64_t b;
@@ -97,168 +149,203 @@ __global__ void __launch_bounds__(kPPC * 64) k_compress_ws(const float *__restri
   const int R = min(g.prow, bb.br - pr0);
   const int C = bb.bc;
   const int nch = (C + 31) >> 5;
-  const int m = st->m;
-  const int center = 1 << (m - 1);
-  const int bar0 = 1 + pair * 2 * kSlots;  // full[s] = bar0 + s, empty[s] = bar0 + kSlots + s
-  const float *xp = x + (bb.r0 + pr0) * g.cols + bb.c0;
-  const double *vp = vbuf + (bb.r0 + pr0) * g.cols + bb.c0;
-  const int16_t *rqp = rqbuf + (bb.r0 + pr0) * g.cols + bb.c0;
-  const uint8_t *clp = clsbuf + (bb.r0 + pr0) * g.cols + bb.c0;
-  unsigned *amb = &st->unresolved;
-
+  const int bar0 = 1 + pair * kSlots;  // empty[s] = bar0 + s (named barriers, 64 threads)
+  const int64_t tb = tile_base(g, p, 0);
 #ifdef PMZ_CMP_PROFILE
-  long long t_start = clock64(), t_wait = 0, t_fwd = 0, t_code = 0, t_flush = 0, t_mark;
-#define TIMED_SYNC(id) { long long t0_ = clock64(); bar_sync_n(id, 64); t_wait += clock64() - t0_; }
-#else
-#define TIMED_SYNC(id) bar_sync_n(id, 64);
+  const long long t_start = clock64();
 #endif
+
   if (role == 0) {
     // ------------------------------ producer ------------------------------
-    uint16_t *cpart = codes + (bb.r0 + pr0) * g.cols + bb.c0;
-    double *bpart = balv + (bb.r0 + pr0) * g.cols + bb.c0;
-    // balance values are appended per row (row-compacted: row r's list starts
-    // at column 0 of its block-row segment), counts per row in zrow
-    unsigned rowcnt = 0;  // lane r's count for row r (lane = row here)
-    auto flush = [&](int chunk) {
-      const int s = chunk % kSlots, col = chunk * 32 + lane;
-      for (int r = 0; r < R; r++) {
-        const uint16_t cd = col < C ? W.code[s][r][lane] : (uint16_t)1;
-        if (col < C) cpart[r * g.cols + col] = cd;
-        const unsigned zm = __ballot_sync(0xffffffffu, cd == 0);
-        const unsigned base = __shfl_sync(0xffffffffu, rowcnt, r);
-        if (cd == 0) bpart[r * g.cols + base + __popc(zm & ((1u << lane) - 1))] = W.v[s][r][lane];
-        if (lane == r) rowcnt += __popc(zm);
+    auto store_rq = [&](int kc) {  // final rq tile of chunk kc back in place
+      if (lane == 0) {
+        bulk_s2g(rqbuf + tb + (int64_t)kc * kTile, W.rq[kc % kSlots], kTile * 2);
+        bulk_commit();
       }
     };
     for (int kc = 0; kc < nch; kc++) {
       const int s = kc % kSlots;
       if (kc >= kSlots) {
-        TIMED_SYNC(bar0 + kSlots + s)  // consumer done with chunk kc-3
-#ifdef PMZ_CMP_PROFILE
-        t_mark = clock64();
-#endif
-        flush(kc - kSlots);
-        __syncwarp();
-#ifdef PMZ_CMP_PROFILE
-        t_flush += clock64() - t_mark;
-#endif
+        bar_sync_n(bar0 + s, 64);  // consumer done with chunk kc - 3
+        store_rq(kc - kSlots);
+        if (lane == 0) bulk_wait_read0();  // the store has read the slot
       }
-#ifdef PMZ_CMP_PROFILE
-      t_mark = clock64();
-#endif
-      const int col = kc * 32 + lane;
-      const bool inb = col < C;
-#if defined(PMZ_CMP_ISOLATE) && PMZ_CMP_ISOLATE == 2
-      if (kc >= 0) { __syncwarp(); bar_arrive_n(bar0 + s, 64); continue; }
-#endif
-      // ring fill from the k_fwdq results (L2-resident): TRUE value, class,
-      // and the code for this m
-      for (int rb = 0; rb < R; rb += 8) {
-        double vv[8];
-        int rq[8];
-        uint8_t cl[8];
-#pragma unroll
-        for (int q = 0; q < 8; q++) {
-          const bool ok = inb && rb + q < R;
-          const int64_t e = (int64_t)(rb + q) * g.cols + col;
-          vv[q] = ok ? __ldg(vp + e) : 0.0;
-          rq[q] = ok ? __ldg(rqp + e) : 0;
-          cl[q] = ok ? __ldg(clp + e) : (uint8_t)0;
-        }
-#pragma unroll
-        for (int q = 0; q < 8; q++) {
-          if (rb + q < R) {
-            W.v[s][rb + q][lane] = vv[q];
-            W.cls[s][rb + q][lane] = cl[q];
-            W.code[s][rb + q][lane] = (uint16_t)code_of_rq(rq[q], center);
-          }
-        }
-      }
-      if (kc == 0 && lane == 0) {
-        W.code[s][0][0] = kAnc;
-        anchors[p] = W.v[s][0][0];  // forced anchor, D1
+      if (lane == 0) {
+        const int64_t o = tb + (int64_t)kc * kTile;
+        mbar_expect_tx(&W.full[s], kTileBytes);
+        bulk_g2s(W.v[s], vbuf + o, kTile * 8, &W.full[s]);
+        bulk_g2s(W.rq[s], rqbuf + o, kTile * 2, &W.full[s]);
+        bulk_g2s(W.cls[s], clsbuf + o, kTile, &W.full[s]);
       }
       __syncwarp();
-#ifdef PMZ_CMP_PROFILE
-      t_code += clock64() - t_mark;
-#endif
-      bar_arrive_n(bar0 + s, 64);  // full[s]
     }
     for (int kc = max(0, nch - kSlots); kc < nch; kc++) {
-      TIMED_SYNC(bar0 + kSlots + kc % kSlots)
-      flush(kc);
+      bar_sync_n(bar0 + kc % kSlots, 64);
+      store_rq(kc);
     }
-    if (lane < R) zrow[p * 32 + lane] = (uint16_t)rowcnt;
+    if (lane == 0) bulk_wait0();
 #ifdef PMZ_CMP_PROFILE
-    if (lane == 0 && p < 65536) { g_cmp_prof[p][0][0] = t_start; g_cmp_prof[p][0][1] = clock64(); g_cmp_prof[p][0][2] = t_wait;
-      g_cmp_ph[p][0] = t_fwd; g_cmp_ph[p][1] = t_code; g_cmp_ph[p][2] = t_flush; }
+    if (lane == 0 && p < 65536) { g_cmp_prof[p][0][0] = t_start; g_cmp_prof[p][0][1] = clock64(); }
 #endif
   } else {
     // ------------------------------ consumer ------------------------------
+    const float *xp = x + (bb.r0 + pr0) * g.cols + bb.c0;
+    unsigned *amb = &st->unresolved;
+    const int center = 1 << (st->m - 1);
     const int nsteps = C + R - 1;
     const int ngroups = (nsteps + 31) >> 5;
+    const bool tlt1 = k.repair_t < 1.0;
+    const double two_ba = k.two_ba, zthr = P.zero_threshold, bnd = P.boundary;
+    const bool lane0 = lane == 0;
     double hl = 0.0, hp = 0.0;
     unsigned zeros = 0, repairs = 0;
-    const double mu = 0x1p-20;
-    const double dpos_m = __dsub_rn(k.dpos, mu), dneg_m = __dadd_rn(k.dneg, mu);
-    const double dpos_p = __dadd_rn(k.dpos, mu), dneg_p = __dsub_rn(k.dneg, mu);
-    const bool tlt1 = k.repair_t < 1.0;
-    for (int kg = 0; kg < ngroups; kg++) {
-      if (kg < nch) TIMED_SYNC(bar0 + kg % kSlots)  // full: chunk kg ready
-      const int t1 = min(nsteps, (kg + 1) * 32);
-#if defined(PMZ_CMP_ISOLATE) && PMZ_CMP_ISOLATE == 1
-      for (int t = t1; t < t1; t++) {
-#else
-      for (int t = kg * 32; t < t1; t++) {
-#endif
-        const double nhl = __shfl_up_sync(0xffffffffu, hl, 1), nhp = __shfl_up_sync(0xffffffffu, hp, 1);
-        const int c = t - lane;
-        if (lane < R && c >= 0 && c < C) {
-          const int s = (c >> 5) % kSlots, j = c & 31;
-          const double v = W.v[s][lane][j];
-          const int code = W.code[s][lane][j];
-          const int cls = W.cls[s][lane][j];
-          const double dq = __dmul_rn((double)(code - center), k.two_ba);  // off the chain
-          const bool hw = c > 0, hn = lane > 0;
-          const double vhat = __dadd_rn(predict_chain<PK>(k, hw ? hl : 0.0, hn ? nhl : 0.0, (hw && hn) ? nhp : 0.0), dq);
-          // check_cls, predicated (D8 log-domain filter)
-          const double d = __dsub_rn(vhat, v);
-          const bool side_ok = cls == 1 ? (vhat <= P.boundary) : (vhat > P.boundary);
-          const bool nz = vhat > P.zero_threshold;
-          const bool in12 = side_ok && nz;
-          const bool is12 = cls == 1 || cls == 2;
-          bool acc = is12 ? (in12 && d < dpos_m && d > dneg_m) : (cls == 0 && !nz);
-          bool vio = is12 && ((tlt1 && !in12) || (in12 && (d > dpos_p || d < dneg_p)));
-          const bool normal = code != 0 && code != kAnc;
-          if (__builtin_expect(normal && !acc && !vio, 0)) {
-            const float xz = zfloor(__ldg(xp + lane * g.cols + c));
-            vio = violates(inv_f32(vhat, P, amb), xz, k.repair_t);
-          }
-          const bool keep = normal && !vio;
-          if (normal && !keep) {
-            W.code[s][lane][j] = 0;
-            repairs++;
-          }
-          zeros += (code == 0 || (normal && !keep)) ? 1u : 0u;
-          hp = hl;
-          hl = keep ? vhat : v;
-        }
+
+    // Filtered bound check (check_cls, D8): class 1 lives in (zthr, bnd],
+    // class 2 in (bnd, inf).  acc: certainly within the bound, vio: certainly
+    // a violation; neither: exact path.
+    auto classify = [&](double vhat, double v, int cls, bool &acc, bool &vio) {
+      const double d = __dsub_rn(vhat, v);
+      const bool gz = vhat > zthr, gb = vhat > bnd;
+      const bool in12 = cls == 1 ? (gz && !gb) : gb;
+      const bool is12 = cls == 1 || cls == 2;
+      acc = is12 ? (in12 && d < k.dpos_m && d > k.dneg_m) : (cls == 0 && !gz);
+      vio = is12 && ((tlt1 && !in12) || (in12 && (d > k.dpos_p || d < k.dneg_p)));
+    };
+    const float *xrow = xp + (int64_t)lane * g.cols;
+    auto exact_vio = [&](double vhat, int c) -> bool {
+      const float xz = zfloor(__ldg(xrow + c));
+      return violates(inv_f32(vhat, P, amb), xz, k.repair_t);
+    };
+    // one element of the general (guarded) path; returns the reconstructed value
+    auto verify = [&](double pred, double v, int rq, int cls, int16_t *rqp, int c, bool anchor) -> double {
+      const bool normal = abs(rq) < center && !anchor;
+      const double vhat = __dadd_rn(pred, __dmul_rn((double)rq, two_ba));
+      bool acc, vio;
+      classify(vhat, v, cls, acc, vio);
+      if (normal && !acc && !vio) vio = exact_vio(vhat, c);
+      const bool keep = normal && !vio;
+      if (normal && vio) {
+        *rqp = kRqOut;
+        repairs++;
       }
+      zeros += (!keep && !anchor) ? 1u : 0u;
+      return keep ? vhat : v;
+    };
+
+#ifdef PMZ_CMP_PROFILE
+    long long t_w = 0, t_st = 0, t_m;
+#endif
+    const double c_two_ba = pin(two_ba), c_zthr = pin(zthr), c_bnd = pin(bnd), c_slope = pin(k.slope);
+    const double c_dpm = pin(k.dpos_m), c_dnm = pin(k.dneg_m), c_dpp = pin(k.dpos_p), c_dnp = pin(k.dneg_p);
+    const int c_tlt1 = pin((int)tlt1), c_center = pin(center);
+    const bool lane_in = lane < R;
+    double pn = 0.0;  // lane - 1's value one column back (the NW input)
+    for (int kg = 0; kg < ngroups; kg++) {
+#ifdef PMZ_CMP_PROFILE
+      t_m = clock64();
+#endif
+      if (kg < nch) mbar_wait(&W.full[kg % kSlots], (unsigned)(kg / kSlots) & 1u);
+#ifdef PMZ_CMP_PROFILE
+      t_w += clock64() - t_m;
+      t_m = clock64();
+#endif
+      const int t0 = kg * 32, t1 = min(nsteps, t0 + 32);
+      const int scur = kg % kSlots, sprev = (kg + kSlots - 1) % kSlots;
+      // One predicated step for every lane: a lane that has not started
+      // (c < 0) keeps hl = 0, which is exactly the W / NW = 0 boundary; a lane
+      // past its row end computes values nobody reads.  Software-pipelined:
+      // step t+1's inputs (ring loads, dq, class predicates) are prepared in
+      // step t's basic block so they fill the latency gaps of t's chain.
+      struct In {
+        double v, dq;
+        int idx;
+        bool started, active, anchor, normal, c1, c2, c0;
+      };
+      auto prep = [&](int t) -> In {
+        In q;
+        const int c = t - lane;
+        q.started = c >= 0;
+        q.active = lane_in & q.started & (c < C);
+        const int cc = min(max(c, 0), C - 1);
+        q.idx = ((cc >> 5) == kg ? scur : sprev) * kTile + lane * 32 + (cc & 31);
+        q.v = W.v[0][q.idx];
+        const int rq = W.rq[0][q.idx];
+        const int cls = W.cls[0][q.idx];
+        q.anchor = lane0 & (c == 0);
+        q.normal = (abs(rq) < c_center) & !q.anchor;
+        q.dq = __dmul_rn((double)rq, c_two_ba);
+        q.c1 = cls == 1;
+        q.c2 = cls == 2;
+        q.c0 = cls == 0;
+        return q;
+      };
+      In cur = prep(t0);
+#pragma unroll kWsUnroll
+      for (int t = t0; t < t1; t++) {
+        const double nhl = __shfl_up_sync(0xffffffffu, hl, 1);
+        const In nxt = prep(min(t + 1, t1 - 1));  // the last step re-reads its own inputs
+        double a;
+        if (PK == 3) {
+          double h = __dsub_rn(__dadd_rn(hl, nhl), pn);
+          h = lane0 ? hl : h;  // no N / NW in row 0 (sign of a zero only, see predict_chain)
+          a = h < 0.0 ? __dmul_rn(c_slope, h) : h;
+        } else {
+          a = predict_steady<PK>(k, hl, nhl, pn, lane0);
+        }
+        double vhat = __dadd_rn(a, cur.dq);
+        // classify (check_cls, D8), branch-free
+        const double d = __dsub_rn(vhat, cur.v);
+        const bool gz = vhat > c_zthr, gb = vhat > c_bnd;
+        const bool in12 = (cur.c1 & gz & !gb) | (cur.c2 & gb);
+        const bool inner = (d < c_dpm) & (d > c_dnm);
+        const bool outer = (d > c_dpp) | (d < c_dnp);
+        bool acc = (in12 & inner) | (cur.c0 & !gz);
+        bool vio = (cur.c1 | cur.c2) & (((c_tlt1 != 0) & !in12) | (in12 & outer));
+        const bool rare = cur.active & ((PK == 3 & (fabs(a) < 0x1p-1020)) | (cur.normal & !acc & !vio));
+        if (__any_sync(0xffffffffu, rare)) {
+          if (rare) {
+            vhat = __dadd_rn(predict_steady<PK>(k, hl, nhl, pn, lane0), cur.dq);
+            const int cls = W.cls[0][cur.idx];
+            classify(vhat, cur.v, cls, acc, vio);
+            if (cur.normal && !acc && !vio) vio = exact_vio(vhat, t - lane);
+          }
+        }
+        const bool keep = cur.normal & !vio;
+        if (cur.active & cur.normal & vio) {
+          W.rq[0][cur.idx] = kRqOut;
+          repairs++;
+        }
+        zeros += (cur.active & !keep & !cur.anchor) ? 1u : 0u;
+        if (cur.active & cur.anchor) anchors[p] = cur.v;  // forced anchor, D1
+        pn = nhl;
+        if (cur.started) {
+          hp = hl;
+          hl = keep ? vhat : cur.v;
+        }
+        cur = nxt;
+      }
+#ifdef PMZ_CMP_PROFILE
+      __syncwarp();
+      t_st += clock64() - t_m;
+#endif
       if (kg >= 1 && kg - 1 < nch) {
+        fence_proxy_async();  // repairs (generic writes) before the async-proxy store
         __syncwarp();
-        bar_arrive_n(bar0 + kSlots + (kg - 1) % kSlots, 64);  // empty: chunk kg-1 final
+        bar_arrive_n(bar0 + (kg - 1) % kSlots, 64);  // empty: chunk kg - 1 final
       }
     }
     if (ngroups == nch) {
+      fence_proxy_async();
       __syncwarp();
-      bar_arrive_n(bar0 + kSlots + (nch - 1) % kSlots, 64);
+      bar_arrive_n(bar0 + (nch - 1) % kSlots, 64);
     }
     for (int o = 16; o > 0; o >>= 1) {
       zeros += __shfl_xor_sync(0xffffffffu, zeros, o);
       repairs += __shfl_xor_sync(0xffffffffu, repairs, o);
     }
 #ifdef PMZ_CMP_PROFILE
-    if (lane == 0 && p < 65536) { g_cmp_prof[p][1][0] = t_start; g_cmp_prof[p][1][1] = clock64(); g_cmp_prof[p][1][2] = t_wait; }
+    if (lane == 0 && p < 65536) { g_cmp_prof[p][1][0] = t_start; g_cmp_prof[p][1][1] = clock64();
+      g_cmp_prof[p][1][2] = t_w; g_cmp_prof[p][1][3] = t_st; }
 #endif
     if (lane == 0) {
       part_zeros[p] = zeros;

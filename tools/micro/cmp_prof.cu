@@ -21,31 +21,19 @@ int main(int argc, char **argv) {
   Geom G = geom_of(&p, &g);
   std::vector<long long> pr(65536 * 8);
   cudaMemcpyFromSymbol(pr.data(), g_cmp_prof, 8 * 65536 * 8);
-  long long tmin = 1LL << 62, tmax = 0; double pw = 0, cw = 0, pd = 0, cd = 0;
+  long long tmin = 1LL << 62, tmax = 0; double pw = 0, cw = 0, pd = 0, cd = 0, cst = 0;
   for (int i = 0; i < G.nparts; i++) {
     long long *q = &pr[i * 8];
     tmin = std::min(tmin, std::min(q[0], q[4])); tmax = std::max(tmax, std::max(q[1], q[5]));
-    pd += q[1] - q[0]; pw += q[2]; cd += q[5] - q[4]; cw += q[6];
+    pd += q[1] - q[0]; pw += q[2]; cd += q[5] - q[4]; cw += q[6]; cst += q[7];
   }
   int n = (int)G.nparts;
   printf("partitions %d  kernel span %lld cycles\n", n, tmax - tmin);
-  std::vector<long long> ph(65536 * 4);
-  cudaMemcpyFromSymbol(ph.data(), g_cmp_ph, 8 * 65536 * 4);
-  double a = 0, b2 = 0, c2 = 0;
-  for (int i = 0; i < G.nparts; i++) { a += ph[i * 4]; b2 += ph[i * 4 + 1]; c2 += ph[i * 4 + 2]; }
-  printf("producer phases: loads+fwd %.0f  codes %.0f  flush %.0f\n", a / G.nparts, b2 / G.nparts, c2 / G.nparts);
-  {
-    std::vector<long long> w(65536 * 6);
-    cudaMemcpyFromSymbol(w.data(), g_wr_prof, 8 * 65536 * 6);
-    double ph[4] = {0};
-    for (int i = 0; i < G.nparts; i++) for (int j = 0; j < 4; j++) ph[j] += (double)(w[i * 6 + j + 1] - w[i * 6 + j]);
-    printf("write_records: stage %.0f  balance %.0f  pass1 %.0f  pack %.0f\n", ph[0] / G.nparts, ph[1] / G.nparts, ph[2] / G.nparts, ph[3] / G.nparts);
-  }
   {
     long long cb[8];
     cudaMemcpyFromSymbol(cb, g_cb_prof, 64);
     printf("codebook: init %lld sort %lld mk %lld lens+cnt %lld canon %lld\n", cb[1] - cb[0], cb[2] - cb[1], cb[3] - cb[2], cb[4] - cb[3], cb[5] - cb[4]);
   }
-  printf("producer: avg %.0f cycles, waiting %.0f\nconsumer: avg %.0f cycles, waiting %.0f\n", pd / n, pw / n, cd / n, cw / n);
+  printf("producer: avg %.0f cycles, waiting %.0f\nconsumer: avg %.0f cycles, mbar wait %.0f, steady groups %.0f\n", pd / n, pw / n, cd / n, cw / n, cst / n);
   return 0;
 }
