@@ -366,6 +366,7 @@ int pmz_compress_finish(const pmz_geom *g, const pmz_params *p, int write_header
   if (write_header)
     k_write_header<<<1, 256, 0, st>>>(d_out, G, k, g->global_rows, at<uint8_t>(d_ws, L.lens), S);
   if (G.nparts > 0) {
+    CK(cudaFuncSetAttribute(k_write_part, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)write_part_smem(12)));
     k_write_part<<<(unsigned)G.nparts, kWT, write_part_smem(hs.m), st>>>(
         G, at<BlkP>(d_ws, L.blkp), at<int16_t>(d_ws, L.rqbuf), at<double>(d_ws, L.vbuf),
         at<double>(d_ws, L.anchors), at<unsigned long long>(d_ws, L.part_bits),

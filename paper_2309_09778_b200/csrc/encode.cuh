@@ -449,6 +449,7 @@ __global__ void __launch_bounds__(kWT) k_write_part(Geom g, const BlkP *__restri
   extern __shared__ __align__(16) unsigned char wp_dyn[];
   __shared__ unsigned sw[kPartWords];
   __shared__ unsigned long long sbal[kBalStage + 1];
+  __shared__ unsigned s_bidx[kBalStage];
   __shared__ unsigned s_wsum[kWT / 32][2];
   __shared__ unsigned s_carry[2];
   count_launch(st);
@@ -573,21 +574,38 @@ __global__ void __launch_bounds__(kWT) k_write_part(Geom g, const BlkP *__restri
     __syncthreads();
     if (tid == 0) { s_carry[0] += rb; s_carry[1] += rz; }
 
-    // ---- balance values: staged sub-rounds of kBalStage values ----
+    // ---- balance values: staged sub-rounds of kBalStage values.  Runs list
+    // their balance points' tile offsets, then the whole CTA gathers the
+    // values (4 loads in flight per thread) and copies them out. ----
     for (unsigned s0 = zr0; s0 < zr0 + rz; s0 += kBalStage) {
       const unsigned s1 = min(zr0 + rz, s0 + kBalStage);
       if (nz && Z < s1 && Z + nz > s0) {
         unsigned zm = zmask, k = Z;
-        const double *vrow = vp + (int64_t)kc * kTile + r * 32;
+        const int tofs = kc * kTile + r * 32;
         while (zm) {
           const int i = __ffs(zm) - 1;
           zm &= zm - 1;
-          if (k >= s0 && k < s1) sbal[k - s0] = __double_as_longlong(__ldg(vrow + i));
+          if (k >= s0 && k < s1) s_bidx[k - s0] = tofs + i;
           k++;
         }
       }
       __syncthreads();
-      copy_s2g_bytes(bal + 8ull * s0, reinterpret_cast<const unsigned *>(sbal), 8 * (s1 - s0), tid, kWT);
+      const unsigned nv = s1 - s0;
+      for (unsigned j0 = 0; j0 < nv; j0 += 4 * kWT) {
+        unsigned long long vv[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          const unsigned j = j0 + u * kWT + tid;
+          vv[u] = j < nv ? __double_as_longlong(__ldg(vp + s_bidx[j])) : 0ull;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          const unsigned j = j0 + u * kWT + tid;
+          if (j < nv) sbal[j] = vv[u];
+        }
+      }
+      __syncthreads();
+      copy_s2g_bytes(bal + 8ull * s0, reinterpret_cast<const unsigned *>(sbal), 8 * nv, tid, kWT);
       __syncthreads();
     }
 
@@ -626,7 +644,9 @@ __global__ void __launch_bounds__(kWT) k_write_part(Geom g, const BlkP *__restri
       unsigned long long acc = 0;
       int nacc = (int)(B & 7);
       unsigned outb = fbyte;
-      for (int i = i0; i < ncol; i++) {
+#pragma unroll
+      for (int i = 0; i < 32; i++) {
+        if (i < i0 || i >= ncol) continue;
         const unsigned cd = code_at(i);
         const int l = (int)len_of(cd);
         acc = (acc << l) | cw_of(cd);
