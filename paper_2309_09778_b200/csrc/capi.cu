@@ -121,6 +121,7 @@ WsLayout compress_layout(const Geom &g) {
   L.cov = take(18 * 8);
   L.hist = take((kMaxAlpha + 1) * 8);
   L.vflag = take((size_t)g.nblocks + 1);  // zeroed with status / cov / hist
+  L.bstat = take(16 * ((size_t)g.nblocks + 1));  // BlkStat per block, zeroed too
   L.lens = take(kMaxAlpha);
   L.cw = take(kMaxAlpha * 4);
   L.cb_keys = take(kMaxAlpha * 8);
@@ -253,7 +254,8 @@ int pmz_compress_analyze(const float *d_in, const pmz_geom *g, const pmz_params 
   // zero status, coverage and histogram (contiguous at the front)
   CK(cudaMemsetAsync(d_ws, 0, L.lens, st));
   if (G.nblocks == 0) return PMZ_OK;
-  k_stats<<<(unsigned)G.nblocks, kBW * 32, 0, st>>>(d_in, G, k, at<BlkP>(d_ws, L.blkp), at<WsStatus>(d_ws, L.status));
+  k_stats<<<(unsigned)G.nparts, 256, 0, st>>>(d_in, G, k, at<BlkP>(d_ws, L.blkp), at<BlkStat>(d_ws, L.bstat),
+                                               at<WsStatus>(d_ws, L.status));
   if (p->m == 0 && n_val > 0)
     k_mark_val<<<(unsigned)((n_val + 255) / 256), 256, 0, st>>>(d_val, n_val, at<uint8_t>(d_ws, L.vflag),
                                                                at<WsStatus>(d_ws, L.status));
@@ -326,12 +328,10 @@ int pmz_compress_finish(const pmz_geom *g, const pmz_params *p, int write_header
                                        at<unsigned long long>(d_ws, L.cb_keys), at<unsigned long long>(d_ws, L.cb_w),
                                        at<unsigned>(d_ws, L.cb_parent), at<uint8_t>(d_ws, L.lens),
                                        at<unsigned>(d_ws, L.cw));
-  if (G.nparts > 0) {
-    unsigned grid = (unsigned)((G.nparts + kWarps - 1) / kWarps);
-    k_part_bits<kWarps><<<grid, kWarps * 32, 0, st>>>(G, at<BlkP>(d_ws, L.blkp), at<int16_t>(d_ws, L.rqbuf),
-                                                      at<uint8_t>(d_ws, L.lens),
-                                                      at<unsigned long long>(d_ws, L.part_bits), S);
-  }
+  if (G.nparts > 0)
+    k_part_bits<<<(unsigned)G.nparts, kPbW * 32, 0, st>>>(G, at<BlkP>(d_ws, L.blkp), at<int16_t>(d_ws, L.rqbuf),
+                                                         at<uint8_t>(d_ws, L.lens),
+                                                         at<unsigned long long>(d_ws, L.part_bits), S);
   k_block_sizes<<<(unsigned)((G.nblocks + 1 + 255) / 256), 256, 0, st>>>(
       G, at<BlkP>(d_ws, L.blkp), at<unsigned long long>(d_ws, L.part_bits),
       at<unsigned long long>(d_ws, L.part_zeros), at<unsigned long long>(d_ws, L.rec_size), S);
@@ -339,7 +339,24 @@ int pmz_compress_finish(const pmz_geom *g, const pmz_params *p, int write_header
   CK(cub::DeviceScan::ExclusiveSum(at<void>(d_ws, L.cub_tmp), cb, at<unsigned long long>(d_ws, L.rec_size),
                                    at<unsigned long long>(d_ws, L.rec_off), (int)(G.nblocks + 1), st));
   k_finish_status<<<1, 1, 0, st>>>(G, k, write_header, at<unsigned long long>(d_ws, L.rec_off), out_cap, S);
-  // size check on the host: the writers need the final offsets anyway
+  // the writers read m, the header size and the capacity verdict from the
+  // device status: one host synchronisation, at the end
+  if (d_out != nullptr) {
+    if (write_header)
+      k_write_header<<<1, 256, 0, st>>>(d_out, G, k, g->global_rows, at<uint8_t>(d_ws, L.lens), S);
+    if (G.nparts > 0) {
+      k_write_part<<<(unsigned)G.nparts, kWT, kWpSmem, st>>>(
+          G, at<BlkP>(d_ws, L.blkp), at<int16_t>(d_ws, L.rqbuf), at<double>(d_ws, L.vbuf),
+          at<double>(d_ws, L.anchors), at<unsigned long long>(d_ws, L.part_bits),
+          at<unsigned long long>(d_ws, L.part_zeros), at<unsigned long long>(d_ws, L.rec_off),
+          at<uint8_t>(d_ws, L.lens), at<unsigned>(d_ws, L.cw), d_out, S);
+    }
+    if (d_block_offsets)
+      k_block_offsets<<<(unsigned)((G.nblocks + 1 + 255) / 256), 256, 0, st>>>(
+          G, k, write_header, at<unsigned long long>(d_ws, L.rec_off), S, (unsigned long long *)d_block_offsets);
+  }
+  s = launch_check();
+  if (s) return s;
   WsStatus hs;
   CK(cudaMemcpyAsync(&hs, S, sizeof(WsStatus), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
@@ -362,27 +379,6 @@ int pmz_compress_finish(const pmz_geom *g, const pmz_params *p, int write_header
   if (err) return err;
   if (hs.unresolved) return PMZ_ERR_UNRESOLVED_ROUNDING;
   if (d_out == nullptr) return PMZ_ERR_CAPACITY;
-  unsigned long long rec_base = hs.header_bytes;
-  if (write_header)
-    k_write_header<<<1, 256, 0, st>>>(d_out, G, k, g->global_rows, at<uint8_t>(d_ws, L.lens), S);
-  if (G.nparts > 0) {
-    CK(cudaFuncSetAttribute(k_write_part, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)write_part_smem(12)));
-    k_write_part<<<(unsigned)G.nparts, kWT, write_part_smem(hs.m), st>>>(
-        G, at<BlkP>(d_ws, L.blkp), at<int16_t>(d_ws, L.rqbuf), at<double>(d_ws, L.vbuf),
-        at<double>(d_ws, L.anchors), at<unsigned long long>(d_ws, L.part_bits),
-        at<unsigned long long>(d_ws, L.part_zeros), at<unsigned long long>(d_ws, L.rec_off),
-        at<uint8_t>(d_ws, L.lens), at<unsigned>(d_ws, L.cw), hs.m, d_out, rec_base, S);
-  }
-  if (d_block_offsets)
-    k_block_offsets<<<(unsigned)((G.nblocks + 1 + 255) / 256), 256, 0, st>>>(
-        G, k, write_header, at<unsigned long long>(d_ws, L.rec_off), S, (unsigned long long *)d_block_offsets);
-  s = launch_check();
-  if (s) return s;
-  CK(cudaStreamSynchronize(st));
-  CK(cudaMemcpy(&hs, S, sizeof(WsStatus), cudaMemcpyDeviceToHost));
-  if (res) res->launches = hs.launches;
-  err = err_from_bits(hs.err_bits);
-  if (err) return err;
   return PMZ_OK;
 }
 

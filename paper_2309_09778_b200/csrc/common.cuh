@@ -268,7 +268,7 @@ struct WsStatus {
 
 struct WsLayout {
   size_t status, cov, hist, lens, cw, cb_keys, cb_w, cb_parent, blkp, part_bits, part_zeros, anchors, rec_size,
-      rec_off, cub_tmp, codes, balv, zrow, vflag, vbuf, rqbuf, clsbuf, total;
+      rec_off, cub_tmp, codes, balv, zrow, vflag, bstat, vbuf, rqbuf, clsbuf, total;
   size_t cub_bytes;
 };
 

@@ -249,28 +249,31 @@ __global__ void __launch_bounds__(1024) k_codebook(const unsigned long long *his
   CB_STAMP(5)
 }
 
-// K7: per-partition payload bits from the final rq tiles (one warp per
-// partition; 8 residuals per 16-byte load, the anchor excluded).
-template <int NW>
-__global__ void __launch_bounds__(NW * 32) k_part_bits(Geom g, const BlkP *__restrict__ blkp,
-                                                       const int16_t *__restrict__ rqbuf,
-                                                       const uint8_t *__restrict__ lens,
-                                                       unsigned long long *part_bits, WsStatus *st) {
+// K7: per-partition payload bits from the final rq tiles: one CTA per
+// partition, warp w sums chunks w, w + 8, ... (8 residuals per 16-byte load,
+// the anchor excluded).
+constexpr int kPbW = 8;
+__global__ void __launch_bounds__(kPbW * 32) k_part_bits(Geom g, const BlkP *__restrict__ blkp,
+                                                        const int16_t *__restrict__ rqbuf,
+                                                        const uint8_t *__restrict__ lens,
+                                                        unsigned long long *part_bits, WsStatus *st) {
+  __shared__ unsigned long long s_bits;
   count_launch(st);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t p = (int64_t)blockIdx.x * NW + warp;
-  if (p >= g.nparts) return;
+  const int64_t p = blockIdx.x;
   int64_t b;
   int pi;
   part_of(g, p, b, pi);
-  unsigned long long bits = 0;
+  if (threadIdx.x == 0) s_bits = 0;
+  __syncthreads();
   if (!blkp[b].trivial) {
     const int center = 1 << (st->m - 1);
     const BlockBox bb = block_box(g, b);
     const int R = min(g.prow, bb.br - pi * g.prow), C = bb.bc, nch = (C + 31) >> 5;
     const uint4 *tp = reinterpret_cast<const uint4 *>(rqbuf + tile_base(g, p, 0));
+    unsigned bits = 0;
     // vector v of a tile: row v >> 2, columns 8 (v & 3) .. + 7
-    for (int kc = 0; kc < nch; kc++) {
+    for (int kc = warp; kc < nch; kc += kPbW) {
       uint4 q[4];
 #pragma unroll
       for (int u = 0; u < 4; u++) q[u] = __ldg(tp + kc * (kTile / 8) + lane + 32 * u);
@@ -288,8 +291,10 @@ __global__ void __launch_bounds__(NW * 32) k_part_bits(Geom g, const BlkP *__res
       }
     }
     for (int o = 16; o > 0; o >>= 1) bits += __shfl_xor_sync(0xffffffffu, bits, o);
+    if (lane == 0 && bits) atomicAdd(&s_bits, (unsigned long long)bits);
   }
-  if (lane == 0) part_bits[p] = bits;
+  __syncthreads();
+  if (threadIdx.x == 0) part_bits[p] = s_bits;
 }
 
 __host__ __device__ inline uint64_t model_blob_bytes(int S, int H) { return 16 + 8ull * (S + 1) * H + 8ull * H; }
@@ -324,6 +329,7 @@ __device__ __forceinline__ void put_f64(uint8_t *p, double v) { put_bytes(p, &v,
 __global__ void k_write_header(uint8_t *out, Geom g, KParams k, uint64_t global_rows, const uint8_t *lens,
                                WsStatus *st) {
   count_launch(st);
+  if (st->err_bits) return;  // capacity / codebook errors: nothing is written
   const int m = st->m;
   const int n = 1 << m;
   const uint64_t mb = model_blob_bytes(k.S, k.H);
@@ -434,7 +440,8 @@ __device__ __forceinline__ void copy_s2g_bytes(uint8_t *dst, const unsigned *src
 constexpr int kWT = 256;
 constexpr unsigned kPartWords = 4096;  // 16 KB payload staging (else direct byte writes)
 constexpr unsigned kBalStage = 1024;   // balance values per staging sub-round (8 KB)
-__host__ __device__ inline size_t write_part_smem(int m) { return m <= 12 ? (size_t)(1u << m) * 5 : 0; }
+constexpr int kWpTabM = 10;            // codebook tables in shared memory up to this m
+constexpr size_t kWpSmem = (size_t)(1u << kWpTabM) * 5;
 
 __global__ void __launch_bounds__(kWT) k_write_part(Geom g, const BlkP *__restrict__ blkp,
                                                     const int16_t *__restrict__ rqbuf,
@@ -444,8 +451,8 @@ __global__ void __launch_bounds__(kWT) k_write_part(Geom g, const BlkP *__restri
                                                     const unsigned long long *__restrict__ part_zeros,
                                                     const unsigned long long *__restrict__ rec_off,
                                                     const uint8_t *__restrict__ lens,
-                                                    const unsigned *__restrict__ cw, int m, uint8_t *out,
-                                                    unsigned long long rec_base, WsStatus *st) {
+                                                    const unsigned *__restrict__ cw, uint8_t *out,
+                                                    WsStatus *st) {
   extern __shared__ __align__(16) unsigned char wp_dyn[];
   __shared__ unsigned sw[kPartWords];
   __shared__ unsigned long long sbal[kBalStage + 1];
@@ -453,6 +460,11 @@ __global__ void __launch_bounds__(kWT) k_write_part(Geom g, const BlkP *__restri
   __shared__ unsigned s_wsum[kWT / 32][2];
   __shared__ unsigned s_carry[2];
   count_launch(st);
+  // m, the header size and the capacity check come from the device status:
+  // no host round trip between the codebook and the writers
+  if (st->err_bits) return;
+  const int m = st->m;
+  const unsigned long long rec_base = st->header_bytes;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t p = blockIdx.x;
   int64_t b;
@@ -464,9 +476,9 @@ __global__ void __launch_bounds__(kWT) k_write_part(Geom g, const BlkP *__restri
     if (pi == 0 && tid == 0) base[0] = 1;
     return;
   }
-  const bool small_tab = m <= 12;
+  const bool small_tab = m <= kWpTabM;
   unsigned *s_cw = reinterpret_cast<unsigned *>(wp_dyn);
-  uint8_t *s_len = wp_dyn + (small_tab ? (4u << m) : 0u);
+  uint8_t *s_len = wp_dyn + (4u << kWpTabM);
   if (small_tab) {
     for (int i = tid; i < (1 << m); i += kWT) {
       s_len[i] = lens[i];

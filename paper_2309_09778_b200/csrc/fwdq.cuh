@@ -22,12 +22,12 @@
 
 namespace pmz {
 
-constexpr int kFqW = 8;                 // warps per CTA
+constexpr int kFqW = 4;                 // warps per CTA
 constexpr int kFqStrip = kFqW * 32;     // columns per strip
 constexpr size_t kFqSmem = sizeof(double) * 32 * (kFqStrip + 1);
 
 template <int PK>
-__global__ void __launch_bounds__(kFqW * 32, 2) k_fwdq(const float *__restrict__ x, Geom g, KParams k,
+__global__ void __launch_bounds__(kFqW * 32, 5) k_fwdq(const float *__restrict__ x, Geom g, KParams k,
                                                    const BlkP *__restrict__ blkp, const uint8_t *__restrict__ vflag,
                                                    WsStatus *st, double *__restrict__ vbuf, int16_t *__restrict__ rqbuf,
                                                    uint8_t *__restrict__ clsbuf, unsigned long long *__restrict__ cov) {

@@ -356,17 +356,125 @@ __global__ void __launch_bounds__(kPPC * 64) k_compress_ws(const float *__restri
   }
 }
 
-// Block statistics + transform parameters for every block (separate, fully
-// parallel pass so the main kernel starts from resident parameters).
-__global__ void __launch_bounds__(kBW * 32) k_stats(const float *__restrict__ x, Geom g, KParams k,
-                                                    BlkP *__restrict__ blkp, WsStatus *st) {
-  __shared__ BlkP sP;
+// compute_block_stats + make_transform_params (transform.py:84-167) for
+// every block, one CTA per 32-row partition: the partition's min positive
+// normal magnitude / max magnitude / non-finite flag go to per-block slots by
+// atomics (min as atomicMax of the bit complement, so a zeroed workspace is
+// the identity); the last partition of a block to arrive derives the block's
+// parameters (its three logarithms on three warps in parallel).
+struct BlkStat {
+  unsigned nmin;   // ~bits of the min |x| (0 = none)
+  unsigned max;    // bits of the max |x|
+  unsigned flags;  // bit 0: non-finite seen
+  unsigned count;  // partitions done
+};
+
+__global__ void __launch_bounds__(256) k_stats(const float *__restrict__ x, Geom g, KParams k,
+                                               BlkP *__restrict__ blkp, BlkStat *bst, WsStatus *st) {
+  __shared__ bool s_last;
+  __shared__ double s_l[3], s_fn;
   count_launch(st);
-  const BlockBox bb = block_box(g, blockIdx.x);
-  block_stats_params(x, g, k, bb, sP, st);
+  const int64_t p = blockIdx.x;
+  int64_t b;
+  int pi;
+  part_of(g, p, b, pi);
+  const BlockBox bb = block_box(g, b);
+  const int pr0 = pi * g.prow, R = min(g.prow, bb.br - pr0), C = bb.bc;
+  const float *base = x + (bb.r0 + pr0) * g.cols + bb.c0;
+  float mn = INFINITY, mx = 0.0f;
+  int nonfinite = 0;
+  auto acc = [&](float v) {
+    if (!isfinite(v)) nonfinite = 1;
+    const float a = fabsf(v);
+    if (a > 1.17549435e-38f && a <= 3.40282347e38f) { mn = fminf(mn, a); mx = fmaxf(mx, a); }
+  };
+  if ((g.cols & 3) == 0 && (C & 3) == 0) {
+    const int vpr = C >> 2, nv = R * vpr;
+    for (int i0 = threadIdx.x; i0 < nv; i0 += 4 * 256) {
+      float4 q[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const int i = i0 + u * 256;
+        if (i < nv) {
+          const int r = i / vpr, c = (i - r * vpr) << 2;
+          q[u] = __ldg(reinterpret_cast<const float4 *>(base + (int64_t)r * g.cols + c));
+        } else {
+          q[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; u++) { acc(q[u].x); acc(q[u].y); acc(q[u].z); acc(q[u].w); }
+    }
+  } else {
+    const int n = R * C;
+    for (int i0 = threadIdx.x; i0 < n; i0 += 4 * 256) {
+      float q[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const int i = i0 + u * 256;
+        q[u] = 0.f;
+        if (i < n) {
+          const int r = i / C, c = i - r * C;
+          q[u] = __ldg(base + (int64_t)r * g.cols + c);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; u++) acc(q[u]);
+    }
+  }
+  block_minmax<256>(mn, mx, nonfinite);
   if (threadIdx.x == 0) {
-    blkp[blockIdx.x] = sP;
-    if (sP.trivial) atomicAdd(&st->ntrivial, 1ull);
+    BlkStat *bs = bst + b;
+    if (mn != INFINITY) atomicMax(&bs->nmin, ~__float_as_uint(mn));
+    if (mx != 0.0f) atomicMax(&bs->max, __float_as_uint(mx));
+    if (nonfinite) atomicOr(&bs->flags, 1u);
+    __threadfence();
+    s_last = atomicAdd(&bs->count, 1u) == (unsigned)(bb.np - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  // ---- last partition of the block: make_transform_params ----
+  __threadfence();
+  BlkP P{};
+  const volatile BlkStat *vs = bst + b;
+  BlkStat fs;
+  fs.nmin = vs->nmin;
+  fs.max = vs->max;
+  fs.flags = vs->flags;
+  const float gmx = __uint_as_float(fs.max);
+  if (threadIdx.x == 0 && (fs.flags & 1u)) set_err(st, PMZ_ERR_NONFINITE);
+  if (gmx == 0.0f) {
+    P.trivial = 1;
+    if (threadIdx.x == 0) {
+      blkp[b] = P;
+      atomicAdd(&st->ntrivial, 1ull);
+    }
+    return;
+  }
+  const double fp = (double)__uint_as_float(~fs.nmin), amax = (double)gmx;
+  if (threadIdx.x == 0) {
+    // transform.py:160-162
+    s_fn = __ddiv_rn(__dmul_rn(__dmul_rn(__dadd_rn(amax, k.eps0), fp), k.onepbr2), __dsub_rn(fp, k.eps0));
+    if (!isfinite(s_fn)) set_err(st, PMZ_ERR_NONREPRESENTABLE);
+  }
+  __syncthreads();
+  const double fn = s_fn;
+  // the three per-block logarithms in parallel (transform.py:119-123)
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0 && w < 3) {
+    const double arg = w == 0 ? fp : (w == 1 ? fn : __dsub_rn(fp, k.eps0));
+    s_l[w] = pmz_log2_d(arg, &st->unresolved);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    P.factor_pos = fp;
+    P.factor_neg = fn;
+    P.lg_pos = s_l[0];
+    P.lg_neg = s_l[1];
+    P.zero_code = __dadd_rn(-126.0, P.lg_pos);
+    P.zero_threshold = __dadd_rn(P.zero_code, k.b_a);
+    P.boundary = __dsub_rn(__dadd_rn(P.lg_neg, s_l[2]), k.b_a);
+    blkp[b] = P;
   }
 }
 
