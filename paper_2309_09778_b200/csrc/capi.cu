@@ -173,12 +173,10 @@ int launch_ws(const KParams &k, unsigned grid, cudaStream_t st, const float *x, 
 }
 
 template <int PK>
-void launch_fwdq(const KParams &k, cudaStream_t st, const float *x, const Geom &G, void *d_ws, const WsLayout &L) {
-  cudaFuncSetAttribute(k_fwdq<PK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFqSmem);
-  k_fwdq<PK><<<(unsigned)G.nparts, kFqW * 32, kFqSmem, st>>>(
-      x, G, k, at<BlkP>(d_ws, L.blkp), at<uint8_t>(d_ws, L.vflag), at<WsStatus>(d_ws, L.status),
-      at<double>(d_ws, L.vbuf), at<int16_t>(d_ws, L.rqbuf), at<uint8_t>(d_ws, L.clsbuf),
-      at<unsigned long long>(d_ws, L.cov));
+void launch_quant(const KParams &k, cudaStream_t st, const Geom &G, void *d_ws, const WsLayout &L) {
+  k_quant<PK><<<(unsigned)G.nparts, kFqT, 0, st>>>(G, k, at<BlkP>(d_ws, L.blkp), at<uint8_t>(d_ws, L.vflag),
+                                                   at<WsStatus>(d_ws, L.status), at<double>(d_ws, L.vbuf),
+                                                   at<int16_t>(d_ws, L.rqbuf), at<unsigned long long>(d_ws, L.cov));
 }
 
 
@@ -262,9 +260,11 @@ int pmz_compress_analyze(const float *d_in, const pmz_geom *g, const pmz_params 
   // forward map + m-independent TRUE-surface quantization of every element,
   // coverage of the validation blocks in the same pass
   if (G.nparts > 0) {
-    if (k.init_model == 3) launch_fwdq<3>(k, st, d_in, G, d_ws, L);
-    else if (k.init_model == 1) launch_fwdq<1>(k, st, d_in, G, d_ws, L);
-    else launch_fwdq<0>(k, st, d_in, G, d_ws, L);
+    k_fwd<<<(unsigned)G.nparts, kFqT, 0, st>>>(d_in, G, at<BlkP>(d_ws, L.blkp), at<WsStatus>(d_ws, L.status),
+                                               at<double>(d_ws, L.vbuf), at<uint8_t>(d_ws, L.clsbuf));
+    if (k.init_model == 3) launch_quant<3>(k, st, G, d_ws, L);
+    else if (k.init_model == 1) launch_quant<1>(k, st, G, d_ws, L);
+    else launch_quant<0>(k, st, G, d_ws, L);
   }
   return launch_check();
 }

@@ -1,38 +1,30 @@
-// fwdq.cuh -- the fully parallel half of compress_block:
-// forward_map (transform.py:170-185) of every element, its sign/range class,
-// and the TRUE-surface residual quantized WITHOUT the m-dependent clamp
-// (D5): rq = round_half_away(err / (2 b_a)) when
-// |rq| <= 32767, else kRqOut.  code(m) = center + rq when |rq| < center,
-// else 0 -- identical to quantize(err, 2 b_a, m) for every m in [4, 16].
+// fwdq.cuh -- the fully parallel half of compress_block,
+// two kernels over the partition-tiled layout (common.cuh: tile_base):
 //
-// The select_m coverage histogram (D17) over validation
-// blocks falls out of the same pass: m_required(err) = max(4, bitlen|rq| + 1),
-// 17 for kRqOut.
+// k_fwd: forward_map (transform.py:170-185) of every element and its
+//   sign/range class.  One CTA per partition; a thread takes 4 consecutive
+//   columns of one row (a quad: one 16-byte input load, 4 interleaved log2
+//   chains, one 32-byte output store); a warp covers 4 rows x 32 columns.
+//   Pure FP64-throughput work, no shared memory.
 //
-// Outputs go to the partition-tiled layout (common.cuh: tile_base).
-// One CTA per 32-row partition, swept in 256-column strips: 8 warps forward-map
-// a strip (lane = column, 8 interleaved log2 chains per lane) into shared
-// memory, then compute the residuals from the shared tile (W / N / NW inside
-// the partition; the strip's left neighbour column is kept as a halo).  All
-// of it is FP64-throughput work at full occupancy; the sequential
-// verify_and_repair recurrence (wsc.cuh) only consumes the results.
+// k_quant: the TRUE-surface residual quantized WITHOUT the m-dependent clamp
+//   (D5): rq = round_half_away(err / (2 b_a)) when
+//   |rq| <= 32767, else kRqOut, so code(m) = center + rq when |rq| < center,
+//   else 0 -- identical to quantize(err, 2 b_a, m) for every m in [4, 16].
+//   Neighbours W / N / NW come back from L2 (inside the partition; 0 outside).
+//   The select_m coverage histogram (D17) over validation
+//   blocks falls out of the same pass: m_required = max(4, bitlen|rq| + 1),
+//   17 for kRqOut.
 #pragma once
 #include "common.cuh"
 #include "wsc.cuh"
 
 namespace pmz {
 
-constexpr int kFqW = 4;                 // warps per CTA
-constexpr int kFqStrip = kFqW * 32;     // columns per strip
-constexpr size_t kFqSmem = sizeof(double) * 32 * (kFqStrip + 1);
+constexpr int kFqT = 256;  // threads per CTA (both kernels)
 
-template <int PK>
-__global__ void __launch_bounds__(kFqW * 32, 5) k_fwdq(const float *__restrict__ x, Geom g, KParams k,
-                                                   const BlkP *__restrict__ blkp, const uint8_t *__restrict__ vflag,
-                                                   WsStatus *st, double *__restrict__ vbuf, int16_t *__restrict__ rqbuf,
-                                                   uint8_t *__restrict__ clsbuf, unsigned long long *__restrict__ cov) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double(*sv)[kFqStrip + 1] = reinterpret_cast<double(*)[kFqStrip + 1]>(smem_raw);
+__global__ void __launch_bounds__(kFqT) k_fwd(const float *__restrict__ x, Geom g, const BlkP *__restrict__ blkp,
+                                             WsStatus *st, double *__restrict__ vbuf, uint8_t *__restrict__ clsbuf) {
   count_launch(st);
   const int64_t p = blockIdx.x;
   int64_t b;
@@ -41,86 +33,109 @@ __global__ void __launch_bounds__(kFqW * 32, 5) k_fwdq(const float *__restrict__
   const BlkP P = blkp[b];
   if (P.trivial) return;
   const BlockBox bb = block_box(g, b);
-  const int pr0 = pi * g.prow, R = min(g.prow, bb.br - pr0), C = bb.bc;
-  const bool val = vflag[b] != 0;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t off = (bb.r0 + pr0) * g.cols + bb.c0;
-  const float *xp = x + off;
+  const int pr0 = pi * g.prow, R = min(g.prow, bb.br - pr0), C = bb.bc, nch = (C + 31) >> 5;
+  const float *xp = x + (bb.r0 + pr0) * g.cols + bb.c0;
+  const bool vec = ((g.cols & 3) == 0) && ((bb.c0 & 3) == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
+  double *vt = vbuf + tile_base(g, p, 0);
+  uint8_t *ct = clsbuf + tile_base(g, p, 0);
   unsigned *amb = &st->unresolved;
-  __shared__ unsigned h[18];
-  if (threadIdx.x < 18) h[threadIdx.x] = 0;  // first use is after a __syncthreads
+  for (int i = threadIdx.x; i < nch * 256; i += kFqT) {
+    const int kc = i >> 8, r = (i >> 3) & 31, c0 = kc * 32 + (i & 7) * 4;
+    if (r >= R || c0 >= C) continue;
+    const float *src = xp + (int64_t)r * g.cols + c0;
+    float xr[4];
+    if (vec && c0 + 3 < C) {
+      const float4 q = __ldg(reinterpret_cast<const float4 *>(src));
+      xr[0] = q.x; xr[1] = q.y; xr[2] = q.z; xr[3] = q.w;
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; u++) xr[u] = c0 + u < C ? __ldg(src + u) : 0.0f;
+    }
+    double ax[4], lg[4], v[4];
+    unsigned cl = 0;
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const float xz = zfloor(xr[u]);
+      ax[u] = xz != 0.0f ? (double)fabsf(xz) : 1.0;
+    }
+    pmz_log2_f32_fast_n<4>(ax, lg, amb);
+#pragma unroll
+    for (int u = 0; u < 4; u++) {
+      const float xz = zfloor(xr[u]);
+      v[u] = P.zero_code;
+      if (xz > 0.0f) v[u] = __dadd_rn(lg[u], P.lg_pos);
+      else if (xz < 0.0f) v[u] = __dadd_rn(lg[u], P.lg_neg);
+      cl |= (unsigned)xclass(xz) << (8 * u);
+    }
+    const int o = kc * kTile + r * 32 + (c0 & 31);
+    double2 *vo = reinterpret_cast<double2 *>(vt + o);
+    vo[0] = make_double2(v[0], v[1]);
+    vo[1] = make_double2(v[2], v[3]);
+    *reinterpret_cast<unsigned *>(ct + o) = cl;
+  }
+}
 
-  for (int c0 = 0; c0 < C; c0 += kFqStrip) {
-    const int j = 1 + warp * 32 + lane;  // smem column (0 = halo)
-    const int col = c0 + warp * 32 + lane;
-    const bool inb = col < C;
-    // ---- forward map of the strip (next batch's loads issued before this
-    // batch's log2 chains) ----
-    float xn[8];
+template <int PK>
+__global__ void __launch_bounds__(kFqT) k_quant(Geom g, KParams k, const BlkP *__restrict__ blkp,
+                                               const uint8_t *__restrict__ vflag, WsStatus *st,
+                                               const double *__restrict__ vbuf, int16_t *__restrict__ rqbuf,
+                                               unsigned long long *__restrict__ cov) {
+  __shared__ unsigned h[18];
+  count_launch(st);
+  const int64_t p = blockIdx.x;
+  int64_t b;
+  int pi;
+  part_of(g, p, b, pi);
+  if (blkp[b].trivial) return;
+  const BlockBox bb = block_box(g, b);
+  const int pr0 = pi * g.prow, R = min(g.prow, bb.br - pr0), C = bb.bc, nch = (C + 31) >> 5;
+  const bool val = vflag[b] != 0;
+  if (threadIdx.x < 18) h[threadIdx.x] = 0;
+  __syncthreads();
+  const double *vt = vbuf + tile_base(g, p, 0);
+  int16_t *rt = rqbuf + tile_base(g, p, 0);
+  const int lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < nch * 256; i += kFqT) {
+    const int kc = i >> 8, r = (i >> 3) & 31, c0 = kc * 32 + (i & 7) * 4;
+    const bool ok = r < R && c0 < C;
+    int rq[4] = {0, 0, 0, 0};
+    if (ok) {
+      const int o = kc * kTile + r * 32 + (c0 & 31);
+      // this row and the row above, columns c0 - 1 .. c0 + 3 (0 outside the partition)
+      double cur[5], up[5];
+      const double2 *q = reinterpret_cast<const double2 *>(vt + o);
+      const double2 a0 = __ldg(q), a1 = __ldg(q + 1);
+      cur[1] = a0.x; cur[2] = a0.y; cur[3] = a1.x; cur[4] = a1.y;
+      const int ol = (c0 & 31) ? o - 1 : o - kTile + 31;  // left neighbour: previous tile's column 31
+      cur[0] = c0 > 0 ? __ldg(vt + ol) : 0.0;
+      if (r > 0) {
+        const double2 *qu = reinterpret_cast<const double2 *>(vt + o - 32);
+        const double2 b0 = __ldg(qu), b1 = __ldg(qu + 1);
+        up[1] = b0.x; up[2] = b0.y; up[3] = b1.x; up[4] = b1.y;
+        up[0] = c0 > 0 ? __ldg(vt + ol - 32) : 0.0;
+      } else {
 #pragma unroll
-    for (int q = 0; q < 8; q++) xn[q] = (inb && q < R) ? __ldg(xp + (int64_t)q * g.cols + col) : 0.0f;
-    for (int rb = 0; rb < R; rb += 8) {
-      float xr[8];
-#pragma unroll
-      for (int q = 0; q < 8; q++) {
-        xr[q] = xn[q];
-        xn[q] = (inb && rb + 8 + q < R) ? __ldg(xp + (int64_t)(rb + 8 + q) * g.cols + col) : 0.0f;
+        for (int u = 0; u < 5; u++) up[u] = 0.0;
       }
-      double ax[8], lg[8];
 #pragma unroll
-      for (int q = 0; q < 8; q++) {
-        const float xz = zfloor(xr[q]);
-        ax[q] = xz != 0.0f ? (double)fabsf(xz) : 1.0;
+      for (int u = 0; u < 4; u++) {
+        const int c = c0 + u;
+        if (c < C) rq[u] = quantize_rq(__dsub_rn(cur[u + 1], predict_k<PK>(k, cur[u], up[u + 1], up[u])), k);
       }
-      pmz_log2_f32_fast_n<8>(ax, lg, amb);
+      const unsigned lo = ((unsigned)(uint16_t)rq[0]) | ((unsigned)(uint16_t)rq[1] << 16);
+      const unsigned hi = ((unsigned)(uint16_t)rq[2]) | ((unsigned)(uint16_t)rq[3] << 16);
+      *reinterpret_cast<uint2 *>(rt + o) = make_uint2(lo, hi);
+    }
+    if (val) {
 #pragma unroll
-      for (int q = 0; q < 8; q++) {
-        if (inb && rb + q < R) {
-          const float xz = zfloor(xr[q]);
-          double v = P.zero_code;
-          if (xz > 0.0f) v = __dadd_rn(lg[q], P.lg_pos);
-          else if (xz < 0.0f) v = __dadd_rn(lg[q], P.lg_neg);
-          sv[rb + q][j] = v;
-          const int64_t e = tile_elem(g, p, rb + q, col);
-          vbuf[e] = v;
-          clsbuf[e] = xclass(xz);
-        }
+      for (int u = 0; u < 4; u++) {
+        const int c = c0 + u;
+        const bool cnt = ok && c < C && (r | c);  // anchors excluded (D17)
+        const int mm = cnt ? m_of_rq(rq[u]) : -1;
+        const unsigned grp = __match_any_sync(0xffffffffu, mm);
+        if (cnt && (grp & ((1u << lane) - 1)) == 0) atomicAdd(&h[mm], (unsigned)__popc(grp));
       }
     }
-    __syncthreads();
-    // ---- TRUE-surface residuals (independent chains, 4 rows per batch) ----
-    if (inb) {
-      for (int rb = 0; rb < R; rb += 4) {
-        int rq[4];
-#pragma unroll
-        for (int q = 0; q < 4; q++) {
-          const int r = min(rb + q, R - 1);
-          const double v = sv[r][j];
-          double w = 0.0, n = 0.0, nw = 0.0;
-          if (col > 0) w = sv[r][j - 1];
-          if (r > 0) {
-            n = sv[r - 1][j];
-            if (col > 0) nw = sv[r - 1][j - 1];
-          }
-          rq[q] = quantize_rq(__dsub_rn(v, predict_k<PK>(k, w, n, nw)), k);
-        }
-#pragma unroll
-        for (int q = 0; q < 4; q++) {
-          const int r = rb + q;
-          if (r < R) {
-            rqbuf[tile_elem(g, p, r, col)] = (int16_t)rq[q];
-            if (val && !(r == 0 && col == 0)) {  // anchors excluded (D17)
-              const int mm = m_of_rq(rq[q]);
-              const unsigned grp = __match_any_sync(__activemask(), mm);
-              if ((grp & ((1u << lane) - 1)) == 0) atomicAdd(&h[mm], (unsigned)__popc(grp));
-            }
-          }
-        }
-      }
-    }
-    __syncthreads();
-    if (c0 + kFqStrip < C && threadIdx.x < R) sv[threadIdx.x][0] = sv[threadIdx.x][kFqStrip];
-    __syncthreads();
   }
   if (val) {
     __syncthreads();
