@@ -168,7 +168,8 @@ int launch_ws(const KParams &k, unsigned grid, cudaStream_t st, const float *x, 
   k_compress_ws<PK><<<grid, kPPC * 64, kWscSmem, st>>>(x, G, k, at<BlkP>(d_ws, L.blkp), at<WsStatus>(d_ws, L.status),
                                                        at<double>(d_ws, L.vbuf), at<int16_t>(d_ws, L.rqbuf),
                                                        at<uint8_t>(d_ws, L.clsbuf), at<double>(d_ws, L.anchors),
-                                                       at<unsigned long long>(d_ws, L.part_zeros));
+                                                       at<unsigned long long>(d_ws, L.part_zeros),
+                                                       at<uint8_t>(d_ws, L.vflag), at<unsigned long long>(d_ws, L.hist));
   return PMZ_OK;
 }
 
@@ -254,7 +255,7 @@ int pmz_compress_analyze(const float *d_in, const pmz_geom *g, const pmz_params 
   if (G.nblocks == 0) return PMZ_OK;
   k_stats<<<(unsigned)G.nparts, 256, 0, st>>>(d_in, G, k, at<BlkP>(d_ws, L.blkp), at<BlkStat>(d_ws, L.bstat),
                                                at<WsStatus>(d_ws, L.status));
-  if (p->m == 0 && n_val > 0)
+  if (n_val > 0)
     k_mark_val<<<(unsigned)((n_val + 255) / 256), 256, 0, st>>>(d_val, n_val, at<uint8_t>(d_ws, L.vflag),
                                                                at<WsStatus>(d_ws, L.status));
   // forward map + m-independent TRUE-surface quantization of every element,
@@ -285,11 +286,6 @@ int pmz_compress_codes(const float *d_in, const pmz_geom *g, const pmz_params *p
     else if (k.init_model == 1) s = launch_ws<1>(k, grid, st, d_in, G, d_ws, L);
     else s = launch_ws<0>(k, grid, st, d_in, G, d_ws, L);
     if (s) return s;
-  }
-  if (n_val > 0) {
-    dim3 grid(16, (unsigned)n_val);
-    k_val_hist<kNT><<<grid, kNT, 0, st>>>(G, at<BlkP>(d_ws, L.blkp), d_val, at<int16_t>(d_ws, L.rqbuf),
-                                          at<unsigned long long>(d_ws, L.hist), at<WsStatus>(d_ws, L.status));
   }
   return launch_check();
 }
@@ -357,9 +353,13 @@ int pmz_compress_finish(const pmz_geom *g, const pmz_params *p, int write_header
   }
   s = launch_check();
   if (s) return s;
-  WsStatus hs;
-  CK(cudaMemcpyAsync(&hs, S, sizeof(WsStatus), cudaMemcpyDeviceToHost, st));
+  // status and coverage are adjacent at the front of the workspace: one copy
+  static_assert(sizeof(WsStatus) <= 256, "status slot");
+  alignas(8) uint8_t front[256 + 18 * 8];
+  CK(cudaMemcpyAsync(front, d_ws, L.cov + 18 * 8, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  WsStatus hs;
+  memcpy(&hs, front, sizeof(WsStatus));
   if (res) {
     memset(res, 0, sizeof(*res));
     res->header_bytes = hs.header_bytes;
@@ -373,7 +373,7 @@ int pmz_compress_finish(const pmz_geom *g, const pmz_params *p, int write_header
     res->max_code_len = hs.max_len;
     res->unresolved = hs.unresolved;
     res->launches = hs.launches;
-    CK(cudaMemcpy(res->coverage, at<uint64_t>(d_ws, L.cov), 18 * 8, cudaMemcpyDeviceToHost));
+    memcpy(res->coverage, front + L.cov, 18 * 8);
   }
   int err = err_from_bits(hs.err_bits);
   if (err) return err;

@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(kFqT) k_quant(Geom g, KParams k, const BlkP *_
   if (blkp[b].trivial) return;
   const BlockBox bb = block_box(g, b);
   const int pr0 = pi * g.prow, R = min(g.prow, bb.br - pr0), C = bb.bc, nch = (C + 31) >> 5;
-  const bool val = vflag[b] != 0;
+  const bool val = vflag[b] != 0 && k.m_fixed == 0;  // coverage only when select_m runs
   if (threadIdx.x < 18) h[threadIdx.x] = 0;
   __syncthreads();
   const double *vt = vbuf + tile_base(g, p, 0);

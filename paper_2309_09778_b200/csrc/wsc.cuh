@@ -123,7 +123,9 @@ __global__ void __launch_bounds__(kPPC * 64) k_compress_ws(const float *__restri
                                                            const double *__restrict__ vbuf, int16_t *rqbuf,
                                                            const uint8_t *__restrict__ clsbuf,
                                                            double *__restrict__ anchors,
-                                                           unsigned long long *__restrict__ part_zeros) {
+                                                           unsigned long long *__restrict__ part_zeros,
+                                                           const uint8_t *__restrict__ vflag,
+                                                           unsigned long long *__restrict__ hist) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   count_launch(st);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -157,7 +159,21 @@ __global__ void __launch_bounds__(kPPC * 64) k_compress_ws(const float *__restri
 
   if (role == 0) {
     // ------------------------------ producer ------------------------------
+    // validation blocks: the final codes of each finished tile go into the
+    // summed code histogram (D10) before the tile is stored (warp-aggregated)
+    const bool val = vflag[b] != 0;
+    const int center = 1 << (st->m - 1);
+    if (val && pi == 0 && lane == 0) atomicAdd(&hist[kMaxAlpha], 1ull);  // k for the floor (D10)
     auto store_rq = [&](int kc) {  // final rq tile of chunk kc back in place
+      if (val) {
+        const int c = kc * 32 + lane;
+        for (int r = 0; r < R; r++) {
+          const bool ok = c < C && (r | c);  // the anchor is not coded
+          const int code = ok ? code_of_rq(W.rq[kc % kSlots][r * 32 + lane], center) : -1;
+          const unsigned peers = __match_any_sync(0xffffffffu, code);
+          if (ok && (peers & ((1u << lane) - 1)) == 0) atomicAdd(&hist[code], (unsigned long long)__popc(peers));
+        }
+      }
       if (lane == 0) {
         bulk_s2g(rqbuf + tb + (int64_t)kc * kTile, W.rq[kc % kSlots], kTile * 2);
         bulk_commit();
