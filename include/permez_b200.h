@@ -155,6 +155,23 @@ PMZ_API uint64_t *pmz_ws_histogram(void *d_ws, const pmz_params *p, const pmz_ge
 PMZ_API int pmz_compress_finish(const pmz_geom *g, const pmz_params *p, int write_header, uint8_t *d_out, uint64_t out_cap,
                         uint64_t *d_block_offsets, void *d_ws, uint64_t ws_bytes, void *stream, pmz_result *res);
 
+/* pmz_compress_finish split for stream capture (CUDA graphs): _async only
+ * enqueues (the writers read m, sizes and the capacity verdict from the
+ * device status; nothing is written on error); _result synchronises `stream`,
+ * fills *res and returns the status (wrote_output = d_out was non-null). */
+PMZ_API int pmz_compress_finish_async(const pmz_geom *g, const pmz_params *p, int write_header, uint8_t *d_out,
+                                      uint64_t out_cap, uint64_t *d_block_offsets, void *d_ws, uint64_t ws_bytes,
+                                      void *stream);
+PMZ_API int pmz_compress_result(const pmz_geom *g, const pmz_params *p, int wrote_output, void *d_ws,
+                                uint64_t ws_bytes, void *stream, pmz_result *res);
+
+/* All three stages enqueued on `stream` with no host synchronisation (single
+ * GPU): capturable into a CUDA graph; read the outcome with
+ * pmz_compress_result. */
+PMZ_API int pmz_compress_enqueue(const float *d_in, const pmz_geom *g, const pmz_params *p, const int64_t *d_val_blocks,
+                                 int64_t n_val, int write_header, uint8_t *d_out, uint64_t out_cap,
+                                 uint64_t *d_block_offsets, void *d_ws, uint64_t ws_bytes, void *stream);
+
 /* One-call single-GPU compress (cmd_compress minus ingest/training). */
 PMZ_API int pmz_compress(const float *d_in, const pmz_geom *g, const pmz_params *p, const int64_t *d_val_blocks,
                  int64_t n_val, uint8_t *d_out, uint64_t out_cap, uint64_t *d_block_offsets, void *d_ws,

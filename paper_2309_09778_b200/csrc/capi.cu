@@ -309,8 +309,9 @@ __global__ void k_finish_status(Geom g, KParams k, int write_header, const unsig
   if (st->total_bytes > cap) atomicOr(&st->err_bits, 1u << (-PMZ_ERR_CAPACITY));
 }
 
-int pmz_compress_finish(const pmz_geom *g, const pmz_params *p, int write_header, uint8_t *d_out, uint64_t out_cap,
-                        uint64_t *d_block_offsets, void *d_ws, uint64_t ws_bytes, void *stream, pmz_result *res) {
+int pmz_compress_finish_async(const pmz_geom *g, const pmz_params *p, int write_header, uint8_t *d_out,
+                              uint64_t out_cap, uint64_t *d_block_offsets, void *d_ws, uint64_t ws_bytes,
+                              void *stream) {
   int s = check_params(p);
   if (s) return s;
   Geom G = geom_of(p, g);
@@ -351,8 +352,17 @@ int pmz_compress_finish(const pmz_geom *g, const pmz_params *p, int write_header
       k_block_offsets<<<(unsigned)((G.nblocks + 1 + 255) / 256), 256, 0, st>>>(
           G, k, write_header, at<unsigned long long>(d_ws, L.rec_off), S, (unsigned long long *)d_block_offsets);
   }
-  s = launch_check();
+  return launch_check();
+}
+
+int pmz_compress_result(const pmz_geom *g, const pmz_params *p, int wrote_output, void *d_ws, uint64_t ws_bytes,
+                        void *stream, pmz_result *res) {
+  int s = check_params(p);
   if (s) return s;
+  Geom G = geom_of(p, g);
+  WsLayout L = compress_layout(G);
+  if (ws_bytes < L.total) return PMZ_ERR_WORKSPACE;
+  cudaStream_t st = (cudaStream_t)stream;
   // status and coverage are adjacent at the front of the workspace: one copy
   static_assert(sizeof(WsStatus) <= 256, "status slot");
   alignas(8) uint8_t front[256 + 18 * 8];
@@ -378,8 +388,25 @@ int pmz_compress_finish(const pmz_geom *g, const pmz_params *p, int write_header
   int err = err_from_bits(hs.err_bits);
   if (err) return err;
   if (hs.unresolved) return PMZ_ERR_UNRESOLVED_ROUNDING;
-  if (d_out == nullptr) return PMZ_ERR_CAPACITY;
+  if (!wrote_output) return PMZ_ERR_CAPACITY;
   return PMZ_OK;
+}
+
+int pmz_compress_finish(const pmz_geom *g, const pmz_params *p, int write_header, uint8_t *d_out, uint64_t out_cap,
+                        uint64_t *d_block_offsets, void *d_ws, uint64_t ws_bytes, void *stream, pmz_result *res) {
+  int s = pmz_compress_finish_async(g, p, write_header, d_out, out_cap, d_block_offsets, d_ws, ws_bytes, stream);
+  if (s) return s;
+  return pmz_compress_result(g, p, d_out != nullptr, d_ws, ws_bytes, stream, res);
+}
+
+int pmz_compress_enqueue(const float *d_in, const pmz_geom *g, const pmz_params *p, const int64_t *d_val,
+                         int64_t n_val, int write_header, uint8_t *d_out, uint64_t out_cap, uint64_t *d_block_offsets,
+                         void *d_ws, uint64_t ws_bytes, void *stream) {
+  int s = pmz_compress_analyze(d_in, g, p, d_val, n_val, d_ws, ws_bytes, stream);
+  if (s) return s;
+  s = pmz_compress_codes(d_in, g, p, d_val, n_val, d_ws, ws_bytes, stream);
+  if (s) return s;
+  return pmz_compress_finish_async(g, p, write_header, d_out, out_cap, d_block_offsets, d_ws, ws_bytes, stream);
 }
 
 int pmz_compress(const float *d_in, const pmz_geom *g, const pmz_params *p, const int64_t *d_val, int64_t n_val,

@@ -280,6 +280,80 @@ class Codec:
 _codecs: dict = {}
 
 
+class GraphedCompressor:
+    """The whole single-GPU compress pipeline of one geometry captured into a
+    CUDA graph (pmz_compress_enqueue: ~16 kernels, no host synchronisation),
+    replayed per call; the outcome is read with pmz_compress_result (one small
+    device->host copy).  Buffers are fixed at construction: the input is
+    ``x`` (a float32 CUDA tensor the caller keeps alive and refills), or, with
+    ``host_input`` (a pinned float32 CPU tensor), a device copy that the graph
+    itself refills from it (host->device copy inside the graph).  ``run``
+    returns (container bytes as a CUDA uint8 view, CompressInfo)."""
+
+    def __init__(self, codec: Codec, cfg: CompressConfig, x: torch.Tensor | None = None,
+                 host_input: torch.Tensor | None = None, block_offsets: torch.Tensor | None = None):
+        if (x is None) == (host_input is None):
+            raise ConfigError("GraphedCompressor needs exactly one of x (device) or host_input (pinned host)")
+        self.codec, self.cfg = codec, cfg
+        if host_input is not None:
+            if host_input.dtype != torch.float32 or host_input.is_cuda:
+                raise ConfigError("host_input must be a float32 CPU tensor (pinned for asynchronous copies)")
+            self.host = host_input
+            self.x = torch.empty(host_input.shape, dtype=torch.float32, device=codec.device)
+        else:
+            if x.dtype != torch.float32 or not x.is_cuda or not x.is_contiguous():
+                raise ConfigError("x must be a contiguous float32 CUDA tensor")
+            self.host, self.x = None, x
+        self.p, self.g, self.nb, self.val = codec.plan(self.x.shape, cfg)
+        self.d_val = torch.as_tensor(self.val, dtype=torch.int64, device=codec.device)
+        lib = codec.lib
+        wsz, cap = ctypes.c_uint64(0), ctypes.c_uint64(0)
+        check(lib.pmz_workspace_size(ctypes.byref(self.p), ctypes.byref(self.g), ctypes.byref(wsz)), "workspace_size")
+        check(lib.pmz_max_container_size(ctypes.byref(self.p), ctypes.byref(self.g), ctypes.byref(cap)), "max_size")
+        self.ws = torch.empty(max(int(wsz.value), 1), dtype=torch.uint8, device=codec.device)
+        self.out = torch.empty(max(int(cap.value), 1), dtype=torch.uint8, device=codec.device)
+        self.block_offsets = block_offsets
+        # eager run: sets kernel attributes, validates the configuration
+        self._enqueue()
+        self._result()
+        torch.cuda.synchronize(codec.device)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self._enqueue()
+
+    def _enqueue(self):
+        lib = self.codec.lib
+        if self.host is not None:
+            self.x.copy_(self.host, non_blocking=True)
+        check(lib.pmz_compress_enqueue(_ptr(self.x), ctypes.byref(self.g), ctypes.byref(self.p), _ptr(self.d_val),
+                                       int(self.d_val.numel()), 1, _ptr(self.out), self.out.numel(),
+                                       _ptr(self.block_offsets), _ptr(self.ws), self.ws.numel(),
+                                       _stream_ptr(self.codec.device)), "compress_enqueue")
+
+    def _result(self):
+        res = N.Result()
+        check(self.codec.lib.pmz_compress_result(ctypes.byref(self.g), ctypes.byref(self.p), 1, _ptr(self.ws),
+                                                 self.ws.numel(), _stream_ptr(self.codec.device), ctypes.byref(res)),
+              "compress")
+        n = int(res.header_bytes + res.record_bytes)
+        info = CompressInfo(n, int(res.header_bytes), int(res.nblocks), int(res.ntrivial), int(res.nbal),
+                            int(res.nrepair), int(res.ncodes), int(res.m), int(res.max_code_len),
+                            list(res.coverage), tuple(self.x.shape), self.val, int(res.launches))
+        return self.out[:n], info
+
+    def launch(self):
+        """Replay the captured pipeline on the current stream (asynchronous)."""
+        self.graph.replay()
+
+    def result(self):
+        """Synchronise and return (container CUDA view, CompressInfo) of the last launch."""
+        return self._result()
+
+    def run(self):
+        self.launch()
+        return self.result()
+
+
 def _codec(device=None) -> Codec:
     dev = _require_cuda(device)
     key = str(dev)
