@@ -14,6 +14,7 @@
 #include "decompress.cuh"
 #include "encode.cuh"
 #include "fwdq.cuh"
+#include "dec3.cuh"
 
 using namespace pmz;
 
@@ -531,7 +532,7 @@ int pmz_index_blocks(const uint8_t *h, uint64_t n, const pmz_header *hd, uint64_
 namespace {
 struct DecLayout {
   size_t status, blkp, part_bits, part_off, part_zeros, anchors, bal_off, pay_off, blk_nbal, tab, sym, lut, codes,
-      large, total;
+      zrow, large, total;
 };
 DecLayout dec_layout(const Geom &g) {
   DecLayout L{};
@@ -552,20 +553,22 @@ DecLayout dec_layout(const Geom &g) {
   L.blk_nbal = take(8 * (size_t)(g.nblocks + 1));
   L.tab = take(sizeof(DecTab));
   L.sym = take(2 * kMaxAlpha);
-  L.lut = take(4 << kLutBits);
-  L.codes = take(2 * (size_t)(g.rows * g.cols));
-  L.large = take(4 * (size_t)(g.nparts + 1));
+  L.lut = take(4ull * ((1u << kLutBits) + kLut2Max));            // first + second level
+  L.codes = take(2 * (size_t)g.nparts * (size_t)g.nct * kTile);  // partition-tiled
+  L.zrow = take(2 * 32 * (size_t)(g.nparts + 1));                  // code-0 count per partition row
+  L.large = take(4 * (size_t)(g.nparts + 1));                      // work list of long substreams
   L.total = o;
   return L;
 }
 template <int PK>
 int launch_recon(const KParams &k, unsigned grid, cudaStream_t st, const uint8_t *d_buf, const Geom &G, int m,
                  void *d_ws, const DecLayout &L, float *d_out) {
-  CK(cudaFuncSetAttribute(k_reconstruct_ws<PK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDscSmem));
-  k_reconstruct_ws<PK><<<grid, kPPC * 64, kDscSmem, st>>>(
-      d_buf, G, k, m, at<BlkP>(d_ws, L.blkp), at<uint16_t>(d_ws, L.codes), at<double>(d_ws, L.anchors),
-      at<unsigned long long>(d_ws, L.part_zeros), at<unsigned long long>(d_ws, L.bal_off),
-      at<unsigned long long>(d_ws, L.blk_nbal), d_out, at<WsStatus>(d_ws, L.status));
+  CK(cudaFuncSetAttribute(k_reconstruct3<PK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDsc3Smem));
+  k_reconstruct3<PK><<<grid, kPPC * 64, kDsc3Smem, st>>>(
+      d_buf, G, k, m, at<BlkP>(d_ws, L.blkp), at<uint16_t>(d_ws, L.codes), at<uint16_t>(d_ws, L.zrow),
+      at<double>(d_ws, L.anchors), at<unsigned long long>(d_ws, L.part_zeros),
+      at<unsigned long long>(d_ws, L.bal_off), at<unsigned long long>(d_ws, L.blk_nbal), d_out,
+      at<WsStatus>(d_ws, L.status));
   return PMZ_OK;
 }
 
@@ -617,22 +620,22 @@ int pmz_decompress(const uint8_t *d_buf, uint64_t n, const pmz_header *hdr, doub
         at<unsigned long long>(d_ws, L.pay_off), at<unsigned long long>(d_ws, L.blk_nbal), S);
     k_dec_tables<<<1, 1024, 0, st>>>(d_buf + hdr->lens_offset, (int)hdr->m, at<DecTab>(d_ws, L.tab),
                                      at<uint16_t>(d_ws, L.sym), at<unsigned>(d_ws, L.lut), S);
-    unsigned grid = (unsigned)((G.nparts + kWarps - 1) / kWarps);
-    using Small = DecCfg<2, false>;
-    using Large = DecCfg<1, true>;
     CK(cudaMemsetAsync(at<unsigned>(d_ws, L.large), 0, 4, st));
-    CK(cudaFuncSetAttribute(k_decode<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Small::kSmem));
-    CK(cudaFuncSetAttribute(k_decode<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Large::kSmem));
-    k_decode<2, false><<<(unsigned)((G.nparts + 1) / 2), 64, Small::kSmem, st>>>(
-        d_buf, G, at<BlkP>(d_ws, L.blkp), at<DecTab>(d_ws, L.tab), at<uint16_t>(d_ws, L.sym),
+    CK(cudaFuncSetAttribute(k_decode3<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d3_smem<false>()));
+    CK(cudaFuncSetAttribute(k_decode3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d3_smem<true>()));
+    k_decode3<false><<<(unsigned)((G.nparts + D3Cfg<false>::kW - 1) / D3Cfg<false>::kW), D3Cfg<false>::kW * 32,
+                       d3_smem<false>(), st>>>(
+        d_buf, n, G, at<BlkP>(d_ws, L.blkp), at<DecTab>(d_ws, L.tab), at<uint16_t>(d_ws, L.sym),
         at<unsigned>(d_ws, L.lut), at<unsigned long long>(d_ws, L.part_bits),
         at<unsigned long long>(d_ws, L.part_off), at<unsigned long long>(d_ws, L.pay_off),
-        at<uint16_t>(d_ws, L.codes), at<unsigned long long>(d_ws, L.part_zeros), at<unsigned>(d_ws, L.large), S);
-    k_decode<1, true><<<296, 32, Large::kSmem, st>>>(
-        d_buf, G, at<BlkP>(d_ws, L.blkp), at<DecTab>(d_ws, L.tab), at<uint16_t>(d_ws, L.sym),
+        at<uint16_t>(d_ws, L.codes), at<unsigned long long>(d_ws, L.part_zeros), at<uint16_t>(d_ws, L.zrow),
+        at<unsigned>(d_ws, L.large), S);
+    k_decode3<true><<<444, 32, d3_smem<true>(), st>>>(
+        d_buf, n, G, at<BlkP>(d_ws, L.blkp), at<DecTab>(d_ws, L.tab), at<uint16_t>(d_ws, L.sym),
         at<unsigned>(d_ws, L.lut), at<unsigned long long>(d_ws, L.part_bits),
         at<unsigned long long>(d_ws, L.part_off), at<unsigned long long>(d_ws, L.pay_off),
-        at<uint16_t>(d_ws, L.codes), at<unsigned long long>(d_ws, L.part_zeros), at<unsigned>(d_ws, L.large), S);
+        at<uint16_t>(d_ws, L.codes), at<unsigned long long>(d_ws, L.part_zeros), at<uint16_t>(d_ws, L.zrow),
+        at<unsigned>(d_ws, L.large), S);
     const unsigned rgrid = (unsigned)((G.nparts + kPPC - 1) / kPPC);
     int s2;
     if (k.init_model == 3) s2 = launch_recon<3>(k, rgrid, st, d_buf, G, (int)hdr->m, d_ws, L, d_out);

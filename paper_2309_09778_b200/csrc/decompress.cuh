@@ -22,9 +22,20 @@ struct DecTab {
   int zsym;   // that symbol (canonical order)
   int pad;
   unsigned rcp[34];  // ceil(2^32 / l) for l >= 2 (exact floor(n / l) for n < 2^16)
+  int sub_bits;      // second-level table: codewords of kLutBits+1 .. kLutBits+sub_bits bits
+  int has_l2;        // 1 when every long codeword resolves in the second-level table
 };
 
 constexpr int kLutBits = 12;
+constexpr unsigned kLut2Max = 1u << 16;  // second-level entries (256 KB of the decode workspace)
+constexpr unsigned kLutL2Flag = 0x80000000u;
+// Decode table entry: symbol [0,16), length [16,21), run divisor M [21,31)
+// (M = ceil(1024 / l) for 2 <= l <= 16: floor(z / l) == (z * M) >> 10 for
+// z <= 64; 0 = no run detection), bit 31 = second-level pointer.
+__host__ __device__ __forceinline__ unsigned lut_entry(int l, unsigned sym) {
+  const unsigned M = (l >= 2 && l <= 16) ? (1024u + (unsigned)l - 1u) / (unsigned)l : 0u;
+  return sym | ((unsigned)l << 16) | (M << 21);
+}
 
 // D1: per-block record heads -> transform parameters and partition tables.
 __global__ void k_dec_blocks(const uint8_t *__restrict__ buf, unsigned long long n, Geom g, KParams k,
@@ -117,15 +128,52 @@ __global__ void __launch_bounds__(1024) k_dec_tables(const uint8_t *__restrict__
     for (int l = 2; l < 34; l++) tab->rcp[l] = (unsigned)(0x100000000ull / (unsigned long long)l) + 1u;
   }
   __syncthreads();
-  // LUT over the next kLutBits bits: (len << 16) | symbol, or 0 when len > kLutBits
+  // LUT over the next kLutBits bits: (len << 16) | symbol; prefixes of longer
+  // codewords point into a second-level table over the next sub_bits bits
+  // (kLutL2Flag | base), or are 0 (canonical search) when it would not fit.
+  __shared__ unsigned s_nlong, s_fit;
+  if (threadIdx.x == 0) s_nlong = 0;
+  __syncthreads();
+  const int maxl = tab->maxl;
+  const int sub_bits = maxl > kLutBits ? maxl - kLutBits : 0;
   for (int e = threadIdx.x; e < (1 << kLutBits); e += blockDim.x) {
     unsigned v = 0;
-    for (int l = 1; l <= kLutBits && l <= tab->maxl; l++) {
+    for (int l = 1; l <= kLutBits && l <= maxl; l++) {
       unsigned code = (unsigned)e >> (kLutBits - l);
       unsigned d = code - tab->first[l];
-      if (d < tab->count[l]) { v = ((unsigned)l << 16) | sym[tab->offset[l] + d]; break; }
+      if (d < tab->count[l]) { v = lut_entry(l, sym[tab->offset[l] + d]); break; }
     }
     lut[e] = v;
+  }
+  __syncthreads();
+  // long prefixes of a canonical code are the highest prefixes: count them
+  for (int e = threadIdx.x; e < (1 << kLutBits); e += blockDim.x)
+    if (lut[e] == 0) atomicAdd(&s_nlong, 1u);
+  __syncthreads();
+  const unsigned nlong = s_nlong;
+  if (threadIdx.x == 0) {
+    s_fit = sub_bits > 0 && sub_bits <= 16 && ((unsigned long long)nlong << sub_bits) <= kLut2Max;
+    tab->sub_bits = sub_bits;
+    tab->has_l2 = (int)s_fit;
+  }
+  __syncthreads();
+  if (s_fit) {
+    const unsigned p0 = (1u << kLutBits) - nlong;  // first long prefix
+    const unsigned per = 1u << sub_bits, total = nlong << sub_bits;
+    for (unsigned i = threadIdx.x; i < total; i += blockDim.x) {
+      const unsigned pre = p0 + i / per, j = i % per;
+      const unsigned long long bits = ((unsigned long long)pre << sub_bits) | j;  // maxl bits
+      unsigned v = 0;
+      for (int l = kLutBits + 1; l <= maxl; l++) {
+        const unsigned code = (unsigned)(bits >> (maxl - l));
+        const unsigned d = code - tab->first[l];
+        if (d < tab->count[l]) { v = lut_entry(l, sym[tab->offset[l] + d]); break; }
+      }
+      lut[(1u << kLutBits) + i] = v;
+    }
+    __syncthreads();
+    for (unsigned e = p0 + threadIdx.x; e < (1u << kLutBits); e += blockDim.x)
+      lut[e] = kLutL2Flag | ((e - p0) << sub_bits);
   }
 }
 

@@ -38,7 +38,7 @@ __global__ void __launch_bounds__(kPPC * 64) k_reconstruct_ws(const uint8_t *__r
                                                               const unsigned long long *__restrict__ bal_off,
                                                               const unsigned long long *__restrict__ blk_nbal,
                                                               float *__restrict__ out, WsStatus *st) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   count_launch(st);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int pair = warp >> 1, role = warp & 1;
@@ -162,6 +162,175 @@ __global__ void __launch_bounds__(kPPC * 64) k_reconstruct_ws(const uint8_t *__r
           hp = hl;
           hl = vh;
         }
+      }
+      if (kg >= 1 && kg - 1 < nch) {
+        __syncwarp();
+        bar_arrive_n(bar0 + kSlots + (kg - 1) % kSlots, 64);
+      }
+    }
+    if (ngroups == nch) {
+      __syncwarp();
+      bar_arrive_n(bar0 + kSlots + (nch - 1) % kSlots, 64);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_reconstruct3: the same recurrence over the partition-tiled codes written
+// by k_decode3 (dec3.cuh).  Warp pair per partition:
+//   producer (lane = column): per 32-column chunk, loads the code tile, ranks
+//     the chunk's balance points per row (row bases from the per-row zero
+//     counts of the decoder, ballots within the chunk) and gathers their
+//     values from the container into the ring; when the consumer has finished
+//     a chunk it inverse-maps it and stores 32 f32 rows coalesced;
+//   consumer (lane = row): vhat = code 0 ? balance value : predict(W, N, NW) +
+//     dequantize(code) -- predicated, software-pipelined, one shuffle per step
+//     (see k_compress_ws).
+struct DRing3 {
+  double val[kSlots][kTile];     // producer: balance value (code 0); consumer: reconstructed value
+  uint16_t code[kSlots][kTile];
+};
+constexpr size_t kDsc3Smem = sizeof(DRing3) * kPPC;
+
+template <int PK>
+__global__ void __launch_bounds__(kPPC * 64) k_reconstruct3(const uint8_t *__restrict__ buf, Geom g, KParams k, int m,
+                                                            const BlkP *__restrict__ blkp,
+                                                            const uint16_t *__restrict__ codes,
+                                                            const uint16_t *__restrict__ zrow,
+                                                            const double *__restrict__ anchors,
+                                                            const unsigned long long *__restrict__ part_zeros,
+                                                            const unsigned long long *__restrict__ bal_off,
+                                                            const unsigned long long *__restrict__ blk_nbal,
+                                                            float *__restrict__ out, WsStatus *st) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  count_launch(st);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int pair = warp >> 1, role = warp & 1;
+  DRing3 &W = reinterpret_cast<DRing3 *>(smem_raw)[pair];
+  const int64_t p = (int64_t)blockIdx.x * kPPC + pair;
+  if (p >= g.nparts) return;
+  int64_t b;
+  int pi;
+  part_of(g, p, b, pi);
+  const BlockBox bb = block_box(g, b);
+  const int pr0 = pi * g.prow, R = min(g.prow, bb.br - pr0), C = bb.bc;
+  const int nch = (C + 31) >> 5;
+  float *opart = out + (bb.r0 + pr0) * g.cols + bb.c0;
+  const BlkP P = blkp[b];
+  if (P.trivial) {
+    if (role == 0)
+      for (int r = 0; r < R; r++)
+        for (int c = lane; c < C; c += 32) opart[(int64_t)r * g.cols + c] = 0.0f;
+    return;
+  }
+  const int64_t p0 = first_part(g, b);
+  unsigned long long zb = 0, ztot = 0;
+  for (int i = 0; i < bb.np; i++) {
+    const unsigned long long z = part_zeros[p0 + i];
+    if (i < pi) zb += z;
+    ztot += z;
+  }
+  if (ztot != blk_nbal[b]) {
+    if (role == 0 && lane == 0 && pi == 0) set_err(st, ztot > blk_nbal[b] ? PMZ_ERR_BALANCE_UNDERFLOW : PMZ_ERR_CORRUPT);
+    return;
+  }
+  const int center = 1 << (m - 1);
+  const int bar0 = 1 + pair * 2 * kSlots;
+  const uint16_t *ct = codes + tile_base(g, p, 0);
+
+  if (role == 0) {
+    // ------------------------------ producer ------------------------------
+    unsigned *amb = &st->unresolved;
+    const uint8_t *bal = buf + bal_off[b];
+    // balance index of the next code-0 of every row (warp-uniform registers):
+    // partition base + zeros of the rows above (the decoder's per-row counts)
+    unsigned rb[32];
+    {
+      const unsigned zr = lane < R ? zrow[p * 32 + lane] : 0u;
+      unsigned incl = zr;
+      for (int d = 1; d < 32; d <<= 1) {
+        const unsigned t = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += t;
+      }
+      const unsigned excl = (unsigned)zb + incl - zr;
+#pragma unroll
+      for (int r = 0; r < 32; r++) rb[r] = __shfl_sync(0xffffffffu, excl, r);
+    }
+    auto flush = [&](int chunk) {
+      const int s = chunk % kSlots, c = chunk * 32 + lane;
+      if (c < C)
+        for (int r = 0; r < R; r++) opart[(int64_t)r * g.cols + c] = inv_f32(W.val[s][r * 32 + lane], P, amb);
+    };
+    for (int kc = 0; kc < nch; kc++) {
+      const int s = kc % kSlots;
+      if (kc >= kSlots) {
+        bar_sync_n(bar0 + kSlots + s, 64);
+        flush(kc - kSlots);
+        __syncwarp();
+      }
+      const bool inb = kc * 32 + lane < C;
+      uint16_t cr[32];
+#pragma unroll
+      for (int r = 0; r < 32; r++) cr[r] = (inb && r < R) ? __ldg(&ct[kc * kTile + r * 32 + lane]) : (uint16_t)1;
+      if (kc == 0 && lane == 0) cr[0] = kAnc;
+#pragma unroll
+      for (int r = 0; r < 32; r++) {
+        const bool z = cr[r] == 0;
+        const unsigned zm = __ballot_sync(0xffffffffu, z);
+        if (z) W.val[s][r * 32 + lane] = ld_f64_unaligned(bal + 8ull * (rb[r] + __popc(zm & ((1u << lane) - 1))));
+        if (r < R) W.code[s][r * 32 + lane] = cr[r];
+        rb[r] += __popc(zm);
+      }
+      __syncwarp();
+      bar_arrive_n(bar0 + s, 64);  // full[s]
+    }
+    for (int kc = max(0, nch - kSlots); kc < nch; kc++) {
+      bar_sync_n(bar0 + kSlots + kc % kSlots, 64);
+      flush(kc);
+    }
+  } else {
+    // ------------------------------ consumer ------------------------------
+    const double anc = anchors[p];
+    const int nsteps = C + R - 1;
+    const int ngroups = (nsteps + 31) >> 5;
+    const double c_two_ba = pin(k.two_ba);
+    const int c_center = pin(center);
+    const bool lane0 = lane == 0, lane_in = lane < R;
+    double hl = 0.0, pn = 0.0;
+    for (int kg = 0; kg < ngroups; kg++) {
+      if (kg < nch) bar_sync_n(bar0 + kg % kSlots, 64);
+      const int t0 = kg * 32, t1 = min(nsteps, t0 + 32);
+      const int scur = kg % kSlots, sprev = (kg + kSlots - 1) % kSlots;
+      struct In {
+        double v, dq;
+        int idx;
+        bool started, active, bal, anchor;
+      };
+      auto prep = [&](int t) -> In {
+        In q;
+        const int c = t - lane;
+        q.started = c >= 0;
+        q.active = lane_in & q.started & (c < C);
+        const int cc = min(max(c, 0), C - 1);
+        q.idx = ((cc >> 5) == kg ? scur : sprev) * kTile + lane * 32 + (cc & 31);
+        const int code = W.code[0][q.idx];
+        q.v = W.val[0][q.idx];
+        q.anchor = code == kAnc;
+        q.bal = code == 0;
+        q.dq = __dmul_rn((double)(code - c_center), c_two_ba);
+        return q;
+      };
+      In cur = prep(t0);
+#pragma unroll 2
+      for (int t = t0; t < t1; t++) {
+        const double nhl = __shfl_up_sync(0xffffffffu, hl, 1);
+        const In nxt = prep(min(t + 1, t1 - 1));
+        const double vhat = __dadd_rn(predict_steady<PK>(k, hl, nhl, pn, lane0), cur.dq);
+        const double vh = cur.anchor ? anc : (cur.bal ? cur.v : vhat);
+        if (cur.active) W.val[0][cur.idx] = vh;
+        pn = nhl;
+        if (cur.started) hl = vh;
+        cur = nxt;
       }
       if (kg >= 1 && kg - 1 < nch) {
         __syncwarp();
