@@ -16,163 +16,11 @@
 
 namespace pmz {
 
-struct DRing {
-  double val[kSlots][32][32];     // producer: balance value (code 0); consumer: reconstructed value
-  uint16_t code[kSlots][32][32];
-};
-constexpr size_t kDscSmem = sizeof(DRing) * kPPC;
-
 __device__ __forceinline__ double ld_f64_unaligned(const uint8_t *p) {
   unsigned long long v = 0;
 #pragma unroll
   for (int i = 7; i >= 0; i--) v = (v << 8) | __ldg(p + i);
   return __longlong_as_double((long long)v);
-}
-
-template <int PK>
-__global__ void __launch_bounds__(kPPC * 64) k_reconstruct_ws(const uint8_t *__restrict__ buf, Geom g, KParams k, int m,
-                                                              const BlkP *__restrict__ blkp,
-                                                              const uint16_t *__restrict__ codes,
-                                                              const double *__restrict__ anchors,
-                                                              const unsigned long long *__restrict__ part_zeros,
-                                                              const unsigned long long *__restrict__ bal_off,
-                                                              const unsigned long long *__restrict__ blk_nbal,
-                                                              float *__restrict__ out, WsStatus *st) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  count_launch(st);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int pair = warp >> 1, role = warp & 1;
-  DRing &W = reinterpret_cast<DRing *>(smem_raw)[pair];
-  const int64_t p = (int64_t)blockIdx.x * kPPC + pair;
-  if (p >= g.nparts) return;
-  int64_t b;
-  int pi;
-  part_of(g, p, b, pi);
-  const BlockBox bb = block_box(g, b);
-  const int pr0 = pi * g.prow, R = min(g.prow, bb.br - pr0), C = bb.bc;
-  const int nch = (C + 31) >> 5;
-  float *opart = out + (bb.r0 + pr0) * g.cols + bb.c0;
-  const BlkP P = blkp[b];
-  if (P.trivial) {
-    if (role == 0)
-      for (int r = 0; r < R; r++)
-        for (int c = lane; c < C; c += 32) opart[(int64_t)r * g.cols + c] = 0.0f;
-    return;
-  }
-  const int64_t p0 = first_part(g, b);
-  unsigned long long zb = 0, ztot = 0;
-  for (int i = 0; i < bb.np; i++) {
-    const unsigned long long z = part_zeros[p0 + i];
-    if (i < pi) zb += z;
-    ztot += z;
-  }
-  if (ztot != blk_nbal[b]) {
-    if (role == 0 && lane == 0 && pi == 0) set_err(st, ztot > blk_nbal[b] ? PMZ_ERR_BALANCE_UNDERFLOW : PMZ_ERR_CORRUPT);
-    return;
-  }
-  const int center = 1 << (m - 1);
-  const int bar0 = 1 + pair * 2 * kSlots;
-  const uint16_t *cpart = codes + (bb.r0 + pr0) * g.cols + bb.c0;
-
-  if (role == 0) {
-    // ------------------------------ producer ------------------------------
-    unsigned *amb = &st->unresolved;
-    const uint8_t *bal = buf + bal_off[b];
-    // balance index of the first code-0 of every row: count zeros per row
-    // (lane = column; all 32 rows of a chunk loaded at once)
-    unsigned tot[32];
-#pragma unroll
-    for (int r = 0; r < 32; r++) tot[r] = 0;
-    for (int kc = 0; kc < nch; kc++) {
-      const int c = kc * 32 + lane;
-      uint16_t cr[32];
-#pragma unroll
-      for (int r = 0; r < 32; r++) cr[r] = (r < R && c < C) ? __ldg(&cpart[(int64_t)r * g.cols + c]) : (uint16_t)1;
-#pragma unroll
-      for (int r = 0; r < 32; r++) tot[r] += __popc(__ballot_sync(0xffffffffu, cr[r] == 0 && !(r == 0 && c == 0)));
-    }
-    unsigned rb[32];  // next balance index per row (warp-uniform registers)
-    {
-      unsigned acc = (unsigned)zb;
-#pragma unroll
-      for (int r = 0; r < 32; r++) {
-        rb[r] = acc;
-        acc += tot[r];
-      }
-    }
-    auto flush = [&](int chunk) {
-      const int s = chunk % kSlots, c = chunk * 32 + lane;
-      if (c < C)
-        for (int r = 0; r < R; r++) opart[(int64_t)r * g.cols + c] = inv_f32(W.val[s][r][lane], P, amb);
-    };
-    for (int kc = 0; kc < nch; kc++) {
-      const int s = kc % kSlots;
-      if (kc >= kSlots) {
-        bar_sync_n(bar0 + kSlots + s, 64);
-        flush(kc - kSlots);
-        __syncwarp();
-      }
-      const int c = kc * 32 + lane;
-      const bool inb = c < C;
-      uint16_t cr[32];
-#pragma unroll
-      for (int r = 0; r < 32; r++) cr[r] = (inb && r < R) ? __ldg(&cpart[(int64_t)r * g.cols + c]) : (uint16_t)1;
-      if (kc == 0 && lane == 0) cr[0] = kAnc;
-#pragma unroll
-      for (int r = 0; r < 32; r++) {
-        const bool z = cr[r] == 0;
-        const unsigned zm = __ballot_sync(0xffffffffu, z);
-        if (z) W.val[s][r][lane] = ld_f64_unaligned(bal + 8ull * (rb[r] + __popc(zm & ((1u << lane) - 1))));
-        if (r < R) W.code[s][r][lane] = cr[r];
-        rb[r] += __popc(zm);
-      }
-      __syncwarp();
-      bar_arrive_n(bar0 + s, 64);  // full[s]
-    }
-    for (int kc = max(0, nch - kSlots); kc < nch; kc++) {
-      bar_sync_n(bar0 + kSlots + kc % kSlots, 64);
-      flush(kc);
-    }
-  } else {
-    // ------------------------------ consumer ------------------------------
-    const double anc = anchors[p];
-    const int nsteps = C + R - 1;
-    const int ngroups = (nsteps + 31) >> 5;
-    double hl = 0.0, hp = 0.0;
-    for (int kg = 0; kg < ngroups; kg++) {
-      if (kg < nch) bar_sync_n(bar0 + kg % kSlots, 64);
-      const int t1 = min(nsteps, (kg + 1) * 32);
-      for (int t = kg * 32; t < t1; t++) {
-        const double nhl = __shfl_up_sync(0xffffffffu, hl, 1), nhp = __shfl_up_sync(0xffffffffu, hp, 1);
-        const int c = t - lane;
-        if (lane < R && c >= 0 && c < C) {
-          const int s = (c >> 5) % kSlots, j = c & 31;
-          const int code = W.code[s][lane][j];
-          double vh;
-          if (code == kAnc) {
-            vh = anc;
-          } else if (code == 0) {
-            vh = W.val[s][lane][j];
-          } else {
-            const bool hw = c > 0, hn = lane > 0;
-            vh = __dadd_rn(predict_k<PK>(k, hw ? hl : 0.0, hn ? nhl : 0.0, (hw && hn) ? nhp : 0.0),
-                           __dmul_rn((double)(code - center), k.two_ba));
-          }
-          W.val[s][lane][j] = vh;
-          hp = hl;
-          hl = vh;
-        }
-      }
-      if (kg >= 1 && kg - 1 < nch) {
-        __syncwarp();
-        bar_arrive_n(bar0 + kSlots + (kg - 1) % kSlots, 64);
-      }
-    }
-    if (ngroups == nch) {
-      __syncwarp();
-      bar_arrive_n(bar0 + kSlots + (nch - 1) % kSlots, 64);
-    }
-  }
 }
 
 // ---------------------------------------------------------------------------
