@@ -200,3 +200,32 @@ def test_log2_exhaustive_no_ambiguity():
     torch.cuda.synchronize()
     assert int(amb.item()) == 0
     assert mism == 0
+
+
+def test_decoder_runs_fallback(codec, oracle):
+    """Long runs of the balance-point codeword (a smooth field with sparse sign
+    flips): speculative decodes that start out of phase inside a run never
+    meet the true parse within their segment, so the transfer-function
+    fallback of the decoder (dec3.cuh) runs; the output must still be exact."""
+    rng = np.random.default_rng(11)
+    x = _field("C2", (512, 1024)).astype(np.float32)
+    flip = rng.random(x.shape) < 0.85   # mostly incoherent signs -> mostly balance points
+    x = np.where(flip, -x, x).astype(np.float32)
+    _parity(codec, oracle, x, b_r=1e-2, repair_factor=1.0)
+
+
+def test_decoder_large_substreams(codec, oracle):
+    """Fixed m = 16 on white noise: ~16+ bits per codeword, so partition
+    substreams exceed the 8 KB staging of the common decode launch and take
+    the large-stage launch."""
+    rng = np.random.default_rng(12)
+    x = (rng.normal(0, 1, (256, 512)) * 100).astype(np.float32)
+    info, n = _parity(codec, oracle, x, b_r=1e-3, repair_factor=1.0, m=16)
+    assert n > 8192 * 8 * 2  # on average more than 8 KB of payload per partition
+
+
+def test_decoder_tiny_partitions(codec, oracle):
+    """Very short substreams (2-row partitions, 8-column blocks): empty lane
+    segments and codewords spanning several lane segments."""
+    x = _field("C2", (64, 96))
+    _parity(codec, oracle, x, b_r=1e-2, repair_factor=1.0, block_rows=16, block_cols=8, partition_rows=2)
