@@ -28,23 +28,24 @@
 namespace pmz {
 
 constexpr unsigned kD3Bad = 0xffffffffu;
-constexpr unsigned kD3L2Smem = 2048;  // second-level entries kept in shared memory
 #ifndef PMZ_D3W
 #define PMZ_D3W 2
 #endif
 
-// LARGE = false: 4 warps per CTA, substreams up to 8 KB staged; longer ones
-// go to a work list served by the LARGE launch (1 warp per CTA, 32 KB = the
-// longest valid substream, 8191 codewords x 32 bits).
+// The substream is read straight from global memory (the reader prefetches
+// one word ahead, so the load is off the dependency chain) and the decode
+// tables through L1; the per-partition shared state is the boundary bitmap.
+// LARGE = false: substreams up to 16 KB; longer ones go to a work list
+// served by the LARGE launch (32 KB = the longest valid substream, 8191
+// codewords x 32 bits).
 template <bool LARGE>
 struct D3Cfg {
   static constexpr int kW = LARGE ? 1 : PMZ_D3W;
-  static constexpr int kStage = LARGE ? 8192 + 4 : 2048 + 4;
+  static constexpr int kBm = LARGE ? 8192 + 4 : 4096 + 4;  // boundary-bitmap words (substream <= 32 kBm bits)
 };
 template <bool LARGE>
 struct D3Warp {
-  unsigned stage[D3Cfg<LARGE>::kStage];
-  unsigned bm[D3Cfg<LARGE>::kStage];
+  unsigned bm[D3Cfg<LARGE>::kBm];
   unsigned xs[32];               // speculative exit per lane
   unsigned ns[32];               // speculative symbol count per lane
   unsigned ent[33], cnt[32];     // chained true entries / counts (fallback)
@@ -57,10 +58,11 @@ struct D3Warp {
 template <bool LARGE>
 constexpr size_t d3_smem() { return sizeof(D3Warp<LARGE>) * D3Cfg<LARGE>::kW; }
 
-// Big-endian words of the staged substream.
-struct D3Smem {
-  const unsigned *w;
-  __device__ __forceinline__ unsigned word(unsigned i) const { return w[i]; }
+// Big-endian words of the substream, straight from the container: word i
+// covers stream bits [32 i - adj, 32 i + 32 - adj) of an aligned base.
+struct D3Glob {
+  BitSrc bs;
+  __device__ __forceinline__ unsigned word(unsigned i) const { return bs.word(i); }
 };
 // Register bit reader at an arbitrary bit position of a word source whose
 // word 0 starts at stream bit -adj (adj = 0 for the staged source).
@@ -147,16 +149,13 @@ __global__ void __launch_bounds__(D3Cfg<LARGE>::kW * 32) k_decode3(const uint8_t
                                                       unsigned long long *__restrict__ part_zeros,
                                                       uint16_t *__restrict__ zrow_out, unsigned *large_list,
                                                       WsStatus *st) {
-  constexpr int kW = D3Cfg<LARGE>::kW, kStage = D3Cfg<LARGE>::kStage;
-  __shared__ unsigned s_lut[1 << kLutBits];
-  __shared__ unsigned s_lut2[kD3L2Smem];
+  constexpr int kW = D3Cfg<LARGE>::kW, kBm = D3Cfg<LARGE>::kBm;
   __shared__ unsigned long long s_rep[33];
   __shared__ DecTab s_tab;
   extern __shared__ __align__(16) unsigned char dyn3[];
   count_launch(st);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (LARGE && large_list[0] == 0) return;
-  for (int i = threadIdx.x; i < (1 << kLutBits); i += blockDim.x) s_lut[i] = lut[i];
+  if (LARGE && (int64_t)blockIdx.x * kW >= (int64_t)large_list[0]) return;
   if (threadIdx.x == 0) s_tab = *tab;
   if (threadIdx.x <= 32) {  // s_rep[l]: bits 0, l, 2l, ... (boundaries of a run, LSB first)
     unsigned long long r = 0;
@@ -165,21 +164,7 @@ __global__ void __launch_bounds__(D3Cfg<LARGE>::kW * 32) k_decode3(const uint8_t
     s_rep[threadIdx.x] = r;
   }
   __syncthreads();
-  // second-level table in shared memory when it fits
-  unsigned nl2 = 0;
-  if (s_tab.has_l2) {
-    // entries used = (number of long prefixes) << sub_bits; long prefixes are the top ones
-    unsigned first_long = 1u << kLutBits;
-    for (int i = (1 << kLutBits) - 1; i >= 0 && (s_lut[i] & kLutL2Flag); i--) first_long = i;
-    nl2 = ((1u << kLutBits) - first_long) << s_tab.sub_bits;
-  }
-  const bool l2s = nl2 <= kD3L2Smem;
-  for (unsigned i = threadIdx.x; i < (l2s ? nl2 : 0u); i += blockDim.x) s_lut2[i] = lut[(1 << kLutBits) + i];
-  // beyond the shared capacity the long codewords take the canonical search
-  for (int i = threadIdx.x; i < (l2s ? 0 : (1 << kLutBits)); i += blockDim.x)
-    if (s_lut[i] & kLutL2Flag) s_lut[i] = 0;
-  __syncthreads();
-  const unsigned *lut2 = s_lut2;
+  const unsigned *s_lut = lut, *lut2 = lut + (1 << kLutBits);  // through L1
   D3Warp<LARGE> &W = reinterpret_cast<D3Warp<LARGE> *>(dyn3)[warp];
   const int64_t nwork = LARGE ? (int64_t)large_list[0] : g.nparts;
   for (int64_t item = (int64_t)blockIdx.x * kW + warp; item < nwork; item += (int64_t)gridDim.x * kW) {
@@ -200,10 +185,8 @@ __global__ void __launch_bounds__(D3Cfg<LARGE>::kW * 32) k_decode3(const uint8_t
   uint16_t *ct = codes + tile_base(g, p, 0);
   W.zrow[lane] = 0;
   if (lane == 0) W.err = 0;
-  const unsigned long long nbytes64 = (L64 + 7) >> 3;
-  const unsigned long long nw64 = (nbytes64 + 3) >> 2;
   unsigned zeros = 0;
-  if (L64 > 0xffffff00ull || nw64 + 3 > (unsigned long long)kStage) {
+  if (L64 > 0xffffff00ull || ((L64 + 31) >> 5) + 4 > (unsigned long long)kBm) {
     if (!LARGE && L64 <= 32ull * (nsym + 1)) {
       if (lane == 0) large_list[1 + atomicAdd(&large_list[0], 1u)] = (unsigned)p;
       continue;
@@ -212,28 +195,21 @@ __global__ void __launch_bounds__(D3Cfg<LARGE>::kW * 32) k_decode3(const uint8_t
     if (lane == 0) set_err(st, PMZ_ERR_CORRUPT);
     continue;
   } else {
-    const unsigned L = (unsigned)L64, nbytes = (unsigned)nbytes64, nw = (unsigned)nw64;
+    const unsigned L = (unsigned)L64;
     D3_STAMP(0)
 #ifdef PMZ_DEC3_PROFILE
-    if (lane == 0 && p < 65536) { g_d3[p][5] = L; g_d3[p][6] = nsym; g_d3[p][7] = LARGE; }
+    if (lane == 0 && p < 65536) { g_d3[p][5] = L; g_d3[p][6] = nsym; g_d3[p][7] = LARGE; g_d3n[p][2] = clock64(); }
 #endif
-    // stage the substream as big-endian words (+ zero slack words)
-    for (unsigned i = lane; i < nw + 3; i += 32) {
-      unsigned v = 0;
-      if (i < nw) {
-#pragma unroll
-        for (int q = 0; q < 4; q++) {
-          const unsigned by = 4 * i + q;
-          v = (v << 8) | (by < nbytes ? (unsigned)__ldg(src + by) : 0u);
-        }
-      }
-      W.stage[i] = v;
+    BitSrc bsrc;
+    {
+      const uintptr_t a = reinterpret_cast<uintptr_t>(src);
+      bsrc.base = reinterpret_cast<const uint8_t *>(a & ~(uintptr_t)3);
+      bsrc.adj = (unsigned)(8 * (a & 3));
+      bsrc.nbits = L64;
+      bsrc.end = buf + buf_n;
     }
-    __syncwarp();
-#ifdef PMZ_DEC3_PROFILE
-    if (lane == 0 && p < 65536) g_d3n[p][2] = clock64();
-#endif
-    const D3Smem ss{W.stage};
+    const D3Glob ss{bsrc};
+    const unsigned adj = bsrc.adj;
     const unsigned segw = (((L + 31) >> 5) + 31) >> 5;  // words per lane segment
     const unsigned s_i = min(L, 32 * segw * lane), s_n = min(L, 32 * segw * (lane + 1));
     // ---- 1. speculative pass: every codeword boundary of the lane's
@@ -243,8 +219,8 @@ __global__ void __launch_bounds__(D3Cfg<LARGE>::kW * 32) k_decode3(const uint8_t
     {
       const unsigned w0 = s_i >> 5, wend = (s_n + 31) >> 5;
       for (unsigned q = w0; q < wend; q++) W.bm[q] = 0;
-      D3Reader<D3Smem> rd;
-      rd.seek(ss, s_i, 0);
+      D3Reader<D3Glob> rd;
+      rd.seek(ss, s_i, adj);
       unsigned pos = s_i;
       bool bad = false;
 #ifdef PMZ_DEC3_PROFILE
@@ -298,8 +274,8 @@ __global__ void __launch_bounds__(D3Cfg<LARGE>::kW * 32) k_decode3(const uint8_t
     // rest is the speculative parse) or crossing s_n; returns the exit and
     // the symbol count of [from, exit)
     auto walk = [&](unsigned from, unsigned &cnt) -> unsigned {
-      D3Reader<D3Smem> rd;
-      rd.seek(ss, from, 0);
+      D3Reader<D3Glob> rd;
+      rd.seek(ss, from, adj);
       unsigned pos = from, c = 0;
       while (pos < s_n) {
         if ((W.bm[pos >> 5] >> (pos & 31)) & 1u) {
@@ -337,8 +313,8 @@ __global__ void __launch_bounds__(D3Cfg<LARGE>::kW * 32) k_decode3(const uint8_t
       // the current path one step, or finish it and start the next offset
       int o = 1;
       unsigned q = s_i + 1, c = 0;
-      D3Reader<D3Smem> rd;
-      if (D > 1 && q < s_n) rd.seek(ss, q, 0);
+      D3Reader<D3Glob> rd;
+      if (D > 1 && q < s_n) rd.seek(ss, q, adj);
       while (o < D) {
         unsigned e = 0;
         bool fin = false;
@@ -390,7 +366,7 @@ __global__ void __launch_bounds__(D3Cfg<LARGE>::kW * 32) k_decode3(const uint8_t
           o++;
           q = s_i + (unsigned)o;
           c = 0;
-          if (o < D && q < s_n) rd.seek(ss, q, 0);
+          if (o < D && q < s_n) rd.seek(ss, q, adj);
         }
       }
 #ifdef PMZ_DEC3_PROFILE
@@ -433,8 +409,8 @@ __global__ void __launch_bounds__(D3Cfg<LARGE>::kW * 32) k_decode3(const uint8_t
     if (!okall || total != nsym || last != L) {
       if (lane == 0) set_err(st, !okall ? PMZ_ERR_INVALID_PREFIX : (total < nsym ? PMZ_ERR_TRUNCATED : PMZ_ERR_CORRUPT));
     } else if (cnt) {
-      D3Reader<D3Smem> rd;
-      rd.seek(ss, entry, 0);
+      D3Reader<D3Glob> rd;
+      rd.seek(ss, entry, adj);
       const unsigned e0 = incl - cnt + 1;  // raster index of the first symbol (anchor = 0)
       int r = (int)(e0 / (unsigned)C), c = (int)(e0 - (unsigned)r * C);
       int zr = r;

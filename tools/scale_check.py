@@ -1,0 +1,46 @@
+"""Compress/decompress throughput of the GraphedCompressor on a BASELINE
+config at full size (device-resident input, CUDA events).
+usage: python tools/scale_check.py C3 [eps]"""
+import sys
+import time
+
+import torch
+
+sys.path.insert(0, ".")
+import paper_2309_09778_b200 as P  # noqa: E402
+from paper_2309_09778_b200 import synthetic  # noqa: E402
+
+name = sys.argv[1]
+eps = float(sys.argv[2]) if len(sys.argv) > 2 else 1e-2
+t0 = time.time()
+x = synthetic.generate(name, device="cuda").contiguous()
+torch.cuda.synchronize()
+print(f"{name}: shape {tuple(x.shape)} ({x.numel() * 4 / 2**20:.0f} MiB) generated in {time.time() - t0:.1f}s")
+codec = P.Codec("cuda:0")
+cfg = P.CompressConfig(rel_error=eps, repair_factor=1.0)
+gc = P.GraphedCompressor(codec, cfg, x=x)
+flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+ms = []
+for i in range(6):
+    flush.fill_(i)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    gc.launch()
+    b.record()
+    buf, info = gc.result()
+    ms.append(a.elapsed_time(b))
+c = sorted(ms[1:])[len(ms[1:]) // 2]
+print(f"compress: {c:.3f} ms  {x.numel() * 4 / c / 1e6:.1f} GB/s  CR {info.nbytes / (x.numel() * 4):.4f}  m {info.m}")
+h = P.Codec.parse_header(buf.cpu().numpy())
+offs = torch.from_numpy(P.Codec.index_blocks(buf.cpu().numpy(), h).view("int64")).cuda()
+dms = []
+for i in range(4):
+    flush.fill_(i)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    y = codec.decompress_device(buf, h, offs)
+    b.record()
+    torch.cuda.synchronize()
+    dms.append(a.elapsed_time(b))
+d = sorted(dms[1:])[len(dms[1:]) // 2]
+print(f"decompress: {d:.3f} ms  {x.numel() * 4 / d / 1e6:.1f} GB/s")
