@@ -122,12 +122,36 @@ __global__ void __launch_bounds__(1024) k_dec_tables(const uint8_t *__restrict__
     int l0 = 0;
     for (int l = maxl; l >= 1; l--) if (cnt[l]) l0 = l;
     tab->l0 = l0;
-    // symbols in (length, code) order -- sequential, n <= 65536
-    for (int s = 0; s < n; s++) { int l = lens[s]; if (l && l <= 32) sym[fill[l]++] = (uint16_t)s; }
-    tab->zsym = l0 ? sym[tab->offset[l0]] : 0;
     tab->rcp[0] = tab->rcp[1] = 0;
     for (int l = 2; l < 34; l++) tab->rcp[l] = (unsigned)(0x100000000ull / (unsigned long long)l) + 1u;
   }
+  __syncthreads();
+  // symbols in (length, code) order: slot = offset[l] + rank of the symbol
+  // among equal-length symbols in index order (match_any ranks within a
+  // warp, per-(warp, length) counts scanned across warps, 1024 per round)
+  {
+    __shared__ unsigned s_wl[32][34];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int r0 = 0; r0 < n; r0 += blockDim.x) {
+      const int i = r0 + threadIdx.x;
+      const int l = i < n ? min((int)lens[i], 33) : 0;
+      const unsigned peers = __match_any_sync(0xffffffffu, l);
+      const unsigned rank = __popc(peers & ((1u << lane) - 1));
+      for (int q = lane; q < 34; q += 32) s_wl[wid][q] = 0;
+      __syncwarp();
+      if (rank == 0) s_wl[wid][l] = __popc(peers);
+      __syncthreads();
+      if (threadIdx.x < 34) {
+        unsigned acc = fill[threadIdx.x];
+        for (int w = 0; w < nw; w++) { const unsigned t = s_wl[w][threadIdx.x]; s_wl[w][threadIdx.x] = acc; acc += t; }
+        fill[threadIdx.x] = acc;
+      }
+      __syncthreads();
+      if (i < n && l >= 1 && l <= 32) sym[s_wl[wid][l] + rank] = (uint16_t)i;
+      __syncthreads();
+    }
+  }
+  if (threadIdx.x == 0) tab->zsym = tab->l0 ? sym[tab->offset[tab->l0]] : 0;
   __syncthreads();
   // LUT over the next kLutBits bits: (len << 16) | symbol; prefixes of longer
   // codewords point into a second-level table over the next sub_bits bits

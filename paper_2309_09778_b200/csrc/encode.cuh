@@ -78,15 +78,59 @@ __device__ long long g_cb_prof[8];
 #endif
 // Two-queue Huffman merge over sorted leaves keys[0..n) (weight = key >> 17):
 // internal node k gets weight I[k]; P[c] = parent of internal node c.  The
-// queue heads live in registers, refilled 3-4 picks ahead of their use.
+// queue heads live in registers.  Two bulk steps reproduce runs of identical
+// single steps in one go (large alphabets are mostly leaves floored at the
+// same weight):
+//   A. a run of r equal leaves not heavier than the internal head pairs off:
+//      floor(r/2) leaf+leaf merges (the new nodes are heavier, so the head and
+//      the tie rule stay the same throughout);
+//   B. a run of equal internal nodes strictly lighter than the next leaf
+//      pairs off (parents recorded).
+// Runs are found by binary search (both queues are nondecreasing).
 __device__ __forceinline__ void huff_merge(const unsigned long long *__restrict__ keys,
                                            unsigned long long *__restrict__ I, unsigned *__restrict__ P, int n) {
   const unsigned long long INF = ~0ull;
   auto leafw = [&](int i) -> unsigned long long { return i < n ? keys[i] >> 17 : INF; };
-  int li = 0, ii = 0;
-  unsigned long long l0 = leafw(0), l1 = leafw(1), l2 = leafw(2), l3 = leafw(3);
-  unsigned long long i0 = INF, i1 = INF, i2 = INF;
-  for (int k = 0; k < n - 1; k++) {
+  int li = 0, ii = 0, k = 0;
+  unsigned long long l0, l1, l2, l3, i0, i1, i2;
+  auto refresh = [&]() {
+    l0 = leafw(li); l1 = leafw(li + 1); l2 = leafw(li + 2); l3 = leafw(li + 3);
+    i0 = ii < k ? I[ii] : INF; i1 = ii + 1 < k ? I[ii + 1] : INF; i2 = ii + 2 < k ? I[ii + 2] : INF;
+  };
+  refresh();
+  while (k < n - 1) {
+    if (l0 == l1 && l1 != INF && l1 <= i0 && l3 == l0) {  // bulk A (runs >= 4)
+      int lo = li + 3, hi = n - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (leafw(mid) == l0) lo = mid; else hi = mid - 1;
+      }
+      const int nb = (lo - li + 1) >> 1;
+      const unsigned long long w = 2 * l0;
+      for (int j = 0; j < nb; j++) I[k + j] = w;
+      li += 2 * nb;
+      k += nb;
+      refresh();
+      continue;
+    }
+    if (i0 == i1 && i1 != INF && i1 < l0 && i2 == i0 && ii + 3 < k && I[ii + 3] == i0) {  // bulk B (runs >= 4)
+      int lo = ii + 3, hi = k - 1;
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (I[mid] == i0) lo = mid; else hi = mid - 1;
+      }
+      const int nb = (lo - ii + 1) >> 1;
+      const unsigned long long w = 2 * i0;
+      for (int j = 0; j < nb; j++) {
+        P[ii + 2 * j] = k + j;
+        P[ii + 2 * j + 1] = k + j;
+        I[k + j] = w;
+      }
+      ii += 2 * nb;
+      k += nb;
+      refresh();
+      continue;
+    }
     unsigned long long w = 0;
 #pragma unroll
     for (int pick = 0; pick < 2; pick++) {
@@ -105,6 +149,7 @@ __device__ __forceinline__ void huff_merge(const unsigned long long *__restrict_
     if (ii == k) i0 = w;
     else if (ii + 1 == k) i1 = w;
     else if (ii + 2 == k) i2 = w;
+    k++;
   }
   P[n - 2] = n - 2;  // root
 }
@@ -129,15 +174,45 @@ __global__ void __launch_bounds__(1024) k_codebook(const unsigned long long *his
   unsigned *P = in_smem ? reinterpret_cast<unsigned *>(sm + 2 * n) : g_P;
   CB_STAMP(0)
   const unsigned long long kval = hist[kMaxAlpha] > 0 ? hist[kMaxAlpha] : 1ull;
-  for (int s = tid; s < n; s += nt) {
-    unsigned long long f = hist[s];
-    if (f < kval) f = kval;
-    keys[s] = (f << 17) | (unsigned long long)s;
-  }
   if (tid < 64) s_cntI[tid] = 0;
+  // ---- 1. leaves in (frequency, symbol) order: every symbol at or below the
+  // floor k has weight k, the minimum, so those come first in index order;
+  // only the symbols above the floor need sorting ----
+  __shared__ unsigned s_wr[32][2], s_rb[2];
+  if (tid < 2) s_rb[tid] = 0;
+  // the real (above-floor) symbols are collected in a scratch array: the I
+  // region (free until the merge), or the shared buffer for large alphabets
+  unsigned long long *rk = in_smem ? I : sm;
+  const bool rk_fits = in_smem || n <= 2 * kCbSmemSyms;  // 160 KB of shared memory = 20480 keys
+  if (!rk_fits) rk = I;
+  __syncthreads();
+  for (int r0 = 0; r0 < n; r0 += nt) {
+    const int s = r0 + tid;
+    const unsigned long long f = s < n ? hist[s] : 0ull;
+    const bool real = s < n && f > kval;
+    const unsigned br = __ballot_sync(0xffffffffu, real), bf = __ballot_sync(0xffffffffu, s < n && !real);
+    if (lane == 0) { s_wr[wid][0] = __popc(br); s_wr[wid][1] = __popc(bf); }
+    __syncthreads();
+    if (tid < 2) {
+      unsigned acc = s_rb[tid];
+      for (int w = 0; w < nt / 32; w++) { const unsigned t = s_wr[w][tid]; s_wr[w][tid] = acc; acc += t; }
+      s_rb[tid] = acc;
+    }
+    __syncthreads();
+    const unsigned lt = (1u << lane) - 1;
+    if (real) rk[s_wr[wid][0] + __popc(br & lt)] = (f << 17) | (unsigned long long)s;
+    else if (s < n) keys[s_wr[wid][1] + __popc(bf & lt)] = (kval << 17) | (unsigned long long)s;
+    __syncthreads();
+  }
+  const int nr = (int)s_rb[0], nf = n - nr;
+  int np2 = 1;
+  while (np2 < nr) np2 <<= 1;
+  for (int i = nr + tid; i < np2; i += nt) rk[i] = ~0ull;
   __syncthreads();
   CB_STAMP(1)
-  bitonic_sort(keys, n);
+  if (nr > 1) bitonic_sort(rk, np2);
+  for (int i = tid; i < nr; i += nt) keys[nf + i] = rk[i];
+  __syncthreads();
   CB_STAMP(2)
   // ---- 2. two-queue merge (thread 0) ----
   if (tid == 0) {
