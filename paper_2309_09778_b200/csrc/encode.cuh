@@ -87,15 +87,17 @@ __device__ long long g_cb_prof[8];
 //   B. a run of equal internal nodes strictly lighter than the next leaf
 //      pairs off (parents recorded).
 // Runs are found by binary search (both queues are nondecreasing).
+template <class Wt>
 __device__ __forceinline__ void huff_merge(const unsigned long long *__restrict__ keys,
                                            unsigned long long *__restrict__ I, unsigned *__restrict__ P, int n) {
-  const unsigned long long INF = ~0ull;
-  auto leafw = [&](int i) -> unsigned long long { return i < n ? keys[i] >> 17 : INF; };
+  const Wt INF = (Wt)~0ull;
+  auto leafw = [&](int i) -> Wt { return i < n ? (Wt)(keys[i] >> 17) : INF; };
+  auto intw = [&](int i) -> Wt { return (Wt)I[i]; };
   int li = 0, ii = 0, k = 0;
-  unsigned long long l0, l1, l2, l3, i0, i1, i2;
+  Wt l0, l1, l2, l3, i0, i1, i2;
   auto refresh = [&]() {
     l0 = leafw(li); l1 = leafw(li + 1); l2 = leafw(li + 2); l3 = leafw(li + 3);
-    i0 = ii < k ? I[ii] : INF; i1 = ii + 1 < k ? I[ii + 1] : INF; i2 = ii + 2 < k ? I[ii + 2] : INF;
+    i0 = ii < k ? intw(ii) : INF; i1 = ii + 1 < k ? intw(ii + 1) : INF; i2 = ii + 2 < k ? intw(ii + 2) : INF;
   };
   refresh();
   while (k < n - 1) {
@@ -106,21 +108,21 @@ __device__ __forceinline__ void huff_merge(const unsigned long long *__restrict_
         if (leafw(mid) == l0) lo = mid; else hi = mid - 1;
       }
       const int nb = (lo - li + 1) >> 1;
-      const unsigned long long w = 2 * l0;
+      const unsigned long long w = 2ull * l0;
       for (int j = 0; j < nb; j++) I[k + j] = w;
       li += 2 * nb;
       k += nb;
       refresh();
       continue;
     }
-    if (i0 == i1 && i1 != INF && i1 < l0 && i2 == i0 && ii + 3 < k && I[ii + 3] == i0) {  // bulk B (runs >= 4)
+    if (i0 == i1 && i1 != INF && i1 < l0 && i2 == i0 && ii + 3 < k && intw(ii + 3) == i0) {  // bulk B (runs >= 4)
       int lo = ii + 3, hi = k - 1;
       while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
-        if (I[mid] == i0) lo = mid; else hi = mid - 1;
+        if (intw(mid) == i0) lo = mid; else hi = mid - 1;
       }
       const int nb = (lo - ii + 1) >> 1;
-      const unsigned long long w = 2 * i0;
+      const unsigned long long w = 2ull * i0;
       for (int j = 0; j < nb; j++) {
         P[ii + 2 * j] = k + j;
         P[ii + 2 * j + 1] = k + j;
@@ -131,21 +133,26 @@ __device__ __forceinline__ void huff_merge(const unsigned long long *__restrict_
       refresh();
       continue;
     }
-    unsigned long long w = 0;
+    Wt w = 0;
 #pragma unroll
     for (int pick = 0; pick < 2; pick++) {
       // internal only when strictly lighter (ties prefer the leaf); an
-      // exhausted internal queue reads INF
-      if (l0 <= i0) {
-        w += l0;
-        l0 = l1; l1 = l2; l2 = l3; l3 = leafw(li + 4); li++;
-      } else {
-        w += i0;
-        P[ii] = k;
-        i0 = i1; i1 = i2; i2 = (ii + 3 < k) ? I[ii + 3] : INF; ii++;
-      }
+      // exhausted internal queue reads INF.  Branch-free: both refill loads
+      // are unconditional (clamped in-bounds addresses, INF selected past
+      // the end), a leaf pick writes its parent slot to the unused P[n-1].
+      const bool tl = l0 <= i0;
+      const Wt lk = (Wt)(keys[min(li + 4, n - 1)] >> 17);
+      const Wt ik = intw(min(ii + 3, n - 1));
+      const Wt nl3 = li + 4 < n ? lk : INF;
+      const Wt ni2 = ii + 3 < k ? ik : INF;
+      w += tl ? l0 : i0;
+      P[tl ? n - 1 : ii] = (unsigned)k;
+      l0 = tl ? l1 : l0; l1 = tl ? l2 : l1; l2 = tl ? l3 : l2; l3 = tl ? nl3 : l3;
+      i0 = tl ? i0 : i1; i1 = tl ? i1 : i2; i2 = tl ? i2 : ni2;
+      li += tl ? 1 : 0;
+      ii += tl ? 0 : 1;
     }
-    I[k] = w;
+    I[k] = (unsigned long long)w;
     if (ii == k) i0 = w;
     else if (ii + 1 == k) i1 = w;
     else if (ii + 2 == k) i2 = w;
@@ -215,9 +222,27 @@ __global__ void __launch_bounds__(1024) k_codebook(const unsigned long long *his
   __syncthreads();
   CB_STAMP(2)
   // ---- 2. two-queue merge (thread 0) ----
+  // 32-bit weights when the total (the root weight) fits: every node weight
+  // is at most the total
+  __shared__ unsigned long long s_total;
+  if (tid == 0) s_total = 0;
+  __syncthreads();
+  {
+    unsigned long long part = 0;
+    for (int s2 = tid; s2 < n; s2 += nt) part += keys[s2] >> 17;
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    if (lane == 0) atomicAdd(&s_total, part);
+  }
+  __syncthreads();
+  const bool w32 = s_total < 0xffffffffull;
   if (tid == 0) {
-    if (in_smem) huff_merge(sm, sm + n, reinterpret_cast<unsigned *>(sm + 2 * n), n);
-    else huff_merge(g_keys, g_I, g_P, n);
+    if (in_smem) {
+      if (w32) huff_merge<unsigned>(sm, sm + n, reinterpret_cast<unsigned *>(sm + 2 * n), n);
+      else huff_merge<unsigned long long>(sm, sm + n, reinterpret_cast<unsigned *>(sm + 2 * n), n);
+    } else {
+      if (w32) huff_merge<unsigned>(g_keys, g_I, g_P, n);
+      else huff_merge<unsigned long long>(g_keys, g_I, g_P, n);
+    }
   }
   __syncthreads();
   CB_STAMP(3)

@@ -15,9 +15,15 @@ int main(int argc, char **argv) {
   pmz_geom g{(uint64_t)rows, (uint64_t)cols, 0, (uint64_t)rows};
   uint64_t wsb, cap; pmz_workspace_size(&p, &g, &wsb); pmz_max_container_size(&p, &g, &cap);
   void *ws; uint8_t *out; cudaMalloc(&ws, wsb); cudaMalloc(&out, cap);
-  int64_t *d_val; cudaMalloc(&d_val, 8);
+  // validation = every block (a realistic code histogram for the codebook)
+  const int64_t nb = ((rows + 255) / 256) * ((cols + 255) / 256);
+  std::vector<int64_t> hv(nb);
+  for (int64_t i = 0; i < nb; i++) hv[i] = i;
+  int64_t *d_val; cudaMalloc(&d_val, 8 * nb); cudaMemcpy(d_val, hv.data(), 8 * nb, cudaMemcpyHostToDevice);
+  p.m = 0;
   pmz_result res;
-  for (int it = 0; it < 3; it++) printf("compress %d\n", pmz_compress(d_in, &g, &p, d_val, 0, out, cap, nullptr, ws, wsb, 0, &res));
+  for (int it = 0; it < 3; it++) printf("compress %d\n", pmz_compress(d_in, &g, &p, d_val, nb, out, cap, nullptr, ws, wsb, 0, &res));
+  printf("m %d\n", res.m);
   Geom G = geom_of(&p, &g);
   std::vector<long long> pr(65536 * 8);
   cudaMemcpyFromSymbol(pr.data(), g_cmp_prof, 8 * 65536 * 8);
