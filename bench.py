@@ -92,9 +92,11 @@ class ClockSampler:
 
 
 def c2_field(device):
-    import torch
+    """The C2 field, generated on the host (the CPU generator) and copied to
+    `device`: both bench arms (this one and --impl reference) compress the
+    identical field."""
     from paper_2309_09778_b200 import synthetic
-    return synthetic.generate("C2", device=device)
+    return synthetic.generate("C2").to(device)
 
 
 def cpu_reference_time(x: np.ndarray, eps: float, repair: float, reps: int, threads: int):
