@@ -354,6 +354,63 @@ class GraphedCompressor:
         return self.result()
 
 
+class PipelinedCompressor:
+    """Streaming compression of a sequence of same-shaped fields with several
+    in flight: ``depth`` slots, each with its own CUDA stream, device input,
+    workspace, output and captured pipeline (GraphedCompressor).  ``submit``
+    enqueues the host->device copy of the field (from pinned host memory) and
+    the graph replay on the next slot's stream; ``collect`` returns the oldest
+    result: the status read-back, then a device->host copy of exactly the
+    container bytes into pinned memory.  While one slot's result is read, the
+    other slots' copies and kernels proceed, so the PCIe transfers (full
+    duplex) overlap the compute of neighbouring fields."""
+
+    def __init__(self, codec: Codec, cfg: CompressConfig, shape, depth: int = 3):
+        if depth < 1:
+            raise ConfigError("depth must be >= 1")
+        self.codec, self.cfg, self.depth = codec, cfg, depth
+        self.slots = []
+        for _ in range(depth):
+            stream = torch.cuda.Stream(codec.device)
+            with torch.cuda.stream(stream):
+                x = torch.empty(tuple(shape), dtype=torch.float32, device=codec.device)
+                x.zero_()
+                gc = GraphedCompressor(codec, cfg, x=x)
+                host_out = torch.empty(max(int(gc.out.numel()), 1), dtype=torch.uint8, pin_memory=True)
+            self.slots.append({"stream": stream, "gc": gc, "x": x, "host_out": host_out, "busy": False,
+                               "done": torch.cuda.Event()})
+        self._next = 0
+        self._queue = []  # slot indices in submission order
+
+    def submit(self, host_field: torch.Tensor):
+        """Enqueue one field (a float32 CPU tensor, pinned for an asynchronous
+        copy).  Blocks only when every slot is in flight (collect first)."""
+        if len(self._queue) == self.depth:
+            raise ConfigError("all slots in flight: collect() before submitting more")
+        i = self._next
+        self._next = (i + 1) % self.depth
+        sl = self.slots[i]
+        with torch.cuda.stream(sl["stream"]):
+            sl["x"].copy_(host_field, non_blocking=True)
+            sl["gc"].launch()
+        self._queue.append(i)
+        return i
+
+    def collect(self):
+        """(container bytes as a pinned uint8 CPU view, CompressInfo) of the
+        oldest submitted field."""
+        if not self._queue:
+            raise ConfigError("nothing submitted")
+        i = self._queue.pop(0)
+        sl = self.slots[i]
+        with torch.cuda.stream(sl["stream"]):
+            buf, info = sl["gc"].result()      # synchronises this slot's stream
+            sl["host_out"][: info.nbytes].copy_(buf, non_blocking=True)
+            sl["done"].record(sl["stream"])
+        sl["done"].synchronize()
+        return sl["host_out"][: info.nbytes], info
+
+
 def _codec(device=None) -> Codec:
     dev = _require_cuda(device)
     key = str(dev)

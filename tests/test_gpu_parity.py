@@ -229,3 +229,29 @@ def test_decoder_tiny_partitions(codec, oracle):
     segments and codewords spanning several lane segments."""
     x = _field("C2", (64, 96))
     _parity(codec, oracle, x, b_r=1e-2, repair_factor=1.0, block_rows=16, block_cols=8, partition_rows=2)
+
+
+def test_pipelined_and_graphed_match_one_shot(codec):
+    """GraphedCompressor and PipelinedCompressor (several fields in flight)
+    return exactly the containers of the one-shot path, in submission order."""
+    import paper_2309_09778_b200 as P
+    cfg = P.CompressConfig(rel_error=1e-2, repair_factor=1.0)
+    fields = [_field("C2", (300, 520)) * s for s in (1.0, -2.0, 0.5, 3.0)]
+    ref = [codec.compress_device(torch.from_numpy(np.ascontiguousarray(f)).cuda(), cfg)[0].cpu().numpy().tobytes()
+           for f in fields]
+    xg = torch.from_numpy(np.ascontiguousarray(fields[0])).cuda()
+    g = P.GraphedCompressor(codec, cfg, x=xg)
+    for f, r in zip(fields, ref):
+        xg.copy_(torch.from_numpy(np.ascontiguousarray(f)))
+        buf, _ = g.run()
+        assert buf.cpu().numpy().tobytes() == r
+    pc = P.PipelinedCompressor(codec, cfg, fields[0].shape, depth=3)
+    hosts = [torch.from_numpy(np.ascontiguousarray(f)).pin_memory() for f in fields]
+    out = []
+    for h in hosts[:3]:
+        pc.submit(h)
+    out.append(pc.collect()[0].numpy().tobytes())
+    pc.submit(hosts[3])
+    for _ in range(3):
+        out.append(pc.collect()[0].numpy().tobytes())
+    assert out == ref
