@@ -532,7 +532,7 @@ int pmz_index_blocks(const uint8_t *h, uint64_t n, const pmz_header *hd, uint64_
 namespace {
 struct DecLayout {
   size_t status, blkp, part_bits, part_off, part_zeros, anchors, bal_off, pay_off, blk_nbal, tab, sym, lut, codes,
-      zrow, large, total;
+      zrow, large, vh, total;
 };
 DecLayout dec_layout(const Geom &g) {
   DecLayout L{};
@@ -557,6 +557,7 @@ DecLayout dec_layout(const Geom &g) {
   L.codes = take(2 * (size_t)g.nparts * (size_t)g.nct * kTile);  // partition-tiled
   L.zrow = take(2 * 32 * (size_t)(g.nparts + 1));                  // code-0 count per partition row
   L.large = take(4 * (size_t)(g.nparts + 1));                      // work list of long substreams
+  L.vh = take(8 * (size_t)g.nparts * (size_t)g.nct * kTile);        // reconstructed values, tiled
   L.total = o;
   return L;
 }
@@ -568,7 +569,9 @@ int launch_recon(const KParams &k, unsigned grid, cudaStream_t st, const uint8_t
       d_buf, G, k, m, at<BlkP>(d_ws, L.blkp), at<uint16_t>(d_ws, L.codes), at<uint16_t>(d_ws, L.zrow),
       at<double>(d_ws, L.anchors), at<unsigned long long>(d_ws, L.part_zeros),
       at<unsigned long long>(d_ws, L.bal_off), at<unsigned long long>(d_ws, L.blk_nbal), d_out,
-      at<WsStatus>(d_ws, L.status));
+      at<double>(d_ws, L.vh), at<WsStatus>(d_ws, L.status));
+  k_inv<<<(unsigned)G.nparts, 256, 0, st>>>(G, at<BlkP>(d_ws, L.blkp), at<double>(d_ws, L.vh), d_out,
+                                            at<WsStatus>(d_ws, L.status));
   return PMZ_OK;
 }
 

@@ -257,6 +257,7 @@ __device__ __noinline__ dd exp2_dd(double y, int &n) {
 
 // CR64(2^y) as a double (slow path).
 __device__ __noinline__ double pmz_exp2_cr(double y, unsigned *amb) {
+  if (y != y) return y;  // NaN: no table index is ever formed from it
   if (y >= 1024.0) return __longlong_as_double(0x7ff0000000000000LL);
   if (y < -1080.0) return 0.0;
   int n;

@@ -49,7 +49,8 @@ __global__ void __launch_bounds__(kPPC * 64) k_reconstruct3(const uint8_t *__res
                                                             const unsigned long long *__restrict__ part_zeros,
                                                             const unsigned long long *__restrict__ bal_off,
                                                             const unsigned long long *__restrict__ blk_nbal,
-                                                            float *__restrict__ out, WsStatus *st) {
+                                                            float *__restrict__ out, double *__restrict__ vh,
+                                                            WsStatus *st) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   count_launch(st);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -88,7 +89,6 @@ __global__ void __launch_bounds__(kPPC * 64) k_reconstruct3(const uint8_t *__res
 
   if (role == 0) {
     // ------------------------------ producer ------------------------------
-    unsigned *amb = &st->unresolved;
     const uint8_t *bal = buf + bal_off[b];
     // balance index of the next code-0 of every row (warp-uniform registers):
     // partition base + zeros of the rows above (the decoder's per-row counts)
@@ -104,16 +104,20 @@ __global__ void __launch_bounds__(kPPC * 64) k_reconstruct3(const uint8_t *__res
 #pragma unroll
       for (int r = 0; r < 32; r++) rb[r] = __shfl_sync(0xffffffffu, excl, r);
     }
+    // a finished chunk: its reconstructed tile goes out with one bulk store
+    // (the inverse map runs in k_inv at full occupancy)
     auto flush = [&](int chunk) {
-      const int s = chunk % kSlots, c = chunk * 32 + lane;
-      if (c < C)
-        for (int r = 0; r < R; r++) opart[(int64_t)r * g.cols + c] = inv_f32(W.val[s][r * 32 + lane], P, amb);
+      if (lane == 0) {
+        bulk_s2g(vh + tile_base(g, p, chunk), W.val[chunk % kSlots], kTile * 8);
+        bulk_commit();
+      }
     };
     for (int kc = 0; kc < nch; kc++) {
       const int s = kc % kSlots;
       if (kc >= kSlots) {
         bar_sync_n(bar0 + kSlots + s, 64);
         flush(kc - kSlots);
+        if (lane == 0) bulk_wait_read0();  // the store has read the slot
         __syncwarp();
       }
       const bool inb = kc * 32 + lane < C;
@@ -136,6 +140,7 @@ __global__ void __launch_bounds__(kPPC * 64) k_reconstruct3(const uint8_t *__res
       bar_sync_n(bar0 + kSlots + kc % kSlots, 64);
       flush(kc);
     }
+    if (lane == 0) bulk_wait0();
   } else {
     // ------------------------------ consumer ------------------------------
     const double anc = anchors[p];
@@ -181,13 +186,54 @@ __global__ void __launch_bounds__(kPPC * 64) k_reconstruct3(const uint8_t *__res
         cur = nxt;
       }
       if (kg >= 1 && kg - 1 < nch) {
+        fence_proxy_async();  // reconstructed values (generic writes) before the bulk store
         __syncwarp();
         bar_arrive_n(bar0 + kSlots + (kg - 1) % kSlots, 64);
       }
     }
     if (ngroups == nch) {
+      fence_proxy_async();
       __syncwarp();
       bar_arrive_n(bar0 + kSlots + (nch - 1) % kSlots, 64);
+    }
+  }
+}
+
+// inverse_map (transform.py:188-202) + f32 cast (D20) of the reconstructed
+// tiles, one CTA per partition, a thread per 4-column quad (as k_fwd): the
+// FP64 exp2 work at full occupancy, coalesced 16-byte output stores.
+__global__ void __launch_bounds__(256) k_inv(Geom g, const BlkP *__restrict__ blkp,
+                                             const double *__restrict__ vh, float *__restrict__ out,
+                                             WsStatus *st) {
+  count_launch(st);
+  const int64_t p = blockIdx.x;
+  int64_t b;
+  int pi;
+  part_of(g, p, b, pi);
+  const BlkP P = blkp[b];
+  if (P.trivial) return;  // written by the reconstruct kernel
+  const BlockBox bb = block_box(g, b);
+  const int pr0 = pi * g.prow, R = min(g.prow, bb.br - pr0), C = bb.bc, nch = (C + 31) >> 5;
+  float *op = out + (bb.r0 + pr0) * g.cols + bb.c0;
+  const bool vec = ((g.cols & 3) == 0) && ((bb.c0 & 3) == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
+  const double *vt = vh + tile_base(g, p, 0);
+  unsigned *amb = &st->unresolved;
+  for (int i = threadIdx.x; i < nch * 256; i += 256) {
+    const int kc = i >> 8, r = (i >> 3) & 31, c0 = kc * 32 + (i & 7) * 4;
+    if (r >= R || c0 >= C) continue;
+    const double2 *q = reinterpret_cast<const double2 *>(vt + kc * kTile + r * 32 + (c0 & 31));
+    const double2 a0 = __ldg(q), a1 = __ldg(q + 1);
+    const double v[4] = {a0.x, a0.y, a1.x, a1.y};
+    float y[4];
+#pragma unroll
+    for (int u = 0; u < 4; u++) y[u] = c0 + u < C ? inv_f32(v[u], P, amb) : 0.0f;  // padding columns hold garbage
+    float *dst = op + (int64_t)r * g.cols + c0;
+    if (vec && c0 + 3 < C) {
+      *reinterpret_cast<float4 *>(dst) = make_float4(y[0], y[1], y[2], y[3]);
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; u++)
+        if (c0 + u < C) dst[u] = y[u];
     }
   }
 }

@@ -21,8 +21,11 @@
 
 namespace pmz {
 
+#ifndef PMZ_WS_SLOTS
+#define PMZ_WS_SLOTS 3
+#endif
 constexpr int kPPC = 2;      // partitions (warp pairs) per CTA
-constexpr int kSlots = 3;    // ring depth
+constexpr int kSlots = PMZ_WS_SLOTS;    // ring depth
 constexpr uint16_t kAnc = 0xFFFF;
 
 struct alignas(128) PRing {
