@@ -626,14 +626,13 @@ int pmz_decompress(const uint8_t *d_buf, uint64_t n, const pmz_header *hdr, doub
     CK(cudaMemsetAsync(at<unsigned>(d_ws, L.large), 0, 4, st));
     CK(cudaFuncSetAttribute(k_decode3<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d3_smem<false>()));
     CK(cudaFuncSetAttribute(k_decode3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d3_smem<true>()));
-    k_decode3<false><<<(unsigned)((G.nparts + D3Cfg<false>::kW - 1) / D3Cfg<false>::kW), D3Cfg<false>::kW * 32,
-                       d3_smem<false>(), st>>>(
+    k_decode3<false><<<(unsigned)G.nparts, kD3Nl, d3_smem<false>(), st>>>(
         d_buf, n, G, at<BlkP>(d_ws, L.blkp), at<DecTab>(d_ws, L.tab), at<uint16_t>(d_ws, L.sym),
         at<unsigned>(d_ws, L.lut), at<unsigned long long>(d_ws, L.part_bits),
         at<unsigned long long>(d_ws, L.part_off), at<unsigned long long>(d_ws, L.pay_off),
         at<uint16_t>(d_ws, L.codes), at<unsigned long long>(d_ws, L.part_zeros), at<uint16_t>(d_ws, L.zrow),
         at<unsigned>(d_ws, L.large), S);
-    k_decode3<true><<<(unsigned)G.nparts, 32, d3_smem<true>(), st>>>(
+    k_decode3<true><<<(unsigned)G.nparts, kD3Nl, d3_smem<true>(), st>>>(
         d_buf, n, G, at<BlkP>(d_ws, L.blkp), at<DecTab>(d_ws, L.tab), at<uint16_t>(d_ws, L.sym),
         at<unsigned>(d_ws, L.lut), at<unsigned long long>(d_ws, L.part_bits),
         at<unsigned long long>(d_ws, L.part_off), at<unsigned long long>(d_ws, L.pay_off),

@@ -28,35 +28,36 @@
 namespace pmz {
 
 constexpr unsigned kD3Bad = 0xffffffffu;
-#ifndef PMZ_D3W
-#define PMZ_D3W 2
+#ifndef PMZ_D3_WPP
+#define PMZ_D3_WPP 2
 #endif
+constexpr int kD3Wpp = PMZ_D3_WPP;  // warps per partition
+constexpr int kD3Nl = 32 * kD3Wpp;  // lane segments per partition
 
-// The substream is read straight from global memory (the reader prefetches
-// one word ahead, so the load is off the dependency chain) and the decode
-// tables through L1; the per-partition shared state is the boundary bitmap.
+// One CTA per partition, kD3Nl lanes = segments.  The substream is read
+// straight from global memory (the reader prefetches one word ahead, so the
+// load is off the dependency chain) and the decode tables through L1; the
+// shared state is the boundary bitmap plus the per-lane fallback tables.
 // LARGE = false: substreams up to 16 KB; longer ones go to a work list
 // served by the LARGE launch (32 KB = the longest valid substream, 8191
 // codewords x 32 bits).
 template <bool LARGE>
 struct D3Cfg {
-  static constexpr int kW = LARGE ? 1 : PMZ_D3W;
   static constexpr int kBm = LARGE ? 8192 + 4 : 4096 + 4;  // boundary-bitmap words (substream <= 32 kBm bits)
 };
 template <bool LARGE>
-struct D3Warp {
+struct D3Part {
   unsigned bm[D3Cfg<LARGE>::kBm];
-  unsigned xs[32];               // speculative exit per lane
-  unsigned ns[32];               // speculative symbol count per lane
-  unsigned ent[33], cnt[32];     // chained true entries / counts (fallback)
-  unsigned E[32][32];            // fallback: exit per lane per entry offset
-  uint16_t Cn[32][32];           // fallback: symbol count per lane per entry offset
-  uint16_t vis[32][64];          // fallback: (path + 1) << 10 | symbols before s_t + i
+  unsigned xs[kD3Nl], ns[kD3Nl];        // speculative exit / symbol count per lane
+  unsigned ex[kD3Nl], ent[kD3Nl + 1], cnt[kD3Nl];
+  uint16_t E[kD3Nl][32];                // fallback: exit - s_t per entry offset (0xffff: bad)
+  uint16_t Cn[kD3Nl][32];               // fallback: symbol count per entry offset
+  uint16_t vis[kD3Nl][64];              // fallback: (path + 1) << 10 | symbols before s_t + i
   unsigned zrow[32];
-  int err;
+  unsigned wsum[kD3Wpp];
 };
 template <bool LARGE>
-constexpr size_t d3_smem() { return sizeof(D3Warp<LARGE>) * D3Cfg<LARGE>::kW; }
+constexpr size_t d3_smem() { return sizeof(D3Part<LARGE>); }
 
 // Big-endian words of the substream, straight from the container: word i
 // covers stream bits [32 i - adj, 32 i + 32 - adj) of an aligned base.
@@ -129,324 +130,304 @@ __device__ __forceinline__ bool d3_run(unsigned long long buf, int nb, unsigned 
 }
 
 
-#ifdef PMZ_DEC3_PROFILE
-__device__ long long g_d3[65536][8];  // t0, t_spec, t_fix, t_write, rounds, L, nsym, large
-__device__ long long g_d3n[65536][3];  // max-lane iterations: spec, fix (all rounds), stage-end stamp
-#define D3_STAMP(i) if (lane == 0 && p < 65536) g_d3[p][i] = clock64();
-#else
-#define D3_STAMP(i)
-#endif
 template <bool LARGE>
-__global__ void __launch_bounds__(D3Cfg<LARGE>::kW * 32) k_decode3(const uint8_t *__restrict__ buf, unsigned long long buf_n,
-                                                      Geom g, const BlkP *__restrict__ blkp,
-                                                      const DecTab *__restrict__ tab,
-                                                      const uint16_t *__restrict__ sym,
-                                                      const unsigned *__restrict__ lut,
-                                                      const unsigned long long *__restrict__ part_bits,
-                                                      const unsigned long long *__restrict__ part_off,
-                                                      const unsigned long long *__restrict__ pay_off,
-                                                      uint16_t *__restrict__ codes,
-                                                      unsigned long long *__restrict__ part_zeros,
-                                                      uint16_t *__restrict__ zrow_out, unsigned *large_list,
-                                                      WsStatus *st) {
-  constexpr int kW = D3Cfg<LARGE>::kW, kBm = D3Cfg<LARGE>::kBm;
+__global__ void __launch_bounds__(kD3Nl) k_decode3(const uint8_t *__restrict__ buf, unsigned long long buf_n,
+                                                  Geom g, const BlkP *__restrict__ blkp,
+                                                  const DecTab *__restrict__ tab,
+                                                  const uint16_t *__restrict__ sym,
+                                                  const unsigned *__restrict__ lut,
+                                                  const unsigned long long *__restrict__ part_bits,
+                                                  const unsigned long long *__restrict__ part_off,
+                                                  const unsigned long long *__restrict__ pay_off,
+                                                  uint16_t *__restrict__ codes,
+                                                  unsigned long long *__restrict__ part_zeros,
+                                                  uint16_t *__restrict__ zrow_out, unsigned *large_list,
+                                                  WsStatus *st) {
+  constexpr int NL = kD3Nl, kBm = D3Cfg<LARGE>::kBm;
   __shared__ unsigned long long s_rep[33];
   __shared__ DecTab s_tab;
   extern __shared__ __align__(16) unsigned char dyn3[];
+  D3Part<LARGE> &W = *reinterpret_cast<D3Part<LARGE> *>(dyn3);
   count_launch(st);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (LARGE && (int64_t)blockIdx.x * kW >= (int64_t)large_list[0]) return;
-  if (threadIdx.x == 0) s_tab = *tab;
-  if (threadIdx.x <= 32) {  // s_rep[l]: bits 0, l, 2l, ... (boundaries of a run, LSB first)
-    unsigned long long r = 0;
-    if (threadIdx.x >= 1)
-      for (int q = 0; q < 64; q += threadIdx.x) r |= 1ull << q;
-    s_rep[threadIdx.x] = r;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  int64_t p;
+  if (LARGE) {
+    if (blockIdx.x >= large_list[0]) return;
+    p = large_list[1 + blockIdx.x];
+  } else {
+    p = blockIdx.x;
   }
+  if (t == 0) s_tab = *tab;
+  if (t <= 32) {  // s_rep[l]: bits 0, l, 2l, ... (boundaries of a run, LSB first)
+    unsigned long long r = 0;
+    if (t >= 1)
+      for (int q = 0; q < 64; q += t) r |= 1ull << q;
+    s_rep[t] = r;
+  }
+  if (t < 32) W.zrow[t] = 0;
   __syncthreads();
   const unsigned *s_lut = lut, *lut2 = lut + (1 << kLutBits);  // through L1
-  D3Warp<LARGE> &W = reinterpret_cast<D3Warp<LARGE> *>(dyn3)[warp];
-  const int64_t nwork = LARGE ? (int64_t)large_list[0] : g.nparts;
-  for (int64_t item = (int64_t)blockIdx.x * kW + warp; item < nwork; item += (int64_t)gridDim.x * kW) {
-  const int64_t p = LARGE ? (int64_t)large_list[1 + item] : item;
   int64_t b;
   int pi;
   part_of(g, p, b, pi);
   if (blkp[b].trivial) {
-    if (lane == 0) part_zeros[p] = 0;
-    zrow_out[p * 32 + lane] = 0;
-    continue;
+    if (t == 0) part_zeros[p] = 0;
+    if (t < 32) zrow_out[p * 32 + t] = 0;
+    return;
   }
   const BlockBox bb = block_box(g, b);
   const int R = min(g.prow, bb.br - pi * g.prow), C = bb.bc;
   const unsigned nsym = (unsigned)(R * C - 1);
   const unsigned long long L64 = part_bits[p];
+  if (L64 > 0xffffff00ull || ((L64 + 31) >> 5) + 4 > (unsigned long long)kBm) {
+    if (t == 0) {
+      if (!LARGE && L64 <= 32ull * (nsym + 1)) large_list[1 + atomicAdd(&large_list[0], 1u)] = (unsigned)p;
+      else set_err(st, PMZ_ERR_CORRUPT);  // longer than any valid substream (codewords <= 32 bits)
+    }
+    return;
+  }
+  const unsigned L = (unsigned)L64;
   const uint8_t *src = buf + pay_off[b] + part_off[p];
   uint16_t *ct = codes + tile_base(g, p, 0);
-  W.zrow[lane] = 0;
-  if (lane == 0) W.err = 0;
-  unsigned zeros = 0;
-  if (L64 > 0xffffff00ull || ((L64 + 31) >> 5) + 4 > (unsigned long long)kBm) {
-    if (!LARGE && L64 <= 32ull * (nsym + 1)) {
-      if (lane == 0) large_list[1 + atomicAdd(&large_list[0], 1u)] = (unsigned)p;
-      continue;
+  BitSrc bsrc;
+  {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(src);
+    bsrc.base = reinterpret_cast<const uint8_t *>(a & ~(uintptr_t)3);
+    bsrc.adj = (unsigned)(8 * (a & 3));
+    bsrc.nbits = L64;
+    bsrc.end = buf + buf_n;
+  }
+  const D3Glob ss{bsrc};
+  const unsigned adj = bsrc.adj;
+  const unsigned segw = (((L + 31) >> 5) + NL - 1) / NL;  // words per lane segment
+  const unsigned s_i = min(L, 32 * segw * t), s_n = min(L, 32 * segw * (t + 1));
+
+  // ---- 1. speculative pass: every codeword boundary of the lane's segment
+  // goes into the bitmap (a run of k codewords as one periodic mask), the
+  // symbol count into ns ----
+  {
+    const unsigned w0 = s_i >> 5, wend = (s_n + 31) >> 5;
+    for (unsigned q = w0; q < wend; q++) W.bm[q] = 0;
+    D3Reader<D3Glob> rd;
+    rd.seek(ss, s_i, adj);
+    unsigned pos = s_i, nsp = 0;
+    bool bad = false;
+    while (pos < s_n) {
+      rd.refill(ss);
+      int s, l;
+      unsigned k;
+      if (!d3_run(rd.buf, rd.nb, s_n - pos, s_lut, lut2, s_tab, sym, s, l, k)) { bad = true; break; }
+      const unsigned adv = k * (unsigned)l;  // codewords starting before s_n
+      const unsigned long long m = k == 1 ? 1ull : (s_rep[l] & ((1ull << ((k - 1) * l + 1)) - 1ull));
+      const unsigned off = pos & 31, wq = pos >> 5;
+      W.bm[wq] |= (unsigned)(m << off);
+      const unsigned long long hi = off ? (m >> (32 - off)) : (m >> 32);
+      if (hi) {
+        W.bm[wq + 1] |= (unsigned)hi;
+        if (hi >> 32) W.bm[wq + 2] |= (unsigned)(hi >> 32);
+      }
+      rd.skip(adv);
+      pos += adv;
+      nsp += k;
     }
-    // longer than any valid substream (codewords <= 32 bits)
-    if (lane == 0) set_err(st, PMZ_ERR_CORRUPT);
-    continue;
+    W.xs[t] = bad ? kD3Bad : pos;
+    W.ns[t] = nsp;
+  }
+  __syncthreads();
+  // speculative boundaries of [s_i, q): symbols of the speculative path before q
+  auto rank = [&](unsigned q) -> unsigned {
+    unsigned r = 0;
+    const unsigned wa = s_i >> 5, wb = q >> 5;
+    for (unsigned w = wa; w < wb; w++) r += __popc(W.bm[w]);
+    return r + __popc(W.bm[wb] & ((1u << (q & 31)) - 1u));
+  };
+
+  // ---- 2. true exits.  Optimistic round: each lane re-decodes from its
+  // assumed entry (the previous lane's speculative exit) until it lands on
+  // a speculative boundary of its own (then its exit is x_t) or crosses s_n ----
+  unsigned entry = t == 0 ? 0u : W.xs[t - 1];
+  unsigned ex, cnt = 0;
+  if (entry == kD3Bad) {
+    ex = kD3Bad;
+  } else if (entry >= s_n) {  // no codeword starts in this segment
+    ex = entry;
   } else {
-    const unsigned L = (unsigned)L64;
-    D3_STAMP(0)
-#ifdef PMZ_DEC3_PROFILE
-    if (lane == 0 && p < 65536) { g_d3[p][5] = L; g_d3[p][6] = nsym; g_d3[p][7] = LARGE; g_d3n[p][2] = clock64(); }
-#endif
-    BitSrc bsrc;
-    {
-      const uintptr_t a = reinterpret_cast<uintptr_t>(src);
-      bsrc.base = reinterpret_cast<const uint8_t *>(a & ~(uintptr_t)3);
-      bsrc.adj = (unsigned)(8 * (a & 3));
-      bsrc.nbits = L64;
-      bsrc.end = buf + buf_n;
-    }
-    const D3Glob ss{bsrc};
-    const unsigned adj = bsrc.adj;
-    const unsigned segw = (((L + 31) >> 5) + 31) >> 5;  // words per lane segment
-    const unsigned s_i = min(L, 32 * segw * lane), s_n = min(L, 32 * segw * (lane + 1));
-    // ---- 1. speculative pass: every codeword boundary of the lane's
-    // segment goes into the bitmap (a run of k codewords as one periodic
-    // mask), the symbol count into ns ----
-    unsigned xs = s_i, nsp = 0;
-    {
-      const unsigned w0 = s_i >> 5, wend = (s_n + 31) >> 5;
-      for (unsigned q = w0; q < wend; q++) W.bm[q] = 0;
-      D3Reader<D3Glob> rd;
-      rd.seek(ss, s_i, adj);
-      unsigned pos = s_i;
-      bool bad = false;
-#ifdef PMZ_DEC3_PROFILE
-      unsigned it_spec = 0;
-#endif
-      while (pos < s_n) {
-#ifdef PMZ_DEC3_PROFILE
-        it_spec++;
-#endif
-        rd.refill(ss);
-        int s, l;
-        unsigned k;
-        if (!d3_run(rd.buf, rd.nb, s_n - pos, s_lut, lut2, s_tab, sym, s, l, k)) { bad = true; break; }
-        const unsigned adv = k * (unsigned)l;  // codewords starting before s_n
-        // boundaries pos + j l, j < k: LSB-first mask shifted to pos's word
-        const unsigned long long m = k == 1 ? 1ull : (s_rep[l] & ((1ull << ((k - 1) * l + 1)) - 1ull));
-        const unsigned off = pos & 31, wq = pos >> 5;
-        W.bm[wq] |= (unsigned)(m << off);
-        const unsigned long long hi = off ? (m >> (32 - off)) : (m >> 32);
-        if (hi) {
-          W.bm[wq + 1] |= (unsigned)hi;
-          if (hi >> 32) W.bm[wq + 2] |= (unsigned)(hi >> 32);
-        }
-        rd.skip(adv);
-        pos += adv;
-        nsp += k;
+    D3Reader<D3Glob> rd;
+    rd.seek(ss, entry, adj);
+    unsigned pos = entry, c = 0;
+    ex = kD3Bad;
+    bool done = false;
+    while (pos < s_n) {
+      if ((W.bm[pos >> 5] >> (pos & 31)) & 1u) {
+        cnt = c + W.ns[t] - rank(pos);
+        ex = W.xs[t];
+        done = true;
+        break;
       }
-      xs = bad ? kD3Bad : pos;
-#ifdef PMZ_DEC3_PROFILE
-      unsigned mx = it_spec;
-      for (int d = 16; d > 0; d >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, d));
-      if (lane == 0 && p < 65536) g_d3n[p][0] = mx;
-#endif
+      rd.refill(ss);
+      int s, l;
+      unsigned k;
+      if (!d3_run(rd.buf, rd.nb, s_n - pos, s_lut, lut2, s_tab, sym, s, l, k)) { done = true; break; }
+      const unsigned adv = k * (unsigned)l;
+      rd.skip(adv);
+      pos += adv;
+      c += k;
     }
-    W.xs[lane] = xs;
-    W.ns[lane] = nsp;
-    __syncwarp();
-    // speculative boundaries of [s_i, q): symbols of the speculative path before q
-    auto rank = [&](unsigned q) -> unsigned {
-      unsigned r = 0;
-      const unsigned wa = s_i >> 5, wb = q >> 5;
-      for (unsigned w = wa; w < wb; w++) r += __popc(W.bm[w]);
-      return r + __popc(W.bm[wb] & ((1u << (q & 31)) - 1u));
-    };
-    D3_STAMP(1)
-    // ---- 2. true exits.  Optimistic round: each lane re-decodes from its
-    // assumed entry (the previous lane's speculative exit) until it lands on
-    // its own speculative path (then its exit is x_t) or crosses s_n. ----
-    unsigned entry = lane == 0 ? 0u : W.xs[lane - 1];
-    // decode from `from` until landing on a speculative boundary (then the
-    // rest is the speculative parse) or crossing s_n; returns the exit and
-    // the symbol count of [from, exit)
-    auto walk = [&](unsigned from, unsigned &cnt) -> unsigned {
-      D3Reader<D3Glob> rd;
-      rd.seek(ss, from, adj);
-      unsigned pos = from, c = 0;
-      while (pos < s_n) {
-        if ((W.bm[pos >> 5] >> (pos & 31)) & 1u) {
-          cnt = c + W.ns[lane] - rank(pos);
-          return W.xs[lane];
-        }
-        rd.refill(ss);
-        int s, l;
-        unsigned k;
-        if (!d3_run(rd.buf, rd.nb, s_n - pos, s_lut, lut2, s_tab, sym, s, l, k)) return kD3Bad;
-        const unsigned adv = k * (unsigned)l;
-        rd.skip(adv);
-        pos += adv;
-        c += k;
-      }
+    if (!done) {
+      ex = pos;
       cnt = c;
-      return pos;
-    };
-    unsigned ex, cnt = 0;
-    ex = entry == kD3Bad ? kD3Bad : (entry >= s_n ? entry : walk(entry, cnt));
-    const unsigned nent = __shfl_up_sync(0xffffffffu, ex, 1);
-    if (__any_sync(0xffffffffu, lane > 0 && nent != entry)) {
-      // ---- fallback: transfer function of every lane over all entry offsets
-      // [0, D) (the true entry is the first boundary >= s_t, < s_t + maxl);
-      // paths merge into the speculative path (bitmap) or into an earlier
-      // offset's path (window of the first 64 bits), then lane 0 chains. ----
-      const int D = min(s_tab.maxl, 32);
-      for (int i = 0; i < 64; i++) W.vis[lane][i] = 0;
-#ifdef PMZ_DEC3_PROFILE
-      unsigned it_tf = 0, n_new = 0;
-#endif
-      W.E[lane][0] = W.xs[lane];
-      W.Cn[lane][0] = (uint16_t)min(W.ns[lane], 65535u);
-      // one flat work loop per lane (lanes progress independently): advance
-      // the current path one step, or finish it and start the next offset
-      int o = 1;
-      unsigned q = s_i + 1, c = 0;
-      D3Reader<D3Glob> rd;
-      if (D > 1 && q < s_n) rd.seek(ss, q, adj);
-      while (o < D) {
-        unsigned e = 0;
-        bool fin = false;
-        if (q >= s_n) {
-          e = q;
-          fin = true;
-#ifdef PMZ_DEC3_PROFILE
-          n_new++;
-#endif
-        } else if ((W.bm[q >> 5] >> (q & 31)) & 1u) {
-          e = W.xs[lane];
-          c += W.ns[lane] - rank(q);
+    }
+  }
+  W.ex[t] = ex;
+  __syncthreads();
+  const bool moved = t > 0 && W.ex[t - 1] != entry;
+  if (__syncthreads_or(moved)) {
+    // ---- fallback: transfer function of every lane over all entry offsets
+    // [0, D) (the true entry is the first boundary >= s_t, < s_t + maxl);
+    // paths merge into the speculative path (bitmap) or into an earlier
+    // offset's path (window of the first 64 bits), then thread 0 chains ----
+    const int D = min(s_tab.maxl, 32);
+    for (int i = 0; i < 64; i++) W.vis[t][i] = 0;
+    auto rel = [&](unsigned e) -> uint16_t { return e == kD3Bad ? (uint16_t)0xffff : (uint16_t)(e - s_i); };
+    W.E[t][0] = rel(W.xs[t]);
+    W.Cn[t][0] = (uint16_t)min(W.ns[t], 65535u);
+    int o = 1;
+    unsigned q = s_i + 1, c = 0;
+    D3Reader<D3Glob> rd;
+    if (D > 1 && q < s_n) rd.seek(ss, q, adj);
+    while (o < D) {
+      unsigned e = 0;
+      bool fin = false;
+      if (q >= s_n) {
+        e = q;
+        fin = true;
+      } else if ((W.bm[q >> 5] >> (q & 31)) & 1u) {
+        e = W.xs[t];
+        c += W.ns[t] - rank(q);
+        fin = true;
+      } else {
+        const unsigned off = q - s_i;
+        const unsigned v = off < 64u ? W.vis[t][off] : 0u;
+        if (v) {
+          const unsigned o2 = (v >> 10) - 1;
+          e = W.E[t][o2] == 0xffff ? kD3Bad : s_i + W.E[t][o2];
+          c += W.Cn[t][o2] - (v & 1023u);
           fin = true;
         } else {
-          const unsigned off = q - s_i;
-          const unsigned v = off < 64u ? W.vis[lane][off] : 0u;
-          if (v) {
-            const unsigned o2 = (v >> 10) - 1;
-            e = W.E[lane][o2];
-            c += W.Cn[lane][o2] - (v & 1023u);
+          rd.refill(ss);
+          int s, l;
+          unsigned k;
+          if (!d3_run(rd.buf, rd.nb, s_n - q, s_lut, lut2, s_tab, sym, s, l, k)) {
+            e = kD3Bad;
             fin = true;
           } else {
-            rd.refill(ss);
-            int s, l;
-            unsigned k;
-            if (!d3_run(rd.buf, rd.nb, s_n - q, s_lut, lut2, s_tab, sym, s, l, k)) {
-              e = kD3Bad;
-              fin = true;
-            } else {
-#ifdef PMZ_DEC3_PROFILE
-              it_tf++;
-#endif
-              // every boundary of this step inside the window belongs to path o
-              for (unsigned j = 0; j < k; j++) {
-                const unsigned oj = off + j * (unsigned)l;
-                if (oj >= 64u) break;
-                if (!W.vis[lane][oj]) W.vis[lane][oj] = (uint16_t)(((o + 1) << 10) | min(c + j, 1023u));
-              }
-              const unsigned adv = k * (unsigned)l;
-              rd.skip(adv);
-              q += adv;
-              c += k;
+            // every boundary of this step inside the window belongs to path o
+            for (unsigned j = 0; j < k; j++) {
+              const unsigned oj = off + j * (unsigned)l;
+              if (oj >= 64u) break;
+              if (!W.vis[t][oj]) W.vis[t][oj] = (uint16_t)(((o + 1) << 10) | min(c + j, 1023u));
             }
+            const unsigned adv = k * (unsigned)l;
+            rd.skip(adv);
+            q += adv;
+            c += k;
           }
         }
-        if (fin) {
-          W.E[lane][o] = e;
-          W.Cn[lane][o] = (uint16_t)min(c, 65535u);
-          o++;
-          q = s_i + (unsigned)o;
-          c = 0;
-          if (o < D && q < s_n) rd.seek(ss, q, adj);
-        }
       }
-#ifdef PMZ_DEC3_PROFILE
-      {
-        unsigned mx = it_tf, mn = n_new;
-        for (int d = 16; d > 0; d >>= 1) { mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, d)); mn = max(mn, __shfl_xor_sync(0xffffffffu, mn, d)); }
-        if (lane == 0 && p < 65536) { g_d3n[p][1] = mx; g_d3[p][4] = 100 + mn; }
+      if (fin) {
+        W.E[t][o] = rel(e);
+        W.Cn[t][o] = (uint16_t)min(c, 65535u);
+        o++;
+        q = s_i + (unsigned)o;
+        c = 0;
+        if (o < D && q < s_n) rd.seek(ss, q, adj);
       }
-#endif
-      __syncwarp();
-      if (lane == 0) {
-        const unsigned segw2 = 32 * segw;
-        unsigned T = 0;
-        for (int t = 0; t < 32; t++) {
-          W.ent[t] = T;
-          W.cnt[t] = 0;
-          const unsigned si = min(L, segw2 * t), sn = min(L, segw2 * (t + 1));
-          if (T == kD3Bad || T >= sn) continue;  // no codeword starts in segment t
-          const unsigned o = T - si;
-          W.cnt[t] = o < (unsigned)D ? W.Cn[t][o] : 0u;
-          T = o < (unsigned)D ? W.E[t][o] : kD3Bad;
-        }
-        W.ent[32] = T;
-      }
-      __syncwarp();
-      entry = W.ent[lane];
-      ex = W.ent[lane + 1];
-      cnt = W.cnt[lane];
     }
-    D3_STAMP(2)
-    // ---- 3. write pass ----
-    unsigned incl = cnt;
-    for (int d = 1; d < 32; d <<= 1) {
-      const unsigned t = __shfl_up_sync(0xffffffffu, incl, d);
-      if (lane >= d) incl += t;
+    __syncthreads();
+    if (t == 0) {
+      unsigned T = 0;
+      for (int u = 0; u < NL; u++) {
+        W.ent[u] = T;
+        W.cnt[u] = 0;
+        const unsigned si = min(L, 32 * segw * u), sn = min(L, 32 * segw * (u + 1));
+        if (T == kD3Bad || T >= sn) continue;  // no codeword starts in segment u
+        const unsigned oo = T - si;
+        if (oo >= (unsigned)D || W.E[u][oo] == 0xffff) {
+          T = kD3Bad;
+          continue;
+        }
+        W.cnt[u] = W.Cn[u][oo];
+        T = si + W.E[u][oo];
+      }
+      W.ent[NL] = T;
     }
-    const unsigned total = __shfl_sync(0xffffffffu, incl, 31);
-    const unsigned last = __shfl_sync(0xffffffffu, ex, 31);
-    const bool okall = __all_sync(0xffffffffu, ex != kD3Bad);
-    if (!okall || total != nsym || last != L) {
-      if (lane == 0) set_err(st, !okall ? PMZ_ERR_INVALID_PREFIX : (total < nsym ? PMZ_ERR_TRUNCATED : PMZ_ERR_CORRUPT));
-    } else if (cnt) {
-      D3Reader<D3Glob> rd;
-      rd.seek(ss, entry, adj);
-      const unsigned e0 = incl - cnt + 1;  // raster index of the first symbol (anchor = 0)
-      int r = (int)(e0 / (unsigned)C), c = (int)(e0 - (unsigned)r * C);
-      int zr = r;
-      unsigned zc = 0;  // code-0 symbols of row zr not yet added to W.zrow
-      for (unsigned i = 0; i < cnt;) {
-        rd.refill(ss);
-        int s, l;
-        unsigned k;
-        if (!d3_run(rd.buf, rd.nb, 64u, s_lut, lut2, s_tab, sym, s, l, k)) { set_err(st, PMZ_ERR_INVALID_PREFIX); break; }
-        k = min(k, cnt - i);
-        for (unsigned j = 0; j < k; j++) {
-          ct[(c >> 5) * kTile + r * 32 + (c & 31)] = (uint16_t)s;
-          if (s == 0) {
-            if (r != zr) {
-              if (zc) atomicAdd(&W.zrow[zr], zc);
-              zr = r;
-              zc = 0;
-            }
-            zc++;
+    __syncthreads();
+    entry = W.ent[t];
+    ex = W.ent[t + 1];
+    cnt = W.cnt[t];
+  }
+
+  // ---- 3. write pass: CTA scan of the counts, then every lane decodes its
+  // span into the tile layout, counting code-0 symbols per row ----
+  unsigned incl = cnt;
+  for (int d = 1; d < 32; d <<= 1) {
+    const unsigned v = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += v;
+  }
+  if (lane == 31) W.wsum[warp] = incl;
+  W.ex[t] = ex;
+  __syncthreads();
+  unsigned base = 0, total = 0;
+#pragma unroll
+  for (int w = 0; w < kD3Wpp; w++) {
+    if (w < warp) base += W.wsum[w];
+    total += W.wsum[w];
+  }
+  const unsigned last = W.ex[NL - 1];
+  const bool okall = __syncthreads_and(ex != kD3Bad);
+  unsigned zeros = 0;
+  if (!okall || total != nsym || last != L) {
+    if (t == 0) set_err(st, !okall ? PMZ_ERR_INVALID_PREFIX : (total < nsym ? PMZ_ERR_TRUNCATED : PMZ_ERR_CORRUPT));
+  } else if (cnt) {
+    D3Reader<D3Glob> rd;
+    rd.seek(ss, entry, adj);
+    const unsigned e0 = base + incl - cnt + 1;  // raster index of the first symbol (anchor = 0)
+    int r = (int)(e0 / (unsigned)C), c = (int)(e0 - (unsigned)r * C);
+    int zr = r;
+    unsigned zc = 0;  // code-0 symbols of row zr not yet added to W.zrow
+    for (unsigned i = 0; i < cnt;) {
+      rd.refill(ss);
+      int s, l;
+      unsigned k;
+      if (!d3_run(rd.buf, rd.nb, 64u, s_lut, lut2, s_tab, sym, s, l, k)) { set_err(st, PMZ_ERR_INVALID_PREFIX); break; }
+      k = min(k, cnt - i);
+      for (unsigned j = 0; j < k; j++) {
+        ct[(c >> 5) * kTile + r * 32 + (c & 31)] = (uint16_t)s;
+        if (s == 0) {
+          if (r != zr) {
+            if (zc) atomicAdd(&W.zrow[zr], zc);
+            zr = r;
+            zc = 0;
           }
-          if (++c == C) { c = 0; r++; }
+          zc++;
         }
-        if (s == 0) zeros += k;
-        rd.skip(k * (unsigned)l);
-        i += k;
+        if (++c == C) { c = 0; r++; }
       }
-      if (zc) atomicAdd(&W.zrow[zr], zc);
+      if (s == 0) zeros += k;
+      rd.skip(k * (unsigned)l);
+      i += k;
     }
-    __syncwarp();
-    D3_STAMP(3)
+    if (zc) atomicAdd(&W.zrow[zr], zc);
   }
   for (int d = 16; d > 0; d >>= 1) zeros += __shfl_xor_sync(0xffffffffu, zeros, d);
-  if (lane == 0) part_zeros[p] = zeros;
-  zrow_out[p * 32 + lane] = (uint16_t)W.zrow[lane];
-  __syncwarp();
+  if (lane == 0) W.wsum[warp] = zeros;
+  __syncthreads();
+  if (t == 0) {
+    unsigned z = 0;
+    for (int w = 0; w < kD3Wpp; w++) z += W.wsum[w];
+    part_zeros[p] = z;
   }
+  if (t < 32) zrow_out[p * 32 + t] = (uint16_t)W.zrow[t];
 }
 
 }  // namespace pmz
