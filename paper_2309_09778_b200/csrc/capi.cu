@@ -562,11 +562,11 @@ DecLayout dec_layout(const Geom &g) {
   return L;
 }
 template <int PK>
-int launch_recon(const KParams &k, unsigned grid, cudaStream_t st, const uint8_t *d_buf, const Geom &G, int m,
-                 void *d_ws, const DecLayout &L, float *d_out) {
+int launch_recon(const KParams &k, unsigned grid, cudaStream_t st, const uint8_t *d_buf, uint64_t n, const Geom &G,
+                 int m, void *d_ws, const DecLayout &L, float *d_out) {
   CK(cudaFuncSetAttribute(k_reconstruct3<PK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDsc3Smem));
   k_reconstruct3<PK><<<grid, kPPC * 64, kDsc3Smem, st>>>(
-      d_buf, G, k, m, at<BlkP>(d_ws, L.blkp), at<uint16_t>(d_ws, L.codes), at<uint16_t>(d_ws, L.zrow),
+      d_buf, n, G, k, m, at<BlkP>(d_ws, L.blkp), at<uint16_t>(d_ws, L.codes), at<uint16_t>(d_ws, L.zrow),
       at<double>(d_ws, L.anchors), at<unsigned long long>(d_ws, L.part_zeros),
       at<unsigned long long>(d_ws, L.bal_off), at<unsigned long long>(d_ws, L.blk_nbal), d_out,
       at<double>(d_ws, L.vh), at<WsStatus>(d_ws, L.status));
@@ -640,9 +640,9 @@ int pmz_decompress(const uint8_t *d_buf, uint64_t n, const pmz_header *hdr, doub
         at<unsigned>(d_ws, L.large), S);
     const unsigned rgrid = (unsigned)((G.nparts + kPPC - 1) / kPPC);
     int s2;
-    if (k.init_model == 3) s2 = launch_recon<3>(k, rgrid, st, d_buf, G, (int)hdr->m, d_ws, L, d_out);
-    else if (k.init_model == 1) s2 = launch_recon<1>(k, rgrid, st, d_buf, G, (int)hdr->m, d_ws, L, d_out);
-    else s2 = launch_recon<0>(k, rgrid, st, d_buf, G, (int)hdr->m, d_ws, L, d_out);
+    if (k.init_model == 3) s2 = launch_recon<3>(k, rgrid, st, d_buf, n, G, (int)hdr->m, d_ws, L, d_out);
+    else if (k.init_model == 1) s2 = launch_recon<1>(k, rgrid, st, d_buf, n, G, (int)hdr->m, d_ws, L, d_out);
+    else s2 = launch_recon<0>(k, rgrid, st, d_buf, n, G, (int)hdr->m, d_ws, L, d_out);
     if (s2) return s2;
   }
   int s = launch_check();

@@ -16,6 +16,23 @@
 
 namespace pmz {
 
+// 8 little-endian bytes at an arbitrary address: two aligned 8-byte loads and
+// a shift when both lie inside the buffer, else byte by byte.
+__device__ __forceinline__ double ld_f64_at(const uint8_t *p, const uint8_t *end) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  const unsigned sh = (unsigned)(a & 7) * 8;
+  const unsigned long long *q = reinterpret_cast<const unsigned long long *>(a & ~(uintptr_t)7);
+  if (sh == 0) return __longlong_as_double((long long)__ldg(q));
+  if (reinterpret_cast<const uint8_t *>(q + 2) <= end) {
+    const unsigned long long lo = __ldg(q), hi = __ldg(q + 1);
+    return __longlong_as_double((long long)((lo >> sh) | (hi << (64 - sh))));
+  }
+  unsigned long long v = 0;
+#pragma unroll
+  for (int i = 7; i >= 0; i--) v = (v << 8) | __ldg(p + i);
+  return __longlong_as_double((long long)v);
+}
+
 __device__ __forceinline__ double ld_f64_unaligned(const uint8_t *p) {
   unsigned long long v = 0;
 #pragma unroll
@@ -41,7 +58,8 @@ struct DRing3 {
 constexpr size_t kDsc3Smem = sizeof(DRing3) * kPPC;
 
 template <int PK>
-__global__ void __launch_bounds__(kPPC * 64) k_reconstruct3(const uint8_t *__restrict__ buf, Geom g, KParams k, int m,
+__global__ void __launch_bounds__(kPPC * 64) k_reconstruct3(const uint8_t *__restrict__ buf,
+                                                            unsigned long long buf_n, Geom g, KParams k, int m,
                                                             const BlkP *__restrict__ blkp,
                                                             const uint16_t *__restrict__ codes,
                                                             const uint16_t *__restrict__ zrow,
@@ -89,7 +107,7 @@ __global__ void __launch_bounds__(kPPC * 64) k_reconstruct3(const uint8_t *__res
 
   if (role == 0) {
     // ------------------------------ producer ------------------------------
-    const uint8_t *bal = buf + bal_off[b];
+    const uint8_t *bal = buf + bal_off[b], *bend = buf + buf_n;
     // balance index of the next code-0 of every row (warp-uniform registers):
     // partition base + zeros of the rows above (the decoder's per-row counts)
     unsigned rb[32];
@@ -129,7 +147,7 @@ __global__ void __launch_bounds__(kPPC * 64) k_reconstruct3(const uint8_t *__res
       for (int r = 0; r < 32; r++) {
         const bool z = cr[r] == 0;
         const unsigned zm = __ballot_sync(0xffffffffu, z);
-        if (z) W.val[s][r * 32 + lane] = ld_f64_unaligned(bal + 8ull * (rb[r] + __popc(zm & ((1u << lane) - 1))));
+        if (z) W.val[s][r * 32 + lane] = ld_f64_at(bal + 8ull * (rb[r] + __popc(zm & ((1u << lane) - 1))), bend);
         if (r < R) W.code[s][r * 32 + lane] = cr[r];
         rb[r] += __popc(zm);
       }
@@ -218,12 +236,24 @@ __global__ void __launch_bounds__(256) k_inv(Geom g, const BlkP *__restrict__ bl
   const bool vec = ((g.cols & 3) == 0) && ((bb.c0 & 3) == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
   const double *vt = vh + tile_base(g, p, 0);
   unsigned *amb = &st->unresolved;
-  for (int i = threadIdx.x; i < nch * 256; i += 256) {
+  // the next quad's values are loaded before this quad's exp2 work
+  auto load_quad = [&](int i, double (&v)[4]) -> bool {
     const int kc = i >> 8, r = (i >> 3) & 31, c0 = kc * 32 + (i & 7) * 4;
-    if (r >= R || c0 >= C) continue;
+    if (i >= nch * 256 || r >= R || c0 >= C) return false;
     const double2 *q = reinterpret_cast<const double2 *>(vt + kc * kTile + r * 32 + (c0 & 31));
     const double2 a0 = __ldg(q), a1 = __ldg(q + 1);
-    const double v[4] = {a0.x, a0.y, a1.x, a1.y};
+    v[0] = a0.x; v[1] = a0.y; v[2] = a1.x; v[3] = a1.y;
+    return true;
+  };
+  double vn[4];
+  bool hn = load_quad(threadIdx.x, vn);
+  for (int i = threadIdx.x; i < nch * 256; i += 256) {
+    const double v[4] = {vn[0], vn[1], vn[2], vn[3]};
+    const bool h = hn;
+    hn = load_quad(i + 256, vn);
+    if (!h) continue;
+    const int kc = i >> 8, r = (i >> 3) & 31, c0 = kc * 32 + (i & 7) * 4;
+    (void)kc;
     float y[4];
 #pragma unroll
     for (int u = 0; u < 4; u++) y[u] = c0 + u < C ? inv_f32(v[u], P, amb) : 0.0f;  // padding columns hold garbage

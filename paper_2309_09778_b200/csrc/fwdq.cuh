@@ -39,11 +39,12 @@ __global__ void __launch_bounds__(kFqT) k_fwd(const float *__restrict__ x, Geom 
   double *vt = vbuf + tile_base(g, p, 0);
   uint8_t *ct = clsbuf + tile_base(g, p, 0);
   unsigned *amb = &st->unresolved;
-  for (int i = threadIdx.x; i < nch * 256; i += kFqT) {
+  // quad i: row (i >> 3) & 31, columns 32 (i >> 8) + 4 (i & 7) .. + 3; the
+  // next quad's input is loaded before this quad's log2 chains
+  auto load_quad = [&](int i, float (&xr)[4]) -> bool {
     const int kc = i >> 8, r = (i >> 3) & 31, c0 = kc * 32 + (i & 7) * 4;
-    if (r >= R || c0 >= C) continue;
+    if (i >= nch * 256 || r >= R || c0 >= C) return false;
     const float *src = xp + (int64_t)r * g.cols + c0;
-    float xr[4];
     if (vec && c0 + 3 < C) {
       const float4 q = __ldg(reinterpret_cast<const float4 *>(src));
       xr[0] = q.x; xr[1] = q.y; xr[2] = q.z; xr[3] = q.w;
@@ -51,6 +52,16 @@ __global__ void __launch_bounds__(kFqT) k_fwd(const float *__restrict__ x, Geom 
 #pragma unroll
       for (int u = 0; u < 4; u++) xr[u] = c0 + u < C ? __ldg(src + u) : 0.0f;
     }
+    return true;
+  };
+  float xn[4];
+  bool hn = load_quad(threadIdx.x, xn);
+  for (int i = threadIdx.x; i < nch * 256; i += kFqT) {
+    float xr[4] = {xn[0], xn[1], xn[2], xn[3]};
+    const bool h = hn;
+    hn = load_quad(i + kFqT, xn);
+    if (!h) continue;
+    const int kc = i >> 8, r = (i >> 3) & 31, c0 = kc * 32 + (i & 7) * 4;
     double ax[4], lg[4], v[4];
     unsigned cl = 0;
 #pragma unroll
