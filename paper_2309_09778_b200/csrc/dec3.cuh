@@ -47,14 +47,22 @@ struct D3Cfg {
 };
 template <bool LARGE>
 struct D3Part {
+  unsigned lut[1 << kLutBits];          // first-level decode table (second level through L1)
   unsigned bm[D3Cfg<LARGE>::kBm];
   unsigned xs[kD3Nl], ns[kD3Nl];        // speculative exit / symbol count per lane
   unsigned ex[kD3Nl], ent[kD3Nl + 1], cnt[kD3Nl];
-  uint16_t E[kD3Nl][32];                // fallback: exit - s_t per entry offset (0xffff: bad)
-  uint16_t Cn[kD3Nl][32];               // fallback: symbol count per entry offset
-  uint16_t vis[kD3Nl][64];              // fallback: (path + 1) << 10 | symbols before s_t + i
   unsigned zrow[32];
   unsigned wsum[kD3Wpp];
+};
+// Fallback tables of one partition (global scratch, L2-resident; only the
+// partitions whose optimistic round fails touch them), from a pool of
+// kD3FallSlots claimed by compare-and-swap: more slots than CTAs can be
+// resident at once, so a claim always succeeds and no two live CTAs share one.
+constexpr unsigned kD3FallSlots = 2048;
+struct D3Fall {
+  uint16_t E[kD3Nl][32];                // exit - s_t per entry offset (0xffff: bad)
+  uint16_t Cn[kD3Nl][32];               // symbol count per entry offset
+  uint16_t vis[kD3Nl][64];              // (path + 1) << 10 | symbols before s_t + i
 };
 template <bool LARGE>
 constexpr size_t d3_smem() { return sizeof(D3Part<LARGE>); }
@@ -142,10 +150,11 @@ __global__ void __launch_bounds__(kD3Nl) k_decode3(const uint8_t *__restrict__ b
                                                   uint16_t *__restrict__ codes,
                                                   unsigned long long *__restrict__ part_zeros,
                                                   uint16_t *__restrict__ zrow_out, unsigned *large_list,
-                                                  WsStatus *st) {
+                                                  D3Fall *__restrict__ fall, unsigned *fall_busy, WsStatus *st) {
   constexpr int NL = kD3Nl, kBm = D3Cfg<LARGE>::kBm;
   __shared__ unsigned long long s_rep[33];
   __shared__ DecTab s_tab;
+  __shared__ unsigned s_slot;
   extern __shared__ __align__(16) unsigned char dyn3[];
   D3Part<LARGE> &W = *reinterpret_cast<D3Part<LARGE> *>(dyn3);
   count_launch(st);
@@ -165,8 +174,9 @@ __global__ void __launch_bounds__(kD3Nl) k_decode3(const uint8_t *__restrict__ b
     s_rep[t] = r;
   }
   if (t < 32) W.zrow[t] = 0;
+  for (int i = t; i < (1 << kLutBits); i += NL) W.lut[i] = __ldg(lut + i);
   __syncthreads();
-  const unsigned *s_lut = lut, *lut2 = lut + (1 << kLutBits);  // through L1
+  const unsigned *s_lut = W.lut, *lut2 = lut + (1 << kLutBits);  // second level through L1
   int64_t b;
   int pi;
   part_of(g, p, b, pi);
@@ -287,10 +297,17 @@ __global__ void __launch_bounds__(kD3Nl) k_decode3(const uint8_t *__restrict__ b
     // paths merge into the speculative path (bitmap) or into an earlier
     // offset's path (window of the first 64 bits), then thread 0 chains ----
     const int D = min(s_tab.maxl, 32);
-    for (int i = 0; i < 64; i++) W.vis[t][i] = 0;
+    if (t == 0) {
+      unsigned sl = (unsigned)(p % kD3FallSlots);
+      while (atomicCAS(&fall_busy[sl], 0u, 1u) != 0u) sl = (sl + 1) % kD3FallSlots;
+      s_slot = sl;
+    }
+    __syncthreads();
+    D3Fall &F = fall[s_slot];
+    unsigned long long vmask = 0;  // offsets of the window with a F.vis entry (no zeroing, no load per step)
     auto rel = [&](unsigned e) -> uint16_t { return e == kD3Bad ? (uint16_t)0xffff : (uint16_t)(e - s_i); };
-    W.E[t][0] = rel(W.xs[t]);
-    W.Cn[t][0] = (uint16_t)min(W.ns[t], 65535u);
+    F.E[t][0] = rel(W.xs[t]);
+    F.Cn[t][0] = (uint16_t)min(W.ns[t], 65535u);
     int o = 1;
     unsigned q = s_i + 1, c = 0;
     D3Reader<D3Glob> rd;
@@ -307,11 +324,11 @@ __global__ void __launch_bounds__(kD3Nl) k_decode3(const uint8_t *__restrict__ b
         fin = true;
       } else {
         const unsigned off = q - s_i;
-        const unsigned v = off < 64u ? W.vis[t][off] : 0u;
-        if (v) {
+        if (off < 64u && ((vmask >> off) & 1ull)) {
+          const unsigned v = F.vis[t][off];
           const unsigned o2 = (v >> 10) - 1;
-          e = W.E[t][o2] == 0xffff ? kD3Bad : s_i + W.E[t][o2];
-          c += W.Cn[t][o2] - (v & 1023u);
+          e = F.E[t][o2] == 0xffff ? kD3Bad : s_i + F.E[t][o2];
+          c += F.Cn[t][o2] - (v & 1023u);
           fin = true;
         } else {
           rd.refill(ss);
@@ -325,7 +342,10 @@ __global__ void __launch_bounds__(kD3Nl) k_decode3(const uint8_t *__restrict__ b
             for (unsigned j = 0; j < k; j++) {
               const unsigned oj = off + j * (unsigned)l;
               if (oj >= 64u) break;
-              if (!W.vis[t][oj]) W.vis[t][oj] = (uint16_t)(((o + 1) << 10) | min(c + j, 1023u));
+              if (!((vmask >> oj) & 1ull)) {
+                vmask |= 1ull << oj;
+                F.vis[t][oj] = (uint16_t)(((o + 1) << 10) | min(c + j, 1023u));
+              }
             }
             const unsigned adv = k * (unsigned)l;
             rd.skip(adv);
@@ -335,16 +355,30 @@ __global__ void __launch_bounds__(kD3Nl) k_decode3(const uint8_t *__restrict__ b
         }
       }
       if (fin) {
-        W.E[t][o] = rel(e);
-        W.Cn[t][o] = (uint16_t)min(c, 65535u);
+        F.E[t][o] = rel(e);
+        F.Cn[t][o] = (uint16_t)min(c, 65535u);
         o++;
         q = s_i + (unsigned)o;
         c = 0;
         if (o < D && q < s_n) rd.seek(ss, q, adj);
       }
     }
+    // the bitmap is dead now: stage the tables in its space for the serial chain
+    __syncthreads();
+    uint16_t(*sE)[32] = reinterpret_cast<uint16_t(*)[32]>(W.bm);
+    uint16_t(*sC)[32] = reinterpret_cast<uint16_t(*)[32]>(W.bm + NL * 16);
+    {
+      const uint4 *ge = reinterpret_cast<const uint4 *>(F.E[t]), *gc = reinterpret_cast<const uint4 *>(F.Cn[t]);
+      uint4 *se = reinterpret_cast<uint4 *>(sE[t]), *sc = reinterpret_cast<uint4 *>(sC[t]);
+      uint4 a[4], c4[4];
+#pragma unroll
+      for (int i = 0; i < 4; i++) { a[i] = ge[i]; c4[i] = gc[i]; }
+#pragma unroll
+      for (int i = 0; i < 4; i++) { se[i] = a[i]; sc[i] = c4[i]; }
+    }
     __syncthreads();
     if (t == 0) {
+      atomicExch(&fall_busy[s_slot], 0u);  // every lane has copied its tables out (barrier above)
       unsigned T = 0;
       for (int u = 0; u < NL; u++) {
         W.ent[u] = T;
@@ -352,12 +386,12 @@ __global__ void __launch_bounds__(kD3Nl) k_decode3(const uint8_t *__restrict__ b
         const unsigned si = min(L, 32 * segw * u), sn = min(L, 32 * segw * (u + 1));
         if (T == kD3Bad || T >= sn) continue;  // no codeword starts in segment u
         const unsigned oo = T - si;
-        if (oo >= (unsigned)D || W.E[u][oo] == 0xffff) {
+        if (oo >= (unsigned)D || sE[u][oo] == 0xffff) {
           T = kD3Bad;
           continue;
         }
-        W.cnt[u] = W.Cn[u][oo];
-        T = si + W.E[u][oo];
+        W.cnt[u] = sC[u][oo];
+        T = si + sE[u][oo];
       }
       W.ent[NL] = T;
     }
