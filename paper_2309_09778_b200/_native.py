@@ -12,7 +12,8 @@ import os
 from .errors import DeviceError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libpermez_b200.so")
+# PMZ_LIB_PATH: load a variant build instead (A/B experiments under tools/)
+LIB_PATH = os.environ.get("PMZ_LIB_PATH") or os.path.join(_HERE, "_lib", "libpermez_b200.so")
 
 c_double, c_int32, c_uint32, c_uint64, c_int64 = (ctypes.c_double, ctypes.c_int32, ctypes.c_uint32, ctypes.c_uint64,
                                                    ctypes.c_int64)

@@ -260,7 +260,7 @@ struct WsStatus {
   int max_len;           // max codeword length
   int n_val_nontrivial;  // k for the histogram floor (D10)
   unsigned launches;     // kernels of this library that ran (counted on device)
-  int pad[2];
+  int err_site, err_part;  // first error's raising site / partition (diagnostics, PMZ_DEBUG)
   unsigned long long nbal, nrepair, ntrivial, ncodes;
   unsigned long long total_bytes, header_bytes, record_bytes;
   unsigned long long pad2;

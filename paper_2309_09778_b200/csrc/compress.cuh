@@ -8,6 +8,11 @@ namespace pmz {
 __device__ __forceinline__ void set_err(WsStatus *st, int status) {
   atomicOr(&st->err_bits, 1u << (-status));
 }
+// set_err that also records where the first error was raised (site >= 1)
+__device__ __forceinline__ void set_err_at(WsStatus *st, int status, int site, long long part) {
+  set_err(st, status);
+  if (atomicCAS(&st->err_site, 0, site) == 0) st->err_part = (int)part;
+}
 
 // Block-wide min/max reduction helpers (256 threads).
 template <int NT>

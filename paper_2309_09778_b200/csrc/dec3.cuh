@@ -29,15 +29,20 @@ namespace pmz {
 
 constexpr unsigned kD3Bad = 0xffffffffu;
 #ifndef PMZ_D3_WPP
-#define PMZ_D3_WPP 2
+#define PMZ_D3_WPP 8
 #endif
 constexpr int kD3Wpp = PMZ_D3_WPP;  // warps per partition
 constexpr int kD3Nl = 32 * kD3Wpp;  // lane segments per partition
+#ifndef PMZ_D3_ROUNDS
+#define PMZ_D3_ROUNDS 8
+#endif
+constexpr int kD3Rounds = PMZ_D3_ROUNDS;        // optimistic re-walk rounds before the transfer function
 
 // One CTA per partition, kD3Nl lanes = segments.  The substream is read
 // straight from global memory (the reader prefetches one word ahead, so the
-// load is off the dependency chain) and the decode tables through L1; the
-// shared state is the boundary bitmap plus the per-lane fallback tables.
+// load is off the dependency chain); the first-level decode table and the
+// boundary bitmap live in shared memory, the second-level table is read
+// through L1 and the per-lane fallback tables go to a global pool.
 // LARGE = false: substreams up to 16 KB; longer ones go to a work list
 // served by the LARGE launch (32 KB = the longest valid substream, 8191
 // codewords x 32 bits).
@@ -56,9 +61,9 @@ struct D3Part {
 };
 // Fallback tables of one partition (global scratch, L2-resident; only the
 // partitions whose optimistic round fails touch them), from a pool of
-// kD3FallSlots claimed by compare-and-swap: more slots than CTAs can be
-// resident at once, so a claim always succeeds and no two live CTAs share one.
-constexpr unsigned kD3FallSlots = 2048;
+// nslots claimed by compare-and-swap: at least as many slots as CTAs can be
+// resident at once (d3_fall_slots), so a claim always succeeds and no two
+// live CTAs share one.
 struct D3Fall {
   uint16_t E[kD3Nl][32];                // exit - s_t per entry offset (0xffff: bad)
   uint16_t Cn[kD3Nl][32];               // symbol count per entry offset
@@ -150,7 +155,8 @@ __global__ void __launch_bounds__(kD3Nl) k_decode3(const uint8_t *__restrict__ b
                                                   uint16_t *__restrict__ codes,
                                                   unsigned long long *__restrict__ part_zeros,
                                                   uint16_t *__restrict__ zrow_out, unsigned *large_list,
-                                                  D3Fall *__restrict__ fall, unsigned *fall_busy, WsStatus *st) {
+                                                  D3Fall *__restrict__ fall, unsigned *fall_busy, unsigned nslots,
+                                                  WsStatus *st) {
   constexpr int NL = kD3Nl, kBm = D3Cfg<LARGE>::kBm;
   __shared__ unsigned long long s_rep[33];
   __shared__ DecTab s_tab;
@@ -192,7 +198,7 @@ __global__ void __launch_bounds__(kD3Nl) k_decode3(const uint8_t *__restrict__ b
   if (L64 > 0xffffff00ull || ((L64 + 31) >> 5) + 4 > (unsigned long long)kBm) {
     if (t == 0) {
       if (!LARGE && L64 <= 32ull * (nsym + 1)) large_list[1 + atomicAdd(&large_list[0], 1u)] = (unsigned)p;
-      else set_err(st, PMZ_ERR_CORRUPT);  // longer than any valid substream (codewords <= 32 bits)
+      else set_err_at(st, PMZ_ERR_CORRUPT, 1, p);  // longer than any valid substream (codewords <= 32 bits)
     }
     return;
   }
@@ -216,7 +222,9 @@ __global__ void __launch_bounds__(kD3Nl) k_decode3(const uint8_t *__restrict__ b
   // goes into the bitmap (a run of k codewords as one periodic mask), the
   // symbol count into ns ----
   {
-    const unsigned w0 = s_i >> 5, wend = (s_n + 31) >> 5;
+    // an empty segment (s_i == s_n == L) owns no word: the partial last
+    // word belongs to the last non-empty lane
+    const unsigned w0 = s_i >> 5, wend = s_n > s_i ? (s_n + 31) >> 5 : w0;
     for (unsigned q = w0; q < wend; q++) W.bm[q] = 0;
     D3Reader<D3Glob> rd;
     rd.seek(ss, s_i, adj);
@@ -252,54 +260,72 @@ __global__ void __launch_bounds__(kD3Nl) k_decode3(const uint8_t *__restrict__ b
     return r + __popc(W.bm[wb] & ((1u << (q & 31)) - 1u));
   };
 
-  // ---- 2. true exits.  Optimistic round: each lane re-decodes from its
-  // assumed entry (the previous lane's speculative exit) until it lands on
-  // a speculative boundary of its own (then its exit is x_t) or crosses s_n ----
-  unsigned entry = t == 0 ? 0u : W.xs[t - 1];
-  unsigned ex, cnt = 0;
-  if (entry == kD3Bad) {
-    ex = kD3Bad;
-  } else if (entry >= s_n) {  // no codeword starts in this segment
-    ex = entry;
-  } else {
+  // ---- 2. true exits.  Optimistic rounds: each lane decodes from its
+  // assumed entry (first the previous lane's speculative exit) until it lands
+  // on a speculative boundary of its own (then its exit is x_t) or crosses
+  // s_n; lanes whose entry changed walk again.  Lane 0's entry is exact, so
+  // round r fixes lane r; after kD3Rounds the transfer function decides ----
+  auto walk = [&](unsigned e0, unsigned &ex, unsigned &cnt) {
+    cnt = 0;
+    if (e0 == kD3Bad) {
+      ex = kD3Bad;
+      return;
+    }
+    if (e0 >= s_n) {  // no codeword starts in this segment
+      ex = e0;
+      return;
+    }
     D3Reader<D3Glob> rd;
-    rd.seek(ss, entry, adj);
-    unsigned pos = entry, c = 0;
-    ex = kD3Bad;
-    bool done = false;
+    rd.seek(ss, e0, adj);
+    unsigned pos = e0, c = 0;
     while (pos < s_n) {
       if ((W.bm[pos >> 5] >> (pos & 31)) & 1u) {
         cnt = c + W.ns[t] - rank(pos);
         ex = W.xs[t];
-        done = true;
-        break;
+        return;
       }
       rd.refill(ss);
       int s, l;
       unsigned k;
-      if (!d3_run(rd.buf, rd.nb, s_n - pos, s_lut, lut2, s_tab, sym, s, l, k)) { done = true; break; }
+      if (!d3_run(rd.buf, rd.nb, s_n - pos, s_lut, lut2, s_tab, sym, s, l, k)) {
+        ex = kD3Bad;
+        return;
+      }
       const unsigned adv = k * (unsigned)l;
       rd.skip(adv);
       pos += adv;
       c += k;
     }
-    if (!done) {
-      ex = pos;
-      cnt = c;
+    ex = pos;
+    cnt = c;
+  };
+  unsigned entry = t == 0 ? 0u : W.xs[t - 1];
+  unsigned ex, cnt;
+  walk(entry, ex, cnt);
+  bool need_tf;
+  int rr = 0;
+  for (int r = 0;; r++) {
+    rr = r;
+    W.ex[t] = ex;
+    __syncthreads();
+    const unsigned e1 = t == 0 ? 0u : W.ex[t - 1];
+    const bool moved = e1 != entry;
+    need_tf = __syncthreads_or(moved);
+    if (!need_tf || r == kD3Rounds) break;
+    if (moved) {
+      entry = e1;
+      walk(entry, ex, cnt);
     }
   }
-  W.ex[t] = ex;
-  __syncthreads();
-  const bool moved = t > 0 && W.ex[t - 1] != entry;
-  if (__syncthreads_or(moved)) {
+  if (need_tf) {
     // ---- fallback: transfer function of every lane over all entry offsets
     // [0, D) (the true entry is the first boundary >= s_t, < s_t + maxl);
     // paths merge into the speculative path (bitmap) or into an earlier
     // offset's path (window of the first 64 bits), then thread 0 chains ----
     const int D = min(s_tab.maxl, 32);
     if (t == 0) {
-      unsigned sl = (unsigned)(p % kD3FallSlots);
-      while (atomicCAS(&fall_busy[sl], 0u, 1u) != 0u) sl = (sl + 1) % kD3FallSlots;
+      unsigned sl = (unsigned)(p % nslots);
+      while (atomicCAS(&fall_busy[sl], 0u, 1u) != 0u) sl = (sl + 1) % nslots;
       s_slot = sl;
     }
     __syncthreads();
@@ -363,10 +389,13 @@ __global__ void __launch_bounds__(kD3Nl) k_decode3(const uint8_t *__restrict__ b
         if (o < D && q < s_n) rd.seek(ss, q, adj);
       }
     }
-    // the bitmap is dead now: stage the tables in its space for the serial chain
+    // the bitmap is dead now and the LUT is reloaded below: stage the tables
+    // in their (contiguous) space for the serial chain
+    static_assert(offsetof(D3Part<LARGE>, bm) == sizeof(unsigned) << kLutBits, "lut, bm contiguous");
+    static_assert(NL * 32 <= (1 << kLutBits) + kBm, "staging fits lut + bm");
     __syncthreads();
-    uint16_t(*sE)[32] = reinterpret_cast<uint16_t(*)[32]>(W.bm);
-    uint16_t(*sC)[32] = reinterpret_cast<uint16_t(*)[32]>(W.bm + NL * 16);
+    uint16_t(*sE)[32] = reinterpret_cast<uint16_t(*)[32]>(W.lut);
+    uint16_t(*sC)[32] = reinterpret_cast<uint16_t(*)[32]>(W.lut + NL * 16);
     {
       const uint4 *ge = reinterpret_cast<const uint4 *>(F.E[t]), *gc = reinterpret_cast<const uint4 *>(F.Cn[t]);
       uint4 *se = reinterpret_cast<uint4 *>(sE[t]), *sc = reinterpret_cast<uint4 *>(sC[t]);
@@ -396,6 +425,8 @@ __global__ void __launch_bounds__(kD3Nl) k_decode3(const uint8_t *__restrict__ b
       W.ent[NL] = T;
     }
     __syncthreads();
+    for (int i = t; i < (1 << kLutBits); i += NL) W.lut[i] = __ldg(lut + i);
+    __syncthreads();
     entry = W.ent[t];
     ex = W.ent[t + 1];
     cnt = W.cnt[t];
@@ -421,7 +452,9 @@ __global__ void __launch_bounds__(kD3Nl) k_decode3(const uint8_t *__restrict__ b
   const bool okall = __syncthreads_and(ex != kD3Bad);
   unsigned zeros = 0;
   if (!okall || total != nsym || last != L) {
-    if (t == 0) set_err(st, !okall ? PMZ_ERR_INVALID_PREFIX : (total < nsym ? PMZ_ERR_TRUNCATED : PMZ_ERR_CORRUPT));
+    if (t == 0)
+      set_err_at(st, !okall ? PMZ_ERR_INVALID_PREFIX : (total < nsym ? PMZ_ERR_TRUNCATED : PMZ_ERR_CORRUPT),
+                 10 + (total > nsym) + 2 * (total < nsym) + 4 * (last != L) + 8 * !okall + 100 * rr + 1000 * need_tf, p);
   } else if (cnt) {
     D3Reader<D3Glob> rd;
     rd.seek(ss, entry, adj);

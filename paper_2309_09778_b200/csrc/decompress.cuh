@@ -50,7 +50,7 @@ __global__ void k_dec_blocks(const uint8_t *__restrict__ buf, unsigned long long
   BlockBox bb = block_box(g, b);
   int64_t p0 = first_part(g, b);
   BlkP P{};
-  if (o >= n) { set_err(st, PMZ_ERR_CORRUPT); P.trivial = 1; blkp[b] = P; return; }
+  if (o >= n) { set_err_at(st, PMZ_ERR_CORRUPT, 41, b); P.trivial = 1; blkp[b] = P; return; }
   uint8_t triv = buf[o];
   if (triv == 1) {
     P.trivial = 1;
@@ -60,10 +60,10 @@ __global__ void k_dec_blocks(const uint8_t *__restrict__ buf, unsigned long long
     return;
   }
   unsigned long long head = 1 + 16 + 24ull * bb.np + 8;
-  if (triv != 0 || o + head > n) { set_err(st, PMZ_ERR_CORRUPT); P.trivial = 1; blkp[b] = P; return; }
+  if (triv != 0 || o + head > n) { set_err_at(st, PMZ_ERR_CORRUPT, 42, b); P.trivial = 1; blkp[b] = P; return; }
   double fp = get_f64(buf + o + 1), fn = get_f64(buf + o + 9);
   if (!(fp > 0.0) || !(fn > 0.0) || !isfinite(fp) || !isfinite(fn)) {
-    set_err(st, PMZ_ERR_CORRUPT); P.trivial = 1; blkp[b] = P; return;
+    set_err_at(st, PMZ_ERR_CORRUPT, 43, b); P.trivial = 1; blkp[b] = P; return;
   }
   derive_params(fp, fn, k, P, &st->unresolved);
   blkp[b] = P;
@@ -71,14 +71,14 @@ __global__ void k_dec_blocks(const uint8_t *__restrict__ buf, unsigned long long
   for (int i = 0; i < bb.np; i++) {
     const uint8_t *e = buf + o + 17 + 24ull * i;
     unsigned long long off = get_u64(e), len = get_u64(e + 8);
-    if (off != pb * 8) set_err(st, PMZ_ERR_CORRUPT);
+    if (off != pb * 8) set_err_at(st, PMZ_ERR_CORRUPT, 44, b);
     part_off[p0 + i] = pb;
     part_bits[p0 + i] = len;
     anchors[p0 + i] = get_f64(e + 16);
     pb += (len + 7) / 8;
   }
   unsigned long long nb = get_u64(buf + o + 17 + 24ull * bb.np);
-  if (nb > (unsigned long long)bb.br * bb.bc) { set_err(st, PMZ_ERR_CORRUPT); nb = 0; }
+  if (nb > (unsigned long long)bb.br * bb.bc) { set_err_at(st, PMZ_ERR_CORRUPT, 45, b); nb = 0; }
   blk_nbal[b] = nb;
   bal_off[b] = o + head;
   pay_off[b] = o + head + 8 * nb;
@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(1024) k_dec_tables(const uint8_t *__restrict__
   __syncthreads();
   for (int s = threadIdx.x; s < n; s += blockDim.x) {
     int l = lens[s];
-    if (l > 32) set_err(st, PMZ_ERR_CORRUPT);
+    if (l > 32) set_err_at(st, PMZ_ERR_CORRUPT, 46, 0);
     else if (l) atomicAdd(&cnt[l], 1u);
   }
   __syncthreads();
@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(1024) k_dec_tables(const uint8_t *__restrict__
     int maxl = 0;
     for (int l = 1; l <= 32; l++) if (cnt[l]) maxl = l;
     for (int l = 1; l <= maxl; l++) kr += (unsigned long long)cnt[l] << (maxl - l);
-    if (maxl == 0 || kr != (1ull << maxl)) set_err(st, PMZ_ERR_CORRUPT);
+    if (maxl == 0 || kr != (1ull << maxl)) set_err_at(st, PMZ_ERR_CORRUPT, 47, 0);
     unsigned long long c = 0;
     unsigned o = 0;
     tab->first[0] = 0; tab->count[0] = 0; tab->offset[0] = 0;

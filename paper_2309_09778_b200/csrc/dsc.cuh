@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(kPPC * 64) k_reconstruct3(const uint8_t *__res
     ztot += z;
   }
   if (ztot != blk_nbal[b]) {
-    if (role == 0 && lane == 0 && pi == 0) set_err(st, ztot > blk_nbal[b] ? PMZ_ERR_BALANCE_UNDERFLOW : PMZ_ERR_CORRUPT);
+    if (role == 0 && lane == 0 && pi == 0) set_err_at(st, ztot > blk_nbal[b] ? PMZ_ERR_BALANCE_UNDERFLOW : PMZ_ERR_CORRUPT, 30, b);
     return;
   }
   const int center = 1 << (m - 1);

@@ -231,6 +231,27 @@ def test_decoder_tiny_partitions(codec, oracle):
     _parity(codec, oracle, x, b_r=1e-2, repair_factor=1.0, block_rows=16, block_cols=8, partition_rows=2)
 
 
+def test_decoder_repeated_decodes_identical(codec, oracle):
+    """The full C2 field decoded many times back to back (L2 flushed in
+    between, so CTA timing varies): every decode is bit-identical to the
+    oracle's.  Covers races between lane segments of one partition, e.g. a
+    trailing empty segment (s_i == s_n == L, L % 32 != 0) clearing the
+    partial last bitmap word the last non-empty lane is still marking."""
+    import paper_2309_09778_b200 as P
+    x = _field("C2")
+    ocfg = oracle.OracleConfig(b_r=1e-2, repair_factor=1.0)
+    ref, _ = oracle.compress(x, ocfg)
+    yo = oracle.decompress(ref).reshape(-1).view(np.uint32)
+    h = P.Codec.parse_header(np.frombuffer(ref, np.uint8))
+    offs = torch.from_numpy(P.Codec.index_blocks(np.frombuffer(ref, np.uint8), h).view("int64")).cuda()
+    dbuf = torch.from_numpy(np.frombuffer(ref, np.uint8).copy()).cuda()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    for i in range(40):
+        flush.fill_(i)
+        y = codec.decompress_device(dbuf, h, offs)
+        assert np.array_equal(y.cpu().numpy().reshape(-1).view(np.uint32), yo), f"decode {i} differs"
+
+
 def test_pipelined_and_graphed_match_one_shot(codec):
     """GraphedCompressor and PipelinedCompressor (several fields in flight)
     return exactly the containers of the one-shot path, in submission order."""
