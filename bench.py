@@ -34,8 +34,8 @@ HBM_FALLBACK = 6650.0
 METRIC = "compress GB/s at PW_REL 1e-2 (C2 1800x3600 f32)"
 
 
-# kernels per pmz_decompress: k_dec_blocks, k_dec_tables, k_decode3 (common, large), k_reconstruct3, k_inv
-DECOMPRESS_LAUNCHES = 6
+# kernels per pmz_decompress: k_dec_blocks, k_dec_tables, k_decode4, k_reconstruct3, k_inv
+DECOMPRESS_LAUNCHES = 5
 
 def peaks():
     try:

@@ -15,7 +15,7 @@
 #include "decompress.cuh"
 #include "encode.cuh"
 #include "fwdq.cuh"
-#include "dec3.cuh"
+#include "dec4.cuh"
 
 using namespace pmz;
 
@@ -533,21 +533,8 @@ int pmz_index_blocks(const uint8_t *h, uint64_t n, const pmz_header *hd, uint64_
 namespace {
 struct DecLayout {
   size_t status, blkp, part_bits, part_off, part_zeros, anchors, bal_off, pay_off, blk_nbal, tab, sym, lut, codes,
-      zrow, large, vh, fall, fall_busy, total;
+      zrow, vh, total;
 };
-// resident-CTA bound of k_decode3 (threads per SM / lanes per CTA, per SM)
-unsigned d3_fall_slots() {
-  static const unsigned n = [] {
-    int dev = 0, nsm = 0, tps = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) ||
-        cudaDeviceGetAttribute(&tps, cudaDevAttrMaxThreadsPerMultiProcessor, dev)) {
-      (void)cudaGetLastError();
-      return 256u * (2048u / kD3Nl);  // no device (layout query on a CPU host): generous bound
-    }
-    return (unsigned)nsm * (unsigned)(tps / kD3Nl);
-  }();
-  return n;
-}
 DecLayout dec_layout(const Geom &g) {
   DecLayout L{};
   size_t o = 0;
@@ -570,10 +557,7 @@ DecLayout dec_layout(const Geom &g) {
   L.lut = take(4ull * ((1u << kLutBits) + kLut2Max));            // first + second level
   L.codes = take(2 * (size_t)g.nparts * (size_t)g.nct * kTile);  // partition-tiled
   L.zrow = take(2 * 32 * (size_t)(g.nparts + 1));                  // code-0 count per partition row
-  L.large = take(4 * (size_t)(g.nparts + 1));                      // work list of long substreams
   L.vh = take(8 * (size_t)g.nparts * (size_t)g.nct * kTile);        // reconstructed values, tiled
-  L.fall = take(sizeof(D3Fall) * (size_t)d3_fall_slots());         // decoder fallback tables (pool)
-  L.fall_busy = take(4 * (size_t)d3_fall_slots());
   L.total = o;
   return L;
 }
@@ -639,24 +623,12 @@ int pmz_decompress(const uint8_t *d_buf, uint64_t n, const pmz_header *hdr, doub
         at<unsigned long long>(d_ws, L.pay_off), at<unsigned long long>(d_ws, L.blk_nbal), S);
     k_dec_tables<<<1, 1024, 0, st>>>(d_buf + hdr->lens_offset, (int)hdr->m, at<DecTab>(d_ws, L.tab),
                                      at<uint16_t>(d_ws, L.sym), at<unsigned>(d_ws, L.lut), S);
-    CK(cudaMemsetAsync(at<unsigned>(d_ws, L.large), 0, 4, st));
-    CK(cudaMemsetAsync(at<unsigned>(d_ws, L.fall_busy), 0, 4 * (size_t)d3_fall_slots(), st));
-    CK(cudaFuncSetAttribute(k_decode3<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d3_smem<false>()));
-    CK(cudaFuncSetAttribute(k_decode3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d3_smem<true>()));
-    k_decode3<false><<<(unsigned)G.nparts, kD3Nl, d3_smem<false>(), st>>>(
+    CK(cudaFuncSetAttribute(k_decode4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kD4Smem));
+    k_decode4<<<(unsigned)G.nparts, kD4Threads, kD4Smem, st>>>(
         d_buf, n, G, at<BlkP>(d_ws, L.blkp), at<DecTab>(d_ws, L.tab), at<uint16_t>(d_ws, L.sym),
         at<unsigned>(d_ws, L.lut), at<unsigned long long>(d_ws, L.part_bits),
         at<unsigned long long>(d_ws, L.part_off), at<unsigned long long>(d_ws, L.pay_off),
-        at<uint16_t>(d_ws, L.codes), at<unsigned long long>(d_ws, L.part_zeros), at<uint16_t>(d_ws, L.zrow),
-        at<unsigned>(d_ws, L.large), at<D3Fall>(d_ws, L.fall), at<unsigned>(d_ws, L.fall_busy),
-        d3_fall_slots(), S);
-    k_decode3<true><<<(unsigned)G.nparts, kD3Nl, d3_smem<true>(), st>>>(
-        d_buf, n, G, at<BlkP>(d_ws, L.blkp), at<DecTab>(d_ws, L.tab), at<uint16_t>(d_ws, L.sym),
-        at<unsigned>(d_ws, L.lut), at<unsigned long long>(d_ws, L.part_bits),
-        at<unsigned long long>(d_ws, L.part_off), at<unsigned long long>(d_ws, L.pay_off),
-        at<uint16_t>(d_ws, L.codes), at<unsigned long long>(d_ws, L.part_zeros), at<uint16_t>(d_ws, L.zrow),
-        at<unsigned>(d_ws, L.large), at<D3Fall>(d_ws, L.fall), at<unsigned>(d_ws, L.fall_busy),
-        d3_fall_slots(), S);
+        at<uint16_t>(d_ws, L.codes), at<unsigned long long>(d_ws, L.part_zeros), at<uint16_t>(d_ws, L.zrow), S);
     const unsigned rgrid = (unsigned)((G.nparts + kPPC - 1) / kPPC);
     int s2;
     if (k.init_model == 3) s2 = launch_recon<3>(k, rgrid, st, d_buf, n, G, (int)hdr->m, d_ws, L, d_out);
@@ -770,3 +742,10 @@ int pmz_log2_f32_batch(const float *d_x, uint64_t n, double *d_out, uint32_t *d_
   return launch_check();
 }
 
+
+#ifdef PMZ_D3_PROF
+// experiments only (tools/dec_bench.py): the decoder's per-partition phase timestamps
+extern "C" PMZ_API int pmz_d3prof_read(void *host, uint64_t bytes) {
+  return cudaMemcpyFromSymbol(host, pmz::g_d3prof, bytes) == cudaSuccess ? 0 : -1;
+}
+#endif

@@ -1,0 +1,412 @@
+// dec4.cuh -- canonical Huffman decode of the per-partition substreams
+// (decode_next; substream layout SPEC.md:496), one CTA per
+// partition, writing the codes in the partition-tiled layout (common.cuh).
+//
+// The decode is exact by construction -- it never relies on a Huffman code
+// re-synchronising (the reference's skewed codebooks, e.g. 4-bit codewords
+// 0000/0001/0010 for the three commonest codes, keep misaligned parses
+// misaligned for thousands of bits, which made speculative decoders
+// unbounded):
+//   1. word maps: the substream is cut into 32-bit words; for a word, lane q
+//      of a warp takes the codeword starting at bit q (one table lookup) and
+//      pointer jumping over the lanes resolves, for EVERY entry offset
+//      e in [0, 32), the offset at which the parse leaves the word and how
+//      many codewords start inside it.  A warp composes the maps of the words
+//      of a subsegment (one shuffle pair per word) into the subsegment's map
+//      (entry offset -> exit offset, codeword count) -- bounded work: one
+//      lookup per bit, no data-dependent iteration;
+//   2. chain: from entry 0 the subsegment maps give every subsegment's true
+//      entry and codeword count (one short dependent chain in shared memory);
+//   3. write pass: thread j decodes its subsegment's codewords from the true
+//      entry into a shared-memory copy of the partition's code tiles (runs of
+//      a repeated codeword in one step), counting code-0 symbols (balance
+//      points) per row; the tiles then go to global memory coalesced.
+// Every code is complete (Kraft equality is checked when the tables are
+// built, decompress.cuh) and no codeword is longer than 32 bits, so every bit
+// position starts a codeword and a parse leaves a word within 32 bits.
+#pragma once
+#include "common.cuh"
+#include "decompress.cuh"
+
+namespace pmz {
+
+#ifndef PMZ_D4_THREADS
+#define PMZ_D4_THREADS 256
+#endif
+constexpr int kD4Threads = PMZ_D4_THREADS;  // threads = subsegments per partition
+constexpr int kD4Warps = kD4Threads / 32;
+constexpr int kD4Ras = 32 * 256;             // codes staged in shared memory in raster order (R * C <= 8192)
+__device__ __forceinline__ unsigned d4_pad(unsigned i) { return i + ((i >> 6) << 1); }  // one bank word per 64 codes
+
+#ifdef PMZ_D3_PROF
+// per-partition phase timestamps (experiments only: tools/dec_bench.py)
+__device__ unsigned long long g_d3prof[1 << 20];
+__device__ __forceinline__ unsigned d3_smid() { unsigned r; asm volatile("mov.u32 %0, %%smid;" : "=r"(r)); return r; }
+#define D3P(i, v) do { if (threadIdx.x == 0 && p < (1 << 17)) g_d3prof[p * 8 + (i)] = (v); } while (0)
+#else
+#define D3P(i, v) do { } while (0)
+#endif
+
+struct D4Smem {
+  uint16_t sym12[1 << kLutBits];  // first-level table: symbol of the codeword on the next 12 bits
+  uint8_t len12[1 << kLutBits];   // its length; 0: longer than 12 bits (global tables)
+  union {
+    uint16_t map[kD4Threads][32];          // subsegment maps: (count << 5) | exit offset, per entry offset
+    uint16_t ras[kD4Ras + kD4Ras / 32];    // the partition's codes, raster order, padded (write pass)
+  } u;
+  unsigned ent[kD4Threads], cnt[kD4Threads];
+  unsigned zrow[32];
+  unsigned wsum[kD4Warps];
+  unsigned fin;                            // exit offset after the last word
+};
+constexpr size_t kD4Smem = sizeof(D4Smem);
+
+// Register bit reader at an arbitrary bit position of the substream.
+struct D4Reader {
+  unsigned long long buf;  // next stream bits, left-aligned
+  int nb;                  // valid bits in buf (>= 32 after refill)
+  unsigned wi;             // index of the prefetched word
+  unsigned nxt;            // prefetched next word (off the dependency chain)
+  __device__ __forceinline__ void seek(const BitSrc &src, unsigned pos) {
+    const unsigned q = pos + src.adj;
+    wi = q >> 5;
+    const unsigned sh = q & 31;
+    buf = (((unsigned long long)src.word(wi) << 32) | src.word(wi + 1)) << sh;
+    nb = 64 - (int)sh;
+    wi += 2;
+    nxt = src.word(wi);
+  }
+  __device__ __forceinline__ void refill(const BitSrc &src) {
+    if (nb < 32) {
+      buf |= (unsigned long long)nxt << (32 - nb);
+      nb += 32;
+      nxt = src.word(++wi);
+    }
+  }
+  __device__ __forceinline__ void skip(unsigned adv) {
+    buf <<= adv;
+    nb -= (int)adv;
+  }
+};
+
+// Codeword at the top of `top` through the global tables (codewords longer
+// than the shared first level): length, and the symbol through `sym_out`.
+__device__ __forceinline__ unsigned d4_slow(unsigned top, const unsigned *__restrict__ lut,
+                                         const DecTab &tab, const uint16_t *__restrict__ sym, unsigned &sym_out) {
+  unsigned e = __ldg(lut + (top >> (32 - kLutBits)));
+  if (e & kLutL2Flag) e = __ldg(lut + (1 << kLutBits) + (e & 0xffffu) + ((top << kLutBits) >> (32 - tab.sub_bits)));
+  if (e == 0) {
+    for (int ll = kLutBits + 1; ll <= tab.maxl; ll++) {
+      const unsigned d = (top >> (32 - ll)) - tab.first[ll];
+      if (d < tab.count[ll]) {
+        sym_out = sym[tab.offset[ll] + d];
+        return (unsigned)ll;
+      }
+    }
+    sym_out = 0;
+    return 32u;  // unreachable for a complete code
+  }
+  sym_out = e & 0xffffu;
+  return (e >> 16) & 31u;
+}
+
+// Length of the codeword at the top of `top` (32 bits, left-aligned).
+__device__ __forceinline__ unsigned d4_len(unsigned top, const uint8_t *__restrict__ len12,
+                                           const unsigned *__restrict__ lut, const DecTab &tab,
+                                           const uint16_t *__restrict__ sym) {
+  const unsigned l = len12[top >> (32 - kLutBits)];
+  if (__builtin_expect(l != 0, 1)) return l;
+  unsigned sd;
+  return d4_slow(top, lut, tab, sym, sd);
+}
+
+// The codeword at the top of the reader (nb >= 32 valid bits) and how many
+// times it repeats back-to-back inside the valid bits (1 <= k <= lim).
+__device__ __forceinline__ void d4_run(unsigned long long buf, int nb, unsigned lim, const D4Smem &W,
+                                       const unsigned *__restrict__ lut, const DecTab &tab,
+                                       const uint16_t *__restrict__ sym, unsigned &s, unsigned &l, unsigned &k) {
+  const unsigned top = (unsigned)(buf >> 32);
+  const unsigned i = top >> (32 - kLutBits);
+  l = W.len12[i];
+  if (__builtin_expect(l == 0, 0)) {
+    l = d4_slow(top, lut, tab, sym, s);
+    k = 1;
+    return;
+  }
+  s = W.sym12[i];
+  // buf is periodic with period l over its first clz(buf ^ (buf << l)) + l bits
+  const unsigned long long x = buf ^ (buf << l);
+  const unsigned P = (x ? (unsigned)__clzll((long long)x) : 64u) + l;
+  const unsigned z = min(P, (unsigned)nb);
+  k = l == 1 ? z : max(__umulhi(z, tab.rcp[l]), 1u);  // floor(z / l)
+  k = min(k, lim);
+}
+
+__global__ void __launch_bounds__(kD4Threads, 6) k_decode4(const uint8_t *__restrict__ buf, unsigned long long buf_n,
+                                                       Geom g, const BlkP *__restrict__ blkp,
+                                                       const DecTab *__restrict__ tab,
+                                                       const uint16_t *__restrict__ sym,
+                                                       const unsigned *__restrict__ lut,
+                                                       const unsigned long long *__restrict__ part_bits,
+                                                       const unsigned long long *__restrict__ part_off,
+                                                       const unsigned long long *__restrict__ pay_off,
+                                                       uint16_t *__restrict__ codes,
+                                                       unsigned long long *__restrict__ part_zeros,
+                                                       uint16_t *__restrict__ zrow_out, WsStatus *st) {
+  constexpr int NS = kD4Threads;
+  __shared__ DecTab s_tab;
+  extern __shared__ __align__(16) unsigned char dyn4[];
+  D4Smem &W = *reinterpret_cast<D4Smem *>(dyn4);
+  count_launch(st);
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int64_t p = blockIdx.x;
+  if (t == 0) s_tab = *tab;
+  if (t < 32) W.zrow[t] = 0;
+  for (int i = t; i < (1 << kLutBits); i += NS) {
+    const unsigned e = __ldg(lut + i);
+    const bool direct = e != 0 && !(e & kLutL2Flag);
+    W.len12[i] = direct ? (uint8_t)((e >> 16) & 31u) : (uint8_t)0;
+    W.sym12[i] = (uint16_t)(e & 0xffffu);
+  }
+  int64_t b;
+  int pi;
+  part_of(g, p, b, pi);
+  if (blkp[b].trivial) {
+    if (t == 0) part_zeros[p] = 0;
+    if (t < 32) zrow_out[p * 32 + t] = 0;
+    return;
+  }
+  __syncthreads();
+  const BlockBox bb = block_box(g, b);
+  const int R = min(g.prow, bb.br - pi * g.prow), C = bb.bc;
+  const unsigned nsym = (unsigned)(R * C - 1);
+  const unsigned long long L64 = part_bits[p];
+  if (L64 > 32ull * (nsym + 1ull)) {  // longer than any valid substream (codewords <= 32 bits)
+    if (t == 0) set_err_at(st, PMZ_ERR_CORRUPT, 1, p);
+    return;
+  }
+  const unsigned L = (unsigned)L64;
+  D3P(0, clock64());
+  D3P(7, ((unsigned long long)L64 << 16) | 0);
+  BitSrc bs;
+  {
+    const uint8_t *src = buf + pay_off[b] + part_off[p];
+    const uintptr_t a = reinterpret_cast<uintptr_t>(src);
+    bs.base = reinterpret_cast<const uint8_t *>(a & ~(uintptr_t)3);
+    bs.adj = (unsigned)(8 * (a & 3));
+    bs.nbits = L64;
+    bs.end = buf + buf_n;
+  }
+  const unsigned nw = (L + 31) >> 5;            // 32-bit words of the substream
+  const unsigned wps = (nw + NS - 1) / NS;      // words per subsegment
+
+  // ---- 1. subsegment maps (warp w: subsegments 32 w .. 32 w + 31 = the
+  // contiguous words [wa, wb)).  Raw words arrive in coalesced batches of 32
+  // (lane i holds word bbase + i, the next batch is in flight) and are
+  // broadcast by shuffles; two words per step for instruction-level
+  // parallelism.  Pointer jumping needs nj = ceil(log2(32 / l0)) steps. ----
+  {
+    int nj = 0;
+    while ((32 >> nj) > s_tab.l0) nj++;
+    const unsigned wa = min(nw, (unsigned)(warp * 32) * wps), wb = min(nw, (unsigned)(warp * 32 + 32) * wps);
+    unsigned bbase = wa;
+    unsigned cur = bs.word(bbase + lane), nxb = bs.word(bbase + 32 + lane);
+    auto raw = [&](unsigned i) -> unsigned {  // i in [bbase, bbase + 64)
+      const unsigned d = i - bbase;
+      const unsigned v0 = __shfl_sync(0xffffffffu, cur, d & 31), v1 = __shfl_sync(0xffffffffu, nxb, d & 31);
+      return d < 32 ? v0 : v1;
+    };
+    auto advance = [&](unsigned need) {  // keep raw word `need` inside the window
+      if (need >= bbase + 64) {
+        bbase += 32;
+        cur = nxb;
+        nxb = bs.word(bbase + 32 + lane);
+      }
+    };
+    // word map of word w (raw words r0 r1 r2): parse position xa (>= 32: left the word at xa - 32), count c
+    auto word_map = [&](unsigned w, unsigned r0, unsigned r1, unsigned r2, unsigned &xa, unsigned &c) {
+      const unsigned s0 = __funnelshift_l(r1, r0, bs.adj), s1 = __funnelshift_l(r2, r1, bs.adj);
+      const unsigned top = __funnelshift_l(s1, s0, (unsigned)lane);
+      const bool in = 32u * w + (unsigned)lane < L;  // past the end: the offset carries over, nothing starts
+      xa = (unsigned)lane + (in ? d4_len(top, W.len12, lut, s_tab, sym) : 32u);
+      c = in ? 1u : 0u;
+    };
+    auto jump = [&](unsigned &xa, unsigned &c) {
+      const bool open = xa < 32u;
+      const unsigned src = open ? xa : (unsigned)lane;
+      const unsigned x2 = __shfl_sync(0xffffffffu, xa, src), c2 = __shfl_sync(0xffffffffu, c, src);
+      xa = open ? x2 : xa;
+      c += open ? c2 : 0u;
+    };
+    unsigned r0 = 0, r1 = 0;
+    if (wa < wb) {
+      r0 = raw(wa);
+      r1 = raw(wa + 1);
+    }
+    unsigned w = wa;
+    for (int j = warp * 32; j < warp * 32 + 32; j++) {
+      const unsigned w1 = min(nw, (unsigned)(j + 1) * wps);  // end of subsegment j
+      unsigned fx = (unsigned)lane, fc = 0;  // entry offset lane -> offset in word w, codewords so far
+      for (; w + 1 < w1; w += 2) {
+        advance(w + 3);
+        const unsigned r2 = raw(w + 2), r3 = raw(w + 3);
+        unsigned xa, c, xb, cb;
+        word_map(w, r0, r1, r2, xa, c);
+        word_map(w + 1, r1, r2, r3, xb, cb);
+        if (nj == 3) {
+#pragma unroll
+          for (int it = 0; it < 3; it++) {
+            jump(xa, c);
+            jump(xb, cb);
+          }
+        } else {
+          for (int it = 0; it < nj; it++) {
+            jump(xa, c);
+            jump(xb, cb);
+          }
+        }
+        // compose: entry -> fx in word w -> xa(fx) - 32 in word w + 1 -> xb(..) - 32 in word w + 2
+        fc += __shfl_sync(0xffffffffu, c, fx);
+        fx = __shfl_sync(0xffffffffu, xa, fx) - 32u;
+        fc += __shfl_sync(0xffffffffu, cb, fx);
+        fx = __shfl_sync(0xffffffffu, xb, fx) - 32u;
+        r0 = r2;
+        r1 = r3;
+      }
+      if (w < w1) {  // odd word count
+        advance(w + 2);
+        const unsigned r2 = raw(w + 2);
+        unsigned xa, c;
+        word_map(w, r0, r1, r2, xa, c);
+        for (int it = 0; it < nj; it++) jump(xa, c);
+        fc += __shfl_sync(0xffffffffu, c, fx);
+        fx = __shfl_sync(0xffffffffu, xa, fx) - 32u;
+        r0 = r1;
+        r1 = r2;
+        w++;
+      }
+      W.u.map[j][lane] = (uint16_t)((fc << 5) | fx);
+    }
+  }
+  __syncthreads();
+  D3P(1, clock64());
+
+  // ---- 2. the chain from entry 0: true entry and count of every subsegment ----
+  if (t == 0) {
+    unsigned e = 0;
+    for (int j = 0; j < NS; j++) {
+      W.ent[j] = e;
+      W.cnt[j] = 0;
+      if ((unsigned)j * wps >= nw) continue;  // empty subsegment: the offset carries over
+      const unsigned v = W.u.map[j][e];
+      W.cnt[j] = v >> 5;
+      e = v & 31u;
+    }
+    W.fin = e;  // offset after the last word: (end of the last codeword) mod 32
+  }
+  __syncthreads();
+  D3P(2, clock64());
+  const unsigned cnt = W.cnt[t];
+  const unsigned entry = min(L, 32u * wps * (unsigned)t + W.ent[t]);
+
+  // ---- 3. write pass: CTA scan of the counts, then every thread decodes its
+  // span into the shared tiles, counting code-0 symbols per row ----
+  unsigned incl = cnt;
+  for (int d = 1; d < 32; d <<= 1) {
+    const unsigned v = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += v;
+  }
+  if (lane == 31) W.wsum[warp] = incl;
+  __syncthreads();
+  unsigned base = 0, total = 0;
+#pragma unroll
+  for (int w = 0; w < kD4Warps; w++) {
+    if (w < warp) base += W.wsum[w];
+    total += W.wsum[w];
+  }
+  // spans of equal bit length start ~64 codes apart: the padding keeps their
+  // stores in distinct banks (the tiled layout would put them all in one)
+  const bool smem_ras = R * C <= kD4Ras;
+  uint16_t *ct = codes + tile_base(g, p, 0);
+  if (total != nsym || W.fin != (L & 31u)) {
+    if (t == 0)
+      set_err_at(st, total < nsym ? PMZ_ERR_TRUNCATED : PMZ_ERR_CORRUPT,
+                 10 + (total > nsym) + 2 * (total < nsym) + 4 * (W.fin != (L & 31u)), p);
+    return;
+  }
+  const unsigned e0 = base + incl - cnt + 1;  // raster index of the first symbol (anchor = 0)
+  if (smem_ras) {
+    if (cnt) {
+      D4Reader rd;
+      rd.seek(bs, entry);
+      unsigned idx = e0;
+      for (unsigned i = 0; i < cnt;) {
+        rd.refill(bs);
+        unsigned s, l, k;
+        d4_run(rd.buf, rd.nb, cnt - i, W, lut, s_tab, sym, s, l, k);
+        for (unsigned j = 0; j < k; j++) W.u.ras[d4_pad(idx + j)] = (uint16_t)s;
+        idx += k;
+        rd.skip(k * l);
+        i += k;
+      }
+    }
+    __syncthreads();
+    // code-0 symbols per row (the anchor, raster index 0, is not a code)
+    for (int r = warp; r < R; r += kD4Warps) {
+      unsigned z = 0;
+      for (int c = lane; c < C; c += 32) {
+        const unsigned q = (unsigned)(r * C + c);
+        z += (q != 0u && W.u.ras[d4_pad(q)] == 0) ? 1u : 0u;
+      }
+      for (int d = 16; d > 0; d >>= 1) z += __shfl_xor_sync(0xffffffffu, z, d);
+      if (lane == 0) W.zrow[r] = z;
+    }
+  } else if (cnt) {  // wide blocks: codes straight to the global tiles, zeros counted on the way
+    D4Reader rd;
+    rd.seek(bs, entry);
+    int r = (int)(e0 / (unsigned)C), c = (int)(e0 - (unsigned)r * C);
+    int zr = r;
+    unsigned zc = 0;  // code-0 symbols of row zr not yet added to W.zrow
+    for (unsigned i = 0; i < cnt;) {
+      rd.refill(bs);
+      unsigned s, l, k;
+      d4_run(rd.buf, rd.nb, cnt - i, W, lut, s_tab, sym, s, l, k);
+      for (unsigned j = 0; j < k; j++) {
+        ct[(c >> 5) * kTile + r * 32 + (c & 31)] = (uint16_t)s;
+        if (s == 0) {
+          if (r != zr) {
+            if (zc) atomicAdd(&W.zrow[zr], zc);
+            zr = r;
+            zc = 0;
+          }
+          zc++;
+        }
+        if (++c == C) { c = 0; r++; }
+      }
+      rd.skip(k * l);
+      i += k;
+    }
+    if (zc) atomicAdd(&W.zrow[zr], zc);
+  }
+  __syncthreads();
+  D3P(3, clock64());
+  if (t < 32) {
+    const unsigned z = W.zrow[t];
+    zrow_out[p * 32 + t] = (uint16_t)z;
+    unsigned zs = z;
+    for (int d = 16; d > 0; d >>= 1) zs += __shfl_xor_sync(0xffffffffu, zs, d);
+    if (t == 0) part_zeros[p] = zs;
+  }
+  if (smem_ras) {  // rows < R of every used tile, two codes per 4-byte store
+    const int nch = (C + 31) >> 5, per = R * 16;
+    for (int i = t; i < nch * per; i += NS) {
+      const int kc = i / per, o = i - kc * per, r = o >> 4, c = kc * 32 + 2 * (o & 15);
+      const unsigned q = (unsigned)(r * C + c);
+      const unsigned lo = c < C ? W.u.ras[d4_pad(q)] : 0u, hi = c + 1 < C ? W.u.ras[d4_pad(q + 1)] : 0u;
+      reinterpret_cast<unsigned *>(ct + kc * kTile)[o] = lo | (hi << 16);
+    }
+  }
+  D3P(4, clock64());
+}
+
+}  // namespace pmz

@@ -16,30 +16,6 @@
 
 namespace pmz {
 
-// 8 little-endian bytes at an arbitrary address: two aligned 8-byte loads and
-// a shift when both lie inside the buffer, else byte by byte.
-__device__ __forceinline__ double ld_f64_at(const uint8_t *p, const uint8_t *end) {
-  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
-  const unsigned sh = (unsigned)(a & 7) * 8;
-  const unsigned long long *q = reinterpret_cast<const unsigned long long *>(a & ~(uintptr_t)7);
-  if (sh == 0) return __longlong_as_double((long long)__ldg(q));
-  if (reinterpret_cast<const uint8_t *>(q + 2) <= end) {
-    const unsigned long long lo = __ldg(q), hi = __ldg(q + 1);
-    return __longlong_as_double((long long)((lo >> sh) | (hi << (64 - sh))));
-  }
-  unsigned long long v = 0;
-#pragma unroll
-  for (int i = 7; i >= 0; i--) v = (v << 8) | __ldg(p + i);
-  return __longlong_as_double((long long)v);
-}
-
-__device__ __forceinline__ double ld_f64_unaligned(const uint8_t *p) {
-  unsigned long long v = 0;
-#pragma unroll
-  for (int i = 7; i >= 0; i--) v = (v << 8) | __ldg(p + i);
-  return __longlong_as_double((long long)v);
-}
-
 // ---------------------------------------------------------------------------
 // k_reconstruct3: the same recurrence over the partition-tiled codes written
 // by k_decode3 (dec3.cuh).  Warp pair per partition:
@@ -107,7 +83,15 @@ __global__ void __launch_bounds__(kPPC * 64) k_reconstruct3(const uint8_t *__res
 
   if (role == 0) {
     // ------------------------------ producer ------------------------------
+    // balance values: 8-byte little-endian at a block-uniform byte alignment
+    // sh -> value i = (word i >> sh) | (word i+1 << (64 - sh)) of the aligned
+    // base; word i+1 may lie past the buffer only for the last values (byte
+    // path, rare, after the batched loads)
     const uint8_t *bal = buf + bal_off[b], *bend = buf + buf_n;
+    const uintptr_t ba = reinterpret_cast<uintptr_t>(bal);
+    const unsigned sh = (unsigned)(ba & 7) * 8;
+    const unsigned long long *qb = reinterpret_cast<const unsigned long long *>(ba & ~(uintptr_t)7);
+    const long long nw = (long long)((reinterpret_cast<uintptr_t>(bend) - (ba & ~(uintptr_t)7)) >> 3);  // whole words
     // balance index of the next code-0 of every row (warp-uniform registers):
     // partition base + zeros of the rows above (the decoder's per-row counts)
     unsigned rb[32];
@@ -130,26 +114,68 @@ __global__ void __launch_bounds__(kPPC * 64) k_reconstruct3(const uint8_t *__res
         bulk_commit();
       }
     };
+    // codes of a chunk, two rows per register (row 2j low half), padding = 1
+    auto load_codes = [&](int kc, unsigned (&c2)[16]) {
+      const bool inb = kc * 32 + lane < C;
+#pragma unroll
+      for (int j = 0; j < 16; j++) {
+        const unsigned lo = (inb && 2 * j < R) ? __ldg(&ct[kc * kTile + (2 * j) * 32 + lane]) : 1u;
+        const unsigned hi = (inb && 2 * j + 1 < R) ? __ldg(&ct[kc * kTile + (2 * j + 1) * 32 + lane]) : 1u;
+        c2[j] = lo | (hi << 16);
+      }
+    };
+    unsigned cn[16];
+    load_codes(0, cn);
     for (int kc = 0; kc < nch; kc++) {
       const int s = kc % kSlots;
+      unsigned cr2[16];
+#pragma unroll
+      for (int j = 0; j < 16; j++) cr2[j] = cn[j];
+      if (kc + 1 < nch) load_codes(kc + 1, cn);  // next chunk's codes in flight during this gather
+      if (kc == 0 && lane == 0) cr2[0] = (cr2[0] & 0xffff0000u) | kAnc;
       if (kc >= kSlots) {
         bar_sync_n(bar0 + kSlots + s, 64);
         flush(kc - kSlots);
         if (lane == 0) bulk_wait_read0();  // the store has read the slot
         __syncwarp();
       }
-      const bool inb = kc * 32 + lane < C;
-      uint16_t cr[32];
-#pragma unroll
-      for (int r = 0; r < 32; r++) cr[r] = (inb && r < R) ? __ldg(&ct[kc * kTile + r * 32 + lane]) : (uint16_t)1;
-      if (kc == 0 && lane == 0) cr[0] = kAnc;
+      // ballots and balance indices of all rows, then the loads in two
+      // batches of 16 rows (predicated, no branches between them)
+      unsigned zmask = 0;  // bit r: this lane's row r is a balance point
+      long long bi[32];
 #pragma unroll
       for (int r = 0; r < 32; r++) {
-        const bool z = cr[r] == 0;
+        const unsigned c = (cr2[r >> 1] >> ((r & 1) * 16)) & 0xffffu;
+        const bool z = c == 0;
         const unsigned zm = __ballot_sync(0xffffffffu, z);
-        if (z) W.val[s][r * 32 + lane] = ld_f64_at(bal + 8ull * (rb[r] + __popc(zm & ((1u << lane) - 1))), bend);
-        if (r < R) W.code[s][r * 32 + lane] = cr[r];
+        bi[r] = (long long)rb[r] + __popc(zm & ((1u << lane) - 1));
+        zmask |= (unsigned)z << r;
         rb[r] += __popc(zm);
+        if (r < R) W.code[s][r * 32 + lane] = (uint16_t)c;
+      }
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        unsigned long long lo[16], hi[16];
+#pragma unroll
+        for (int j = 0; j < 16; j++) {
+          const int r = h * 16 + j;
+          const bool z = (zmask >> r) & 1u;
+          lo[j] = z ? __ldg(qb + bi[r]) : 0ull;
+          hi[j] = (z && sh) ? __ldg(qb + min(bi[r] + 1, nw - 1)) : 0ull;
+        }
+#pragma unroll
+        for (int j = 0; j < 16; j++) {
+          const int r = h * 16 + j;
+          if ((zmask >> r) & 1u) {
+            unsigned long long v = sh ? ((lo[j] >> sh) | (hi[j] << (64 - sh))) : lo[j];
+            if (sh && bi[r] + 2 > nw) {  // last word partly outside the buffer
+              v = 0;
+              const uint8_t *pb = bal + 8ll * bi[r];
+              for (int i = 7; i >= 0; i--) v = (v << 8) | __ldg(pb + i);
+            }
+            W.val[s][r * 32 + lane] = __longlong_as_double((long long)v);
+          }
+        }
       }
       __syncwarp();
       bar_arrive_n(bar0 + s, 64);  // full[s]
