@@ -532,8 +532,8 @@ int pmz_index_blocks(const uint8_t *h, uint64_t n, const pmz_header *hd, uint64_
 
 namespace {
 struct DecLayout {
-  size_t status, blkp, part_bits, part_off, part_zeros, anchors, bal_off, pay_off, blk_nbal, tab, sym, lut, codes,
-      zrow, vh, total;
+  size_t status, blkp, part_bits, part_off, zflag, anchors, bal_off, pay_off, blk_nbal, tab, sym, lut, codes,
+      vtile, total;
 };
 DecLayout dec_layout(const Geom &g) {
   DecLayout L{};
@@ -547,7 +547,7 @@ DecLayout dec_layout(const Geom &g) {
   L.blkp = take(sizeof(BlkP) * (size_t)(g.nblocks + 1));
   L.part_bits = take(8 * (size_t)(g.nparts + 1));
   L.part_off = take(8 * (size_t)(g.nparts + 1));
-  L.part_zeros = take(8 * (size_t)(g.nparts + 1));
+  L.zflag = take(4 * (size_t)(g.nparts + 1));                     // decoder look-back flags
   L.anchors = take(8 * (size_t)(g.nparts + 1));
   L.bal_off = take(8 * (size_t)(g.nblocks + 1));
   L.pay_off = take(8 * (size_t)(g.nblocks + 1));
@@ -556,21 +556,18 @@ DecLayout dec_layout(const Geom &g) {
   L.sym = take(2 * kMaxAlpha);
   L.lut = take(4ull * ((1u << kLutBits) + kLut2Max));            // first + second level
   L.codes = take(2 * (size_t)g.nparts * (size_t)g.nct * kTile);  // partition-tiled
-  L.zrow = take(2 * 32 * (size_t)(g.nparts + 1));                  // code-0 count per partition row
-  L.vh = take(8 * (size_t)g.nparts * (size_t)g.nct * kTile);        // reconstructed values, tiled
+  L.vtile = take(8 * (size_t)g.nparts * (size_t)g.nct * kTile);   // per-element addends, then reconstructed values
   L.total = o;
   return L;
 }
 template <int PK>
-int launch_recon(const KParams &k, unsigned grid, cudaStream_t st, const uint8_t *d_buf, uint64_t n, const Geom &G,
-                 int m, void *d_ws, const DecLayout &L, float *d_out) {
-  CK(cudaFuncSetAttribute(k_reconstruct3<PK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDsc3Smem));
-  k_reconstruct3<PK><<<grid, kPPC * 64, kDsc3Smem, st>>>(
-      d_buf, n, G, k, m, at<BlkP>(d_ws, L.blkp), at<uint16_t>(d_ws, L.codes), at<uint16_t>(d_ws, L.zrow),
-      at<double>(d_ws, L.anchors), at<unsigned long long>(d_ws, L.part_zeros),
-      at<unsigned long long>(d_ws, L.bal_off), at<unsigned long long>(d_ws, L.blk_nbal), d_out,
-      at<double>(d_ws, L.vh), at<WsStatus>(d_ws, L.status));
-  k_inv<<<(unsigned)G.nparts, 256, 0, st>>>(G, at<BlkP>(d_ws, L.blkp), at<double>(d_ws, L.vh), d_out,
+int launch_recon(const KParams &k, unsigned grid, cudaStream_t st, const Geom &G, void *d_ws, const DecLayout &L,
+                 float *d_out) {
+  CK(cudaFuncSetAttribute(k_reconstruct4<PK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDsc4Smem));
+  k_reconstruct4<PK><<<grid, kPPC * 64, kDsc4Smem, st>>>(
+      G, k, at<BlkP>(d_ws, L.blkp), at<uint16_t>(d_ws, L.codes), at<double>(d_ws, L.vtile),
+      at<double>(d_ws, L.anchors), d_out, at<double>(d_ws, L.vtile), at<WsStatus>(d_ws, L.status));
+  k_inv<<<(unsigned)G.nparts, 256, 0, st>>>(G, at<BlkP>(d_ws, L.blkp), at<double>(d_ws, L.vtile), d_out,
                                             at<WsStatus>(d_ws, L.status));
   return PMZ_OK;
 }
@@ -616,24 +613,26 @@ int pmz_decompress(const uint8_t *d_buf, uint64_t n, const pmz_header *hdr, doub
   WsStatus *S = at<WsStatus>(d_ws, L.status);
   CK(cudaMemsetAsync(S, 0, sizeof(WsStatus), st));
   if (G.nblocks > 0) {
-    k_dec_blocks<<<(unsigned)((G.nblocks + 127) / 128), 128, 0, st>>>(
+    k_dec_blocks<<<(unsigned)((G.nblocks + 3) / 4), 128, 0, st>>>(
         d_buf, n, G, k, (const unsigned long long *)d_boff, at<BlkP>(d_ws, L.blkp),
         at<unsigned long long>(d_ws, L.part_bits), at<unsigned long long>(d_ws, L.part_off),
         at<double>(d_ws, L.anchors), at<unsigned long long>(d_ws, L.bal_off),
         at<unsigned long long>(d_ws, L.pay_off), at<unsigned long long>(d_ws, L.blk_nbal), S);
     k_dec_tables<<<1, 1024, 0, st>>>(d_buf + hdr->lens_offset, (int)hdr->m, at<DecTab>(d_ws, L.tab),
                                      at<uint16_t>(d_ws, L.sym), at<unsigned>(d_ws, L.lut), S);
+    CK(cudaMemsetAsync(at<unsigned>(d_ws, L.zflag), 0, 4 * (size_t)G.nparts, st));
     CK(cudaFuncSetAttribute(k_decode4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kD4Smem));
     k_decode4<<<(unsigned)G.nparts, kD4Threads, kD4Smem, st>>>(
         d_buf, n, G, at<BlkP>(d_ws, L.blkp), at<DecTab>(d_ws, L.tab), at<uint16_t>(d_ws, L.sym),
         at<unsigned>(d_ws, L.lut), at<unsigned long long>(d_ws, L.part_bits),
         at<unsigned long long>(d_ws, L.part_off), at<unsigned long long>(d_ws, L.pay_off),
-        at<uint16_t>(d_ws, L.codes), at<unsigned long long>(d_ws, L.part_zeros), at<uint16_t>(d_ws, L.zrow), S);
+        at<unsigned long long>(d_ws, L.bal_off), at<unsigned long long>(d_ws, L.blk_nbal), 1 << ((int)hdr->m - 1),
+        k.two_ba, at<unsigned>(d_ws, L.zflag), at<uint16_t>(d_ws, L.codes), at<double>(d_ws, L.vtile), S);
     const unsigned rgrid = (unsigned)((G.nparts + kPPC - 1) / kPPC);
     int s2;
-    if (k.init_model == 3) s2 = launch_recon<3>(k, rgrid, st, d_buf, n, G, (int)hdr->m, d_ws, L, d_out);
-    else if (k.init_model == 1) s2 = launch_recon<1>(k, rgrid, st, d_buf, n, G, (int)hdr->m, d_ws, L, d_out);
-    else s2 = launch_recon<0>(k, rgrid, st, d_buf, n, G, (int)hdr->m, d_ws, L, d_out);
+    if (k.init_model == 3) s2 = launch_recon<3>(k, rgrid, st, G, d_ws, L, d_out);
+    else if (k.init_model == 1) s2 = launch_recon<1>(k, rgrid, st, G, d_ws, L, d_out);
+    else s2 = launch_recon<0>(k, rgrid, st, G, d_ws, L, d_out);
     if (s2) return s2;
   }
   int s = launch_check();

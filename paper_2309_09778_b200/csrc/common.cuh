@@ -40,6 +40,7 @@ struct Geom {
 // 1024 elements; rows >= R / columns >= C are padding).  A chunk is then one
 // bulk copy.
 constexpr int kTile = 1024;
+constexpr uint16_t kAnc = 0xFFFF;  // code-tile marker of the partition anchor (raster element 0)
 __host__ __device__ __forceinline__ int64_t tile_base(const Geom &g, int64_t p, int kc) {
   return (p * g.nct + kc) * (int64_t)kTile;
 }

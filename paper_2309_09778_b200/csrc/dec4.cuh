@@ -57,9 +57,17 @@ struct D4Smem {
   unsigned ent[kD4Threads], cnt[kD4Threads];
   unsigned zrow[32];
   unsigned wsum[kD4Warps];
+  unsigned long long zb;                   // code-0 symbols of the earlier partitions of the block
   unsigned fin;                            // exit offset after the last word
 };
 constexpr size_t kD4Smem = sizeof(D4Smem);
+
+// Decoupled look-back flags: code-0 count + 1 once known, kD4Poison when the
+// partition failed (reset to 0 before every launch).
+constexpr unsigned kD4Poison = 0xffffffffu;
+__device__ __forceinline__ void d4_publish(unsigned *f, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(f), "r"(v) : "memory");
+}
 
 // Register bit reader at an arbitrary bit position of the substream.
 struct D4Reader {
@@ -150,9 +158,11 @@ __global__ void __launch_bounds__(kD4Threads, 6) k_decode4(const uint8_t *__rest
                                                        const unsigned long long *__restrict__ part_bits,
                                                        const unsigned long long *__restrict__ part_off,
                                                        const unsigned long long *__restrict__ pay_off,
-                                                       uint16_t *__restrict__ codes,
-                                                       unsigned long long *__restrict__ part_zeros,
-                                                       uint16_t *__restrict__ zrow_out, WsStatus *st) {
+                                                       const unsigned long long *__restrict__ bal_off,
+                                                       const unsigned long long *__restrict__ blk_nbal,
+                                                       int center, double two_ba, unsigned *zflag,
+                                                       uint16_t *__restrict__ codes, double *__restrict__ vtile,
+                                                       WsStatus *st) {
   constexpr int NS = kD4Threads;
   __shared__ DecTab s_tab;
   extern __shared__ __align__(16) unsigned char dyn4[];
@@ -171,18 +181,17 @@ __global__ void __launch_bounds__(kD4Threads, 6) k_decode4(const uint8_t *__rest
   int64_t b;
   int pi;
   part_of(g, p, b, pi);
-  if (blkp[b].trivial) {
-    if (t == 0) part_zeros[p] = 0;
-    if (t < 32) zrow_out[p * 32 + t] = 0;
-    return;
-  }
+  if (blkp[b].trivial) return;
   __syncthreads();
   const BlockBox bb = block_box(g, b);
   const int R = min(g.prow, bb.br - pi * g.prow), C = bb.bc;
   const unsigned nsym = (unsigned)(R * C - 1);
   const unsigned long long L64 = part_bits[p];
   if (L64 > 32ull * (nsym + 1ull)) {  // longer than any valid substream (codewords <= 32 bits)
-    if (t == 0) set_err_at(st, PMZ_ERR_CORRUPT, 1, p);
+    if (t == 0) {
+      set_err_at(st, PMZ_ERR_CORRUPT, 1, p);
+      d4_publish(zflag + p, kD4Poison);  // later partitions of the block must not wait forever
+    }
     return;
   }
   const unsigned L = (unsigned)L64;
@@ -329,9 +338,11 @@ __global__ void __launch_bounds__(kD4Threads, 6) k_decode4(const uint8_t *__rest
   const bool smem_ras = R * C <= kD4Ras;
   uint16_t *ct = codes + tile_base(g, p, 0);
   if (total != nsym || W.fin != (L & 31u)) {
-    if (t == 0)
+    if (t == 0) {
       set_err_at(st, total < nsym ? PMZ_ERR_TRUNCATED : PMZ_ERR_CORRUPT,
                  10 + (total > nsym) + 2 * (total < nsym) + 4 * (W.fin != (L & 31u)), p);
+      d4_publish(zflag + p, kD4Poison);
+    }
     return;
   }
   const unsigned e0 = base + incl - cnt + 1;  // raster index of the first symbol (anchor = 0)
@@ -390,20 +401,100 @@ __global__ void __launch_bounds__(kD4Threads, 6) k_decode4(const uint8_t *__rest
   }
   __syncthreads();
   D3P(3, clock64());
+  // ---- 4. balance values (D9: block list, partitions in order, raster order
+  // within).  This partition publishes its code-0 count; it adds up the counts
+  // of the earlier partitions of its block (decoupled look-back: those are
+  // lower-numbered CTAs, already resident or finished) ----
   if (t < 32) {
     const unsigned z = W.zrow[t];
-    zrow_out[p * 32 + t] = (uint16_t)z;
-    unsigned zs = z;
-    for (int d = 16; d > 0; d >>= 1) zs += __shfl_xor_sync(0xffffffffu, zs, d);
-    if (t == 0) part_zeros[p] = zs;
+    unsigned incl = z;
+    for (int d = 1; d < 32; d <<= 1) {
+      const unsigned v = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += v;
+    }
+    W.zrow[t] = incl - z;  // code-0 symbols of the rows above
+    const unsigned zp = __shfl_sync(0xffffffffu, incl, 31);
+    if (t == 0) {
+      d4_publish(zflag + p, zp + 1u);
+      unsigned long long zb = 0;
+      bool poisoned = false;
+      for (int64_t q = first_part(g, b); q < p; q++) {
+        unsigned v;
+        long long spins = 0;
+        do {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(zflag + q) : "memory");
+        } while (v == 0u && ++spins < (1ll << 28));
+        if (v == 0u) {  // never published (cannot happen): fail instead of hanging
+          set_err_at(st, PMZ_ERR_CORRUPT, 31, p);
+          v = kD4Poison;
+        }
+        if (v == kD4Poison) poisoned = true;  // that partition failed and reported its error
+        zb += v - 1u;
+      }
+      const unsigned long long nb = blk_nbal[b];
+      const bool last = pi == bb.np - 1;
+      if (!poisoned && (zb + zp > nb || (last && zb + zp != nb)))
+        set_err_at(st, zb + zp > nb ? PMZ_ERR_BALANCE_UNDERFLOW : PMZ_ERR_CORRUPT, 30, p);
+      if (poisoned || zb + zp > nb || (last && zb + zp != nb)) zb = ~0ull;
+      W.zb = zb;
+    }
   }
-  if (smem_ras) {  // rows < R of every used tile, two codes per 4-byte store
-    const int nch = (C + 31) >> 5, per = R * 16;
-    for (int i = t; i < nch * per; i += NS) {
-      const int kc = i / per, o = i - kc * per, r = o >> 4, c = kc * 32 + 2 * (o & 15);
-      const unsigned q = (unsigned)(r * C + c);
-      const unsigned lo = c < C ? W.u.ras[d4_pad(q)] : 0u, hi = c + 1 < C ? W.u.ras[d4_pad(q + 1)] : 0u;
-      reinterpret_cast<unsigned *>(ct + kc * kTile)[o] = lo | (hi << 16);
+  __syncthreads();
+  const unsigned long long zb = W.zb;
+  if (zb == ~0ull) return;
+  D3P(5, clock64());
+  // codes and per-element addends, tiled for the reconstruction: the balance
+  // value at code-0 positions, (code - center) * 2 b_a elsewhere (D6)
+  {
+    const uint8_t *bal = buf + bal_off[b];
+    const uintptr_t ba = reinterpret_cast<uintptr_t>(bal);
+    const unsigned sh = (unsigned)(ba & 7) * 8;
+    const unsigned long long *qb = reinterpret_cast<const unsigned long long *>(ba & ~(uintptr_t)7);
+    const long long nwd = (long long)((reinterpret_cast<uintptr_t>(buf + buf_n) - (ba & ~(uintptr_t)7)) >> 3);
+    const int nch = (C + 31) >> 5;
+    double *vt = vtile + tile_base(g, p, 0);
+    // a warp takes a row, four 32-column chunks at a time: ballots and ranks
+    // first, then the (independent) balance loads, then the coalesced stores
+    auto ldbal = [&](long long i) -> unsigned long long {
+      unsigned long long u = __ldg(qb + i);
+      if (sh) {
+        if (i + 2 <= nwd) u = (u >> sh) | (__ldg(qb + i + 1) << (64 - sh));
+        else {  // the value ends the buffer: byte loads
+          u = 0;
+          for (int k = 7; k >= 0; k--) u = (u << 8) | __ldg(bal + 8 * i + k);
+        }
+      }
+      return u;
+    };
+    for (int r = warp; r < R; r += kD4Warps) {
+      unsigned long long base = zb + W.zrow[r];
+      for (int k0 = 0; k0 < nch; k0 += 4) {
+        unsigned code[4];
+        long long bi[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          const int c = (k0 + u) * 32 + lane;
+          unsigned cd = 1u;
+          if (c < C) cd = smem_ras ? W.u.ras[d4_pad((unsigned)(r * C + c))] : ct[(k0 + u) * kTile + r * 32 + lane];
+          if (r == 0 && c == 0) cd = kAnc;
+          code[u] = cd;
+          const unsigned zm = __ballot_sync(0xffffffffu, cd == 0u);
+          bi[u] = cd == 0u ? (long long)(base + __popc(zm & ((1u << lane) - 1u))) : -1ll;
+          base += __popc(zm);
+        }
+        unsigned long long val[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) val[u] = bi[u] >= 0 ? ldbal(bi[u]) : 0ull;
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          const int kc = k0 + u;
+          if (kc < nch) {
+            const double dq = __dmul_rn((double)((int)code[u] - center), two_ba);
+            vt[kc * kTile + r * 32 + lane] = bi[u] >= 0 ? __longlong_as_double((long long)val[u]) : dq;
+            ct[kc * kTile + r * 32 + lane] = (uint16_t)code[u];
+          }
+        }
+      }
     }
   }
   D3P(4, clock64());

@@ -38,51 +38,88 @@ __host__ __device__ __forceinline__ unsigned lut_entry(int l, unsigned sym) {
   return sym | ((unsigned)l << 16) | (M << 21);
 }
 
-// D1: per-block record heads -> transform parameters and partition tables.
+// D1: per-block record heads -> transform parameters and partition tables,
+// one warp per block: the three CR log2 of derive_params on three lanes, the
+// partition entries on all lanes with a warp scan of their byte lengths.
 __global__ void k_dec_blocks(const uint8_t *__restrict__ buf, unsigned long long n, Geom g, KParams k,
                              const unsigned long long *__restrict__ boff, BlkP *blkp,
                              unsigned long long *part_bits, unsigned long long *part_off, double *anchors,
                              unsigned long long *bal_off, unsigned long long *pay_off,
                              unsigned long long *blk_nbal, WsStatus *st) {
-  int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (b >= g.nblocks) return;
-  unsigned long long o = boff[b];
-  BlockBox bb = block_box(g, b);
-  int64_t p0 = first_part(g, b);
+  const unsigned long long o = boff[b];
+  const BlockBox bb = block_box(g, b);
+  const int64_t p0 = first_part(g, b);
   BlkP P{};
-  if (o >= n) { set_err_at(st, PMZ_ERR_CORRUPT, 41, b); P.trivial = 1; blkp[b] = P; return; }
-  uint8_t triv = buf[o];
+  P.trivial = 1;
+  const unsigned long long head = 1 + 16 + 24ull * bb.np + 8;
+  const uint8_t triv = o < n ? buf[o] : (uint8_t)2;
   if (triv == 1) {
-    P.trivial = 1;
-    blkp[b] = P;
-    for (int i = 0; i < bb.np; i++) { part_bits[p0 + i] = 0; part_off[p0 + i] = 0; }
-    blk_nbal[b] = 0;
+    for (int i = lane; i < bb.np; i += 32) { part_bits[p0 + i] = 0; part_off[p0 + i] = 0; }
+    if (lane == 0) { blkp[b] = P; blk_nbal[b] = 0; }
     return;
   }
-  unsigned long long head = 1 + 16 + 24ull * bb.np + 8;
-  if (triv != 0 || o + head > n) { set_err_at(st, PMZ_ERR_CORRUPT, 42, b); P.trivial = 1; blkp[b] = P; return; }
-  double fp = get_f64(buf + o + 1), fn = get_f64(buf + o + 9);
+  if (triv != 0 || o + head > n) {
+    if (lane == 0) { set_err_at(st, PMZ_ERR_CORRUPT, 41, b); blkp[b] = P; }
+    return;
+  }
+  const double fp = get_f64(buf + o + 1), fn = get_f64(buf + o + 9);
   if (!(fp > 0.0) || !(fn > 0.0) || !isfinite(fp) || !isfinite(fn)) {
-    set_err_at(st, PMZ_ERR_CORRUPT, 43, b); P.trivial = 1; blkp[b] = P; return;
+    if (lane == 0) { set_err_at(st, PMZ_ERR_CORRUPT, 43, b); blkp[b] = P; }
+    return;
   }
-  derive_params(fp, fn, k, P, &st->unresolved);
-  blkp[b] = P;
-  unsigned long long pb = 0;
-  for (int i = 0; i < bb.np; i++) {
-    const uint8_t *e = buf + o + 17 + 24ull * i;
-    unsigned long long off = get_u64(e), len = get_u64(e + 8);
-    if (off != pb * 8) set_err_at(st, PMZ_ERR_CORRUPT, 44, b);
-    part_off[p0 + i] = pb;
-    part_bits[p0 + i] = len;
-    anchors[p0 + i] = get_f64(e + 16);
-    pb += (len + 7) / 8;
+  // derive_params (compress.cuh) with its three log2 on lanes 0..2
+  const double la = lane < 3 ? pmz_log2_d(lane == 0 ? fp : (lane == 1 ? fn : __dsub_rn(fp, k.eps0)), &st->unresolved)
+                             : 0.0;
+  const double lg_pos = __shfl_sync(0xffffffffu, la, 0), lg_neg = __shfl_sync(0xffffffffu, la, 1),
+               lg_pe = __shfl_sync(0xffffffffu, la, 2);
+  P.factor_pos = fp;
+  P.factor_neg = fn;
+  P.lg_pos = lg_pos;
+  P.lg_neg = lg_neg;
+  P.zero_code = __dadd_rn(-126.0, lg_pos);            // transform.py:121
+  P.zero_threshold = __dadd_rn(P.zero_code, k.b_a);   // :122
+  P.boundary = __dsub_rn(__dadd_rn(lg_neg, lg_pe), k.b_a);  // :123
+  P.trivial = 0;
+  if (lane == 0) blkp[b] = P;
+  unsigned long long pb = 0;  // payload bytes of the partitions before this chunk of 32
+  bool bad = false;
+  for (int i0 = 0; i0 < bb.np; i0 += 32) {
+    const int i = i0 + lane;
+    unsigned long long off = 0, len = 0;
+    double anc = 0.0;
+    if (i < bb.np) {
+      const uint8_t *e = buf + o + 17 + 24ull * i;
+      off = get_u64(e);
+      len = get_u64(e + 8);
+      anc = get_f64(e + 16);
+    }
+    const unsigned long long by = (len + 7) / 8;
+    unsigned long long incl = by;
+    for (int d = 1; d < 32; d <<= 1) {
+      const unsigned long long v = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += v;
+    }
+    const unsigned long long excl = pb + incl - by;
+    if (i < bb.np) {
+      bad |= off != excl * 8;
+      part_off[p0 + i] = excl;
+      part_bits[p0 + i] = len;
+      anchors[p0 + i] = anc;
+    }
+    pb += __shfl_sync(0xffffffffu, incl, 31);
   }
-  unsigned long long nb = get_u64(buf + o + 17 + 24ull * bb.np);
-  if (nb > (unsigned long long)bb.br * bb.bc) { set_err_at(st, PMZ_ERR_CORRUPT, 45, b); nb = 0; }
-  blk_nbal[b] = nb;
-  bal_off[b] = o + head;
-  pay_off[b] = o + head + 8 * nb;
-  if (o + head + 8 * nb + pb > n) set_err(st, PMZ_ERR_TRUNCATED);
+  if (__any_sync(0xffffffffu, bad) && lane == 0) set_err_at(st, PMZ_ERR_CORRUPT, 44, b);
+  if (lane == 0) {
+    unsigned long long nb = get_u64(buf + o + 17 + 24ull * bb.np);
+    if (nb > (unsigned long long)bb.br * bb.bc) { set_err_at(st, PMZ_ERR_CORRUPT, 45, b); nb = 0; }
+    blk_nbal[b] = nb;
+    bal_off[b] = o + head;
+    pay_off[b] = o + head + 8 * nb;
+    if (o + head + 8 * nb + pb > n) set_err(st, PMZ_ERR_TRUNCATED);
+  }
 }
 
 // D2: canonical decode tables from the header's code lengths.

@@ -26,7 +26,6 @@ namespace pmz {
 #endif
 constexpr int kPPC = 2;      // partitions (warp pairs) per CTA
 constexpr int kSlots = PMZ_WS_SLOTS;    // ring depth
-constexpr uint16_t kAnc = 0xFFFF;
 
 struct alignas(128) PRing {
   double v[kSlots][kTile];         // TRUE values

@@ -88,8 +88,10 @@ if hasattr(codec.lib, "pmz_d3prof_read") and not a.compress:
     ph = np.diff(A[:, :5], axis=1)
     print("d3prof parts", len(A), "start spread (cyc) p50/max", np.percentile(A[:, 0] - t0, 50), (A[:, 0] - t0).max(),
           "end max", (A[:, 4] - t0).max())
-    for i, nm in enumerate(["maps", "chain", "write", "copy"]):
-        print(f"   {nm:7s} cycles p50 {np.percentile(ph[:, i], 50):9.0f} p90 {np.percentile(ph[:, i], 90):9.0f} max {ph[:, i].max():9.0f}")
+    T = np.stack([A[:, 0], A[:, 1], A[:, 2], A[:, 3], A[:, 5], A[:, 4]], 1)
+    ph = np.diff(T, axis=1)
+    for i, nm in enumerate(["maps", "chain", "write", "lookback", "gather"]):
+        print(f"   {nm:8s} cycles p50 {np.percentile(ph[:, i], 50):9.0f} p90 {np.percentile(ph[:, i], 90):9.0f} max {ph[:, i].max():9.0f}")
 mode = "compress" if a.compress else "decompress"
 print(f"== {lib} {a.field} {mode}: {tot * 1e3:.1f} us/call  {x.numel() * 4 / tot / 1e6:.1f} GB/s  "
       f"CR={info.nbytes / (x.numel() * 4):.4f}  hash={dig}")
