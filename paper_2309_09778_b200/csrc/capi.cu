@@ -748,3 +748,10 @@ extern "C" PMZ_API int pmz_d3prof_read(void *host, uint64_t bytes) {
   return cudaMemcpyFromSymbol(host, pmz::g_d3prof, bytes) == cudaSuccess ? 0 : -1;
 }
 #endif
+
+#ifdef PMZ_CMP_PROFILE
+// experiments only: the codebook kernel's phase timestamps
+extern "C" PMZ_API int pmz_cbprof_read(void *host) {
+  return cudaMemcpyFromSymbol(host, pmz::g_cb_prof, 8 * sizeof(long long)) == cudaSuccess ? 0 : -1;
+}
+#endif

@@ -210,91 +210,80 @@ __global__ void __launch_bounds__(kD4Threads, 6) k_decode4(const uint8_t *__rest
   const unsigned wps = (nw + NS - 1) / NS;      // words per subsegment
 
   // ---- 1. subsegment maps (warp w: subsegments 32 w .. 32 w + 31 = the
-  // contiguous words [wa, wb)).  Raw words arrive in coalesced batches of 32
-  // (lane i holds word bbase + i, the next batch is in flight) and are
+  // contiguous words [wa, wb)).  Stream words arrive in coalesced batches of
+  // 32 (lane i holds word bbase + i, the next batch is in flight) and are
   // broadcast by shuffles; two words per step for instruction-level
-  // parallelism.  Pointer jumping needs nj = ceil(log2(32 / l0)) steps. ----
+  // parallelism.  A parse state is packed as (count << 8) | position, so a
+  // pointer-jumping step or a composition is one shuffle; nj =
+  // ceil(log2(32 / l0)) jumps resolve a word. ----
   {
     int nj = 0;
     while ((32 >> nj) > s_tab.l0) nj++;
     const unsigned wa = min(nw, (unsigned)(warp * 32) * wps), wb = min(nw, (unsigned)(warp * 32 + 32) * wps);
     unsigned bbase = wa;
-    unsigned cur = bs.word(bbase + lane), nxb = bs.word(bbase + 32 + lane);
-    auto raw = [&](unsigned i) -> unsigned {  // i in [bbase, bbase + 64)
+    auto sword = [&](unsigned i) -> unsigned { return __funnelshift_l(bs.word(i + 1), bs.word(i), bs.adj); };
+    unsigned cur = sword(bbase + lane), nxb = sword(bbase + 32 + lane);
+    auto sw = [&](unsigned i) -> unsigned {  // stream word i, i in [bbase, bbase + 64)
       const unsigned d = i - bbase;
       const unsigned v0 = __shfl_sync(0xffffffffu, cur, d & 31), v1 = __shfl_sync(0xffffffffu, nxb, d & 31);
       return d < 32 ? v0 : v1;
     };
-    auto advance = [&](unsigned need) {  // keep raw word `need` inside the window
+    auto advance = [&](unsigned need) {  // keep stream word `need` inside the window
       if (need >= bbase + 64) {
         bbase += 32;
         cur = nxb;
-        nxb = bs.word(bbase + 32 + lane);
+        nxb = sword(bbase + 32 + lane);
       }
     };
-    // word map of word w (raw words r0 r1 r2): parse position xa (>= 32: left the word at xa - 32), count c
-    auto word_map = [&](unsigned w, unsigned r0, unsigned r1, unsigned r2, unsigned &xa, unsigned &c) {
-      const unsigned s0 = __funnelshift_l(r1, r0, bs.adj), s1 = __funnelshift_l(r2, r1, bs.adj);
+    // word w's parse from bit `lane`: (count << 8) | position (>= 32: left the word at position - 32)
+    auto word_init = [&](unsigned w, unsigned s0, unsigned s1) -> unsigned {
       const unsigned top = __funnelshift_l(s1, s0, (unsigned)lane);
       const bool in = 32u * w + (unsigned)lane < L;  // past the end: the offset carries over, nothing starts
-      xa = (unsigned)lane + (in ? d4_len(top, W.len12, lut, s_tab, sym) : 32u);
-      c = in ? 1u : 0u;
+      return in ? ((unsigned)lane + d4_len(top, W.len12, lut, s_tab, sym)) | 0x100u : (unsigned)lane + 32u;
     };
-    auto jump = [&](unsigned &xa, unsigned &c) {
-      const bool open = xa < 32u;
-      const unsigned src = open ? xa : (unsigned)lane;
-      const unsigned x2 = __shfl_sync(0xffffffffu, xa, src), c2 = __shfl_sync(0xffffffffu, c, src);
-      xa = open ? x2 : xa;
-      c += open ? c2 : 0u;
+    auto jump = [&](unsigned &pk) {
+      const unsigned x = pk & 0xffu;
+      const bool open = x < 32u;
+      const unsigned v = __shfl_sync(0xffffffffu, pk, open ? x : (unsigned)lane);
+      pk = open ? v + (pk & ~0xffu) : pk;
     };
-    unsigned r0 = 0, r1 = 0;
+    auto compose = [&](unsigned &F, unsigned pk) {  // entry -> F.pos in this word -> pk(F.pos) - 32 in the next
+      const unsigned v = __shfl_sync(0xffffffffu, pk, F & 0xffu);
+      F = v - 32u + (F & ~0xffu);
+    };
+    unsigned s0 = 0, s1 = 0;
     if (wa < wb) {
-      r0 = raw(wa);
-      r1 = raw(wa + 1);
+      s0 = sw(wa);
+      s1 = sw(wa + 1);
     }
     unsigned w = wa;
     for (int j = warp * 32; j < warp * 32 + 32; j++) {
       const unsigned w1 = min(nw, (unsigned)(j + 1) * wps);  // end of subsegment j
-      unsigned fx = (unsigned)lane, fc = 0;  // entry offset lane -> offset in word w, codewords so far
+      unsigned F = (unsigned)lane;  // entry offset lane -> (codewords so far << 8) | offset in word w
       for (; w + 1 < w1; w += 2) {
         advance(w + 3);
-        const unsigned r2 = raw(w + 2), r3 = raw(w + 3);
-        unsigned xa, c, xb, cb;
-        word_map(w, r0, r1, r2, xa, c);
-        word_map(w + 1, r1, r2, r3, xb, cb);
-        if (nj == 3) {
-#pragma unroll
-          for (int it = 0; it < 3; it++) {
-            jump(xa, c);
-            jump(xb, cb);
-          }
-        } else {
-          for (int it = 0; it < nj; it++) {
-            jump(xa, c);
-            jump(xb, cb);
-          }
+        const unsigned s2 = sw(w + 2), s3 = sw(w + 3);
+        unsigned pa = word_init(w, s0, s1), pb = word_init(w + 1, s1, s2);
+        for (int it = 0; it < nj; it++) {
+          jump(pa);
+          jump(pb);
         }
-        // compose: entry -> fx in word w -> xa(fx) - 32 in word w + 1 -> xb(..) - 32 in word w + 2
-        fc += __shfl_sync(0xffffffffu, c, fx);
-        fx = __shfl_sync(0xffffffffu, xa, fx) - 32u;
-        fc += __shfl_sync(0xffffffffu, cb, fx);
-        fx = __shfl_sync(0xffffffffu, xb, fx) - 32u;
-        r0 = r2;
-        r1 = r3;
+        compose(F, pa);
+        compose(F, pb);
+        s0 = s2;
+        s1 = s3;
       }
       if (w < w1) {  // odd word count
         advance(w + 2);
-        const unsigned r2 = raw(w + 2);
-        unsigned xa, c;
-        word_map(w, r0, r1, r2, xa, c);
-        for (int it = 0; it < nj; it++) jump(xa, c);
-        fc += __shfl_sync(0xffffffffu, c, fx);
-        fx = __shfl_sync(0xffffffffu, xa, fx) - 32u;
-        r0 = r1;
-        r1 = r2;
+        const unsigned s2 = sw(w + 2);
+        unsigned pa = word_init(w, s0, s1);
+        for (int it = 0; it < nj; it++) jump(pa);
+        compose(F, pa);
+        s0 = s1;
+        s1 = s2;
         w++;
       }
-      W.u.map[j][lane] = (uint16_t)((fc << 5) | fx);
+      W.u.map[j][lane] = (uint16_t)(((F >> 8) << 5) | (F & 0xffu));
     }
   }
   __syncthreads();

@@ -38,11 +38,12 @@ __global__ void __launch_bounds__(NT) k_val_hist(Geom g, const BlkP *__restrict_
   }
 }
 
-// Bitonic sort of n (power of two) u64 keys, ascending, by one CTA.
-__device__ void bitonic_sort(unsigned long long *a, int n) {
+// Bitonic sort of n (power of two) u64 keys, ascending, by the first nt
+// threads of a CTA (the others have exited).
+__device__ void bitonic_sort(unsigned long long *a, int n, int nt) {
   for (int k = 2; k <= n; k <<= 1) {
     for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      for (int i = threadIdx.x; i < n; i += nt) {
         int l = i ^ j;
         if (l > i) {
           unsigned long long x = a[i], y = a[l];
@@ -172,9 +173,12 @@ __global__ void __launch_bounds__(1024) k_codebook(const unsigned long long *his
   __shared__ unsigned s_wl[32][33];
   __shared__ int s_maxl;
   count_launch(st);
-  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5;
   const int m = st->m;
   const int n = 1 << m;
+  // small alphabets: fewer threads, cheaper barriers (the rest exit now)
+  const int nt = min((int)blockDim.x, max(128, n));
+  if ((int)threadIdx.x >= nt) return;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const bool in_smem = n <= kCbSmemSyms;
   unsigned long long *keys = in_smem ? sm : g_keys;
   unsigned long long *I = in_smem ? sm + n : g_I;
@@ -217,7 +221,7 @@ __global__ void __launch_bounds__(1024) k_codebook(const unsigned long long *his
   for (int i = nr + tid; i < np2; i += nt) rk[i] = ~0ull;
   __syncthreads();
   CB_STAMP(1)
-  if (nr > 1) bitonic_sort(rk, np2);
+  if (nr > 1) bitonic_sort(rk, np2, nt);
   for (int i = tid; i < nr; i += nt) keys[nf + i] = rk[i];
   __syncthreads();
   CB_STAMP(2)
