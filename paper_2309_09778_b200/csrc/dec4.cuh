@@ -412,7 +412,7 @@ __global__ void __launch_bounds__(kD4Threads, 6) k_decode4(const uint8_t *__rest
         long long spins = 0;
         do {
           asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(zflag + q) : "memory");
-        } while (v == 0u && ++spins < (1ll << 28));
+        } while (v == 0u && ++spins < (1ll << 22));
         if (v == 0u) {  // never published (cannot happen): fail instead of hanging
           set_err_at(st, PMZ_ERR_CORRUPT, 31, p);
           v = kD4Poison;

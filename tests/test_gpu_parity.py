@@ -82,7 +82,8 @@ def test_edge_shapes(codec, oracle, shape):
     _parity(codec, oracle, x, b_r=1e-2, repair_factor=1.0)
 
 
-@pytest.mark.parametrize("br,bc,pr", [(64, 128, 16), (32, 32, 8), (100, 60, 7), (256, 256, 32), (512, 64, 32)])
+@pytest.mark.parametrize("br,bc,pr", [(64, 128, 16), (32, 32, 8), (100, 60, 7), (256, 256, 32), (512, 64, 32),
+                                      (64, 512, 32), (40, 1000, 20)])
 def test_block_geometries(codec, oracle, br, bc, pr):
     x = _field("C2", (300, 500))
     _parity(codec, oracle, x, b_r=1e-2, repair_factor=1.0, block_rows=br, block_cols=bc, partition_rows=pr)
@@ -203,10 +204,10 @@ def test_log2_exhaustive_no_ambiguity():
 
 
 def test_decoder_runs_fallback(codec, oracle):
-    """Long runs of the balance-point codeword (a smooth field with sparse sign
-    flips): speculative decodes that start out of phase inside a run never
-    meet the true parse within their segment, so the transfer-function
-    fallback of the decoder (dec3.cuh) runs; the output must still be exact."""
+    """Long runs of the balance-point codeword (mostly incoherent signs): a
+    parse that starts out of phase inside a run stays out of phase for the
+    whole run.  The word-map decoder (dec4.cuh) never relies on
+    re-synchronisation; the output must be exact."""
     rng = np.random.default_rng(11)
     x = _field("C2", (512, 1024)).astype(np.float32)
     flip = rng.random(x.shape) < 0.85   # mostly incoherent signs -> mostly balance points
@@ -216,8 +217,8 @@ def test_decoder_runs_fallback(codec, oracle):
 
 def test_decoder_large_substreams(codec, oracle):
     """Fixed m = 16 on white noise: ~16+ bits per codeword, so partition
-    substreams exceed the 8 KB staging of the common decode launch and take
-    the large-stage launch."""
+    substreams are long (many words per subsegment map) and codewords exceed
+    the 12-bit shared decode table (global second level)."""
     rng = np.random.default_rng(12)
     x = (rng.normal(0, 1, (256, 512)) * 100).astype(np.float32)
     info, n = _parity(codec, oracle, x, b_r=1e-3, repair_factor=1.0, m=16)
@@ -225,8 +226,8 @@ def test_decoder_large_substreams(codec, oracle):
 
 
 def test_decoder_tiny_partitions(codec, oracle):
-    """Very short substreams (2-row partitions, 8-column blocks): empty lane
-    segments and codewords spanning several lane segments."""
+    """Very short substreams (2-row partitions, 8-column blocks): mostly empty
+    subsegments, codewords spanning several of them."""
     x = _field("C2", (64, 96))
     _parity(codec, oracle, x, b_r=1e-2, repair_factor=1.0, block_rows=16, block_cols=8, partition_rows=2)
 
@@ -234,9 +235,9 @@ def test_decoder_tiny_partitions(codec, oracle):
 def test_decoder_repeated_decodes_identical(codec, oracle):
     """The full C2 field decoded many times back to back (L2 flushed in
     between, so CTA timing varies): every decode is bit-identical to the
-    oracle's.  Covers races between lane segments of one partition, e.g. a
-    trailing empty segment (s_i == s_n == L, L % 32 != 0) clearing the
-    partial last bitmap word the last non-empty lane is still marking."""
+    oracle's.  Covers races between the CTAs of one block (the decoupled
+    look-back over the earlier partitions' balance counts) and between the
+    warps of one partition."""
     import paper_2309_09778_b200 as P
     x = _field("C2")
     ocfg = oracle.OracleConfig(b_r=1e-2, repair_factor=1.0)
@@ -276,3 +277,47 @@ def test_pipelined_and_graphed_match_one_shot(codec):
     for _ in range(3):
         out.append(pc.collect()[0].numpy().tobytes())
     assert out == ref
+
+
+def _record_fields(buf: bytes, P):
+    """Offsets of block 0's record and its partition table."""
+    b = np.frombuffer(buf, np.uint8)
+    h = P.Codec.parse_header(b)
+    offs = P.Codec.index_blocks(b, h)
+    return int(offs[0]), h
+
+
+@pytest.mark.parametrize("what", ["bits_minus1", "bits_plus1", "bits_huge", "nbal_plus", "nbal_minus"])
+def test_decompress_corrupted_tables(codec, oracle, what):
+    """Targeted corruption of block 0's record.  Every partition of a block
+    waits for the balance counts of the partitions before it (decoupled
+    look-back), so a failing partition must still release the later ones:
+    the call raises a container/coding error instead of hanging.  The +-1 bit
+    length edits keep the record framing (byte lengths) intact, so they reach
+    the device decoder; the others fail the host-side framing."""
+    import struct
+    import paper_2309_09778_b200 as P
+    from paper_2309_09778_b200 import errors as E
+    x = _field("C2", (256, 512))
+    buf, _ = oracle.compress(x, oracle.OracleConfig(b_r=1e-2, repair_factor=1.0))
+    o, h = _record_fields(buf, P)
+    a = bytearray(buf)
+    assert a[o] == 0  # non-trivial block
+    np_ = (int(h.block_rows) + int(h.partition_rows) - 1) // int(h.partition_rows)
+    nb_at = o + 17 + 24 * np_
+    if what.startswith("bits_") and what != "bits_huge":
+        d = -1 if what == "bits_minus1" else 1
+        for pi in range(np_):  # a partition whose byte length survives the edit
+            (bl,) = struct.unpack_from("<Q", a, o + 17 + 24 * pi + 8)
+            if bl > 8 and (bl + d + 7) // 8 == (bl + 7) // 8:
+                struct.pack_into("<Q", a, o + 17 + 24 * pi + 8, bl + d)
+                break
+        else:
+            pytest.skip("no partition length allows a framing-preserving edit")
+    elif what == "bits_huge":
+        struct.pack_into("<Q", a, o + 17 + 24 + 8, 1 << 40)
+    else:
+        (nb,) = struct.unpack_from("<Q", a, nb_at)
+        struct.pack_into("<Q", a, nb_at, nb + (1 if what == "nbal_plus" else -1))
+    with pytest.raises(E.PermezError):
+        P.decompress(bytes(a), device="cuda:0")
