@@ -198,6 +198,14 @@ PMZ_API int pmz_decompress_workspace_size(const pmz_header *hdr, uint64_t *bytes
  * derive_transform_params (transform.py:118). */
 PMZ_API int pmz_decompress(const uint8_t *d_buf, uint64_t n, const pmz_header *hdr, double b_a,
                    const uint64_t *d_block_offsets, float *d_out, void *d_ws, uint64_t ws_bytes, void *stream);
+/* pmz_decompress split for streaming: enqueue every kernel on `stream` (no
+ * host synchronisation, the status stays in the workspace), then
+ * pmz_decompress_result synchronises the stream and maps the device status
+ * (same return codes as pmz_decompress). */
+PMZ_API int pmz_decompress_enqueue(const uint8_t *d_buf, uint64_t n, const pmz_header *hdr, double b_a,
+                                   const uint64_t *d_block_offsets, float *d_out, void *d_ws, uint64_t ws_bytes,
+                                   void *stream);
+PMZ_API int pmz_decompress_result(const pmz_header *hdr, void *d_ws, uint64_t ws_bytes, void *stream);
 
 /* --- transform module (transform.py) on device ------------------------------ */
 

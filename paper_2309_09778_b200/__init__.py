@@ -6,8 +6,9 @@ Public entry points mirror the reference package: ``compress`` /
 """
 from . import errors
 from .errors import PermezError
-from .pipeline import Codec, CompressConfig, CompressInfo, GraphedCompressor, PipelinedCompressor, compress, decompress
+from .pipeline import (Codec, CompressConfig, CompressInfo, GraphedCompressor, PipelinedCompressor,
+                       PipelinedDecompressor, compress, decompress)
 from .predictor import PerceptronModel, init_model, lorenzo_coefficients
 
-__all__ = ["compress", "decompress", "Codec", "GraphedCompressor", "PipelinedCompressor", "CompressConfig", "CompressInfo", "PerceptronModel", "init_model",
+__all__ = ["compress", "decompress", "Codec", "GraphedCompressor", "PipelinedCompressor", "PipelinedDecompressor", "CompressConfig", "CompressInfo", "PerceptronModel", "init_model",
            "lorenzo_coefficients", "errors", "PermezError"]

@@ -76,6 +76,8 @@ _SIGS = {
     "pmz_index_blocks": (c_int32, [VP, c_uint64, ctypes.POINTER(Header), VP]),
     "pmz_decompress_workspace_size": (c_int32, [ctypes.POINTER(Header), ctypes.POINTER(c_uint64)]),
     "pmz_decompress": (c_int32, [VP, c_uint64, ctypes.POINTER(Header), c_double, VP, VP, VP, c_uint64, VP]),
+    "pmz_decompress_enqueue": (c_int32, [VP, c_uint64, ctypes.POINTER(Header), c_double, VP, VP, VP, c_uint64, VP]),
+    "pmz_decompress_result": (c_int32, [ctypes.POINTER(Header), VP, c_uint64, VP]),
     "pmz_transform_params": (c_int32, [VP, ctypes.POINTER(Geom), ctypes.POINTER(Params), VP, VP, VP, c_uint64, VP]),
     "pmz_forward_map": (c_int32, [VP, c_uint64, VP, VP, VP]),
     "pmz_inverse_map": (c_int32, [VP, c_uint64, VP, VP, VP, VP]),

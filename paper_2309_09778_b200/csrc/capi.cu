@@ -602,8 +602,8 @@ int pmz_decompress_workspace_size(const pmz_header *hdr, uint64_t *bytes) {
   return PMZ_OK;
 }
 
-int pmz_decompress(const uint8_t *d_buf, uint64_t n, const pmz_header *hdr, double b_a, const uint64_t *d_boff,
-                   float *d_out, void *d_ws, uint64_t ws_bytes, void *stream) {
+int pmz_decompress_enqueue(const uint8_t *d_buf, uint64_t n, const pmz_header *hdr, double b_a,
+                           const uint64_t *d_boff, float *d_out, void *d_ws, uint64_t ws_bytes, void *stream) {
   Geom G = hdr_geom(hdr);
   DecLayout L = dec_layout(G);
   if (ws_bytes < L.total) return PMZ_ERR_WORKSPACE;
@@ -635,18 +635,31 @@ int pmz_decompress(const uint8_t *d_buf, uint64_t n, const pmz_header *hdr, doub
     else s2 = launch_recon<0>(k, rgrid, st, G, d_ws, L, d_out);
     if (s2) return s2;
   }
-  int s = launch_check();
-  if (s) return s;
+  return launch_check();
+}
+
+int pmz_decompress_result(const pmz_header *hdr, void *d_ws, uint64_t ws_bytes, void *stream) {
+  Geom G = hdr_geom(hdr);
+  DecLayout L = dec_layout(G);
+  if (ws_bytes < L.total) return PMZ_ERR_WORKSPACE;
+  cudaStream_t st = (cudaStream_t)stream;
   WsStatus hs;
-  CK(cudaMemcpyAsync(&hs, S, sizeof(WsStatus), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(&hs, at<WsStatus>(d_ws, L.status), sizeof(WsStatus), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
-  s = err_from_bits(hs.err_bits);
+  const int s = err_from_bits(hs.err_bits);
   if (s && getenv("PMZ_DEBUG"))
     fprintf(stderr, "pmz_decompress: status %d bits 0x%x first site %d part %d\n", s, hs.err_bits, hs.err_site,
             hs.err_part);
   if (s) return s;
   if (hs.unresolved) return PMZ_ERR_UNRESOLVED_ROUNDING;
   return PMZ_OK;
+}
+
+int pmz_decompress(const uint8_t *d_buf, uint64_t n, const pmz_header *hdr, double b_a, const uint64_t *d_boff,
+                   float *d_out, void *d_ws, uint64_t ws_bytes, void *stream) {
+  const int s = pmz_decompress_enqueue(d_buf, n, hdr, b_a, d_boff, d_out, d_ws, ws_bytes, stream);
+  if (s) return s;
+  return pmz_decompress_result(hdr, d_ws, ws_bytes, stream);
 }
 
 // ---------------------------------------------------------------------------

@@ -411,6 +411,80 @@ class PipelinedCompressor:
         return sl["host_out"][: info.nbytes], info
 
 
+class PipelinedDecompressor:
+    """Streaming decompression of a sequence of containers of one geometry
+    with several in flight (the mirror of PipelinedCompressor): ``depth``
+    slots, each with its own CUDA stream, device container buffer, block
+    index, workspace and output.  ``submit`` enqueues the host->device copy
+    of the container (pinned host bytes), the decode kernels
+    (pmz_decompress_enqueue) and the device->host copy of the float32 grid
+    into pinned memory; ``collect`` synchronises the oldest slot, maps its
+    device status (pmz_decompress_result) and returns the grid."""
+
+    def __init__(self, codec: Codec, container: bytes | np.ndarray, depth: int = 3):
+        if depth < 1:
+            raise ConfigError("depth must be >= 1")
+        buf = np.frombuffer(container, dtype=np.uint8) if isinstance(container, (bytes, bytearray)) else container
+        self.codec, self.depth = codec, depth
+        self.h = Codec.parse_header(buf)
+        lib = codec.lib
+        wsz = ctypes.c_uint64(0)
+        check(lib.pmz_decompress_workspace_size(ctypes.byref(self.h), ctypes.byref(wsz)), "workspace")
+        self.shape = (int(self.h.rows), int(self.h.cols))
+        self.cap = int(buf.size) + 64
+        self.slots = []
+        for _ in range(depth):
+            stream = torch.cuda.Stream(codec.device)
+            self.slots.append({
+                "stream": stream,
+                "buf": torch.empty(self.cap, dtype=torch.uint8, device=codec.device),
+                "offs": torch.empty(int(self.h.nblocks) + 1, dtype=torch.int64, device=codec.device),
+                "ws": torch.empty(max(int(wsz.value), 1), dtype=torch.uint8, device=codec.device),
+                "h_offs": torch.empty(int(self.h.nblocks) + 1, dtype=torch.int64, pin_memory=True),
+                "out": torch.empty(self.shape, dtype=torch.float32, device=codec.device),
+                "host_out": torch.empty(self.shape, dtype=torch.float32, pin_memory=True),
+                "n": 0})
+        self._next = 0
+        self._queue = []
+
+    def submit(self, host_container: torch.Tensor, block_offsets: np.ndarray | None = None):
+        """Enqueue one container: a pinned uint8 CPU tensor of the same
+        geometry; ``block_offsets`` (pmz_index_blocks) is computed when absent."""
+        if len(self._queue) == self.depth:
+            raise ConfigError("all slots in flight: collect() before submitting more")
+        n = int(host_container.numel())
+        if n > self.cap:
+            raise ConfigError("container larger than the slot buffer")
+        if block_offsets is None:
+            block_offsets = Codec.index_blocks(host_container.numpy(), self.h)
+        i = self._next
+        self._next = (i + 1) % self.depth
+        sl = self.slots[i]
+        lib = self.codec.lib
+        with torch.cuda.stream(sl["stream"]):
+            sl["buf"][:n].copy_(host_container, non_blocking=True)
+            sl["h_offs"].copy_(torch.from_numpy(np.asarray(block_offsets).view(np.int64)))  # slot is idle: safe
+            sl["offs"].copy_(sl["h_offs"], non_blocking=True)
+            check(lib.pmz_decompress_enqueue(_ptr(sl["buf"]), n, ctypes.byref(self.h), host_b_a(self.h.b_r),
+                                             _ptr(sl["offs"]), _ptr(sl["out"]), _ptr(sl["ws"]), sl["ws"].numel(),
+                                             ctypes.c_void_p(sl["stream"].cuda_stream)), "decompress")
+            sl["host_out"].copy_(sl["out"], non_blocking=True)
+        sl["n"] = n
+        self._queue.append(i)
+        return i
+
+    def collect(self) -> torch.Tensor:
+        """The oldest submitted container's float32 grid (a pinned CPU tensor
+        view, valid until its slot is reused)."""
+        if not self._queue:
+            raise ConfigError("nothing submitted")
+        i = self._queue.pop(0)
+        sl = self.slots[i]
+        check(self.codec.lib.pmz_decompress_result(ctypes.byref(self.h), _ptr(sl["ws"]), sl["ws"].numel(),
+                                                   ctypes.c_void_p(sl["stream"].cuda_stream)), "decompress")
+        return sl["host_out"]
+
+
 def _codec(device=None) -> Codec:
     dev = _require_cuda(device)
     key = str(dev)
