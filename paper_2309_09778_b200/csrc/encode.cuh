@@ -547,83 +547,21 @@ constexpr unsigned kBalStage = 1024;   // balance values per staging sub-round (
 constexpr int kWpTabM = 10;            // codebook tables in shared memory up to this m
 constexpr size_t kWpSmem = (size_t)(1u << kWpTabM) * 5;
 
-__global__ void __launch_bounds__(kWT) k_write_part(Geom g, const BlkP *__restrict__ blkp,
-                                                    const int16_t *__restrict__ rqbuf,
-                                                    const double *__restrict__ vbuf,
-                                                    const double *__restrict__ anchors,
-                                                    const unsigned long long *__restrict__ part_bits,
-                                                    const unsigned long long *__restrict__ part_zeros,
-                                                    const unsigned long long *__restrict__ rec_off,
-                                                    const uint8_t *__restrict__ lens,
-                                                    const unsigned *__restrict__ cw, uint8_t *out,
-                                                    WsStatus *st) {
-  extern __shared__ __align__(16) unsigned char wp_dyn[];
-  __shared__ unsigned sw[kPartWords];
-  __shared__ unsigned long long sbal[kBalStage + 1];
-  __shared__ unsigned s_bidx[kBalStage];
-  __shared__ unsigned s_wsum[kWT / 32][2];
-  __shared__ unsigned s_carry[2];
-  count_launch(st);
-  // m, the header size and the capacity check come from the device status:
-  // no host round trip between the codebook and the writers
-  if (st->err_bits) return;
-  const int m = st->m;
-  const unsigned long long rec_base = st->header_bytes;
+// The partition's runs (see k_write_part), with the codebook tables in shared
+// memory (SMALL) or read through L1: a uniform branch per CTA instead of a
+// predicated pair of loads per symbol.
+template <bool SMALL>
+__device__ __forceinline__ void wp_runs(const Geom &g, const BlkP &P, int64_t b, int64_t p, int pi,
+                                        unsigned long long nbal, unsigned long long zb, unsigned long long pb,
+                                        uint8_t *base, unsigned head, int m, const int16_t *__restrict__ rqbuf,
+                                        const double *__restrict__ vbuf,
+                                        const unsigned long long *__restrict__ part_bits,
+                                        const uint8_t *__restrict__ lens, const unsigned *__restrict__ cw,
+                                        const uint8_t *s_len, const unsigned *s_cw, unsigned *sw,
+                                        unsigned long long *sbal, unsigned *s_bidx, unsigned (*s_wsum)[2],
+                                        unsigned *s_carry) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t p = blockIdx.x;
-  int64_t b;
-  int pi;
-  part_of(g, p, b, pi);
-  uint8_t *base = out + rec_base + rec_off[b];
-  const BlkP P = blkp[b];
-  if (P.trivial) {
-    if (pi == 0 && tid == 0) base[0] = 1;
-    return;
-  }
-  const bool small_tab = m <= kWpTabM;
-  unsigned *s_cw = reinterpret_cast<unsigned *>(wp_dyn);
-  uint8_t *s_len = wp_dyn + (4u << kWpTabM);
-  if (small_tab) {
-    for (int i = tid; i < (1 << m); i += kWT) {
-      s_len[i] = lens[i];
-      s_cw[i] = cw[i];
-    }
-  }
   const BlockBox bb = block_box(g, b);
-  const int64_t p0 = first_part(g, b);
-  unsigned long long zb = 0, pb = 0, nbal = 0;
-  for (int i = 0; i < bb.np; i++) {
-    const unsigned long long z = part_zeros[p0 + i], by = (part_bits[p0 + i] + 7) / 8;
-    if (i < pi) { zb += z; pb += by; }
-    nbal += z;
-  }
-  const unsigned head = 25 + 24u * bb.np;
-  if (pi == 0) {
-    // record head: trivial flag, factors, partition table, balance count
-    for (unsigned i = tid; i < head; i += kWT) {
-      unsigned long long word;
-      unsigned byte;
-      if (i == 0) { base[0] = 0; continue; }
-      if (i < 17) {
-        word = __double_as_longlong(i < 9 ? P.factor_pos : P.factor_neg);
-        byte = (i - 1) & 7;
-      } else if (i < 17 + 24u * bb.np) {
-        const unsigned q = i - 17, pq = q / 24, f = (q % 24) / 8;
-        if (f == 0) {
-          unsigned long long off = 0;
-          for (unsigned t = 0; t < pq; t++) off += (part_bits[p0 + t] + 7) / 8;
-          word = off * 8;
-        } else {
-          word = f == 1 ? part_bits[p0 + pq] : __double_as_longlong(anchors[p0 + pq]);
-        }
-        byte = q & 7;
-      } else {
-        word = nbal;
-        byte = (i - 17 - 24u * bb.np) & 7;
-      }
-      base[i] = (uint8_t)(word >> (8 * byte));
-    }
-  }
   uint8_t *bal = base + head + 8ull * zb;
   uint8_t *pay = base + head + 8ull * nbal + pb;
   const int R = min(g.prow, bb.br - pi * g.prow), C = bb.bc, nch = (C + 31) >> 5;
@@ -633,12 +571,8 @@ __global__ void __launch_bounds__(kWT) k_write_part(Geom g, const BlkP *__restri
   const unsigned total_bits = (unsigned)part_bits[p];
   const unsigned nwords = (total_bits + 31) >> 5;
   const bool staged = nwords <= kPartWords;
-  for (unsigned i = tid; i < (staged ? nwords : 0u); i += kWT) sw[i] = 0;
-  if (tid < 2) s_carry[tid] = 0;
-  __syncthreads();  // tables, sw, carry
-
-  auto len_of = [&](unsigned c) -> unsigned { return small_tab ? s_len[c] : __ldg(&lens[c]); };
-  auto cw_of = [&](unsigned c) -> unsigned { return small_tab ? s_cw[c] : __ldg(&cw[c]); };
+  auto len_of = [&](unsigned c) -> unsigned { return SMALL ? (unsigned)s_len[c] : (unsigned)__ldg(&lens[c]); };
+  auto cw_of = [&](unsigned c) -> unsigned { return SMALL ? s_cw[c] : __ldg(&cw[c]); };
   const int nrun = R * nch;
   for (int q0 = 0; q0 < nrun; q0 += kWT) {
     const int q = q0 + tid;
@@ -655,10 +589,15 @@ __global__ void __launch_bounds__(kWT) k_write_part(Geom g, const BlkP *__restri
         w[4 * u] = x4.x; w[4 * u + 1] = x4.y; w[4 * u + 2] = x4.z; w[4 * u + 3] = x4.w;
       }
     }
-    auto code_at = [&](int i) -> unsigned {
-      return (unsigned)code_of_rq((int)(int16_t)(w[i >> 1] >> (16 * (i & 1))), center);
-    };
+    // codes of the run, two per register (computed once for both passes)
     const int i0 = (r == 0 && kc == 0) ? 1 : 0;  // the anchor
+#pragma unroll
+    for (int u = 0; u < 16; u++) {
+      const unsigned lo = (unsigned)code_of_rq((int)(int16_t)(w[u] & 0xffffu), center);
+      const unsigned hi = (unsigned)code_of_rq((int)(int16_t)(w[u] >> 16), center);
+      w[u] = lo | (hi << 16);
+    }
+    auto code_at = [&](int i) -> unsigned { return (w[i >> 1] >> (16 * (i & 1))) & 0xffffu; };
     unsigned bits = 0, zmask = 0;
 #pragma unroll
     for (int i = 0; i < 32; i++) {
@@ -779,11 +718,99 @@ __global__ void __launch_bounds__(kWT) k_write_part(Geom g, const BlkP *__restri
       __syncthreads();
     }
   }
-  if (staged) {
+  if (staged) {  // MSB-first words -> byte order, then aligned word stores
     __syncthreads();
-    const unsigned nbytes = (total_bits + 7) >> 3;
-    for (unsigned i = tid; i < nbytes; i += kWT) pay[i] = (uint8_t)(sw[i >> 2] >> (24 - 8 * (i & 3)));
+    for (unsigned i = tid; i < nwords; i += kWT) sw[i] = __byte_perm(sw[i], 0, 0x0123);
+    __syncthreads();
+    copy_s2g_bytes(pay, sw, (total_bits + 7) >> 3, tid, kWT);
   }
+}
+
+__global__ void __launch_bounds__(kWT) k_write_part(Geom g, const BlkP *__restrict__ blkp,
+                                                    const int16_t *__restrict__ rqbuf,
+                                                    const double *__restrict__ vbuf,
+                                                    const double *__restrict__ anchors,
+                                                    const unsigned long long *__restrict__ part_bits,
+                                                    const unsigned long long *__restrict__ part_zeros,
+                                                    const unsigned long long *__restrict__ rec_off,
+                                                    const uint8_t *__restrict__ lens,
+                                                    const unsigned *__restrict__ cw, uint8_t *out,
+                                                    WsStatus *st) {
+  extern __shared__ __align__(16) unsigned char wp_dyn[];
+  __shared__ unsigned sw[kPartWords];
+  __shared__ unsigned long long sbal[kBalStage + 1];
+  __shared__ unsigned s_bidx[kBalStage];
+  __shared__ unsigned s_wsum[kWT / 32][2];
+  __shared__ unsigned s_carry[2];
+  count_launch(st);
+  // m, the header size and the capacity check come from the device status:
+  // no host round trip between the codebook and the writers
+  if (st->err_bits) return;
+  const int m = st->m;
+  const unsigned long long rec_base = st->header_bytes;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t p = blockIdx.x;
+  int64_t b;
+  int pi;
+  part_of(g, p, b, pi);
+  uint8_t *base = out + rec_base + rec_off[b];
+  const BlkP P = blkp[b];
+  if (P.trivial) {
+    if (pi == 0 && tid == 0) base[0] = 1;
+    return;
+  }
+  const bool small_tab = m <= kWpTabM;
+  unsigned *s_cw = reinterpret_cast<unsigned *>(wp_dyn);
+  uint8_t *s_len = wp_dyn + (4u << kWpTabM);
+  if (small_tab) {
+    for (int i = tid; i < (1 << m); i += kWT) {
+      s_len[i] = lens[i];
+      s_cw[i] = cw[i];
+    }
+  }
+  const BlockBox bb = block_box(g, b);
+  const int64_t p0 = first_part(g, b);
+  unsigned long long zb = 0, pb = 0, nbal = 0;
+  for (int i = 0; i < bb.np; i++) {
+    const unsigned long long z = part_zeros[p0 + i], by = (part_bits[p0 + i] + 7) / 8;
+    if (i < pi) { zb += z; pb += by; }
+    nbal += z;
+  }
+  const unsigned head = 25 + 24u * bb.np;
+  if (pi == 0) {
+    // record head: trivial flag, factors, partition table, balance count
+    for (unsigned i = tid; i < head; i += kWT) {
+      unsigned long long word;
+      unsigned byte;
+      if (i == 0) { base[0] = 0; continue; }
+      if (i < 17) {
+        word = __double_as_longlong(i < 9 ? P.factor_pos : P.factor_neg);
+        byte = (i - 1) & 7;
+      } else if (i < 17 + 24u * bb.np) {
+        const unsigned q = i - 17, pq = q / 24, f = (q % 24) / 8;
+        if (f == 0) {
+          unsigned long long off = 0;
+          for (unsigned t = 0; t < pq; t++) off += (part_bits[p0 + t] + 7) / 8;
+          word = off * 8;
+        } else {
+          word = f == 1 ? part_bits[p0 + pq] : __double_as_longlong(anchors[p0 + pq]);
+        }
+        byte = q & 7;
+      } else {
+        word = nbal;
+        byte = (i - 17 - 24u * bb.np) & 7;
+      }
+      base[i] = (uint8_t)(word >> (8 * byte));
+    }
+  }
+  for (unsigned i = tid; i < (((unsigned)part_bits[p] + 31) >> 5 <= kPartWords ? ((unsigned)part_bits[p] + 31) >> 5 : 0u);
+       i += kWT)
+    sw[i] = 0;
+  if (tid < 2) s_carry[tid] = 0;
+  __syncthreads();  // tables, sw, carry
+
+  if (small_tab) wp_runs<true>(g, P, b, p, pi, nbal, zb, pb, base, head, m, rqbuf, vbuf, part_bits, lens, cw, s_len, s_cw, sw, sbal, s_bidx, s_wsum, s_carry);
+  else wp_runs<false>(g, P, b, p, pi, nbal, zb, pb, base, head, m, rqbuf, vbuf, part_bits, lens, cw, s_len, s_cw, sw, sbal, s_bidx, s_wsum, s_carry);
 }
 
 }  // namespace pmz
