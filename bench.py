@@ -172,11 +172,14 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    # PMZ_BENCH_SHARDED=1: the sharded code path (NCCL collectives included)
+    # on a single rank, to check it on one GPU
+    sharded = world > 1 or bool(os.environ.get("PMZ_BENCH_SHARDED"))
+    if sharded:
+        dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
 
     def allreduce(t):
-        if world > 1:
+        if sharded:
             dist.all_reduce(t)
 
     from paper_2309_09778_b200.sharding import exchange_record_sizes, local_validation_blocks, plan_shard
@@ -315,6 +318,86 @@ def main():
                 assert pinfo.nbytes == infok.nbytes
             launches_pipe = K * infok.launches
             pipe = {"ms": pipe_ms, "depth": depth}
+        # sharded (N > 1, or PMZ_BENCH_SHARDED=1 for a 1-rank check): the same
+        # `depth` fields in flight per rank.  A slot's field -- the staged
+        # stages with the two NCCL histogram all-reduces -- is one captured
+        # CUDA graph; every slot has its own communicator, so the collectives
+        # of concurrently replayed graphs never share one.  A slot's status
+        # is read, and its record size all-gathered (default group, host
+        # order), when the slot comes round.
+        if sharded and args.pipeline > 1:
+            depth = args.pipeline
+            pool = [x.clone() for _ in range(8)]
+            wsz, cap = ctypes.c_uint64(0), ctypes.c_uint64(0)
+            p0_ = P.pipeline.make_params(cfg, 3)
+            g0_ = N.Geom(x.shape[0], x.shape[1], b0, grows)
+            lib.pmz_workspace_size(ctypes.byref(p0_), ctypes.byref(g0_), ctypes.byref(wsz))
+            lib.pmz_max_container_size(ctypes.byref(p0_), ctypes.byref(g0_), ctypes.byref(cap))
+            sslots = []
+            for _ in range(depth):
+                grp = dist.new_group(list(range(world)))
+                sl = {"s": torch.cuda.Stream(dev), "x": x.clone(),
+                      "ws": torch.empty(int(wsz.value), dtype=torch.uint8, device=dev),
+                      "out": torch.empty(int(cap.value), dtype=torch.uint8, device=dev), "offs": offs.clone(),
+                      "pg": None, "busy": False}
+
+                def ar_(t, grp=grp):
+                    dist.all_reduce(t, group=grp)
+
+                def enq(sl=sl, ar_=ar_):
+                    return codec.compress_staged_async(sl["x"], cfg, block_row0=b0, global_rows=grows, d_val=d_val,
+                                                       allreduce=ar_, ws=sl["ws"], out=sl["out"],
+                                                       block_offsets=sl["offs"])
+                with torch.cuda.stream(sl["s"]):  # eager warm-up (communicator set-up), then capture
+                    sl["pg"] = enq()
+                    codec.staged_result(*sl["pg"], sl["ws"], sl["out"])
+                    torch.cuda.synchronize()
+                    sl["graph"] = torch.cuda.CUDAGraph()
+                    with torch.cuda.graph(sl["graph"], stream=sl["s"]):
+                        enq()
+                sslots.append(sl)
+            torch.cuda.synchronize()
+
+            def sh_step(k_):
+                sl = sslots[k_ % depth]
+                with torch.cuda.stream(sl["s"]):
+                    if sl["busy"]:
+                        inf_ = codec.staged_result(*sl["pg"], sl["ws"], sl["out"])
+                        exchange_record_sizes(inf_.nbytes - inf_.header_bytes, device=dev)
+                    sl["x"].copy_(pool[k_ % 8], non_blocking=True)
+                    sl["graph"].replay()
+                    sl["busy"] = True
+
+            def sh_drain():
+                last = None
+                for sl in sslots:
+                    with torch.cuda.stream(sl["s"]):
+                        if sl["busy"]:
+                            last = codec.staged_result(*sl["pg"], sl["ws"], sl["out"])
+                            exchange_record_sizes(last.nbytes - last.header_bytes, device=dev)
+                            sl["busy"] = False
+                return last
+
+            for k_ in range(max(args.warmup, depth)):
+                sh_step(k_)
+            sh_drain()
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            pa, pb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            pa.record()
+            for sl in sslots:
+                sl["s"].wait_event(pa)
+            for k_ in range(K):
+                sh_step(k_)
+            for sl in sslots:
+                torch.cuda.current_stream().wait_stream(sl["s"])
+            pb.record()
+            lastinfo = sh_drain()
+            torch.cuda.synchronize()
+            assert lastinfo.nbytes == infok.nbytes
+            pipe = {"ms": pa.elapsed_time(pb), "depth": depth}
+            launches_pipe = K * infok.launches
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -322,6 +405,12 @@ def main():
     if world > 1:
         dist.all_reduce(tot, op=dist.ReduceOp.MAX)
     c_tot, d_tot = float(tot[0]), float(tot[1])
+    pipe_ms_max = None
+    if pipe is not None:  # the job's device time, max over ranks
+        pt = torch.tensor([pipe["ms"]], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(pt, op=dist.ReduceOp.MAX)
+        pipe_ms_max = float(pt[0])
     # total bytes = sum over ranks (shards are whole block-rows, ~equal)
     nb_t = torch.tensor([float(n_elem * 4), float(infok.nbytes)], dtype=torch.float64, device=dev)
     if world > 1:
@@ -521,7 +610,7 @@ def main():
                   "l2": "flushed between steps (256 MiB write)"}
         value, ms_step = comp_gbs, c_tot / K
         if pipe is not None:
-            ms_step = pipe["ms"] / K
+            ms_step = pipe_ms_max / K
             value = bytes_all / (ms_step / 1e3) / 1e9
             launches = launches_pipe + K * DECOMPRESS_LAUNCHES
         line = {
@@ -534,8 +623,10 @@ def main():
                        "l2": ("inputs rotate over 8 distinct resident copies (208 MB > 126 MB L2), each step "
                               "copies its field into the slot's input buffer (counted)") if pipe is not None
                        else "flushed between steps (256 MiB write), inputs < L2",
-                       "pipeline": (f"{pipe['depth']} fields in flight (streams + captured graphs); "
-                                    "single_stream = one at a time") if pipe is not None else "one at a time",
+                       "pipeline": ((f"{pipe['depth']} fields in flight per rank (streams; staged stages with the "
+                                     "NCCL histogram all-reduces on each field's stream)") if sharded else
+                                    (f"{pipe['depth']} fields in flight (streams + captured graphs); "
+                                     "single_stream = one at a time")) if pipe is not None else "one at a time",
                        "parallelism": f"shard{world}" if world > 1 else "single"},
             "single_stream": single,
             "compression_ratio": cr, "max_rel_err": max_rel, "m": infok.m,

@@ -248,6 +248,45 @@ class Codec:
                             list(res.coverage), tuple(x.shape), None, int(res.launches))
         return out[:n], info
 
+    def compress_staged_async(self, x: torch.Tensor, cfg: CompressConfig, *, block_row0: int, global_rows: int,
+                              d_val: torch.Tensor, allreduce=None, ws: torch.Tensor | None = None,
+                              out: torch.Tensor | None = None, block_offsets: torch.Tensor | None = None):
+        """compress_staged without a host synchronisation: the stages and the
+        two histogram all-reduces are only enqueued on the current stream
+        (NCCL collectives are stream-ordered), so several shards' fields can
+        be in flight; ``ws``/``out`` are the caller's per-slot buffers.  Read
+        the outcome with ``staged_result``."""
+        (rows, cols), S = grid_view_shape(tuple(x.shape))
+        p = make_params(cfg, S)
+        g = N.Geom(rows, cols, block_row0, global_rows)
+        lib = self.lib
+        stream = _stream_ptr(self.device)
+        nv = int(d_val.numel())
+        check(lib.pmz_compress_analyze(_ptr(x), ctypes.byref(g), ctypes.byref(p), _ptr(d_val), nv, _ptr(ws),
+                                       ws.numel(), stream), "compress_analyze")
+        if allreduce is not None:
+            off = lib.pmz_ws_coverage(_ptr(ws), ctypes.byref(p), ctypes.byref(g)) - ws.data_ptr()
+            allreduce(ws[off: off + 18 * 8].view(torch.int64))
+        check(lib.pmz_compress_codes(_ptr(x), ctypes.byref(g), ctypes.byref(p), _ptr(d_val), nv, _ptr(ws),
+                                     ws.numel(), stream), "compress_codes")
+        if allreduce is not None:
+            off = lib.pmz_ws_histogram(_ptr(ws), ctypes.byref(p), ctypes.byref(g)) - ws.data_ptr()
+            allreduce(ws[off: off + (65536 + 1) * 8].view(torch.int64))
+        check(lib.pmz_compress_finish_async(ctypes.byref(g), ctypes.byref(p), 1, _ptr(out), out.numel(),
+                                            _ptr(block_offsets), _ptr(ws), ws.numel(), stream), "compress_finish")
+        return p, g
+
+    def staged_result(self, p, g, ws: torch.Tensor, out: torch.Tensor) -> CompressInfo:
+        """Synchronise the current stream and decode the status of a field
+        enqueued by ``compress_staged_async``."""
+        res = N.Result()
+        check(self.lib.pmz_compress_result(ctypes.byref(g), ctypes.byref(p), 1, _ptr(ws), ws.numel(),
+                                           _stream_ptr(self.device), ctypes.byref(res)), "compress")
+        return CompressInfo(int(res.header_bytes + res.record_bytes), int(res.header_bytes), int(res.nblocks),
+                            int(res.ntrivial), int(res.nbal), int(res.nrepair), int(res.ncodes), int(res.m),
+                            int(res.max_code_len), list(res.coverage), (int(g.rows), int(g.cols)), None,
+                            int(res.launches))
+
     # ---- decompression ------------------------------------------------
     @staticmethod
     def parse_header(buf: np.ndarray) -> N.Header:
