@@ -1,0 +1,51 @@
+"""CLI: flag handling and the
+per-family exit codes on CPU; file round trips and the bench sweep on the GPU."""
+import numpy as np
+import pytest
+
+from paper_2309_09778_b200 import cli
+
+
+def test_exit_codes_per_family(tmp_path, capsys):
+    out = str(tmp_path / "x.pmz")
+    assert cli.main(["compress", "--input", str(tmp_path / "missing.f32"), "--output", out]) == 7  # IngestError
+    assert cli.main(["compress", "--input", "gen:C2", "--rel-error", "0", "--output", out]) == 2  # ConfigError
+    assert cli.main(["compress", "--input", "x.sgy", "--format", "segy", "--output", out]) == 2
+    assert cli.main(["compress", "--input", "gen:C2", "--grid", "lr:1e-3", "--output", out]) == 2
+    assert cli.main(["compress", "--input", "gen:C2", "--threads", "0", "--output", out]) == 2
+    assert cli.main(["decompress", "--input", str(tmp_path / "missing.pmz")]) == 7
+    raw = tmp_path / "a.f32"
+    np.zeros(10, np.float32).tofile(raw)
+    assert cli.main(["compress", "--input", str(raw), "--dims", "3x4", "--output", out]) == 7  # size mismatch
+    capsys.readouterr()
+
+
+@pytest.mark.gpu
+def test_cli_roundtrip_and_original(tmp_path, capsys):
+    x = np.ascontiguousarray(np.random.default_rng(3).normal(0, 1, (200, 300)).astype(np.float32) * 10)
+    src, cont, dst = tmp_path / "x.f32", tmp_path / "x.pmz", tmp_path / "y.f32"
+    x.tofile(src)
+    assert cli.main(["compress", "--input", str(src), "--dims", "200x300", "--rel-error", "1e-3",
+                     "--output", str(cont)]) == 0
+    line = capsys.readouterr().out.strip().splitlines()[-1].split(",")
+    assert float(line[7]) <= 1.5e-3  # max_rel_error column, SPEC default repair factor 1.5
+    assert cli.main(["decompress", "--input", str(cont), "--output", str(dst), "--original", str(src),
+                     "--dims", "200x300"]) == 0
+    out = capsys.readouterr().out
+    y = np.fromfile(dst, np.float32).reshape(200, 300)
+    assert float(out.split("max_rel_error,")[1].split()[0]) <= 1.5e-3
+    import paper_2309_09778_b200 as P
+    assert np.array_equal(y, P.decompress(cont.read_bytes(), device="cuda:0"))
+    b = bytearray(cont.read_bytes())
+    b[:4] = b"XXXX"
+    (tmp_path / "bad.pmz").write_bytes(bytes(b))
+    assert cli.main(["decompress", "--input", str(tmp_path / "bad.pmz")]) == 6  # ContainerError (BadMagic)
+
+
+@pytest.mark.gpu
+def test_cli_bench_rows_and_cr_monotone(capsys):
+    assert cli.main(["bench", "--input", "gen:sine2d", "--dims", "256x256", "--bench-bounds", "1e-4,1e-3,1e-2"]) == 0
+    rows = [r.split(",") for r in capsys.readouterr().out.strip().splitlines()]
+    assert rows[0][0] == "dataset" and len(rows) == 4
+    cr = [float(r[6]) for r in rows[1:]]
+    assert cr[0] >= cr[1] >= cr[2]  # AC8: CR non-increasing as b_r grows
