@@ -207,6 +207,23 @@ PMZ_API int pmz_decompress_enqueue(const uint8_t *d_buf, uint64_t n, const pmz_h
                                    void *stream);
 PMZ_API int pmz_decompress_result(const pmz_header *hdr, void *d_ws, uint64_t ws_bytes, void *stream);
 
+/* --- trainer objective ------------ */
+
+/* Sums over the samples of train_step's objective with the perceptron of `p`
+ * (p->w1, w2, slope, S): d_out12[0..7] = d(sum r^2)/d w1 (row-major (S+1) x H,
+ * bias row last), [8..9] d/d w2, [10] sum r^2, [11] sample count, where
+ * r = predict(surface) - target.  Deterministic (fixed summation order).
+ * pmz_train_gradient: samples = every element but the partition anchors of
+ * the blocks listed in d_blocks, surfaces from the TRUE forward-mapped values
+ * (the compress workspace of pmz_workspace_size; synchronises `stream`).
+ * pmz_train_gradient_batch: samples given as surfaces (n x S, row-major) and
+ * targets; d_ws of PMZ_TRAIN_BATCH_WS bytes; stream-ordered. */
+#define PMZ_TRAIN_BATCH_WS (296 * 12 * 8)
+PMZ_API int pmz_train_gradient(const float *d_in, const pmz_geom *g, const pmz_params *p, const int64_t *d_blocks,
+                               int64_t n_blocks, double *d_out12, void *d_ws, uint64_t ws_bytes, void *stream);
+PMZ_API int pmz_train_gradient_batch(const double *d_surf, const double *d_tgt, uint64_t n, const pmz_params *p,
+                                     double *d_out12, void *d_ws, uint64_t ws_bytes, void *stream);
+
 /* --- transform module (transform.py) on device ------------------------------ */
 
 /* Per-block transform parameters: 10 doubles per block in TransformParams

@@ -12,9 +12,10 @@ SPEC.md:540-549): dataset, b_r, CR, max relative error, compress and
 decompress MB/s (device time of the call, file I/O excluded).  The compute
 runs on the GPU through the library; there is no CPU path.  ``--threads`` is
 accepted for flag compatibility (the device decides its own parallelism;
-output is deterministic for any value).  Not supported here:
-``--format segy`` (SEG-Y ingest, row f3) and ``--save-model`` / ``--grid``
-(the trainer, row f1): they raise ConfigError (exit code 2).
+output is deterministic for any value).  ``--train`` / ``--grid``
+run the inline training sweep (training.py); ``--save-model`` /
+``--load-model`` write / read the model blob.  Not supported here: ``--format
+segy`` (SEG-Y ingest, row f3) raises ConfigError (exit code 2).
 """
 from __future__ import annotations
 
@@ -89,16 +90,33 @@ def _read_input(a) -> tuple[np.ndarray, str]:
     return x, os.path.basename(src)
 
 
-def _model(a):
+def _model(a, x=None, rel=None):
+    """--load-model (a model blob), else the inline training sweep when
+    --train / --grid is given (SPEC.md:582, training.py), else init_model;
+    --save-model writes the model used."""
+    model = None
+    if a.load_model:
+        try:
+            with open(a.load_model, "rb") as f:
+                model = PerceptronModel.from_bytes(f.read())
+        except OSError as ex:
+            raise E.IngestError(f"cannot read model {a.load_model!r}: {ex}")
+    elif (a.train or a.grid) and x is not None:
+        import torch
+        from . import pipeline as P, training
+        br, bc = _dims(a.block_size)
+        cfg = P.CompressConfig(rel_error=rel, block_rows=br, block_cols=bc, partition_rows=a.partition_rows,
+                               repair_factor=a.repair_factor, coverage_target=a.coverage_target,
+                               sample_rate=a.sample_rate, seed=a.seed)
+        codec = P._codec(a.device)
+        grid = training.parse_grid(a.grid) if a.grid else None
+        model = training.train(codec, torch.from_numpy(np.ascontiguousarray(x)).to(codec.device), cfg, grid).model
     if a.save_model:
-        raise E.ConfigError("--save-model needs the trainer (SURVEY.md §8(f) row f1), not part of this build")
-    if not a.load_model:
-        return None
-    try:
-        with open(a.load_model, "rb") as f:
-            return PerceptronModel.from_bytes(f.read())
-    except OSError as ex:
-        raise E.IngestError(f"cannot read model {a.load_model!r}: {ex}")
+        from .predictor import init_model
+        m = model if model is not None else init_model(1 if (x is not None and (x.ndim == 1 or x.shape[0] == 1)) else 3)
+        with open(a.save_model, "wb") as f:
+            f.write(m.to_bytes())
+    return model
 
 
 def _max_rel(x: np.ndarray, y: np.ndarray) -> float:
@@ -158,7 +176,7 @@ def cmd_compress(a) -> int:
     x, name = _read_input(a)
     if not a.output:
         raise E.ConfigError("--output is required")
-    cont, info, tc = _compress_one(x, a.rel_error, a, _model(a))
+    cont, info, tc = _compress_one(x, a.rel_error, a, _model(a, x, a.rel_error))
     with open(a.output, "wb") as f:
         f.write(cont)
     y, td = _decompress_one(cont, a, x.shape)
@@ -184,11 +202,10 @@ def cmd_decompress(a) -> int:
 
 def cmd_bench(a) -> int:
     x, name = _read_input(a)
-    model = _model(a)
     print(CSV_HEADER)
     for tok in a.bench_bounds.split(","):
         rel = float(tok)
-        cont, info, tc = _compress_one(x, rel, a, model)
+        cont, info, tc = _compress_one(x, rel, a, _model(a, x, rel))
         y, td = _decompress_one(cont, a, x.shape)
         print(_csv(name, rel, x, len(cont), _max_rel(x, y), tc, td), flush=True)
     return 0
@@ -209,7 +226,8 @@ def parser() -> argparse.ArgumentParser:
         s.add_argument("--sample-rate", type=float, default=0.1)
         s.add_argument("--coverage-target", type=float, default=0.99)
         s.add_argument("--repair-factor", type=float, default=1.5)
-        s.add_argument("--grid", help="trainer sweep grid (not part of this build)")
+        s.add_argument("--grid", help='trainer sweep grid, e.g. "lr:1e-3,1e-4;l2:0,1e-4,1e-2" (implies --train)')
+        s.add_argument("--train", action="store_true", help="inline training sweep (default grid) before compressing")
         s.add_argument("--threads", type=int, default=int(os.environ.get("PERMEZ_THREADS", "1")))
         s.add_argument("--seed", type=int, default=0)
         s.add_argument("--save-model")
@@ -226,7 +244,8 @@ def main(argv=None) -> int:
         if a.threads < 1:
             raise E.ConfigError("--threads must be >= 1")
         if a.grid:
-            raise E.ConfigError("--grid needs the trainer (SURVEY.md §8(f) row f1), not part of this build")
+            from . import training
+            training.parse_grid(a.grid)  # validate before any device work
         if not (0.0 < a.rel_error < 1.0):
             raise E.ConfigError("--rel-error must lie in (0, 1)")
         return {"compress": cmd_compress, "decompress": cmd_decompress, "bench": cmd_bench}[a.cmd](a)

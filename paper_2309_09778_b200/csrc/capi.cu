@@ -16,6 +16,7 @@
 #include "encode.cuh"
 #include "fwdq.cuh"
 #include "dec4.cuh"
+#include "train.cuh"
 
 using namespace pmz;
 
@@ -768,3 +769,50 @@ extern "C" PMZ_API int pmz_cbprof_read(void *host) {
   return cudaMemcpyFromSymbol(host, pmz::g_cb_prof, 8 * sizeof(long long)) == cudaSuccess ? 0 : -1;
 }
 #endif
+
+// ---------------------------------------------------------------------------
+// trainer objective
+
+int pmz_train_gradient(const float *d_in, const pmz_geom *g, const pmz_params *p, const int64_t *d_blocks,
+                       int64_t n_blocks, double *d_out12, void *d_ws, uint64_t ws_bytes, void *stream) {
+  int s = check_params(p);
+  if (s) return s;
+  Geom G = geom_of(p, g);
+  WsLayout L = compress_layout(G);
+  if (ws_bytes < L.total) return PMZ_ERR_WORKSPACE;
+  cudaStream_t st = (cudaStream_t)stream;
+  KParams k = kparams(p);
+  CK(cudaMemsetAsync(d_ws, 0, L.lens, st));  // status, flags, block stats
+  CK(cudaMemsetAsync(d_out12, 0, sizeof(double) * kTrC, st));
+  if (G.nblocks == 0 || n_blocks <= 0) return launch_check();
+  k_stats<<<(unsigned)G.nparts, 256, 0, st>>>(d_in, G, k, at<BlkP>(d_ws, L.blkp), at<BlkStat>(d_ws, L.bstat),
+                                               at<WsStatus>(d_ws, L.status));
+  // the training blocks are flagged in the validation-flag slots (no quantization runs here)
+  k_mark_val<<<(unsigned)((n_blocks + 255) / 256), 256, 0, st>>>(d_blocks, n_blocks, at<uint8_t>(d_ws, L.vflag),
+                                                                   at<WsStatus>(d_ws, L.status));
+  k_fwd<<<(unsigned)G.nparts, kFqT, 0, st>>>(d_in, G, at<BlkP>(d_ws, L.blkp), at<WsStatus>(d_ws, L.status),
+                                             at<double>(d_ws, L.vbuf), at<uint8_t>(d_ws, L.clsbuf));
+  // per-partition partials in the (unused here) rq tiles: >= 2 KB per partition
+  double *part = at<double>(d_ws, L.rqbuf);
+  k_train_tiles<<<(unsigned)G.nparts, kTrT, 0, st>>>(G, k, at<BlkP>(d_ws, L.blkp), at<uint8_t>(d_ws, L.vflag),
+                                                    at<double>(d_ws, L.vbuf), part);
+  k_train_reduce<<<1, 32, 0, st>>>(part, G.nparts, d_out12);
+  s = launch_check();
+  if (s) return s;
+  WsStatus hs;
+  CK(cudaMemcpyAsync(&hs, at<WsStatus>(d_ws, L.status), sizeof(WsStatus), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return err_from_bits(hs.err_bits);
+}
+
+int pmz_train_gradient_batch(const double *d_surf, const double *d_tgt, uint64_t n, const pmz_params *p,
+                             double *d_out12, void *d_ws, uint64_t ws_bytes, void *stream) {
+  if (!p || (p->S != 1 && p->S != 3) || p->H != 2) return PMZ_ERR_CONFIG;
+  if (ws_bytes < (uint64_t)PMZ_TRAIN_BATCH_WS) return PMZ_ERR_WORKSPACE;
+  cudaStream_t st = (cudaStream_t)stream;
+  KParams k = kparams(p);
+  const unsigned grid = PMZ_TRAIN_BATCH_WS / (kTrC * 8);
+  k_train_batch<<<grid, kTrT, 0, st>>>(k, d_surf, d_tgt, n, reinterpret_cast<double *>(d_ws));
+  k_train_reduce<<<1, 32, 0, st>>>(reinterpret_cast<const double *>(d_ws), grid, d_out12);
+  return launch_check();
+}

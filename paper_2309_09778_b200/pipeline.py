@@ -535,8 +535,11 @@ def _codec(device=None) -> Codec:
 def compress(data, rel_error: float = 1e-2, block_size=(256, 256), partition_rows: int = 32,
              model: PerceptronModel | None = None, repair_factor: float = REPAIR_FACTOR_SPEC,
              coverage_target: float = COVERAGE_TARGET, sample_rate: float = SAMPLE_RATE, seed: int = 0,
-             m: int = 0, device=None, return_info: bool = False):
-    """cmd_compress minus ingest/training: array in, container bytes out."""
+             m: int = 0, device=None, return_info: bool = False, train: bool = False, grid=None):
+    """cmd_compress minus ingest: array in, container bytes
+    out.  ``train=True`` (or a ``grid`` of HyperConfigs) runs the inline
+    training sweep first (training.py) and compresses with the
+    selected model; the default is ``model`` or init_model (BASELINE runs)."""
     cfg = CompressConfig(rel_error, int(block_size[0]), int(block_size[1]), partition_rows, repair_factor,
                          coverage_target, sample_rate, seed, m, model)
     codec = _codec(device)
@@ -545,6 +548,10 @@ def compress(data, rel_error: float = 1e-2, block_size=(256, 256), partition_row
     else:
         a = np.ascontiguousarray(np.asarray(data), dtype=np.float32)
         x = torch.from_numpy(a).to(codec.device)
+    if train or grid is not None:
+        from dataclasses import replace
+        from . import training
+        cfg = replace(cfg, model=training.train(codec, x, cfg, grid).model)
     buf, info = codec.compress_device(x, cfg)
     host = buf.cpu().numpy().tobytes()
     return (host, info) if return_info else host

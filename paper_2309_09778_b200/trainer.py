@@ -4,7 +4,7 @@ Only the seeded block sampling + 8:2 split that name the validation blocks
 live here (host-side integer work); ``select_m``'s residual
 histogram and ``estimate_codebook``'s validation histogram + Huffman build run
 on the GPU inside the compress stages (csrc/compress.cuh, csrc/encode.cuh).
-The training sweep itself is SURVEY.md §8(f) row f1 (out of this round).
+The training sweep itself is training.py.
 """
 from __future__ import annotations
 

@@ -11,7 +11,7 @@ def test_exit_codes_per_family(tmp_path, capsys):
     assert cli.main(["compress", "--input", str(tmp_path / "missing.f32"), "--output", out]) == 7  # IngestError
     assert cli.main(["compress", "--input", "gen:C2", "--rel-error", "0", "--output", out]) == 2  # ConfigError
     assert cli.main(["compress", "--input", "x.sgy", "--format", "segy", "--output", out]) == 2
-    assert cli.main(["compress", "--input", "gen:C2", "--grid", "lr:1e-3", "--output", out]) == 2
+    assert cli.main(["compress", "--input", "gen:C2", "--grid", "lr:0", "--output", out]) == 2  # lr > 0
     assert cli.main(["compress", "--input", "gen:C2", "--threads", "0", "--output", out]) == 2
     assert cli.main(["decompress", "--input", str(tmp_path / "missing.pmz")]) == 7
     raw = tmp_path / "a.f32"
@@ -49,3 +49,18 @@ def test_cli_bench_rows_and_cr_monotone(capsys):
     assert rows[0][0] == "dataset" and len(rows) == 4
     cr = [float(r[6]) for r in rows[1:]]
     assert cr[0] >= cr[1] >= cr[2]  # AC8: CR non-increasing as b_r grows
+
+
+@pytest.mark.gpu
+def test_cli_train_save_load_model(tmp_path, capsys):
+    """--train runs the sweep; the saved model blob reloads and gives the
+    identical container (SPEC.md:607 --save-model / --load-model)."""
+    c1, c2, mb = tmp_path / "a.pmz", tmp_path / "b.pmz", tmp_path / "m.bin"
+    base = ["compress", "--input", "gen:C2", "--dims", "400x600", "--rel-error", "1e-2"]
+    assert cli.main(base + ["--train", "--save-model", str(mb), "--output", str(c1)]) == 0
+    assert cli.main(base + ["--load-model", str(mb), "--output", str(c2)]) == 0
+    capsys.readouterr()
+    assert c1.read_bytes() == c2.read_bytes()
+    from paper_2309_09778_b200.predictor import PerceptronModel, init_model
+    m = PerceptronModel.from_bytes(mb.read_bytes())
+    assert not np.array_equal(m.w1, init_model(3).w1)
