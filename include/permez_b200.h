@@ -224,6 +224,17 @@ PMZ_API int pmz_train_gradient(const float *d_in, const pmz_geom *g, const pmz_p
 PMZ_API int pmz_train_gradient_batch(const double *d_surf, const double *d_tgt, uint64_t n, const pmz_params *p,
                                      double *d_out12, void *d_ws, uint64_t ws_bytes, void *stream);
 
+/* --- SEG-Y ingest ----------------- */
+
+/* read_segy's sample conversion: d_traces = the trace records of a rev-0
+ * file (n_traces x (240-byte header + ns big-endian 32-bit samples)) in
+ * device memory -> d_out[n_traces][ns] IEEE float32, traces as rows.
+ * format_code 1 (IBM hex float, exact in double, one rounding to float32) or
+ * 5 (IEEE); anything else -> PMZ_ERR_CONFIG (UnsupportedFormatCode is
+ * raised by the host reader before).  Stream-ordered. */
+PMZ_API int pmz_segy_samples(const uint8_t *d_traces, uint64_t n_traces, uint32_t ns, int format_code, float *d_out,
+                             void *stream);
+
 /* --- transform module (transform.py) on device ------------------------------ */
 
 /* Per-block transform parameters: 10 doubles per block in TransformParams

@@ -303,3 +303,16 @@ def slow_counts():
     a = np.zeros(3, np.int64)
     lib().orc_slow_counts(_ptr(a))
     return a.tolist()
+
+
+def ibm_to_ieee(words: np.ndarray) -> np.ndarray:
+    """Oracle of the IBM hex-float conversion (read_segy):
+    (-1)^s * 0.fraction * 16^(exponent - 64), evaluated exactly in double and
+    rounded once to float32."""
+    w = np.asarray(words, dtype=np.uint32)
+    frac = (w & 0xFFFFFF).astype(np.float64)
+    e = ((w >> 24) & 0x7F).astype(np.int64)
+    v = np.ldexp(frac, (4 * (e - 64) - 24).astype(np.int32))
+    with np.errstate(over="ignore"):
+        f = v.astype(np.float32)
+    return np.where((w >> 31) == 1, -f, f).astype(np.float32)

@@ -81,6 +81,7 @@ _SIGS = {
     "pmz_train_gradient": (c_int32, [VP, ctypes.POINTER(Geom), ctypes.POINTER(Params), VP, c_int64, VP, VP, c_uint64,
                                      VP]),
     "pmz_train_gradient_batch": (c_int32, [VP, VP, c_uint64, ctypes.POINTER(Params), VP, VP, c_uint64, VP]),
+    "pmz_segy_samples": (c_int32, [VP, c_uint64, c_uint32, c_int32, VP, VP]),
     "pmz_transform_params": (c_int32, [VP, ctypes.POINTER(Geom), ctypes.POINTER(Params), VP, VP, VP, c_uint64, VP]),
     "pmz_forward_map": (c_int32, [VP, c_uint64, VP, VP, VP]),
     "pmz_inverse_map": (c_int32, [VP, c_uint64, VP, VP, VP, VP]),

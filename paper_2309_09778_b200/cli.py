@@ -14,8 +14,8 @@ runs on the GPU through the library; there is no CPU path.  ``--threads`` is
 accepted for flag compatibility (the device decides its own parallelism;
 output is deterministic for any value).  ``--train`` / ``--grid``
 run the inline training sweep (training.py); ``--save-model`` /
-``--load-model`` write / read the model blob.  Not supported here: ``--format
-segy`` (SEG-Y ingest, row f3) raises ConfigError (exit code 2).
+``--load-model`` write / read the model blob; ``--format segy`` reads rev-0
+SEG-Y (format codes 1 and 5, ingest.py).
 """
 from __future__ import annotations
 
@@ -66,11 +66,13 @@ def _read_input(a) -> tuple[np.ndarray, str]:
     src = a.input
     if src.startswith("gen:"):
         return _generate(src[4:], _dims(a.dims) if a.dims else None, a.seed), src
-    fmt = a.format or ("raw32" if src.endswith((".f32", ".raw")) else "npy" if src.endswith(".npy") else None)
-    if fmt == "segy":
-        raise E.ConfigError("SEG-Y ingest is not part of this build (SURVEY.md §8(f) row f3)")
+    fmt = a.format or ("raw32" if src.endswith((".f32", ".raw")) else "npy" if src.endswith(".npy") else
+                       "segy" if src.endswith((".sgy", ".segy")) else None)
     if not os.path.exists(src):
         raise E.IngestError(f"cannot read {src!r}")
+    if fmt == "segy":  # traces as rows, sample conversion on the device (ingest.py)
+        from . import ingest
+        return ingest.read_segy(src, a.device).cpu().numpy(), os.path.basename(src)
     try:
         if fmt == "npy":
             x = np.load(src)

@@ -17,6 +17,7 @@
 #include "fwdq.cuh"
 #include "dec4.cuh"
 #include "train.cuh"
+#include "segy.cuh"
 
 using namespace pmz;
 
@@ -814,5 +815,18 @@ int pmz_train_gradient_batch(const double *d_surf, const double *d_tgt, uint64_t
   const unsigned grid = PMZ_TRAIN_BATCH_WS / (kTrC * 8);
   k_train_batch<<<grid, kTrT, 0, st>>>(k, d_surf, d_tgt, n, reinterpret_cast<double *>(d_ws));
   k_train_reduce<<<1, 32, 0, st>>>(reinterpret_cast<const double *>(d_ws), grid, d_out12);
+  return launch_check();
+}
+
+// ---------------------------------------------------------------------------
+// SEG-Y ingest
+
+int pmz_segy_samples(const uint8_t *d_traces, uint64_t n_traces, uint32_t ns, int format_code, float *d_out,
+                     void *stream) {
+  if (format_code != 1 && format_code != 5) return PMZ_ERR_CONFIG;
+  if (n_traces == 0 || ns == 0) return PMZ_OK;
+  const uint64_t n = n_traces * ns;
+  const unsigned grid = (unsigned)std::min<uint64_t>((n + 255) / 256, 148ull * 16);
+  k_segy_samples<<<grid, 256, 0, (cudaStream_t)stream>>>(d_traces, n_traces, ns, format_code, d_out);
   return launch_check();
 }

@@ -10,7 +10,7 @@ def test_exit_codes_per_family(tmp_path, capsys):
     out = str(tmp_path / "x.pmz")
     assert cli.main(["compress", "--input", str(tmp_path / "missing.f32"), "--output", out]) == 7  # IngestError
     assert cli.main(["compress", "--input", "gen:C2", "--rel-error", "0", "--output", out]) == 2  # ConfigError
-    assert cli.main(["compress", "--input", "x.sgy", "--format", "segy", "--output", out]) == 2
+    assert cli.main(["compress", "--input", str(tmp_path / "x.sgy"), "--format", "segy", "--output", out]) == 7
     assert cli.main(["compress", "--input", "gen:C2", "--grid", "lr:0", "--output", out]) == 2  # lr > 0
     assert cli.main(["compress", "--input", "gen:C2", "--threads", "0", "--output", out]) == 2
     assert cli.main(["decompress", "--input", str(tmp_path / "missing.pmz")]) == 7
