@@ -1,6 +1,6 @@
 // decompress.cuh -- read_container record parsing and the canonical Huffman
 // decode tables (decode_next); the decode itself is in
-// dec3.cuh, decompress_block + inverse_map
+// dec4.cuh, decompress_block + inverse_map
 // (transform.py:188-202) in dsc.cuh.
 #pragma once
 #include "common.cuh"

@@ -748,7 +748,7 @@ __global__ void __launch_bounds__(kWT) k_write_part(Geom g, const BlkP *__restri
   if (st->err_bits) return;
   const int m = st->m;
   const unsigned long long rec_base = st->header_bytes;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x;
   const int64_t p = blockIdx.x;
   int64_t b;
   int pi;
