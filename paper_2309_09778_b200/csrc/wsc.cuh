@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(kPPC * 64) k_compress_ws(const float *__restri
       // step t+1's inputs (ring loads, dq, class predicates) are prepared in
       // step t's basic block so they fill the latency gaps of t's chain.
       struct In {
-        double v, dq;
+        double v, dq, dqmv;
         int idx;
         bool started, active, anchor, normal, c1, c2, c0;
       };
@@ -292,6 +292,7 @@ __global__ void __launch_bounds__(kPPC * 64) k_compress_ws(const float *__restri
         q.anchor = lane0 & (c == 0);
         q.normal = (abs(rq) < c_center) & !q.anchor;
         q.dq = __dmul_rn((double)rq, c_two_ba);
+        q.dqmv = __dsub_rn(q.dq, q.v);  // d = a + (dq - v): off the chain (see below)
         q.c1 = cls == 1;
         q.c2 = cls == 2;
         q.c0 = cls == 0;
@@ -312,7 +313,11 @@ __global__ void __launch_bounds__(kPPC * 64) k_compress_ws(const float *__restri
         }
         double vhat = __dadd_rn(a, cur.dq);
         // classify (check_cls, D8), branch-free
-        const double d = __dsub_rn(vhat, cur.v);
+        // log-domain filter on d = (a + dq) - v evaluated as a + (dq - v): the
+        // two differ by a few ulp of |vhat| (< 2^-40 here), far inside the
+        // filter's 2^-20 margin, so every decision is the one the exact d
+        // gives, and d no longer waits for vhat
+        const double d = __dadd_rn(a, cur.dqmv);
         const bool gz = vhat > c_zthr, gb = vhat > c_bnd;
         const bool in12 = (cur.c1 & gz & !gb) | (cur.c2 & gb);
         const bool inner = (d < c_dpm) & (d > c_dnm);
