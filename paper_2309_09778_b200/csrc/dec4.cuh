@@ -48,8 +48,6 @@ __device__ __forceinline__ unsigned d3_smid() { unsigned r; asm volatile("mov.u3
 #endif
 
 struct D4Smem {
-  uint16_t sym12[1 << kLutBits];  // first-level table: symbol of the codeword on the next 12 bits
-  uint8_t len12[1 << kLutBits];   // its length; 0: longer than 12 bits (global tables)
   union {
     uint16_t map[kD4Threads][32];          // subsegment maps: (count << 5) | exit offset, per entry offset
     uint16_t ras[kD4Ras + kD4Ras / 32];    // the partition's codes, raster order, padded (write pass)
@@ -130,18 +128,18 @@ __device__ __forceinline__ unsigned d4_len(unsigned top, const uint8_t *__restri
 
 // The codeword at the top of the reader (nb >= 32 valid bits) and how many
 // times it repeats back-to-back inside the valid bits (1 <= k <= lim).
-__device__ __forceinline__ void d4_run(unsigned long long buf, int nb, unsigned lim, const D4Smem &W,
-                                       const unsigned *__restrict__ lut, const DecTab &tab,
+__device__ __forceinline__ void d4_run(unsigned long long buf, int nb, unsigned lim, const uint8_t *len12,
+                                       const uint16_t *sym12, const unsigned *__restrict__ lut, const DecTab &tab,
                                        const uint16_t *__restrict__ sym, unsigned &s, unsigned &l, unsigned &k) {
   const unsigned top = (unsigned)(buf >> 32);
   const unsigned i = top >> (32 - kLutBits);
-  l = W.len12[i];
+  l = len12[i];
   if (__builtin_expect(l == 0, 0)) {
     l = d4_slow(top, lut, tab, sym, s);
     k = 1;
     return;
   }
-  s = W.sym12[i];
+  s = sym12[i];
   // buf is periodic with period l over its first clz(buf ^ (buf << l)) + l bits
   const unsigned long long x = buf ^ (buf << l);
   const unsigned P = (x ? (unsigned)__clzll((long long)x) : 64u) + l;
@@ -165,6 +163,12 @@ __global__ void __launch_bounds__(kD4Threads, 6) k_decode4(const uint8_t *__rest
                                                        WsStatus *st) {
   constexpr int NS = kD4Threads;
   __shared__ DecTab s_tab;
+  // first-level tables as static shared arrays: addressed directly (a
+  // pointer into the dynamic block costs a generic-to-shared conversion per
+  // lookup): symbol of the codeword on the next 12 bits, and its length (0:
+  // longer than 12 bits, global tables)
+  __shared__ uint16_t s_sym12[1 << kLutBits];
+  __shared__ uint8_t s_len12[1 << kLutBits];
   extern __shared__ __align__(16) unsigned char dyn4[];
   D4Smem &W = *reinterpret_cast<D4Smem *>(dyn4);
   count_launch(st);
@@ -175,8 +179,8 @@ __global__ void __launch_bounds__(kD4Threads, 6) k_decode4(const uint8_t *__rest
   for (int i = t; i < (1 << kLutBits); i += NS) {
     const unsigned e = __ldg(lut + i);
     const bool direct = e != 0 && !(e & kLutL2Flag);
-    W.len12[i] = direct ? (uint8_t)((e >> 16) & 31u) : (uint8_t)0;
-    W.sym12[i] = (uint16_t)(e & 0xffffu);
+    s_len12[i] = direct ? (uint8_t)((e >> 16) & 31u) : (uint8_t)0;
+    s_sym12[i] = (uint16_t)(e & 0xffffu);
   }
   int64_t b;
   int pi;
@@ -239,7 +243,8 @@ __global__ void __launch_bounds__(kD4Threads, 6) k_decode4(const uint8_t *__rest
     auto word_init = [&](unsigned w, unsigned s0, unsigned s1) -> unsigned {
       const unsigned top = __funnelshift_l(s1, s0, (unsigned)lane);
       const bool in = 32u * w + (unsigned)lane < L;  // past the end: the offset carries over, nothing starts
-      return in ? ((unsigned)lane + d4_len(top, W.len12, lut, s_tab, sym)) | 0x100u : (unsigned)lane + 32u;
+      const unsigned l = d4_len(top, s_len12, lut, s_tab, sym);  // every lane (branch-free select below)
+      return in ? ((unsigned)lane + l) | 0x100u : (unsigned)lane + 32u;
     };
     auto jump = [&](unsigned &pk) {
       const unsigned x = pk & 0xffu;
@@ -343,7 +348,7 @@ __global__ void __launch_bounds__(kD4Threads, 6) k_decode4(const uint8_t *__rest
       for (unsigned i = 0; i < cnt;) {
         rd.refill(bs);
         unsigned s, l, k;
-        d4_run(rd.buf, rd.nb, cnt - i, W, lut, s_tab, sym, s, l, k);
+        d4_run(rd.buf, rd.nb, cnt - i, s_len12, s_sym12, lut, s_tab, sym, s, l, k);
         for (unsigned j = 0; j < k; j++) W.u.ras[d4_pad(idx + j)] = (uint16_t)s;
         idx += k;
         rd.skip(k * l);
@@ -370,7 +375,7 @@ __global__ void __launch_bounds__(kD4Threads, 6) k_decode4(const uint8_t *__rest
     for (unsigned i = 0; i < cnt;) {
       rd.refill(bs);
       unsigned s, l, k;
-      d4_run(rd.buf, rd.nb, cnt - i, W, lut, s_tab, sym, s, l, k);
+      d4_run(rd.buf, rd.nb, cnt - i, s_len12, s_sym12, lut, s_tab, sym, s, l, k);
       for (unsigned j = 0; j < k; j++) {
         ct[(c >> 5) * kTile + r * 32 + (c & 31)] = (uint16_t)s;
         if (s == 0) {
