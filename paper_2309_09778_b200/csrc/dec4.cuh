@@ -53,6 +53,7 @@ struct D4Smem {
     uint16_t ras[kD4Ras + kD4Ras / 32];    // the partition's codes, raster order, padded (write pass)
   } u;
   unsigned ent[kD4Threads], cnt[kD4Threads];
+  unsigned char on[kD4Threads], hit[kD4Threads];  // chain membership rounds (speculative path)
   unsigned zrow[32];
   unsigned wsum[kD4Warps];
   unsigned long long zb;                   // code-0 symbols of the earlier partitions of the block
@@ -124,6 +125,25 @@ __device__ __forceinline__ unsigned d4_len(unsigned top, const uint8_t *__restri
   if (__builtin_expect(l != 0, 1)) return l;
   unsigned sd;
   return d4_slow(top, lut, tab, sym, sd);
+}
+
+// Length l of the codeword at the top of the reader (nb >= 32 valid bits)
+// and how many back-to-back repeats of it start within the next lim bits
+// (k >= 1; a run is periodic with period l, clz(buf ^ (buf << l)) + l bits).
+__device__ __forceinline__ unsigned d4_len_run(unsigned long long buf, int nb, unsigned lim,
+                                               const uint8_t *len12, const unsigned *__restrict__ lut,
+                                               const DecTab &tab, const uint16_t *__restrict__ sym, unsigned &l) {
+  const unsigned top = (unsigned)(buf >> 32);
+  l = len12[top >> (32 - kLutBits)];
+  if (__builtin_expect(l == 0, 0)) {
+    unsigned sd;
+    l = d4_slow(top, lut, tab, sym, sd);
+    return 1;
+  }
+  const unsigned long long xx = buf ^ (buf << l);
+  const unsigned P = (xx ? (unsigned)__clzll((long long)xx) : 64u) + l;
+  const unsigned z = min(min(P, (unsigned)nb), lim + l - 1u);  // codewords starting before lim
+  return l == 1 ? z : max(__umulhi(z, tab.rcp[l]), 1u);
 }
 
 // The codeword at the top of the reader (nb >= 32 valid bits) and how many
@@ -213,6 +233,107 @@ __global__ void __launch_bounds__(kD4Threads, 6) k_decode4(const uint8_t *__rest
   const unsigned nw = (L + 31) >> 5;            // 32-bit words of the substream
   const unsigned wps = (nw + NS - 1) / NS;      // words per subsegment
 
+  // ---- 0. speculative decode (the cheap path, ~20x fewer instructions than
+  // the word maps).  Thread t parses its subsegment [s_t, s_t+1) from s_t,
+  // marking every codeword start in a bitmap; then it continues past its
+  // subsegment ("overrun") until it lands on a marked start of a later
+  // subsegment -- from there that subsegment's parse IS the continuation --
+  // or the end.  The true parse is thread 0's, its overrun, the parse +
+  // overrun of the thread it landed in, and so on (chain membership rounds).
+  // A parse that has not synchronised within kD4Cap subsegments (the
+  // reference's skewed codebooks can keep misaligned parses misaligned for
+  // thousands of bits) sends the whole partition to the exact word maps. ----
+  constexpr unsigned kBmWords = (unsigned)(sizeof(W.u) / 4);
+  constexpr unsigned kD4Cap = 16;
+  bool use_maps = nw + 2 > kBmWords;
+  if (!use_maps) {
+    unsigned *bm = reinterpret_cast<unsigned *>(&W.u);
+    const unsigned seg = 32u * wps;
+    const unsigned s_i = min(L, seg * (unsigned)t), s_n = min(L, seg * (unsigned)(t + 1));
+    for (unsigned q = min(nw, wps * (unsigned)t); q < min(nw, wps * (unsigned)(t + 1)); q++) bm[q] = 0;
+    if (t == 0) bm[nw] = bm[nw + 1] = 0;  // window reads past the last word
+    unsigned pos = s_i, nsp = 0;
+    if (s_i < s_n) {
+      D4Reader rd;
+      rd.seek(bs, s_i);
+      while (pos < s_n) {
+        rd.refill(bs);
+        unsigned l;
+        const unsigned k = d4_len_run(rd.buf, rd.nb, s_n - pos, s_len12, lut, s_tab, sym, l);
+        for (unsigned j = 0, q = pos; j < k; j++, q += l) bm[q >> 5] |= 1u << (q & 31);  // own words only
+        rd.skip(k * l);
+        pos += k * l;
+        nsp += k;
+      }
+    }
+    __syncthreads();  // every subsegment's starts are marked
+    unsigned y = pos, nov = 0;
+    bool hard = false;
+    if (y < L) {
+      D4Reader rd;
+      rd.seek(bs, y);
+      const unsigned cap = s_n + kD4Cap * seg;
+      while (y < L) {
+        const unsigned wq = y >> 5, off = y & 31;
+        unsigned long long win = ((unsigned long long)bm[wq] | ((unsigned long long)bm[wq + 1] << 32)) >> off;
+        if (off) win |= (unsigned long long)bm[wq + 2] << (64 - off);
+        if (win & 1ull) break;  // landed on a later subsegment's parse
+        if (y >= cap) {
+          hard = true;
+          break;
+        }
+        rd.refill(bs);
+        unsigned l;
+        unsigned k = d4_len_run(rd.buf, rd.nb, L - y, s_len12, lut, s_tab, sym, l);
+        if (k > 1) {  // a run stops at its first codeword that starts on a marked position
+          unsigned long long per = 0;
+          for (unsigned j = 1; j < k; j++) per |= 1ull << (j * l);
+          const unsigned long long hm = win & per;
+          if (hm) k = ((unsigned)__ffsll((long long)hm) - 1u) / l;
+        }
+        rd.skip(k * l);
+        y += k * l;
+        nov += k;
+      }
+    }
+    use_maps = __syncthreads_or(hard);
+    if (!use_maps) {
+      // chain membership: S_0 = all threads, S_{i+1} = {0} + landing threads
+      // of S_i: decreasing supersets of the true chain (usually stable after
+      // one round); the round that changes nothing stored the entries
+      const unsigned nxt = y >= L ? (unsigned)NS : min(y / seg, (unsigned)NS);
+      W.on[t] = 1;
+      for (;;) {
+        W.hit[t] = t == 0;
+        __syncthreads();
+        if (W.on[t] && nxt < (unsigned)NS) {
+          W.hit[nxt] = 1;
+          W.ent[nxt] = y;
+        }
+        __syncthreads();
+        const bool ch = W.hit[t] != W.on[t];
+        W.on[t] = W.hit[t];
+        if (!__syncthreads_or(ch)) break;
+      }
+      const bool on = W.on[t];
+      const unsigned e = t == 0 ? 0u : W.ent[t];
+      unsigned c = 0;
+      if (on) {  // spec codewords from the entry on (rank = marked starts before it) + the overrun
+        unsigned rk = 0;
+        for (unsigned q = s_i >> 5; q < (e >> 5); q++) rk += __popc(bm[q]);
+        if (e & 31) rk += __popc(bm[e >> 5] & ((1u << (e & 31)) - 1u));
+        c = nsp - rk + nov;
+      }
+      const bool bad = on && nxt == (unsigned)NS && y != L;
+      const bool anybad = __syncthreads_or(bad);
+      W.ent[t] = on ? e : L;
+      W.cnt[t] = c;
+      if (t == 0) W.fin = anybad ? 0xffffffffu : (L & 31u);
+      __syncthreads();
+    }
+  }
+  D3P(6, use_maps ? 1ull : 0ull);
+  if (use_maps) {
   // ---- 1. subsegment maps (warp w: subsegments 32 w .. 32 w + 31 = the
   // contiguous words [wa, wb)).  Stream words arrive in coalesced batches of
   // 32 (lane i holds word bbase + i, the next batch is in flight) and are
@@ -298,7 +419,7 @@ __global__ void __launch_bounds__(kD4Threads, 6) k_decode4(const uint8_t *__rest
   if (t == 0) {
     unsigned e = 0;
     for (int j = 0; j < NS; j++) {
-      W.ent[j] = e;
+      W.ent[j] = min(L, 32u * wps * (unsigned)j + e);
       W.cnt[j] = 0;
       if ((unsigned)j * wps >= nw) continue;  // empty subsegment: the offset carries over
       const unsigned v = W.u.map[j][e];
@@ -308,9 +429,10 @@ __global__ void __launch_bounds__(kD4Threads, 6) k_decode4(const uint8_t *__rest
     W.fin = e;  // offset after the last word: (end of the last codeword) mod 32
   }
   __syncthreads();
+  }  // use_maps
   D3P(2, clock64());
   const unsigned cnt = W.cnt[t];
-  const unsigned entry = min(L, 32u * wps * (unsigned)t + W.ent[t]);
+  const unsigned entry = W.ent[t];
 
   // ---- 3. write pass: CTA scan of the counts, then every thread decodes its
   // span into the shared tiles, counting code-0 symbols per row ----

@@ -92,6 +92,7 @@ if hasattr(codec.lib, "pmz_d3prof_read") and not a.compress:
     ph = np.diff(A[:, :5], axis=1)
     print("d3prof parts", len(A), "start spread (cyc) p50/max", np.percentile(A[:, 0] - t0, 50), (A[:, 0] - t0).max(),
           "end max", (A[:, 4] - t0).max())
+    print("   partitions on the word-map path:", int((A[:, 6] == 1).sum()), "of", len(A))
     T = np.stack([A[:, 0], A[:, 1], A[:, 2], A[:, 3], A[:, 5], A[:, 4]], 1)
     ph = np.diff(T, axis=1)
     for i, nm in enumerate(["maps", "chain", "write", "lookback", "gather"]):
