@@ -61,6 +61,21 @@ struct D4Smem {
 };
 constexpr size_t kD4Smem = sizeof(D4Smem);
 
+// Starts of a run of k codewords of length l beginning at bit pos, OR-ed
+// into the bitmap as one periodic mask (k * l <= 64): at most three words.
+__device__ __forceinline__ void d4_mark_run(unsigned *bm, const unsigned long long *rep, unsigned pos, unsigned l,
+                                            unsigned k) {
+  // rep[l]: bits 0, l, 2l, ... below 64; k l <= 64, so (k - 1) l + 1 <= 64
+  const unsigned long long m = rep[l] & (k >= 64 ? ~0ull : ((1ull << ((k - 1) * l + 1)) - 1ull));
+  const unsigned off = pos & 31, w = pos >> 5;
+  bm[w] |= (unsigned)(m << off);
+  const unsigned long long hi = off ? (m >> (32 - off)) : (m >> 32);
+  if (hi) {
+    bm[w + 1] |= (unsigned)hi;
+    if (hi >> 32) bm[w + 2] |= (unsigned)(hi >> 32);
+  }
+}
+
 // Decoupled look-back flags: code-0 count + 1 once known, kD4Poison when the
 // partition failed (reset to 0 before every launch).
 constexpr unsigned kD4Poison = 0xffffffffu;
@@ -189,6 +204,7 @@ __global__ void __launch_bounds__(kD4Threads, 6) k_decode4(const uint8_t *__rest
   // longer than 12 bits, global tables)
   __shared__ uint16_t s_sym12[1 << kLutBits];
   __shared__ uint8_t s_len12[1 << kLutBits];
+  __shared__ unsigned long long s_rep[33];  // s_rep[l]: bits 0, l, 2l, ... (a run's starts)
   extern __shared__ __align__(16) unsigned char dyn4[];
   D4Smem &W = *reinterpret_cast<D4Smem *>(dyn4);
   count_launch(st);
@@ -196,6 +212,12 @@ __global__ void __launch_bounds__(kD4Threads, 6) k_decode4(const uint8_t *__rest
   const int64_t p = blockIdx.x;
   if (t == 0) s_tab = *tab;
   if (t < 32) W.zrow[t] = 0;
+  if (t <= 32) {
+    unsigned long long r = 0;
+    if (t >= 1)
+      for (int q = 0; q < 64; q += t) r |= 1ull << q;
+    s_rep[t] = r;
+  }
   for (int i = t; i < (1 << kLutBits); i += NS) {
     const unsigned e = __ldg(lut + i);
     const bool direct = e != 0 && !(e & kLutL2Flag);
@@ -260,7 +282,7 @@ __global__ void __launch_bounds__(kD4Threads, 6) k_decode4(const uint8_t *__rest
         rd.refill(bs);
         unsigned l;
         const unsigned k = d4_len_run(rd.buf, rd.nb, s_n - pos, s_len12, lut, s_tab, sym, l);
-        for (unsigned j = 0, q = pos; j < k; j++, q += l) bm[q >> 5] |= 1u << (q & 31);  // own words only
+        d4_mark_run(bm, s_rep, pos, l, k);  // own words only: every start < s_n
         rd.skip(k * l);
         pos += k * l;
         nsp += k;
