@@ -266,7 +266,10 @@ __global__ void __launch_bounds__(kD4Threads, 6) k_decode4(const uint8_t *__rest
   // reference's skewed codebooks can keep misaligned parses misaligned for
   // thousands of bits) sends the whole partition to the exact word maps. ----
   constexpr unsigned kBmWords = (unsigned)(sizeof(W.u) / 4);
-  constexpr unsigned kD4Cap = 16;
+#ifndef PMZ_D4_CAP
+#define PMZ_D4_CAP 16
+#endif
+  constexpr unsigned kD4Cap = PMZ_D4_CAP;
   bool use_maps = nw + 2 > kBmWords;
   if (!use_maps) {
     unsigned *bm = reinterpret_cast<unsigned *>(&W.u);
