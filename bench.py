@@ -155,8 +155,12 @@ def main():
     ap.add_argument("--eps", type=float, default=1e-2)
     ap.add_argument("--repair", type=float, default=1.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--pipeline", type=int, default=3,
-                    help="N=1: fields in flight for value/e2e (streams + captured graphs); 1 = one at a time")
+    ap.add_argument("--pipeline", type=int, default=6,
+                    help="fields / containers in flight on the device for value (streams + captured graphs); "
+                         "1 = one at a time")
+    ap.add_argument("--e2e-pipeline", type=int, default=3,
+                    help="fields in flight for the host-to-host e2e numbers (PCIe-bound: more depth only adds "
+                         "contention)")
     ap.add_argument("--profile-steps", type=int, default=0, help="(ncu) run this many steps, no JSON timing claims")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.profile_steps == 0 else args.warmup
@@ -467,18 +471,18 @@ def main():
     # pinned host field -> H2D -> graph -> status read-back -> D2H of the
     # container into pinned memory, every step; device-clock events around
     # the whole job (the last collect synchronises)
-    if world == 1 and args.pipeline > 1:
-        pc = P.PipelinedCompressor(codec, cfg, x.shape, depth=args.pipeline)
-        for _ in range(args.pipeline):
+    if world == 1 and args.e2e_pipeline > 1:
+        pc = P.PipelinedCompressor(codec, cfg, x.shape, depth=args.e2e_pipeline)
+        for _ in range(args.e2e_pipeline):
             pc.submit(h_in)
-        for _ in range(args.pipeline):
+        for _ in range(args.e2e_pipeline):
             pc.collect()
         torch.cuda.synchronize()
-        ne = max(2 * args.pipeline, K)
+        ne = max(2 * args.e2e_pipeline, K)
         ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ea.record()
         nsub = 0
-        for _ in range(args.pipeline):
+        for _ in range(args.e2e_pipeline):
             pc.submit(h_in)
             nsub += 1
         for _ in range(ne):
@@ -545,18 +549,19 @@ def main():
         dpipe = {"ms": da.elapsed_time(db2), "depth": depth}
         launches += K * DECOMPRESS_LAUNCHES
         # e2e through the public streaming API
-        pd = P.PipelinedDecompressor(codec, full_host, depth=depth)
+        edepth = max(1, args.e2e_pipeline)
+        pd = P.PipelinedDecompressor(codec, full_host, depth=edepth)
         hoffs = P.Codec.index_blocks(full_host, hdr)
-        for _ in range(depth):
+        for _ in range(edepth):
             pd.submit(h_cont, hoffs)
-        for _ in range(depth):
+        for _ in range(edepth):
             pd.collect()
         torch.cuda.synchronize()
-        ne = max(2 * depth, K)
+        ne = max(2 * edepth, K)
         ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ea.record()
         nsub = 0
-        for _ in range(depth):
+        for _ in range(edepth):
             pd.submit(h_cont, P.Codec.index_blocks(full_host, hdr))
             nsub += 1
         for _ in range(ne):
@@ -634,14 +639,14 @@ def main():
                             "ms_per_step": dpipe["ms"] / K,
                             "pipeline": f"{dpipe['depth']} containers in flight (streams, enqueue/result API)",
                             "single_stream": {"value": dec_gbs, "unit": "GB/s", "ms_per_step": d_tot / K},
-                            "e2e": {"value": e2e_dp, "unit": "GB/s", "api": f"PipelinedDecompressor depth {dpipe['depth']}",
+                            "e2e": {"value": e2e_dp, "unit": "GB/s", "api": f"PipelinedDecompressor depth {args.e2e_pipeline}",
                                     "h2d_bytes_per_step": int(info.nbytes), "d2h_bytes_per_step": int(n_elem * 4)},
                             "e2e_serial": {"value": e2e_d, "unit": "GB/s"}} if dpipe is not None else
                            {"value": dec_gbs, "unit": "GB/s", "ms_per_step": d_tot / K,
                             "e2e": {"value": e2e_d, "unit": "GB/s"}}),
             "e2e": {"value": e2e_c, "unit": "GB/s", "h2d_bytes_per_step": int(n_elem * 4),
                     "d2h_bytes_per_step": int(info.nbytes),
-                    "api": (f"PipelinedCompressor depth {args.pipeline}" if world == 1 and args.pipeline > 1
+                    "api": (f"PipelinedCompressor depth {args.e2e_pipeline}" if world == 1 and args.e2e_pipeline > 1
                             else "GraphedCompressor / compress_staged, one at a time")},
             "e2e_serial": e2e_serial,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
