@@ -325,13 +325,11 @@ __global__ void __launch_bounds__(kPPC * 64) k_compress_ws(const float *__restri
         bool acc = (in12 & inner) | (cur.c0 & !gz);
         bool vio = (cur.c1 | cur.c2) & (((c_tlt1 != 0) & !in12) | (in12 & outer));
         const bool rare = cur.active & ((PK == 3 & (fabs(a) < 0x1p-1020)) | (cur.normal & !acc & !vio));
-        if (__any_sync(0xffffffffu, rare)) {
-          if (rare) {
-            vhat = __dadd_rn(predict_steady<PK>(k, hl, nhl, pn, lane0), cur.dq);
-            const int cls = W.cls[0][cur.idx];
-            classify(vhat, cur.v, cls, acc, vio);
-            if (cur.normal && !acc && !vio) vio = exact_vio(vhat, t - lane);
-          }
+        if (__builtin_expect(rare, 0)) {  // per-lane branch, no warp vote on the dependency chain
+          vhat = __dadd_rn(predict_steady<PK>(k, hl, nhl, pn, lane0), cur.dq);
+          const int cls = W.cls[0][cur.idx];
+          classify(vhat, cur.v, cls, acc, vio);
+          if (cur.normal && !acc && !vio) vio = exact_vio(vhat, t - lane);
         }
         const bool keep = cur.normal & !vio;
         if (cur.active & cur.normal & vio) {
