@@ -23,7 +23,7 @@ ap.add_argument("--iters", type=int, default=10)
 ap.add_argument("--compress", action="store_true")
 a = ap.parse_args()
 
-shape = {"C2": None, "C3q": (128, 512, 512), "C4": None}[a.field]
+shape = {"C1": None, "C2": None, "C3q": (128, 512, 512), "C4": None}[a.field]
 name = "C3" if a.field == "C3q" else a.field
 x = synthetic.generate(name, shape=shape).cuda()
 codec = Codec()
