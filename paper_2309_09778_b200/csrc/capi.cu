@@ -533,6 +533,8 @@ int pmz_index_blocks(const uint8_t *h, uint64_t n, const pmz_header *hd, uint64_
 // decompression
 
 namespace {
+// every block is one partition of one row (1-D inputs, block_rows == 1)
+bool one_row_parts(const Geom &G) { return G.br == 1 || G.rows == 1; }
 struct DecLayout {
   size_t status, blkp, part_bits, part_off, zflag, anchors, bal_off, pay_off, blk_nbal, tab, sym, lut, codes,
       vtile, total;
@@ -565,6 +567,14 @@ DecLayout dec_layout(const Geom &g) {
 template <int PK>
 int launch_recon(const KParams &k, unsigned grid, cudaStream_t st, const Geom &G, void *d_ws, const DecLayout &L,
                  float *d_out) {
+  if (one_row_parts(G)) {
+    k_reconstruct_1d<PK><<<(unsigned)((G.nparts + 31) / 32), 32, 0, st>>>(
+        G, k, at<BlkP>(d_ws, L.blkp), at<uint16_t>(d_ws, L.codes), at<double>(d_ws, L.vtile),
+        at<double>(d_ws, L.anchors), d_out, at<WsStatus>(d_ws, L.status));
+    k_inv<<<(unsigned)G.nparts, 256, 0, st>>>(G, at<BlkP>(d_ws, L.blkp), at<double>(d_ws, L.vtile), d_out,
+                                              at<WsStatus>(d_ws, L.status));
+    return PMZ_OK;
+  }
   CK(cudaFuncSetAttribute(k_reconstruct4<PK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDsc4Smem));
   k_reconstruct4<PK><<<grid, kPPC * 64, kDsc4Smem, st>>>(
       G, k, at<BlkP>(d_ws, L.blkp), at<uint16_t>(d_ws, L.codes), at<double>(d_ws, L.vtile),
@@ -622,6 +632,18 @@ int pmz_decompress_enqueue(const uint8_t *d_buf, uint64_t n, const pmz_header *h
         at<unsigned long long>(d_ws, L.pay_off), at<unsigned long long>(d_ws, L.blk_nbal), S);
     k_dec_tables<<<1, 1024, 0, st>>>(d_buf + hdr->lens_offset, (int)hdr->m, at<DecTab>(d_ws, L.tab),
                                      at<uint16_t>(d_ws, L.sym), at<unsigned>(d_ws, L.lut), S);
+    if (one_row_parts(G)) {
+      k_decode_1d<<<(unsigned)((G.nparts + kD1T - 1) / kD1T), kD1T, 0, st>>>(
+          d_buf, n, G, at<BlkP>(d_ws, L.blkp), at<DecTab>(d_ws, L.tab), at<uint16_t>(d_ws, L.sym),
+          at<unsigned>(d_ws, L.lut), at<unsigned long long>(d_ws, L.part_bits),
+          at<unsigned long long>(d_ws, L.part_off), at<unsigned long long>(d_ws, L.pay_off),
+          at<unsigned long long>(d_ws, L.bal_off), at<unsigned long long>(d_ws, L.blk_nbal), 1 << ((int)hdr->m - 1),
+          k.two_ba, at<uint16_t>(d_ws, L.codes), at<double>(d_ws, L.vtile), S);
+      k_gather_1d<<<(unsigned)((G.nparts + 3) / 4), 128, 0, st>>>(
+          d_buf, n, G, at<BlkP>(d_ws, L.blkp), at<unsigned long long>(d_ws, L.bal_off),
+          at<unsigned long long>(d_ws, L.blk_nbal), 1 << ((int)hdr->m - 1), k.two_ba, at<uint16_t>(d_ws, L.codes),
+          at<double>(d_ws, L.vtile), S);
+    } else {
     CK(cudaMemsetAsync(at<unsigned>(d_ws, L.zflag), 0, 4 * (size_t)G.nparts, st));
     CK(cudaFuncSetAttribute(k_decode4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kD4Smem));
     k_decode4<<<(unsigned)G.nparts, kD4Threads, kD4Smem, st>>>(
@@ -630,6 +652,7 @@ int pmz_decompress_enqueue(const uint8_t *d_buf, uint64_t n, const pmz_header *h
         at<unsigned long long>(d_ws, L.part_off), at<unsigned long long>(d_ws, L.pay_off),
         at<unsigned long long>(d_ws, L.bal_off), at<unsigned long long>(d_ws, L.blk_nbal), 1 << ((int)hdr->m - 1),
         k.two_ba, at<unsigned>(d_ws, L.zflag), at<uint16_t>(d_ws, L.codes), at<double>(d_ws, L.vtile), S);
+    }
     const unsigned rgrid = (unsigned)((G.nparts + kPPC - 1) / kPPC);
     int s2;
     if (k.init_model == 3) s2 = launch_recon<3>(k, rgrid, st, G, d_ws, L, d_out);

@@ -642,3 +642,129 @@ __global__ void __launch_bounds__(kD4Threads, 6) k_decode4(const uint8_t *__rest
 }
 
 }  // namespace pmz
+
+namespace pmz {
+
+// ---------------------------------------------------------------------------
+// One-row partitions (1-D inputs, or block_rows == 1: every block is one
+// partition of one row).  A 32-row-tile CTA per partition would idle 31/32 of
+// its work; here a THREAD decodes a whole partition substream (lane per
+// partition), writing row 0 of the partition's code + addend tiles exactly as
+// k_decode4 does, so k_reconstruct_1d / k_inv consume the same layout.  A
+// block is one partition: its balance list starts at index 0 (no look-back).
+constexpr int kD1T = 32;  // small CTAs: the partitions spread over every SM
+__global__ void __launch_bounds__(kD1T) k_decode_1d(const uint8_t *__restrict__ buf, unsigned long long buf_n,
+                                                   Geom g, const BlkP *__restrict__ blkp,
+                                                   const DecTab *__restrict__ tab,
+                                                   const uint16_t *__restrict__ sym,
+                                                   const unsigned *__restrict__ lut,
+                                                   const unsigned long long *__restrict__ part_bits,
+                                                   const unsigned long long *__restrict__ part_off,
+                                                   const unsigned long long *__restrict__ pay_off,
+                                                   const unsigned long long *__restrict__ bal_off,
+                                                   const unsigned long long *__restrict__ blk_nbal, int center,
+                                                   double two_ba, uint16_t *__restrict__ codes,
+                                                   double *__restrict__ vtile, WsStatus *st) {
+  __shared__ DecTab s_tab;
+  __shared__ uint16_t s_sym12[1 << kLutBits];
+  __shared__ uint8_t s_len12[1 << kLutBits];
+  count_launch(st);
+  if (threadIdx.x == 0) s_tab = *tab;
+  for (int i = threadIdx.x; i < (1 << kLutBits); i += kD1T) {
+    const unsigned e = __ldg(lut + i);
+    s_len12[i] = (e != 0 && !(e & kLutL2Flag)) ? (uint8_t)((e >> 16) & 31u) : (uint8_t)0;
+    s_sym12[i] = (uint16_t)(e & 0xffffu);
+  }
+  __syncthreads();
+  const int64_t p = (int64_t)blockIdx.x * kD1T + threadIdx.x;
+  if (p >= g.nparts) return;
+  int64_t b;
+  int pi;
+  part_of(g, p, b, pi);
+  if (blkp[b].trivial) return;
+  const BlockBox bb = block_box(g, b);
+  const int C = bb.bc;
+  const unsigned nsym = (unsigned)(C - 1);
+  const unsigned long long L64 = part_bits[p];
+  if (L64 > 32ull * (nsym + 1ull)) {
+    set_err_at(st, PMZ_ERR_CORRUPT, 1, p);
+    return;
+  }
+  BitSrc bs;
+  {
+    const uint8_t *src = buf + pay_off[b] + part_off[p];
+    const uintptr_t a = reinterpret_cast<uintptr_t>(src);
+    bs.base = reinterpret_cast<const uint8_t *>(a & ~(uintptr_t)3);
+    bs.adj = (unsigned)(8 * (a & 3));
+    bs.nbits = L64;
+    bs.end = buf + buf_n;
+  }
+  uint16_t *ct = codes + tile_base(g, p, 0);
+  ct[0] = kAnc;
+  unsigned pos = 0, c = 1;
+  D4Reader rd;
+  rd.seek(bs, 0);
+  while (c <= nsym) {
+    rd.refill(bs);
+    unsigned s, l, k;
+    d4_run(rd.buf, rd.nb, nsym + 1 - c, s_len12, s_sym12, lut, s_tab, sym, s, l, k);
+    for (unsigned j = 0; j < k; j++, c++) ct[(c >> 5) * kTile + (c & 31)] = (uint16_t)s;
+    rd.skip(k * l);
+    pos += k * l;
+  }
+  if (pos != (unsigned)L64) set_err_at(st, pos < L64 ? PMZ_ERR_CORRUPT : PMZ_ERR_TRUNCATED, 12, p);
+}
+
+// The addends of one-row partitions (a warp per partition, lane = column of
+// a 32-column chunk): balance value at code 0 (ranked by ballots, the block's
+// list from index 0), (code - center) * 2 b_a elsewhere -- coalesced.
+__global__ void __launch_bounds__(128) k_gather_1d(const uint8_t *__restrict__ buf, unsigned long long buf_n,
+                                                  Geom g, const BlkP *__restrict__ blkp,
+                                                  const unsigned long long *__restrict__ bal_off,
+                                                  const unsigned long long *__restrict__ blk_nbal, int center,
+                                                  double two_ba, const uint16_t *__restrict__ codes,
+                                                  double *__restrict__ vtile, WsStatus *st) {
+  const int lane = threadIdx.x & 31;
+  const int64_t p = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (p >= g.nparts) return;
+  int64_t b;
+  int pi;
+  part_of(g, p, b, pi);
+  if (blkp[b].trivial || st->err_bits) return;
+  const int C = block_box(g, b).bc, nch = (C + 31) >> 5;
+  const uint8_t *bal = buf + bal_off[b];
+  const uintptr_t ba = reinterpret_cast<uintptr_t>(bal);
+  const unsigned sh = (unsigned)(ba & 7) * 8;
+  const unsigned long long *qb = reinterpret_cast<const unsigned long long *>(ba & ~(uintptr_t)7);
+  const long long nwd = (long long)((reinterpret_cast<uintptr_t>(buf + buf_n) - (ba & ~(uintptr_t)7)) >> 3);
+  const unsigned long long nbal = blk_nbal[b];
+  const uint16_t *ct = codes + tile_base(g, p, 0);
+  double *vt = vtile + tile_base(g, p, 0);
+  unsigned long long base = 0;
+  for (int kc = 0; kc < nch; kc++) {
+    const int c = kc * 32 + lane;
+    const unsigned code = c < C ? ct[kc * kTile + lane] : 1u;  // the anchor reads kAnc: not a code
+    const unsigned zm = __ballot_sync(0xffffffffu, code == 0u);
+    double v = __dmul_rn((double)((int)code - center), two_ba);
+    if (code == 0u) {
+      const long long i = (long long)(base + __popc(zm & ((1u << lane) - 1u)));
+      if ((unsigned long long)i < nbal) {
+        unsigned long long u = __ldg(qb + i);
+        if (sh) {
+          if (i + 2 <= nwd) u = (u >> sh) | (__ldg(qb + i + 1) << (64 - sh));
+          else {
+            u = 0;
+            for (int q = 7; q >= 0; q--) u = (u << 8) | __ldg(bal + 8 * i + q);
+          }
+        }
+        v = __longlong_as_double((long long)u);
+      }
+    }
+    base += __popc(zm);
+    if (c < C) vt[kc * kTile + lane] = v;
+  }
+  if (lane == 0 && base != nbal)
+    set_err_at(st, base > nbal ? PMZ_ERR_BALANCE_UNDERFLOW : PMZ_ERR_CORRUPT, 30, p);
+}
+
+}  // namespace pmz

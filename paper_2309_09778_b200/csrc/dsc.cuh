@@ -205,3 +205,76 @@ __global__ void __launch_bounds__(256) k_inv(Geom g, const BlkP *__restrict__ bl
 }
 
 }  // namespace pmz
+
+namespace pmz {
+
+// One-row partitions: the W-only recurrence, a lane per partition (no
+// shuffles), 32 partitions per warp.  Every 32-column chunk of the warp's
+// partitions is staged through shared memory with coalesced loads (lane =
+// column), run from there (lane = partition) and written back the same way;
+// the reconstructed values replace the addends for k_inv.
+template <int PK>
+__global__ void __launch_bounds__(32) k_reconstruct_1d(Geom g, KParams k, const BlkP *__restrict__ blkp,
+                                                        const uint16_t *__restrict__ codes, double *vtile,
+                                                        const double *__restrict__ anchors, float *__restrict__ out,
+                                                        WsStatus *st) {
+  __shared__ double sv[1][32][33];
+  __shared__ uint16_t sc[1][32][34];
+  count_launch(st);
+  const int lane = threadIdx.x & 31, w = 0;  // one warp per CTA: the CTAs spread over every SM
+  const int64_t p0 = (int64_t)blockIdx.x * 32;  // the warp's first partition
+  if (p0 >= g.nparts) return;
+  const int64_t p = p0 + lane;
+  const bool mine = p < g.nparts;
+  int C = 0, nch_max = 0;
+  bool live = false;
+  double hl = 0.0;
+  if (mine) {
+    int64_t b;
+    int pi;
+    part_of(g, p, b, pi);
+    const BlockBox bb = block_box(g, b);
+    C = bb.bc;
+    if (blkp[b].trivial) {
+      float *o = out + (bb.r0 + pi * g.prow) * g.cols + bb.c0;
+      for (int c = 0; c < C; c++) o[c] = 0.0f;
+    } else {
+      live = true;
+      hl = anchors[p];
+    }
+  }
+  if (__any_sync(0xffffffffu, live) && st->err_bits) return;
+  int cmax = C;
+  for (int o = 16; o > 0; o >>= 1) cmax = max(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
+  nch_max = (cmax + 31) >> 5;
+  const unsigned lm = __ballot_sync(0xffffffffu, live);
+  for (int kc = 0; kc < nch_max; kc++) {
+    // stage: partition i's chunk kc, lane = column
+    for (int i = 0; i < 32; i++) {
+      if (!((lm >> i) & 1u)) continue;
+      const int64_t o = tile_base(g, p0 + i, kc) + lane;
+      sv[w][i][lane] = vtile[o];
+      sc[w][i][lane] = codes[o];
+    }
+    __syncwarp();
+    if (live) {
+      for (int j = 0; j < 32; j++) {
+        const int c = kc * 32 + j;
+        if (c >= C) break;
+        if (c == 0) { sv[w][lane][0] = hl; continue; }  // the anchor (D1)
+        const double a = sv[w][lane][j];
+        const double vhat = __dadd_rn(predict_steady<PK>(k, hl, 0.0, 0.0, true), a);
+        hl = sc[w][lane][j] == 0 ? a : vhat;
+        sv[w][lane][j] = hl;
+      }
+    }
+    __syncwarp();
+    for (int i = 0; i < 32; i++) {
+      if (!((lm >> i) & 1u)) continue;
+      vtile[tile_base(g, p0 + i, kc) + lane] = sv[w][i][lane];
+    }
+    __syncwarp();
+  }
+}
+
+}  // namespace pmz

@@ -83,7 +83,7 @@ def test_edge_shapes(codec, oracle, shape):
 
 
 @pytest.mark.parametrize("br,bc,pr", [(64, 128, 16), (32, 32, 8), (100, 60, 7), (256, 256, 32), (512, 64, 32),
-                                      (64, 512, 32), (40, 1000, 20)])
+                                      (64, 512, 32), (40, 1000, 20), (1, 100, 32), (1, 256, 1)])
 def test_block_geometries(codec, oracle, br, bc, pr):
     x = _field("C2", (300, 500))
     _parity(codec, oracle, x, b_r=1e-2, repair_factor=1.0, block_rows=br, block_cols=bc, partition_rows=pr)
