@@ -321,3 +321,30 @@ def test_decompress_corrupted_tables(codec, oracle, what):
         struct.pack_into("<Q", a, nb_at, nb + (1 if what == "nbal_plus" else -1))
     with pytest.raises(E.PermezError):
         P.decompress(bytes(a), device="cuda:0")
+
+
+@pytest.mark.parametrize("d", [-1, 1])
+def test_decompress_corrupted_1d(codec, oracle, d):
+    """One-row partitions take the 1-D decoder: a framing-preserving +-1 bit
+    edit of a partition's substream length must raise, not hang or pass."""
+    import struct
+    import paper_2309_09778_b200 as P
+    from paper_2309_09778_b200 import errors as E
+    x = _field("C1", (1 << 16,))
+    buf, _ = oracle.compress(x, oracle.OracleConfig(b_r=1e-2, repair_factor=1.0, S=1))
+    b = np.frombuffer(buf, np.uint8)
+    h = P.Codec.parse_header(b)
+    offs = P.Codec.index_blocks(b, h)
+    a = bytearray(buf)
+    for blk in range(int(h.nblocks)):
+        o = int(offs[blk])
+        if a[o] != 0:
+            continue
+        (bl,) = struct.unpack_from("<Q", a, o + 17 + 8)
+        if bl > 8 and (bl + d + 7) // 8 == (bl + 7) // 8:
+            struct.pack_into("<Q", a, o + 17 + 8, bl + d)
+            break
+    else:
+        pytest.skip("no framing-preserving edit")
+    with pytest.raises(E.PermezError):
+        P.decompress(bytes(a), device="cuda:0")
