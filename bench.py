@@ -486,10 +486,11 @@ def main():
             pc.submit(h_in)
             nsub += 1
         for _ in range(ne):
-            hb, hi = pc.collect()
+            hb, hi = pc.collect(block=False)  # copy-out in flight while the next field goes in
             if nsub < ne:
                 pc.submit(h_in)
                 nsub += 1
+        pc.wait()
         eb.record()
         torch.cuda.synchronize()
         assert hi.nbytes == infok.nbytes and bytes(hb.numpy()[:64]) == bytes(full_host[:64])
@@ -565,10 +566,11 @@ def main():
             pd.submit(h_cont, P.Codec.index_blocks(full_host, hdr))
             nsub += 1
         for _ in range(ne):
-            yh = pd.collect()
+            yh = pd.collect(block=False)  # copy-out in flight while the next container goes in
             if nsub < ne:
                 pd.submit(h_cont, P.Codec.index_blocks(full_host, hdr))
                 nsub += 1
+        pd.wait()
         eb.record()
         torch.cuda.synchronize()
         assert torch.equal(yh, out.cpu())

@@ -430,24 +430,37 @@ class PipelinedCompressor:
         self._next = (i + 1) % self.depth
         sl = self.slots[i]
         with torch.cuda.stream(sl["stream"]):
+            # the slot's previous container copy-out must have landed before
+            # its graph runs again (collect(block=False) leaves it in flight)
+            sl["stream"].wait_event(sl["done"])
             sl["x"].copy_(host_field, non_blocking=True)
             sl["gc"].launch()
         self._queue.append(i)
         return i
 
-    def collect(self):
+    def collect(self, block: bool = True):
         """(container bytes as a pinned uint8 CPU view, CompressInfo) of the
-        oldest submitted field."""
+        oldest submitted field.  With ``block=False`` the device->host copy of
+        the container is only enqueued: submit the next field right away (its
+        host->device copy then overlaps this copy-out on the full-duplex link)
+        and call ``wait()`` before reading the bytes."""
         if not self._queue:
             raise ConfigError("nothing submitted")
         i = self._queue.pop(0)
         sl = self.slots[i]
         with torch.cuda.stream(sl["stream"]):
-            buf, info = sl["gc"].result()      # synchronises this slot's stream
+            buf, info = sl["gc"].result()      # synchronises this slot's stream (status read-back)
             sl["host_out"][: info.nbytes].copy_(buf, non_blocking=True)
             sl["done"].record(sl["stream"])
-        sl["done"].synchronize()
+        self._last = sl["done"]
+        if block:
+            sl["done"].synchronize()
         return sl["host_out"][: info.nbytes], info
+
+    def wait(self):
+        """Wait for the copy-out of the last collected field."""
+        if getattr(self, "_last", None) is not None:
+            self._last.synchronize()
 
 
 class PipelinedDecompressor:
@@ -480,6 +493,7 @@ class PipelinedDecompressor:
                 "offs": torch.empty(int(self.h.nblocks) + 1, dtype=torch.int64, device=codec.device),
                 "ws": torch.empty(max(int(wsz.value), 1), dtype=torch.uint8, device=codec.device),
                 "h_offs": torch.empty(int(self.h.nblocks) + 1, dtype=torch.int64, pin_memory=True),
+                "done": torch.cuda.Event(),
                 "out": torch.empty(self.shape, dtype=torch.float32, device=codec.device),
                 "host_out": torch.empty(self.shape, dtype=torch.float32, pin_memory=True),
                 "n": 0})
@@ -507,21 +521,35 @@ class PipelinedDecompressor:
             check(lib.pmz_decompress_enqueue(_ptr(sl["buf"]), n, ctypes.byref(self.h), host_b_a(self.h.b_r),
                                              _ptr(sl["offs"]), _ptr(sl["out"]), _ptr(sl["ws"]), sl["ws"].numel(),
                                              ctypes.c_void_p(sl["stream"].cuda_stream)), "decompress")
-            sl["host_out"].copy_(sl["out"], non_blocking=True)
         sl["n"] = n
         self._queue.append(i)
         return i
 
-    def collect(self) -> torch.Tensor:
+    def collect(self, block: bool = True) -> torch.Tensor:
         """The oldest submitted container's float32 grid (a pinned CPU tensor
-        view, valid until its slot is reused)."""
+        view, valid until its slot is reused).  The status is read first
+        (synchronising the slot's kernels), then the grid is copied out; with
+        ``block=False`` that copy is left in flight -- submit the next
+        container right away (its host->device copy overlaps this copy-out)
+        and call ``wait()`` before reading the grid."""
         if not self._queue:
             raise ConfigError("nothing submitted")
         i = self._queue.pop(0)
         sl = self.slots[i]
         check(self.codec.lib.pmz_decompress_result(ctypes.byref(self.h), _ptr(sl["ws"]), sl["ws"].numel(),
                                                    ctypes.c_void_p(sl["stream"].cuda_stream)), "decompress")
+        with torch.cuda.stream(sl["stream"]):
+            sl["host_out"].copy_(sl["out"], non_blocking=True)
+            sl["done"].record(sl["stream"])
+        self._last = sl["done"]
+        if block:
+            sl["done"].synchronize()
         return sl["host_out"]
+
+    def wait(self):
+        """Wait for the copy-out of the last collected container."""
+        if getattr(self, "_last", None) is not None:
+            self._last.synchronize()
 
 
 def _codec(device=None) -> Codec:
