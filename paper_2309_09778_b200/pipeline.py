@@ -506,19 +506,24 @@ class PipelinedDecompressor:
         if len(self._queue) == self.depth:
             raise ConfigError("all slots in flight: collect() before submitting more")
         n = int(host_container.numel())
-        if n > self.cap:
-            raise ConfigError("container larger than the slot buffer")
+        h = Codec.parse_header(host_container.numpy())  # m / codebook / header size vary per container
+        if (h.rows, h.cols, h.block_rows, h.block_cols, h.partition_rows) != \
+                (self.h.rows, self.h.cols, self.h.block_rows, self.h.block_cols, self.h.partition_rows):
+            raise ConfigError("PipelinedDecompressor: container of another geometry")
         if block_offsets is None:
-            block_offsets = Codec.index_blocks(host_container.numpy(), self.h)
+            block_offsets = Codec.index_blocks(host_container.numpy(), h)
         i = self._next
         self._next = (i + 1) % self.depth
         sl = self.slots[i]
         lib = self.codec.lib
+        if n > sl["buf"].numel():  # the slot is idle (collected): grow its container buffer
+            sl["buf"] = torch.empty(n + (n >> 3), dtype=torch.uint8, device=self.codec.device)
         with torch.cuda.stream(sl["stream"]):
             sl["buf"][:n].copy_(host_container, non_blocking=True)
             sl["h_offs"].copy_(torch.from_numpy(np.asarray(block_offsets).view(np.int64)))  # slot is idle: safe
             sl["offs"].copy_(sl["h_offs"], non_blocking=True)
-            check(lib.pmz_decompress_enqueue(_ptr(sl["buf"]), n, ctypes.byref(self.h), host_b_a(self.h.b_r),
+            sl["h"] = h
+            check(lib.pmz_decompress_enqueue(_ptr(sl["buf"]), n, ctypes.byref(h), host_b_a(h.b_r),
                                              _ptr(sl["offs"]), _ptr(sl["out"]), _ptr(sl["ws"]), sl["ws"].numel(),
                                              ctypes.c_void_p(sl["stream"].cuda_stream)), "decompress")
         sl["n"] = n
@@ -536,7 +541,7 @@ class PipelinedDecompressor:
             raise ConfigError("nothing submitted")
         i = self._queue.pop(0)
         sl = self.slots[i]
-        check(self.codec.lib.pmz_decompress_result(ctypes.byref(self.h), _ptr(sl["ws"]), sl["ws"].numel(),
+        check(self.codec.lib.pmz_decompress_result(ctypes.byref(sl["h"]), _ptr(sl["ws"]), sl["ws"].numel(),
                                                    ctypes.c_void_p(sl["stream"].cuda_stream)), "decompress")
         with torch.cuda.stream(sl["stream"]):
             sl["host_out"].copy_(sl["out"], non_blocking=True)

@@ -348,3 +348,35 @@ def test_decompress_corrupted_1d(codec, oracle, d):
         pytest.skip("no framing-preserving edit")
     with pytest.raises(E.PermezError):
         P.decompress(bytes(a), device="cuda:0")
+
+
+def test_pipelined_decompressor_and_async_staged(codec, oracle):
+    """PipelinedDecompressor (several containers in flight, blocking and
+    non-blocking collect) returns the oracle's grids in submission order;
+    the async staged compress (the sharded bench path, here without
+    collectives) returns the one-shot container."""
+    import paper_2309_09778_b200 as P
+    cfg = P.CompressConfig(rel_error=1e-2, repair_factor=1.0)
+    fields = [_field("C2", (300, 520)) * s for s in (1.0, -2.0, 0.5, 3.0)]
+    conts = [codec.compress_device(torch.from_numpy(np.ascontiguousarray(f)).cuda(), cfg)[0].cpu().numpy().tobytes()
+             for f in fields]
+    pd = P.PipelinedDecompressor(codec, conts[0], depth=3)
+    out = []
+    for c in conts[:3]:
+        pd.submit(torch.from_numpy(np.frombuffer(c, np.uint8).copy()).pin_memory())
+    out.append(pd.collect().clone())
+    pd.submit(torch.from_numpy(np.frombuffer(conts[3], np.uint8).copy()).pin_memory())
+    for _ in range(3):
+        y = pd.collect(block=False)
+        pd.wait()
+        out.append(y.clone())
+    for y, c in zip(out, conts):
+        assert np.array_equal(y.numpy().view(np.uint32), oracle.decompress(c).view(np.uint32))
+    x = torch.from_numpy(np.ascontiguousarray(fields[1])).cuda()
+    ws = torch.empty(1 << 28, dtype=torch.uint8, device="cuda")
+    ob = torch.empty(1 << 24, dtype=torch.uint8, device="cuda")
+    val = torch.as_tensor(P.pipeline.validation_blocks(2 * 3, cfg.sample_rate, cfg.seed), dtype=torch.int64,
+                          device="cuda")
+    pg = codec.compress_staged_async(x, cfg, block_row0=0, global_rows=300, d_val=val, ws=ws, out=ob)
+    info = codec.staged_result(*pg, ws, ob)
+    assert ob[: info.nbytes].cpu().numpy().tobytes() == conts[1]
