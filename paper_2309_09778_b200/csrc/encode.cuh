@@ -543,7 +543,13 @@ __device__ __forceinline__ void copy_s2g_bytes(uint8_t *dst, const unsigned *src
 // assembled MSB-first into shared-memory words, copied out at the end.
 constexpr int kWT = 256;
 constexpr unsigned kPartWords = 4096;  // 16 KB payload staging (else direct byte writes)
-constexpr unsigned kBalStage = 1024;   // balance values per staging sub-round (8 KB)
+#ifndef PMZ_BAL_STAGE
+#define PMZ_BAL_STAGE 2048
+#endif
+constexpr unsigned kBalStage = PMZ_BAL_STAGE;   // balance values per staging sub-round
+#ifndef PMZ_BAL_ILP
+#define PMZ_BAL_ILP 4
+#endif
 constexpr int kWpTabM = 10;            // codebook tables in shared memory up to this m
 constexpr size_t kWpSmem = (size_t)(1u << kWpTabM) * 5;
 
@@ -646,15 +652,15 @@ __device__ __forceinline__ void wp_runs(const Geom &g, const BlkP &P, int64_t b,
       }
       __syncthreads();
       const unsigned nv = s1 - s0;
-      for (unsigned j0 = 0; j0 < nv; j0 += 4 * kWT) {
-        unsigned long long vv[4];
+      for (unsigned j0 = 0; j0 < nv; j0 += PMZ_BAL_ILP * kWT) {
+        unsigned long long vv[PMZ_BAL_ILP];
 #pragma unroll
-        for (int u = 0; u < 4; u++) {
+        for (int u = 0; u < PMZ_BAL_ILP; u++) {
           const unsigned j = j0 + u * kWT + tid;
           vv[u] = j < nv ? __double_as_longlong(__ldg(vp + s_bidx[j])) : 0ull;
         }
 #pragma unroll
-        for (int u = 0; u < 4; u++) {
+        for (int u = 0; u < PMZ_BAL_ILP; u++) {
           const unsigned j = j0 + u * kWT + tid;
           if (j < nv) sbal[j] = vv[u];
         }
