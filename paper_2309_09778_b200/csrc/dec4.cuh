@@ -76,6 +76,23 @@ __device__ __forceinline__ void d4_mark_run(unsigned *bm, const unsigned long lo
   }
 }
 
+// ras[d4_pad(idx + j)] = s for j < k: contiguous inside each 64-code row of
+// the padded raster; 4-byte stores of code pairs (the padding is even, so a
+// pair is aligned iff its raster index is)
+__device__ __forceinline__ void d4_fill(uint16_t *ras, unsigned idx, unsigned k, unsigned s) {
+  const unsigned pair = s | (s << 16);
+  const unsigned end = idx + k;
+  while (idx < end) {
+    const unsigned n = min(end, (idx | 63u) + 1u) - idx;  // inside this 64-code row
+    uint16_t *d = ras + d4_pad(idx);
+    unsigned j = 0;
+    if (idx & 1u) d[j++] = (uint16_t)s;
+    for (; j + 2 <= n; j += 2) *reinterpret_cast<unsigned *>(d + j) = pair;
+    if (j < n) d[j] = (uint16_t)s;
+    idx += n;
+  }
+}
+
 // Decoupled look-back flags: code-0 count + 1 once known, kD4Poison when the
 // partition failed (reset to 0 before every launch).
 constexpr unsigned kD4Poison = 0xffffffffu;
@@ -312,7 +329,8 @@ __global__ void __launch_bounds__(kD4Threads, 6) k_decode4(const uint8_t *__rest
         unsigned k = d4_len_run(rd.buf, rd.nb, L - y, s_len12, lut, s_tab, sym, l);
         if (k > 1) {  // a run stops at its first codeword that starts on a marked position
           unsigned long long per = 0;
-          for (unsigned j = 1; j < k; j++) per |= 1ull << (j * l);
+          const unsigned n = (k - 1) * l + 1;  // <= 64 (k l <= 64)
+          per = s_rep[l] & (n >= 64 ? ~0ull : ((1ull << n) - 1ull)) & ~1ull;
           const unsigned long long hm = win & per;
           if (hm) k = ((unsigned)__ffsll((long long)hm) - 1u) / l;
         }
@@ -496,7 +514,8 @@ __global__ void __launch_bounds__(kD4Threads, 6) k_decode4(const uint8_t *__rest
         rd.refill(bs);
         unsigned s, l, k;
         d4_run(rd.buf, rd.nb, cnt - i, s_len12, s_sym12, lut, s_tab, sym, s, l, k);
-        for (unsigned j = 0; j < k; j++) W.u.ras[d4_pad(idx + j)] = (uint16_t)s;
+        if (k == 1) W.u.ras[d4_pad(idx)] = (uint16_t)s;
+        else d4_fill(W.u.ras, idx, k, s);
         idx += k;
         rd.skip(k * l);
         i += k;
