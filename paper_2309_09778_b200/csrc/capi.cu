@@ -168,6 +168,13 @@ constexpr int kNT = 256;
 template <int PK>
 int launch_ws(const KParams &k, unsigned grid, cudaStream_t st, const float *x, const Geom &G, void *d_ws,
               const WsLayout &L) {
+  if (G.br == 1 || G.rows == 1) {  // one-row partitions: a thread per partition
+    k_compress_1d<PK><<<(unsigned)((G.nparts + 31) / 32), 32, 0, st>>>(
+        x, G, k, at<BlkP>(d_ws, L.blkp), at<WsStatus>(d_ws, L.status), at<double>(d_ws, L.vbuf),
+        at<int16_t>(d_ws, L.rqbuf), at<uint8_t>(d_ws, L.clsbuf), at<double>(d_ws, L.anchors),
+        at<unsigned long long>(d_ws, L.part_zeros), at<uint8_t>(d_ws, L.vflag), at<unsigned long long>(d_ws, L.hist));
+    return PMZ_OK;
+  }
   CK(cudaFuncSetAttribute(k_compress_ws<PK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWscSmem));
   k_compress_ws<PK><<<grid, kPPC * 64, kWscSmem, st>>>(x, G, k, at<BlkP>(d_ws, L.blkp), at<WsStatus>(d_ws, L.status),
                                                        at<double>(d_ws, L.vbuf), at<int16_t>(d_ws, L.rqbuf),

@@ -377,6 +377,100 @@ __global__ void __launch_bounds__(kPPC * 64) k_compress_ws(const float *__restri
   }
 }
 
+// verify_and_repair for one-row partitions (1-D inputs,
+// block_rows == 1): a thread per partition runs its row's recurrence
+// (W-only surface, row-0 semantics of the consumer above: same predict,
+// same check_cls filter + exact f32 test, same repair), so 32 partitions
+// advance per warp step instead of one active lane per warp pair.
+template <int PK>
+__global__ void __launch_bounds__(32) k_compress_1d(const float *__restrict__ x, Geom g, KParams k,
+                                                    const BlkP *__restrict__ blkp, WsStatus *st,
+                                                    const double *__restrict__ vbuf, int16_t *rqbuf,
+                                                    const uint8_t *__restrict__ clsbuf,
+                                                    double *__restrict__ anchors,
+                                                    unsigned long long *__restrict__ part_zeros,
+                                                    const uint8_t *__restrict__ vflag,
+                                                    unsigned long long *__restrict__ hist) {
+  count_launch(st);
+  const int64_t p = (int64_t)blockIdx.x * 32 + threadIdx.x;
+  if (p >= g.nparts) return;
+  int64_t b;
+  int pi;
+  part_of(g, p, b, pi);
+  const BlkP P = blkp[b];
+  if (P.trivial) {
+    part_zeros[p] = 0;
+    return;
+  }
+  const BlockBox bb = block_box(g, b);
+  const int pr0 = pi * g.prow, C = bb.bc;
+  const int center = 1 << (st->m - 1);
+  const bool val = vflag[b] != 0;
+  const bool tlt1 = k.repair_t < 1.0;
+  const double two_ba = k.two_ba, zthr = P.zero_threshold, bnd = P.boundary;
+  const float *xrow = x + (bb.r0 + pr0) * g.cols + bb.c0;
+  unsigned *amb = &st->unresolved;
+  const int64_t tb = tile_base(g, p, 0);
+  if (val && pi == 0) atomicAdd(&hist[kMaxAlpha], 1ull);  // k for the floor (D10)
+  double hl = 0.0;
+  unsigned zeros = 0, repairs = 0;
+  // inputs kPf elements ahead in registers: the loads (one L1 miss per
+  // sector) run under the recurrence's dependency chain
+  constexpr int kPf = 8;
+  auto at_c = [&](int c) -> int64_t { return tb + (int64_t)(c >> 5) * kTile + (c & 31); };  // row 0
+  double pv[kPf];
+  int prq[kPf], pcls[kPf];
+#pragma unroll
+  for (int u = 0; u < kPf; u++) {
+    const int64_t i = at_c(min(u, C - 1));
+    pv[u] = vbuf[i];
+    prq[u] = rqbuf[i];
+    pcls[u] = clsbuf[i];
+  }
+  for (int c0 = 0; c0 < C; c0 += kPf)
+#pragma unroll
+  for (int u = 0; u < kPf; u++) {
+    const int c = c0 + u;
+    if (c >= C) break;
+    const int64_t i = at_c(c);
+    const double v = pv[u];
+    const int rq = prq[u];
+    const int cls = pcls[u];
+    {
+      const int64_t j = at_c(min(c + kPf, C - 1));
+      pv[u] = vbuf[j];
+      prq[u] = rqbuf[j];
+      pcls[u] = clsbuf[j];
+    }
+    const bool anchor = c == 0;
+    const bool normal = abs(rq) < center && !anchor;
+    const double vhat = __dadd_rn(predict_steady<PK>(k, hl, 0.0, 0.0, true), __dmul_rn((double)rq, two_ba));
+    // check_cls (D8), as classify() in k_compress_ws
+    const double d = __dsub_rn(vhat, v);
+    const bool gz = vhat > zthr, gb = vhat > bnd;
+    const bool in12 = cls == 1 ? (gz && !gb) : gb;
+    const bool is12 = cls == 1 || cls == 2;
+    const bool acc = is12 ? (in12 && d < k.dpos_m && d > k.dneg_m) : (cls == 0 && !gz);
+    bool vio = is12 && ((tlt1 && !in12) || (in12 && (d > k.dpos_p || d < k.dneg_p)));
+    if (normal && !acc && !vio) vio = violates(inv_f32(vhat, P, amb), zfloor(__ldg(xrow + c)), k.repair_t);
+    const bool keep = normal && !vio;
+    int fin = rq;
+    if (normal && vio) {
+      fin = kRqOut;
+      rqbuf[i] = kRqOut;
+      repairs++;
+    }
+    zeros += (!keep && !anchor) ? 1u : 0u;
+    if (anchor) anchors[p] = v;  // forced anchor, D1
+    if (val && !anchor) atomicAdd(&hist[code_of_rq(fin, center)], 1ull);
+    hl = keep ? vhat : v;
+  }
+  part_zeros[p] = zeros;
+  atomicAdd(&st->nbal, (unsigned long long)zeros);
+  if (repairs) atomicAdd(&st->nrepair, (unsigned long long)repairs);
+  atomicAdd(&st->ncodes, (unsigned long long)(C - 1));
+}
+
 // compute_block_stats + make_transform_params (transform.py:84-167) for
 // every block, one CTA per 32-row partition: the partition's min positive
 // normal magnitude / max magnitude / non-finite flag go to per-block slots by
