@@ -23,6 +23,21 @@ namespace pmz {
 
 constexpr int kFqT = 256;  // threads per CTA (both kernels)
 
+// Quads of a partition: quad i covers row r, columns c0 .. c0 + 3 of chunk
+// kc; 8 R quads per 32-column chunk, so short partitions (one-row 1-D
+// inputs) keep every thread busy.  nq = the quads, rounded up to whole warps
+// (the warp collectives in k_quant need every lane).
+struct QuadMap {
+  int q8, nq, nqw;
+  __device__ QuadMap(int R, int nch) : q8(8 * R), nq(nch * 8 * R), nqw((nch * 8 * R + 31) & ~31) {}
+  __device__ void at(int i, int &kc, int &r, int &c0) const {
+    kc = i / q8;
+    const int rem = i - kc * q8;
+    r = rem >> 3;
+    c0 = kc * 32 + (rem & 7) * 4;
+  }
+};
+
 __global__ void __launch_bounds__(kFqT) k_fwd(const float *__restrict__ x, Geom g, const BlkP *__restrict__ blkp,
                                              WsStatus *st, double *__restrict__ vbuf, uint8_t *__restrict__ clsbuf) {
   count_launch(st);
@@ -41,9 +56,12 @@ __global__ void __launch_bounds__(kFqT) k_fwd(const float *__restrict__ x, Geom 
   unsigned *amb = &st->unresolved;
   // quad i: row (i >> 3) & 31, columns 32 (i >> 8) + 4 (i & 7) .. + 3; the
   // next quad's input is loaded before this quad's log2 chains
+  const QuadMap qm(R, nch);
   auto load_quad = [&](int i, float (&xr)[4]) -> bool {
-    const int kc = i >> 8, r = (i >> 3) & 31, c0 = kc * 32 + (i & 7) * 4;
-    if (i >= nch * 256 || r >= R || c0 >= C) return false;
+    if (i >= qm.nq) return false;
+    int kc, r, c0;
+    qm.at(i, kc, r, c0);
+    if (c0 >= C) return false;
     const float *src = xp + (int64_t)r * g.cols + c0;
     if (vec && c0 + 3 < C) {
       const float4 q = __ldg(reinterpret_cast<const float4 *>(src));
@@ -56,12 +74,13 @@ __global__ void __launch_bounds__(kFqT) k_fwd(const float *__restrict__ x, Geom 
   };
   float xn[4];
   bool hn = load_quad(threadIdx.x, xn);
-  for (int i = threadIdx.x; i < nch * 256; i += kFqT) {
+  for (int i = threadIdx.x; i < qm.nq; i += kFqT) {
     float xr[4] = {xn[0], xn[1], xn[2], xn[3]};
     const bool h = hn;
     hn = load_quad(i + kFqT, xn);
     if (!h) continue;
-    const int kc = i >> 8, r = (i >> 3) & 31, c0 = kc * 32 + (i & 7) * 4;
+    int kc, r, c0;
+    qm.at(i, kc, r, c0);
     double ax[4], lg[4], v[4];
     unsigned cl = 0;
 #pragma unroll
@@ -106,9 +125,11 @@ __global__ void __launch_bounds__(kFqT) k_quant(Geom g, KParams k, const BlkP *_
   const double *vt = vbuf + tile_base(g, p, 0);
   int16_t *rt = rqbuf + tile_base(g, p, 0);
   const int lane = threadIdx.x & 31;
-  for (int i = threadIdx.x; i < nch * 256; i += kFqT) {
-    const int kc = i >> 8, r = (i >> 3) & 31, c0 = kc * 32 + (i & 7) * 4;
-    const bool ok = r < R && c0 < C;
+  const QuadMap qm(R, nch);
+  for (int i = threadIdx.x; i < qm.nqw; i += kFqT) {
+    int kc, r, c0;
+    qm.at(min(i, qm.nq - 1), kc, r, c0);
+    const bool ok = i < qm.nq && c0 < C;
     int rq[4] = {0, 0, 0, 0};
     if (ok) {
       const int o = kc * kTile + r * 32 + (c0 & 31);
