@@ -31,7 +31,7 @@ struct QuadMap {
   int q8, nq, nqw;
   __device__ QuadMap(int R, int nch) : q8(8 * R), nq(nch * 8 * R), nqw((nch * 8 * R + 31) & ~31) {}
   __device__ void at(int i, int &kc, int &r, int &c0) const {
-    kc = i / q8;
+    kc = q8 == 256 ? i >> 8 : i / q8;  // full 32-row partitions: shifts
     const int rem = i - kc * q8;
     r = rem >> 3;
     c0 = kc * 32 + (rem & 7) * 4;
