@@ -111,6 +111,21 @@ typedef struct pmz_header {
   uint64_t lens_offset;   /* byte offset of the 2^m code lengths             */
 } pmz_header;
 
+/* A block whose per-block logarithm of a general double (lg_neg =
+ * np.log2(factor_neg), transform.py:120; np.log2(factor_pos - eps0), :123)
+ * lies so close to a rounding midpoint that numpy may round it differently
+ * from the correctly rounded value.  The library lists such blocks; the host
+ * fills lg[i] = np.log2(arg[i]) for every bit i of mask and hands the entries
+ * back, so per-block parameters equal the reference's bit for bit (DESIGN
+ * D22).  Callers that skip this step get the CR values. */
+typedef struct pmz_np_fix {
+  int64_t block;
+  double arg[2];   /* factor_neg, factor_pos - eps0 */
+  double lg[2];    /* filled by the host: np.log2(arg[i]) */
+  int32_t mask;    /* bit i: arg[i] needs the host */
+  int32_t pad;
+} pmz_np_fix;
+
 /* library / ABI identification */
 PMZ_API int pmz_abi_version(void);
 PMZ_API const char *pmz_status_string(int status);
@@ -123,6 +138,25 @@ PMZ_API int pmz_workspace_size(const pmz_params *p, const pmz_geom *g, uint64_t 
 PMZ_API int pmz_max_container_size(const pmz_params *p, const pmz_geom *g, uint64_t *bytes);
 
 /* --- compression --------------------------------------------------------- */
+
+/* Stage 1a: compute_block_stats + make_transform_params (transform.py:84-167)
+ * for every block of the shard (device, CR logarithms); zeroes the status,
+ * coverage and histogram.  Stage 1b (pmz_compress_transform): forward map and
+ * the select_m coverage of the validation blocks.  pmz_compress_analyze =
+ * 1a + 1b.  Between the two the host may resolve the listed general-double
+ * logarithms with numpy: pmz_compress_np_fixups synchronises `stream` and
+ * copies up to `cap` entries (returns the count, or a negative status);
+ * pmz_compress_np_apply uploads the host's values and re-derives the listed
+ * blocks' parameters (stream-ordered). */
+PMZ_API int pmz_compress_stats(const float *d_in, const pmz_geom *g, const pmz_params *p, void *d_ws,
+                               uint64_t ws_bytes, void *stream);
+PMZ_API int pmz_compress_transform(const float *d_in, const pmz_geom *g, const pmz_params *p,
+                                   const int64_t *d_val_blocks, int64_t n_val, void *d_ws, uint64_t ws_bytes,
+                                   void *stream);
+PMZ_API int64_t pmz_compress_np_fixups(const pmz_geom *g, const pmz_params *p, void *d_ws, uint64_t ws_bytes,
+                                       void *stream, pmz_np_fix *h_fix, int64_t cap);
+PMZ_API int pmz_compress_np_apply(const pmz_geom *g, const pmz_params *p, void *d_ws, uint64_t ws_bytes,
+                                  void *stream, const pmz_np_fix *h_fix, int64_t n);
 
 /* Stage 1: per-block stats + transform parameters for every block of the
  * shard, and the select_m coverage histogram over the validation blocks the
@@ -206,6 +240,19 @@ PMZ_API int pmz_decompress_enqueue(const uint8_t *d_buf, uint64_t n, const pmz_h
                                    const uint64_t *d_block_offsets, float *d_out, void *d_ws, uint64_t ws_bytes,
                                    void *stream);
 PMZ_API int pmz_decompress_result(const pmz_header *hdr, void *d_ws, uint64_t ws_bytes, void *stream);
+/* pmz_decompress_enqueue split at the numpy fixup point: _prepare parses the
+ * block records and derives the per-block parameters (+ decode tables);
+ * pmz_decompress_np_fixups / _np_apply as for compression; _run decodes and
+ * reconstructs.  pmz_decompress_enqueue = _prepare + _run. */
+PMZ_API int pmz_decompress_prepare(const uint8_t *d_buf, uint64_t n, const pmz_header *hdr, double b_a,
+                                   const uint64_t *d_block_offsets, void *d_ws, uint64_t ws_bytes, void *stream);
+PMZ_API int pmz_decompress_run(const uint8_t *d_buf, uint64_t n, const pmz_header *hdr, double b_a,
+                               const uint64_t *d_block_offsets, float *d_out, void *d_ws, uint64_t ws_bytes,
+                               void *stream);
+PMZ_API int64_t pmz_decompress_np_fixups(const pmz_header *hdr, void *d_ws, uint64_t ws_bytes, void *stream,
+                                         pmz_np_fix *h_fix, int64_t cap);
+PMZ_API int pmz_decompress_np_apply(const pmz_header *hdr, double b_a, void *d_ws, uint64_t ws_bytes, void *stream,
+                                    const pmz_np_fix *h_fix, int64_t n);
 
 /* --- trainer objective ------------ */
 

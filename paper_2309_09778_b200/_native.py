@@ -51,6 +51,12 @@ class Header(ctypes.Structure):
     ]
 
 
+class NpFix(ctypes.Structure):
+    """pmz_np_fix: a block whose general-double log2 numpy must decide (D22)."""
+    _fields_ = [("block", c_int64), ("arg", c_double * 2), ("lg", c_double * 2), ("mask", c_int32),
+                ("pad", c_int32)]
+
+
 _SIGS = {
     "pmz_abi_version": (c_int32, []),
     "pmz_status_string": (ctypes.c_char_p, [c_int32]),
@@ -86,10 +92,44 @@ _SIGS = {
     "pmz_forward_map": (c_int32, [VP, c_uint64, VP, VP, VP]),
     "pmz_inverse_map": (c_int32, [VP, c_uint64, VP, VP, VP, VP]),
     "pmz_log2_f32_batch": (c_int32, [VP, c_uint64, VP, VP, c_int32, VP]),
+    "pmz_compress_stats": (c_int32, [VP, ctypes.POINTER(Geom), ctypes.POINTER(Params), VP, c_uint64, VP]),
+    "pmz_compress_transform": (c_int32, [VP, ctypes.POINTER(Geom), ctypes.POINTER(Params), VP, c_int64, VP, c_uint64,
+                                         VP]),
+    "pmz_compress_np_fixups": (c_int64, [ctypes.POINTER(Geom), ctypes.POINTER(Params), VP, c_uint64, VP, VP, c_int64]),
+    "pmz_compress_np_apply": (c_int32, [ctypes.POINTER(Geom), ctypes.POINTER(Params), VP, c_uint64, VP, VP, c_int64]),
+    "pmz_decompress_prepare": (c_int32, [VP, c_uint64, ctypes.POINTER(Header), c_double, VP, VP, c_uint64, VP]),
+    "pmz_decompress_run": (c_int32, [VP, c_uint64, ctypes.POINTER(Header), c_double, VP, VP, VP, c_uint64, VP]),
+    "pmz_decompress_np_fixups": (c_int64, [ctypes.POINTER(Header), VP, c_uint64, VP, VP, c_int64]),
+    "pmz_decompress_np_apply": (c_int32, [ctypes.POINTER(Header), c_double, VP, c_uint64, VP, VP, c_int64]),
 }
 
 EXPORTS = tuple(_SIGS)
 _lib = None
+
+
+def resolve_np_log2(read, apply, cap: int = 4096) -> int:
+    """Host half of the numpy-exact per-block logarithms (DESIGN D22): ``read``
+    = pmz_*_np_fixups bound to a workspace (synchronises the stream),
+    ``apply`` = pmz_*_np_apply.  Fills lg[i] = np.log2(arg[i]) -- the
+    reference's own arithmetic (transform.py:120, :123) -- and hands the
+    entries back.  Returns the number of listed blocks."""
+    import numpy as np
+    buf = (NpFix * cap)()
+    n = int(read(buf, cap))
+    if n < 0:
+        return n
+    if n > cap:
+        buf = (NpFix * n)()
+        n = int(read(buf, n))
+        if n < 0:
+            return n
+    if n == 0:
+        return 0
+    a = np.frombuffer(buf, dtype=np.dtype([("block", "<i8"), ("arg", "<f8", 2), ("lg", "<f8", 2), ("mask", "<i4"),
+                                           ("pad", "<i4")]), count=n)
+    a["lg"] = np.log2(a["arg"])  # both args: the unflagged one is ignored by the device
+    s = int(apply(buf, n))
+    return s if s < 0 else n
 
 
 def load():

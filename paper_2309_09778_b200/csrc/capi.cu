@@ -126,6 +126,7 @@ WsLayout compress_layout(const Geom &g) {
   L.hist = take((kMaxAlpha + 1) * 8);
   L.vflag = take((size_t)g.nblocks + 1);  // zeroed with status / cov / hist
   L.bstat = take(16 * ((size_t)g.nblocks + 1));  // BlkStat per block, zeroed too
+  L.npfix = take(sizeof(pmz_np_fix) * ((size_t)g.nblocks + 1));
   L.lens = take(kMaxAlpha);
   L.cw = take(kMaxAlpha * 4);
   L.cb_keys = take(kMaxAlpha * 8);
@@ -252,8 +253,8 @@ uint64_t *pmz_ws_histogram(void *d_ws, const pmz_params *p, const pmz_geom *g) {
   return at<uint64_t>(d_ws, compress_layout(geom_of(p, g)).hist);
 }
 
-int pmz_compress_analyze(const float *d_in, const pmz_geom *g, const pmz_params *p, const int64_t *d_val,
-                         int64_t n_val, void *d_ws, uint64_t ws_bytes, void *stream) {
+int pmz_compress_stats(const float *d_in, const pmz_geom *g, const pmz_params *p, void *d_ws, uint64_t ws_bytes,
+                       void *stream) {
   int s = check_params(p);
   if (s) return s;
   Geom G = geom_of(p, g);
@@ -261,13 +262,26 @@ int pmz_compress_analyze(const float *d_in, const pmz_geom *g, const pmz_params 
   if (ws_bytes < L.total) return PMZ_ERR_WORKSPACE;
   cudaStream_t st = (cudaStream_t)stream;
   KParams k = kparams(p);
-  // zero status, coverage and histogram (contiguous at the front)
+  // zero status, coverage, histogram, flags and block stats (contiguous at the front)
   CK(cudaMemsetAsync(d_ws, 0, L.lens, st));
   if (G.nblocks == 0) return PMZ_OK;
   k_stats<<<(unsigned)G.nparts, 256, 0, st>>>(d_in, G, k, at<BlkP>(d_ws, L.blkp), at<BlkStat>(d_ws, L.bstat),
-                                               at<WsStatus>(d_ws, L.status));
+                                               at<WsStatus>(d_ws, L.status), at<pmz_np_fix>(d_ws, L.npfix));
+  return launch_check();
+}
+
+int pmz_compress_transform(const float *d_in, const pmz_geom *g, const pmz_params *p, const int64_t *d_val,
+                           int64_t n_val, void *d_ws, uint64_t ws_bytes, void *stream) {
+  int s = check_params(p);
+  if (s) return s;
+  Geom G = geom_of(p, g);
+  WsLayout L = compress_layout(G);
+  if (ws_bytes < L.total) return PMZ_ERR_WORKSPACE;
+  cudaStream_t st = (cudaStream_t)stream;
+  KParams k = kparams(p);
+  if (G.nblocks == 0) return PMZ_OK;
   if (n_val > 0)
-    k_mark_val<<<(unsigned)((n_val + 255) / 256), 256, 0, st>>>(d_val, n_val, at<uint8_t>(d_ws, L.vflag),
+    k_mark_val<<<(unsigned)((n_val + 255) / 256), 256, 0, st>>>(d_val, n_val, G.nblocks, at<uint8_t>(d_ws, L.vflag),
                                                                at<WsStatus>(d_ws, L.status));
   // forward map + m-independent TRUE-surface quantization of every element,
   // coverage of the validation blocks in the same pass
@@ -279,6 +293,60 @@ int pmz_compress_analyze(const float *d_in, const pmz_geom *g, const pmz_params 
     else launch_quant<0>(k, st, G, d_ws, L);
   }
   return launch_check();
+}
+
+int pmz_compress_analyze(const float *d_in, const pmz_geom *g, const pmz_params *p, const int64_t *d_val,
+                         int64_t n_val, void *d_ws, uint64_t ws_bytes, void *stream) {
+  int s = pmz_compress_stats(d_in, g, p, d_ws, ws_bytes, stream);
+  if (s) return s;
+  return pmz_compress_transform(d_in, g, p, d_val, n_val, d_ws, ws_bytes, stream);
+}
+
+namespace {
+int64_t read_np_fixups(WsStatus *d_status, const pmz_np_fix *d_fix, cudaStream_t st, pmz_np_fix *h, int64_t cap) {
+  unsigned long long n = 0;
+  if (cudaMemcpyAsync(&n, &d_status->nfix, sizeof(n), cudaMemcpyDeviceToHost, st) != cudaSuccess) return PMZ_ERR_CUDA;
+  if (cudaStreamSynchronize(st) != cudaSuccess) return PMZ_ERR_CUDA;
+  const int64_t k = (int64_t)n < cap ? (int64_t)n : cap;
+  if (k > 0 && h) {
+    if (cudaMemcpyAsync(h, d_fix, sizeof(pmz_np_fix) * (size_t)k, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+      return PMZ_ERR_CUDA;
+    if (cudaStreamSynchronize(st) != cudaSuccess) return PMZ_ERR_CUDA;
+  }
+  return (int64_t)n;
+}
+int apply_np_fixups(pmz_np_fix *d_fix, BlkP *d_blkp, WsStatus *d_status, int64_t nmax, double eps0, double b_a,
+                    cudaStream_t st, const pmz_np_fix *h, int64_t n) {
+  if (n <= 0) return PMZ_OK;
+  if (n > nmax) return PMZ_ERR_CONFIG;
+  for (int64_t i = 0; i < n; i++)
+    if (h[i].block < 0 || h[i].block >= nmax) return PMZ_ERR_CONFIG;
+  CK(cudaMemcpyAsync(d_fix, h, sizeof(pmz_np_fix) * (size_t)n, cudaMemcpyHostToDevice, st));
+  k_np_apply<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(d_fix, n, eps0, b_a, d_blkp, d_status);
+  CK(cudaStreamSynchronize(st));  // h may be released by the caller
+  return launch_check();
+}
+}  // namespace
+
+int64_t pmz_compress_np_fixups(const pmz_geom *g, const pmz_params *p, void *d_ws, uint64_t ws_bytes, void *stream,
+                               pmz_np_fix *h_fix, int64_t cap) {
+  int s = check_params(p);
+  if (s) return s;
+  WsLayout L = compress_layout(geom_of(p, g));
+  if (ws_bytes < L.total) return PMZ_ERR_WORKSPACE;
+  return read_np_fixups(at<WsStatus>(d_ws, L.status), at<pmz_np_fix>(d_ws, L.npfix), (cudaStream_t)stream, h_fix,
+                        cap);
+}
+
+int pmz_compress_np_apply(const pmz_geom *g, const pmz_params *p, void *d_ws, uint64_t ws_bytes, void *stream,
+                          const pmz_np_fix *h_fix, int64_t n) {
+  int s = check_params(p);
+  if (s) return s;
+  Geom G = geom_of(p, g);
+  WsLayout L = compress_layout(G);
+  if (ws_bytes < L.total) return PMZ_ERR_WORKSPACE;
+  return apply_np_fixups(at<pmz_np_fix>(d_ws, L.npfix), at<BlkP>(d_ws, L.blkp), at<WsStatus>(d_ws, L.status),
+                         G.nblocks, p->eps0, p->b_a, (cudaStream_t)stream, h_fix, n);
 }
 
 int pmz_compress_codes(const float *d_in, const pmz_geom *g, const pmz_params *p, const int64_t *d_val,
@@ -543,7 +611,7 @@ namespace {
 // every block is one partition of one row (1-D inputs, block_rows == 1)
 bool one_row_parts(const Geom &G) { return G.br == 1 || G.rows == 1; }
 struct DecLayout {
-  size_t status, blkp, part_bits, part_off, zflag, anchors, bal_off, pay_off, blk_nbal, tab, sym, lut, codes,
+  size_t status, blkp, part_bits, part_off, zflag, anchors, bal_off, pay_off, blk_nbal, tab, sym, lut, npfix, codes,
       vtile, total;
 };
 DecLayout dec_layout(const Geom &g) {
@@ -566,6 +634,7 @@ DecLayout dec_layout(const Geom &g) {
   L.tab = take(sizeof(DecTab));
   L.sym = take(2 * kMaxAlpha);
   L.lut = take(4ull * ((1u << kLutBits) + kLut2Max));            // first + second level
+  L.npfix = take(sizeof(pmz_np_fix) * (size_t)(g.nblocks + 1));
   L.codes = take(2 * (size_t)g.nparts * (size_t)g.nct * kTile);  // partition-tiled
   L.vtile = take(8 * (size_t)g.nparts * (size_t)g.nct * kTile);   // per-element addends, then reconstructed values
   L.total = o;
@@ -621,8 +690,8 @@ int pmz_decompress_workspace_size(const pmz_header *hdr, uint64_t *bytes) {
   return PMZ_OK;
 }
 
-int pmz_decompress_enqueue(const uint8_t *d_buf, uint64_t n, const pmz_header *hdr, double b_a,
-                           const uint64_t *d_boff, float *d_out, void *d_ws, uint64_t ws_bytes, void *stream) {
+int pmz_decompress_prepare(const uint8_t *d_buf, uint64_t n, const pmz_header *hdr, double b_a,
+                           const uint64_t *d_boff, void *d_ws, uint64_t ws_bytes, void *stream) {
   Geom G = hdr_geom(hdr);
   DecLayout L = dec_layout(G);
   if (ws_bytes < L.total) return PMZ_ERR_WORKSPACE;
@@ -636,9 +705,41 @@ int pmz_decompress_enqueue(const uint8_t *d_buf, uint64_t n, const pmz_header *h
         d_buf, n, G, k, (const unsigned long long *)d_boff, at<BlkP>(d_ws, L.blkp),
         at<unsigned long long>(d_ws, L.part_bits), at<unsigned long long>(d_ws, L.part_off),
         at<double>(d_ws, L.anchors), at<unsigned long long>(d_ws, L.bal_off),
-        at<unsigned long long>(d_ws, L.pay_off), at<unsigned long long>(d_ws, L.blk_nbal), S);
+        at<unsigned long long>(d_ws, L.pay_off), at<unsigned long long>(d_ws, L.blk_nbal), S,
+        at<pmz_np_fix>(d_ws, L.npfix));
     k_dec_tables<<<1, 1024, 0, st>>>(d_buf + hdr->lens_offset, (int)hdr->m, at<DecTab>(d_ws, L.tab),
                                      at<uint16_t>(d_ws, L.sym), at<unsigned>(d_ws, L.lut), S);
+  }
+  return launch_check();
+}
+
+int64_t pmz_decompress_np_fixups(const pmz_header *hdr, void *d_ws, uint64_t ws_bytes, void *stream, pmz_np_fix *h_fix,
+                                 int64_t cap) {
+  DecLayout L = dec_layout(hdr_geom(hdr));
+  if (ws_bytes < L.total) return PMZ_ERR_WORKSPACE;
+  return read_np_fixups(at<WsStatus>(d_ws, L.status), at<pmz_np_fix>(d_ws, L.npfix), (cudaStream_t)stream, h_fix,
+                        cap);
+}
+
+int pmz_decompress_np_apply(const pmz_header *hdr, double b_a, void *d_ws, uint64_t ws_bytes, void *stream,
+                            const pmz_np_fix *h_fix, int64_t n) {
+  Geom G = hdr_geom(hdr);
+  DecLayout L = dec_layout(G);
+  if (ws_bytes < L.total) return PMZ_ERR_WORKSPACE;
+  return apply_np_fixups(at<pmz_np_fix>(d_ws, L.npfix), at<BlkP>(d_ws, L.blkp), at<WsStatus>(d_ws, L.status),
+                         G.nblocks, 0x1p-126, b_a, (cudaStream_t)stream, h_fix, n);
+}
+
+int pmz_decompress_run(const uint8_t *d_buf, uint64_t n, const pmz_header *hdr, double b_a, const uint64_t *d_boff,
+                       float *d_out, void *d_ws, uint64_t ws_bytes, void *stream) {
+  Geom G = hdr_geom(hdr);
+  DecLayout L = dec_layout(G);
+  if (ws_bytes < L.total) return PMZ_ERR_WORKSPACE;
+  if (!(b_a > 0.0)) return PMZ_ERR_CONFIG;
+  cudaStream_t st = (cudaStream_t)stream;
+  KParams k = hdr_kparams(hdr, b_a);
+  WsStatus *S = at<WsStatus>(d_ws, L.status);
+  if (G.nblocks > 0) {
     if (one_row_parts(G)) {
       k_decode_1d<<<(unsigned)((G.nparts + kD1T - 1) / kD1T), kD1T, 0, st>>>(
           d_buf, n, G, at<BlkP>(d_ws, L.blkp), at<DecTab>(d_ws, L.tab), at<uint16_t>(d_ws, L.sym),
@@ -668,6 +769,13 @@ int pmz_decompress_enqueue(const uint8_t *d_buf, uint64_t n, const pmz_header *h
     if (s2) return s2;
   }
   return launch_check();
+}
+
+int pmz_decompress_enqueue(const uint8_t *d_buf, uint64_t n, const pmz_header *hdr, double b_a,
+                           const uint64_t *d_boff, float *d_out, void *d_ws, uint64_t ws_bytes, void *stream) {
+  const int s = pmz_decompress_prepare(d_buf, n, hdr, b_a, d_boff, d_ws, ws_bytes, stream);
+  if (s) return s;
+  return pmz_decompress_run(d_buf, n, hdr, b_a, d_boff, d_out, d_ws, ws_bytes, stream);
 }
 
 int pmz_decompress_result(const pmz_header *hdr, void *d_ws, uint64_t ws_bytes, void *stream) {
@@ -816,10 +924,12 @@ int pmz_train_gradient(const float *d_in, const pmz_geom *g, const pmz_params *p
   CK(cudaMemsetAsync(d_ws, 0, L.lens, st));  // status, flags, block stats
   CK(cudaMemsetAsync(d_out12, 0, sizeof(double) * kTrC, st));
   if (G.nblocks == 0 || n_blocks <= 0) return launch_check();
+  // (the training objective keeps the device's CR per-block logarithms: no host fixup)
   k_stats<<<(unsigned)G.nparts, 256, 0, st>>>(d_in, G, k, at<BlkP>(d_ws, L.blkp), at<BlkStat>(d_ws, L.bstat),
-                                               at<WsStatus>(d_ws, L.status));
+                                               at<WsStatus>(d_ws, L.status), nullptr);
   // the training blocks are flagged in the validation-flag slots (no quantization runs here)
-  k_mark_val<<<(unsigned)((n_blocks + 255) / 256), 256, 0, st>>>(d_blocks, n_blocks, at<uint8_t>(d_ws, L.vflag),
+  k_mark_val<<<(unsigned)((n_blocks + 255) / 256), 256, 0, st>>>(d_blocks, n_blocks, G.nblocks,
+                                                                   at<uint8_t>(d_ws, L.vflag),
                                                                    at<WsStatus>(d_ws, L.status));
   k_fwd<<<(unsigned)G.nparts, kFqT, 0, st>>>(d_in, G, at<BlkP>(d_ws, L.blkp), at<WsStatus>(d_ws, L.status),
                                              at<double>(d_ws, L.vbuf), at<uint8_t>(d_ws, L.clsbuf));

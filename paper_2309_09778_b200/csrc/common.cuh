@@ -264,14 +264,49 @@ struct WsStatus {
   int err_site, err_part;  // first error's raising site / partition (diagnostics, PMZ_DEBUG)
   unsigned long long nbal, nrepair, ntrivial, ncodes;
   unsigned long long total_bytes, header_bytes, record_bytes;
-  unsigned long long pad2;
+  unsigned long long nfix;  // blocks whose general-double log2 numpy must decide (pmz_*_np_fixups)
 };
 
 struct WsLayout {
   size_t status, cov, hist, lens, cw, cb_keys, cb_w, cb_parent, blkp, part_bits, part_zeros, anchors, rec_size,
-      rec_off, cub_tmp, codes, balv, zrow, vflag, bstat, vbuf, rqbuf, clsbuf, total;
+      rec_off, cub_tmp, codes, balv, zrow, vflag, bstat, npfix, vbuf, rqbuf, clsbuf, total;
   size_t cub_bytes;
 };
+
+// ---------------------------------------------------------------------------
+// numpy-exact per-block logarithms of general doubles (DESIGN D22).
+//
+// lg_neg = np.log2(factor_neg) (transform.py:120) and np.log2(factor_pos -
+// eps0) (:123) take doubles that are in general not float32 values, so the
+// exhaustive float32 table does not cover them.  The device computes the CR
+// double; when the exact log2 lies within 2^-56 of a rounding midpoint (numpy
+// is never more than 2^-62.6 beyond one on the exhaustive float32 scan), the
+// block goes on a list that the host resolves with np.log2 itself
+// (pmz_compress_np_fixups / pmz_compress_np_apply, pipeline.py), after which
+// the block's parameters are re-derived on the device.
+static_assert(sizeof(pmz_np_fix) == 48, "pmz_np_fix layout");
+
+__device__ __forceinline__ bool np_log2_undecided(double x) {
+  const float f = __double2float_rn(x);
+  if ((double)f == x && f >= 1.17549435e-38f && f <= 3.40282347e38f) return false;  // exact via the table
+  return !dd_round_certain(log2_dd_general(x), 0x1p-56);
+}
+
+// append block b to the fixup list when one of its two general logarithms is undecided
+__device__ __forceinline__ void np_fix_note(WsStatus *st, pmz_np_fix *fix, int64_t b, double fn, double fpe) {
+  const int mask = (np_log2_undecided(fn) ? 1 : 0) | (np_log2_undecided(fpe) ? 2 : 0);
+  if (mask) {
+    const unsigned long long i = atomicAdd(&st->nfix, 1ull);
+    pmz_np_fix e;
+    e.block = b;
+    e.arg[0] = fn;
+    e.arg[1] = fpe;
+    e.lg[0] = e.lg[1] = 0.0;
+    e.mask = mask;
+    e.pad = 0;
+    fix[i] = e;
+  }
+}
 
 // count one executed kernel (first thread of the grid)
 __device__ __forceinline__ void count_launch(WsStatus *st) {

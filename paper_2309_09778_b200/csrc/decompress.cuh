@@ -45,7 +45,7 @@ __global__ void k_dec_blocks(const uint8_t *__restrict__ buf, unsigned long long
                              const unsigned long long *__restrict__ boff, BlkP *blkp,
                              unsigned long long *part_bits, unsigned long long *part_off, double *anchors,
                              unsigned long long *bal_off, unsigned long long *pay_off,
-                             unsigned long long *blk_nbal, WsStatus *st) {
+                             unsigned long long *blk_nbal, WsStatus *st, pmz_np_fix *npfix) {
   const int lane = threadIdx.x & 31;
   const int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (b >= g.nblocks) return;
@@ -83,7 +83,10 @@ __global__ void k_dec_blocks(const uint8_t *__restrict__ buf, unsigned long long
   P.zero_threshold = __dadd_rn(P.zero_code, k.b_a);   // :122
   P.boundary = __dsub_rn(__dadd_rn(lg_neg, lg_pe), k.b_a);  // :123
   P.trivial = 0;
-  if (lane == 0) blkp[b] = P;
+  if (lane == 0) {
+    blkp[b] = P;
+    if (npfix) np_fix_note(st, npfix, b, fn, __dsub_rn(fp, k.eps0));
+  }
   unsigned long long pb = 0;  // payload bytes of the partitions before this chunk of 32
   bool bad = false;
   for (int i0 = 0; i0 < bb.np; i0 += 32) {

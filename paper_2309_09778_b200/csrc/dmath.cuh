@@ -1,23 +1,68 @@
-// dmath.cuh -- correctly rounded log2 / exp2 on sm_100a FP64 pipes.
+// dmath.cuh -- numpy-exact log2 / CR exp2 on sm_100a FP64 pipes.
 //
 // The reference evaluates the transform with numpy in float64
-// (transform.py:95-98, 118-123, 177-182, 195-199).  This repo pins np.log2 /
-// np.exp2 to their correctly rounded (CR) values (decision D22);
-// the CPU oracle does the same with long double / __float128 arithmetic, so
-// GPU and oracle agree bit for bit.
+// (transform.py:95-98, 118-123, 177-182, 195-199).  log2 of a float32-valued
+// argument returns exactly np.log2's double: a correctly rounded (CR) log2
+// plus the exhaustive exception table of tools/log2_exceptions.py (DESIGN.md,
+// decision D22).  log2 of other doubles and exp2 are CR (the f32 outputs of
+// the inverse map equal numpy's).  The CPU oracle does the same with long
+// double / __float128 arithmetic and the same table.
 //
-//  * pmz_log2_f32(x):   CR log2 of a positive normal float (as double).
+//  * pmz_log2_f32(x):   np.log2 of a positive normal float (as double): CR + table.
 //    Table + double-double Horner (~2^-88 abs error), ambiguity test against a
 //    2^-80 relative bound, exact-path fallback with an all-double-double series.
-//  * pmz_log2_d(x):     CR log2 of any positive normal double (slow path;
+//  * pmz_log2_d(x):     CR log2 of any positive normal double, np.log2 when x
+//                       is float32-valued (slow path;
 //    per-block scalars only: lg_pos/lg_neg/log2(factor_pos - eps0)).
 //  * pmz_inv_f32(y):    (float)CR64(2^y)  -- the f32 cast of the CR double
 //    exp2, exactly what inverse_map(..).astype(float32) produces.
 #pragma once
 #include <cstdint>
 #include "dmath_tables.cuh"
+#include "np_log2_exc.inc"
 
 namespace pmz {
+
+// numpy's log2 (the reference's arithmetic, transform.py:119-123, :178-180) on
+// top of the CR result: tools/log2_exceptions.py compared np.log2 (numpy
+// 2.3.5, AVX512_SPR dispatch) with the CR double for EVERY positive normal
+// float32 and lists the 14 395 inputs where they differ (word = f32 pattern |
+// 1 << 31 when numpy is one ulp above CR).  For float32-valued arguments the
+// functions below therefore return exactly np.log2's bits.
+__device__ const uint32_t pmz_np_log2_exc[PMZ_NP_LOG2_EXC_N] = {PMZ_NP_LOG2_EXC_INIT};
+// per result binade b (index b - PMZ_NP_LOG2_BAND_MIN): the largest distance
+// of an exception's exact log2 from the rounding midpoint (binades b-1..b+1);
+// the fast path treats results that close to a midpoint as undecided, so every
+// exception reaches np_log2_adjust.
+__device__ const double pmz_np_log2_band[PMZ_NP_LOG2_BAND_N] = {PMZ_NP_LOG2_BAND_INIT};
+
+__device__ __forceinline__ double np_log2_band(double r) {
+  const int i = (int)((__double_as_longlong(r) >> 52) & 0x7ff) - 1023 - PMZ_NP_LOG2_BAND_MIN;
+  return (unsigned)i < (unsigned)PMZ_NP_LOG2_BAND_N ? __ldg(&pmz_np_log2_band[i]) : 0.0;
+}
+
+// cr = CR log2(x); returns np.log2(x) when x is a positive normal float32 value.
+__device__ __noinline__ double np_log2_adjust(double x, double cr) {
+  const float f = __double2float_rn(x);
+  if ((double)f != x || !(f >= 1.17549435e-38f) || !(f <= 3.40282347e38f)) return cr;
+  const uint32_t pat = __float_as_uint(f);
+  int lo = 0, hi = PMZ_NP_LOG2_EXC_N;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if ((__ldg(&pmz_np_log2_exc[mid]) & 0x7fffffffu) < pat) lo = mid + 1;
+    else hi = mid;
+  }
+  if (lo < PMZ_NP_LOG2_EXC_N) {
+    const uint32_t w = __ldg(&pmz_np_log2_exc[lo]);
+    if ((w & 0x7fffffffu) == pat) {
+      // one ulp towards +inf (w >> 31) or -inf; cr != 0 (log2 1 = 0 is exact)
+      const long long b = __double_as_longlong(cr);
+      const bool up = (w >> 31) != 0;
+      return __longlong_as_double((cr > 0.0) == up ? b + 1 : b - 1);
+    }
+  }
+  return cr;
+}
 
 struct dd { double hi, lo; };
 
@@ -101,18 +146,22 @@ __device__ __noinline__ dd log2_dd_general(double x) {
 
 // CR log2 of any positive normal double.  *amb set when the 2^-96 relative
 // bound could not decide the rounding (never observed; counted by callers).
-__device__ __noinline__ double pmz_log2_d(double x, unsigned *amb) {
+__device__ __noinline__ double pmz_log2_cr_d(double x, unsigned *amb) {
   dd r = log2_dd_general(x);
   if (!dd_round_certain(r, fabs(r.hi) * 0x1p-96)) {
     if (amb) atomicAdd(amb, 1u);
   }
   return r.hi;
 }
+// np.log2 for float32-valued x (exception table), CR for any other double.
+__device__ __forceinline__ double pmz_log2_d(double x, unsigned *amb) {
+  return np_log2_adjust(x, pmz_log2_cr_d(x, amb));
+}
 
 // CR log2 of a positive normal float value (passed as double, 24-bit mantissa).
 // Fast path: r = m*c - 1 is exact (24-bit m times a 29-bit c), series terms
 // 1..4 in double-double and 5..12 in double.
-__device__ __noinline__ double pmz_log2_f32(double x, unsigned *amb) {
+__device__ __noinline__ double pmz_log2_f32_cr(double x, unsigned *amb) {
   double m; int e;
   int i = log2_split(x, m, e);
   double c = __ldg(&pmz_log2_tab_c[i]);
@@ -136,7 +185,11 @@ __device__ __noinline__ double pmz_log2_f32(double x, unsigned *amb) {
   dd T = dd_add(dd{__ldg(&pmz_log2_tab_hi[i]), __ldg(&pmz_log2_tab_lo[i])}, S);
   dd R = (e == 0) ? T : dd_add(dd{(double)e, 0.0}, T);
   if (__builtin_expect(dd_round_certain(R, fabs(R.hi) * 0x1p-80), 1)) return R.hi;
-  return pmz_log2_d(x, amb);
+  return pmz_log2_cr_d(x, amb);
+}
+// np.log2 of a positive normal float value (as double): CR + exception table.
+__device__ __noinline__ double pmz_log2_f32(double x, unsigned *amb) {
+  return np_log2_adjust(x, pmz_log2_f32_cr(x, amb));
 }
 
 // Fast CR log2 of a positive normal float value (as double).  One table
@@ -171,7 +224,8 @@ __device__ __forceinline__ double pmz_log2_f32_fast(double x, unsigned *amb) {
   else C.lo = 0.0;
   const double lo = __dadd_rn(__dadd_rn(A.lo, C.lo), __dadd_rn(T1.x, slo));
   const dd R = fast_two_sum(C.hi, lo);
-  if (__builtin_expect(dd_round_certain(R, __fma_rn(fabs(R.hi), 0x1p-64, 0x1p-72)), 1)) return R.hi;
+  const double B = fmax(__fma_rn(fabs(R.hi), 0x1p-64, 0x1p-72), __fma_rn(np_log2_band(R.hi), 2.0, 0x1p-74));
+  if (__builtin_expect(dd_round_certain(R, B), 1)) return R.hi;
   return pmz_log2_f32(x, amb);
 }
 
@@ -224,7 +278,8 @@ __device__ __forceinline__ void pmz_log2_f32_fast_n(const double (&x)[N], double
     const double lo = __dadd_rn(__dadd_rn(A.lo, C.lo), __dadd_rn(Tl[u], slo));
     const dd R = fast_two_sum(C.hi, lo);
     out[u] = R.hi;
-    if (!dd_round_certain(R, __fma_rn(fabs(R.hi), 0x1p-64, 0x1p-72))) {
+    const double B = fmax(__fma_rn(fabs(R.hi), 0x1p-64, 0x1p-72), __fma_rn(np_log2_band(R.hi), 2.0, 0x1p-74));
+    if (!dd_round_certain(R, B)) {
       ok = false;
       out[u] = -INFINITY;  // marker: recompute on the precise path
     }

@@ -175,11 +175,16 @@ __global__ void __launch_bounds__(kFqT) k_quant(Geom g, KParams k, const BlkP *_
   }
 }
 
-// validation flags: vflag[val_ids[i]] = 1
-__global__ void k_mark_val(const int64_t *__restrict__ ids, int64_t n, uint8_t *vflag, WsStatus *st) {
+// validation flags: vflag[val_ids[i]] = 1; an id outside [0, nblocks) is a
+// caller error (ConfigError), never a write
+__global__ void k_mark_val(const int64_t *__restrict__ ids, int64_t n, int64_t nblocks, uint8_t *vflag,
+                           WsStatus *st) {
   count_launch(st);
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) vflag[ids[i]] = 1;
+  if (i >= n) return;
+  const int64_t b = ids[i];
+  if (b >= 0 && b < nblocks) vflag[b] = 1;
+  else set_err(st, PMZ_ERR_CONFIG);
 }
 
 }  // namespace pmz

@@ -485,7 +485,8 @@ struct BlkStat {
 };
 
 __global__ void __launch_bounds__(256) k_stats(const float *__restrict__ x, Geom g, KParams k,
-                                               BlkP *__restrict__ blkp, BlkStat *bst, WsStatus *st) {
+                                               BlkP *__restrict__ blkp, BlkStat *bst, WsStatus *st,
+                                               pmz_np_fix *npfix) {
   __shared__ bool s_last;
   __shared__ double s_l[3], s_fn;
   count_launch(st);
@@ -590,7 +591,22 @@ __global__ void __launch_bounds__(256) k_stats(const float *__restrict__ x, Geom
     P.zero_threshold = __dadd_rn(P.zero_code, k.b_a);
     P.boundary = __dsub_rn(__dadd_rn(P.lg_neg, s_l[2]), k.b_a);
     blkp[b] = P;
+    if (npfix) np_fix_note(st, npfix, b, fn, __dsub_rn(fp, k.eps0));
   }
+}
+
+// the host's np.log2 values for the listed blocks -> re-derived parameters
+__global__ void k_np_apply(const pmz_np_fix *__restrict__ fix, long long n, double eps0, double b_a, BlkP *blkp,
+                           WsStatus *st) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const pmz_np_fix e = fix[i];
+  BlkP P = blkp[e.block];
+  if (P.trivial) return;
+  if (e.mask & 1) P.lg_neg = e.lg[0];
+  const double lpe = (e.mask & 2) ? e.lg[1] : pmz_log2_d(__dsub_rn(P.factor_pos, eps0), &st->unresolved);
+  P.boundary = __dsub_rn(__dadd_rn(P.lg_neg, lpe), b_a);  // transform.py:123
+  blkp[e.block] = P;
 }
 
 }  // namespace pmz

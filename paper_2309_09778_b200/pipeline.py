@@ -134,6 +134,35 @@ class Codec:
             setattr(self, name, cur)
         return cur
 
+    # ---- numpy-exact per-block logarithms (DESIGN D22) ---------------------
+    def np_fix_compress(self, p, g, ws: torch.Tensor, stream) -> int:
+        """Resolve the blocks whose general-double log2 (np.log2(factor_neg),
+        transform.py:120) the device left to numpy.  Synchronises ``stream``."""
+        lib = self.lib
+        return N.resolve_np_log2(
+            lambda b, cap: lib.pmz_compress_np_fixups(ctypes.byref(g), ctypes.byref(p), _ptr(ws), ws.numel(), stream,
+                                                      b, cap),
+            lambda b, n: check(lib.pmz_compress_np_apply(ctypes.byref(g), ctypes.byref(p), _ptr(ws), ws.numel(),
+                                                         stream, b, n), "np_apply"))
+
+    def np_fix_decompress(self, h, ws: torch.Tensor, stream) -> int:
+        lib = self.lib
+        return N.resolve_np_log2(
+            lambda b, cap: lib.pmz_decompress_np_fixups(ctypes.byref(h), _ptr(ws), ws.numel(), stream, b, cap),
+            lambda b, n: check(lib.pmz_decompress_np_apply(ctypes.byref(h), host_b_a(h.b_r), _ptr(ws), ws.numel(),
+                                                           stream, b, n), "np_apply"))
+
+    def analyze(self, x, p, g, d_val, ws, stream):
+        """Stage 1: block stats + parameters, the host's np.log2 for the
+        listed blocks, then forward map + coverage (pmz_compress_stats /
+        _np_fixups / _np_apply / pmz_compress_transform)."""
+        lib = self.lib
+        check(lib.pmz_compress_stats(_ptr(x), ctypes.byref(g), ctypes.byref(p), _ptr(ws), ws.numel(), stream),
+              "compress_stats")
+        check(self.np_fix_compress(p, g, ws, stream), "np_fixups")
+        check(lib.pmz_compress_transform(_ptr(x), ctypes.byref(g), ctypes.byref(p), _ptr(d_val), int(d_val.numel()),
+                                         _ptr(ws), ws.numel(), stream), "compress_transform")
+
     # ---- compression --------------------------------------------------
     def plan(self, shape, cfg: CompressConfig):
         (rows, cols), S = grid_view_shape(tuple(shape))
@@ -165,15 +194,17 @@ class Codec:
             out_capacity = int(x.numel() * 4 * 1.25) + 65536 + 64 * max(nb, 1) * 12
         out = self._buf("_out", out_capacity)
         res = N.Result()
-        s = lib.pmz_compress(_ptr(x), ctypes.byref(g), ctypes.byref(p), _ptr(d_val), int(d_val.numel()), _ptr(out),
-                             out.numel(), _ptr(block_offsets), _ptr(ws), ws.numel(), _stream_ptr(self.device),
-                             ctypes.byref(res))
-        if s == -16:  # capacity: retry with the exact size
+        stream = _stream_ptr(self.device)
+        self.analyze(x, p, g, d_val, ws, stream)
+        check(lib.pmz_compress_codes(_ptr(x), ctypes.byref(g), ctypes.byref(p), _ptr(d_val), int(d_val.numel()),
+                                     _ptr(ws), ws.numel(), stream), "compress_codes")
+        s = lib.pmz_compress_finish(ctypes.byref(g), ctypes.byref(p), 1, _ptr(out), out.numel(), _ptr(block_offsets),
+                                    _ptr(ws), ws.numel(), stream, ctypes.byref(res))
+        if s == -16:  # capacity: write again into a buffer of the exact size
             need = int(res.header_bytes + res.record_bytes)
             out = self._buf("_out", need)
-            s = lib.pmz_compress(_ptr(x), ctypes.byref(g), ctypes.byref(p), _ptr(d_val), int(d_val.numel()),
-                                 _ptr(out), out.numel(), _ptr(block_offsets), _ptr(ws), ws.numel(),
-                                 _stream_ptr(self.device), ctypes.byref(res))
+            s = lib.pmz_compress_finish(ctypes.byref(g), ctypes.byref(p), 1, _ptr(out), out.numel(),
+                                        _ptr(block_offsets), _ptr(ws), ws.numel(), stream, ctypes.byref(res))
         check(s, "compress")
         n = int(res.header_bytes + res.record_bytes)
         info = CompressInfo(n, int(res.header_bytes), int(res.nblocks), int(res.ntrivial), int(res.nbal),
@@ -222,8 +253,7 @@ class Codec:
         nv = int(d_val.numel())
         if events is not None:
             events[0].record()
-        check(lib.pmz_compress_analyze(_ptr(x), ctypes.byref(g), ctypes.byref(p), _ptr(d_val), nv, _ptr(ws),
-                                       ws.numel(), stream), "compress_analyze")
+        self.analyze(x, p, g, d_val, ws, stream)
         if allreduce is not None:
             off = lib.pmz_ws_coverage(_ptr(ws), ctypes.byref(p), ctypes.byref(g)) - ws.data_ptr()
             allreduce(ws[off: off + 18 * 8].view(torch.int64))
@@ -262,8 +292,7 @@ class Codec:
         lib = self.lib
         stream = _stream_ptr(self.device)
         nv = int(d_val.numel())
-        check(lib.pmz_compress_analyze(_ptr(x), ctypes.byref(g), ctypes.byref(p), _ptr(d_val), nv, _ptr(ws),
-                                       ws.numel(), stream), "compress_analyze")
+        self.analyze(x, p, g, d_val, ws, stream)  # (one host synchronisation: the numpy log2 fixups)
         if allreduce is not None:
             off = lib.pmz_ws_coverage(_ptr(ws), ctypes.byref(p), ctypes.byref(g)) - ws.data_ptr()
             allreduce(ws[off: off + 18 * 8].view(torch.int64))
@@ -311,8 +340,14 @@ class Codec:
         ws = self._buf("_dws", wsz.value)
         if out is None:
             out = torch.empty((int(h.rows), int(h.cols)), dtype=torch.float32, device=self.device)
-        check(lib.pmz_decompress(_ptr(d_buf), d_buf.numel(), ctypes.byref(h), host_b_a(h.b_r), _ptr(d_offsets),
-                                 _ptr(out), _ptr(ws), ws.numel(), _stream_ptr(self.device)), "decompress")
+        stream = _stream_ptr(self.device)
+        b_a = host_b_a(h.b_r)
+        check(lib.pmz_decompress_prepare(_ptr(d_buf), d_buf.numel(), ctypes.byref(h), b_a, _ptr(d_offsets), _ptr(ws),
+                                         ws.numel(), stream), "decompress")
+        check(self.np_fix_decompress(h, ws, stream), "np_fixups")
+        check(lib.pmz_decompress_run(_ptr(d_buf), d_buf.numel(), ctypes.byref(h), b_a, _ptr(d_offsets), _ptr(out),
+                                     _ptr(ws), ws.numel(), stream), "decompress")
+        check(lib.pmz_decompress_result(ctypes.byref(h), _ptr(ws), ws.numel(), stream), "decompress")
         return out
 
 
@@ -320,9 +355,9 @@ _codecs: dict = {}
 
 
 class GraphedCompressor:
-    """The whole single-GPU compress pipeline of one geometry captured into a
-    CUDA graph (pmz_compress_enqueue: ~16 kernels, no host synchronisation),
-    replayed per call; the outcome is read with pmz_compress_result (one small
+    """The whole single-GPU compress pipeline of one geometry captured into two
+    CUDA graphs (block stats; then transform + codes + finish, ~16 kernels)
+    around the host's numpy log2 fixups, replayed per call; the outcome is read with pmz_compress_result (one small
     device->host copy).  Buffers are fixed at construction: the input is
     ``x`` (a float32 CUDA tensor the caller keeps alive and refills), or, with
     ``host_input`` (a pinned float32 CPU tensor), a device copy that the graph
@@ -353,21 +388,40 @@ class GraphedCompressor:
         self.out = torch.empty(max(int(cap.value), 1), dtype=torch.uint8, device=codec.device)
         self.block_offsets = block_offsets
         # eager run: sets kernel attributes, validates the configuration
-        self._enqueue()
+        self._enqueue_stats()
+        self._fix()
+        self._enqueue_rest()
         self._result()
         torch.cuda.synchronize(codec.device)
+        self.graph_stats = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph_stats):
+            self._enqueue_stats()
         self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.graph):
-            self._enqueue()
+            self._enqueue_rest()
 
-    def _enqueue(self):
-        lib = self.codec.lib
+    def _enqueue_stats(self):
         if self.host is not None:
             self.x.copy_(self.host, non_blocking=True)
-        check(lib.pmz_compress_enqueue(_ptr(self.x), ctypes.byref(self.g), ctypes.byref(self.p), _ptr(self.d_val),
-                                       int(self.d_val.numel()), 1, _ptr(self.out), self.out.numel(),
-                                       _ptr(self.block_offsets), _ptr(self.ws), self.ws.numel(),
-                                       _stream_ptr(self.codec.device)), "compress_enqueue")
+        check(self.codec.lib.pmz_compress_stats(_ptr(self.x), ctypes.byref(self.g), ctypes.byref(self.p),
+                                                _ptr(self.ws), self.ws.numel(), _stream_ptr(self.codec.device)),
+              "compress_stats")
+
+    def _fix(self):
+        # the only host step: np.log2 of the listed blocks' general doubles (D22)
+        check(self.codec.np_fix_compress(self.p, self.g, self.ws, _stream_ptr(self.codec.device)), "np_fixups")
+
+    def _enqueue_rest(self):
+        lib = self.codec.lib
+        stream = _stream_ptr(self.codec.device)
+        nv = int(self.d_val.numel())
+        check(lib.pmz_compress_transform(_ptr(self.x), ctypes.byref(self.g), ctypes.byref(self.p), _ptr(self.d_val),
+                                         nv, _ptr(self.ws), self.ws.numel(), stream), "compress_transform")
+        check(lib.pmz_compress_codes(_ptr(self.x), ctypes.byref(self.g), ctypes.byref(self.p), _ptr(self.d_val), nv,
+                                     _ptr(self.ws), self.ws.numel(), stream), "compress_codes")
+        check(lib.pmz_compress_finish_async(ctypes.byref(self.g), ctypes.byref(self.p), 1, _ptr(self.out),
+                                            self.out.numel(), _ptr(self.block_offsets), _ptr(self.ws),
+                                            self.ws.numel(), stream), "compress_finish")
 
     def _result(self):
         res = N.Result()
@@ -381,7 +435,11 @@ class GraphedCompressor:
         return self.out[:n], info
 
     def launch(self):
-        """Replay the captured pipeline on the current stream (asynchronous)."""
+        """Replay the captured pipeline on the current stream: the stats graph,
+        the host's numpy log2 fixups (one synchronisation), then the rest
+        (asynchronous)."""
+        self.graph_stats.replay()
+        self._fix()
         self.graph.replay()
 
     def result(self):
@@ -469,7 +527,7 @@ class PipelinedDecompressor:
     slots, each with its own CUDA stream, device container buffer, block
     index, workspace and output.  ``submit`` enqueues the host->device copy
     of the container (pinned host bytes), the decode kernels
-    (pmz_decompress_enqueue) and the device->host copy of the float32 grid
+    (pmz_decompress_prepare, the numpy log2 fixups, pmz_decompress_run) and the device->host copy of the float32 grid
     into pinned memory; ``collect`` synchronises the oldest slot, maps its
     device status (pmz_decompress_result) and returns the grid."""
 
@@ -523,9 +581,12 @@ class PipelinedDecompressor:
             sl["h_offs"].copy_(torch.from_numpy(np.asarray(block_offsets).view(np.int64)))  # slot is idle: safe
             sl["offs"].copy_(sl["h_offs"], non_blocking=True)
             sl["h"] = h
-            check(lib.pmz_decompress_enqueue(_ptr(sl["buf"]), n, ctypes.byref(h), host_b_a(h.b_r),
-                                             _ptr(sl["offs"]), _ptr(sl["out"]), _ptr(sl["ws"]), sl["ws"].numel(),
-                                             ctypes.c_void_p(sl["stream"].cuda_stream)), "decompress")
+            stream = ctypes.c_void_p(sl["stream"].cuda_stream)
+            check(lib.pmz_decompress_prepare(_ptr(sl["buf"]), n, ctypes.byref(h), host_b_a(h.b_r), _ptr(sl["offs"]),
+                                             _ptr(sl["ws"]), sl["ws"].numel(), stream), "decompress")
+            check(self.codec.np_fix_decompress(h, sl["ws"], stream), "np_fixups")
+            check(lib.pmz_decompress_run(_ptr(sl["buf"]), n, ctypes.byref(h), host_b_a(h.b_r), _ptr(sl["offs"]),
+                                         _ptr(sl["out"]), _ptr(sl["ws"]), sl["ws"].numel(), stream), "decompress")
         sl["n"] = n
         self._queue.append(i)
         return i

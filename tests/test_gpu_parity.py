@@ -156,7 +156,7 @@ def test_decompress_corrupted_payload(codec, oracle):
 
 
 def test_log2_device_matches_oracle(oracle):
-    """Device CR log2 for f32 inputs vs the oracle on 2^20 random floats."""
+    """Device log2 for f32 inputs vs the oracle and np.log2 on 2^20 random floats."""
     import ctypes
     from paper_2309_09778_b200 import _native as N
     lib = N.load()
@@ -173,14 +173,16 @@ def test_log2_device_matches_oracle(oracle):
     got = out.cpu().numpy()
     ref = np.array([oracle.log2(float(v)) for v in xs[:200000]])
     assert np.array_equal(got[:200000], ref)
+    assert np.array_equal(got, np.log2(xs.astype(np.float64)))
     assert int(amb.item()) == 0
 
 
 @pytest.mark.slow
 def test_log2_exhaustive_no_ambiguity():
-    """All 2^31 - 2^23 positive normal finite floats: the production (two-level
-    table) log2 equals the precise double-double path bit for bit, and no
-    rounding is ever left undecided (amb == 0)."""
+    """All 2^31 - 2^24 positive normal finite floats: the production (two-level
+    table) log2 equals the precise double-double path bit for bit, both equal
+    the box's own np.log2 (the reference's arithmetic, transform.py:178-180)
+    bit for bit, and no rounding is ever left undecided (amb == 0)."""
     import ctypes
     from paper_2309_09778_b200 import _native as N
     lib = N.load()
@@ -189,7 +191,7 @@ def test_log2_exhaustive_no_ambiguity():
     out0 = torch.empty(chunk, dtype=torch.float64, device="cuda")
     out1 = torch.empty(chunk, dtype=torch.float64, device="cuda")
     start = 0x00800000
-    mism = 0
+    mism = mism_np = 0
     while start < 0x7f800000:
         n = min(chunk, 0x7f800000 - start)
         xs = torch.arange(start, start + n, dtype=torch.int64, device="cuda").to(torch.int32).view(torch.float32)
@@ -197,10 +199,13 @@ def test_log2_exhaustive_no_ambiguity():
             assert lib.pmz_log2_f32_batch(ctypes.c_void_p(xs.data_ptr()), n, ctypes.c_void_p(o.data_ptr()),
                                           ctypes.c_void_p(amb.data_ptr()), v, None) == 0
         mism += int((out0[:n] != out1[:n]).sum())
+        ref = np.log2(np.arange(start, start + n, dtype=np.uint32).view(np.float32).astype(np.float64))
+        mism_np += int((out0[:n].cpu().numpy() != ref).sum())
         start += n
     torch.cuda.synchronize()
     assert int(amb.item()) == 0
     assert mism == 0
+    assert mism_np == 0
 
 
 def test_decoder_runs_fallback(codec, oracle):
