@@ -289,6 +289,23 @@ PMZ_API int pmz_segy_samples(const uint8_t *d_traces, uint64_t n_traces, uint32_
 PMZ_API int pmz_transform_params(const float *d_in, const pmz_geom *g, const pmz_params *p, double *d_params10,
                          uint8_t *d_trivial, void *d_ws, uint64_t ws_bytes, void *stream);
 
+/* compute_block_stats (transform.py:84-107) over n doubles (the reference
+ * upcasts every element type to float64, :95): d_out6 = abs_min over nonzero
+ * magnitudes, abs_max, has_zero, has_negative, nonfinite, count (abs_min =
+ * abs_max = 0 when there is no nonzero element).  d_scratch: 64 device bytes.
+ * Stream-ordered. */
+PMZ_API int pmz_block_stats(const double *d_x, uint64_t n, double *d_out6, void *d_scratch, void *stream);
+
+/* derive_transform_params (transform.py:110-135): d_in4 = factor_pos,
+ * factor_neg, b_r, epsilon0; b_a = float(np.log2(1.0 + b_r)) from the host
+ * (:118); d_out10 in TransformParams field order.  *d_mask bit i: np.log2 of
+ * (factor_neg, factor_pos - epsilon0, factor_pos, epsilon0)[i] is too close
+ * to a rounding midpoint to be decided without numpy (see pmz_np_fix). */
+PMZ_API int pmz_derive_params(const double *d_in4, double b_a, double *d_out10, int32_t *d_mask, void *stream);
+
+/* zero_sub_floor_magnitudes (transform.py:205-210): out = x with |x| <= eps0 -> 0. */
+PMZ_API int pmz_zero_sub_floor(const double *d_x, uint64_t n, double eps0, double *d_out, void *stream);
+
 /* forward_map / inverse_map (transform.py:170-202) elementwise with one
  * parameter set (TransformParams fields, transform.py:61-81). */
 PMZ_API int pmz_forward_map(const double *d_x, uint64_t n, const double *params10, double *d_v, void *stream);

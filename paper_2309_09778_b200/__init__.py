@@ -4,11 +4,11 @@ compress/decompress path (arXiv 2309.09778).
 Public entry points mirror the reference package: ``compress`` /
 ``decompress`` (pipeline), the transform module, the exception hierarchy.
 """
-from . import errors
+from . import errors, transform
 from .errors import PermezError
 from .pipeline import (Codec, CompressConfig, CompressInfo, GraphedCompressor, PipelinedCompressor,
                        PipelinedDecompressor, compress, decompress)
 from .predictor import PerceptronModel, init_model, lorenzo_coefficients
 
 __all__ = ["compress", "decompress", "Codec", "GraphedCompressor", "PipelinedCompressor", "PipelinedDecompressor", "CompressConfig", "CompressInfo", "PerceptronModel", "init_model",
-           "lorenzo_coefficients", "errors", "PermezError"]
+           "lorenzo_coefficients", "errors", "transform", "PermezError"]

@@ -92,6 +92,9 @@ _SIGS = {
     "pmz_forward_map": (c_int32, [VP, c_uint64, VP, VP, VP]),
     "pmz_inverse_map": (c_int32, [VP, c_uint64, VP, VP, VP, VP]),
     "pmz_log2_f32_batch": (c_int32, [VP, c_uint64, VP, VP, c_int32, VP]),
+    "pmz_block_stats": (c_int32, [VP, c_uint64, VP, VP, VP]),
+    "pmz_derive_params": (c_int32, [VP, c_double, VP, VP, VP]),
+    "pmz_zero_sub_floor": (c_int32, [VP, c_uint64, c_double, VP, VP]),
     "pmz_compress_stats": (c_int32, [VP, ctypes.POINTER(Geom), ctypes.POINTER(Params), VP, c_uint64, VP]),
     "pmz_compress_transform": (c_int32, [VP, ctypes.POINTER(Geom), ctypes.POINTER(Params), VP, c_int64, VP, c_uint64,
                                          VP]),

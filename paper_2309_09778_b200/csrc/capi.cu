@@ -881,6 +881,112 @@ int pmz_inverse_map(const double *d_v, uint64_t n, const double *params10, doubl
   return launch_check();
 }
 
+// compute_block_stats (transform.py:84-107) over n doubles: one CTA per 8192
+// elements, warp/CTA reductions, atomics on order-preserving bit patterns.
+// out[0..5] = abs_min (nonzero), abs_max, has_zero, has_negative, nonfinite, count.
+__global__ void k_block_stats_f64(const double *__restrict__ x, uint64_t n, unsigned long long *acc) {
+  unsigned long long mn = ~0ull, mx = 0ull;  // bit patterns of non-negative doubles order like the values
+  int zero = 0, neg = 0, nonfin = 0;
+  const uint64_t base = (uint64_t)blockIdx.x * 8192;
+  for (uint64_t i = base + threadIdx.x; i < n && i < base + 8192; i += blockDim.x) {
+    const double v = x[i];
+    if (!isfinite(v)) { nonfin = 1; continue; }
+    const double a = fabs(v);
+    if (a > 0.0) {
+      const unsigned long long b = (unsigned long long)__double_as_longlong(a);
+      mn = min(mn, b);
+      mx = max(mx, b);
+    } else {
+      zero = 1;
+    }
+    if (v < 0.0) neg = 1;
+  }
+  for (int o = 16; o; o >>= 1) {
+    mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  zero = __any_sync(0xffffffffu, zero);
+  neg = __any_sync(0xffffffffu, neg);
+  nonfin = __any_sync(0xffffffffu, nonfin);
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(&acc[0], mn);
+    atomicMax(&acc[1], mx);
+    if (zero) atomicOr(&acc[2], 1ull);
+    if (neg) atomicOr(&acc[3], 1ull);
+    if (nonfin) atomicOr(&acc[4], 1ull);
+  }
+}
+__global__ void k_block_stats_init(unsigned long long *acc) {
+  acc[0] = ~0ull;
+  acc[1] = acc[2] = acc[3] = acc[4] = 0ull;
+}
+__global__ void k_block_stats_out(const unsigned long long *acc, uint64_t n, double *out) {
+  const bool any = acc[0] != ~0ull;
+  out[0] = any ? __longlong_as_double((long long)acc[0]) : 0.0;
+  out[1] = any ? __longlong_as_double((long long)acc[1]) : 0.0;
+  out[2] = (double)acc[2];
+  out[3] = (double)acc[3];
+  out[4] = (double)acc[4];
+  out[5] = (double)n;
+}
+
+int pmz_block_stats(const double *d_x, uint64_t n, double *d_out6, void *d_scratch, void *stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  unsigned long long *acc = reinterpret_cast<unsigned long long *>(d_scratch);
+  k_block_stats_init<<<1, 1, 0, st>>>(acc);
+  if (n > 0) k_block_stats_f64<<<(unsigned)((n + 8191) / 8192), 256, 0, st>>>(d_x, n, acc);
+  k_block_stats_out<<<1, 1, 0, st>>>(acc, n, d_out6);
+  return launch_check();
+}
+
+// derive_transform_params (transform.py:110-135) on the device: in4 = factor_pos,
+// factor_neg, b_r, epsilon0; out10 in TransformParams field order; mask bit i
+// set when np.log2 of (factor_neg, factor_pos - epsilon0, factor_pos,
+// epsilon0)[i] must be decided by the host (numpy), see pmz_np_fix.
+__global__ void k_derive_params(const double *in4, double b_a, double *out10, int *mask) {
+  const int lane = threadIdx.x;
+  const double fp = in4[0], fn = in4[1], b_r = in4[2], e0 = in4[3];
+  const double arg = lane == 0 ? fn : (lane == 1 ? __dsub_rn(fp, e0) : (lane == 2 ? fp : e0));
+  double l = 0.0;
+  int und = 0;
+  if (lane < 4) {
+    l = pmz_log2_d(arg, nullptr);
+    und = np_log2_undecided(arg) ? 1 : 0;
+  }
+  const unsigned bal = __ballot_sync(0xffffffffu, und);
+  const double lg_neg = __shfl_sync(0xffffffffu, l, 0), lpe = __shfl_sync(0xffffffffu, l, 1),
+               lg_pos = __shfl_sync(0xffffffffu, l, 2), l0 = __shfl_sync(0xffffffffu, l, 3);
+  if (lane == 0) {
+    const double zc = __dadd_rn(l0, lg_pos);
+    out10[0] = fp; out10[1] = fn; out10[2] = e0; out10[3] = b_r; out10[4] = b_a;
+    out10[5] = __dsub_rn(__dadd_rn(lg_neg, lpe), b_a);  // boundary, :123
+    out10[6] = zc;                                        // zero_code_value, :121
+    out10[7] = __dadd_rn(zc, b_a);                        // zero_threshold, :122
+    out10[8] = lg_pos; out10[9] = lg_neg;
+    *mask = (int)(bal & 15u);
+  }
+}
+
+int pmz_derive_params(const double *d_in4, double b_a, double *d_out10, int32_t *d_mask, void *stream) {
+  k_derive_params<<<1, 32, 0, (cudaStream_t)stream>>>(d_in4, b_a, d_out10, d_mask);
+  return launch_check();
+}
+
+// zero_sub_floor_magnitudes (transform.py:205-210) elementwise on doubles
+__global__ void k_zero_sub_floor(const double *__restrict__ x, uint64_t n, double eps0, double *out) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const double v = x[i];
+    out[i] = fabs(v) <= eps0 ? 0.0 : v;
+  }
+}
+
+int pmz_zero_sub_floor(const double *d_x, uint64_t n, double eps0, double *d_out, void *stream) {
+  if (n == 0) return PMZ_OK;
+  const unsigned grid = (unsigned)std::min<uint64_t>((n + 255) / 256, 148ull * 16);
+  k_zero_sub_floor<<<grid, 256, 0, (cudaStream_t)stream>>>(d_x, n, eps0, d_out);
+  return launch_check();
+}
+
 __global__ void k_log2_batch(const float *x, uint64_t n, double *out, unsigned *amb, int variant) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     const double a = (double)x[i];

@@ -142,15 +142,15 @@ class Codec:
         return N.resolve_np_log2(
             lambda b, cap: lib.pmz_compress_np_fixups(ctypes.byref(g), ctypes.byref(p), _ptr(ws), ws.numel(), stream,
                                                       b, cap),
-            lambda b, n: check(lib.pmz_compress_np_apply(ctypes.byref(g), ctypes.byref(p), _ptr(ws), ws.numel(),
-                                                         stream, b, n), "np_apply"))
+            lambda b, n: lib.pmz_compress_np_apply(ctypes.byref(g), ctypes.byref(p), _ptr(ws), ws.numel(), stream, b,
+                                                   n))
 
     def np_fix_decompress(self, h, ws: torch.Tensor, stream) -> int:
         lib = self.lib
         return N.resolve_np_log2(
             lambda b, cap: lib.pmz_decompress_np_fixups(ctypes.byref(h), _ptr(ws), ws.numel(), stream, b, cap),
-            lambda b, n: check(lib.pmz_decompress_np_apply(ctypes.byref(h), host_b_a(h.b_r), _ptr(ws), ws.numel(),
-                                                           stream, b, n), "np_apply"))
+            lambda b, n: lib.pmz_decompress_np_apply(ctypes.byref(h), host_b_a(h.b_r), _ptr(ws), ws.numel(), stream,
+                                                     b, n))
 
     def analyze(self, x, p, g, d_val, ws, stream):
         """Stage 1: block stats + parameters, the host's np.log2 for the
@@ -159,7 +159,7 @@ class Codec:
         lib = self.lib
         check(lib.pmz_compress_stats(_ptr(x), ctypes.byref(g), ctypes.byref(p), _ptr(ws), ws.numel(), stream),
               "compress_stats")
-        check(self.np_fix_compress(p, g, ws, stream), "np_fixups")
+        check(min(self.np_fix_compress(p, g, ws, stream), 0), "np_fixups")
         check(lib.pmz_compress_transform(_ptr(x), ctypes.byref(g), ctypes.byref(p), _ptr(d_val), int(d_val.numel()),
                                          _ptr(ws), ws.numel(), stream), "compress_transform")
 
@@ -344,7 +344,7 @@ class Codec:
         b_a = host_b_a(h.b_r)
         check(lib.pmz_decompress_prepare(_ptr(d_buf), d_buf.numel(), ctypes.byref(h), b_a, _ptr(d_offsets), _ptr(ws),
                                          ws.numel(), stream), "decompress")
-        check(self.np_fix_decompress(h, ws, stream), "np_fixups")
+        check(min(self.np_fix_decompress(h, ws, stream), 0), "np_fixups")
         check(lib.pmz_decompress_run(_ptr(d_buf), d_buf.numel(), ctypes.byref(h), b_a, _ptr(d_offsets), _ptr(out),
                                      _ptr(ws), ws.numel(), stream), "decompress")
         check(lib.pmz_decompress_result(ctypes.byref(h), _ptr(ws), ws.numel(), stream), "decompress")
@@ -409,7 +409,7 @@ class GraphedCompressor:
 
     def _fix(self):
         # the only host step: np.log2 of the listed blocks' general doubles (D22)
-        check(self.codec.np_fix_compress(self.p, self.g, self.ws, _stream_ptr(self.codec.device)), "np_fixups")
+        check(min(self.codec.np_fix_compress(self.p, self.g, self.ws, _stream_ptr(self.codec.device)), 0), "np_fixups")
 
     def _enqueue_rest(self):
         lib = self.codec.lib
@@ -584,7 +584,7 @@ class PipelinedDecompressor:
             stream = ctypes.c_void_p(sl["stream"].cuda_stream)
             check(lib.pmz_decompress_prepare(_ptr(sl["buf"]), n, ctypes.byref(h), host_b_a(h.b_r), _ptr(sl["offs"]),
                                              _ptr(sl["ws"]), sl["ws"].numel(), stream), "decompress")
-            check(self.codec.np_fix_decompress(h, sl["ws"], stream), "np_fixups")
+            check(min(self.codec.np_fix_decompress(h, sl["ws"], stream), 0), "np_fixups")
             check(lib.pmz_decompress_run(_ptr(sl["buf"]), n, ctypes.byref(h), host_b_a(h.b_r), _ptr(sl["offs"]),
                                          _ptr(sl["out"]), _ptr(sl["ws"]), sl["ws"].numel(), stream), "decompress")
         sl["n"] = n
