@@ -1,22 +1,30 @@
 """Benchmark of the B200 PW_REL block compression path (BASELINE.json metric:
 "compress/decompress GB/s at PW_REL 1e-2 (1/2/4/8 B200); compression ratio").
 
-Workload (N=1): config C2 of BASELINE.json -- float32 1800x3600 exp(GRF k^-3)
-sign-flipped on 30% of a smooth mask, PW_REL 1e-2, repair_factor 1.0 (every
-point |x'-x| <= eps|x|), Lorenzo-init perceptron, 256x256 blocks, 32-row
-partitions.  A step = one compress of the field resident in HBM; decompress is
-timed the same way and reported beside it.  N>1: the field is N copies of C2
-stacked along the slowest axis and sharded into whole block-rows, one shard
-per rank (weak scaling); shards exchange only the select_m / codebook
-histograms (NCCL all-reduce) and the per-shard sizes (NCCL all-gather).
+Workload: config C5 of BASELINE.json (configs[4], the metric's 1/2/4/8-GPU
+configuration, which fits one B200): float32 1024x1024x2048 (8 GiB, 2^31
+points) Gaussian random field k^-3, mixed sign, seed 4, generated on the
+device (synthetic stand-in: no public dataset), viewed as the 2-D grid
+1048576 x 2048 (D18); PW_REL 1e-2, repair_factor 1.0 (every point
+|x'-x| <= eps|x|), init_model (Lorenzo) perceptron, 256x256 blocks, 32-row
+partitions.  A step = one compress of the field resident in HBM (one at a
+time; the 8 GiB input is far larger than the 126 MB L2); decompress is timed
+the same way and reported beside it.  N > 1 (torchrun): the SAME field is
+sharded by whole block-rows (slowest axis) across the ranks -- strong scaling;
+shards exchange only the select_m / codebook histograms (NCCL all-reduce) and
+the per-shard sizes (NCCL all-gather).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C5]
 
-Prints ONE JSON line on rank 0.
+Prints ONE JSON line on rank 0.  ``--impl reference`` times the reference
+CPU path -- the C restatement in oracle/ (the reference ships no compress
+code) -- on all host cores over a fixed block-row subset of
+the same field.
 """
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import statistics
@@ -31,19 +39,19 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 HBM_FALLBACK = 6650.0
-METRIC = "compress GB/s at PW_REL 1e-2 (C2 1800x3600 f32)"
+METRIC = "compress GB/s at PW_REL 1e-2"
+EPS0 = 1.1754943508222875e-38
+# CPU sample: a contiguous slab of block-rows = 1/64 of C5
+SAMPLE_FRACTION = 64
 
-
-# kernels per pmz_decompress: k_dec_blocks, k_dec_tables, k_decode4, k_reconstruct3, k_inv
-DECOMPRESS_LAUNCHES = 5
 
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             d = json.load(f)
-        return float(d["hbm_gbs"]), "measured"
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
     except Exception:
-        return HBM_FALLBACK, "fallback"
+        return HBM_FALLBACK, "fallback (B200_PROFILING.md)"
 
 
 class ClockSampler:
@@ -52,10 +60,7 @@ class ClockSampler:
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index: int):
-        self.index = index
-        self.samples = []
-        self._stop = threading.Event()
-        self._t = None
+        self.index, self.samples, self._stop, self._t = index, [], threading.Event(), None
 
     def _run(self):
         while not self._stop.is_set():
@@ -67,7 +72,7 @@ class ClockSampler:
                     self.samples.append([v.strip() for v in out.split(",")])
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(0.1)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -91,55 +96,69 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-def c2_field(device):
-    """The C2 field, generated on the host (the CPU generator) and copied to
-    `device`: both bench arms (this one and --impl reference) compress the
-    identical field."""
+def workload(name: str, eps: float):
     from paper_2309_09778_b200 import synthetic
-    return synthetic.generate("C2").to(device)
+    shape, _, seed, desc = synthetic.CONFIGS[name]
+    return (f"{name}: f32 {'x'.join(map(str, shape))} ({np.prod(shape) * 4 / 2**30:.3g} GiB) {desc}, seed {seed}; "
+            f"PW_REL {eps:g}, repair 1.0; 256x256 blocks, 32-row partitions, init_model")
 
 
-def cpu_reference_time(x: np.ndarray, eps: float, repair: float, reps: int, threads: int):
-    """Oracle restatement of the reference path (CPU, all host threads)."""
+def field_2d(name: str, dev):
+    """The config's field generated on `dev`, as its 2-D grid view (D18)."""
+    from paper_2309_09778_b200 import synthetic
+    from paper_2309_09778_b200.pipeline import grid_view_shape
+    x = synthetic.generate(name, device=dev)
+    (r, c), _ = grid_view_shape(tuple(x.shape))
+    return x.reshape(r, c)
+
+
+def cpu_sample(x2d):
+    """The fixed CPU sample: the first 1/64 of the block-rows (whole blocks)."""
+    rows = x2d.shape[0]
+    nbr = (rows + 255) // 256
+    take = max(1, nbr // SAMPLE_FRACTION) * 256
+    return x2d[: min(rows, take)]
+
+
+def oracle_compress_time(xs: np.ndarray, eps: float, reps: int, threads: int):
     from oracle import oracle as O
-    cfg = O.OracleConfig(b_r=eps, repair_factor=repair)
-    O.compress(x, cfg, nthreads=threads)  # warm
-    t0 = time.perf_counter()
+    cfg = O.OracleConfig(b_r=eps, repair_factor=1.0)
+    O.compress(xs, cfg, nthreads=threads)  # warm
+    ts = []
     for _ in range(reps):
-        buf, _ = O.compress(x, cfg, nthreads=threads)
-    dt = (time.perf_counter() - t0) / reps
-    return dt, len(buf)
+        t0 = time.perf_counter()
+        buf, info = O.compress(xs, cfg, nthreads=threads)
+        ts.append(time.perf_counter() - t0)
+    return ts, buf, info
 
 
 def run_reference(args):
+    """--impl reference: the reference CPU path (oracle/ restatement, all host
+    threads) on the fixed 1/64 block-row sample of the same field."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     import torch
-    from paper_2309_09778_b200 import synthetic
-    x = synthetic.generate("C2").numpy()
+    dev = torch.device("cuda", 0) if torch.cuda.is_available() else torch.device("cpu")
+    x = field_2d(args.config, dev)
+    xs = np.ascontiguousarray(cpu_sample(x).cpu().numpy())
+    del x
     threads = os.cpu_count() or 1
-    from oracle import oracle as O
-    cfg = O.OracleConfig(b_r=args.eps, repair_factor=args.repair)
-    for _ in range(args.warmup):
-        O.compress(x, cfg, nthreads=threads)
-    ts = []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        buf, _ = O.compress(x, cfg, nthreads=threads)
-        ts.append(time.perf_counter() - t0)
+    ts, buf, _ = oracle_compress_time(xs, args.eps, args.warmup + args.steps, threads)
+    ts = ts[args.warmup:] or ts
     t = sum(ts) / len(ts)
-    gbs = x.nbytes / t / 1e9
+    gbs = xs.nbytes / t / 1e9
+    sample = (f"first 1/{SAMPLE_FRACTION} of the block-rows of the {args.config} field "
+              f"({xs.shape[0]}x{xs.shape[1]} f32, {xs.nbytes / 2**20:.0f} MiB) per step")
     line = {
         "impl": "reference", "metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "C2 1800x3600 f32 exp(GRF k^-3) sign-flipped, PW_REL 1e-2, repair 1.0",
-                   "path": "oracle/permez_oracle.c (C restatement of the reference path; the reference ships "
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": workload(args.config, args.eps),
+                   "path": "oracle/permez_oracle.c (C restatement of the reference path: the reference ships "
                            "no compress code) + numpy split, OpenMP over blocks"},
-        "compression_ratio": len(buf) / x.nbytes,
-        "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": threads, "kind": "port",
-                         "sample": f"full C2 field per step, {args.steps} steps"},
+        "compression_ratio": len(buf) / xs.nbytes,
+        "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": threads, "kind": "port", "sample": sample},
         "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -149,102 +168,87 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C5", help="BASELINE config (C5 = the metric's configuration)")
     ap.add_argument("--eps", type=float, default=1e-2)
-    ap.add_argument("--repair", type=float, default=1.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--pipeline", type=int, default=6,
-                    help="fields / containers in flight on the device for value (streams + captured graphs); "
-                         "1 = one at a time")
-    ap.add_argument("--e2e-pipeline", type=int, default=3,
-                    help="fields in flight for the host-to-host e2e numbers (PCIe-bound: more depth only adds "
-                         "contention)")
+    ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=0, help="(ncu) run this many steps, no JSON timing claims")
     args = ap.parse_args()
-    args.warmup = max(args.warmup, 3) if args.profile_steps == 0 else args.warmup
+    if args.profile_steps == 0:
+        args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
         return run_reference(args)
 
     import torch
     import torch.distributed as dist
     import paper_2309_09778_b200 as P
+    from paper_2309_09778_b200 import _native as N
+    from paper_2309_09778_b200.sharding import exchange_record_sizes, local_validation_blocks, plan_shard
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    # PMZ_BENCH_SHARDED=1: the sharded code path (NCCL collectives included)
-    # on a single rank, to check it on one GPU
     sharded = world > 1 or bool(os.environ.get("PMZ_BENCH_SHARDED"))
     if sharded:
         dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
 
     def allreduce(t):
-        if sharded:
-            dist.all_reduce(t)
+        dist.all_reduce(t)
 
-    from paper_2309_09778_b200.sharding import exchange_record_sizes, local_validation_blocks, plan_shard
-    cfg = P.CompressConfig(rel_error=args.eps, repair_factor=args.repair)
-    base = c2_field(dev)                      # 1800 x 3600, seed 1
-    R0, C = base.shape
-    grows = R0 * world
+    cfg = P.CompressConfig(rel_error=args.eps, repair_factor=1.0)
+    xg = field_2d(args.config, dev)  # every rank builds the same field (same seed), keeps its rows
+    grows, C = xg.shape
     plan = plan_shard(grows, C, cfg.block_rows, cfg.block_cols, world, rank)
-    b0, r0, r1 = plan.block_row0, plan.row0, plan.row1
+    x = xg[plan.row0: plan.row1]
+    xs_host = np.ascontiguousarray(cpu_sample(xg).cpu().numpy()) if (rank == 0 and world == 1) else None
     d_val = torch.as_tensor(local_validation_blocks(plan, cfg.sample_rate, cfg.seed), dtype=torch.int64, device=dev)
-    idx = torch.arange(r0, r1, device=dev) % R0
-    x = base[idx].contiguous()                # this rank's shard of the stacked field
-    del base
     codec = P.Codec(dev)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
-    offs = torch.empty(((x.shape[0] + 255) // 256) * ((C + 255) // 256) + 1, dtype=torch.int64, device=dev)
+    nblk = plan.nblocks
+    offs = torch.empty(nblk + 1, dtype=torch.int64, device=dev)
 
     def compress_once(ev=None):
-        out = codec.compress_staged(x, cfg, block_row0=b0, global_rows=grows, allreduce=allreduce,
-                                    block_offsets=offs, events=ev, d_val=d_val)
-        if world > 1:  # the final NCCL gather of per-shard sizes -> container offsets
-            exchange_record_sizes(out[1].nbytes - out[1].header_bytes, device=dev)
-        return out
+        buf, info = codec.compress_staged(x, cfg, block_row0=plan.block_row0, global_rows=grows,
+                                          allreduce=allreduce if sharded else None, block_offsets=offs, events=ev,
+                                          d_val=d_val)
+        if sharded:  # the final NCCL gather of per-shard sizes -> container offsets
+            exchange_record_sizes(info.nbytes - info.header_bytes, device=dev)
+        return buf, info
 
-    # one compress to build the decompress inputs
     buf, info = compress_once()
-    from paper_2309_09778_b200 import _native as N
-    import ctypes
-
     full = buf.cpu().numpy()
-    hdr = N.Header()
-    # parse the header of this shard's container (header + own records)
-    lib = N.load()
-    st = lib.pmz_parse_header(full.ctypes.data_as(ctypes.c_void_p), full.size, ctypes.byref(hdr))
-    if st != 0:
-        raise RuntimeError(f"header parse failed {st}")
-    hdr.rows = x.shape[0]
-    hdr.nblocks = offs.numel() - 1
+    hdr = P.Codec.parse_header(full)
+    hdr.rows = x.shape[0]  # this shard's grid (the header carries the global rows)
+    hdr.nblocks = nblk
     dbuf = buf.clone()
     doffs = offs.clone()
-    out = torch.empty(x.shape, dtype=torch.float32, device=dev)
+    y = torch.empty(x.shape, dtype=torch.float32, device=dev)
 
-    def decompress_once():
-        return codec.decompress_device(dbuf, hdr, doffs, out=out)
+    def decompress_once(ev=None):
+        return codec.decompress_device(dbuf, hdr, doffs, out=y, events=ev)
 
-    # correctness guard on the benchmarked data: bound + zeros exact
-    y = decompress_once()
+    # correctness guard on the benchmarked data: every point within the bound, zeros exact
+    decompress_once()
     torch.cuda.synchronize()
-    xz = torch.where(x.abs() <= 1.1754943508222875e-38, torch.zeros_like(x), x)
-    nz = xz != 0
-    rel = ((y.double() - xz.double()).abs() / xz.double().abs().clamp_min(1e-300))[nz]
-    max_rel = float(rel.max()) if rel.numel() else 0.0
-    zeros_ok = bool((y[~nz] == 0).all())
-    assert max_rel <= args.eps * args.repair and zeros_ok, (max_rel, zeros_ok)
+    max_rel, zeros_ok = 0.0, True
+    for r0 in range(0, x.shape[0], 65536):
+        xa, ya = x[r0: r0 + 65536].double(), y[r0: r0 + 65536].double()
+        xz = torch.where(xa.abs() <= EPS0, torch.zeros_like(xa), xa)
+        nz = xz != 0
+        if bool(nz.any()):
+            max_rel = max(max_rel, float(((ya - xz).abs() / xz.abs())[nz].max()))
+        zeros_ok &= bool((ya[~nz] == 0).all())
+    assert max_rel <= args.eps and zeros_ok, (max_rel, zeros_ok)
+    del xa, ya, xz, nz
 
-    # warm-up
     for _ in range(args.warmup):
         compress_once()
         decompress_once()
     torch.cuda.synchronize()
-
     if args.profile_steps:
         for _ in range(args.profile_steps):
             compress_once()
@@ -252,415 +256,175 @@ def main():
         torch.cuda.synchronize()
         return 0
 
-    n_elem = x.numel()
     K = args.steps
-    c_ms, codes_ms, d_ms = [], [], []
+    c_ms, d_ms, c_stage, d_stage = [], [], [], []
     launches = 0
     sampler = ClockSampler(local)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    # single GPU: the whole compress pipeline replayed as one CUDA graph
-    gc = P.GraphedCompressor(codec, cfg, x=x, block_offsets=offs) if world == 1 else None
     with sampler:
         for _ in range(K):
-            flush.fill_(1)  # L2 flush, outside the timed events
-            if gc is not None:
-                ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-                ev[0].record()
-                gc.launch()
-                ev[1].record()
-                bufk, infok = gc.result()
-            else:
-                ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-                bufk, infok = compress_once(ev)
-            dstart, dstop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            flush.fill_(2)
-            dstart.record()
-            decompress_once()
-            dstop.record()
-            torch.cuda.synchronize()
-            c_ms.append(ev[0].elapsed_time(ev[-1]))
-            d_ms.append(dstart.elapsed_time(dstop))
-            launches += infok.launches + DECOMPRESS_LAUNCHES
-        # single GPU, several fields in flight: `depth` captured pipelines on
-        # their own streams; each step first copies its field (device to
-        # device) from a pool of 8 distinct resident copies (8 x 26 MB > L2,
-        # so no step finds its input in L2), then replays the graph
-        pipe = None
-        if world == 1 and args.pipeline > 1:
-            depth = args.pipeline
-            pool = [x.clone() for _ in range(8)]
-            slots = []
-            for _ in range(depth):
-                s_ = torch.cuda.Stream(dev)
-                with torch.cuda.stream(s_):
-                    xi = x.clone()
-                    slots.append((s_, xi, P.GraphedCompressor(codec, cfg, x=xi)))
-            torch.cuda.synchronize()
-
-            def run_pipe(nsteps):
-                for k_ in range(nsteps):
-                    s_, xi, g_ = slots[k_ % depth]
-                    with torch.cuda.stream(s_):
-                        xi.copy_(pool[k_ % 8], non_blocking=True)
-                        g_.launch()
-                for s_, _, _ in slots:
-                    torch.cuda.current_stream().wait_stream(s_)
-
-            run_pipe(max(args.warmup, depth))
-            torch.cuda.synchronize()
-            pa, pb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            pa.record()
-            run_pipe(K)
-            pb.record()
-            torch.cuda.synchronize()
-            pipe_ms = pa.elapsed_time(pb)
-            for s_, xi, g_ in slots:  # every slot's last field decoded its status cleanly
-                with torch.cuda.stream(s_):
-                    _, pinfo = g_.result()
-                assert pinfo.nbytes == infok.nbytes
-            launches_pipe = K * infok.launches
-            pipe = {"ms": pipe_ms, "depth": depth}
-        # sharded (N > 1, or PMZ_BENCH_SHARDED=1 for a 1-rank check): the same
-        # `depth` fields in flight per rank.  A slot's field -- the staged
-        # stages with the two NCCL histogram all-reduces -- is one captured
-        # CUDA graph; every slot has its own communicator, so the collectives
-        # of concurrently replayed graphs never share one.  A slot's status
-        # is read, and its record size all-gathered (default group, host
-        # order), when the slot comes round.
-        if sharded and args.pipeline > 1:
-            depth = args.pipeline
-            pool = [x.clone() for _ in range(8)]
-            wsz, cap = ctypes.c_uint64(0), ctypes.c_uint64(0)
-            p0_ = P.pipeline.make_params(cfg, 3)
-            g0_ = N.Geom(x.shape[0], x.shape[1], b0, grows)
-            lib.pmz_workspace_size(ctypes.byref(p0_), ctypes.byref(g0_), ctypes.byref(wsz))
-            lib.pmz_max_container_size(ctypes.byref(p0_), ctypes.byref(g0_), ctypes.byref(cap))
-            sslots = []
-            for _ in range(depth):
-                grp = dist.new_group(list(range(world)))
-                sl = {"s": torch.cuda.Stream(dev), "x": x.clone(),
-                      "ws": torch.empty(int(wsz.value), dtype=torch.uint8, device=dev),
-                      "out": torch.empty(int(cap.value), dtype=torch.uint8, device=dev), "offs": offs.clone(),
-                      "pg": None, "busy": False}
-
-                def ar_(t, grp=grp):
-                    dist.all_reduce(t, group=grp)
-
-                def enq(sl=sl, ar_=ar_):
-                    return codec.compress_staged_async(sl["x"], cfg, block_row0=b0, global_rows=grows, d_val=d_val,
-                                                       allreduce=ar_, ws=sl["ws"], out=sl["out"],
-                                                       block_offsets=sl["offs"])
-                with torch.cuda.stream(sl["s"]):  # eager warm-up (communicator set-up), then capture
-                    sl["pg"] = enq()
-                    codec.staged_result(*sl["pg"], sl["ws"], sl["out"])
-                    torch.cuda.synchronize()
-                    sl["graph"] = torch.cuda.CUDAGraph()
-                    with torch.cuda.graph(sl["graph"], stream=sl["s"]):
-                        enq()
-                sslots.append(sl)
-            torch.cuda.synchronize()
-
-            def sh_step(k_):
-                sl = sslots[k_ % depth]
-                with torch.cuda.stream(sl["s"]):
-                    if sl["busy"]:
-                        inf_ = codec.staged_result(*sl["pg"], sl["ws"], sl["out"])
-                        exchange_record_sizes(inf_.nbytes - inf_.header_bytes, device=dev)
-                    sl["x"].copy_(pool[k_ % 8], non_blocking=True)
-                    sl["graph"].replay()
-                    sl["busy"] = True
-
-            def sh_drain():
-                last = None
-                for sl in sslots:
-                    with torch.cuda.stream(sl["s"]):
-                        if sl["busy"]:
-                            last = codec.staged_result(*sl["pg"], sl["ws"], sl["out"])
-                            exchange_record_sizes(last.nbytes - last.header_bytes, device=dev)
-                            sl["busy"] = False
-                return last
-
-            for k_ in range(max(args.warmup, depth)):
-                sh_step(k_)
-            sh_drain()
-            if world > 1:
+            if sharded:
                 dist.barrier()
             torch.cuda.synchronize()
-            pa, pb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            pa.record()
-            for sl in sslots:
-                sl["s"].wait_event(pa)
-            for k_ in range(K):
-                sh_step(k_)
-            for sl in sslots:
-                torch.cuda.current_stream().wait_stream(sl["s"])
-            pb.record()
-            lastinfo = sh_drain()
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            bufk, infok = compress_once(ev)  # synchronises (status read-back)
             torch.cuda.synchronize()
-            assert lastinfo.nbytes == infok.nbytes
-            pipe = {"ms": pa.elapsed_time(pb), "depth": depth}
-            launches_pipe = K * infok.launches
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
+            c_ms.append(ev[0].elapsed_time(ev[3]))
+            c_stage.append([ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]), ev[2].elapsed_time(ev[3])])
+            launches += infok.launches
+            if sharded:
+                dist.barrier()
+            torch.cuda.synchronize()
+            dev_ = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            decompress_once(dev_)
+            torch.cuda.synchronize()
+            d_ms.append(dev_[0].elapsed_time(dev_[2]))
+            d_stage.append([dev_[0].elapsed_time(dev_[1]), dev_[1].elapsed_time(dev_[2])])
+            launches += codec.last_decompress_launches
+    assert infok.nbytes == info.nbytes
+
+    # whole-job time = max over ranks of the per-step device time
     tot = torch.tensor([sum(c_ms), sum(d_ms)], dtype=torch.float64, device=dev)
-    if world > 1:
+    if sharded:
         dist.all_reduce(tot, op=dist.ReduceOp.MAX)
-    c_tot, d_tot = float(tot[0]), float(tot[1])
-    pipe_ms_max = None
-    if pipe is not None:  # the job's device time, max over ranks
-        pt = torch.tensor([pipe["ms"]], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(pt, op=dist.ReduceOp.MAX)
-        pipe_ms_max = float(pt[0])
-    # total bytes = sum over ranks (shards are whole block-rows, ~equal)
-    nb_t = torch.tensor([float(n_elem * 4), float(infok.nbytes)], dtype=torch.float64, device=dev)
-    if world > 1:
+    c_step, d_step = float(tot[0]) / K, float(tot[1]) / K
+    nb_t = torch.tensor([float(x.numel() * 4), float(info.nbytes - info.header_bytes)], dtype=torch.float64,
+                        device=dev)
+    if sharded:
         dist.all_reduce(nb_t)
-    bytes_all, cbytes_all = float(nb_t[0]), float(nb_t[1])
-    comp_gbs = bytes_all / (c_tot / K / 1e3) / 1e9
-    dec_gbs = bytes_all / (d_tot / K / 1e3) / 1e9
-    cr = cbytes_all / bytes_all
+    bytes_all = float(nb_t[0])
+    cr = (float(nb_t[1]) + info.header_bytes) / bytes_all
+    comp_gbs = bytes_all / (c_step / 1e3) / 1e9
+    dec_gbs = bytes_all / (d_step / 1e3) / 1e9
 
-    # e2e through the public API with host buffers (pinned), every step
-    e2e_c, e2e_d = None, None
-    h_in = torch.empty(x.shape, dtype=torch.float32, pin_memory=True)
-    h_in.copy_(x)
-    h_out = torch.empty(int(info.nbytes) + (1 << 20), dtype=torch.uint8, pin_memory=True)
-    h_y = torch.empty(x.shape, dtype=torch.float32, pin_memory=True)
-    full_host = np.ascontiguousarray(bufk.cpu().numpy())
-    h_cont = torch.from_numpy(full_host).pin_memory()
-    e_ms, ed_ms = [], []
-    gce = P.GraphedCompressor(codec, cfg, host_input=h_in) if world == 1 else None
-    for i in range(max(3, K // 2)):
-        flush.fill_(3)
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s.record()
-        if gce is not None:  # graph: pinned H2D + pipeline; then status readback; D2H of the container
-            gce.launch()
-            b2, i2 = gce.result()
-        else:
-            xd = h_in.to(dev, non_blocking=True)
-            b2, i2 = codec.compress_staged(xd, cfg, block_row0=b0, global_rows=grows, allreduce=allreduce,
-                                           d_val=d_val)
-            exchange_record_sizes(i2.nbytes - i2.header_bytes, device=dev)
-        h_out[: i2.nbytes].copy_(b2, non_blocking=True)
-        e.record()
-        torch.cuda.synchronize()
-        e_ms.append(s.elapsed_time(e))
-        # decompress e2e: host container -> index walk -> H2D -> decode -> D2H
-        s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s2.record()
-        hoffs = P.Codec.index_blocks(full_host, hdr) if world == 1 else None
-        db = h_cont.to(dev, non_blocking=True)
-        do = torch.from_numpy(hoffs.view(np.int64)).to(dev, non_blocking=True) if hoffs is not None else doffs
-        yy = codec.decompress_device(db, hdr, do)
-        h_y.copy_(yy, non_blocking=True)
-        e2.record()
-        torch.cuda.synchronize()
-        ed_ms.append(s2.elapsed_time(e2))
-    et = torch.tensor([sum(e_ms) / len(e_ms), sum(ed_ms) / len(ed_ms)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(et, op=dist.ReduceOp.MAX)
-    e2e_c = bytes_all / (float(et[0]) / 1e3) / 1e9
-    e2e_d = bytes_all / (float(et[1]) / 1e3) / 1e9
-    e2e_serial = {"value": e2e_c, "unit": "GB/s", "ms_per_step": float(et[0])}
-    # e2e with several fields in flight through the public streaming API:
-    # pinned host field -> H2D -> graph -> status read-back -> D2H of the
-    # container into pinned memory, every step; device-clock events around
-    # the whole job (the last collect synchronises)
-    if world == 1 and args.e2e_pipeline > 1:
-        pc = P.PipelinedCompressor(codec, cfg, x.shape, depth=args.e2e_pipeline)
-        for _ in range(args.e2e_pipeline):
-            pc.submit(h_in)
-        for _ in range(args.e2e_pipeline):
-            pc.collect()
-        torch.cuda.synchronize()
-        ne = max(2 * args.e2e_pipeline, K)
-        ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ea.record()
-        nsub = 0
-        for _ in range(args.e2e_pipeline):
-            pc.submit(h_in)
-            nsub += 1
-        for _ in range(ne):
-            hb, hi = pc.collect(block=False)  # copy-out in flight while the next field goes in
-            if nsub < ne:
-                pc.submit(h_in)
-                nsub += 1
-        pc.wait()
-        eb.record()
-        torch.cuda.synchronize()
-        assert hi.nbytes == infok.nbytes and bytes(hb.numpy()[:64]) == bytes(full_host[:64])
-        e2e_c = bytes_all / (ea.elapsed_time(eb) / ne / 1e3) / 1e9
+    # e2e through the public API with pinned host buffers, every step: H2D of
+    # the field, compress, D2H of the container; H2D of the container + block
+    # index walk on the host, decompress, D2H of the float32 grid
+    e2e_c = e2e_d = None
+    if not args.no_e2e:
+        h_in = torch.empty(x.shape, dtype=torch.float32, pin_memory=True)
+        h_in.copy_(x)
+        h_out = torch.empty(int(info.nbytes) + (1 << 20), dtype=torch.uint8, pin_memory=True)
+        h_cont = torch.empty(int(info.nbytes), dtype=torch.uint8, pin_memory=True)
+        h_cont.copy_(buf)
+        h_y = torch.empty(x.shape, dtype=torch.float32, pin_memory=True)
+        xd = torch.empty_like(x)
+        e_ms, ed_ms = [], []
+        for _ in range(max(2, min(K, 3))):
+            if sharded:
+                dist.barrier()
+            torch.cuda.synchronize()
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            xd.copy_(h_in, non_blocking=True)
+            b2, i2 = codec.compress_staged(xd, cfg, block_row0=plan.block_row0, global_rows=grows,
+                                           allreduce=allreduce if sharded else None, d_val=d_val)
+            if sharded:
+                exchange_record_sizes(i2.nbytes - i2.header_bytes, device=dev)
+            h_out[: i2.nbytes].copy_(b2, non_blocking=True)
+            e.record()
+            torch.cuda.synchronize()
+            e_ms.append(s.elapsed_time(e))
+            if sharded:
+                dist.barrier()
+            torch.cuda.synchronize()
+            s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s2.record()
+            hoffs = P.Codec.index_blocks(h_cont.numpy(), hdr)
+            db = h_cont.to(dev, non_blocking=True)
+            do = torch.from_numpy(hoffs.view(np.int64)).to(dev, non_blocking=True)
+            yy = codec.decompress_device(db, hdr, do)
+            h_y.copy_(yy, non_blocking=True)
+            e2.record()
+            torch.cuda.synchronize()
+            ed_ms.append(s2.elapsed_time(e2))
+        assert torch.equal(h_y[:1024], y[:1024].cpu())
+        et = torch.tensor([sum(e_ms) / len(e_ms), sum(ed_ms) / len(ed_ms)], dtype=torch.float64, device=dev)
+        if sharded:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        e2e_c = {"value": bytes_all / (float(et[0]) / 1e3) / 1e9, "unit": "GB/s", "ms_per_step": float(et[0]),
+                 "h2d_bytes_per_step": int(x.numel() * 4), "d2h_bytes_per_step": int(info.nbytes),
+                 "api": "Codec.compress_staged from a pinned host field, container copied to pinned host memory"}
+        e2e_d = {"value": bytes_all / (float(et[1]) / 1e3) / 1e9, "unit": "GB/s", "ms_per_step": float(et[1]),
+                 "h2d_bytes_per_step": int(info.nbytes), "d2h_bytes_per_step": int(x.numel() * 4),
+                 "api": "Codec.index_blocks + decompress_device from a pinned host container, grid to pinned host"}
 
-    # decompress with several containers in flight (single GPU): `depth`
-    # slots, each with its own stream, device container copy, workspace and
-    # output; pmz_decompress_enqueue per step, the status of a slot is read
-    # (pmz_decompress_result) only when the slot comes round again.  Device
-    # events around the whole job.  e2e: PipelinedDecompressor (pinned host
-    # container -> H2D -> decode -> D2H of the f32 grid, every step).
-    dpipe, e2e_dp = None, None
-    if world == 1 and args.pipeline > 1:
-        depth = args.pipeline
-        dslots = []
-        for _ in range(depth):
-            s_ = torch.cuda.Stream(dev)
-            wsz = ctypes.c_uint64(0)
-            lib.pmz_decompress_workspace_size(ctypes.byref(hdr), ctypes.byref(wsz))
-            dslots.append((s_, dbuf.clone(), torch.empty(int(wsz.value), dtype=torch.uint8, device=dev),
-                           torch.empty(x.shape, dtype=torch.float32, device=dev)))
-        torch.cuda.synchronize()
-        b_a = P.pipeline.host_b_a(hdr.b_r)
-
-        def dec_enqueue(k_):
-            s_, db_, ws_, o_ = dslots[k_ % depth]
-            if k_ >= depth:  # the slot's previous container: status check (synchronises that stream only)
-                P.errors.check(lib.pmz_decompress_result(ctypes.byref(hdr), ctypes.c_void_p(ws_.data_ptr()),
-                                                         ws_.numel(), ctypes.c_void_p(s_.cuda_stream)), "decompress")
-            P.errors.check(lib.pmz_decompress_enqueue(ctypes.c_void_p(db_.data_ptr()), db_.numel(), ctypes.byref(hdr),
-                                                      b_a, ctypes.c_void_p(doffs.data_ptr()),
-                                                      ctypes.c_void_p(o_.data_ptr()), ctypes.c_void_p(ws_.data_ptr()),
-                                                      ws_.numel(), ctypes.c_void_p(s_.cuda_stream)), "decompress")
-
-        def dec_drain():
-            for s_, db_, ws_, o_ in dslots:
-                P.errors.check(lib.pmz_decompress_result(ctypes.byref(hdr), ctypes.c_void_p(ws_.data_ptr()),
-                                                         ws_.numel(), ctypes.c_void_p(s_.cuda_stream)), "decompress")
-
-        for k_ in range(max(args.warmup, depth)):
-            dec_enqueue(k_)
-        dec_drain()
-        torch.cuda.synchronize()
-        da, db2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        da.record()
-        for k_ in range(K):
-            if k_ < depth:
-                dslots[k_][0].wait_event(da)
-            dec_enqueue(depth + k_)  # every slot was used in the warm-up: status checks throughout
-        for s_, _, _, _ in dslots:
-            torch.cuda.current_stream().wait_stream(s_)
-        db2.record()
-        dec_drain()
-        torch.cuda.synchronize()
-        for _, _, _, o_ in dslots:  # every slot decoded the container exactly
-            assert torch.equal(o_, out)
-        dpipe = {"ms": da.elapsed_time(db2), "depth": depth}
-        launches += K * DECOMPRESS_LAUNCHES
-        # e2e through the public streaming API
-        edepth = max(1, args.e2e_pipeline)
-        pd = P.PipelinedDecompressor(codec, full_host, depth=edepth)
-        hoffs = P.Codec.index_blocks(full_host, hdr)
-        for _ in range(edepth):
-            pd.submit(h_cont, hoffs)
-        for _ in range(edepth):
-            pd.collect()
-        torch.cuda.synchronize()
-        ne = max(2 * edepth, K)
-        ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ea.record()
-        nsub = 0
-        for _ in range(edepth):
-            pd.submit(h_cont, P.Codec.index_blocks(full_host, hdr))
-            nsub += 1
-        for _ in range(ne):
-            yh = pd.collect(block=False)  # copy-out in flight while the next container goes in
-            if nsub < ne:
-                pd.submit(h_cont, P.Codec.index_blocks(full_host, hdr))
-                nsub += 1
-        pd.wait()
-        eb.record()
-        torch.cuda.synchronize()
-        assert torch.equal(yh, out.cpu())
-        e2e_dp = bytes_all / (ea.elapsed_time(eb) / ne / 1e3) / 1e9
-
-    # dominant kernel: the verify_and_repair recurrence (k_compress_ws, the
-    # codes stage = k_select_m + k_compress_ws), timed with events around the
-    # stage on the launching stream in a staged pass after the timed loop.
-    # Algorithmic bytes per element: reads v (8) + rq (2) + class (1) tiles,
-    # writes the final rq tile (2) = 13 B (roofline table).
-    for _ in range(3):
-        flush.fill_(4)
-        evs = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-        compress_once(evs)
-        torch.cuda.synchronize()
-        codes_ms.append(evs[1].elapsed_time(evs[2]))
+    # roofline: algorithmic bytes per element 4 + 4 CR
+    # (compress reads the f32 field and writes the container; decompress the
+    # reverse) x elements processed, divided by the event-timed duration of
+    # the dominant stage (and of the whole pipeline)
     hbm, peak_kind = peaks()
-    codes_avg = sum(codes_ms) / len(codes_ms) / 1e3
-    alg_bytes = n_elem * 13.0
-    achieved = alg_bytes / codes_avg / 1e9
+    n_local = x.numel()
+    alg = 4.0 + 4.0 * cr
+    cs = np.mean(np.array(c_stage), axis=0)
+    ds = np.mean(np.array(d_stage), axis=0)
+    names_c = codec.stage_names_compress
+    names_d = codec.stage_names_decompress
+    ic, id_ = int(np.argmax(cs)), int(np.argmax(ds))
+
+    def roof(ms, what):
+        ach = alg * n_local / (ms / 1e3) / 1e9
+        return {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                "kernel": what, "ms": ms, "alg_bytes_per_elem": alg, "peak_kind": peak_kind}
+
     traffic = None
     tr_path = os.path.join(ROOT, "profiles", "traffic_latest.json")
     if os.path.exists(tr_path):
         try:
-            traffic = json.load(open(tr_path)).get("k_compress_ws_bytes_per_launch")
+            traffic = json.load(open(tr_path)).get("compress_dominant_bytes_per_launch")
         except Exception:
             traffic = None
+    roof_c = roof(float(cs[ic]), names_c[ic])
+    roof_c["traffic"] = traffic
+    roof_c["pipeline"] = roof(c_step, "whole compress")
+    roof_d = roof(float(ds[id_]), names_d[id_])
+    roof_d["pipeline"] = roof(d_step, "whole decompress")
 
-    cpu_base = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    # CPU baseline + parity on the same sample (rank 0, N = 1): the oracle
+    # restatement of the reference path on all host cores, and the CUDA path
+    # on the identical sample -- containers must be byte-identical
+    cpu_base, parity = None, None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and xs_host is not None:
+        threads = os.cpu_count() or 1
         try:
-            xs = x.cpu().numpy()
-            threads = os.cpu_count() or 1
-            dt, _ = cpu_reference_time(xs, args.eps, args.repair, reps=3, threads=threads)
-            cpu_base = {"value": xs.nbytes / dt / 1e9, "unit": "GB/s", "cores": threads, "kind": "port",
-                        "sample": "full C2 field x3 compressions (oracle restatement, OpenMP over blocks)"}
-        except Exception as ex:  # the CPU baseline is reported, never required
-            cpu_base = {"value": None, "unit": "GB/s", "cores": os.cpu_count(), "kind": "port",
-                        "sample": f"failed: {ex!r}"}
+            ts, ref, rinfo = oracle_compress_time(xs_host, args.eps, 2, threads)
+            cpu_base = {"value": xs_host.nbytes / min(ts) / 1e9, "unit": "GB/s", "cores": threads, "kind": "port",
+                        "sample": f"first 1/{SAMPLE_FRACTION} of the block-rows ({xs_host.shape[0]}x{xs_host.shape[1]}"
+                                  f" f32, {xs_host.nbytes / 2**20:.0f} MiB), oracle restatement, OpenMP over blocks, "
+                                  "best of 2"}
+            gbuf, ginfo = codec.compress_device(torch.from_numpy(xs_host).to(dev), cfg)
+            g = gbuf.cpu().numpy().tobytes()
+            a, b = np.frombuffer(g, np.uint8), np.frombuffer(ref, np.uint8)
+            n = min(a.size, b.size)
+            parity = {"sample": "the CPU sample above", "container_identical": g == ref,
+                      "differing_bytes": int((a[:n] != b[:n]).sum()) + abs(a.size - b.size),
+                      "m": [ginfo.m, rinfo["m"]], "balance_count": [ginfo.nbal, rinfo["nbal"]],
+                      "repairs": [ginfo.nrepair, rinfo["nrepair"]],
+                      "cr_delta": (len(g) - len(ref)) / len(ref)}
+        except Exception as ex:  # reported, never required
+            cpu_base = {"value": None, "unit": "GB/s", "cores": threads, "kind": "port", "sample": f"failed: {ex!r}"}
 
     clocks = sampler.summary()
     if rank == 0:
-        single = {"value": comp_gbs, "unit": "GB/s", "ms_per_step": c_tot / K,
-                  "l2": "flushed between steps (256 MiB write)"}
-        value, ms_step = comp_gbs, c_tot / K
-        if pipe is not None:
-            ms_step = pipe_ms_max / K
-            value = bytes_all / (ms_step / 1e3) / 1e9
-            launches = launches_pipe + K * DECOMPRESS_LAUNCHES
         line = {
-            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": K,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "metric": METRIC, "value": comp_gbs, "unit": "GB/s", "n_gpus": world, "steps": K,
+            "warmup": args.warmup, "ms_per_step": c_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "C2: 1800x3600 f32 exp(GRF k^-3), 30% sign-flipped; PW_REL 1e-2, repair 1.0; "
-                                   "per rank one C2-sized shard of the stacked field",
-                       "block": "256x256", "partition_rows": 32, "model": "init_model (Lorenzo)",
-                       "l2": ("inputs rotate over 8 distinct resident copies (208 MB > 126 MB L2), each step "
-                              "copies its field into the slot's input buffer (counted)") if pipe is not None
-                       else "flushed between steps (256 MiB write), inputs < L2",
-                       "pipeline": ((f"{pipe['depth']} fields in flight per rank (streams; staged stages with the "
-                                     "NCCL histogram all-reduces on each field's stream)") if sharded else
-                                    (f"{pipe['depth']} fields in flight (streams + captured graphs); "
-                                     "single_stream = one at a time")) if pipe is not None else "one at a time",
-                       "parallelism": f"shard{world}" if world > 1 else "single"},
-            "single_stream": single,
-            "compression_ratio": cr, "max_rel_err": max_rel, "m": infok.m,
-            "decompress": ({"value": bytes_all / (dpipe["ms"] / K / 1e3) / 1e9, "unit": "GB/s",
-                            "ms_per_step": dpipe["ms"] / K,
-                            "pipeline": f"{dpipe['depth']} containers in flight (streams, enqueue/result API)",
-                            "single_stream": {"value": dec_gbs, "unit": "GB/s", "ms_per_step": d_tot / K},
-                            "e2e": {"value": e2e_dp, "unit": "GB/s", "api": f"PipelinedDecompressor depth {args.e2e_pipeline}",
-                                    "h2d_bytes_per_step": int(info.nbytes), "d2h_bytes_per_step": int(n_elem * 4)},
-                            "e2e_serial": {"value": e2e_d, "unit": "GB/s"}} if dpipe is not None else
-                           {"value": dec_gbs, "unit": "GB/s", "ms_per_step": d_tot / K,
-                            "e2e": {"value": e2e_d, "unit": "GB/s"}}),
-            "e2e": {"value": e2e_c, "unit": "GB/s", "h2d_bytes_per_step": int(n_elem * 4),
-                    "d2h_bytes_per_step": int(info.nbytes),
-                    "api": (f"PipelinedCompressor depth {args.e2e_pipeline}" if world == 1 and args.e2e_pipeline > 1
-                            else "GraphedCompressor / compress_staged, one at a time")},
-            "e2e_serial": e2e_serial,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": traffic, "kernel": "k_compress_ws (codes stage)",
-                         "peak_kind": peak_kind,
-                         "alg_bytes_per_elem": 13.0},
+            "config": {"workload": workload(args.config, args.eps),
+                       "l2": "input 8 GiB >> 126 MB L2 (no flush needed), one field at a time",
+                       "parallelism": f"shard{world} (whole block-rows)" if world > 1 else "single"},
+            "compression_ratio": cr, "max_rel_err": max_rel, "m": info.m,
+            "decompress": {"value": dec_gbs, "unit": "GB/s", "ms_per_step": d_step, "roofline": roof_d,
+                           "e2e": e2e_d},
+            "e2e": e2e_c,
+            "roofline": roof_c,
+            "stages_ms": {"compress": dict(zip(names_c, cs.tolist())), "decompress": dict(zip(names_d, ds.tolist()))},
+            "parity": parity,
             "cpu_baseline": cpu_base,
             "gpu_launches": launches,
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if sharded:
         dist.destroy_process_group()
     return 0
 

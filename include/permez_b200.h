@@ -240,6 +240,9 @@ PMZ_API int pmz_decompress_enqueue(const uint8_t *d_buf, uint64_t n, const pmz_h
                                    const uint64_t *d_block_offsets, float *d_out, void *d_ws, uint64_t ws_bytes,
                                    void *stream);
 PMZ_API int pmz_decompress_result(const pmz_header *hdr, void *d_ws, uint64_t ws_bytes, void *stream);
+/* pmz_decompress_result that also reports the kernels this library ran for
+ * the call (res->launches, counted on the device) and nblocks / m. */
+PMZ_API int pmz_decompress_status(const pmz_header *hdr, void *d_ws, uint64_t ws_bytes, void *stream, pmz_result *res);
 /* pmz_decompress_enqueue split at the numpy fixup point: _prepare parses the
  * block records and derives the per-block parameters (+ decode tables);
  * pmz_decompress_np_fixups / _np_apply as for compression; _run decodes and

@@ -101,6 +101,7 @@ _SIGS = {
     "pmz_compress_np_fixups": (c_int64, [ctypes.POINTER(Geom), ctypes.POINTER(Params), VP, c_uint64, VP, VP, c_int64]),
     "pmz_compress_np_apply": (c_int32, [ctypes.POINTER(Geom), ctypes.POINTER(Params), VP, c_uint64, VP, VP, c_int64]),
     "pmz_decompress_prepare": (c_int32, [VP, c_uint64, ctypes.POINTER(Header), c_double, VP, VP, c_uint64, VP]),
+    "pmz_decompress_status": (c_int32, [ctypes.POINTER(Header), VP, c_uint64, VP, ctypes.POINTER(Result)]),
     "pmz_decompress_run": (c_int32, [VP, c_uint64, ctypes.POINTER(Header), c_double, VP, VP, VP, c_uint64, VP]),
     "pmz_decompress_np_fixups": (c_int64, [ctypes.POINTER(Header), VP, c_uint64, VP, VP, c_int64]),
     "pmz_decompress_np_apply": (c_int32, [ctypes.POINTER(Header), c_double, VP, c_uint64, VP, VP, c_int64]),

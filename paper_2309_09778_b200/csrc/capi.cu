@@ -795,6 +795,27 @@ int pmz_decompress_result(const pmz_header *hdr, void *d_ws, uint64_t ws_bytes, 
   return PMZ_OK;
 }
 
+int pmz_decompress_status(const pmz_header *hdr, void *d_ws, uint64_t ws_bytes, void *stream, pmz_result *res) {
+  Geom G = hdr_geom(hdr);
+  DecLayout L = dec_layout(G);
+  if (ws_bytes < L.total) return PMZ_ERR_WORKSPACE;
+  cudaStream_t st = (cudaStream_t)stream;
+  WsStatus hs;
+  CK(cudaMemcpyAsync(&hs, at<WsStatus>(d_ws, L.status), sizeof(WsStatus), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  if (res) {
+    memset(res, 0, sizeof(*res));
+    res->nblocks = (uint64_t)G.nblocks;
+    res->m = (int32_t)hdr->m;
+    res->unresolved = hs.unresolved;
+    res->launches = hs.launches;
+  }
+  const int s = err_from_bits(hs.err_bits);
+  if (s) return s;
+  if (hs.unresolved) return PMZ_ERR_UNRESOLVED_ROUNDING;
+  return PMZ_OK;
+}
+
 int pmz_decompress(const uint8_t *d_buf, uint64_t n, const pmz_header *hdr, double b_a, const uint64_t *d_boff,
                    float *d_out, void *d_ws, uint64_t ws_bytes, void *stream) {
   const int s = pmz_decompress_enqueue(d_buf, n, hdr, b_a, d_boff, d_out, d_ws, ws_bytes, stream);

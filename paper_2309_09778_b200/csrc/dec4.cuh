@@ -743,6 +743,7 @@ __global__ void __launch_bounds__(128) k_gather_1d(const uint8_t *__restrict__ b
                                                   const unsigned long long *__restrict__ blk_nbal, int center,
                                                   double two_ba, const uint16_t *__restrict__ codes,
                                                   double *__restrict__ vtile, WsStatus *st) {
+  count_launch(st);
   const int lane = threadIdx.x & 31;
   const int64_t p = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
   if (p >= g.nparts) return;

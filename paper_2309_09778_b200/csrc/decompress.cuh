@@ -46,6 +46,7 @@ __global__ void k_dec_blocks(const uint8_t *__restrict__ buf, unsigned long long
                              unsigned long long *part_bits, unsigned long long *part_off, double *anchors,
                              unsigned long long *bal_off, unsigned long long *pay_off,
                              unsigned long long *blk_nbal, WsStatus *st, pmz_np_fix *npfix) {
+  count_launch(st);
   const int lane = threadIdx.x & 31;
   const int64_t b = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (b >= g.nblocks) return;
@@ -128,6 +129,7 @@ __global__ void k_dec_blocks(const uint8_t *__restrict__ buf, unsigned long long
 // D2: canonical decode tables from the header's code lengths.
 __global__ void __launch_bounds__(1024) k_dec_tables(const uint8_t *__restrict__ lens, int m, DecTab *tab,
                                                      uint16_t *sym, unsigned *lut, WsStatus *st) {
+  count_launch(st);
   __shared__ unsigned cnt[34];
   __shared__ unsigned fill[34];
   const int n = 1 << m;

@@ -598,6 +598,7 @@ __global__ void __launch_bounds__(256) k_stats(const float *__restrict__ x, Geom
 // the host's np.log2 values for the listed blocks -> re-derived parameters
 __global__ void k_np_apply(const pmz_np_fix *__restrict__ fix, long long n, double eps0, double b_a, BlkP *blkp,
                            WsStatus *st) {
+  count_launch(st);
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const pmz_np_fix e = fix[i];

@@ -332,8 +332,19 @@ class Codec:
                                    offs.ctypes.data_as(ctypes.c_void_p)), "read_container")
         return offs
 
+    # stage names of the ``events`` of compress_staged / decompress_device
+    stage_names_compress = ("analyze (block stats, numpy fixups, forward map, coverage)",
+                            "codes (select_m, compress_block + verify_and_repair)",
+                            "finish (codebook, encode, container)")
+    stage_names_decompress = ("prepare (block records, parameters, decode tables)",
+                              "run (decode, decompress_block, inverse map)")
+    last_decompress_launches = 0
+
     def decompress_device(self, d_buf: torch.Tensor, h: N.Header, d_offsets: torch.Tensor,
-                          out: torch.Tensor | None = None) -> torch.Tensor:
+                          out: torch.Tensor | None = None, events=None) -> torch.Tensor:
+        """decompress_block of every block + inverse map into a float32 CUDA
+        grid.  ``events`` (3 CUDA events) time the prepare and run stages on
+        the launching stream."""
         lib = self.lib
         wsz = ctypes.c_uint64(0)
         check(lib.pmz_decompress_workspace_size(ctypes.byref(h), ctypes.byref(wsz)), "workspace")
@@ -342,12 +353,21 @@ class Codec:
             out = torch.empty((int(h.rows), int(h.cols)), dtype=torch.float32, device=self.device)
         stream = _stream_ptr(self.device)
         b_a = host_b_a(h.b_r)
+        if events is not None:
+            events[0].record()
         check(lib.pmz_decompress_prepare(_ptr(d_buf), d_buf.numel(), ctypes.byref(h), b_a, _ptr(d_offsets), _ptr(ws),
                                          ws.numel(), stream), "decompress")
         check(min(self.np_fix_decompress(h, ws, stream), 0), "np_fixups")
+        if events is not None:
+            events[1].record()
         check(lib.pmz_decompress_run(_ptr(d_buf), d_buf.numel(), ctypes.byref(h), b_a, _ptr(d_offsets), _ptr(out),
                                      _ptr(ws), ws.numel(), stream), "decompress")
-        check(lib.pmz_decompress_result(ctypes.byref(h), _ptr(ws), ws.numel(), stream), "decompress")
+        if events is not None:
+            events[2].record()
+        res = N.Result()
+        check(lib.pmz_decompress_status(ctypes.byref(h), _ptr(ws), ws.numel(), stream, ctypes.byref(res)),
+              "decompress")
+        self.last_decompress_launches = int(res.launches)
         return out
 
 
