@@ -265,11 +265,11 @@ def main():
             if sharded:
                 dist.barrier()
             torch.cuda.synchronize()
-            ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(codec.stage_names_compress) + 1)]
             bufk, infok = compress_once(ev)  # synchronises (status read-back)
             torch.cuda.synchronize()
-            c_ms.append(ev[0].elapsed_time(ev[3]))
-            c_stage.append([ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]), ev[2].elapsed_time(ev[3])])
+            c_ms.append(ev[0].elapsed_time(ev[-1]))
+            c_stage.append([ev[i].elapsed_time(ev[i + 1]) for i in range(len(ev) - 1)])
             launches += infok.launches
             if sharded:
                 dist.barrier()

@@ -185,17 +185,30 @@ PMZ_API uint64_t *pmz_ws_histogram(void *d_ws, const pmz_params *p, const pmz_ge
  * d_out[0] when write_header != 0 and this shard's block records right after
  * it (or at d_out[0] when write_header == 0).  Synchronises `stream` and fills
  * *res.  Returns PMZ_ERR_CAPACITY (res filled with the required sizes) when
- * out_cap is too small. */
-PMZ_API int pmz_compress_finish(const pmz_geom *g, const pmz_params *p, int write_header, uint8_t *d_out, uint64_t out_cap,
-                        uint64_t *d_block_offsets, void *d_ws, uint64_t ws_bytes, void *stream, pmz_result *res);
+ * out_cap is too small (call pmz_compress_write_async again with a larger
+ * buffer: the encoded state stays in the workspace).  d_in: the shard's input
+ * (the throughput path codes every block after the codebook). */
+PMZ_API int pmz_compress_finish(const float *d_in, const pmz_geom *g, const pmz_params *p, int write_header,
+                                uint8_t *d_out, uint64_t out_cap, uint64_t *d_block_offsets, void *d_ws,
+                                uint64_t ws_bytes, void *stream, pmz_result *res);
 
-/* pmz_compress_finish split for stream capture (CUDA graphs): _async only
- * enqueues (the writers read m, sizes and the capacity verdict from the
- * device status; nothing is written on error); _result synchronises `stream`,
- * fills *res and returns the status (wrote_output = d_out was non-null). */
-PMZ_API int pmz_compress_finish_async(const pmz_geom *g, const pmz_params *p, int write_header, uint8_t *d_out,
-                                      uint64_t out_cap, uint64_t *d_block_offsets, void *d_ws, uint64_t ws_bytes,
-                                      void *stream);
+/* Stage 3 in two parts: pmz_compress_encode = build_codebook + (throughput
+ * path) compress_block / verify_and_repair of every block with the final
+ * codebook, or (latency path) the per-partition payload bits;
+ * pmz_compress_write_async = record sizes and offsets, header, block records,
+ * block index.  pmz_compress_finish_async = both, enqueue only (stream
+ * capture: the writers read m, sizes and the capacity verdict from the device
+ * status; nothing is written on error); pmz_compress_result synchronises
+ * `stream`, fills *res and returns the status (wrote_output = d_out was
+ * non-null). */
+PMZ_API int pmz_compress_encode(const float *d_in, const pmz_geom *g, const pmz_params *p, void *d_ws,
+                                uint64_t ws_bytes, void *stream);
+PMZ_API int pmz_compress_write_async(const pmz_geom *g, const pmz_params *p, int write_header, uint8_t *d_out,
+                                     uint64_t out_cap, uint64_t *d_block_offsets, void *d_ws, uint64_t ws_bytes,
+                                     void *stream);
+PMZ_API int pmz_compress_finish_async(const float *d_in, const pmz_geom *g, const pmz_params *p, int write_header,
+                                      uint8_t *d_out, uint64_t out_cap, uint64_t *d_block_offsets, void *d_ws,
+                                      uint64_t ws_bytes, void *stream);
 PMZ_API int pmz_compress_result(const pmz_geom *g, const pmz_params *p, int wrote_output, void *d_ws,
                                 uint64_t ws_bytes, void *stream, pmz_result *res);
 

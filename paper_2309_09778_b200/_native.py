@@ -68,10 +68,13 @@ _SIGS = {
     "pmz_compress_codes": (c_int32, [VP, ctypes.POINTER(Geom), ctypes.POINTER(Params), VP, c_int64, VP, c_uint64,
                                      VP]),
     "pmz_ws_histogram": (VP, [VP, ctypes.POINTER(Params), ctypes.POINTER(Geom)]),
-    "pmz_compress_finish": (c_int32, [ctypes.POINTER(Geom), ctypes.POINTER(Params), c_int32, VP, c_uint64, VP, VP,
-                                      c_uint64, VP, ctypes.POINTER(Result)]),
-    "pmz_compress_finish_async": (c_int32, [ctypes.POINTER(Geom), ctypes.POINTER(Params), c_int32, VP, c_uint64, VP,
-                                            VP, c_uint64, VP]),
+    "pmz_compress_finish": (c_int32, [VP, ctypes.POINTER(Geom), ctypes.POINTER(Params), c_int32, VP, c_uint64, VP,
+                                      VP, c_uint64, VP, ctypes.POINTER(Result)]),
+    "pmz_compress_finish_async": (c_int32, [VP, ctypes.POINTER(Geom), ctypes.POINTER(Params), c_int32, VP, c_uint64,
+                                            VP, VP, c_uint64, VP]),
+    "pmz_compress_encode": (c_int32, [VP, ctypes.POINTER(Geom), ctypes.POINTER(Params), VP, c_uint64, VP]),
+    "pmz_compress_write_async": (c_int32, [ctypes.POINTER(Geom), ctypes.POINTER(Params), c_int32, VP, c_uint64, VP,
+                                           VP, c_uint64, VP]),
     "pmz_compress_result": (c_int32, [ctypes.POINTER(Geom), ctypes.POINTER(Params), c_int32, VP, c_uint64, VP,
                                       ctypes.POINTER(Result)]),
     "pmz_compress_enqueue": (c_int32, [VP, ctypes.POINTER(Geom), ctypes.POINTER(Params), VP, c_int64, c_int32, VP,

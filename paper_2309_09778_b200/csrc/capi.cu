@@ -18,6 +18,8 @@
 #include "dec4.cuh"
 #include "train.cuh"
 #include "segy.cuh"
+#include "tdec.cuh"
+#include "tcmp.cuh"
 
 using namespace pmz;
 
@@ -166,6 +168,44 @@ int launch_check() {
 
 constexpr int kNT = 256;
 
+// every block is one partition of one row (1-D inputs, block_rows == 1)
+bool one_row_parts(const Geom &G) { return G.br == 1 || G.rows == 1; }
+
+// Throughput path (tdec.cuh / tcmp.cuh) or latency path (dec4/dsc, fwdq/wsc):
+// the throughput kernels need partition-level parallelism only, the latency
+// kernels also split each partition's work across a CTA.  PMZ_PATH=latency |
+// throughput overrides the size rule (tests exercise both on small fields).
+bool use_tpath(const Geom &G) {
+  if (one_row_parts(G)) return false;
+  const char *e = getenv("PMZ_PATH");
+  if (e && e[0] == 'l') return false;
+  if (e && e[0] == 't') return true;
+  return G.nparts >= kTputMinParts;
+}
+
+// the throughput-path views of the compress workspace: final codes (raster,
+// tcode_base) in rqbuf, per-row balance lists in vbuf, per-row {bits, count} in clsbuf
+template <int PK, int MODE>
+void launch_tmain(const float *x, const Geom &G, const KParams &k, const int64_t *d_val, int64_t n_val, void *d_ws,
+                  const WsLayout &L, cudaStream_t st) {
+  unsigned grid;
+  if (MODE == kTMain) grid = (unsigned)((G.nparts + kTCW - 1) / kTCW);
+  else grid = (unsigned)(n_val * ((G.np_full + kTCW - 1) / kTCW));
+  if (grid == 0) return;
+  cudaFuncSetAttribute(k_t_main<PK, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTCmpSmem);
+  k_t_main<PK, MODE><<<grid, kTCW * 32, kTCmpSmem, st>>>(
+      x, G, k, at<BlkP>(d_ws, L.blkp), at<WsStatus>(d_ws, L.status), d_val, n_val, at<uint16_t>(d_ws, L.rqbuf),
+      at<double>(d_ws, L.vbuf), at<unsigned>(d_ws, L.clsbuf), at<double>(d_ws, L.anchors),
+      at<unsigned long long>(d_ws, L.part_bits), at<unsigned long long>(d_ws, L.part_zeros),
+      at<uint8_t>(d_ws, L.lens), at<unsigned long long>(d_ws, L.hist), at<unsigned long long>(d_ws, L.cov));
+}
+template <int MODE>
+void launch_tmain_pk(const float *x, const Geom &G, const KParams &k, const int64_t *d_val, int64_t n_val,
+                     void *d_ws, const WsLayout &L, cudaStream_t st) {
+  if (k.init_model == 3) launch_tmain<3, MODE>(x, G, k, d_val, n_val, d_ws, L, st);
+  else launch_tmain<0, MODE>(x, G, k, d_val, n_val, d_ws, L, st);
+}
+
 template <int PK>
 int launch_ws(const KParams &k, unsigned grid, cudaStream_t st, const float *x, const Geom &G, void *d_ws,
               const WsLayout &L) {
@@ -283,6 +323,12 @@ int pmz_compress_transform(const float *d_in, const pmz_geom *g, const pmz_param
   if (n_val > 0)
     k_mark_val<<<(unsigned)((n_val + 255) / 256), 256, 0, st>>>(d_val, n_val, G.nblocks, at<uint8_t>(d_ws, L.vflag),
                                                                at<WsStatus>(d_ws, L.status));
+  if (use_tpath(G)) {
+    // throughput path: only the coverage of the validation blocks' TRUE
+    // residuals here (select_m); the forward map runs fused in k_t_main
+    if (k.m_fixed == 0 && n_val > 0) launch_tmain_pk<kTCoverage>(d_in, G, k, d_val, n_val, d_ws, L, st);
+    return launch_check();
+  }
   // forward map + m-independent TRUE-surface quantization of every element,
   // coverage of the validation blocks in the same pass
   if (G.nparts > 0) {
@@ -359,6 +405,12 @@ int pmz_compress_codes(const float *d_in, const pmz_geom *g, const pmz_params *p
   cudaStream_t st = (cudaStream_t)stream;
   KParams k = kparams(p);
   k_select_m<<<1, 32, 0, st>>>(at<unsigned long long>(d_ws, L.cov), k, at<WsStatus>(d_ws, L.status));
+  if (use_tpath(G)) {
+    // throughput path: the validation blocks' final codes -> histogram
+    // (estimate_codebook); every block is coded after the codebook
+    if (n_val > 0) launch_tmain_pk<kTValCodes>(d_in, G, k, d_val, n_val, d_ws, L, st);
+    return launch_check();
+  }
   if (G.nparts > 0) {
     const unsigned grid = (unsigned)((G.nparts + kPPC - 1) / kPPC);
     if (k.init_model == 3) s = launch_ws<3>(k, grid, st, d_in, G, d_ws, L);
@@ -388,9 +440,8 @@ __global__ void k_finish_status(Geom g, KParams k, int write_header, const unsig
   if (st->total_bytes > cap) atomicOr(&st->err_bits, 1u << (-PMZ_ERR_CAPACITY));
 }
 
-int pmz_compress_finish_async(const pmz_geom *g, const pmz_params *p, int write_header, uint8_t *d_out,
-                              uint64_t out_cap, uint64_t *d_block_offsets, void *d_ws, uint64_t ws_bytes,
-                              void *stream) {
+int pmz_compress_encode(const float *d_in, const pmz_geom *g, const pmz_params *p, void *d_ws, uint64_t ws_bytes,
+                        void *stream) {
   int s = check_params(p);
   if (s) return s;
   Geom G = geom_of(p, g);
@@ -404,10 +455,29 @@ int pmz_compress_finish_async(const pmz_geom *g, const pmz_params *p, int write_
                                        at<unsigned long long>(d_ws, L.cb_keys), at<unsigned long long>(d_ws, L.cb_w),
                                        at<unsigned>(d_ws, L.cb_parent), at<uint8_t>(d_ws, L.lens),
                                        at<unsigned>(d_ws, L.cw));
-  if (G.nparts > 0)
-    k_part_bits<<<(unsigned)G.nparts, kPbW * 32, 0, st>>>(G, at<BlkP>(d_ws, L.blkp), at<int16_t>(d_ws, L.rqbuf),
-                                                         at<uint8_t>(d_ws, L.lens),
-                                                         at<unsigned long long>(d_ws, L.part_bits), S);
+  if (G.nparts > 0) {
+    if (use_tpath(G)) {
+      launch_tmain_pk<kTMain>(d_in, G, k, nullptr, 0, d_ws, L, st);
+    } else {
+      k_part_bits<<<(unsigned)G.nparts, kPbW * 32, 0, st>>>(G, at<BlkP>(d_ws, L.blkp), at<int16_t>(d_ws, L.rqbuf),
+                                                           at<uint8_t>(d_ws, L.lens),
+                                                           at<unsigned long long>(d_ws, L.part_bits), S);
+    }
+  }
+  return launch_check();
+}
+
+int pmz_compress_write_async(const pmz_geom *g, const pmz_params *p, int write_header, uint8_t *d_out,
+                             uint64_t out_cap, uint64_t *d_block_offsets, void *d_ws, uint64_t ws_bytes,
+                             void *stream) {
+  int s = check_params(p);
+  if (s) return s;
+  Geom G = geom_of(p, g);
+  WsLayout L = compress_layout(G);
+  if (ws_bytes < L.total) return PMZ_ERR_WORKSPACE;
+  cudaStream_t st = (cudaStream_t)stream;
+  KParams k = kparams(p);
+  WsStatus *S = at<WsStatus>(d_ws, L.status);
   k_block_sizes<<<(unsigned)((G.nblocks + 1 + 255) / 256), 256, 0, st>>>(
       G, at<BlkP>(d_ws, L.blkp), at<unsigned long long>(d_ws, L.part_bits),
       at<unsigned long long>(d_ws, L.part_zeros), at<unsigned long long>(d_ws, L.rec_size), S);
@@ -420,7 +490,13 @@ int pmz_compress_finish_async(const pmz_geom *g, const pmz_params *p, int write_
   if (d_out != nullptr) {
     if (write_header)
       k_write_header<<<1, 256, 0, st>>>(d_out, G, k, g->global_rows, at<uint8_t>(d_ws, L.lens), S);
-    if (G.nparts > 0) {
+    if (G.nparts > 0 && use_tpath(G)) {
+      k_t_write<<<(unsigned)((G.nparts + kTCW - 1) / kTCW), kTCW * 32, 0, st>>>(
+          G, at<BlkP>(d_ws, L.blkp), at<uint16_t>(d_ws, L.rqbuf), at<double>(d_ws, L.vbuf),
+          at<unsigned>(d_ws, L.clsbuf), at<double>(d_ws, L.anchors), at<unsigned long long>(d_ws, L.part_bits),
+          at<unsigned long long>(d_ws, L.part_zeros), at<unsigned long long>(d_ws, L.rec_off),
+          at<uint8_t>(d_ws, L.lens), at<unsigned>(d_ws, L.cw), d_out, S);
+    } else if (G.nparts > 0) {
       k_write_part<<<(unsigned)G.nparts, kWT, kWpSmem, st>>>(
           G, at<BlkP>(d_ws, L.blkp), at<int16_t>(d_ws, L.rqbuf), at<double>(d_ws, L.vbuf),
           at<double>(d_ws, L.anchors), at<unsigned long long>(d_ws, L.part_bits),
@@ -432,6 +508,14 @@ int pmz_compress_finish_async(const pmz_geom *g, const pmz_params *p, int write_
           G, k, write_header, at<unsigned long long>(d_ws, L.rec_off), S, (unsigned long long *)d_block_offsets);
   }
   return launch_check();
+}
+
+int pmz_compress_finish_async(const float *d_in, const pmz_geom *g, const pmz_params *p, int write_header,
+                              uint8_t *d_out, uint64_t out_cap, uint64_t *d_block_offsets, void *d_ws,
+                              uint64_t ws_bytes, void *stream) {
+  const int s = pmz_compress_encode(d_in, g, p, d_ws, ws_bytes, stream);
+  if (s) return s;
+  return pmz_compress_write_async(g, p, write_header, d_out, out_cap, d_block_offsets, d_ws, ws_bytes, stream);
 }
 
 int pmz_compress_result(const pmz_geom *g, const pmz_params *p, int wrote_output, void *d_ws, uint64_t ws_bytes,
@@ -471,9 +555,11 @@ int pmz_compress_result(const pmz_geom *g, const pmz_params *p, int wrote_output
   return PMZ_OK;
 }
 
-int pmz_compress_finish(const pmz_geom *g, const pmz_params *p, int write_header, uint8_t *d_out, uint64_t out_cap,
-                        uint64_t *d_block_offsets, void *d_ws, uint64_t ws_bytes, void *stream, pmz_result *res) {
-  int s = pmz_compress_finish_async(g, p, write_header, d_out, out_cap, d_block_offsets, d_ws, ws_bytes, stream);
+int pmz_compress_finish(const float *d_in, const pmz_geom *g, const pmz_params *p, int write_header, uint8_t *d_out,
+                        uint64_t out_cap, uint64_t *d_block_offsets, void *d_ws, uint64_t ws_bytes, void *stream,
+                        pmz_result *res) {
+  int s = pmz_compress_finish_async(d_in, g, p, write_header, d_out, out_cap, d_block_offsets, d_ws, ws_bytes,
+                                    stream);
   if (s) return s;
   return pmz_compress_result(g, p, d_out != nullptr, d_ws, ws_bytes, stream, res);
 }
@@ -485,7 +571,8 @@ int pmz_compress_enqueue(const float *d_in, const pmz_geom *g, const pmz_params 
   if (s) return s;
   s = pmz_compress_codes(d_in, g, p, d_val, n_val, d_ws, ws_bytes, stream);
   if (s) return s;
-  return pmz_compress_finish_async(g, p, write_header, d_out, out_cap, d_block_offsets, d_ws, ws_bytes, stream);
+  return pmz_compress_finish_async(d_in, g, p, write_header, d_out, out_cap, d_block_offsets, d_ws, ws_bytes,
+                                   stream);
 }
 
 int pmz_compress(const float *d_in, const pmz_geom *g, const pmz_params *p, const int64_t *d_val, int64_t n_val,
@@ -495,7 +582,7 @@ int pmz_compress(const float *d_in, const pmz_geom *g, const pmz_params *p, cons
   if (s) return s;
   s = pmz_compress_codes(d_in, g, p, d_val, n_val, d_ws, ws_bytes, stream);
   if (s) return s;
-  return pmz_compress_finish(g, p, 1, d_out, out_cap, d_block_offsets, d_ws, ws_bytes, stream, res);
+  return pmz_compress_finish(d_in, g, p, 1, d_out, out_cap, d_block_offsets, d_ws, ws_bytes, stream, res);
 }
 
 // ---------------------------------------------------------------------------
@@ -608,11 +695,10 @@ int pmz_index_blocks(const uint8_t *h, uint64_t n, const pmz_header *hd, uint64_
 // decompression
 
 namespace {
-// every block is one partition of one row (1-D inputs, block_rows == 1)
-bool one_row_parts(const Geom &G) { return G.br == 1 || G.rows == 1; }
 struct DecLayout {
   size_t status, blkp, part_bits, part_off, zflag, anchors, bal_off, pay_off, blk_nbal, tab, sym, lut, npfix, codes,
-      vtile, total;
+      vtile, rowz, total;
+  bool tpath;
 };
 DecLayout dec_layout(const Geom &g) {
   DecLayout L{};
@@ -635,8 +721,16 @@ DecLayout dec_layout(const Geom &g) {
   L.sym = take(2 * kMaxAlpha);
   L.lut = take(4ull * ((1u << kLutBits) + kLut2Max));            // first + second level
   L.npfix = take(sizeof(pmz_np_fix) * (size_t)(g.nblocks + 1));
-  L.codes = take(2 * (size_t)g.nparts * (size_t)g.nct * kTile);  // partition-tiled
-  L.vtile = take(8 * (size_t)g.nparts * (size_t)g.nct * kTile);   // per-element addends, then reconstructed values
+  L.tpath = use_tpath(g);
+  if (L.tpath) {
+    L.codes = take(2 * (size_t)g.nparts * (size_t)g.prow * (size_t)g.bc);  // raster per partition (tcode_base)
+    L.rowz = take(2 * (size_t)g.nparts * (size_t)g.prow + 2);
+    L.vtile = o;
+  } else {
+    L.codes = take(2 * (size_t)g.nparts * (size_t)g.nct * kTile);  // partition-tiled
+    L.vtile = take(8 * (size_t)g.nparts * (size_t)g.nct * kTile);   // per-element addends, then reconstructed values
+    L.rowz = o;
+  }
   L.total = o;
   return L;
 }
@@ -739,6 +833,29 @@ int pmz_decompress_run(const uint8_t *d_buf, uint64_t n, const pmz_header *hdr, 
   cudaStream_t st = (cudaStream_t)stream;
   KParams k = hdr_kparams(hdr, b_a);
   WsStatus *S = at<WsStatus>(d_ws, L.status);
+  if (G.nblocks > 0 && L.tpath) {
+    const int center = 1 << ((int)hdr->m - 1);
+    CK(cudaFuncSetAttribute(k_t_decode, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTDecSmem));
+    k_t_decode<<<(unsigned)((G.nparts + kTDT - 1) / kTDT), kTDT, kTDecSmem, st>>>(
+        d_buf, n, G, at<BlkP>(d_ws, L.blkp), at<DecTab>(d_ws, L.tab), at<uint16_t>(d_ws, L.sym),
+        at<unsigned>(d_ws, L.lut), at<unsigned long long>(d_ws, L.part_bits), at<unsigned long long>(d_ws, L.part_off),
+        at<unsigned long long>(d_ws, L.pay_off), 1 << (int)hdr->m, at<uint16_t>(d_ws, L.codes),
+        at<unsigned>(d_ws, L.zflag), S);
+    const unsigned grid = (unsigned)((G.nparts + kTRW - 1) / kTRW);
+#define PMZ_T_RECON(PKV)                                                                                            \
+  do {                                                                                                              \
+    CK(cudaFuncSetAttribute(k_t_recon<PKV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTRecSmem));          \
+    k_t_recon<PKV><<<grid, kTRW * 32, kTRecSmem, st>>>(                                                             \
+        d_buf, n, G, k, at<BlkP>(d_ws, L.blkp), at<uint16_t>(d_ws, L.codes), at<unsigned>(d_ws, L.zflag),           \
+        at<double>(d_ws, L.anchors), at<unsigned long long>(d_ws, L.bal_off),          \
+        at<unsigned long long>(d_ws, L.blk_nbal), center, d_out, S);                                                \
+  } while (0)
+    if (k.init_model == 3) PMZ_T_RECON(3);
+    else if (k.init_model == 1) PMZ_T_RECON(1);
+    else PMZ_T_RECON(0);
+#undef PMZ_T_RECON
+    return launch_check();
+  }
   if (G.nblocks > 0) {
     if (one_row_parts(G)) {
       k_decode_1d<<<(unsigned)((G.nparts + kD1T - 1) / kD1T), kD1T, 0, st>>>(

@@ -152,6 +152,14 @@ class Codec:
             lambda b, n: lib.pmz_decompress_np_apply(ctypes.byref(h), host_b_a(h.b_r), _ptr(ws), ws.numel(), stream,
                                                      b, n))
 
+    def _write(self, p, g, write_header, out, block_offsets, ws, stream, res) -> int:
+        s = self.lib.pmz_compress_write_async(ctypes.byref(g), ctypes.byref(p), int(write_header), _ptr(out),
+                                              out.numel(), _ptr(block_offsets), _ptr(ws), ws.numel(), stream)
+        if s:
+            return s
+        return self.lib.pmz_compress_result(ctypes.byref(g), ctypes.byref(p), 1, _ptr(ws), ws.numel(), stream,
+                                            ctypes.byref(res))
+
     def analyze(self, x, p, g, d_val, ws, stream):
         """Stage 1: block stats + parameters, the host's np.log2 for the
         listed blocks, then forward map + coverage (pmz_compress_stats /
@@ -198,13 +206,12 @@ class Codec:
         self.analyze(x, p, g, d_val, ws, stream)
         check(lib.pmz_compress_codes(_ptr(x), ctypes.byref(g), ctypes.byref(p), _ptr(d_val), int(d_val.numel()),
                                      _ptr(ws), ws.numel(), stream), "compress_codes")
-        s = lib.pmz_compress_finish(ctypes.byref(g), ctypes.byref(p), 1, _ptr(out), out.numel(), _ptr(block_offsets),
-                                    _ptr(ws), ws.numel(), stream, ctypes.byref(res))
-        if s == -16:  # capacity: write again into a buffer of the exact size
-            need = int(res.header_bytes + res.record_bytes)
-            out = self._buf("_out", need)
-            s = lib.pmz_compress_finish(ctypes.byref(g), ctypes.byref(p), 1, _ptr(out), out.numel(),
-                                        _ptr(block_offsets), _ptr(ws), ws.numel(), stream, ctypes.byref(res))
+        check(lib.pmz_compress_encode(_ptr(x), ctypes.byref(g), ctypes.byref(p), _ptr(ws), ws.numel(), stream),
+              "compress_encode")
+        s = self._write(p, g, 1, out, block_offsets, ws, stream, res)
+        if s == -16:  # capacity: write again into a buffer of the exact size (the encoded state is kept)
+            out = self._buf("_out", int(res.header_bytes + res.record_bytes))
+            s = self._write(p, g, 1, out, block_offsets, ws, stream, res)
         check(s, "compress")
         n = int(res.header_bytes + res.record_bytes)
         info = CompressInfo(n, int(res.header_bytes), int(res.nblocks), int(res.ntrivial), int(res.nbal),
@@ -220,8 +227,8 @@ class Codec:
         global block-row ``block_row0``).  ``allreduce(tensor)`` sums a device
         int64 tensor across shards (NCCL) between stages: the select_m coverage
         histogram and the validation-code histogram, so every shard derives the
-        same m and codebook.  ``events`` (4 CUDA events) time
-        the stages on the launching stream."""
+        same m and codebook.  ``events`` (5 CUDA events) time
+        the stages (stage_names_compress) on the launching stream."""
         if x.dtype != torch.float32 or not x.is_cuda:
             raise ConfigError("compress_staged expects a float32 CUDA tensor")
         x = x.contiguous()
@@ -261,17 +268,20 @@ class Codec:
             events[1].record()
         check(lib.pmz_compress_codes(_ptr(x), ctypes.byref(g), ctypes.byref(p), _ptr(d_val), nv, _ptr(ws),
                                      ws.numel(), stream), "compress_codes")
-        if events is not None:
-            events[2].record()
         if allreduce is not None:
             off = lib.pmz_ws_histogram(_ptr(ws), ctypes.byref(p), ctypes.byref(g)) - ws.data_ptr()
             allreduce(ws[off: off + (65536 + 1) * 8].view(torch.int64))
-        res = N.Result()
-        s = lib.pmz_compress_finish(ctypes.byref(g), ctypes.byref(p), int(write_header), _ptr(out), out.numel(),
-                                    _ptr(block_offsets), _ptr(ws), ws.numel(), stream, ctypes.byref(res))
-        check(s, "compress_finish")
+        if events is not None:
+            events[2].record()
+        check(lib.pmz_compress_encode(_ptr(x), ctypes.byref(g), ctypes.byref(p), _ptr(ws), ws.numel(), stream),
+              "compress_encode")
         if events is not None:
             events[3].record()
+        res = N.Result()
+        s = self._write(p, g, write_header, out, block_offsets, ws, stream, res)
+        check(s, "compress_finish")
+        if events is not None:
+            events[4].record()
         n = int(res.header_bytes + res.record_bytes)
         info = CompressInfo(n, int(res.header_bytes), int(res.nblocks), int(res.ntrivial), int(res.nbal),
                             int(res.nrepair), int(res.ncodes), int(res.m), int(res.max_code_len),
@@ -301,7 +311,7 @@ class Codec:
         if allreduce is not None:
             off = lib.pmz_ws_histogram(_ptr(ws), ctypes.byref(p), ctypes.byref(g)) - ws.data_ptr()
             allreduce(ws[off: off + (65536 + 1) * 8].view(torch.int64))
-        check(lib.pmz_compress_finish_async(ctypes.byref(g), ctypes.byref(p), 1, _ptr(out), out.numel(),
+        check(lib.pmz_compress_finish_async(_ptr(x), ctypes.byref(g), ctypes.byref(p), 1, _ptr(out), out.numel(),
                                             _ptr(block_offsets), _ptr(ws), ws.numel(), stream), "compress_finish")
         return p, g
 
@@ -333,9 +343,11 @@ class Codec:
         return offs
 
     # stage names of the ``events`` of compress_staged / decompress_device
-    stage_names_compress = ("analyze (block stats, numpy fixups, forward map, coverage)",
-                            "codes (select_m, compress_block + verify_and_repair)",
-                            "finish (codebook, encode, container)")
+    stage_names_compress = ("analyze (block stats, numpy fixups, select_m coverage)",
+                            "codes (select_m, validation codes / latency path: verify_and_repair)",
+                            "encode (codebook; throughput path: k_t_main = forward map + compress_block + "
+                            "verify_and_repair of every block)",
+                            "write (record sizes/offsets, header, block records)")
     stage_names_decompress = ("prepare (block records, parameters, decode tables)",
                               "run (decode, decompress_block, inverse map)")
     last_decompress_launches = 0
@@ -439,7 +451,8 @@ class GraphedCompressor:
                                          nv, _ptr(self.ws), self.ws.numel(), stream), "compress_transform")
         check(lib.pmz_compress_codes(_ptr(self.x), ctypes.byref(self.g), ctypes.byref(self.p), _ptr(self.d_val), nv,
                                      _ptr(self.ws), self.ws.numel(), stream), "compress_codes")
-        check(lib.pmz_compress_finish_async(ctypes.byref(self.g), ctypes.byref(self.p), 1, _ptr(self.out),
+        check(lib.pmz_compress_finish_async(_ptr(self.x), ctypes.byref(self.g), ctypes.byref(self.p), 1,
+                                            _ptr(self.out),
                                             self.out.numel(), _ptr(self.block_offsets), _ptr(self.ws),
                                             self.ws.numel(), stream), "compress_finish")
 

@@ -32,25 +32,49 @@ def _check_bound(x, y, bound):
     assert rel.max(initial=0.0) <= bound
 
 
+class _path:
+    """PMZ_PATH override (the library reads it at every call)."""
+
+    def __init__(self, path):
+        self.path, self.old = path, None
+
+    def __enter__(self):
+        import os
+        self.old = os.environ.get("PMZ_PATH")
+        os.environ["PMZ_PATH"] = self.path
+
+    def __exit__(self, *a):
+        import os
+        if self.old is None:
+            os.environ.pop("PMZ_PATH", None)
+        else:
+            os.environ["PMZ_PATH"] = self.old
+
+
 def _parity(codec, oracle, x, **kw):
     import paper_2309_09778_b200 as P
     ocfg = oracle.OracleConfig(**{k: v for k, v in kw.items()})
     pcfg = P.CompressConfig(rel_error=kw.get("b_r", 1e-2), repair_factor=kw.get("repair_factor", 1.5),
                             block_rows=kw.get("block_rows", 256), block_cols=kw.get("block_cols", 256),
                             partition_rows=kw.get("partition_rows", 32), m=kw.get("m", 0))
-    dbuf, info = codec.compress_device(torch.from_numpy(np.ascontiguousarray(x)).cuda(), pcfg)
-    gpu = dbuf.cpu().numpy().tobytes()
     ref, rinfo = oracle.compress(x, ocfg)
-    assert info.m == rinfo["m"]
-    assert info.nbal == rinfo["nbal"] and info.nrepair == rinfo["nrepair"]
-    if gpu != ref:
-        a, b = np.frombuffer(gpu, np.uint8), np.frombuffer(ref, np.uint8)
-        n = min(a.size, b.size)
-        d = np.nonzero(a[:n] != b[:n])[0]
-        pytest.fail(f"container mismatch: len {a.size} vs {b.size}, first diff {d[:5]}")
-    y = P.decompress(gpu, device="cuda:0")
+    xd = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    for path in ("latency", "throughput"):  # both compress paths (PMZ_PATH overrides the size rule)
+        with _path(path):
+            dbuf, info = codec.compress_device(xd, pcfg)
+        gpu = dbuf.cpu().numpy().tobytes()
+        assert info.m == rinfo["m"], path
+        assert info.nbal == rinfo["nbal"] and info.nrepair == rinfo["nrepair"], path
+        if gpu != ref:
+            a, b = np.frombuffer(gpu, np.uint8), np.frombuffer(ref, np.uint8)
+            n = min(a.size, b.size)
+            d = np.nonzero(a[:n] != b[:n])[0]
+            pytest.fail(f"{path}: container mismatch: len {a.size} vs {b.size}, first diff {d[:5]}")
     yo = oracle.decompress(ref)
-    assert np.array_equal(y.reshape(-1).view(np.uint32), yo.reshape(-1).view(np.uint32))
+    for path in ("latency", "throughput"):  # both decoders (PMZ_PATH overrides the size rule)
+        with _path(path):
+            y = P.decompress(gpu, device="cuda:0")
+        assert np.array_equal(y.reshape(-1).view(np.uint32), yo.reshape(-1).view(np.uint32)), path
     bound = kw.get("b_r", 1e-2) * kw.get("repair_factor", 1.5)
     _check_bound(x, y, bound)
     return info, len(gpu)
