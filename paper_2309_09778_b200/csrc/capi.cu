@@ -19,14 +19,18 @@
 #include "train.cuh"
 #include "segy.cuh"
 #include "tdec.cuh"
-#include "tcmp.cuh"
+#include "cmain.cuh"
 
 using namespace pmz;
 
+static int cuda_fail(cudaError_t e) {
+  if (getenv("PMZ_DEBUG")) fprintf(stderr, "permez: CUDA error: %s\n", cudaGetErrorString(e));
+  return PMZ_ERR_CUDA;
+}
 #define CK(x)                                   \
   do {                                          \
     cudaError_t e_ = (x);                       \
-    if (e_ != cudaSuccess) return PMZ_ERR_CUDA; \
+    if (e_ != cudaSuccess) return cuda_fail(e_); \
   } while (0)
 
 namespace {
@@ -105,6 +109,25 @@ KParams kparams(const pmz_params *p) {
   k.dpos_p = k.dpos + 0x1p-20;
   k.dneg_p = k.dneg - 0x1p-20;
   k.init_model = is_init_model(p->S, p->w1, p->w2);
+  // certified-rounding margins of the approximate TRUE residual (cmain.cuh):
+  // |v~ - v| < 2^-41 per surface value moves a hidden pre-activation by at most
+  // sum_k |w1_kj| 2^-41 (+ roundings) and the residual by amp 2^-41; 2^-37
+  // leaves 16x headroom over the rounding terms for |v| < 2^9
+  double amp = 1.0, hsum = 1.0;
+  for (int j = 0; j < p->H && j < 2; j++) {
+    double sj = 0.0;
+    for (int q = 0; q < p->S; q++) sj += std::fabs(p->w1[q * p->H + j]);
+    amp += std::fabs(p->w2[j]) * sj;
+    hsum = std::max(hsum, sj + 1.0);
+  }
+  k.q_half_m = 0.5 - std::max(0x1p-20, k.inv_two_ba * amp * 0x1p-37);
+  k.h_marg = hsum * 0x1p-36;
+  k.lk[0] = 1.4426950408889634;   // 1 / ln 2
+  k.lk[1] = -0.7213475204444817;  // -1 / (2 ln 2)
+  k.lk[2] = 0.48089834696298783;  // 1 / (3 ln 2)
+  k.lk[3] = -0.36067376022224085; // -1 / (4 ln 2)
+  k.rnd_magic = 0x1.8p52;
+  k.e_magic = 4503601774854144.0;
   return k;
 }
 
@@ -113,6 +136,21 @@ size_t cub_scan_bytes(int64_t n) {
   cub::DeviceScan::ExclusiveSum(nullptr, bytes, (unsigned long long *)nullptr, (unsigned long long *)nullptr,
                                 (int)(n > 0 ? n : 1));
   return bytes;
+}
+
+// every block is one partition of one row (1-D inputs, block_rows == 1)
+bool one_row_parts(const Geom &G) { return G.br == 1 || G.rows == 1; }
+
+// Throughput path (tdec.cuh / tcmp.cuh) or latency path (dec4/dsc, fwdq/wsc):
+// the throughput kernels need partition-level parallelism only, the latency
+// kernels also split each partition's work across a CTA.  PMZ_PATH=latency |
+// throughput overrides the size rule (tests exercise both on small fields).
+bool use_tpath(const Geom &G) {
+  if (one_row_parts(G)) return false;
+  const char *e = getenv("PMZ_PATH");
+  if (e && e[0] == 'l') return false;
+  if (e && e[0] == 't') return true;
+  return G.nparts >= kTputMinParts;
 }
 
 WsLayout compress_layout(const Geom &g) {
@@ -144,7 +182,7 @@ WsLayout compress_layout(const Geom &g) {
   L.cub_tmp = take(L.cub_bytes);
   const size_t ntile = (size_t)g.nparts * (size_t)g.nct * kTile;  // partition-tiled elements
   L.vbuf = take(8 * ntile);
-  L.rqbuf = take(2 * ntile);
+  L.rqbuf = take((use_tpath(g) ? 4 : 2) * ntile);  // throughput path: per-row bitstreams (32 bits per code max)
   L.clsbuf = take(ntile);
   L.total = o;
   return L;
@@ -163,47 +201,59 @@ int err_from_bits(unsigned bits) {
 
 int launch_check() {
   cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess && getenv("PMZ_DEBUG")) fprintf(stderr, "permez: CUDA error: %s\n", cudaGetErrorString(e));
   return e == cudaSuccess ? PMZ_OK : PMZ_ERR_CUDA;
 }
 
 constexpr int kNT = 256;
 
-// every block is one partition of one row (1-D inputs, block_rows == 1)
-bool one_row_parts(const Geom &G) { return G.br == 1 || G.rows == 1; }
 
-// Throughput path (tdec.cuh / tcmp.cuh) or latency path (dec4/dsc, fwdq/wsc):
-// the throughput kernels need partition-level parallelism only, the latency
-// kernels also split each partition's work across a CTA.  PMZ_PATH=latency |
-// throughput overrides the size rule (tests exercise both on small fields).
-bool use_tpath(const Geom &G) {
-  if (one_row_parts(G)) return false;
-  const char *e = getenv("PMZ_PATH");
-  if (e && e[0] == 'l') return false;
-  if (e && e[0] == 't') return true;
-  return G.nparts >= kTputMinParts;
+// the throughput-path views of the compress workspace: per-row balance
+// lists in vbuf, per-row bitstreams in rqbuf, per-row {bits, count} in clsbuf
+CMainOut cmain_out(void *d_ws, const WsLayout &L) {
+  CMainOut o;
+  o.rowbits = at<unsigned>(d_ws, L.rqbuf);
+  o.balrow = at<double>(d_ws, L.vbuf);
+  o.rowinfo = at<uint2>(d_ws, L.clsbuf);
+  o.anchors = at<double>(d_ws, L.anchors);
+  o.part_bits = at<unsigned long long>(d_ws, L.part_bits);
+  o.part_zeros = at<unsigned long long>(d_ws, L.part_zeros);
+  o.lens = at<uint8_t>(d_ws, L.lens);
+  o.cw = at<unsigned>(d_ws, L.cw);
+  o.hist = at<unsigned long long>(d_ws, L.hist);
+  o.cov = at<unsigned long long>(d_ws, L.cov);
+  return o;
 }
-
-// the throughput-path views of the compress workspace: final codes (raster,
-// tcode_base) in rqbuf, per-row balance lists in vbuf, per-row {bits, count} in clsbuf
 template <int PK, int MODE>
-void launch_tmain(const float *x, const Geom &G, const KParams &k, const int64_t *d_val, int64_t n_val, void *d_ws,
+void launch_cmain(const float *x, const Geom &G, const KParams &k, const int64_t *d_val, int64_t n_val, void *d_ws,
                   const WsLayout &L, cudaStream_t st) {
   unsigned grid;
-  if (MODE == kTMain) grid = (unsigned)((G.nparts + kTCW - 1) / kTCW);
-  else grid = (unsigned)(n_val * ((G.np_full + kTCW - 1) / kTCW));
+  if (MODE == kCMain) grid = (unsigned)((G.nparts + kCW - 1) / kCW);
+  else grid = (unsigned)(n_val * ((G.np_full + kCW - 1) / kCW));
   if (grid == 0) return;
-  cudaFuncSetAttribute(k_t_main<PK, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTCmpSmem);
-  k_t_main<PK, MODE><<<grid, kTCW * 32, kTCmpSmem, st>>>(
-      x, G, k, at<BlkP>(d_ws, L.blkp), at<WsStatus>(d_ws, L.status), d_val, n_val, at<uint16_t>(d_ws, L.rqbuf),
-      at<double>(d_ws, L.vbuf), at<unsigned>(d_ws, L.clsbuf), at<double>(d_ws, L.anchors),
-      at<unsigned long long>(d_ws, L.part_bits), at<unsigned long long>(d_ws, L.part_zeros),
-      at<uint8_t>(d_ws, L.lens), at<unsigned long long>(d_ws, L.hist), at<unsigned long long>(d_ws, L.cov));
+  // m is selected on the device: size for the largest shared-memory table
+  const int smem = (int)cmain_smem_bytes(MODE, MODE == kCHist ? 13 : 12);
+  cudaFuncSetAttribute(k_c_main<PK, MODE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  k_c_main<PK, MODE, true><<<grid, kCW * 32, smem, st>>>(x, G, k, at<BlkP>(d_ws, L.blkp),
+                                                         at<WsStatus>(d_ws, L.status), d_val, n_val,
+                                                         cmain_out(d_ws, L));
+  if (getenv("PMZ_DEBUG")) {
+    const cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) fprintf(stderr, "permez: k_c_main<%d,%d,1>: %s\n", PK, MODE, cudaGetErrorString(e));
+  }
+  if (MODE == kCMain) {  // alphabets above 2^12 (m is selected on the device): codewords from global memory
+    const int smem2 = (int)cmain_smem_bytes(MODE, 16);
+    cudaFuncSetAttribute(k_c_main<PK, MODE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
+    k_c_main<PK, MODE, false><<<grid, kCW * 32, smem2, st>>>(x, G, k, at<BlkP>(d_ws, L.blkp),
+                                                             at<WsStatus>(d_ws, L.status), d_val, n_val,
+                                                             cmain_out(d_ws, L));
+  }
 }
 template <int MODE>
 void launch_tmain_pk(const float *x, const Geom &G, const KParams &k, const int64_t *d_val, int64_t n_val,
                      void *d_ws, const WsLayout &L, cudaStream_t st) {
-  if (k.init_model == 3) launch_tmain<3, MODE>(x, G, k, d_val, n_val, d_ws, L, st);
-  else launch_tmain<0, MODE>(x, G, k, d_val, n_val, d_ws, L, st);
+  if (k.init_model == 3) launch_cmain<3, MODE>(x, G, k, d_val, n_val, d_ws, L, st);
+  else launch_cmain<0, MODE>(x, G, k, d_val, n_val, d_ws, L, st);
 }
 
 template <int PK>
@@ -325,8 +375,8 @@ int pmz_compress_transform(const float *d_in, const pmz_geom *g, const pmz_param
                                                                at<WsStatus>(d_ws, L.status));
   if (use_tpath(G)) {
     // throughput path: only the coverage of the validation blocks' TRUE
-    // residuals here (select_m); the forward map runs fused in k_t_main
-    if (k.m_fixed == 0 && n_val > 0) launch_tmain_pk<kTCoverage>(d_in, G, k, d_val, n_val, d_ws, L, st);
+    // residuals here (select_m); the forward map runs fused in k_c_main
+    if (k.m_fixed == 0 && n_val > 0) launch_tmain_pk<kCCov>(d_in, G, k, d_val, n_val, d_ws, L, st);
     return launch_check();
   }
   // forward map + m-independent TRUE-surface quantization of every element,
@@ -408,7 +458,7 @@ int pmz_compress_codes(const float *d_in, const pmz_geom *g, const pmz_params *p
   if (use_tpath(G)) {
     // throughput path: the validation blocks' final codes -> histogram
     // (estimate_codebook); every block is coded after the codebook
-    if (n_val > 0) launch_tmain_pk<kTValCodes>(d_in, G, k, d_val, n_val, d_ws, L, st);
+    if (n_val > 0) launch_tmain_pk<kCHist>(d_in, G, k, d_val, n_val, d_ws, L, st);
     return launch_check();
   }
   if (G.nparts > 0) {
@@ -457,7 +507,7 @@ int pmz_compress_encode(const float *d_in, const pmz_geom *g, const pmz_params *
                                        at<unsigned>(d_ws, L.cw));
   if (G.nparts > 0) {
     if (use_tpath(G)) {
-      launch_tmain_pk<kTMain>(d_in, G, k, nullptr, 0, d_ws, L, st);
+      launch_tmain_pk<kCMain>(d_in, G, k, nullptr, 0, d_ws, L, st);
     } else {
       k_part_bits<<<(unsigned)G.nparts, kPbW * 32, 0, st>>>(G, at<BlkP>(d_ws, L.blkp), at<int16_t>(d_ws, L.rqbuf),
                                                            at<uint8_t>(d_ws, L.lens),
@@ -491,11 +541,10 @@ int pmz_compress_write_async(const pmz_geom *g, const pmz_params *p, int write_h
     if (write_header)
       k_write_header<<<1, 256, 0, st>>>(d_out, G, k, g->global_rows, at<uint8_t>(d_ws, L.lens), S);
     if (G.nparts > 0 && use_tpath(G)) {
-      k_t_write<<<(unsigned)((G.nparts + kTCW - 1) / kTCW), kTCW * 32, 0, st>>>(
-          G, at<BlkP>(d_ws, L.blkp), at<uint16_t>(d_ws, L.rqbuf), at<double>(d_ws, L.vbuf),
-          at<unsigned>(d_ws, L.clsbuf), at<double>(d_ws, L.anchors), at<unsigned long long>(d_ws, L.part_bits),
-          at<unsigned long long>(d_ws, L.part_zeros), at<unsigned long long>(d_ws, L.rec_off),
-          at<uint8_t>(d_ws, L.lens), at<unsigned>(d_ws, L.cw), d_out, S);
+      k_c_write<<<(unsigned)((G.nparts + kCWW - 1) / kCWW), kCWW * 32, 0, st>>>(
+          G, at<BlkP>(d_ws, L.blkp), at<unsigned>(d_ws, L.rqbuf), at<double>(d_ws, L.vbuf),
+          at<uint2>(d_ws, L.clsbuf), at<double>(d_ws, L.anchors), at<unsigned long long>(d_ws, L.part_bits),
+          at<unsigned long long>(d_ws, L.part_zeros), at<unsigned long long>(d_ws, L.rec_off), d_out, S);
     } else if (G.nparts > 0) {
       k_write_part<<<(unsigned)G.nparts, kWT, kWpSmem, st>>>(
           G, at<BlkP>(d_ws, L.blkp), at<int16_t>(d_ws, L.rqbuf), at<double>(d_ws, L.vbuf),
@@ -1139,6 +1188,11 @@ int pmz_log2_f32_batch(const float *d_x, uint64_t n, double *d_out, uint32_t *d_
 }
 
 
+#ifdef PMZ_CSTATS
+extern "C" PMZ_API int pmz_cstats_read(void *host) {
+  return cudaMemcpyFromSymbol(host, pmz::g_cstats, sizeof(pmz::g_cstats)) == cudaSuccess ? 0 : -1;
+}
+#endif
 #ifdef PMZ_D3_PROF
 // experiments only (tools/dec_bench.py): the decoder's per-partition phase timestamps
 extern "C" PMZ_API int pmz_d3prof_read(void *host, uint64_t bytes) {

@@ -18,6 +18,10 @@ struct KParams {
   double dpos, dneg;       // log2(1 + t), log2(1 - t): violation thresholds in the log domain
   double dpos_m, dneg_m;   // dpos - mu, dneg + mu: inside -> certainly within the bound (mu = 2^-20)
   double dpos_p, dneg_p;   // dpos + mu, dneg - mu: outside -> certainly a violation
+  double q_half_m;         // 1/2 - M: |frac(q~)| below it rounds like the exact q (cmain.cuh)
+  double h_marg;           // |h~| below it: leaky-ReLU sign not certain from approximate surfaces
+  double lk[4];            // log2(1 + r) series k1..k4 of the approximate forward map (cmain.cuh)
+  double rnd_magic, e_magic;  // 1.5 2^52 (round to integer), 2^52 + 2^31 (int -> double)
   int init_model;          // weights equal init_model: constant-folded predictor
   double w1[8], w2[2];
   int S, H, block_rows, block_cols, partition_rows, m_fixed;

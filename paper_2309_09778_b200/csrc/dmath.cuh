@@ -20,6 +20,7 @@
 #include <cstdint>
 #include "dmath_tables.cuh"
 #include "np_log2_exc.inc"
+#include "np_log2_hash.inc"
 
 namespace pmz {
 
@@ -60,6 +61,26 @@ __device__ __noinline__ double np_log2_adjust(double x, double cr) {
       const bool up = (w >> 31) != 0;
       return __longlong_as_double((cr > 0.0) == up ? b + 1 : b - 1);
     }
+  }
+  return cr;
+}
+
+// the same exceptions as an open-addressing hash set (tools/gen_log2_hash.py):
+// one or two probes instead of the binary search
+__device__ const uint32_t pmz_np_log2_hash[1 << PMZ_NP_LOG2_HASH_BITS] = {PMZ_NP_LOG2_HASH_INIT};
+
+// cr = CR log2 of the positive normal float with bits pat; returns np.log2
+__device__ __forceinline__ double np_log2_adjust_bits(uint32_t pat, double cr) {
+  uint32_t h = (pat * 0x9E3779B1u) >> (32 - PMZ_NP_LOG2_HASH_BITS);
+  for (int n = 0; n < PMZ_NP_LOG2_HASH_MAXPROBE; n++) {
+    const uint32_t w = __ldg(&pmz_np_log2_hash[h]);
+    if (w == 0) break;
+    if ((w & 0x7fffffffu) == pat) {
+      const long long b = __double_as_longlong(cr);
+      const bool up = (w >> 31) != 0;
+      return __longlong_as_double((cr > 0.0) == up ? b + 1 : b - 1);
+    }
+    h = (h + 1) & ((1u << PMZ_NP_LOG2_HASH_BITS) - 1);
   }
   return cr;
 }

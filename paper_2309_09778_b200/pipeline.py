@@ -345,7 +345,7 @@ class Codec:
     # stage names of the ``events`` of compress_staged / decompress_device
     stage_names_compress = ("analyze (block stats, numpy fixups, select_m coverage)",
                             "codes (select_m, validation codes / latency path: verify_and_repair)",
-                            "encode (codebook; throughput path: k_t_main = forward map + compress_block + "
+                            "encode (codebook; throughput path: k_c_main = forward map + compress_block + "
                             "verify_and_repair of every block)",
                             "write (record sizes/offsets, header, block records)")
     stage_names_decompress = ("prepare (block records, parameters, decode tables)",

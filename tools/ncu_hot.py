@@ -11,7 +11,7 @@ import sys
 
 rep, kern = sys.argv[1], sys.argv[2]
 n = int(sys.argv[3]) if len(sys.argv) > 3 else 25
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "-k", f"regex:{kern}", "--print-source", "sass"],
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--kernel-name-base", "mangled", "-k", f"regex:{kern}", "--print-source", "sass"],
                      capture_output=True, text=True).stdout
 rows = [r for r in csv.reader(io.StringIO(out))]
 hi = next(i for i, r in enumerate(rows) if r and r[0] == 'Address')

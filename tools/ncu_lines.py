@@ -9,7 +9,7 @@ import sys
 
 rep, kern = sys.argv[1], sys.argv[2]
 n = int(sys.argv[3]) if len(sys.argv) > 3 else 30
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "-k", f"regex:{kern}", "--print-source",
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--kernel-name-base", "mangled", "-k", f"regex:{kern}", "--print-source",
                       "cuda,sass"], capture_output=True, text=True).stdout
 fname, rows = None, []
 for r in csv.reader(io.StringIO(out)):
