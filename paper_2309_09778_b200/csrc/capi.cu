@@ -20,6 +20,7 @@
 #include "segy.cuh"
 #include "tdec.cuh"
 #include "cmain.cuh"
+#include "dmain.cuh"
 
 using namespace pmz;
 
@@ -745,8 +746,8 @@ int pmz_index_blocks(const uint8_t *h, uint64_t n, const pmz_header *hd, uint64_
 
 namespace {
 struct DecLayout {
-  size_t status, blkp, part_bits, part_off, zflag, anchors, bal_off, pay_off, blk_nbal, tab, sym, lut, npfix, codes,
-      vtile, rowz, total;
+  size_t status, blkp, part_bits, part_off, zflag, anchors, bal_off, pay_off, blk_nbal, tab, sym, lut, lut1, npfix,
+      codes, vtile, rowz, total;
   bool tpath;
 };
 DecLayout dec_layout(const Geom &g) {
@@ -769,11 +770,12 @@ DecLayout dec_layout(const Geom &g) {
   L.tab = take(sizeof(DecTab));
   L.sym = take(2 * kMaxAlpha);
   L.lut = take(4ull * ((1u << kLutBits) + kLut2Max));            // first + second level
+  L.lut1 = take(4ull << kDLutBits);                               // k_d_decode's first level
   L.npfix = take(sizeof(pmz_np_fix) * (size_t)(g.nblocks + 1));
   L.tpath = use_tpath(g);
   if (L.tpath) {
     L.codes = take(2 * (size_t)g.nparts * (size_t)g.prow * (size_t)g.bc);  // raster per partition (tcode_base)
-    L.rowz = take(2 * (size_t)g.nparts * (size_t)g.prow + 2);
+    L.rowz = take(4 * (size_t)g.nparts * (size_t)g.prow + 4);  // code-0 count per row
     L.vtile = o;
   } else {
     L.codes = take(2 * (size_t)g.nparts * (size_t)g.nct * kTile);  // partition-tiled
@@ -852,6 +854,9 @@ int pmz_decompress_prepare(const uint8_t *d_buf, uint64_t n, const pmz_header *h
         at<pmz_np_fix>(d_ws, L.npfix));
     k_dec_tables<<<1, 1024, 0, st>>>(d_buf + hdr->lens_offset, (int)hdr->m, at<DecTab>(d_ws, L.tab),
                                      at<uint16_t>(d_ws, L.sym), at<unsigned>(d_ws, L.lut), S);
+    if (L.tpath)
+      k_d_lut<<<(1u << kDLutBits) / 256, 256, 0, st>>>(at<DecTab>(d_ws, L.tab), at<uint16_t>(d_ws, L.sym),
+                                                      1 << (int)hdr->m, at<unsigned>(d_ws, L.lut1), S);
   }
   return launch_check();
 }
@@ -884,19 +889,18 @@ int pmz_decompress_run(const uint8_t *d_buf, uint64_t n, const pmz_header *hdr, 
   WsStatus *S = at<WsStatus>(d_ws, L.status);
   if (G.nblocks > 0 && L.tpath) {
     const int center = 1 << ((int)hdr->m - 1);
-    CK(cudaFuncSetAttribute(k_t_decode, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTDecSmem));
-    k_t_decode<<<(unsigned)((G.nparts + kTDT - 1) / kTDT), kTDT, kTDecSmem, st>>>(
-        d_buf, n, G, at<BlkP>(d_ws, L.blkp), at<DecTab>(d_ws, L.tab), at<uint16_t>(d_ws, L.sym),
-        at<unsigned>(d_ws, L.lut), at<unsigned long long>(d_ws, L.part_bits), at<unsigned long long>(d_ws, L.part_off),
-        at<unsigned long long>(d_ws, L.pay_off), 1 << (int)hdr->m, at<uint16_t>(d_ws, L.codes),
-        at<unsigned>(d_ws, L.zflag), S);
-    const unsigned grid = (unsigned)((G.nparts + kTRW - 1) / kTRW);
+    k_d_decode<<<(unsigned)((G.nparts + kDDT - 1) / kDDT), kDDT, 0, st>>>(
+        d_buf, n, G, at<BlkP>(d_ws, L.blkp), at<DecTab>(d_ws, L.tab), at<uint16_t>(d_ws, L.sym), 1 << (int)hdr->m,
+        at<unsigned>(d_ws, L.lut1), at<unsigned long long>(d_ws, L.part_bits), at<unsigned long long>(d_ws, L.part_off),
+        at<unsigned long long>(d_ws, L.pay_off), at<uint16_t>(d_ws, L.codes), at<unsigned>(d_ws, L.zflag),
+        at<unsigned>(d_ws, L.rowz), S);
+    const unsigned grid = (unsigned)((G.nparts + kDRW - 1) / kDRW);
 #define PMZ_T_RECON(PKV)                                                                                            \
   do {                                                                                                              \
-    CK(cudaFuncSetAttribute(k_t_recon<PKV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTRecSmem));          \
-    k_t_recon<PKV><<<grid, kTRW * 32, kTRecSmem, st>>>(                                                             \
+    CK(cudaFuncSetAttribute(k_d_recon<PKV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDRecSmem));          \
+    k_d_recon<PKV><<<grid, kDRW * 32, kDRecSmem, st>>>(                                                             \
         d_buf, n, G, k, at<BlkP>(d_ws, L.blkp), at<uint16_t>(d_ws, L.codes), at<unsigned>(d_ws, L.zflag),           \
-        at<double>(d_ws, L.anchors), at<unsigned long long>(d_ws, L.bal_off),          \
+        at<unsigned>(d_ws, L.rowz), at<double>(d_ws, L.anchors), at<unsigned long long>(d_ws, L.bal_off),           \
         at<unsigned long long>(d_ws, L.blk_nbal), center, d_out, S);                                                \
   } while (0)
     if (k.init_model == 3) PMZ_T_RECON(3);

@@ -218,7 +218,7 @@ constexpr unsigned kClsHi = 0x7effc99eu;  // bits of 1.7e38f
 template <int PK>
 __device__ __noinline__ int c_rare(const KParams &k, const BlkP *Pp, int lane, float xz, double v, double w, double n,
                                    double nw, double hl, double nhl, double pn, bool anchor, int center,
-                                   unsigned *amb, double *hnew, unsigned *repairs) {
+                                   unsigned *amb, double *hnew, bool *repaired) {
   const bool lane0 = lane == 0;
   if (!anchor) {
     const BlkP P = *Pp;
@@ -237,7 +237,7 @@ __device__ __noinline__ int c_rare(const KParams &k, const BlkP *Pp, int lane, f
         *hnew = vh;
         return center + rq;
       }
-      *repairs += 1;
+      *repaired = true;
     }
   }
   *hnew = v;
@@ -410,10 +410,12 @@ __global__ void __launch_bounds__(kCW * 32, 2)
         // decoder simulation on the RECONSTRUCTED surface (exact FP64, D3 order)
         const double nhl = __shfl_up_sync(0xffffffffu, hl, 1);
         double ar;
-        if (PK == 3) {
+        if (PK == 3) {  // predict_init (D3): a w2_0 + a w2_1 with w2 = 1/2, exactly as written
           double h = __dsub_rn(__dadd_rn(hl, nhl), pn);
           h = lane0 ? hl : h;
           ar = h < 0.0 ? __dmul_rn(slope, h) : h;
+          const double a2 = __dmul_rn(ar, 0.5);
+          ar = __dadd_rn(a2, a2);
         } else {
           ar = predict_steady<PK>(k, hl, nhl, pn, lane0);
         }
@@ -424,8 +426,7 @@ __global__ void __launch_bounds__(kCW * 32, 2)
         const bool in12 = normal & (neg ? gb : (gz & !gb));
         const bool inner = (d < k.dpos_m) & (d > k.dneg_m);
         const bool outer = (d > k.dpos_p) | (d < k.dneg_p);
-        const bool tiny = PK == 3 && fabs(ar) < 0x1p-1020;
-        const bool sure = !qamb & !tiny & !anchor;
+        const bool sure = !qamb & !anchor;
         const bool accept = sure & !out & ((in12 & inner) | ((u == 0) & !gz));
         // certain violations (D8): out-of-range residual, d outside the bound by more than the
         // margin, a sign flip at t < 1 -> balance point (verify_and_repair)
@@ -444,7 +445,11 @@ __global__ void __launch_bounds__(kCW * 32, 2)
             double v, w, n, nw;
             exact4(v, w, n, nw);
             const float xz = __uint_as_float(u | (neg ? 0x80000000u : 0u));
-            fin = c_rare<PK>(k, Pp, lane, xz, v, w, n, nw, hl, nhl, pn, anchor, center, amb, &hnew, &repairs);
+            bool rep = false;
+            double hr;  // (addressed only here: the common path keeps hnew in registers)
+            fin = c_rare<PK>(k, Pp, lane, xz, v, w, n, nw, hl, nhl, pn, anchor, center, amb, &hr, &rep);
+            hnew = hr;
+            repairs += rep ? 1u : 0u;
             vbal = v;
             if (MODE == kCMain && anchor) o.anchors[p] = v;  // forced anchor, D1
           }

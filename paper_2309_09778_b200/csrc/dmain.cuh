@@ -1,0 +1,433 @@
+// dmain.cuh -- throughput-path decompression, issue-efficient version:
+// decode_next as k_d_decode, then decompress_block
+// + inverse_map (transform.py:188-202) + the float32 cast
+// (D20) as k_d_recon.
+//
+// k_d_decode: a THREAD per partition substream, decoded serially.  The
+//   codeword length is the largest l with first_l << (32 - l) <= the next 32
+//   stream bits (canonical codes: the left-justified first codewords grow with
+//   the length), found by a five-step binary search over the shared table; the
+//   symbol is offset_l + the codeword's rank among length-l codewords.  The
+//   stream is read from global memory in 16-byte words, one word ahead; codes
+//   leave in 16-byte groups of eight (raster per partition, tcode_base),
+//   per-row code-0 counts on the side.
+// k_d_recon: a WARP per partition, lane = row (the mirror of k_c_main): code
+//   tiles stream into a 32 x 64 ring by cp.async three 8-column chunks ahead;
+//   at step t lane r reconstructs column t - r: vhat = predict(RECONSTRUCTED
+//   W, N, NW) + dequantize(code), or the row's next balance value at code 0
+//   (held in a two-deep register queue refilled by plain loads), or the
+//   anchor; the inverse map to float32 (256-entry shared table + degree-4
+//   series, exact fallback near float32 rounding midpoints) and 8-column
+//   output chunks stored from a 32 x 64 float ring once every row finished them.
+#pragma once
+#include "common.cuh"
+#include "compress.cuh"
+#include "decompress.cuh"
+#include "wsc.cuh"
+#include "tdec.cuh"
+#include "cmain.cuh"
+
+namespace pmz {
+
+constexpr int kDDT = 256;          // decoder threads (partitions) per CTA
+constexpr int kDSymSmem = 1 << 12;  // canonical symbol table in shared memory up to this alphabet
+
+// First-level decode table over the top 12 stream bits (built once per
+// container by k_d_lut): a codeword of <= 12 bits gives {symbol, length}
+// directly; a longer one gives the range [lmin, lmax] of codeword lengths
+// under that prefix (bit 31 set), the length then found by a short scan.
+constexpr int kDLutBits = 12;
+__device__ __forceinline__ int d_len_of(unsigned top, const unsigned *lj, int maxl) {
+  int l = 1;
+#pragma unroll
+  for (int s = 16; s; s >>= 1) {
+    const int c = l + s;
+    if (c <= maxl && lj[c] <= top) l = c;
+  }
+  return l;
+}
+__global__ void k_d_lut(const DecTab *__restrict__ tab, const uint16_t *__restrict__ sym, int nalpha, unsigned *lut1,
+                        WsStatus *st) {
+  __shared__ unsigned s_lj[34];
+  count_launch(st);
+  if (threadIdx.x < 34) {
+    const unsigned l = threadIdx.x;
+    s_lj[l] = (l >= 1 && l <= 32) ? (l == 32 ? tab->first[l] : tab->first[l] << (32 - l)) : 0u;
+  }
+  __syncthreads();
+  const int maxl = tab->maxl;
+  const unsigned pfx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (pfx >= (1u << kDLutBits)) return;
+  const unsigned lo = pfx << (32 - kDLutBits), hi = lo | ((1u << (32 - kDLutBits)) - 1u);
+  const int l0 = d_len_of(lo, s_lj, maxl), l1 = d_len_of(hi, s_lj, maxl);
+  if (l0 <= kDLutBits) {
+    unsigned idx = tab->offset[l0] + ((lo - s_lj[l0]) >> (32 - l0));
+    idx = idx < (unsigned)nalpha ? idx : (unsigned)nalpha - 1u;
+    lut1[pfx] = (unsigned)sym[idx] | ((unsigned)l0 << 16);
+  } else {
+    lut1[pfx] = 0x80000000u | ((unsigned)l0 << 16) | ((unsigned)l1 << 21);
+  }
+}
+
+__global__ void __launch_bounds__(kDDT) k_d_decode(const uint8_t *__restrict__ buf, unsigned long long buf_n, Geom g,
+                                                   const BlkP *__restrict__ blkp, const DecTab *__restrict__ tab,
+                                                   const uint16_t *__restrict__ sym, int nalpha,
+                                                   const unsigned *__restrict__ lut1,
+                                                   const unsigned long long *__restrict__ part_bits,
+                                                   const unsigned long long *__restrict__ part_off,
+                                                   const unsigned long long *__restrict__ pay_off,
+                                                   uint16_t *__restrict__ codes, unsigned *__restrict__ part_z,
+                                                   unsigned *__restrict__ rowz, WsStatus *st) {
+  __shared__ unsigned s_lj[34], s_off[34];
+  __shared__ unsigned s_lut[1 << kDLutBits];
+  __shared__ uint16_t s_sym[kDSymSmem];
+  __shared__ __align__(16) unsigned s_ring[kDDT][16];  // per-thread stream ring (4 x 16 B)
+  count_launch(st);
+  if (threadIdx.x < 34) {
+    const unsigned l = threadIdx.x;
+    s_lj[l] = (l >= 1 && l <= 32) ? (l == 32 ? tab->first[l] : tab->first[l] << (32 - l)) : 0xffffffffu;
+    s_off[l] = tab->offset[l];
+  }
+  for (int i = threadIdx.x; i < (1 << kDLutBits); i += kDDT) s_lut[i] = lut1[i];
+  const bool sym_smem = nalpha <= kDSymSmem;
+  if (sym_smem)
+    for (int i = threadIdx.x; i < nalpha; i += kDDT) s_sym[i] = sym[i];
+  __syncthreads();
+  const int64_t p = (int64_t)blockIdx.x * kDDT + threadIdx.x;
+  if (p >= g.nparts) return;
+  int64_t b;
+  int pi;
+  part_of(g, p, b, pi);
+  const BlockBox bb = block_box(g, b);
+  const int R = min(g.prow, bb.br - pi * g.prow), C = bb.bc;
+  unsigned *rz = rowz + p * g.prow;
+  if (blkp[b].trivial) {
+    part_z[p] = 0;
+    for (int r = 0; r < R; r++) rz[r] = 0;
+    return;
+  }
+  const unsigned n = (unsigned)(R * C);
+  const unsigned long long L64 = part_bits[p];
+  const uint8_t *src = buf + pay_off[b] + part_off[p];
+  if (L64 > 32ull * n || pay_off[b] + part_off[p] + (L64 + 7) / 8 > buf_n) {
+    set_err_at(st, PMZ_ERR_CORRUPT, 71, p);
+    return;
+  }
+  // reader: the stream's aligned 16-byte blocks stream into a 4-block shared
+  // ring per thread by cp.async three blocks ahead; 32 bits at a time come
+  // out of the ring (no register waits on global memory)
+  const uintptr_t a = reinterpret_cast<uintptr_t>(src);
+  const uint4 *qb = reinterpret_cast<const uint4 *>(a & ~(uintptr_t)15);
+  const uint4 *qlast = reinterpret_cast<const uint4 *>((reinterpret_cast<uintptr_t>(buf + buf_n) - 1) & ~(uintptr_t)15);
+  const unsigned ring_s = smem_u32(&s_ring[threadIdx.x][0]);
+  auto issue = [&](unsigned k) {  // block k -> slot k & 3
+    const uint4 *q = qb + k;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(ring_s + 16u * (k & 3u)), "l"(q <= qlast ? q : qlast)
+                 : "memory");
+    cp_async_commit();
+  };
+  issue(0);
+  issue(1);
+  issue(2);
+  issue(3);
+  cp_async_wait<3>();
+  unsigned wi = (unsigned)(a >> 2) & 3u;  // next 32-bit word (index from qb)
+  unsigned long long bits = 0;
+  int nb = 0;
+  unsigned long long used = 0;
+  auto refill = [&]() {
+    const unsigned w = lds_u32(ring_s + ((wi & 15u) << 2));
+    wi++;
+    if ((wi & 3u) == 0) {  // block (wi >> 2) - 1 consumed: its slot takes block (wi >> 2) + 3
+      issue((wi >> 2) + 3u);
+      cp_async_wait<3>();  // block wi >> 2 has landed
+    }
+    bits |= (unsigned long long)__byte_perm(w, 0, 0x0123) << (32 - nb);
+    nb += 32;
+  };
+  refill();
+  refill();
+  {
+    const int sb = (int)(a & 3) * 8;
+    bits <<= sb;
+    nb -= sb;
+  }
+  auto decode = [&]() -> unsigned {
+    if (nb <= 32) refill();
+    const unsigned top = (unsigned)(bits >> 32);
+    const unsigned e = s_lut[top >> (32 - kDLutBits)];
+    unsigned l = (e >> 16) & 31u, s = e & 0xffffu;
+    if (e & 0x80000000u) {  // longer than the table: scan the lengths possible under this prefix
+      const unsigned lmax = (e >> 21) & 31u;
+      while (l < lmax && s_lj[l + 1] <= top) l++;
+      unsigned idx = s_off[l] + ((top - s_lj[l]) >> (32 - l));
+      idx = idx < (unsigned)nalpha ? idx : (unsigned)nalpha - 1u;
+      s = sym_smem ? s_sym[idx] : __ldg(sym + idx);
+    }
+    bits <<= l;
+    nb -= (int)l;
+    used += l;
+    return s;
+  };
+  uint16_t *cp = codes + tcode_base(g, p);
+  unsigned zt = 0, zr = 0;
+  if ((C & 7) == 0 && ((g.prow * g.bc) & 7) == 0) {
+    // groups of eight codes of one row, one 16-byte store
+    int col = 0, r = 0;
+    for (unsigned i0 = 0; i0 < n; i0 += 8) {
+      unsigned w[4];
+#pragma unroll
+      for (int j = 0; j < 8; j += 2) {
+        const unsigned s0 = (i0 + j == 0) ? (unsigned)kAnc : decode();
+        const unsigned s1 = decode();
+        zr += (s0 == 0 ? 1u : 0u) + (s1 == 0 ? 1u : 0u);
+        w[j >> 1] = s0 | (s1 << 16);
+      }
+      *reinterpret_cast<uint4 *>(cp + i0) = make_uint4(w[0], w[1], w[2], w[3]);
+      col += 8;
+      if (col == C) {
+        rz[r++] = zr;
+        zt += zr;
+        zr = 0;
+        col = 0;
+      }
+    }
+  } else {
+    int col = 0, r = 0;
+    for (unsigned i = 0; i < n; i++) {
+      const unsigned s = i == 0 ? (unsigned)kAnc : decode();
+      cp[i] = (uint16_t)s;
+      zr += s == 0 ? 1u : 0u;
+      if (++col == C) {
+        rz[r++] = zr;
+        zt += zr;
+        zr = 0;
+        col = 0;
+      }
+    }
+  }
+  part_z[p] = zt;
+  if (used != L64) set_err_at(st, used < L64 ? PMZ_ERR_CORRUPT : PMZ_ERR_TRUNCATED, 72, p);
+  cp_async_wait<0>();  // nothing in flight into shared memory at exit
+}
+
+// ---------------------------------------------------------------------------
+constexpr int kDRW = 8;  // partitions (warps) per reconstruct CTA
+__device__ const double kDExp2Tab[257] = {
+#include "dmain_tables.inc"
+};
+struct DRecWarp {
+  uint16_t code[32 * kCRing];     // code ring: column c of row r at r * 64 + (c & 63)
+  unsigned long long bal[32 * 8]; // per row: the aligned 8-byte words around its next balance values
+};
+constexpr size_t kDRecSmem = sizeof(DRecWarp) * kDRW + 257 * 8;
+
+__device__ __forceinline__ unsigned long long lds_u64(unsigned a) {
+  unsigned long long v;
+  asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ unsigned lds_u16(unsigned a) {
+  unsigned short v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts_f32(unsigned a, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
+}
+
+// (float) of the CR double 2^y for y in (-125, 127) (inverse_map's exp2 + the D20
+// cast): 2^(j/256) from the shared table times a degree-4 series in
+// t = y - n - j/256 (|t| <= 2^-9, relative error < 2^-50), 2^n through the
+// exponent field; when the double lands within 2^-42 of a float32 rounding
+// midpoint the exact path decides (pmz_exp2_to_f32)
+__device__ __forceinline__ float d_exp2_f32(double y, unsigned tab_s, unsigned *amb) {
+  const double tn = __dadd_rn(y, 0x1.8p52);
+  const double nn = __dsub_rn(tn, 0x1.8p52);
+  const double f = __dsub_rn(y, nn);
+  const double tj = __fma_rn(f, 256.0, 0x1.8p52);
+  const double jj = __dsub_rn(tj, 0x1.8p52);
+  const double t = __fma_rn(jj, -0.00390625, f);  // exact
+  double q = __fma_rn(t, 0x1.3b2ab6fba4e77p-7, 0x1.c6b08d704a0c0p-5);
+  q = __fma_rn(t, q, 0x1.ebfbdff82c58fp-3);
+  q = __fma_rn(t, q, 0x1.62e42fefa39efp-1);
+  q = __fma_rn(t, q, 1.0);
+  const int j = __double2loint(tj), n = __double2loint(tn);
+  const double a0 = __dmul_rn(lds_f64(tab_s + 8u * (unsigned)(j + 128)), q);
+  const double a = __hiloint2double(__double2hiint(a0) + (n << 20), __double2loint(a0));
+  const unsigned lo29 = (unsigned)__double2loint(a0) & 0x1fffffffu;
+  const unsigned dist = (unsigned)abs((int)lo29 - 0x10000000);
+  if (__builtin_expect((dist > 1024u) & ((unsigned)(n + 124) < 250u), 1)) return __double2float_rn(a);
+  return pmz_exp2_to_f32(y, amb);
+}
+
+template <int PK>
+__global__ void __launch_bounds__(kDRW * 32, 3)
+    k_d_recon(const uint8_t *__restrict__ buf, unsigned long long buf_n, Geom g, const __grid_constant__ KParams k,
+              const BlkP *__restrict__ blkp, const uint16_t *__restrict__ codes, const unsigned *__restrict__ part_z,
+              const unsigned *__restrict__ rowz, const double *__restrict__ anchors,
+              const unsigned long long *__restrict__ bal_off, const unsigned long long *__restrict__ blk_nbal,
+              int center, float *__restrict__ out, WsStatus *st) {
+  extern __shared__ __align__(16) unsigned char smem_d[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  DRecWarp &S = reinterpret_cast<DRecWarp *>(smem_d)[warp];
+  double *s_e2 = reinterpret_cast<double *>(smem_d + sizeof(DRecWarp) * kDRW);
+  count_launch(st);
+  for (int i = threadIdx.x; i < 257; i += blockDim.x) s_e2[i] = kDExp2Tab[i];
+  __syncthreads();
+  const int64_t p = (int64_t)blockIdx.x * kDRW + warp;
+  if (p >= g.nparts) return;
+  int64_t b;
+  int pi;
+  part_of(g, p, b, pi);
+  const BlockBox bb = block_box(g, b);
+  const int pr0 = pi * g.prow, R = min(g.prow, bb.br - pr0), C = bb.bc;
+  float *op = out + (bb.r0 + pr0) * g.cols + bb.c0;
+  const BlkP P = blkp[b];
+  if (P.trivial) {
+    for (int r = 0; r < R; r++)
+      for (int c = lane; c < C; c += 32) op[(int64_t)r * g.cols + c] = 0.0f;
+    return;
+  }
+  if (st->err_bits) return;  // the decoder failed
+  const uint16_t *cb = codes + tcode_base(g, p);
+  // balance list of this row (D9): the block's list after the earlier partitions'
+  // and the earlier rows' code-0 counts
+  unsigned long long bj, bend;
+  {
+    const int64_t p0 = first_part(g, b);
+    unsigned zp = lane < pi ? part_z[p0 + lane] : 0u;
+    for (int o = 16; o; o >>= 1) zp += __shfl_xor_sync(0xffffffffu, zp, o);
+    const unsigned zr = lane < R ? rowz[p * g.prow + lane] : 0u;
+    unsigned incl = zr;
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    bj = (unsigned long long)zp + incl - zr;
+    bend = (unsigned long long)zp + incl;
+    const unsigned long long nbal = blk_nbal[b];
+    if (lane == 31 && pi == bb.np - 1 && bend != nbal)
+      set_err_at(st, bend > nbal ? PMZ_ERR_BALANCE_UNDERFLOW : PMZ_ERR_CORRUPT, 73, p);
+    if (__any_sync(0xffffffffu, bend > nbal)) {  // corrupt counts: never read past the list
+      if (lane == 0) set_err_at(st, PMZ_ERR_BALANCE_UNDERFLOW, 74, p);
+      return;
+    }
+  }
+  // balance values j of this row (bal_off + 8 j, any alignment): value j is
+  // bytes of the aligned words j and j + 1 (bq), which stream into an 8-word
+  // shared ring per row by cp.async six words ahead of their use
+  const uint8_t *bbase = buf + bal_off[b];
+  const unsigned bsh = (unsigned)(reinterpret_cast<uintptr_t>(bbase) & 7) * 8;
+  const unsigned long long *bq = reinterpret_cast<const unsigned long long *>(reinterpret_cast<uintptr_t>(bbase) & ~(uintptr_t)7);
+  const unsigned long long *bqlast =
+      reinterpret_cast<const unsigned long long *>((reinterpret_cast<uintptr_t>(buf + buf_n) - 1) & ~(uintptr_t)7);
+  const unsigned bal_s = smem_u32(S.bal + lane * 8);
+  auto issue_word = [&](unsigned long long w) {  // word w -> slot w & 7 (one cp.async group)
+    const unsigned long long *ap = bq + w;
+    const bool ok = w <= bend && ap <= bqlast;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(bal_s + 8u * (unsigned)(w & 7)),
+                 "l"(ok ? ap : bq), "r"(ok ? 8u : 0u)
+                 : "memory");
+    cp_async_commit();
+  };
+  for (unsigned i = 0; i < 7; i++) issue_word(bj + i);
+  const double anc = anchors[p];
+  unsigned *amb = &st->unresolved;
+  const double two_ba = k.two_ba, slope = k.slope;
+  const double zthr = P.zero_threshold, bnd = P.boundary, lgp = P.lg_pos, lgn = P.lg_neg;
+  const double cmagic = 4503599627370496.0 + (double)center;  // 2^52 + center
+  const bool lane0 = lane == 0, lane_in = lane < R;
+  const unsigned code_s = smem_u32(S.code + lane * kCRing), tab_s = smem_u32(s_e2);
+  const int nsteps = C + R - 1;
+  const bool vcode = (C & 7) == 0 && ((g.prow * g.bc) & 7) == 0;
+  const bool vout = ((g.cols & 3) == 0) && ((bb.c0 & 3) == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
+  // code chunk kc (columns 8 kc .. 8 kc + 7 of every row): each lane loads its
+  // row's 16 bytes one group ahead into registers and stores them into the
+  // ring when the group starts (cp.async is left to the balance words)
+  auto ld_codes = [&](int kc) -> uint4 {
+    const int c0 = kc * 8;
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    if (c0 < C && lane_in) {
+      const uint16_t *srcp = cb + (int64_t)lane * C + c0;
+      if (vcode) {
+        v = __ldg(reinterpret_cast<const uint4 *>(srcp));
+      } else {
+        unsigned h[8];
+        for (int c = 0; c < 8; c++) h[c] = c0 + c < C ? srcp[c] : 0u;
+        v = make_uint4(h[0] | (h[1] << 16), h[2] | (h[3] << 16), h[4] | (h[5] << 16), h[6] | (h[7] << 16));
+      }
+    }
+    return v;
+  };
+  auto st_codes = [&](int kc, uint4 v) {
+    *reinterpret_cast<uint4 *>(S.code + lane * kCRing + ((kc * 8) & (kCRing - 1))) = v;
+  };
+  // outputs: each lane's row, four columns per 16-byte store (the sectors
+  // complete in L2 across consecutive stores)
+  float4 ob = make_float4(0.f, 0.f, 0.f, 0.f);
+  float *orow = op + (int64_t)lane * g.cols;
+  double hl = 0.0, pn = 0.0;
+  uint4 cnext = ld_codes(0);
+  for (int t0 = 0; t0 < nsteps; t0 += 8) {
+    __syncwarp();
+    st_codes(t0 >> 3, cnext);
+    cnext = ld_codes((t0 >> 3) + 1);
+    __syncwarp();
+    const int t1 = min(nsteps, t0 + 8);
+#pragma unroll 2
+    for (int t = t0; t < t1; t++) {
+      const int c = t - lane;
+      const bool started = c >= 0;
+      const bool active = lane_in & ((unsigned)c < (unsigned)C);
+      const bool anchor = lane0 & (c == 0);
+      const unsigned cidx = (unsigned)(c & (kCRing - 1));
+      const unsigned code = lds_u16(code_s + (cidx << 1));
+      // dequantize: (code - center) exactly via the 2^52 magic, times 2 b_a
+      const double dq = __dmul_rn(__dsub_rn(__hiloint2double(0x43300000, (int)code), cmagic), two_ba);
+      const double nhl = __shfl_up_sync(0xffffffffu, hl, 1);
+      double a;
+      if (PK == 3) {  // predict_init (D3): a w2_0 + a w2_1 with w2 = 1/2, exactly as written
+        double h = __dsub_rn(__dadd_rn(hl, nhl), pn);
+        h = lane0 ? hl : h;
+        a = h < 0.0 ? __dmul_rn(slope, h) : h;
+        const double a2 = __dmul_rn(a, 0.5);
+        a = __dadd_rn(a2, a2);
+      } else {
+        a = predict_steady<PK>(k, hl, nhl, pn, lane0);
+      }
+      const bool isbal = active & (code == 0) & !anchor;
+      double qv = 0.0;
+      if (isbal) {  // the row's next balance value (words bj, bj + 1 landed: issued 6 groups ago)
+        cp_async_wait<5>();
+        const unsigned long long lo = lds_u64(bal_s + 8u * (unsigned)(bj & 7));
+        const unsigned long long hw = lds_u64(bal_s + 8u * (unsigned)((bj + 1) & 7));
+        qv = __longlong_as_double((long long)(bsh ? ((lo >> bsh) | (hw << (64 - bsh))) : lo));
+        issue_word(bj + 7);
+        bj++;
+      }
+      const double vh = anchor ? anc : (isbal ? qv : __dadd_rn(a, dq));
+      pn = nhl;
+      hl = started ? vh : hl;
+      // inverse_map (transform.py:188-202) + float32 cast (D20)
+      // (lanes outside the partition and zero outputs evaluate 2^0.5 instead)
+      const bool negv = vh > bnd, zero = vh <= zthr;
+      const float e = d_exp2_f32((active & !zero) ? __dsub_rn(vh, negv ? lgn : lgp) : 0.5, tab_s, amb);
+      const float y = zero ? 0.0f : (negv ? -e : e);
+      if (active) ob = make_float4(ob.y, ob.z, ob.w, y);
+      if (vout) {
+        if (active & ((c & 3) == 3)) *reinterpret_cast<float4 *>(orow + (c - 3)) = ob;
+      } else if (active) {
+        orow[c] = y;
+      }
+    }
+  }
+  cp_async_wait<0>();
+  // the row's last 1-3 columns when C is not a multiple of 4
+  if (vout && lane_in && (C & 3)) {
+    const float v4[4] = {ob.x, ob.y, ob.z, ob.w};
+    for (int q = 0; q < (C & 3); q++) orow[C - (C & 3) + q] = v4[4 - (C & 3) + q];
+  }
+}
+
+}  // namespace pmz
