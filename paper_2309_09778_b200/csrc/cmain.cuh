@@ -122,9 +122,10 @@ __device__ __forceinline__ double c_log2_exact(unsigned u, unsigned l2_s, unsign
   q = __fma_rn(r, q, kE3);
   q = __fma_rn(r, q, kE2);
   const double tail = __fma_rn(r, kE1lo, __dmul_rn(__dmul_rn(r, r), q));
-  const int e = (int)(u >> 23) - 127;
-  dd A = {T.y, 0.0};
-  if (e != 0) A = fast_two_sum((double)e, T.y);
+  // e + thi exactly as a double-double (|e| >= 1 > |thi|, or e = 0: (thi, 0))
+  const double ed = __dsub_rn(__hiloint2double(0x43300000, (int)(((u >> 23) - 127u) ^ 0x80000000u)),
+                              4503601774854144.0);
+  const dd A = fast_two_sum(ed, T.y);
   const dd B = two_sum(A.hi, P.hi);
   const double lo = __dadd_rn(__dadd_rn(__dadd_rn(A.lo, tlo), __dadd_rn(P.lo, tail)), B.lo);
   const dd R = fast_two_sum(B.hi, lo);
@@ -132,11 +133,9 @@ __device__ __forceinline__ double c_log2_exact(unsigned u, unsigned l2_s, unsign
   const double band = (unsigned)bi < (unsigned)PMZ_NP_LOG2_BAND_N ? lds_f64(band_s + 8u * (unsigned)bi) : 0.0;
   // |R - log2 x| < 2^-70 (series truncation 2^-74.5, tail rounding 2^-71.5) + 2^-104 |L| (dd sums)
   const double bacc = __fma_rn(fabs(R.hi), 0x1p-98, 0x1p-69);
-  if (__builtin_expect(dd_round_certain(R, bacc), 1)) {
-    // CR decided; numpy deviates from it only within `band` of a midpoint
-    if (band != 0.0 && !dd_round_certain(R, __dadd_rn(band, bacc))) return np_log2_adjust_bits(u, R.hi);
-    return R.hi;
-  }
+  // numpy deviates from the CR result only within `band` of a rounding midpoint
+  if (__builtin_expect(dd_round_certain(R, __dadd_rn(band, bacc)), 1)) return R.hi;
+  if (dd_round_certain(R, bacc)) return np_log2_adjust_bits(u, R.hi);  // CR decided: the exception table
   return pmz_log2_f32((double)__uint_as_float(u), amb);
 }
 
@@ -314,6 +313,7 @@ __global__ void __launch_bounds__(kCW * 32, 2)
     };
     const int center = 1 << (m - 1);
     const double two_ba = k.two_ba, inv = k.inv_two_ba, slope = k.slope;
+    const bool tlt1 = k.repair_t < 1.0;
     const double zthr = P.zero_threshold, bnd = P.boundary;
     const double lgp = P.lg_pos, lgn = P.lg_neg, zcode = P.zero_code;
     unsigned *amb = &st->unresolved;
@@ -430,7 +430,7 @@ __global__ void __launch_bounds__(kCW * 32, 2)
         const bool accept = sure & !out & ((in12 & inner) | ((u == 0) & !gz));
         // certain violations (D8): out-of-range residual, d outside the bound by more than the
         // margin, a sign flip at t < 1 -> balance point (verify_and_repair)
-        const bool vcert = sure & (out | (normal & (in12 ? outer : k.repair_t < 1.0)));
+        const bool vcert = sure & (out | (normal & (in12 ? outer : tlt1)));
         int fin = center + rq;
         double hnew = vhat, vbal = 0.0;
         CSTAT(0, active & !accept & !vcert);
@@ -441,6 +441,8 @@ __global__ void __launch_bounds__(kCW * 32, 2)
             fin = 0;
             hnew = vbal;
             repairs += out ? 0u : 1u;
+            if (MODE == kCMain) brow[nb] = vbal;  // the row's balance list (D9)
+            nb++;
           } else if (active & !accept) {  // anchor, ties, the filter's undecided band: all exact
             double v, w, n, nw;
             exact4(v, w, n, nw);
@@ -450,8 +452,11 @@ __global__ void __launch_bounds__(kCW * 32, 2)
             fin = c_rare<PK>(k, Pp, lane, xz, v, w, n, nw, hl, nhl, pn, anchor, center, amb, &hr, &rep);
             hnew = hr;
             repairs += rep ? 1u : 0u;
-            vbal = v;
             if (MODE == kCMain && anchor) o.anchors[p] = v;  // forced anchor, D1
+            if (fin == 0 && !anchor) {
+              if (MODE == kCMain) brow[nb] = v;
+              nb++;
+            }
           }
         }
         pn = nhl;
@@ -466,7 +471,6 @@ __global__ void __launch_bounds__(kCW * 32, 2)
           }
         } else {
           const bool enc = active & !anchor;
-          if (enc & (fin == 0)) brow[nb++] = vbal;  // the row's balance list (D9)
           if (STAB) {  // branch-free: lanes without a code take the empty entry
             const uint2 e = lds_v2(tab_s + ((unsigned)(enc ? fin : nalpha) << 3));
             acc |= (unsigned long long)e.x << ((64 - na - (int)e.y) & 63);
