@@ -50,9 +50,11 @@ def _generate(kind: str, dims, seed: int) -> np.ndarray:
         return synthetic.generate(kind, shape=dims).numpy()
     r, c = dims or (512, 512)
     rng = np.random.default_rng(seed)
-    if kind == "sine2d":
+    if kind == "sine2d":  # sin(2 pi r / rows) sin(2 pi c / cols) + 2.0, strictly positive
         i, j = np.meshgrid(np.arange(r), np.arange(c), indexing="ij")
-        return (np.sin(2 * np.pi * i / 64.0) * np.cos(2 * np.pi * j / 97.0) * 100).astype(np.float32)
+        return (np.sin(2 * np.pi * i / r) * np.sin(2 * np.pi * j / c) + 2.0).astype(np.float32)
+    if kind == "constant":
+        return np.full((r, c), 1.0, np.float32)
     if kind == "gaussian-field":
         import torch
         g = torch.Generator().manual_seed(seed)
@@ -76,15 +78,17 @@ def _read_input(a) -> tuple[np.ndarray, str]:
     try:
         if fmt == "npy":
             x = np.load(src)
-        elif fmt in ("raw32", "raw64"):
-            x = np.fromfile(src, dtype=np.float32 if fmt == "raw32" else np.float64)
+        elif fmt == "raw64":
+            raise E.ConfigError("--format raw64: 64-bit elements are not supported by the device path (raw32 only)")
+        elif fmt == "raw32":
+            x = np.fromfile(src, dtype=np.float32)
             if a.dims:
                 r, c = _dims(a.dims)
                 if x.size != r * c:
                     raise E.IngestError(f"{src!r} holds {x.size} values, --dims asks for {r * c}")
                 x = x.reshape(r, c)
         else:
-            raise E.ConfigError(f"unknown --format {fmt!r} (raw32 | raw64 | npy | gen:<kind>)")
+            raise E.ConfigError(f"unknown --format {fmt!r} (raw32 | npy | segy | gen:<kind>)")
     except OSError as ex:
         raise E.IngestError(f"cannot read {src!r}: {ex}")
     if x.dtype != np.float32:

@@ -71,23 +71,36 @@ def record_offsets(sizes, header_bytes: int) -> np.ndarray:
     return header_bytes + np.concatenate([[0], np.cumsum(s)[:-1]])
 
 
+def _host_backend(group=None) -> bool:
+    """gloo (the CPU backend of the multi-process tests) takes host tensors."""
+    import torch.distributed as dist
+    return dist.get_backend(group) != "nccl"
+
+
 def exchange_record_sizes(nbytes: int, group=None, device=None):
     """All-gather of (record bytes) over the process group -> per-rank sizes."""
     import torch
     import torch.distributed as dist
     world = dist.get_world_size(group)
-    t = torch.tensor([int(nbytes)], dtype=torch.int64, device=device)
+    t = torch.tensor([int(nbytes)], dtype=torch.int64, device="cpu" if _host_backend(group) else device)
     out = [torch.zeros_like(t) for _ in range(world)]
     dist.all_gather(out, t, group=group)
     return [int(o.item()) for o in out]
 
 
 def make_allreduce(group=None):
-    """Sum-all-reduce callback used between the compress stages."""
+    """Sum-all-reduce callback used between the compress stages (NCCL on the
+    device tensor; through host memory for a CPU backend)."""
     import torch.distributed as dist
+    host = _host_backend(group)
 
     def _ar(t):
-        dist.all_reduce(t, group=group)
+        if host and t.is_cuda:
+            h = t.cpu()
+            dist.all_reduce(h, group=group)
+            t.copy_(h)
+        else:
+            dist.all_reduce(t, group=group)
     return _ar
 
 

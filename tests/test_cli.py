@@ -20,6 +20,23 @@ def test_exit_codes_per_family(tmp_path, capsys):
     capsys.readouterr()
 
 
+def test_generators_follow_spec(tmp_path):
+    """sine2d = sin(2 pi r/rows) sin(2 pi c/cols) + 2.0 (strictly
+    positive, no zeros); constant -> all equal; same seed -> identical; raw64
+    is reported unsupported (ConfigError, exit 2)."""
+    x = cli._generate("sine2d", (64, 48), 0)
+    r, c = np.meshgrid(np.arange(64), np.arange(48), indexing="ij")
+    ref = (np.sin(2 * np.pi * r / 64) * np.sin(2 * np.pi * c / 48) + 2.0).astype(np.float32)
+    assert x.dtype == np.float32 and np.array_equal(x, ref) and x.min() >= 1.0
+    k = cli._generate("constant", (5, 7), 0)
+    assert np.all(k == k.flat[0])
+    assert np.array_equal(cli._generate("white-noise", (9, 9), 4), cli._generate("white-noise", (9, 9), 4))
+    raw = tmp_path / "a.f64"
+    np.zeros(12, np.float64).tofile(raw)
+    assert cli.main(["compress", "--input", str(raw), "--format", "raw64", "--dims", "3x4",
+                     "--output", str(tmp_path / "o.pmz")]) == 2
+
+
 @pytest.mark.gpu
 def test_cli_roundtrip_and_original(tmp_path, capsys):
     x = np.ascontiguousarray(np.random.default_rng(3).normal(0, 1, (200, 300)).astype(np.float32) * 10)

@@ -161,22 +161,33 @@ def test_config_errors(codec):
             P.compress(np.ones((8, 8), np.float32), rel_error=br, device="cuda:0")
 
 
-def test_decompress_corrupted_payload(codec, oracle):
-    """Flipped payload bits surface as coding/container errors, never a crash."""
+@pytest.mark.parametrize("path", ["latency", "throughput"])
+def test_decompress_corrupted_payload(codec, oracle, path):
+    """AC7: 20 mutated payload fixtures.  Each either raises a
+    coding/container error or decodes to a grid that differs from the clean
+    decode -- a flipped payload byte must never pass unnoticed -- and never
+    crashes or hangs."""
     import paper_2309_09778_b200 as P
     from paper_2309_09778_b200 import errors as E
     x = _field("C2", (256, 256))
     buf, _ = oracle.compress(x, oracle.OracleConfig(b_r=1e-2))
+    with _path(path):
+        clean = P.decompress(buf, device="cuda:0")
     a = bytearray(buf)
-    for k in range(1, 21):  # AC7: 20 mutated fixtures
+    raised = 0
+    for k in range(1, 21):
         b = bytearray(a)
         pos = len(b) - 37 * k
         b[pos] ^= 0xFF
         try:
-            y = P.decompress(bytes(b), device="cuda:0")
-            assert y.shape == (256, 256)
+            with _path(path):
+                y = P.decompress(bytes(b), device="cuda:0")
         except E.PermezError:
-            pass
+            raised += 1
+            continue
+        assert y.shape == (256, 256)
+        assert not np.array_equal(y.view(np.uint32), clean.view(np.uint32)), f"mutation at byte {pos} passed unnoticed"
+    assert raised > 0
 
 
 def test_log2_device_matches_oracle(oracle):
@@ -316,8 +327,9 @@ def _record_fields(buf: bytes, P):
     return int(offs[0]), h
 
 
+@pytest.mark.parametrize("path", ["latency", "throughput"])
 @pytest.mark.parametrize("what", ["bits_minus1", "bits_plus1", "bits_huge", "nbal_plus", "nbal_minus"])
-def test_decompress_corrupted_tables(codec, oracle, what):
+def test_decompress_corrupted_tables(codec, oracle, what, path):
     """Targeted corruption of block 0's record.  Every partition of a block
     waits for the balance counts of the partitions before it (decoupled
     look-back), so a failing partition must still release the later ones:
@@ -348,7 +360,7 @@ def test_decompress_corrupted_tables(codec, oracle, what):
     else:
         (nb,) = struct.unpack_from("<Q", a, nb_at)
         struct.pack_into("<Q", a, nb_at, nb + (1 if what == "nbal_plus" else -1))
-    with pytest.raises(E.PermezError):
+    with pytest.raises(E.PermezError), _path(path):
         P.decompress(bytes(a), device="cuda:0")
 
 
