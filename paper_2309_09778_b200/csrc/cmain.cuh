@@ -667,8 +667,8 @@ __global__ void __launch_bounds__(kCWW * 32) k_c_write(Geom g, const BlkP *__res
   if (nbytes == 0) return;
   const unsigned rstart = ib - ri.x;  // exclusive prefix: first bit of this lane's row
   const unsigned *rbase = rowbits + (p * g.prow) * (int64_t)g.bc;
-  if (C < 33) {
-    // rows may be shorter than a word: one lane assembles the partition bit by bit (edge blocks only)
+  if (C < 129) {
+    // rows may be shorter than a 16-byte chunk: one lane assembles the partition byte by byte (narrow blocks)
     if (lane == 0) {
       unsigned long long accb = 0;
       int nacc = 0;
@@ -693,49 +693,80 @@ __global__ void __launch_bounds__(kCWW * 32) k_c_write(Geom g, const BlkP *__res
     }
     return;
   }
-  // words of the container overlapping [pay0, pay0 + nbytes)
-  const unsigned long long w0 = pay0 >> 2, w1 = (pay0 + nbytes - 1) >> 2;
-  const unsigned nw = (unsigned)(w1 - w0 + 1);
-  int rlo = 0;  // warp-uniform: the row of this round's first word
-  for (unsigned j0 = 0; j0 < nw; j0 += 32) {
-    const unsigned j = j0 + lane;
-    const long long sb = 8ll * (long long)((w0 + j) * 4ull) - 8ll * (long long)pay0;  // stream bit of the word's first byte
+  // 16-byte chunks of the container overlapping [pay0, pay0 + nbytes): each
+  // lane assembles 128 stream bits from at most two rows (rows hold >= 128
+  // bits when C > 128; narrower blocks took the lane-0 path above), the two
+  // ends byte by byte
+  const unsigned long long q0 = pay0 >> 4, q1 = (pay0 + nbytes - 1) >> 4;
+  const unsigned nq = (unsigned)(q1 - q0 + 1);
+  int rlo = 0;  // warp-uniform: the row of the next round's first chunk
+  for (unsigned jb = 0; jb < nq; jb += 32) {
+    const unsigned j = jb + lane;
+    const long long sb = 8ll * (long long)((q0 + j) * 16ull) - 8ll * (long long)pay0;  // stream bit of the chunk
     const unsigned s = sb < 0 ? 0u : (unsigned)sb;
     const unsigned s_last = __shfl_sync(0xffffffffu, s, 31);
-    // row holding bit s: the last row starting at or before it (rows are >= 32 bits, so a word meets at most two)
     int r = rlo;
     for (int q = rlo + 1; q < R; q++) {
       const unsigned st_q = __shfl_sync(0xffffffffu, rstart, q);
       if (st_q > s_last) break;
       r = s >= st_q ? q : r;
     }
-    const unsigned rs = __shfl_sync(0xffffffffu, rstart, r & 31);
-    const unsigned rl = __shfl_sync(0xffffffffu, ri.x, r & 31);
-    unsigned v = 0;
-    if (j < nw && s < total) {
-      const unsigned off = s - rs;
-      const unsigned *rp = rbase + (int64_t)r * g.bc;
-      const unsigned a0 = rp[off >> 5];
-      const unsigned a1 = (off >> 5) + 1 < (rl + 31) / 32 ? rp[(off >> 5) + 1] : 0u;
-      v = __funnelshift_l(a1, a0, off & 31);
-      const unsigned left = rl - off;  // bits of row r from s
-      if (left < 32) {
-        v &= ~(0xffffffffu >> left);  // keep the row's last bits
-        if (r + 1 < R) v |= rbase[(int64_t)(r + 1) * g.bc] >> left;
-      }
-      if (sb < 0) v >>= (unsigned)(-sb);
-    }
     rlo = __shfl_sync(0xffffffffu, r, 31);
-    if (j < nw) {
-      const unsigned long long A = (w0 + j) * 4ull;
-      if (A >= pay0 && A + 4 <= pay0 + nbytes) {
-        *reinterpret_cast<unsigned *>(out + A) = bswap32(v);
-      } else {
+    const unsigned off = s - __shfl_sync(0xffffffffu, rstart, r & 31);
+    const unsigned rl = __shfl_sync(0xffffffffu, ri.x, r & 31);
+    if (j >= nq) continue;
+    unsigned o[4] = {0u, 0u, 0u, 0u};
+    if (s < total) {
+      const unsigned *rp = rbase + (int64_t)r * g.bc;
+      const unsigned nwr = (rl + 31) >> 5, wb = off >> 5, sh = off & 31;
+      unsigned w[5];
 #pragma unroll
-        for (int q = 0; q < 4; q++) {
-          const unsigned long long a = A + q;
-          if (a >= pay0 && a < pay0 + nbytes) out[a] = (uint8_t)(v >> (24 - 8 * q));
+      for (int k = 0; k < 5; k++) w[k] = wb + k < nwr ? __ldg(rp + wb + k) : 0u;
+      const unsigned left = rl - off;  // bits of row r from s (the row's words are zero past its end)
+      unsigned n[4] = {0u, 0u, 0u, 0u};
+      if (left < 128 && r + 1 < R) {
+        const unsigned *np_ = rbase + (int64_t)(r + 1) * g.bc;
+#pragma unroll
+        for (int k = 0; k < 4; k++) n[k] = __ldg(np_ + k);
+      }
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        unsigned v = __funnelshift_l(w[k + 1], w[k], sh);  // row r bits from off + 32 k
+        // row r + 1 bits: its bit (32 k - left + i) lands at position i of this word
+        const int dpos = 32 * k - (int)left;
+        unsigned t = 0;
+        if (dpos >= 0) {
+          const unsigned di = (unsigned)dpos >> 5, ds = (unsigned)dpos & 31;
+          const unsigned na = di < 4 ? n[di] : 0u, nb2 = di + 1 < 4 ? n[di + 1] : 0u;
+          t = __funnelshift_l(nb2, na, ds);
+        } else if (dpos > -32) {
+          t = n[0] >> (unsigned)(-dpos);
         }
+        if (left <= 32u * k) v = 0u;
+        else if (left < 32u * (k + 1)) v &= ~(0xffffffffu >> (left - 32u * k));
+        o[k] = v | t;
+      }
+      if (sb < 0) {  // the chunk starts before the stream: shift right by -sb bits (< 128)
+        const unsigned d = (unsigned)(-sb);
+        unsigned t4[4];
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+          const int src = k - (int)(d >> 5);
+          const unsigned hiw = src >= 0 ? o[src] : 0u, low = src - 1 >= 0 ? o[src - 1] : 0u;
+          t4[k] = (d & 31) ? ((hiw >> (d & 31)) | (low << (32 - (d & 31)))) : hiw;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; k++) o[k] = t4[k];
+      }
+    }
+    const unsigned long long A = (q0 + j) * 16ull;
+    if (A >= pay0 && A + 16 <= pay0 + nbytes) {
+      *reinterpret_cast<uint4 *>(out + A) = make_uint4(bswap32(o[0]), bswap32(o[1]), bswap32(o[2]), bswap32(o[3]));
+    } else {
+#pragma unroll
+      for (int qb = 0; qb < 16; qb++) {
+        const unsigned long long aq = A + qb;
+        if (aq >= pay0 && aq < pay0 + nbytes) out[aq] = (uint8_t)(o[qb >> 2] >> (24 - 8 * (qb & 3)));
       }
     }
   }
