@@ -366,17 +366,22 @@ def main():
         return {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
                 "kernel": what, "ms": ms, "alg_bytes_per_elem": alg, "peak_kind": peak_kind}
 
-    traffic = None
+    # DRAM bytes per launch of the dominant kernels from the committed ncu
+    # capture of this configuration (tools/profile_round.sh -> profiles/)
+    tr = {}
     tr_path = os.path.join(ROOT, "profiles", "traffic_latest.json")
-    if os.path.exists(tr_path):
+    if os.path.exists(tr_path) and world == 1:
         try:
-            traffic = json.load(open(tr_path)).get("compress_dominant_bytes_per_launch")
+            tr = json.load(open(tr_path))
         except Exception:
-            traffic = None
+            tr = {}
     roof_c = roof(float(cs[ic]), names_c[ic])
-    roof_c["traffic"] = traffic
+    roof_c["traffic"] = tr.get("compress_dominant_bytes_per_launch")
+    roof_c["traffic_kernel"] = tr.get("compress_dominant_kernel")
     roof_c["pipeline"] = roof(c_step, "whole compress")
     roof_d = roof(float(ds[id_]), names_d[id_])
+    roof_d["traffic"] = tr.get("decompress_dominant_bytes_per_launch")
+    roof_d["traffic_kernel"] = tr.get("decompress_dominant_kernel")
     roof_d["pipeline"] = roof(d_step, "whole decompress")
 
     # CPU baseline + parity on the same sample (rank 0, N = 1): the oracle

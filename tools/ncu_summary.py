@@ -56,10 +56,18 @@ def main():
             except (KeyError, ValueError):
                 pass
     open(dst, "w").write("\n".join(lines) + "\n")
+    tr = {}
     for name, b in traffic.items():
-        if "k_compress_ws" in name:
-            path = os.path.join(os.path.dirname(__file__), "..", "profiles", "traffic_latest.json")
-            json.dump({"k_compress_ws_bytes_per_launch": b, "source": os.path.basename(dst)}, open(path, "w"))
+        if "k_c_main<3, 0, 1>" in name:  # the dominant compress kernel (bench roofline.traffic)
+            tr["compress_dominant_bytes_per_launch"] = b
+            tr["compress_dominant_kernel"] = name
+        if "k_d_recon" in name:  # the dominant decompress kernel
+            tr["decompress_dominant_bytes_per_launch"] = b
+            tr["decompress_dominant_kernel"] = name
+    if tr:
+        tr["source"] = os.path.basename(dst)
+        path = os.path.join(os.path.dirname(__file__), "..", "profiles", "traffic_latest.json")
+        json.dump(tr, open(path, "w"), indent=1)
     print("\n".join(lines))
 
 

@@ -1,14 +1,22 @@
 #!/bin/bash
 # Run on the GPU box (gpurun): bench line, launch list, full captures of the
-# dominant compress / decompress kernels.  Outputs under gpurun_out/.
+# dominant compress / decompress kernels at the metric's configuration (C5).
+# Outputs under gpurun_out/; summarise here with tools/launches.py and
+# tools/ncu_summary.py, then copy into profiles/ (see profiles/README.md).
 set -u
 mkdir -p gpurun_out
-timeout 600 python bench.py --steps 20 --warmup 5 > gpurun_out/bench.log 2>&1
+timeout 900 python bench.py > gpurun_out/bench.log 2>&1
+echo "bench rc=$?"
 tail -1 gpurun_out/bench.log > gpurun_out/bench.json
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
-  python bench.py --warmup 0 --profile-steps 2 --no-cpu-baseline > gpurun_out/ncu_launches.log 2>&1
-for k in k_compress_ws k_write_part k_fwd k_quant k_codebook k_decode4 k_reconstruct4 k_inv; do
-  timeout 600 ncu --set full --clock-control none --import-source on -k regex:$k -c 1 -o gpurun_out/full_$k \
-    python bench.py --warmup 0 --profile-steps 1 --no-cpu-baseline > gpurun_out/ncu_$k.log 2>&1
-done
+# every launch of one compress + one decompress step (cold, serialised: shares, not absolutes)
+timeout 900 python bench.py --warmup 0 --profile-steps 1 --no-cpu-baseline --no-e2e > gpurun_out/plain_prof.log 2>&1 && \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
+  python bench.py --warmup 0 --profile-steps 1 --no-cpu-baseline --no-e2e > gpurun_out/ncu_launches.log 2>&1
+echo "launches rc=$?"
+# the dominant kernels, one launch each (C5 through tools/scale_prof.py)
+python tools/scale_prof.py C5 > gpurun_out/plain5.log 2>&1 && \
+timeout 1200 ncu --set full --clock-control none --import-source on --kernel-name-base mangled \
+  -k regex:"k_c_mainILi3ELi0ELb1|k_c_write|k_stats|k_d_decode|k_d_reconILi3" -c 5 -o gpurun_out/full_c5 \
+  python tools/scale_prof.py C5 > gpurun_out/ncu_full.log 2>&1
+echo "full rc=$?"
 ls -la gpurun_out
