@@ -175,6 +175,7 @@ def main():
     ap.add_argument("--eps", type=float, default=1e-2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-fp32", action="store_true", help="skip the FP32 perceptron perf-mode measurement")
     ap.add_argument("--profile-steps", type=int, default=0, help="(ncu) run this many steps, no JSON timing claims")
     args = ap.parse_args()
     if args.profile_steps == 0:
@@ -296,6 +297,82 @@ def main():
     comp_gbs = bytes_all / (c_step / 1e3) / 1e9
     dec_gbs = bytes_all / (d_step / 1e3) / 1e9
 
+    # FP32 perceptron perf mode (north star; container version 2): the same
+    # field and timing, plus the perceptron-rounding mismatch counters against
+    # the FP64 path (final codes and balance points compared position by
+    # position through the code dumps) and the bound on every point
+    fp32 = None
+    if not args.no_fp32:
+        from paper_2309_09778_b200.pipeline import code_mismatches
+        cfg32 = P.CompressConfig(rel_error=args.eps, repair_factor=1.0, precision="fp32")
+        offs32 = torch.empty(nblk + 1, dtype=torch.int64, device=dev)
+
+        def compress32(ev=None, c=cfg32):
+            b, i = codec.compress_staged(x, c, block_row0=plan.block_row0, global_rows=grows,
+                                         allreduce=allreduce if sharded else None, block_offsets=offs32, events=ev,
+                                         d_val=d_val)
+            if sharded:
+                exchange_record_sizes(i.nbytes - i.header_bytes, device=dev)
+            return b, i
+
+        b32, i32 = compress32()
+        h32 = P.Codec.parse_header(b32[: min(int(i32.nbytes), 1 << 20)].cpu().numpy())
+        h32.rows, h32.nblocks = x.shape[0], nblk
+        db32, do32 = b32.clone(), offs32.clone()
+        y32 = torch.empty(x.shape, dtype=torch.float32, device=dev)
+        codec.decompress_device(db32, h32, do32, out=y32)
+        torch.cuda.synchronize()
+        mr32 = 0.0
+        for r0 in range(0, x.shape[0], 65536):
+            xa, ya = x[r0: r0 + 65536].double(), y32[r0: r0 + 65536].double()
+            xz = torch.where(xa.abs() <= EPS0, torch.zeros_like(xa), xa)
+            nz = xz != 0
+            if bool(nz.any()):
+                mr32 = max(mr32, float(((ya - xz).abs() / xz.abs())[nz].max()))
+            assert bool((ya[~nz] == 0).all())
+        assert mr32 <= args.eps, mr32
+        del xa, ya, xz, nz
+        c32_ms, d32_ms = [], []
+        for it in range(1 + K):
+            if sharded:
+                dist.barrier()
+            torch.cuda.synchronize()
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(codec.stage_names_compress) + 1)]
+            compress32(ev)
+            torch.cuda.synchronize()
+            dv = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            codec.decompress_device(db32, h32, do32, out=y32, events=dv)
+            torch.cuda.synchronize()
+            if it:  # the first pass warms up
+                c32_ms.append(ev[0].elapsed_time(ev[-1]))
+                d32_ms.append(dv[0].elapsed_time(dv[2]))
+        t32 = torch.tensor([sum(c32_ms) / K, sum(d32_ms) / K], dtype=torch.float64, device=dev)
+        # mismatch counters: one compress of each precision into a code dump
+        nd = codec.code_dump_numel(x.shape, cfg)
+        dmp = {}
+        for prec in ("fp64", "fp32"):
+            dmp[prec] = torch.full((nd,), 0xFFFE, dtype=torch.int32, device=dev).to(torch.uint16)
+            cd = P.CompressConfig(rel_error=args.eps, repair_factor=1.0, precision=prec, code_dump=dmp[prec])
+            compress32(c=cd)
+        cm = code_mismatches(dmp["fp64"], dmp["fp32"])
+        del dmp
+        cnt = torch.tensor([cm["codes"], cm["code_mismatches"], cm["balance_mismatches"],
+                            int(i32.nbytes - i32.header_bytes), int(i32.nbal)], dtype=torch.float64, device=dev)
+        if sharded:
+            dist.all_reduce(t32, op=dist.ReduceOp.MAX)
+            dist.all_reduce(cnt)
+        cr32 = (float(cnt[3]) + i32.header_bytes) / bytes_all
+        fp32 = {"value": bytes_all / (float(t32[0]) / 1e3) / 1e9, "unit": "GB/s", "ms_per_step": float(t32[0]),
+                "decompress": {"value": bytes_all / (float(t32[1]) / 1e3) / 1e9, "unit": "GB/s",
+                               "ms_per_step": float(t32[1])},
+                "container_version": int(h32.version), "compression_ratio": cr32,
+                "cr_delta_vs_fp64": (cr32 - cr) / cr, "max_rel_err": mr32,
+                "codes": int(cnt[0]), "code_mismatches_vs_fp64": int(cnt[1]),
+                "code_mismatch_frac": float(cnt[1]) / max(1.0, float(cnt[0])),
+                "balance_point_mismatches_vs_fp64": int(cnt[2]), "balance_count": int(cnt[4]),
+                "note": "float32 surfaces, predictor, quantizer and recurrence; every point within the bound"}
+        del y32, db32, b32
+
     # e2e through the public API with pinned host buffers, every step: H2D of
     # the field, compress, D2H of the container; H2D of the container + block
     # index walk on the host, decompress, D2H of the float32 grid
@@ -305,7 +382,7 @@ def main():
         h_in.copy_(x)
         h_out = torch.empty(int(info.nbytes) + (1 << 20), dtype=torch.uint8, pin_memory=True)
         h_cont = torch.empty(int(info.nbytes), dtype=torch.uint8, pin_memory=True)
-        h_cont.copy_(buf)
+        h_cont.copy_(dbuf)  # (the FP64 container: the codec buffer now holds the FP32 run)
         h_y = torch.empty(x.shape, dtype=torch.float32, pin_memory=True)
         xd = torch.empty_like(x)
         e_ms, ed_ms = [], []
@@ -424,6 +501,7 @@ def main():
             "roofline": roof_c,
             "stages_ms": {"compress": dict(zip(names_c, cs.tolist())), "decompress": dict(zip(names_d, ds.tolist()))},
             "parity": parity,
+            "fp32_mode": fp32,
             "cpu_baseline": cpu_base,
             "gpu_launches": launches,
             "clocks": clocks,

@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define PMZ_ABI_VERSION 1
+#define PMZ_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define PMZ_API __attribute__((visibility("default")))
@@ -79,6 +79,19 @@ typedef struct pmz_params {
   int32_t S;              /* surface size: 3 (2-D) or 1 (1-D)   */
   int32_t H;              /* hidden width, 2                                 */
   int32_t m;              /* code width; 0 = select_m on validation blocks   */
+  int32_t precision;      /* 0: FP64 parity -- the reference's arithmetic,
+                           *    container version 1 (the default);
+                           * 1: FP32 perceptron perf mode (north star):
+                           *    float32 surfaces, predictor, quantizer and
+                           *    recurrence, container version 2; 2-D fields
+                           *    only (throughput path), codes may differ from
+                           *    version 1 where float32 rounding moves them   */
+  int32_t reserved;       /* 0                                               */
+  uint64_t d_code_dump;   /* 0, or a device address of
+                           * pmz_code_dump_elems() uint16: every final code
+                           * (raster per 32-row partition, 0xFFFF at the
+                           * anchor) -- for counting code mismatches between
+                           * the two precisions                              */
 } pmz_params;
 
 /* Shard geometry: this process holds rows [0, rows) of its shard, which are
@@ -128,6 +141,9 @@ typedef struct pmz_np_fix {
 
 /* library / ABI identification */
 PMZ_API int pmz_abi_version(void);
+/* elements of the pmz_params::d_code_dump buffer for a shard geometry:
+ * partitions x partition_rows x block_cols */
+PMZ_API int pmz_code_dump_elems(const pmz_params *p, const pmz_geom *g, uint64_t *elems);
 PMZ_API const char *pmz_status_string(int status);
 
 /* Workspace bytes for a shard.  Replaces nothing in the reference (the

@@ -25,7 +25,7 @@ class Params(ctypes.Structure):
         ("b_r", c_double), ("b_a", c_double), ("onepbr2", c_double), ("eps0", c_double), ("repair_t", c_double),
         ("coverage_target", c_double), ("slope", c_double), ("w1", c_double * 8), ("w2", c_double * 2),
         ("block_rows", c_int32), ("block_cols", c_int32), ("partition_rows", c_int32), ("S", c_int32),
-        ("H", c_int32), ("m", c_int32),
+        ("H", c_int32), ("m", c_int32), ("precision", c_int32), ("reserved", c_int32), ("d_code_dump", c_uint64),
     ]
 
 
@@ -59,6 +59,7 @@ class NpFix(ctypes.Structure):
 
 _SIGS = {
     "pmz_abi_version": (c_int32, []),
+    "pmz_code_dump_elems": (c_int32, [ctypes.POINTER(Params), ctypes.POINTER(Geom), ctypes.POINTER(c_uint64)]),
     "pmz_status_string": (ctypes.c_char_p, [c_int32]),
     "pmz_workspace_size": (c_int32, [ctypes.POINTER(Params), ctypes.POINTER(Geom), ctypes.POINTER(c_uint64)]),
     "pmz_max_container_size": (c_int32, [ctypes.POINTER(Params), ctypes.POINTER(Geom), ctypes.POINTER(c_uint64)]),
@@ -150,7 +151,7 @@ def load():
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
-        if lib.pmz_abi_version() != 1:
+        if lib.pmz_abi_version() != 2:
             raise DeviceError("ABI version mismatch")
         _lib = lib
     return _lib

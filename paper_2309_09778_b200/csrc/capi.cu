@@ -20,6 +20,7 @@
 #include "segy.cuh"
 #include "tdec.cuh"
 #include "cmain.cuh"
+#include "cmain32.cuh"
 #include "dmain.cuh"
 
 using namespace pmz;
@@ -46,6 +47,9 @@ int check_params(const pmz_params *p) {
   if (p->H != 2) return PMZ_ERR_CONFIG;
   if (p->m != 0 && (p->m < 4 || p->m > 16)) return PMZ_ERR_CONFIG;
   if (!(p->b_a > 0.0) || !(p->repair_t > 0.0)) return PMZ_ERR_CONFIG;
+  if (p->precision != 0 && p->precision != 1) return PMZ_ERR_CONFIG;
+  if ((p->precision == 1 || p->d_code_dump) && (p->S != 3 || p->block_rows == 1))
+    return PMZ_ERR_CONFIG;  // FP32 mode and code dumps: 2-D fields (throughput path)
   return PMZ_OK;
 }
 
@@ -69,8 +73,11 @@ Geom make_geom(int64_t rows, int64_t cols, int br, int bc, int prow, int64_t blo
 }
 
 Geom geom_of(const pmz_params *p, const pmz_geom *g) {
-  return make_geom((int64_t)g->rows, (int64_t)g->cols, p->block_rows, p->block_cols, p->partition_rows,
-                   (int64_t)g->block_row0);
+  Geom G = make_geom((int64_t)g->rows, (int64_t)g->cols, p->block_rows, p->block_cols, p->partition_rows,
+                     (int64_t)g->block_row0);
+  G.fp32 = p->precision == 1;
+  G.force_tpath = p->d_code_dump != 0;
+  return G;
 }
 
 // weights equal init_model(S) -> constant-folded predictor
@@ -110,6 +117,8 @@ KParams kparams(const pmz_params *p) {
   k.dpos_p = k.dpos + 0x1p-20;
   k.dneg_p = k.dneg - 0x1p-20;
   k.init_model = is_init_model(p->S, p->w1, p->w2);
+  k.precision = p->precision;
+  k.code_dump = p->d_code_dump;
   // certified-rounding margins of the approximate TRUE residual (cmain.cuh):
   // |v~ - v| < 2^-41 per surface value moves a hidden pre-activation by at most
   // sum_k |w1_kj| 2^-41 (+ roundings) and the residual by amp 2^-41; 2^-37
@@ -147,6 +156,7 @@ bool one_row_parts(const Geom &G) { return G.br == 1 || G.rows == 1; }
 // kernels also split each partition's work across a CTA.  PMZ_PATH=latency |
 // throughput overrides the size rule (tests exercise both on small fields).
 bool use_tpath(const Geom &G) {
+  if (G.fp32 || G.force_tpath) return true;  // the FP32 perf mode and the code dump: throughput path only
   if (one_row_parts(G)) return false;
   const char *e = getenv("PMZ_PATH");
   if (e && e[0] == 'l') return false;
@@ -223,6 +233,7 @@ CMainOut cmain_out(void *d_ws, const WsLayout &L) {
   o.cw = at<unsigned>(d_ws, L.cw);
   o.hist = at<unsigned long long>(d_ws, L.hist);
   o.cov = at<unsigned long long>(d_ws, L.cov);
+  o.dump = nullptr;
   return o;
 }
 template <int PK, int MODE>
@@ -232,22 +243,25 @@ void launch_cmain(const float *x, const Geom &G, const KParams &k, const int64_t
   if (MODE == kCMain) grid = (unsigned)((G.nparts + kCW - 1) / kCW);
   else grid = (unsigned)(n_val * ((G.np_full + kCW - 1) / kCW));
   if (grid == 0) return;
-  // m is selected on the device: size for the largest shared-memory table
+  CMainOut o = cmain_out(d_ws, L);
+  if (MODE == kCMain) o.dump = reinterpret_cast<uint16_t *>(k.code_dump);
+  // m is selected on the device: size for the largest shared-memory table;
+  // alphabets above 2^12 take the launch whose codewords come from global memory
   const int smem = (int)cmain_smem_bytes(MODE, MODE == kCHist ? 13 : 12);
-  cudaFuncSetAttribute(k_c_main<PK, MODE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  k_c_main<PK, MODE, true><<<grid, kCW * 32, smem, st>>>(x, G, k, at<BlkP>(d_ws, L.blkp),
-                                                         at<WsStatus>(d_ws, L.status), d_val, n_val,
-                                                         cmain_out(d_ws, L));
+  const int smem2 = (int)cmain_smem_bytes(MODE, 16);
+  auto *fa = k.precision ? k_c_main32<PK, MODE, true> : k_c_main<PK, MODE, true>;
+  auto *fb = k.precision ? k_c_main32<PK, MODE, false> : k_c_main<PK, MODE, false>;
+  cudaFuncSetAttribute(fa, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  fa<<<grid, kCW * 32, smem, st>>>(x, G, k, at<BlkP>(d_ws, L.blkp), at<WsStatus>(d_ws, L.status), d_val, n_val, o);
   if (getenv("PMZ_DEBUG")) {
     const cudaError_t e = cudaStreamSynchronize(st);
-    if (e != cudaSuccess) fprintf(stderr, "permez: k_c_main<%d,%d,1>: %s\n", PK, MODE, cudaGetErrorString(e));
+    if (e != cudaSuccess) fprintf(stderr, "permez: k_c_main%s<%d,%d,1>: %s\n", k.precision ? "32" : "", PK, MODE,
+                                  cudaGetErrorString(e));
   }
-  if (MODE == kCMain) {  // alphabets above 2^12 (m is selected on the device): codewords from global memory
-    const int smem2 = (int)cmain_smem_bytes(MODE, 16);
-    cudaFuncSetAttribute(k_c_main<PK, MODE, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
-    k_c_main<PK, MODE, false><<<grid, kCW * 32, smem2, st>>>(x, G, k, at<BlkP>(d_ws, L.blkp),
-                                                             at<WsStatus>(d_ws, L.status), d_val, n_val,
-                                                             cmain_out(d_ws, L));
+  if (MODE == kCMain) {
+    cudaFuncSetAttribute(fb, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
+    fb<<<grid, kCW * 32, smem2, st>>>(x, G, k, at<BlkP>(d_ws, L.blkp), at<WsStatus>(d_ws, L.status), d_val, n_val,
+                                      o);
   }
 }
 template <int MODE>
@@ -289,6 +303,14 @@ void launch_quant(const KParams &k, cudaStream_t st, const Geom &G, void *d_ws, 
 // C linkage comes from the declarations in permez_b200.h.
 
 int pmz_abi_version(void) { return PMZ_ABI_VERSION; }
+
+int pmz_code_dump_elems(const pmz_params *p, const pmz_geom *g, uint64_t *elems) {
+  int s = check_params(p);
+  if (s) return s;
+  const Geom G = geom_of(p, g);
+  *elems = (uint64_t)G.nparts * (uint64_t)G.prow * (uint64_t)G.bc;
+  return PMZ_OK;
+}
 
 const char *pmz_status_string(int s) {
   switch (s) {
@@ -666,7 +688,7 @@ int pmz_parse_header(const uint8_t *h, uint64_t n, pmz_header *hd) {
   if (memcmp(mg, "PMEZ", 4) != 0) return PMZ_ERR_BAD_MAGIC;
   hd->version = r.v<uint16_t>();
   if (r.err) return PMZ_ERR_CORRUPT;
-  if (hd->version != 1) return PMZ_ERR_UNSUPPORTED_VERSION;
+  if (hd->version != 1 && hd->version != 2) return PMZ_ERR_UNSUPPORTED_VERSION;  // 2: FP32 perf mode
   hd->elem = r.v<uint8_t>();
   hd->rows = r.v<uint64_t>();
   hd->cols = r.v<uint64_t>();
@@ -806,8 +828,10 @@ int launch_recon(const KParams &k, unsigned grid, cudaStream_t st, const Geom &G
 }
 
 Geom hdr_geom(const pmz_header *h) {
-  return make_geom((int64_t)h->rows, (int64_t)h->cols, (int)h->block_rows, (int)h->block_cols,
-                   (int)h->partition_rows, 0);
+  Geom G = make_geom((int64_t)h->rows, (int64_t)h->cols, (int)h->block_rows, (int)h->block_cols,
+                     (int)h->partition_rows, 0);
+  G.fp32 = h->version == 2;
+  return G;
 }
 KParams hdr_kparams(const pmz_header *h, double b_a) {
   KParams k{};
@@ -826,6 +850,7 @@ KParams hdr_kparams(const pmz_header *h, double b_a) {
   k.m_fixed = (int)h->m;
   k.inv_two_ba = 1.0 / (2.0 * b_a);
   k.init_model = is_init_model(k.S, k.w1, k.w2);
+  k.precision = h->version == 2 ? 1 : 0;
   return k;
 }
 }  // namespace
@@ -897,8 +922,9 @@ int pmz_decompress_run(const uint8_t *d_buf, uint64_t n, const pmz_header *hdr, 
     const unsigned grid = (unsigned)((G.nparts + kDRW - 1) / kDRW);
 #define PMZ_T_RECON(PKV)                                                                                            \
   do {                                                                                                              \
-    CK(cudaFuncSetAttribute(k_d_recon<PKV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDRecSmem));          \
-    k_d_recon<PKV><<<grid, kDRW * 32, kDRecSmem, st>>>(                                                             \
+    auto *fr = k.precision ? k_d_recon32<PKV> : k_d_recon<PKV>;                                                    \
+    CK(cudaFuncSetAttribute(fr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDRecSmem));                      \
+    fr<<<grid, kDRW * 32, kDRecSmem, st>>>(                                                                         \
         d_buf, n, G, k, at<BlkP>(d_ws, L.blkp), at<uint16_t>(d_ws, L.codes), at<unsigned>(d_ws, L.zflag),           \
         at<unsigned>(d_ws, L.rowz), at<double>(d_ws, L.anchors), at<unsigned long long>(d_ws, L.bal_off),           \
         at<unsigned long long>(d_ws, L.blk_nbal), center, d_out, S);                                                \

@@ -67,6 +67,7 @@ struct CMainOut {
   const uint8_t *lens;
   const unsigned *cw;
   unsigned long long *hist, *cov;
+  uint16_t *dump;               // optional: every final code, raster per partition (tcode_base), kAnc at the anchor
 };
 
 __host__ __device__ inline size_t cmain_smem_bytes(int mode, int m) {
@@ -327,6 +328,7 @@ __global__ void __launch_bounds__(kCW * 32, 2)
     unsigned *wp = MODE == kCMain ? o.rowbits + row * (int64_t)g.bc : nullptr;
     unsigned *const wp0 = wp;
     double *brow = MODE == kCMain ? o.balrow + row * (int64_t)g.bc : nullptr;
+    uint16_t *dump = (MODE == kCMain && o.dump) ? o.dump + tcode_base(g, p) + (int64_t)lane * C : nullptr;
 #ifdef PMZ_CSTATS
     unsigned cst[2] = {0, 0};
 #endif
@@ -471,6 +473,7 @@ __global__ void __launch_bounds__(kCW * 32, 2)
           }
         } else {
           const bool enc = active & !anchor;
+          if (dump != nullptr && active) dump[c] = anchor ? kAnc : (uint16_t)fin;
           if (STAB) {  // branch-free: lanes without a code take the empty entry
             const uint2 e = lds_v2(tab_s + ((unsigned)(enc ? fin : nalpha) << 3));
             acc |= (unsigned long long)e.x << ((64 - na - (int)e.y) & 63);

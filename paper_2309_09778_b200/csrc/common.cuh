@@ -23,6 +23,8 @@ struct KParams {
   double lk[4];            // log2(1 + r) series k1..k4 of the approximate forward map (cmain.cuh)
   double rnd_magic, e_magic;  // 1.5 2^52 (round to integer), 2^52 + 2^31 (int -> double)
   int init_model;          // weights equal init_model: constant-folded predictor
+  int precision;           // 0: FP64 parity (container version 1); 1: FP32 perceptron perf mode (version 2)
+  unsigned long long code_dump;  // device address of the optional final-code dump (CMainOut::dump), 0 = none
   double w1[8], w2[2];
   int S, H, block_rows, block_cols, partition_rows, m_fixed;
 };
@@ -37,6 +39,8 @@ struct Geom {
   int64_t nparts;
   int br_last;               // rows of the last block-row
   int nct;                   // 32x32 tiles per partition row-strip (ceil(bc / 32))
+  int fp32;                  // FP32 perceptron perf mode (container version 2): throughput path only
+  int force_tpath;           // a final-code dump was requested (throughput-path kernels write it)
 };
 
 // Partition-tiled layout of the per-element compress arrays (v, rq, cls):

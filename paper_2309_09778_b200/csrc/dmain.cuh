@@ -26,6 +26,7 @@
 #include "wsc.cuh"
 #include "tdec.cuh"
 #include "cmain.cuh"
+#include "cmain32.cuh"
 
 namespace pmz {
 
@@ -409,6 +410,171 @@ __global__ void __launch_bounds__(kDRW * 32, 3)
       const double vh = anchor ? anc : (isbal ? qv : __dadd_rn(a, dq));
       pn = nhl;
       hl = started ? vh : hl;
+      // inverse_map (transform.py:188-202) + float32 cast (D20)
+      // (lanes outside the partition and zero outputs evaluate 2^0.5 instead)
+      const bool negv = vh > bnd, zero = vh <= zthr;
+      const float e = d_exp2_f32((active & !zero) ? __dsub_rn(vh, negv ? lgn : lgp) : 0.5, tab_s, amb);
+      const float y = zero ? 0.0f : (negv ? -e : e);
+      if (active) ob = make_float4(ob.y, ob.z, ob.w, y);
+      if (vout) {
+        if (active & ((c & 3) == 3)) *reinterpret_cast<float4 *>(orow + (c - 3)) = ob;
+      } else if (active) {
+        orow[c] = y;
+      }
+    }
+  }
+  cp_async_wait<0>();
+  // the row's last 1-3 columns when C is not a multiple of 4
+  if (vout && lane_in && (C & 3)) {
+    const float v4[4] = {ob.x, ob.y, ob.z, ob.w};
+    for (int q = 0; q < (C & 3); q++) orow[C - (C & 3) + q] = v4[4 - (C & 3) + q];
+  }
+}
+
+// FP32 perceptron perf mode (container version 2): the mirror of k_c_main32
+// -- the same sweep as k_d_recon with the float32 recurrence; balance values
+// and anchors are the encoder's float32 values stored as doubles; the output
+// is inverse_map((double)vhat) exactly as the encoder's bound check saw it.
+template <int PK>
+__global__ void __launch_bounds__(kDRW * 32, 3)
+    k_d_recon32(const uint8_t *__restrict__ buf, unsigned long long buf_n, Geom g, const __grid_constant__ KParams k,
+              const BlkP *__restrict__ blkp, const uint16_t *__restrict__ codes, const unsigned *__restrict__ part_z,
+              const unsigned *__restrict__ rowz, const double *__restrict__ anchors,
+              const unsigned long long *__restrict__ bal_off, const unsigned long long *__restrict__ blk_nbal,
+              int center, float *__restrict__ out, WsStatus *st) {
+  extern __shared__ __align__(16) unsigned char smem_d[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  DRecWarp &S = reinterpret_cast<DRecWarp *>(smem_d)[warp];
+  double *s_e2 = reinterpret_cast<double *>(smem_d + sizeof(DRecWarp) * kDRW);
+  count_launch(st);
+  for (int i = threadIdx.x; i < 257; i += blockDim.x) s_e2[i] = kDExp2Tab[i];
+  __syncthreads();
+  const int64_t p = (int64_t)blockIdx.x * kDRW + warp;
+  if (p >= g.nparts) return;
+  int64_t b;
+  int pi;
+  part_of(g, p, b, pi);
+  const BlockBox bb = block_box(g, b);
+  const int pr0 = pi * g.prow, R = min(g.prow, bb.br - pr0), C = bb.bc;
+  float *op = out + (bb.r0 + pr0) * g.cols + bb.c0;
+  const BlkP P = blkp[b];
+  if (P.trivial) {
+    for (int r = 0; r < R; r++)
+      for (int c = lane; c < C; c += 32) op[(int64_t)r * g.cols + c] = 0.0f;
+    return;
+  }
+  if (st->err_bits) return;  // the decoder failed
+  const uint16_t *cb = codes + tcode_base(g, p);
+  // balance list of this row (D9): the block's list after the earlier partitions'
+  // and the earlier rows' code-0 counts
+  unsigned long long bj, bend;
+  {
+    const int64_t p0 = first_part(g, b);
+    unsigned zp = lane < pi ? part_z[p0 + lane] : 0u;
+    for (int o = 16; o; o >>= 1) zp += __shfl_xor_sync(0xffffffffu, zp, o);
+    const unsigned zr = lane < R ? rowz[p * g.prow + lane] : 0u;
+    unsigned incl = zr;
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    bj = (unsigned long long)zp + incl - zr;
+    bend = (unsigned long long)zp + incl;
+    const unsigned long long nbal = blk_nbal[b];
+    if (lane == 31 && pi == bb.np - 1 && bend != nbal)
+      set_err_at(st, bend > nbal ? PMZ_ERR_BALANCE_UNDERFLOW : PMZ_ERR_CORRUPT, 73, p);
+    if (__any_sync(0xffffffffu, bend > nbal)) {  // corrupt counts: never read past the list
+      if (lane == 0) set_err_at(st, PMZ_ERR_BALANCE_UNDERFLOW, 74, p);
+      return;
+    }
+  }
+  // balance values j of this row (bal_off + 8 j, any alignment): value j is
+  // bytes of the aligned words j and j + 1 (bq), which stream into an 8-word
+  // shared ring per row by cp.async six words ahead of their use
+  const uint8_t *bbase = buf + bal_off[b];
+  const unsigned bsh = (unsigned)(reinterpret_cast<uintptr_t>(bbase) & 7) * 8;
+  const unsigned long long *bq = reinterpret_cast<const unsigned long long *>(reinterpret_cast<uintptr_t>(bbase) & ~(uintptr_t)7);
+  const unsigned long long *bqlast =
+      reinterpret_cast<const unsigned long long *>((reinterpret_cast<uintptr_t>(buf + buf_n) - 1) & ~(uintptr_t)7);
+  const unsigned bal_s = smem_u32(S.bal + lane * 8);
+  auto issue_word = [&](unsigned long long w) {  // word w -> slot w & 7 (one cp.async group)
+    const unsigned long long *ap = bq + w;
+    const bool ok = w <= bend && ap <= bqlast;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(bal_s + 8u * (unsigned)(w & 7)),
+                 "l"(ok ? ap : bq), "r"(ok ? 8u : 0u)
+                 : "memory");
+    cp_async_commit();
+  };
+  for (unsigned i = 0; i < 7; i++) issue_word(bj + i);
+  const double anc = anchors[p];
+  unsigned *amb = &st->unresolved;
+  const float two_ba32 = (float)k.two_ba;
+  const double zthr = P.zero_threshold, bnd = P.boundary, lgp = P.lg_pos, lgn = P.lg_neg;
+  const double cmagic = 4503599627370496.0 + (double)center;  // 2^52 + center
+  const bool lane0 = lane == 0, lane_in = lane < R;
+  const unsigned code_s = smem_u32(S.code + lane * kCRing), tab_s = smem_u32(s_e2);
+  const int nsteps = C + R - 1;
+  const bool vcode = (C & 7) == 0 && ((g.prow * g.bc) & 7) == 0;
+  const bool vout = ((g.cols & 3) == 0) && ((bb.c0 & 3) == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
+  // code chunk kc (columns 8 kc .. 8 kc + 7 of every row): each lane loads its
+  // row's 16 bytes one group ahead into registers and stores them into the
+  // ring when the group starts (cp.async is left to the balance words)
+  auto ld_codes = [&](int kc) -> uint4 {
+    const int c0 = kc * 8;
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    if (c0 < C && lane_in) {
+      const uint16_t *srcp = cb + (int64_t)lane * C + c0;
+      if (vcode) {
+        v = __ldg(reinterpret_cast<const uint4 *>(srcp));
+      } else {
+        unsigned h[8];
+        for (int c = 0; c < 8; c++) h[c] = c0 + c < C ? srcp[c] : 0u;
+        v = make_uint4(h[0] | (h[1] << 16), h[2] | (h[3] << 16), h[4] | (h[5] << 16), h[6] | (h[7] << 16));
+      }
+    }
+    return v;
+  };
+  auto st_codes = [&](int kc, uint4 v) {
+    *reinterpret_cast<uint4 *>(S.code + lane * kCRing + ((kc * 8) & (kCRing - 1))) = v;
+  };
+  // outputs: each lane's row, four columns per 16-byte store (the sectors
+  // complete in L2 across consecutive stores)
+  float4 ob = make_float4(0.f, 0.f, 0.f, 0.f);
+  float *orow = op + (int64_t)lane * g.cols;
+  float hl = 0.0f, pn = 0.0f;
+  uint4 cnext = ld_codes(0);
+  for (int t0 = 0; t0 < nsteps; t0 += 8) {
+    __syncwarp();
+    st_codes(t0 >> 3, cnext);
+    cnext = ld_codes((t0 >> 3) + 1);
+    __syncwarp();
+    const int t1 = min(nsteps, t0 + 8);
+#pragma unroll 2
+    for (int t = t0; t < t1; t++) {
+      const int c = t - lane;
+      const bool started = c >= 0;
+      const bool active = lane_in & ((unsigned)c < (unsigned)C);
+      const bool anchor = lane0 & (c == 0);
+      const unsigned cidx = (unsigned)(c & (kCRing - 1));
+      const unsigned code = lds_u16(code_s + (cidx << 1));
+      // FP32 perceptron perf mode (container version 2, cmain32.cuh): the float32 mirror recurrence
+      const float dq = __fmul_rn((float)((int)code - center), two_ba32);
+      const float nhl = __shfl_up_sync(0xffffffffu, hl, 1);
+      const float a = c_pred32<PK>(k, hl, nhl, pn, lane0);
+      const bool isbal = active & (code == 0) & !anchor;
+      double qv = 0.0;
+      if (isbal) {  // the row's next balance value (words bj, bj + 1 landed: issued 6 groups ago)
+        cp_async_wait<5>();
+        const unsigned long long lo = lds_u64(bal_s + 8u * (unsigned)(bj & 7));
+        const unsigned long long hw = lds_u64(bal_s + 8u * (unsigned)((bj + 1) & 7));
+        qv = __longlong_as_double((long long)(bsh ? ((lo >> bsh) | (hw << (64 - bsh))) : lo));
+        issue_word(bj + 7);
+        bj++;
+      }
+      const float vh32 = anchor ? (float)anc : (isbal ? (float)qv : __fadd_rn(a, dq));
+      const double vh = (double)vh32;
+      pn = nhl;
+      hl = started ? vh32 : hl;
       // inverse_map (transform.py:188-202) + float32 cast (D20)
       // (lanes outside the partition and zero outputs evaluate 2^0.5 instead)
       const bool negv = vh > bnd, zero = vh <= zthr;

@@ -440,7 +440,7 @@ __global__ void k_write_header(uint8_t *out, Geom g, KParams k, uint64_t global_
   if (threadIdx.x == 0) {
     uint8_t *p = out;
     p[0] = 'P'; p[1] = 'M'; p[2] = 'E'; p[3] = 'Z';
-    unsigned short ver = 1;
+    unsigned short ver = k.precision ? 2 : 1;  // D12: 2 = FP32 perceptron perf mode
     put_bytes(p + 4, &ver, 2);
     p[6] = 0;
     unsigned long long rows = global_rows, cols = (unsigned long long)g.cols;

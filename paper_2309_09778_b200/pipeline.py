@@ -44,6 +44,14 @@ class CompressConfig:
     seed: int = 0
     m: int = 0
     model: PerceptronModel | None = None
+    # "fp64": the reference's arithmetic, container version 1 (bit-exact parity);
+    # "fp32": the north star's FP32 perceptron perf mode, container version 2
+    # (2-D fields; codes may differ from fp64 where float32 rounding moves them)
+    precision: str = "fp64"
+    # optional uint16 CUDA tensor of Codec.code_dump_numel() elements: receives
+    # every final code (raster per partition, 0xFFFF at anchors) -- for counting
+    # code mismatches between the two precisions
+    code_dump: object = None
 
 
 @dataclass
@@ -98,6 +106,12 @@ def make_params(cfg: CompressConfig, S: int) -> N.Params:
         p.w2[i] = float(v)
     p.block_rows, p.block_cols, p.partition_rows = cfg.block_rows, cfg.block_cols, cfg.partition_rows
     p.S, p.H, p.m = S, 2, cfg.m
+    if cfg.precision not in ("fp64", "fp32"):
+        raise ConfigError(f"precision must be 'fp64' or 'fp32', got {cfg.precision!r}")
+    p.precision = 1 if cfg.precision == "fp32" else 0
+    if p.precision and S != 3:
+        raise ConfigError("the FP32 perf mode is defined for 2-D fields (S = 3)")
+    p.d_code_dump = int(cfg.code_dump.data_ptr()) if cfg.code_dump is not None else 0
     return p
 
 
@@ -180,6 +194,13 @@ class Codec:
             if rows and cols else 0
         val = validation_blocks(nb, cfg.sample_rate, cfg.seed)
         return p, g, nb, val
+
+    def code_dump_numel(self, shape, cfg: CompressConfig) -> int:
+        """Elements of a CompressConfig.code_dump buffer for a field of ``shape``."""
+        p, g, _, _ = self.plan(shape, cfg)
+        n = ctypes.c_uint64(0)
+        check(self.lib.pmz_code_dump_elems(ctypes.byref(p), ctypes.byref(g), ctypes.byref(n)), "code_dump_elems")
+        return int(n.value)
 
     def compress_device(self, x: torch.Tensor, cfg: CompressConfig | None = None, out_capacity: int | None = None,
                         plan=None, d_val: torch.Tensor | None = None, block_offsets: torch.Tensor | None = None):
@@ -699,3 +720,15 @@ def decompress(container: bytes, device=None, shape=None) -> np.ndarray:
     if h.rows == 1 and h.S == 1:
         return res.reshape(-1)
     return res
+
+
+def code_mismatches(a: torch.Tensor, b: torch.Tensor) -> dict:
+    """Compare two code dumps of the same field (CompressConfig.code_dump,
+    both pre-filled with the same value so the padding agrees): positions whose
+    final code differs, and positions that are a balance point (code 0) in
+    exactly one of them -- the north star's perceptron-rounding mismatch
+    counters for the FP32 perf mode against the FP64 path."""
+    valid = (a != 0xFFFF) & (a != 0xFFFE)
+    diff = (a != b) & valid
+    bal = ((a == 0) != (b == 0)) & valid
+    return {"codes": int(valid.sum()), "code_mismatches": int(diff.sum()), "balance_mismatches": int(bal.sum())}
