@@ -25,7 +25,7 @@ def test_library_exports_every_header_symbol():
     for s in syms:
         assert hasattr(lib, s), s
     assert set(syms) == set(N.EXPORTS)
-    assert lib.pmz_abi_version() == 1
+    assert lib.pmz_abi_version() == 2
     assert lib.pmz_status_string(-14) == b"Corrupt"
 
 
