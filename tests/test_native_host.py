@@ -61,7 +61,7 @@ def test_parse_header_and_index_match_oracle(oracle):
 
 @pytest.mark.parametrize("mutate,exc", [
     (lambda b: b"QMEZ" + b[4:], "BadMagic"),
-    (lambda b: b[:4] + b"\x02\x00" + b[6:], "UnsupportedVersion"),
+    (lambda b: b[:4] + b"\x03\x00" + b[6:], "UnsupportedVersion"),  # 1: FP64 parity, 2: FP32 perf mode
     (lambda b: b[:51] + bytes([3]) + b[52:], "Corrupt"),        # m out of range
     (lambda b: b[:20], "Corrupt"),
 ])
