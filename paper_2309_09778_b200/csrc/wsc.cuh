@@ -497,47 +497,37 @@ __global__ void __launch_bounds__(256) k_stats(const float *__restrict__ x, Geom
   const BlockBox bb = block_box(g, b);
   const int pr0 = pi * g.prow, R = min(g.prow, bb.br - pr0), C = bb.bc;
   const float *base = x + (bb.r0 + pr0) * g.cols + bb.c0;
-  float mn = INFINITY, mx = 0.0f;
-  int nonfinite = 0;
-  auto acc = [&](float v) {
-    if (!isfinite(v)) nonfinite = 1;
-    const float a = fabsf(v);
-    if (a > 1.17549435e-38f && a <= 3.40282347e38f) { mn = fminf(mn, a); mx = fmaxf(mx, a); }
+  // min / max of the positive normal magnitudes on the bit patterns (ordered
+  // like the values for non-negative floats), non-finite flag
+  unsigned umn = 0xffffffffu, umx = 0u, nf = 0u;
+  auto acc = [&](unsigned bits) {
+    const unsigned a = bits & 0x7fffffffu;
+    nf |= a >= 0x7f800000u ? 1u : 0u;
+    const bool ok = (a > 0x00800000u) & (a < 0x7f800000u);  // zero_sub_floor: |x| <= 2^-126 is zero
+    umn = ok ? min(umn, a) : umn;
+    umx = ok ? max(umx, a) : umx;
   };
-  if ((g.cols & 3) == 0 && (C & 3) == 0) {
-    const int vpr = C >> 2, nv = R * vpr;
-    for (int i0 = threadIdx.x; i0 < nv; i0 += 4 * 256) {
-      float4 q[4];
-#pragma unroll
-      for (int u = 0; u < 4; u++) {
-        const int i = i0 + u * 256;
-        if (i < nv) {
-          const int r = i / vpr, c = (i - r * vpr) << 2;
-          q[u] = __ldg(reinterpret_cast<const float4 *>(base + (int64_t)r * g.cols + c));
-        } else {
-          q[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-        }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if ((g.cols & 3) == 0 && (C & 3) == 0 && ((bb.c0 & 3) == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0)) {
+    // warp w takes rows w, w + 8, ...; lanes the row's 16-byte vectors (no index division)
+    const int vpr = C >> 2;
+#pragma unroll 4
+    for (int r = warp; r < R; r += 8) {
+      const uint4 *rowp = reinterpret_cast<const uint4 *>(base + (int64_t)r * g.cols);
+      for (int c0 = 0; c0 < vpr; c0 += 64) {
+        uint4 q0 = make_uint4(0u, 0u, 0u, 0u), q1 = q0;
+        if (c0 + lane < vpr) q0 = __ldg(rowp + c0 + lane);
+        if (c0 + 32 + lane < vpr) q1 = __ldg(rowp + c0 + 32 + lane);
+        acc(q0.x); acc(q0.y); acc(q0.z); acc(q0.w);
+        acc(q1.x); acc(q1.y); acc(q1.z); acc(q1.w);
       }
-#pragma unroll
-      for (int u = 0; u < 4; u++) { acc(q[u].x); acc(q[u].y); acc(q[u].z); acc(q[u].w); }
     }
   } else {
-    const int n = R * C;
-    for (int i0 = threadIdx.x; i0 < n; i0 += 4 * 256) {
-      float q[4];
-#pragma unroll
-      for (int u = 0; u < 4; u++) {
-        const int i = i0 + u * 256;
-        q[u] = 0.f;
-        if (i < n) {
-          const int r = i / C, c = i - r * C;
-          q[u] = __ldg(base + (int64_t)r * g.cols + c);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < 4; u++) acc(q[u]);
-    }
+    for (int r = warp; r < R; r += 8)
+      for (int c = lane; c < C; c += 32) acc(__float_as_uint(__ldg(base + (int64_t)r * g.cols + c)));
   }
+  float mn = umn == 0xffffffffu ? INFINITY : __uint_as_float(umn), mx = __uint_as_float(umx);
+  int nonfinite = (int)nf;
   block_minmax<256>(mn, mx, nonfinite);
   if (threadIdx.x == 0) {
     BlkStat *bs = bst + b;
