@@ -121,9 +121,9 @@ __global__ void __launch_bounds__(kDDT) k_d_decode(const uint8_t *__restrict__ b
   const uint4 *qb = reinterpret_cast<const uint4 *>(a & ~(uintptr_t)15);
   const uint4 *qlast = reinterpret_cast<const uint4 *>((reinterpret_cast<uintptr_t>(buf + buf_n) - 1) & ~(uintptr_t)15);
   const unsigned ring_s = smem_u32(&s_ring[threadIdx.x][0]);
+  const unsigned klast = (unsigned)(qlast - qb);  // last readable block (index from qb)
   auto issue = [&](unsigned k) {  // block k -> slot k & 3
-    const uint4 *q = qb + k;
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(ring_s + 16u * (k & 3u)), "l"(q <= qlast ? q : qlast)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(ring_s + 16u * (k & 3u)), "l"(qb + min(k, klast))
                  : "memory");
     cp_async_commit();
   };
@@ -132,10 +132,10 @@ __global__ void __launch_bounds__(kDDT) k_d_decode(const uint8_t *__restrict__ b
   issue(2);
   issue(3);
   cp_async_wait<3>();
-  unsigned wi = (unsigned)(a >> 2) & 3u;  // next 32-bit word (index from qb)
+  const unsigned wi0 = (unsigned)(a >> 2) & 3u;
+  unsigned wi = wi0;  // next 32-bit word (index from qb)
   unsigned long long bits = 0;
   int nb = 0;
-  unsigned long long used = 0;
   auto refill = [&]() {
     const unsigned w = lds_u32(ring_s + ((wi & 15u) << 2));
     wi++;
@@ -148,11 +148,9 @@ __global__ void __launch_bounds__(kDDT) k_d_decode(const uint8_t *__restrict__ b
   };
   refill();
   refill();
-  {
-    const int sb = (int)(a & 3) * 8;
-    bits <<= sb;
-    nb -= sb;
-  }
+  const int sb = (int)(a & 3) * 8;  // bits of the first word before the stream
+  bits <<= sb;
+  nb -= sb;
   auto decode = [&]() -> unsigned {
     if (nb <= 32) refill();
     const unsigned top = (unsigned)(bits >> 32);
@@ -161,13 +159,11 @@ __global__ void __launch_bounds__(kDDT) k_d_decode(const uint8_t *__restrict__ b
     if (e & 0x80000000u) {  // longer than the table: scan the lengths possible under this prefix
       const unsigned lmax = (e >> 21) & 31u;
       while (l < lmax && s_lj[l + 1] <= top) l++;
-      unsigned idx = s_off[l] + ((top - s_lj[l]) >> (32 - l));
-      idx = idx < (unsigned)nalpha ? idx : (unsigned)nalpha - 1u;
-      s = sym_smem ? s_sym[idx] : __ldg(sym + idx);
+      const unsigned idx = s_off[l] + ((top - s_lj[l]) >> (32 - l));  // < nalpha for a complete code
+      s = sym_smem ? s_sym[idx & (kDSymSmem - 1)] : __ldg(sym + min(idx, (unsigned)nalpha - 1u));
     }
     bits <<= l;
     nb -= (int)l;
-    used += l;
     return s;
   };
   uint16_t *cp = codes + tcode_base(g, p);
@@ -181,9 +177,10 @@ __global__ void __launch_bounds__(kDDT) k_d_decode(const uint8_t *__restrict__ b
       for (int j = 0; j < 8; j += 2) {
         const unsigned s0 = (i0 + j == 0) ? (unsigned)kAnc : decode();
         const unsigned s1 = decode();
-        zr += (s0 == 0 ? 1u : 0u) + (s1 == 0 ? 1u : 0u);
         w[j >> 1] = s0 | (s1 << 16);
       }
+      zr += (__popc(__vcmpeq2(w[0], 0u)) + __popc(__vcmpeq2(w[1], 0u)) + __popc(__vcmpeq2(w[2], 0u)) +
+             __popc(__vcmpeq2(w[3], 0u))) >> 4;
       *reinterpret_cast<uint4 *>(cp + i0) = make_uint4(w[0], w[1], w[2], w[3]);
       col += 8;
       if (col == C) {
@@ -208,6 +205,7 @@ __global__ void __launch_bounds__(kDDT) k_d_decode(const uint8_t *__restrict__ b
     }
   }
   part_z[p] = zt;
+  const unsigned long long used = 32ull * (wi - wi0) - (unsigned)sb - (unsigned)nb;  // stream bits consumed
   if (used != L64) set_err_at(st, used < L64 ? PMZ_ERR_CORRUPT : PMZ_ERR_TRUNCATED, 72, p);
   cp_async_wait<0>();  // nothing in flight into shared memory at exit
 }
