@@ -792,7 +792,7 @@ DecLayout dec_layout(const Geom &g) {
   L.tab = take(sizeof(DecTab));
   L.sym = take(2 * kMaxAlpha);
   L.lut = take(4ull * ((1u << kLutBits) + kLut2Max));            // first + second level
-  L.lut1 = take(4ull << kDLutBits);                               // k_d_decode's first level
+  L.lut1 = take(kDLutBytes + 16);                                 // k_d_decode's tables + subtable counter
   L.npfix = take(sizeof(pmz_np_fix) * (size_t)(g.nblocks + 1));
   L.tpath = use_tpath(g);
   if (L.tpath) {
@@ -879,9 +879,18 @@ int pmz_decompress_prepare(const uint8_t *d_buf, uint64_t n, const pmz_header *h
         at<pmz_np_fix>(d_ws, L.npfix));
     k_dec_tables<<<1, 1024, 0, st>>>(d_buf + hdr->lens_offset, (int)hdr->m, at<DecTab>(d_ws, L.tab),
                                      at<uint16_t>(d_ws, L.sym), at<unsigned>(d_ws, L.lut), S);
-    if (L.tpath)
-      k_d_lut<<<(1u << kDLutBits) / 256, 256, 0, st>>>(at<DecTab>(d_ws, L.tab), at<uint16_t>(d_ws, L.sym),
-                                                      1 << (int)hdr->m, at<unsigned>(d_ws, L.lut1), S);
+    if (L.tpath) {
+      unsigned *lut_n = at<unsigned>(d_ws, L.lut1 + kDLutBytes);
+      CK(cudaMemsetAsync(lut_n, 0, 4, st));
+      if (d_lut16((int)hdr->m))
+        k_d_lut<uint16_t><<<(1u << DLut<uint16_t>::LB) / 256, 256, 0, st>>>(
+            at<DecTab>(d_ws, L.tab), at<uint16_t>(d_ws, L.sym), 1 << (int)hdr->m, at<uint16_t>(d_ws, L.lut1), lut_n,
+            S);
+      else
+        k_d_lut<unsigned><<<(1u << DLut<unsigned>::LB) / 256, 256, 0, st>>>(
+            at<DecTab>(d_ws, L.tab), at<uint16_t>(d_ws, L.sym), 1 << (int)hdr->m, at<unsigned>(d_ws, L.lut1), lut_n,
+            S);
+    }
   }
   return launch_check();
 }
@@ -914,11 +923,18 @@ int pmz_decompress_run(const uint8_t *d_buf, uint64_t n, const pmz_header *hdr, 
   WsStatus *S = at<WsStatus>(d_ws, L.status);
   if (G.nblocks > 0 && L.tpath) {
     const int center = 1 << ((int)hdr->m - 1);
-    k_d_decode<<<(unsigned)((G.nparts + kDDT - 1) / kDDT), kDDT, 0, st>>>(
-        d_buf, n, G, at<BlkP>(d_ws, L.blkp), at<DecTab>(d_ws, L.tab), at<uint16_t>(d_ws, L.sym), 1 << (int)hdr->m,
-        at<unsigned>(d_ws, L.lut1), at<unsigned long long>(d_ws, L.part_bits), at<unsigned long long>(d_ws, L.part_off),
-        at<unsigned long long>(d_ws, L.pay_off), at<uint16_t>(d_ws, L.codes), at<unsigned>(d_ws, L.zflag),
-        at<unsigned>(d_ws, L.rowz), S);
+#define PMZ_T_DECODE(E)                                                                                             \
+  do {                                                                                                              \
+    CK(cudaFuncSetAttribute(k_d_decode<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d_dec_smem<E>()));     \
+    k_d_decode<E><<<(unsigned)((G.nparts + kDDT - 1) / kDDT), kDDT, d_dec_smem<E>(), st>>>(                         \
+        d_buf, n, G, at<BlkP>(d_ws, L.blkp), at<DecTab>(d_ws, L.tab), at<uint16_t>(d_ws, L.sym), 1 << (int)hdr->m, \
+        at<E>(d_ws, L.lut1), at<unsigned long long>(d_ws, L.part_bits), at<unsigned long long>(d_ws, L.part_off),  \
+        at<unsigned long long>(d_ws, L.pay_off), at<uint16_t>(d_ws, L.codes), at<unsigned>(d_ws, L.zflag),         \
+        at<unsigned>(d_ws, L.rowz), S);                                                                             \
+  } while (0)
+    if (d_lut16((int)hdr->m)) PMZ_T_DECODE(uint16_t);
+    else PMZ_T_DECODE(unsigned);
+#undef PMZ_T_DECODE
     const unsigned grid = (unsigned)((G.nparts + kDRW - 1) / kDRW);
 #define PMZ_T_RECON(PKV)                                                                                            \
   do {                                                                                                              \

@@ -30,14 +30,39 @@
 
 namespace pmz {
 
-constexpr int kDDT = 256;          // decoder threads (partitions) per CTA
-constexpr int kDSymSmem = 1 << 12;  // canonical symbol table in shared memory up to this alphabet
+constexpr int kDDT = 512;          // decoder threads (partitions) per CTA
+constexpr int kDRB = 8;            // 16-byte stream blocks in each thread's shared ring
 
-// First-level decode table over the top 12 stream bits (built once per
-// container by k_d_lut): a codeword of <= 12 bits gives {symbol, length}
-// directly; a longer one gives the range [lmin, lmax] of codeword lengths
-// under that prefix (bit 31 set), the length then found by a short scan.
-constexpr int kDLutBits = 12;
+// First-level decode table over the top LB stream bits (built once per
+// container by k_d_lut): entry = symbol | length << SB for a codeword of at
+// most LB bits.  Alphabets up to 2^11 pack the entry into 16 bits (LB = 14:
+// 32 KB; C5 hits 99.4 % of its codes there) and give a longer codeword's
+// prefix a second-level table over the next k = clamp(maxl - LB, 1, 4) bits
+// (entry length 0, low bits = subtable + 1; L2E entries in all); larger
+// alphabets use 32-bit entries over 13 bits.  Entry 0: a binary search over
+// the canonical firsts.
+template <typename E>
+struct DLut;
+template <>
+struct DLut<uint16_t> {
+  static constexpr int LB = 14, SB = 11, L2E = 4096;
+};
+template <>
+struct DLut<unsigned> {
+  static constexpr int LB = 13, SB = 16, L2E = 0;
+};
+template <typename E>
+__host__ __device__ constexpr size_t d_lut_bytes() {
+  return sizeof(E) * ((1u << DLut<E>::LB) + (size_t)DLut<E>::L2E);
+}
+constexpr size_t kDLutBytes = d_lut_bytes<uint16_t>() > d_lut_bytes<unsigned>() ? d_lut_bytes<uint16_t>()
+                                                                                 : d_lut_bytes<unsigned>();
+__host__ __device__ inline bool d_lut16(int m) { return m <= 11; }
+template <typename E>
+__device__ __forceinline__ int d_l2_bits(int maxl) {
+  return min(max(maxl - DLut<E>::LB, 1), 4);
+}
+
 __device__ __forceinline__ int d_len_of(unsigned top, const unsigned *lj, int maxl) {
   int l = 1;
 #pragma unroll
@@ -47,8 +72,12 @@ __device__ __forceinline__ int d_len_of(unsigned top, const unsigned *lj, int ma
   }
   return l;
 }
-__global__ void k_d_lut(const DecTab *__restrict__ tab, const uint16_t *__restrict__ sym, int nalpha, unsigned *lut1,
-                        WsStatus *st) {
+// lut: [1 << LB] first level, then L2E entries of 2^k-entry subtables;
+// lut_n (a device counter, zeroed by the caller) hands out the subtables
+template <typename E>
+__global__ void k_d_lut(const DecTab *__restrict__ tab, const uint16_t *__restrict__ sym, int nalpha, E *lut,
+                        unsigned *lut_n, WsStatus *st) {
+  constexpr int LB = DLut<E>::LB, SB = DLut<E>::SB, L2E = DLut<E>::L2E;
   __shared__ unsigned s_lj[34];
   count_launch(st);
   if (threadIdx.x < 34) {
@@ -58,41 +87,63 @@ __global__ void k_d_lut(const DecTab *__restrict__ tab, const uint16_t *__restri
   __syncthreads();
   const int maxl = tab->maxl;
   const unsigned pfx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (pfx >= (1u << kDLutBits)) return;
-  const unsigned lo = pfx << (32 - kDLutBits), hi = lo | ((1u << (32 - kDLutBits)) - 1u);
-  const int l0 = d_len_of(lo, s_lj, maxl), l1 = d_len_of(hi, s_lj, maxl);
-  if (l0 <= kDLutBits) {
+  if (pfx >= (1u << LB)) return;
+  auto entry = [&](unsigned lo, int lim) -> unsigned {  // the codeword every extension of lo starts with
+    const int l0 = d_len_of(lo, s_lj, maxl);
+    if (l0 > lim) return 0u;
     unsigned idx = tab->offset[l0] + ((lo - s_lj[l0]) >> (32 - l0));
     idx = idx < (unsigned)nalpha ? idx : (unsigned)nalpha - 1u;
-    lut1[pfx] = (unsigned)sym[idx] | ((unsigned)l0 << 16);
-  } else {
-    lut1[pfx] = 0x80000000u | ((unsigned)l0 << 16) | ((unsigned)l1 << 21);
+    return (unsigned)sym[idx] | ((unsigned)l0 << SB);
+  };
+  const unsigned lo = pfx << (32 - LB);
+  unsigned e = entry(lo, LB);
+  if (e == 0u && L2E > 0) {
+    const int k = d_l2_bits<E>(maxl);
+    const unsigned j = atomicAdd(lut_n, 1u);
+    if (j < (unsigned)(L2E >> k)) {
+      E *sub = lut + (1u << LB) + ((size_t)j << k);
+      for (unsigned x = 0; x < (1u << k); x++) sub[x] = (E)entry(lo | (x << (32 - LB - k)), LB + k);
+      e = j + 1u;
+    }
   }
+  lut[pfx] = (E)e;
 }
 
+// k_d_decode: dynamic shared memory = the tables + the per-thread stream rings
+template <typename E>
+__host__ __device__ constexpr size_t d_dec_smem() {
+  return d_lut_bytes<E>() + (size_t)kDDT * kDRB * 16;
+}
+
+template <typename E>
 __global__ void __launch_bounds__(kDDT) k_d_decode(const uint8_t *__restrict__ buf, unsigned long long buf_n, Geom g,
                                                    const BlkP *__restrict__ blkp, const DecTab *__restrict__ tab,
                                                    const uint16_t *__restrict__ sym, int nalpha,
-                                                   const unsigned *__restrict__ lut1,
+                                                   const E *__restrict__ lut1,
                                                    const unsigned long long *__restrict__ part_bits,
                                                    const unsigned long long *__restrict__ part_off,
                                                    const unsigned long long *__restrict__ pay_off,
                                                    uint16_t *__restrict__ codes, unsigned *__restrict__ part_z,
                                                    unsigned *__restrict__ rowz, WsStatus *st) {
+  constexpr int LB = DLut<E>::LB, SB = DLut<E>::SB, L2E = DLut<E>::L2E;
+  extern __shared__ __align__(16) unsigned char smem_d[];
+  E *s_lut = reinterpret_cast<E *>(smem_d);
+  const E *s_l2 = s_lut + (1u << LB);
+  unsigned *s_ring0 = reinterpret_cast<unsigned *>(smem_d + d_lut_bytes<E>());  // kDRB blocks per thread
   __shared__ unsigned s_lj[34], s_off[34];
-  __shared__ unsigned s_lut[1 << kDLutBits];
-  __shared__ uint16_t s_sym[kDSymSmem];
-  __shared__ __align__(16) unsigned s_ring[kDDT][16];  // per-thread stream ring (4 x 16 B)
   count_launch(st);
   if (threadIdx.x < 34) {
     const unsigned l = threadIdx.x;
     s_lj[l] = (l >= 1 && l <= 32) ? (l == 32 ? tab->first[l] : tab->first[l] << (32 - l)) : 0xffffffffu;
     s_off[l] = tab->offset[l];
   }
-  for (int i = threadIdx.x; i < (1 << kDLutBits); i += kDDT) s_lut[i] = lut1[i];
-  const bool sym_smem = nalpha <= kDSymSmem;
-  if (sym_smem)
-    for (int i = threadIdx.x; i < nalpha; i += kDDT) s_sym[i] = sym[i];
+  {
+    const uint4 *src = reinterpret_cast<const uint4 *>(lut1);
+    uint4 *dst = reinterpret_cast<uint4 *>(s_lut);
+    for (int i = threadIdx.x; i < (int)(d_lut_bytes<E>() / 16); i += kDDT) dst[i] = src[i];
+  }
+  const int maxl = tab->maxl;
+  const int k2 = d_l2_bits<E>(maxl);
   __syncthreads();
   const int64_t p = (int64_t)blockIdx.x * kDDT + threadIdx.x;
   if (p >= g.nparts) return;
@@ -114,35 +165,46 @@ __global__ void __launch_bounds__(kDDT) k_d_decode(const uint8_t *__restrict__ b
     set_err_at(st, PMZ_ERR_CORRUPT, 71, p);
     return;
   }
-  // reader: the stream's aligned 16-byte blocks stream into a 4-block shared
-  // ring per thread by cp.async three blocks ahead; 32 bits at a time come
-  // out of the ring (no register waits on global memory)
+  // reader: the stream's aligned 16-byte blocks stream into a kDRB-block
+  // shared ring per thread by cp.async; 32 bits at a time come out of the
+  // ring.  The copies are issued and waited for at warp-uniform points (every
+  // eight codes, see `ahead`), so each commit group holds the whole warp's
+  // copies and a wait covers the lanes' own blocks, not their neighbours'.
   const uintptr_t a = reinterpret_cast<uintptr_t>(src);
   const uint4 *qb = reinterpret_cast<const uint4 *>(a & ~(uintptr_t)15);
   const uint4 *qlast = reinterpret_cast<const uint4 *>((reinterpret_cast<uintptr_t>(buf + buf_n) - 1) & ~(uintptr_t)15);
-  const unsigned ring_s = smem_u32(&s_ring[threadIdx.x][0]);
+  const unsigned ring_s = smem_u32(s_ring0 + threadIdx.x * (kDRB * 4));
   const unsigned klast = (unsigned)(qlast - qb);  // last readable block (index from qb)
-  auto issue = [&](unsigned k) {  // block k -> slot k & 3
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(ring_s + 16u * (k & 3u)), "l"(qb + min(k, klast))
+  auto issue = [&](unsigned k) {  // block k -> slot k % kDRB
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(ring_s + 16u * (k & (kDRB - 1u))),
+                 "l"(qb + min(k, klast))
                  : "memory");
-    cp_async_commit();
   };
-  issue(0);
-  issue(1);
-  issue(2);
-  issue(3);
-  cp_async_wait<3>();
+#pragma unroll
+  for (unsigned k = 0; k < kDRB; k++) issue(k);
+  cp_async_commit();
+  cp_async_wait<0>();
+  unsigned nexti = kDRB;  // next block to copy
   const unsigned wi0 = (unsigned)(a >> 2) & 3u;
   unsigned wi = wi0;  // next 32-bit word (index from qb)
-  unsigned long long bits = 0;
+  // before every eight codes: refill the free slots (block k may replace
+  // block k - kDRB once word 4 (k - kDRB) + 3 has been read) and wait for the
+  // group committed two calls earlier (one when codewords can exceed 24 bits):
+  // eight codes and the <= 63 buffered bits read at most 8 (10) words, so the
+  // blocks of the next eight codes were issued at least that long ago.
+  const bool wide = maxl > 24;
+  auto ahead = [&]() {
+    const unsigned lim = (wi >> 2) + (kDRB - 1u);
+    while (nexti <= lim) issue(nexti++);
+    cp_async_commit();
+    if (wide) cp_async_wait<1>();
+    else cp_async_wait<2>();
+  };
+  unsigned long long bits = 0;  // left-justified, zeros below the nb valid bits
   int nb = 0;
-  auto refill = [&]() {
-    const unsigned w = lds_u32(ring_s + ((wi & 15u) << 2));
+  auto refill = [&]() {  // nb < 32 -> nb >= 32
+    const unsigned w = lds_u32(ring_s + ((wi & (kDRB * 4u - 1u)) << 2));
     wi++;
-    if ((wi & 3u) == 0) {  // block (wi >> 2) - 1 consumed: its slot takes block (wi >> 2) + 3
-      issue((wi >> 2) + 3u);
-      cp_async_wait<3>();  // block wi >> 2 has landed
-    }
     bits |= (unsigned long long)__byte_perm(w, 0, 0x0123) << (32 - nb);
     nb += 32;
   };
@@ -151,49 +213,82 @@ __global__ void __launch_bounds__(kDDT) k_d_decode(const uint8_t *__restrict__ b
   const int sb = (int)(a & 3) * 8;  // bits of the first word before the stream
   bits <<= sb;
   nb -= sb;
-  auto decode = [&]() -> unsigned {
-    if (nb <= 32) refill();
+  if (nb < 32) refill();
+  // a codeword longer than the table: binary search over the canonical
+  // firsts; leaves nb >= 32 like every refill
+  auto slow = [&]() -> unsigned {
+    if (nb < 32) refill();
     const unsigned top = (unsigned)(bits >> 32);
-    const unsigned e = s_lut[top >> (32 - kDLutBits)];
-    unsigned l = (e >> 16) & 31u, s = e & 0xffffu;
-    if (e & 0x80000000u) {  // longer than the table: scan the lengths possible under this prefix
-      const unsigned lmax = (e >> 21) & 31u;
-      while (l < lmax && s_lj[l + 1] <= top) l++;
-      const unsigned idx = s_off[l] + ((top - s_lj[l]) >> (32 - l));  // < nalpha for a complete code
-      s = sym_smem ? s_sym[idx & (kDSymSmem - 1)] : __ldg(sym + min(idx, (unsigned)nalpha - 1u));
-    }
+    const int l = d_len_of(top, s_lj, maxl);
+    const unsigned idx = s_off[l] + ((top - s_lj[l]) >> (32 - l));  // < nalpha for a complete code
+    const unsigned s = __ldg(sym + min(idx, (unsigned)nalpha - 1u));
     bits <<= l;
-    nb -= (int)l;
+    nb -= l;
+    if (nb < 32) refill();
     return s;
   };
+  // longer than the first level: the second-level table, else the search;
+  // leaves nb >= LB
+  auto dec_long = [&](unsigned e) -> unsigned {
+    if (L2E > 0 && e != 0u) {
+      if (nb < 32) refill();
+      const unsigned e2 = s_l2[((e - 1u) << k2) | (((unsigned)(bits >> 32) << LB) >> (32 - k2))];
+      if (e2 != 0u) {
+        const unsigned l = e2 >> SB;
+        bits <<= l;
+        nb -= (int)l;
+        return e2 & ((1u << SB) - 1u);
+      }
+    }
+    return slow();
+  };
+  // one codeword; needs nb >= LB valid bits (a table hit is at most LB bits)
+  auto dec = [&]() -> unsigned {
+    const unsigned e = s_lut[(unsigned)(bits >> (64 - LB))];
+    if (e < (1u << SB)) return dec_long(e);
+    const unsigned l = e >> SB;
+    bits <<= l;
+    nb -= (int)l;
+    return e & ((1u << SB) - 1u);
+  };
   uint16_t *cp = codes + tcode_base(g, p);
-  unsigned zt = 0, zr = 0;
+  unsigned zt = 0;
   if ((C & 7) == 0 && ((g.prow * g.bc) & 7) == 0) {
-    // groups of eight codes of one row, one 16-byte store
-    int col = 0, r = 0;
-    for (unsigned i0 = 0; i0 < n; i0 += 8) {
-      unsigned w[4];
+    // groups of eight codes of one row, one 16-byte store; one refill check
+    // per pair (nb >= 32 before it, a hit takes <= LB <= 14 bits)
+    bool first = true;
+    for (int r = 0; r < R; r++) {
+      unsigned zr = 0;
+      for (int c0 = 0; c0 < C; c0 += 8) {
+        ahead();
+        unsigned w[4];
 #pragma unroll
-      for (int j = 0; j < 8; j += 2) {
-        const unsigned s0 = (i0 + j == 0) ? (unsigned)kAnc : decode();
-        const unsigned s1 = decode();
-        w[j >> 1] = s0 | (s1 << 16);
+        for (int j = 0; j < 4; j++) {
+          if (nb < 32) refill();
+          unsigned s0;
+          if (j == 0 && first) {
+            s0 = kAnc;
+            first = false;
+          } else {
+            s0 = dec();
+          }
+          const unsigned s1 = dec();
+          zr += (s0 == 0u) + (s1 == 0u);
+          w[j] = s0 | (s1 << 16);
+        }
+        *reinterpret_cast<uint4 *>(cp) = make_uint4(w[0], w[1], w[2], w[3]);
+        cp += 8;
       }
-      zr += (__popc(__vcmpeq2(w[0], 0u)) + __popc(__vcmpeq2(w[1], 0u)) + __popc(__vcmpeq2(w[2], 0u)) +
-             __popc(__vcmpeq2(w[3], 0u))) >> 4;
-      *reinterpret_cast<uint4 *>(cp + i0) = make_uint4(w[0], w[1], w[2], w[3]);
-      col += 8;
-      if (col == C) {
-        rz[r++] = zr;
-        zt += zr;
-        zr = 0;
-        col = 0;
-      }
+      rz[r] = zr;
+      zt += zr;
     }
   } else {
     int col = 0, r = 0;
+    unsigned zr = 0;
     for (unsigned i = 0; i < n; i++) {
-      const unsigned s = i == 0 ? (unsigned)kAnc : decode();
+      if ((i & 7u) == 0) ahead();
+      if (nb < 32) refill();
+      const unsigned s = i == 0 ? (unsigned)kAnc : dec();
       cp[i] = (uint16_t)s;
       zr += s == 0 ? 1u : 0u;
       if (++col == C) {
