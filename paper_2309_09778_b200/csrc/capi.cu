@@ -378,7 +378,7 @@ int pmz_compress_stats(const float *d_in, const pmz_geom *g, const pmz_params *p
   // zero status, coverage, histogram, flags and block stats (contiguous at the front)
   CK(cudaMemsetAsync(d_ws, 0, L.lens, st));
   if (G.nblocks == 0) return PMZ_OK;
-  k_stats<<<(unsigned)G.nparts, 256, 0, st>>>(d_in, G, k, at<BlkP>(d_ws, L.blkp), at<BlkStat>(d_ws, L.bstat),
+  k_stats<<<(unsigned)G.nblocks, kST, 0, st>>>(d_in, G, k, at<BlkP>(d_ws, L.blkp), at<BlkStat>(d_ws, L.bstat),
                                                at<WsStatus>(d_ws, L.status), at<pmz_np_fix>(d_ws, L.npfix));
   return launch_check();
 }
@@ -1269,7 +1269,7 @@ int pmz_train_gradient(const float *d_in, const pmz_geom *g, const pmz_params *p
   CK(cudaMemsetAsync(d_out12, 0, sizeof(double) * kTrC, st));
   if (G.nblocks == 0 || n_blocks <= 0) return launch_check();
   // (the training objective keeps the device's CR per-block logarithms: no host fixup)
-  k_stats<<<(unsigned)G.nparts, 256, 0, st>>>(d_in, G, k, at<BlkP>(d_ws, L.blkp), at<BlkStat>(d_ws, L.bstat),
+  k_stats<<<(unsigned)G.nblocks, kST, 0, st>>>(d_in, G, k, at<BlkP>(d_ws, L.blkp), at<BlkStat>(d_ws, L.bstat),
                                                at<WsStatus>(d_ws, L.status), nullptr);
   // the training blocks are flagged in the validation-flag slots (no quantization runs here)
   k_mark_val<<<(unsigned)((n_blocks + 255) / 256), 256, 0, st>>>(d_blocks, n_blocks, G.nblocks,

@@ -472,11 +472,11 @@ __global__ void __launch_bounds__(32) k_compress_1d(const float *__restrict__ x,
 }
 
 // compute_block_stats + make_transform_params (transform.py:84-167) for
-// every block, one CTA per 32-row partition: the partition's min positive
-// normal magnitude / max magnitude / non-finite flag go to per-block slots by
-// atomics (min as atomicMax of the bit complement, so a zeroed workspace is
-// the identity); the last partition of a block to arrive derives the block's
-// parameters (its three logarithms on three warps in parallel).
+// every block, one CTA per block: the min positive normal magnitude, the max
+// magnitude and the non-finite flag from one pass over the block (four rows
+// of 16-byte loads in flight per warp), then the block's parameters (its
+// three logarithms on three warps in parallel).  BlkStat is the layout of
+// the workspace slots the earlier partition-parallel version accumulated in.
 struct BlkStat {
   unsigned nmin;   // ~bits of the min |x| (0 = none)
   unsigned max;    // bits of the max |x|
@@ -484,72 +484,96 @@ struct BlkStat {
   unsigned count;  // partitions done
 };
 
-__global__ void __launch_bounds__(256) k_stats(const float *__restrict__ x, Geom g, KParams k,
+constexpr int kST = 512;  // k_stats threads: one CTA per block
+__global__ void __launch_bounds__(kST) k_stats(const float *__restrict__ x, Geom g, KParams k,
                                                BlkP *__restrict__ blkp, BlkStat *bst, WsStatus *st,
                                                pmz_np_fix *npfix) {
-  __shared__ bool s_last;
   __shared__ double s_l[3], s_fn;
+  __shared__ unsigned s_mn[kST / 32], s_mx[kST / 32];
   count_launch(st);
-  const int64_t p = blockIdx.x;
-  int64_t b;
-  int pi;
-  part_of(g, p, b, pi);
+  const int64_t b = blockIdx.x;
   const BlockBox bb = block_box(g, b);
-  const int pr0 = pi * g.prow, R = min(g.prow, bb.br - pr0), C = bb.bc;
-  const float *base = x + (bb.r0 + pr0) * g.cols + bb.c0;
-  // min / max of the positive normal magnitudes on the bit patterns (ordered
-  // like the values for non-negative floats), non-finite flag
-  unsigned umn = 0xffffffffu, umx = 0u, nf = 0u;
+  const int R = bb.br, C = bb.bc;
+  const float *base = x + bb.r0 * g.cols + bb.c0;
+  // on the magnitude bit patterns (ordered like the values): the minimum of
+  // (a - 0x00800001) mod 2^32 is the smallest magnitude above the floor
+  // (zero_sub_floor: |x| <= 2^-126 is zero, those wrap to the top), the
+  // maximum of a is the largest magnitude, >= 0x7f800000 for Inf / NaN
+  unsigned umn = 0xffffffffu, umx = 0u;
   auto acc = [&](unsigned bits) {
     const unsigned a = bits & 0x7fffffffu;
-    nf |= a >= 0x7f800000u ? 1u : 0u;
-    const bool ok = (a > 0x00800000u) & (a < 0x7f800000u);  // zero_sub_floor: |x| <= 2^-126 is zero
-    umn = ok ? min(umn, a) : umn;
-    umx = ok ? max(umx, a) : umx;
+    umn = min(umn, a - 0x00800001u);
+    umx = max(umx, a);
   };
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int NW = kST / 32;
   if ((g.cols & 3) == 0 && (C & 3) == 0 && ((bb.c0 & 3) == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0)) {
-    // warp w takes rows w, w + 8, ...; lanes the row's 16-byte vectors (no index division)
+    // warp w takes rows w, w + NW, ...; lanes the row's 16-byte vectors
     const int vpr = C >> 2;
-#pragma unroll 4
-    for (int r = warp; r < R; r += 8) {
-      const uint4 *rowp = reinterpret_cast<const uint4 *>(base + (int64_t)r * g.cols);
-      for (int c0 = 0; c0 < vpr; c0 += 64) {
-        uint4 q0 = make_uint4(0u, 0u, 0u, 0u), q1 = q0;
-        if (c0 + lane < vpr) q0 = __ldg(rowp + c0 + lane);
-        if (c0 + 32 + lane < vpr) q1 = __ldg(rowp + c0 + 32 + lane);
+    if (vpr == 64) {  // 256-column blocks: two vectors per lane per row, four rows per pass
+      const uint4 *p0 = reinterpret_cast<const uint4 *>(base) + lane;
+      const int64_t rs = g.cols >> 2;
+      int r = warp;
+      for (; r + 3 * NW < R; r += 4 * NW) {
+        uint4 q[8];
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+          q[2 * i] = __ldg(p0 + (int64_t)(r + i * NW) * rs);
+          q[2 * i + 1] = __ldg(p0 + (int64_t)(r + i * NW) * rs + 32);
+        }
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+          acc(q[i].x);
+          acc(q[i].y);
+          acc(q[i].z);
+          acc(q[i].w);
+        }
+      }
+      for (; r < R; r += NW) {
+        const uint4 q0 = __ldg(p0 + (int64_t)r * rs), q1 = __ldg(p0 + (int64_t)r * rs + 32);
         acc(q0.x); acc(q0.y); acc(q0.z); acc(q0.w);
         acc(q1.x); acc(q1.y); acc(q1.z); acc(q1.w);
       }
+    } else {
+      for (int r = warp; r < R; r += NW) {
+        const uint4 *rowp = reinterpret_cast<const uint4 *>(base + (int64_t)r * g.cols);
+        for (int v = lane; v < vpr; v += 32) {
+          const uint4 q0 = __ldg(rowp + v);
+          acc(q0.x); acc(q0.y); acc(q0.z); acc(q0.w);
+        }
+      }
     }
   } else {
-    for (int r = warp; r < R; r += 8)
+    for (int r = warp; r < R; r += NW)
       for (int c = lane; c < C; c += 32) acc(__float_as_uint(__ldg(base + (int64_t)r * g.cols + c)));
   }
-  float mn = umn == 0xffffffffu ? INFINITY : __uint_as_float(umn), mx = __uint_as_float(umx);
-  int nonfinite = (int)nf;
-  block_minmax<256>(mn, mx, nonfinite);
-  if (threadIdx.x == 0) {
-    BlkStat *bs = bst + b;
-    if (mn != INFINITY) atomicMax(&bs->nmin, ~__float_as_uint(mn));
-    if (mx != 0.0f) atomicMax(&bs->max, __float_as_uint(mx));
-    if (nonfinite) atomicOr(&bs->flags, 1u);
-    __threadfence();
-    s_last = atomicAdd(&bs->count, 1u) == (unsigned)(bb.np - 1);
+  for (int o = 16; o; o >>= 1) {
+    umn = min(umn, __shfl_xor_sync(0xffffffffu, umn, o));
+    umx = max(umx, __shfl_xor_sync(0xffffffffu, umx, o));
+  }
+  if (lane == 0) {
+    s_mn[warp] = umn;
+    s_mx[warp] = umx;
   }
   __syncthreads();
-  if (!s_last) return;
-  // ---- last partition of the block: make_transform_params ----
-  __threadfence();
+  umn = s_mn[0];
+  umx = s_mx[0];
+#pragma unroll
+  for (int i = 1; i < NW; i++) {
+    umn = min(umn, s_mn[i]);
+    umx = max(umx, s_mx[i]);
+  }
+  (void)bst;
   BlkP P{};
-  const volatile BlkStat *vs = bst + b;
-  BlkStat fs;
-  fs.nmin = vs->nmin;
-  fs.max = vs->max;
-  fs.flags = vs->flags;
-  const float gmx = __uint_as_float(fs.max);
-  if (threadIdx.x == 0 && (fs.flags & 1u)) set_err(st, PMZ_ERR_NONFINITE);
-  if (gmx == 0.0f) {
+  if (umx >= 0x7f800000u) {  // NaN / Inf: the compress fails; nothing downstream touches the block
+    P.trivial = 1;
+    if (threadIdx.x == 0) {
+      set_err(st, PMZ_ERR_NONFINITE);
+      blkp[b] = P;
+    }
+    return;
+  }
+  if (umx <= 0x00800000u) {  // every magnitude at or below the floor
     P.trivial = 1;
     if (threadIdx.x == 0) {
       blkp[b] = P;
@@ -557,7 +581,8 @@ __global__ void __launch_bounds__(256) k_stats(const float *__restrict__ x, Geom
     }
     return;
   }
-  const double fp = (double)__uint_as_float(~fs.nmin), amax = (double)gmx;
+  const float gmx = __uint_as_float(umx);
+  const double fp = (double)__uint_as_float(umn + 0x00800001u), amax = (double)gmx;
   if (threadIdx.x == 0) {
     // transform.py:160-162
     s_fn = __ddiv_rn(__dmul_rn(__dmul_rn(__dadd_rn(amax, k.eps0), fp), k.onepbr2), __dsub_rn(fp, k.eps0));
