@@ -41,7 +41,9 @@
 namespace pmz {
 
 constexpr int kCW = 8;        // warps (partitions) per CTA
-constexpr int kCWW = 4;       // warps (partitions) per CTA of k_c_write
+constexpr int kCWW = 4;  // warps (partitions) per CTA of k_c_write
+constexpr int kWU = 4;   // k_c_write: balance words per lane per round
+constexpr int kQU = 2;   // k_c_write: 16-byte stream chunks per lane per round
 constexpr int kCRing = 64;    // ring columns per warp (32 x 64 floats = 8 KB)
 constexpr int kCTabMax = 1 << 12;   // packed codeword table in shared memory up to this alphabet
 constexpr int kCHistMax = 1 << 13;  // validation histogram in shared memory up to this alphabet
@@ -622,43 +624,55 @@ __global__ void __launch_bounds__(kCWW * 32) k_c_write(Geom g, const BlkP *__res
     const unsigned sh = (unsigned)(B0 & 7) * 8;  // bit shift of the values against the aligned words
     const unsigned nwd = (unsigned)(w1 - w0 + 1);
     const double *bbase = balrow + (p * g.prow) * (int64_t)g.bc;
-    // value j of the partition's list (j < nz): row search over the rows' value prefixes
+    // value j of the partition's list (j < nz): row search over the rows' value
+    // prefixes; kWU words per lane per round, their loads issued together; the
+    // word's low value (jA = jB - 1) is the previous word's high one (a shuffle)
     int rlo = 0;
-    for (unsigned j0 = 0; j0 < nwd; j0 += 32) {
-      const unsigned jw = j0 + lane;
-      // the word holds the top sh/8 bytes of value jB - 1 and the low bytes of value jB,
-      // jB = ceil(ob / 8) with ob = the word's first byte relative to the list (> -8)
-      const long long ob = 8ll * (long long)(w0 + jw) - (long long)B0;
-      const long long jb = (ob + 7) >> 3, ja = jb - 1;
-      const unsigned jlast = __shfl_sync(0xffffffffu, (unsigned)jb, 31);
-      const unsigned jA = ja < 0 ? 0u : (unsigned)ja, jB = (unsigned)jb;
-      // rows of values jA and jB (warp-uniform loop: every lane shuffles)
-      int rA = rlo, rB = rlo;
-      for (int q = rlo + 1; q < R; q++) {
-        const unsigned st_q = __shfl_sync(0xffffffffu, zstart, q);
-        if (st_q > jlast) break;
-        rA = jA >= st_q ? q : rA;
-        rB = jB >= st_q ? q : rB;
-      }
-      const unsigned sA = __shfl_sync(0xffffffffu, zstart, rA), sB = __shfl_sync(0xffffffffu, zstart, rB);
-      unsigned long long vA = 0, vB = 0;
-      if (jw < nwd) {
-        if (ja >= 0 && jA < nz)
-          vA = (unsigned long long)__double_as_longlong(bbase[(int64_t)rA * g.bc + (jA - sA)]);
-        if (jB < nz) vB = (unsigned long long)__double_as_longlong(bbase[(int64_t)rB * g.bc + (jB - sB)]);
-      }
-      rlo = __shfl_sync(0xffffffffu, rB, 31);
-      // little-endian: the word = the top bytes of vA, then the low bytes of vB
-      const unsigned long long v = sh ? ((vA >> (64 - sh)) | (vB << sh)) : vB;
-      if (jw < nwd) {
-        const unsigned long long A = (w0 + jw) * 8ull;
-        if (A >= B0 && A + 8 <= B0 + 8ull * nz) {
-          *reinterpret_cast<unsigned long long *>(out + A) = v;
-        } else {
+    unsigned long long carry = 0;  // the high value of the round's last word
+    for (unsigned j0 = 0; j0 < nwd; j0 += 32u * kWU) {
+      const double *pb[kWU];
 #pragma unroll
-          for (int qb = 0; qb < 8; qb++) {
-            const unsigned long long a = A + qb;
-            if (a >= B0 && a < B0 + 8ull * nz) out[a] = (uint8_t)(v >> (8 * qb));
+      for (int u = 0; u < kWU; u++) {
+        pb[u] = nullptr;
+        if (j0 + 32u * u < nwd) {  // warp-uniform
+          const unsigned jw = j0 + 32u * u + lane;
+          // the word holds the top sh/8 bytes of value jB - 1 and the low bytes of value jB,
+          // jB = ceil(ob / 8) with ob = the word's first byte relative to the list (> -8)
+          const long long ob = 8ll * (long long)(w0 + jw) - (long long)B0;
+          const unsigned jB = (unsigned)((ob + 7) >> 3);
+          const unsigned jlast = __shfl_sync(0xffffffffu, jB, 31);
+          int rB = rlo;  // row of value jB (warp-uniform loop: every lane shuffles)
+          for (int q = rlo + 1; q < R; q++) {
+            const unsigned st_q = __shfl_sync(0xffffffffu, zstart, q);
+            if (st_q > jlast) break;
+            rB = jB >= st_q ? q : rB;
+          }
+          const unsigned sB = __shfl_sync(0xffffffffu, zstart, rB);
+          if (jw < nwd && jB < nz) pb[u] = bbase + (int64_t)rB * g.bc + (jB - sB);
+          rlo = __shfl_sync(0xffffffffu, rB, 31);
+        }
+      }
+      unsigned long long vb[kWU];
+#pragma unroll
+      for (int u = 0; u < kWU; u++) vb[u] = pb[u] ? (unsigned long long)__double_as_longlong(__ldg(pb[u])) : 0ull;
+#pragma unroll
+      for (int u = 0; u < kWU; u++) {
+        const unsigned jw = j0 + 32u * u + lane;
+        const unsigned long long up = __shfl_up_sync(0xffffffffu, vb[u], 1);
+        const unsigned long long vA = lane == 0 ? carry : up;
+        carry = __shfl_sync(0xffffffffu, vb[u], 31);
+        // little-endian: the word = the top bytes of vA, then the low bytes of vB
+        const unsigned long long v = sh ? ((vA >> (64 - sh)) | (vb[u] << sh)) : vb[u];
+        if (jw < nwd) {
+          const unsigned long long A = (w0 + jw) * 8ull;
+          if (A >= B0 && A + 8 <= B0 + 8ull * nz) {
+            *reinterpret_cast<unsigned long long *>(out + A) = v;
+          } else {
+#pragma unroll
+            for (int qb = 0; qb < 8; qb++) {
+              const unsigned long long a = A + qb;
+              if (a >= B0 && a < B0 + 8ull * nz) out[a] = (uint8_t)(v >> (8 * qb));
+            }
           }
         }
       }
@@ -699,77 +713,104 @@ __global__ void __launch_bounds__(kCWW * 32) k_c_write(Geom g, const BlkP *__res
   // 16-byte chunks of the container overlapping [pay0, pay0 + nbytes): each
   // lane assembles 128 stream bits from at most two rows (rows hold >= 128
   // bits when C > 128; narrower blocks took the lane-0 path above), the two
-  // ends byte by byte
+  // ends byte by byte; kQU chunks per lane per round, their loads issued together
   const unsigned long long q0 = pay0 >> 4, q1 = (pay0 + nbytes - 1) >> 4;
   const unsigned nq = (unsigned)(q1 - q0 + 1);
-  int rlo = 0;  // warp-uniform: the row of the next round's first chunk
-  for (unsigned jb = 0; jb < nq; jb += 32) {
-    const unsigned j = jb + lane;
-    const long long sb = 8ll * (long long)((q0 + j) * 16ull) - 8ll * (long long)pay0;  // stream bit of the chunk
-    const unsigned s = sb < 0 ? 0u : (unsigned)sb;
-    const unsigned s_last = __shfl_sync(0xffffffffu, s, 31);
-    int r = rlo;
-    for (int q = rlo + 1; q < R; q++) {
-      const unsigned st_q = __shfl_sync(0xffffffffu, rstart, q);
-      if (st_q > s_last) break;
-      r = s >= st_q ? q : r;
-    }
-    rlo = __shfl_sync(0xffffffffu, r, 31);
-    const unsigned off = s - __shfl_sync(0xffffffffu, rstart, r & 31);
-    const unsigned rl = __shfl_sync(0xffffffffu, ri.x, r & 31);
-    if (j >= nq) continue;
-    unsigned o[4] = {0u, 0u, 0u, 0u};
-    if (s < total) {
-      const unsigned *rp = rbase + (int64_t)r * g.bc;
-      const unsigned nwr = (rl + 31) >> 5, wb = off >> 5, sh = off & 31;
-      unsigned w[5];
+  int rlo = 0;  // warp-uniform: the row of the next chunk
+  for (unsigned jb = 0; jb < nq; jb += 32u * kQU) {
+    unsigned w[kQU][5], nx[kQU][4], offv[kQU], rlv[kQU];
+    long long sbv[kQU];
 #pragma unroll
-      for (int k = 0; k < 5; k++) w[k] = wb + k < nwr ? __ldg(rp + wb + k) : 0u;
-      const unsigned left = rl - off;  // bits of row r from s (the row's words are zero past its end)
-      unsigned n[4] = {0u, 0u, 0u, 0u};
-      if (left < 128 && r + 1 < R) {
-        const unsigned *np_ = rbase + (int64_t)(r + 1) * g.bc;
+    for (int u = 0; u < kQU; u++) {
+      const unsigned j = jb + 32u * u + lane;
+      const long long sb = 8ll * (long long)((q0 + j) * 16ull) - 8ll * (long long)pay0;  // stream bit of the chunk
+      const unsigned s = sb < 0 ? 0u : (unsigned)sb;
+      sbv[u] = sb;
+      offv[u] = 0u;
+      rlv[u] = 0u;
 #pragma unroll
-        for (int k = 0; k < 4; k++) n[k] = __ldg(np_ + k);
-      }
+      for (int k = 0; k < 5; k++) w[u][k] = 0u;
 #pragma unroll
-      for (int k = 0; k < 4; k++) {
-        unsigned v = __funnelshift_l(w[k + 1], w[k], sh);  // row r bits from off + 32 k
-        // row r + 1 bits: its bit (32 k - left + i) lands at position i of this word
-        const int dpos = 32 * k - (int)left;
-        unsigned t = 0;
-        if (dpos >= 0) {
-          const unsigned di = (unsigned)dpos >> 5, ds = (unsigned)dpos & 31;
-          const unsigned na = di < 4 ? n[di] : 0u, nb2 = di + 1 < 4 ? n[di + 1] : 0u;
-          t = __funnelshift_l(nb2, na, ds);
-        } else if (dpos > -32) {
-          t = n[0] >> (unsigned)(-dpos);
+      for (int k = 0; k < 4; k++) nx[u][k] = 0u;
+      if (jb + 32u * u < nq) {  // warp-uniform
+        const unsigned s_last = __shfl_sync(0xffffffffu, s, 31);
+        int r = rlo;
+        for (int q = rlo + 1; q < R; q++) {
+          const unsigned st_q = __shfl_sync(0xffffffffu, rstart, q);
+          if (st_q > s_last) break;
+          r = s >= st_q ? q : r;
         }
-        if (left <= 32u * k) v = 0u;
-        else if (left < 32u * (k + 1)) v &= ~(0xffffffffu >> (left - 32u * k));
-        o[k] = v | t;
+        rlo = __shfl_sync(0xffffffffu, r, 31);
+        const unsigned off = s - __shfl_sync(0xffffffffu, rstart, r & 31);
+        const unsigned rl = __shfl_sync(0xffffffffu, ri.x, r & 31);
+        offv[u] = off;
+        rlv[u] = rl;
+        if (j < nq && s < total) {
+          const unsigned *rp = rbase + (int64_t)r * g.bc;
+          const unsigned nwr = (rl + 31) >> 5, wb = off >> 5;
+#pragma unroll
+          for (int k = 0; k < 5; k++) w[u][k] = wb + k < nwr ? __ldg(rp + wb + k) : 0u;
+          if (rl - off < 128 && r + 1 < R) {
+            const unsigned *np_ = rbase + (int64_t)(r + 1) * g.bc;
+#pragma unroll
+            for (int k = 0; k < 4; k++) nx[u][k] = __ldg(np_ + k);
+          }
+        }
       }
-      if (sb < 0) {  // the chunk starts before the stream: shift right by -sb bits (< 128)
-        const unsigned d = (unsigned)(-sb);
-        unsigned t4[4];
+    }
+#pragma unroll
+    for (int u = 0; u < kQU; u++) {
+      const unsigned j = jb + 32u * u + lane;
+      if (j >= nq) continue;
+      const long long sb = sbv[u];
+      const unsigned s = sb < 0 ? 0u : (unsigned)sb;
+      unsigned o[4] = {0u, 0u, 0u, 0u};
+      if (s < total) {
+        const unsigned sh = offv[u] & 31;
+        const unsigned left = rlv[u] - offv[u];  // bits of row r from s (the row's words are zero past its end)
 #pragma unroll
         for (int k = 0; k < 4; k++) {
-          const int src = k - (int)(d >> 5);
-          const unsigned hiw = src >= 0 ? o[src] : 0u, low = src - 1 >= 0 ? o[src - 1] : 0u;
-          t4[k] = (d & 31) ? ((hiw >> (d & 31)) | (low << (32 - (d & 31)))) : hiw;
+          unsigned v = __funnelshift_l(w[u][k + 1], w[u][k], sh);  // row r bits from off + 32 k
+          // row r + 1 bits: its bit (32 k - left + i) lands at position i of this word
+          const int dpos = 32 * k - (int)left;
+          unsigned t = 0;
+          if (dpos >= 0) {  // dpos < 128: di <= 3
+            const unsigned di = (unsigned)dpos >> 5, ds = (unsigned)dpos & 31;
+            const unsigned na = di == 0 ? nx[u][0] : (di == 1 ? nx[u][1] : (di == 2 ? nx[u][2] : nx[u][3]));
+            const unsigned nb2 = di == 0 ? nx[u][1] : (di == 1 ? nx[u][2] : (di == 2 ? nx[u][3] : 0u));
+            t = __funnelshift_l(nb2, na, ds);
+          } else if (dpos > -32) {
+            t = nx[u][0] >> (unsigned)(-dpos);
+          }
+          if (left <= 32u * k) v = 0u;
+          else if (left < 32u * (k + 1)) v &= ~(0xffffffffu >> (left - 32u * k));
+          o[k] = v | t;
         }
-#pragma unroll
-        for (int k = 0; k < 4; k++) o[k] = t4[k];
+        if (sb < 0) {  // the chunk starts before the stream: shift the 128 bits right by -sb (< 128)
+          const unsigned d = (unsigned)(-sb);
+          unsigned long long hi = ((unsigned long long)o[0] << 32) | o[1], lo = ((unsigned long long)o[2] << 32) | o[3];
+          if (d >= 64) {
+            lo = hi >> (d - 64);
+            hi = 0ull;
+          } else {
+            lo = (lo >> d) | (hi << (64 - d));
+            hi >>= d;
+          }
+          o[0] = (unsigned)(hi >> 32);
+          o[1] = (unsigned)hi;
+          o[2] = (unsigned)(lo >> 32);
+          o[3] = (unsigned)lo;
+        }
       }
-    }
-    const unsigned long long A = (q0 + j) * 16ull;
-    if (A >= pay0 && A + 16 <= pay0 + nbytes) {
-      *reinterpret_cast<uint4 *>(out + A) = make_uint4(bswap32(o[0]), bswap32(o[1]), bswap32(o[2]), bswap32(o[3]));
-    } else {
+      const unsigned long long A = (q0 + j) * 16ull;
+      if (A >= pay0 && A + 16 <= pay0 + nbytes) {
+        *reinterpret_cast<uint4 *>(out + A) = make_uint4(bswap32(o[0]), bswap32(o[1]), bswap32(o[2]), bswap32(o[3]));
+      } else {
 #pragma unroll
-      for (int qb = 0; qb < 16; qb++) {
-        const unsigned long long aq = A + qb;
-        if (aq >= pay0 && aq < pay0 + nbytes) out[aq] = (uint8_t)(o[qb >> 2] >> (24 - 8 * (qb & 3)));
+        for (int qb = 0; qb < 16; qb++) {
+          const unsigned long long aq = A + qb;
+          if (aq >= pay0 && aq < pay0 + nbytes) out[aq] = (uint8_t)(o[qb >> 2] >> (24 - 8 * (qb & 3)));
+        }
       }
     }
   }
