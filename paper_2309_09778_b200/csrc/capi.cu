@@ -239,12 +239,21 @@ CMainOut cmain_out(void *d_ws, const WsLayout &L) {
 template <int PK, int MODE>
 void launch_cmain(const float *x, const Geom &G, const KParams &k, const int64_t *d_val, int64_t n_val, void *d_ws,
                   const WsLayout &L, cudaStream_t st) {
+  // kCMain: a warp sweeps a chain of up to `chain` consecutive partitions of a
+  // block as one wavefront (PMZ_CHAIN overrides the default for experiments)
+  int chain = 8;
+  if (const char *e = getenv("PMZ_CHAIN")) chain = atoi(e) > 0 ? atoi(e) : chain;
   unsigned grid;
-  if (MODE == kCMain) grid = (unsigned)((G.nparts + kCW - 1) / kCW);
+  if (MODE == kCMain) grid = (unsigned)((c_nchains(G, chain) + kCW - 1) / kCW);
   else grid = (unsigned)(n_val * ((G.np_full + kCW - 1) / kCW));
   if (grid == 0) return;
   CMainOut o = cmain_out(d_ws, L);
-  if (MODE == kCMain) o.dump = reinterpret_cast<uint16_t *>(k.code_dump);
+  if (MODE == kCMain) {
+    o.dump = reinterpret_cast<uint16_t *>(k.code_dump);
+    // the rows add their bit / balance counts to their partition's totals
+    cudaMemsetAsync(o.part_bits, 0, (size_t)G.nparts * sizeof(unsigned long long), st);
+    cudaMemsetAsync(o.part_zeros, 0, (size_t)G.nparts * sizeof(unsigned long long), st);
+  }
   // m is selected on the device: size for the largest shared-memory table;
   // alphabets above 2^12 take the launch whose codewords come from global memory
   const int smem = (int)cmain_smem_bytes(MODE, MODE == kCHist ? 13 : 12);
@@ -252,7 +261,8 @@ void launch_cmain(const float *x, const Geom &G, const KParams &k, const int64_t
   auto *fa = k.precision ? k_c_main32<PK, MODE, true> : k_c_main<PK, MODE, true>;
   auto *fb = k.precision ? k_c_main32<PK, MODE, false> : k_c_main<PK, MODE, false>;
   cudaFuncSetAttribute(fa, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  fa<<<grid, kCW * 32, smem, st>>>(x, G, k, at<BlkP>(d_ws, L.blkp), at<WsStatus>(d_ws, L.status), d_val, n_val, o);
+  fa<<<grid, kCW * 32, smem, st>>>(x, G, k, at<BlkP>(d_ws, L.blkp), at<WsStatus>(d_ws, L.status), d_val, n_val, o,
+                                   chain);
   if (getenv("PMZ_DEBUG")) {
     const cudaError_t e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) fprintf(stderr, "permez: k_c_main%s<%d,%d,1>: %s\n", k.precision ? "32" : "", PK, MODE,
@@ -261,7 +271,7 @@ void launch_cmain(const float *x, const Geom &G, const KParams &k, const int64_t
   if (MODE == kCMain) {
     cudaFuncSetAttribute(fb, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
     fb<<<grid, kCW * 32, smem2, st>>>(x, G, k, at<BlkP>(d_ws, L.blkp), at<WsStatus>(d_ws, L.status), d_val, n_val,
-                                      o);
+                                      o, chain);
   }
 }
 template <int MODE>

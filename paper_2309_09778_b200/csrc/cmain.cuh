@@ -206,6 +206,32 @@ __device__ __forceinline__ bool c_part(const Geom &g, int mode, const int64_t *v
   return true;
 }
 
+// chain ch of the kCMain sweep: up to L consecutive partitions of one block,
+// swept by one warp as ONE wavefront (the 31-step ramp is paid once per chain)
+__host__ __device__ inline int64_t c_nchains(const Geom &g, int L) {
+  if (g.nbr <= 0) return 0;
+  return (g.nbr - 1) * g.nbc * (int64_t)((g.np_full + L - 1) / L) + g.nbc * (int64_t)((g.np_last + L - 1) / L);
+}
+__device__ __forceinline__ bool c_chain(const Geom &g, int L, int64_t ch, int64_t &p, int64_t &b, int &pi, int &cnt) {
+  const int cf = (g.np_full + L - 1) / L, cl = (g.np_last + L - 1) / L;
+  const int64_t nfull = (g.nbr - 1) * g.nbc * (int64_t)cf;
+  int np;
+  if (ch < nfull) {
+    b = ch / cf;
+    pi = (int)(ch - b * cf) * L;
+    np = g.np_full;
+  } else {
+    const int64_t q = ch - nfull;
+    if (q >= g.nbc * (int64_t)cl) return false;
+    b = (g.nbr - 1) * g.nbc + q / cl;
+    pi = (int)(q % cl) * L;
+    np = g.np_last;
+  }
+  cnt = min(L, np - pi);
+  p = first_part(g, b) + pi;
+  return true;
+}
+
 // classification of a zero-floored float from its bits (xclass, wsc.cuh):
 // 0 zero, 1 / 2 positive / negative inside the filter's range, 3 extreme
 constexpr unsigned kClsLo = 0x017fe470u;  // bits of 4.7e-38f
@@ -257,7 +283,7 @@ __device__ unsigned long long g_cstats[16];
 template <int PK, int MODE, bool STAB>
 __global__ void __launch_bounds__(kCW * 32, 2)
     k_c_main(const float *__restrict__ x, Geom g, const __grid_constant__ KParams k, const BlkP *__restrict__ blkp,
-             WsStatus *st, const int64_t *__restrict__ val_ids, int64_t nval, CMainOut o) {
+             WsStatus *st, const int64_t *__restrict__ val_ids, int64_t nval, CMainOut o, int chain) {
   extern __shared__ __align__(16) unsigned char smem_c[];
   __shared__ unsigned s_cov[18];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -284,32 +310,49 @@ __global__ void __launch_bounds__(kCW * 32, 2)
   if (MODE == kCCov && threadIdx.x < 18) s_cov[threadIdx.x] = 0;
   __syncthreads();
 
+  // kCMain: a chain of cnt consecutive partitions of one block per warp, swept
+  // as one wavefront -- lane r goes from the last column of a partition's row
+  // straight to the first column of its row in the next partition, so only
+  // the chain's first partition pays the 31-step ramp.  The other modes take
+  // one partition of a validation block (cnt = 1).
   int64_t p, b;
-  int pi;
-  const bool have = c_part(g, MODE, val_ids, nval, p, b, pi);
+  int pi, cnt = 1;
+  bool have;
+  if (MODE == kCMain) have = c_chain(g, chain, (int64_t)blockIdx.x * kCW + warp, p, b, pi, cnt);
+  else have = c_part(g, MODE, val_ids, nval, p, b, pi);
   const BlkP *Pp = blkp + (have ? b : 0);
   const BlkP P = have ? *Pp : BlkP{};
   if (have && !P.trivial) {
     const BlockBox bb = block_box(g, b);
-    const int pr0 = pi * g.prow, R = min(g.prow, bb.br - pr0), C = bb.bc;
-    const int nsteps = C + R - 1;
-    const float *xp = x + (bb.r0 + pr0) * g.cols + bb.c0;
+    const int C = bb.bc, Cp = (C + 7) & ~7;       // columns; padded to whole 8-column chunks in the sweep
+    const int rows_left = bb.br - pi * g.prow;    // rows of the block from the chain's first partition on
+    const int nsteps = cnt * Cp + 31;
     const bool vx = ((g.cols & 3) == 0) && ((bb.c0 & 3) == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
-    auto load_chunk = [&](int kc) {  // columns 8 kc .. 8 kc + 7 of every row
-      const int c0 = kc * 8;
-      if (c0 < C) {
-        if (vx && c0 + 8 <= C) {
+    // loader (warp-uniform): the next chunk = columns l_c0 .. l_c0 + 7 of partition l_q of the chain
+    const float *l_xp = x + (bb.r0 + pi * g.prow) * g.cols + bb.c0;
+    int l_c0 = 0, l_q = 0;
+    auto load_chunk = [&](int kc) {
+      if (l_q < cnt) {
+        const int R = min(g.prow, rows_left - l_q * g.prow);
+        const int slot = (kc * 8) & (kCRing - 1);
+        if (vx && l_c0 + 8 <= C) {
 #pragma unroll
           for (int j = 0; j < 2; j++) {  // 16 rows x 32 B per instruction
             const int r = j * 16 + (lane >> 1), h = (lane & 1) * 4;
-            if (r < R) cp_async16(ring + r * kCRing + (c0 & (kCRing - 1)) + h, xp + (int64_t)r * g.cols + c0 + h);
+            if (r < R) cp_async16(ring + r * kCRing + slot + h, l_xp + (int64_t)r * g.cols + l_c0 + h);
           }
         } else {
 #pragma unroll 1
           for (int j = 0; j < 8; j++) {
-            const int r = j * 4 + (lane >> 3), cc = c0 + (lane & 7);
-            if (r < R && cc < C) cp_async4(ring + r * kCRing + (cc & (kCRing - 1)), xp + (int64_t)r * g.cols + cc);
+            const int r = j * 4 + (lane >> 3), cc = l_c0 + (lane & 7);
+            if (r < R && cc < C) cp_async4(ring + r * kCRing + slot + (lane & 7), l_xp + (int64_t)r * g.cols + cc);
           }
+        }
+        l_c0 += 8;
+        if (l_c0 >= Cp) {
+          l_c0 = 0;
+          l_q++;
+          l_xp += (int64_t)g.prow * g.cols;
         }
       }
       cp_async_commit();
@@ -320,15 +363,18 @@ __global__ void __launch_bounds__(kCW * 32, 2)
     const double zthr = P.zero_threshold, bnd = P.boundary;
     const double lgp = P.lg_pos, lgn = P.lg_neg, zcode = P.zero_code;
     unsigned *amb = &st->unresolved;
-    const bool lane0 = lane == 0, lane_in = lane < R;
+    const bool lane0 = lane == 0;
+    bool lane_in = lane < min(g.prow, rows_left);
+    int c = -lane;     // column in the lane's current partition (< 0: not started)
+    int qleft = cnt;   // partitions of the chain this lane has not finished
     double vW = 0.0, pnt = 0.0;  // TRUE: own previous value (W), lane - 1's one column back (NW)
     double hl = 0.0, pn = 0.0;   // RECONSTRUCTED (exact): same
+    double nvt = 0.0, nhl = 0.0;  // N of the coming step: lane - 1's values, shuffled at the end of the step before
     unsigned long long acc = 0;  // row encoder: pending bits, left-aligned
     int na = 0;
-    unsigned nb = 0, repairs = 0;
-    const int64_t row = p * g.prow + lane;
+    unsigned nb = 0, repairs = 0, tz = 0;
+    int64_t row = p * g.prow + lane;
     unsigned *wp = MODE == kCMain ? o.rowbits + row * (int64_t)g.bc : nullptr;
-    unsigned *const wp0 = wp;
     double *brow = MODE == kCMain ? o.balrow + row * (int64_t)g.bc : nullptr;
     uint16_t *dump = (MODE == kCMain && o.dump) ? o.dump + tcode_base(g, p) + (int64_t)lane * C : nullptr;
 #ifdef PMZ_CSTATS
@@ -346,14 +392,16 @@ __global__ void __launch_bounds__(kCW * 32, 2)
       cp_async_wait<3>();
       __syncwarp();
       const int t1 = min(nsteps, t0 + 8);
-#pragma unroll 2
-      for (int t = t0; t < t1; t++) {
-        const int c = t - lane;
-        const bool started = c >= 0;
+      // one sweep step; SW: some lane ends its row within these 8 steps (the
+      // row-end branch is compiled only into that copy of the body)
+      auto step = [&](const int t, auto swc) {
+        constexpr bool SW = decltype(swc)::value;
+        const int gc = t - lane;  // column of the chain's sweep: the ring slot
+        const bool started = gc >= 0;
         const bool active = lane_in & ((unsigned)c < (unsigned)C);
         const bool anchor = lane0 & (c == 0);
         // zero_sub_floor_magnitudes + class from the bits (transform.py:205-210; D8 classes)
-        const unsigned u0 = lds_u32(ring_s + ((unsigned)(c & (kCRing - 1)) << 2));
+        const unsigned u0 = lds_u32(ring_s + ((unsigned)(gc & (kCRing - 1)) << 2));
         const unsigned u = (u0 & 0x7fffffffu) <= 0x00800000u ? 0u : (u0 & 0x7fffffffu);
         const bool neg = (int)u0 < 0;
         const bool normal = (u - (kClsLo + 1u)) < (kClsHi - kClsLo - 1u);
@@ -374,7 +422,6 @@ __global__ void __launch_bounds__(kCW * 32, 2)
           va = u == 0 ? zcode : va;
         }
         // TRUE-surface residual from approximate surfaces, certified rounding
-        const double nvt = __shfl_up_sync(0xffffffffu, vW, 1);
         bool hamb;
         const double at = c_pred_approx<PK>(k, vW, nvt, pnt, lane0, hamb);
         pnt = nvt;
@@ -389,10 +436,10 @@ __global__ void __launch_bounds__(kCW * 32, 2)
         auto exact4 = [&](double &v, double &w, double &n, double &nw) {
           const float *myring = ring + lane * kCRing;
           v = c_fwd_exact(u, neg, P, l2_s, band_s, amb);
-          w = c > 0 ? c_fwd_exact_f(zfloor(myring[(c - 1) & (kCRing - 1)]), P, l2_s, band_s, amb) : 0.0;
-          n = lane0 ? 0.0 : c_fwd_exact_f(zfloor(ring[(lane - 1) * kCRing + (c & (kCRing - 1))]), P, l2_s, band_s, amb);
+          w = c > 0 ? c_fwd_exact_f(zfloor(myring[(gc - 1) & (kCRing - 1)]), P, l2_s, band_s, amb) : 0.0;
+          n = lane0 ? 0.0 : c_fwd_exact_f(zfloor(ring[(lane - 1) * kCRing + (gc & (kCRing - 1))]), P, l2_s, band_s, amb);
           nw = (lane0 || c == 0) ? 0.0
-                                 : c_fwd_exact_f(zfloor(ring[(lane - 1) * kCRing + ((c - 1) & (kCRing - 1))]), P,
+                                 : c_fwd_exact_f(zfloor(ring[(lane - 1) * kCRing + ((gc - 1) & (kCRing - 1))]), P,
                                                  l2_s, band_s, amb);
         };
         if (MODE == kCCov) {
@@ -404,94 +451,133 @@ __global__ void __launch_bounds__(kCW * 32, 2)
               rqx = quantize_rq(__dsub_rn(v, predict_steady<PK>(k, w, n, nw, lane0)), k);
             }
           }
-          const bool cnt = active & !anchor;
-          const int mm = cnt ? m_of_rq(rqx) : -1;
+          const bool cnt1 = active & !anchor;
+          const int mm = cnt1 ? m_of_rq(rqx) : -1;
           const unsigned grp = __match_any_sync(0xffffffffu, mm);
-          if (cnt && (grp & ((1u << lane) - 1)) == 0) atomicAdd(&s_cov[mm], (unsigned)__popc(grp));
-          continue;
-        }
-        const bool out = qbig | (abs(rq) >= center);
-        // decoder simulation on the RECONSTRUCTED surface (exact FP64, D3 order)
-        const double nhl = __shfl_up_sync(0xffffffffu, hl, 1);
-        double ar;
-        if (PK == 3) {  // predict_init (D3): a w2_0 + a w2_1 with w2 = 1/2, exactly as written
-          double h = __dsub_rn(__dadd_rn(hl, nhl), pn);
-          h = lane0 ? hl : h;
-          ar = h < 0.0 ? __dmul_rn(slope, h) : h;
-          const double a2 = __dmul_rn(ar, 0.5);
-          ar = __dadd_rn(a2, a2);
+          if (cnt1 && (grp & ((1u << lane) - 1)) == 0) atomicAdd(&s_cov[mm], (unsigned)__popc(grp));
         } else {
-          ar = predict_steady<PK>(k, hl, nhl, pn, lane0);
-        }
-        const double dq = __dmul_rn(qi, two_ba);
-        const double vhat = __dadd_rn(ar, dq);
-        const double d = __dadd_rn(ar, __dsub_rn(dq, va));  // vhat - v to ~2^-40: inside the filter's 2^-20 margin
-        const bool gz = vhat > zthr, gb = vhat > bnd;
-        const bool in12 = normal & (neg ? gb : (gz & !gb));
-        const bool inner = (d < k.dpos_m) & (d > k.dneg_m);
-        const bool outer = (d > k.dpos_p) | (d < k.dneg_p);
-        const bool sure = !qamb & !anchor;
-        const bool accept = sure & !out & ((in12 & inner) | ((u == 0) & !gz));
-        // certain violations (D8): out-of-range residual, d outside the bound by more than the
-        // margin, a sign flip at t < 1 -> balance point (verify_and_repair)
-        const bool vcert = sure & (out | (normal & (in12 ? outer : tlt1)));
-        int fin = center + rq;
-        double hnew = vhat, vbal = 0.0;
-        CSTAT(0, active & !accept & !vcert);
-        CSTAT(1, active & vcert);
-        if (__builtin_expect(__any_sync(0xffffffffu, active & !accept), 0)) {
-          if (active & vcert) {  // balance point: the TRUE value, numpy-exact
-            vbal = c_fwd_exact(u, neg, P, l2_s, band_s, amb);
-            fin = 0;
-            hnew = vbal;
-            repairs += out ? 0u : 1u;
-            if (MODE == kCMain) brow[nb] = vbal;  // the row's balance list (D9)
-            nb++;
-          } else if (active & !accept) {  // anchor, ties, the filter's undecided band: all exact
-            double v, w, n, nw;
-            exact4(v, w, n, nw);
-            const float xz = __uint_as_float(u | (neg ? 0x80000000u : 0u));
-            bool rep = false;
-            double hr;  // (addressed only here: the common path keeps hnew in registers)
-            fin = c_rare<PK>(k, Pp, lane, xz, v, w, n, nw, hl, nhl, pn, anchor, center, amb, &hr, &rep);
-            hnew = hr;
-            repairs += rep ? 1u : 0u;
-            if (MODE == kCMain && anchor) o.anchors[p] = v;  // forced anchor, D1
-            if (fin == 0 && !anchor) {
-              if (MODE == kCMain) brow[nb] = v;
+          const bool out = qbig | (abs(rq) >= center);
+          // decoder simulation on the RECONSTRUCTED surface (exact FP64, D3 order)
+          double ar;
+          if (PK == 3) {  // predict_init (D3): a w2_0 + a w2_1 with w2 = 1/2, exactly as written
+            double h = __dsub_rn(__dadd_rn(hl, nhl), pn);
+            h = lane0 ? hl : h;
+            ar = h < 0.0 ? __dmul_rn(slope, h) : h;
+            const double a2 = __dmul_rn(ar, 0.5);
+            ar = __dadd_rn(a2, a2);
+          } else {
+            ar = predict_steady<PK>(k, hl, nhl, pn, lane0);
+          }
+          const double dq = __dmul_rn(qi, two_ba);
+          const double vhat = __dadd_rn(ar, dq);
+          const double d = __dadd_rn(ar, __dsub_rn(dq, va));  // vhat - v to ~2^-40: inside the filter's 2^-20 margin
+          const bool gz = vhat > zthr, gb = vhat > bnd;
+          const bool in12 = normal & (neg ? gb : (gz & !gb));
+          const bool inner = (d < k.dpos_m) & (d > k.dneg_m);
+          const bool outer = (d > k.dpos_p) | (d < k.dneg_p);
+          const bool sure = !qamb & !anchor;
+          const bool accept = sure & !out & ((in12 & inner) | ((u == 0) & !gz));
+          // certain violations (D8): out-of-range residual, d outside the bound by more than the
+          // margin, a sign flip at t < 1 -> balance point (verify_and_repair)
+          const bool vcert = sure & (out | (normal & (in12 ? outer : tlt1)));
+          int fin = center + rq;
+          double hnew = vhat, vbal = 0.0;
+          CSTAT(0, active & !accept & !vcert);
+          CSTAT(1, active & vcert);
+          if (__builtin_expect(__any_sync(0xffffffffu, active & !accept), 0)) {
+            if (active & vcert) {  // balance point: the TRUE value, numpy-exact
+              vbal = c_fwd_exact(u, neg, P, l2_s, band_s, amb);
+              fin = 0;
+              hnew = vbal;
+              repairs += out ? 0u : 1u;
+              if (MODE == kCMain) brow[nb] = vbal;  // the row's balance list (D9)
               nb++;
+            } else if (active & !accept) {  // anchor, ties, the filter's undecided band: all exact
+              double v, w, n, nw;
+              exact4(v, w, n, nw);
+              const float xz = __uint_as_float(u | (neg ? 0x80000000u : 0u));
+              bool rep = false;
+              double hr;  // (addressed only here: the common path keeps hnew in registers)
+              fin = c_rare<PK>(k, Pp, lane, xz, v, w, n, nw, hl, nhl, pn, anchor, center, amb, &hr, &rep);
+              hnew = hr;
+              repairs += rep ? 1u : 0u;
+              if (MODE == kCMain && anchor) o.anchors[p + (cnt - qleft)] = v;  // forced anchor, D1
+              if (fin == 0 && !anchor) {
+                if (MODE == kCMain) brow[nb] = v;
+                nb++;
+              }
             }
           }
-        }
-        pn = nhl;
-        hl = started ? hnew : hl;
-        if (MODE == kCHist) {
-          const bool cnt = active & !anchor;
-          const int key = cnt ? fin : -1;
-          const unsigned grp = __match_any_sync(0xffffffffu, key);
-          if (cnt && (grp & ((1u << lane) - 1)) == 0) {
-            if (hist_smem) atomicAdd(&s_hist[fin], (unsigned)__popc(grp));
-            else atomicAdd(&o.hist[fin], (unsigned long long)__popc(grp));
+          pn = nhl;
+          hl = started ? hnew : hl;
+          if (MODE == kCHist) {
+            const bool cnt1 = active & !anchor;
+            const int key = cnt1 ? fin : -1;
+            const unsigned grp = __match_any_sync(0xffffffffu, key);
+            if (cnt1 && (grp & ((1u << lane) - 1)) == 0) {
+              if (hist_smem) atomicAdd(&s_hist[fin], (unsigned)__popc(grp));
+              else atomicAdd(&o.hist[fin], (unsigned long long)__popc(grp));
+            }
+          } else {
+            const bool enc = active & !anchor;
+            if (dump != nullptr && active) dump[c] = anchor ? kAnc : (uint16_t)fin;
+            if (STAB) {  // branch-free: lanes without a code take the empty entry
+              const uint2 e = lds_v2(tab_s + ((unsigned)(enc ? fin : nalpha) << 3));
+              acc |= (unsigned long long)e.x << ((64 - na - (int)e.y) & 63);
+              na += (int)e.y;
+            } else if (enc) {
+              const unsigned cwv = __ldg(o.cw + fin);
+              const int len = __ldg(o.lens + fin);
+              acc |= (unsigned long long)cwv << (64 - na - len);
+              na += len;
+            }
+            if (na >= 32) {
+              *wp++ = (unsigned)(acc >> 32);
+              acc <<= 32;
+              na -= 32;
+            }
           }
+          nhl = __shfl_up_sync(0xffffffffu, hl, 1);
+        }
+        nvt = __shfl_up_sync(0xffffffffu, vW, 1);
+        // end of the lane's row: close it and move to the same row of the chain's next
+        // partition (surfaces restart from 0: partition-local neighbours, D2)
+        if (SW && c == Cp - 1) {
+          if (MODE == kCMain) {
+            if (lane_in) {
+              const unsigned bits = 32u * (unsigned)(wp - (o.rowbits + row * (int64_t)g.bc)) + (unsigned)na;
+              if (na) *wp = (unsigned)(acc >> 32);
+              o.rowinfo[row] = make_uint2(bits, nb);
+              const int64_t pc = p + (cnt - qleft);
+              atomicAdd(&o.part_bits[pc], (unsigned long long)bits);  // zeroed before the launch
+              if (nb) atomicAdd(&o.part_zeros[pc], (unsigned long long)nb);
+              tz += nb;
+            }
+            row += g.prow;
+            wp = o.rowbits + row * (int64_t)g.bc;
+            brow = o.balrow + row * (int64_t)g.bc;
+            if (dump != nullptr) dump = o.dump + tcode_base(g, p + (cnt - qleft) + 1) + (int64_t)lane * C;
+          }
+          qleft--;
+          lane_in = qleft > 0 && lane < min(g.prow, rows_left - (cnt - qleft) * g.prow);
+          acc = 0;
+          na = 0;
+          nb = 0;
+          vW = 0.0;
+          pnt = 0.0;
+          hl = 0.0;
+          pn = 0.0;
+          c = qleft > 0 ? 0 : -(1 << 30);
         } else {
-          const bool enc = active & !anchor;
-          if (dump != nullptr && active) dump[c] = anchor ? kAnc : (uint16_t)fin;
-          if (STAB) {  // branch-free: lanes without a code take the empty entry
-            const uint2 e = lds_v2(tab_s + ((unsigned)(enc ? fin : nalpha) << 3));
-            acc |= (unsigned long long)e.x << ((64 - na - (int)e.y) & 63);
-            na += (int)e.y;
-          } else if (enc) {
-            const unsigned cwv = __ldg(o.cw + fin);
-            const int len = __ldg(o.lens + fin);
-            acc |= (unsigned long long)cwv << (64 - na - len);
-            na += len;
-          }
-          if (na >= 32) {
-            *wp++ = (unsigned)(acc >> 32);
-            acc <<= 32;
-            na -= 32;
-          }
+          c++;
         }
+      };
+      if (__any_sync(0xffffffffu, (unsigned)(Cp - 1 - c) < 8u)) {
+#pragma unroll 1
+        for (int t = t0; t < t1; t++) step(t, std::true_type{});
+      } else {
+#pragma unroll 2
+        for (int t = t0; t < t1; t++) step(t, std::false_type{});
       }
     }
     cp_async_wait<0>();
@@ -500,34 +586,19 @@ __global__ void __launch_bounds__(kCW * 32, 2)
       if (cst[i]) atomicAdd(&g_cstats[i], (unsigned long long)cst[i]);
 #endif
     if (MODE == kCMain) {
-      unsigned bits = 32u * (unsigned)(wp - wp0) + (unsigned)na;
-      if (lane_in) {
-        if (na) *wp = (unsigned)(acc >> 32);
-        o.rowinfo[row] = make_uint2(bits, nb);
-      } else {
-        bits = 0;
-        nb = 0;
-      }
-      unsigned long long tb = bits, tz = nb;
       unsigned tr = repairs;
       for (int s = 16; s; s >>= 1) {
-        tb += __shfl_xor_sync(0xffffffffu, tb, s);
         tz += __shfl_xor_sync(0xffffffffu, tz, s);
         tr += __shfl_xor_sync(0xffffffffu, tr, s);
       }
       if (lane == 0) {
-        o.part_bits[p] = tb;
-        o.part_zeros[p] = tz;
-        atomicAdd(&st->nbal, tz);
+        atomicAdd(&st->nbal, (unsigned long long)tz);
         if (tr) atomicAdd(&st->nrepair, (unsigned long long)tr);
-        atomicAdd(&st->ncodes, (unsigned long long)(R * C - 1));
+        atomicAdd(&st->ncodes, (unsigned long long)((int64_t)min(cnt * g.prow, rows_left) * C - cnt));
       }
     } else if (MODE == kCHist) {
       if (pi == 0 && lane == 0) atomicAdd(&o.hist[kMaxAlpha], 1ull);  // k for the floor (D10)
     }
-  } else if (have && MODE == kCMain && lane == 0) {
-    o.part_bits[p] = 0;
-    o.part_zeros[p] = 0;
   }
   if (MODE == kCCov) {
     __syncthreads();

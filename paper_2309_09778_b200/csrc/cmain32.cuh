@@ -54,7 +54,7 @@ __device__ __forceinline__ float rhaz32(float q) { return copysignf(floorf(__fad
 template <int PK, int MODE, bool STAB>
 __global__ void __launch_bounds__(kCW * 32, 2)
     k_c_main32(const float *__restrict__ x, Geom g, const __grid_constant__ KParams k, const BlkP *__restrict__ blkp,
-               WsStatus *st, const int64_t *__restrict__ val_ids, int64_t nval, CMainOut o) {
+               WsStatus *st, const int64_t *__restrict__ val_ids, int64_t nval, CMainOut o, int chain) {
   extern __shared__ __align__(16) unsigned char smem_c[];
   __shared__ unsigned s_cov[18];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -77,32 +77,44 @@ __global__ void __launch_bounds__(kCW * 32, 2)
   if (MODE == kCCov && threadIdx.x < 18) s_cov[threadIdx.x] = 0;
   __syncthreads();
 
+  // kCMain: a chain of consecutive partitions per warp, one wavefront (see k_c_main)
   int64_t p, b;
-  int pi;
-  const bool have = c_part(g, MODE, val_ids, nval, p, b, pi);
+  int pi, cnt = 1;
+  bool have;
+  if (MODE == kCMain) have = c_chain(g, chain, (int64_t)blockIdx.x * kCW + warp, p, b, pi, cnt);
+  else have = c_part(g, MODE, val_ids, nval, p, b, pi);
   const BlkP *Pp = blkp + (have ? b : 0);
   const BlkP P = have ? *Pp : BlkP{};
   if (have && !P.trivial) {
     const BlockBox bb = block_box(g, b);
-    const int pr0 = pi * g.prow, R = min(g.prow, bb.br - pr0), C = bb.bc;
-    const int nsteps = C + R - 1;
-    const float *xp = x + (bb.r0 + pr0) * g.cols + bb.c0;
+    const int C = bb.bc, Cp = (C + 7) & ~7;
+    const int rows_left = bb.br - pi * g.prow;
+    const int nsteps = cnt * Cp + 31;
     const bool vx = ((g.cols & 3) == 0) && ((bb.c0 & 3) == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
+    const float *l_xp = x + (bb.r0 + pi * g.prow) * g.cols + bb.c0;
+    int l_c0 = 0, l_q = 0;
     auto load_chunk = [&](int kc) {
-      const int c0 = kc * 8;
-      if (c0 < C) {
-        if (vx && c0 + 8 <= C) {
+      if (l_q < cnt) {
+        const int R = min(g.prow, rows_left - l_q * g.prow);
+        const int slot = (kc * 8) & (kCRing - 1);
+        if (vx && l_c0 + 8 <= C) {
 #pragma unroll
           for (int j = 0; j < 2; j++) {
             const int r = j * 16 + (lane >> 1), h = (lane & 1) * 4;
-            if (r < R) cp_async16(ring + r * kCRing + (c0 & (kCRing - 1)) + h, xp + (int64_t)r * g.cols + c0 + h);
+            if (r < R) cp_async16(ring + r * kCRing + slot + h, l_xp + (int64_t)r * g.cols + l_c0 + h);
           }
         } else {
 #pragma unroll 1
           for (int j = 0; j < 8; j++) {
-            const int r = j * 4 + (lane >> 3), cc = c0 + (lane & 7);
-            if (r < R && cc < C) cp_async4(ring + r * kCRing + (cc & (kCRing - 1)), xp + (int64_t)r * g.cols + cc);
+            const int r = j * 4 + (lane >> 3), cc = l_c0 + (lane & 7);
+            if (r < R && cc < C) cp_async4(ring + r * kCRing + slot + (lane & 7), l_xp + (int64_t)r * g.cols + cc);
           }
+        }
+        l_c0 += 8;
+        if (l_c0 >= Cp) {
+          l_c0 = 0;
+          l_q++;
+          l_xp += (int64_t)g.prow * g.cols;
         }
       }
       cp_async_commit();
@@ -122,14 +134,16 @@ __global__ void __launch_bounds__(kCW * 32, 2)
     const float mu = 0x1p-21f + 0x1p-24f * (4.0f * lmax + 4.0f) + 0x1p-22f;
     const float dpm = (float)k.dpos - mu, dnm = (float)k.dneg + mu, dpp = (float)k.dpos + mu, dnp = (float)k.dneg - mu;
     unsigned *amb = &st->unresolved;
-    const bool lane0 = lane == 0, lane_in = lane < R;
+    const bool lane0 = lane == 0;
+    bool lane_in = lane < min(g.prow, rows_left);
+    int c = -lane, qleft = cnt;
     float vW = 0.0f, pnt = 0.0f, hl = 0.0f, pn = 0.0f;
+    float nvt = 0.0f, nhl = 0.0f;  // N of the coming step (shuffled at the end of the step before)
     unsigned long long acc = 0;
     int na = 0;
-    unsigned nb = 0, repairs = 0;
-    const int64_t row = p * g.prow + lane;
+    unsigned nb = 0, repairs = 0, tz = 0;
+    int64_t row = p * g.prow + lane;
     unsigned *wp = MODE == kCMain ? o.rowbits + row * (int64_t)g.bc : nullptr;
-    unsigned *const wp0 = wp;
     double *brow = MODE == kCMain ? o.balrow + row * (int64_t)g.bc : nullptr;
     uint16_t *dump = (MODE == kCMain && o.dump) ? o.dump + tcode_base(g, p) + (int64_t)lane * C : nullptr;
     const unsigned ring_s = smem_u32(ring + lane * kCRing), tab_s = smem_u32(s_tab);
@@ -142,13 +156,15 @@ __global__ void __launch_bounds__(kCW * 32, 2)
       cp_async_wait<3>();
       __syncwarp();
       const int t1 = min(nsteps, t0 + 8);
-#pragma unroll 2
-      for (int t = t0; t < t1; t++) {
-        const int c = t - lane;
-        const bool started = c >= 0;
+      // one sweep step; SW: some lane ends its row within these 8 steps (the
+      // row-end branch is compiled only into that copy of the body)
+      auto step = [&](const int t, auto swc) {
+        constexpr bool SW = decltype(swc)::value;
+        const int gc = t - lane;
+        const bool started = gc >= 0;
         const bool active = lane_in & ((unsigned)c < (unsigned)C);
         const bool anchor = lane0 & (c == 0);
-        const unsigned u0 = lds_u32(ring_s + ((unsigned)(c & (kCRing - 1)) << 2));
+        const unsigned u0 = lds_u32(ring_s + ((unsigned)(gc & (kCRing - 1)) << 2));
         const unsigned u = (u0 & 0x7fffffffu) <= 0x00800000u ? 0u : (u0 & 0x7fffffffu);
         const bool neg = (int)u0 < 0;
         const float xz = __uint_as_float(u | (neg ? 0x80000000u : 0u));
@@ -156,7 +172,6 @@ __global__ void __launch_bounds__(kCW * 32, 2)
         float v = __fadd_rn(__log2f(__uint_as_float(u | (u == 0 ? 0x3f800000u : 0u))), neg ? lgn : lgp);
         v = u == 0 ? zc : v;
         // TRUE-surface residual and quantization in float32
-        const float nvt = __shfl_up_sync(0xffffffffu, vW, 1);
         const float at = c_pred32<PK>(k, vW, nvt, pnt, lane0);
         pnt = nvt;
         vW = started ? v : vW;
@@ -164,99 +179,122 @@ __global__ void __launch_bounds__(kCW * 32, 2)
         const bool big = !(fabsf(qr) < 32768.0f);
         const int rq = big ? (int)kRqOut : (int)qr;
         if (MODE == kCCov) {
-          const bool cnt = active & !anchor;
-          const int mm = cnt ? m_of_rq(rq) : -1;
+          const bool cnt1 = active & !anchor;
+          const int mm = cnt1 ? m_of_rq(rq) : -1;
           const unsigned grp = __match_any_sync(0xffffffffu, mm);
-          if (cnt && (grp & ((1u << lane) - 1)) == 0) atomicAdd(&s_cov[mm], (unsigned)__popc(grp));
-          continue;
-        }
-        const bool out = big | (abs(rq) >= center);
-        // decoder simulation (float32, the mirror of k_d_recon32)
-        const float nhl = __shfl_up_sync(0xffffffffu, hl, 1);
-        const float ar = c_pred32<PK>(k, hl, nhl, pn, lane0);
-        const float vhat = __fadd_rn(ar, __fmul_rn(out ? 0.0f : qr, two_ba));
-        const float d = __fsub_rn(vhat, v);
-        const bool normal = (u - (kClsLo + 1u)) < (kClsHi - kClsLo - 1u);
-        // certainly on the right side of zero_threshold / boundary (D8 classes), certainly flipped
-        const bool in12 = normal & (neg ? (vhat > bndU) : ((vhat > zthrU) & (vhat <= bndD)));
-        const bool flip = normal & (neg ? (vhat <= bndD) : ((vhat <= zthrD) | (vhat > bndU)));
-        const bool inner = (d < dpm) & (d > dnm), outer = (d > dpp) | (d < dnp);
-        const bool accept = !anchor & !out & ((in12 & inner) | ((u == 0) & (vhat <= zthrD)));
-        const bool vcert = !anchor & (out | (in12 & outer) | (flip & tlt1));
-        bool keep = accept;
-        if (__builtin_expect(__any_sync(0xffffffffu, active & !accept & !vcert), 0)) {
-          if (active & !accept & !vcert) {  // anchor, thresholds, extremes: the exact float32 test (D8)
-            if (!anchor && !out) keep = !violates(inv_f32((double)vhat, P, amb), xz, k.repair_t);
-          }
-        }
-        const int fin = keep ? center + rq : 0;
-        repairs += (active & !keep & !anchor & !out) ? 1u : 0u;
-        pn = nhl;
-        hl = started ? (keep ? vhat : v) : hl;
-        if (MODE == kCHist) {
-          const bool cnt = active & !anchor;
-          const int key = cnt ? fin : -1;
-          const unsigned grp = __match_any_sync(0xffffffffu, key);
-          if (cnt && (grp & ((1u << lane) - 1)) == 0) {
-            if (hist_smem) atomicAdd(&s_hist[fin], (unsigned)__popc(grp));
-            else atomicAdd(&o.hist[fin], (unsigned long long)__popc(grp));
-          }
+          if (cnt1 && (grp & ((1u << lane) - 1)) == 0) atomicAdd(&s_cov[mm], (unsigned)__popc(grp));
         } else {
-          const bool enc = active & !anchor;
-          if (enc & (fin == 0)) {
-            brow[nb] = (double)v;  // the row's balance list (D9): the encoder's float32 value, exactly
-            nb++;
+          const bool out = big | (abs(rq) >= center);
+          // decoder simulation (float32, the mirror of k_d_recon32)
+          const float ar = c_pred32<PK>(k, hl, nhl, pn, lane0);
+          const float vhat = __fadd_rn(ar, __fmul_rn(out ? 0.0f : qr, two_ba));
+          const float d = __fsub_rn(vhat, v);
+          const bool normal = (u - (kClsLo + 1u)) < (kClsHi - kClsLo - 1u);
+          // certainly on the right side of zero_threshold / boundary (D8 classes), certainly flipped
+          const bool in12 = normal & (neg ? (vhat > bndU) : ((vhat > zthrU) & (vhat <= bndD)));
+          const bool flip = normal & (neg ? (vhat <= bndD) : ((vhat <= zthrD) | (vhat > bndU)));
+          const bool inner = (d < dpm) & (d > dnm), outer = (d > dpp) | (d < dnp);
+          const bool accept = !anchor & !out & ((in12 & inner) | ((u == 0) & (vhat <= zthrD)));
+          const bool vcert = !anchor & (out | (in12 & outer) | (flip & tlt1));
+          bool keep = accept;
+          if (__builtin_expect(__any_sync(0xffffffffu, active & !accept & !vcert), 0)) {
+            if (active & !accept & !vcert) {  // anchor, thresholds, extremes: the exact float32 test (D8)
+              if (!anchor && !out) keep = !violates(inv_f32((double)vhat, P, amb), xz, k.repair_t);
+            }
           }
-          if (active & anchor) o.anchors[p] = (double)v;  // forced anchor, D1
-          if (dump != nullptr && active) dump[c] = anchor ? kAnc : (uint16_t)fin;
-          if (STAB) {
-            const uint2 e = lds_v2(tab_s + ((unsigned)(enc ? fin : nalpha) << 3));
-            acc |= (unsigned long long)e.x << ((64 - na - (int)e.y) & 63);
-            na += (int)e.y;
-          } else if (enc) {
-            const unsigned cwv = __ldg(o.cw + fin);
-            const int len = __ldg(o.lens + fin);
-            acc |= (unsigned long long)cwv << (64 - na - len);
-            na += len;
+          const int fin = keep ? center + rq : 0;
+          repairs += (active & !keep & !anchor & !out) ? 1u : 0u;
+          pn = nhl;
+          hl = started ? (keep ? vhat : v) : hl;
+          if (MODE == kCHist) {
+            const bool cnt1 = active & !anchor;
+            const int key = cnt1 ? fin : -1;
+            const unsigned grp = __match_any_sync(0xffffffffu, key);
+            if (cnt1 && (grp & ((1u << lane) - 1)) == 0) {
+              if (hist_smem) atomicAdd(&s_hist[fin], (unsigned)__popc(grp));
+              else atomicAdd(&o.hist[fin], (unsigned long long)__popc(grp));
+            }
+          } else {
+            const bool enc = active & !anchor;
+            if (enc & (fin == 0)) {
+              brow[nb] = (double)v;  // the row's balance list (D9): the encoder's float32 value, exactly
+              nb++;
+            }
+            if (active & anchor) o.anchors[p + (cnt - qleft)] = (double)v;  // forced anchor, D1
+            if (dump != nullptr && active) dump[c] = anchor ? kAnc : (uint16_t)fin;
+            if (STAB) {
+              const uint2 e = lds_v2(tab_s + ((unsigned)(enc ? fin : nalpha) << 3));
+              acc |= (unsigned long long)e.x << ((64 - na - (int)e.y) & 63);
+              na += (int)e.y;
+            } else if (enc) {
+              const unsigned cwv = __ldg(o.cw + fin);
+              const int len = __ldg(o.lens + fin);
+              acc |= (unsigned long long)cwv << (64 - na - len);
+              na += len;
+            }
+            if (na >= 32) {
+              *wp++ = (unsigned)(acc >> 32);
+              acc <<= 32;
+              na -= 32;
+            }
           }
-          if (na >= 32) {
-            *wp++ = (unsigned)(acc >> 32);
-            acc <<= 32;
-            na -= 32;
-          }
+          nhl = __shfl_up_sync(0xffffffffu, hl, 1);
         }
+        nvt = __shfl_up_sync(0xffffffffu, vW, 1);
+        // end of the lane's row: close it, move to the same row of the chain's next partition
+        if (SW && c == Cp - 1) {
+          if (MODE == kCMain) {
+            if (lane_in) {
+              const unsigned bits = 32u * (unsigned)(wp - (o.rowbits + row * (int64_t)g.bc)) + (unsigned)na;
+              if (na) *wp = (unsigned)(acc >> 32);
+              o.rowinfo[row] = make_uint2(bits, nb);
+              const int64_t pc = p + (cnt - qleft);
+              atomicAdd(&o.part_bits[pc], (unsigned long long)bits);  // zeroed before the launch
+              if (nb) atomicAdd(&o.part_zeros[pc], (unsigned long long)nb);
+              tz += nb;
+            }
+            row += g.prow;
+            wp = o.rowbits + row * (int64_t)g.bc;
+            brow = o.balrow + row * (int64_t)g.bc;
+            if (dump != nullptr) dump = o.dump + tcode_base(g, p + (cnt - qleft) + 1) + (int64_t)lane * C;
+          }
+          qleft--;
+          lane_in = qleft > 0 && lane < min(g.prow, rows_left - (cnt - qleft) * g.prow);
+          acc = 0;
+          na = 0;
+          nb = 0;
+          vW = 0.0f;
+          pnt = 0.0f;
+          hl = 0.0f;
+          pn = 0.0f;
+          c = qleft > 0 ? 0 : -(1 << 30);
+        } else {
+          c++;
+        }
+      };
+      if (__any_sync(0xffffffffu, (unsigned)(Cp - 1 - c) < 8u)) {
+#pragma unroll 1
+        for (int t = t0; t < t1; t++) step(t, std::true_type{});
+      } else {
+#pragma unroll 2
+        for (int t = t0; t < t1; t++) step(t, std::false_type{});
       }
     }
     cp_async_wait<0>();
     if (MODE == kCMain) {
-      unsigned bits = 32u * (unsigned)(wp - wp0) + (unsigned)na;
-      if (lane_in) {
-        if (na) *wp = (unsigned)(acc >> 32);
-        o.rowinfo[row] = make_uint2(bits, nb);
-      } else {
-        bits = 0;
-        nb = 0;
-      }
-      unsigned long long tb = bits, tz = nb;
       unsigned tr = repairs;
       for (int s = 16; s; s >>= 1) {
-        tb += __shfl_xor_sync(0xffffffffu, tb, s);
         tz += __shfl_xor_sync(0xffffffffu, tz, s);
         tr += __shfl_xor_sync(0xffffffffu, tr, s);
       }
       if (lane == 0) {
-        o.part_bits[p] = tb;
-        o.part_zeros[p] = tz;
-        atomicAdd(&st->nbal, tz);
+        atomicAdd(&st->nbal, (unsigned long long)tz);
         if (tr) atomicAdd(&st->nrepair, (unsigned long long)tr);
-        atomicAdd(&st->ncodes, (unsigned long long)(R * C - 1));
+        atomicAdd(&st->ncodes, (unsigned long long)((int64_t)min(cnt * g.prow, rows_left) * C - cnt));
       }
     } else if (MODE == kCHist) {
       if (pi == 0 && lane == 0) atomicAdd(&o.hist[kMaxAlpha], 1ull);
     }
-  } else if (have && MODE == kCMain && lane == 0) {
-    o.part_bits[p] = 0;
-    o.part_zeros[p] = 0;
   }
   if (MODE == kCCov) {
     __syncthreads();

@@ -2,6 +2,7 @@
 // quantizer, workspace layout.
 #pragma once
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 #include "../../include/permez_b200.h"
 #include "dmath.cuh"
