@@ -221,7 +221,8 @@ def main():
         return buf, info
 
     buf, info = compress_once()
-    full = buf.cpu().numpy()
+    full_t = buf.cpu()
+    full = full_t.numpy()
     hdr = P.Codec.parse_header(full)
     hdr.rows = x.shape[0]  # this shard's grid (the header carries the global rows)
     hdr.nblocks = nblk
@@ -373,57 +374,58 @@ def main():
                 "note": "float32 surfaces, predictor, quantizer and recurrence; every point within the bound"}
         del y32, db32, b32
 
-    # e2e through the public API with pinned host buffers, every step: H2D of
-    # the field, compress, D2H of the container; H2D of the container + block
-    # index walk on the host, decompress, D2H of the float32 grid
+    # e2e through the public host-to-host API (hostpipe.HostPipeline) with
+    # pinned host buffers, every step: the field goes host->device in slabs of
+    # whole block-rows, each slab is compressed and its records go device->host
+    # while the next slab uploads (validation blocks first, so m and the
+    # codebook exist before the first slab is encoded); the reverse for
+    # decompress (block index walk on the host inside the timed region).
+    # Wall clock around the call with a device synchronise on both sides.
     e2e_c = e2e_d = None
     if not args.no_e2e:
+        pipe = P.HostPipeline(codec)
         h_in = torch.empty(x.shape, dtype=torch.float32, pin_memory=True)
         h_in.copy_(x)
         h_out = torch.empty(int(info.nbytes) + (1 << 20), dtype=torch.uint8, pin_memory=True)
-        h_cont = torch.empty(int(info.nbytes), dtype=torch.uint8, pin_memory=True)
-        h_cont.copy_(dbuf)  # (the FP64 container: the codec buffer now holds the FP32 run)
         h_y = torch.empty(x.shape, dtype=torch.float32, pin_memory=True)
-        xd = torch.empty_like(x)
         e_ms, ed_ms = [], []
-        for _ in range(max(2, min(K, 3))):
+        for it in range(1 + max(2, min(K, 3))):
             if sharded:
                 dist.barrier()
             torch.cuda.synchronize()
-            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            s.record()
-            xd.copy_(h_in, non_blocking=True)
-            b2, i2 = codec.compress_staged(xd, cfg, block_row0=plan.block_row0, global_rows=grows,
-                                           allreduce=allreduce if sharded else None, d_val=d_val)
+            t0 = time.perf_counter()
+            n2, i2 = pipe.compress(h_in, cfg, h_out, block_row0=plan.block_row0, global_rows=grows,
+                                   allreduce=allreduce if sharded else None)
             if sharded:
                 exchange_record_sizes(i2.nbytes - i2.header_bytes, device=dev)
-            h_out[: i2.nbytes].copy_(b2, non_blocking=True)
-            e.record()
             torch.cuda.synchronize()
-            e_ms.append(s.elapsed_time(e))
+            t1 = time.perf_counter()
+            bi, bo = pipe.last_h2d_bytes, pipe.last_d2h_bytes
             if sharded:
                 dist.barrier()
             torch.cuda.synchronize()
-            s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            s2.record()
-            hoffs = P.Codec.index_blocks(h_cont.numpy(), hdr)
-            db = h_cont.to(dev, non_blocking=True)
-            do = torch.from_numpy(hoffs.view(np.int64)).to(dev, non_blocking=True)
-            yy = codec.decompress_device(db, hdr, do)
-            h_y.copy_(yy, non_blocking=True)
-            e2.record()
+            t2 = time.perf_counter()
+            pipe.decompress(h_out[:n2], h_y, shard_rows=x.shape[0] if sharded else None)
             torch.cuda.synchronize()
-            ed_ms.append(s2.elapsed_time(e2))
-        assert torch.equal(h_y[:1024], y[:1024].cpu())
+            t3 = time.perf_counter()
+            if it:  # the first pass allocates the slab buffers
+                e_ms.append(1e3 * (t1 - t0))
+                ed_ms.append(1e3 * (t3 - t2))
+                di, do_ = pipe.last_h2d_bytes, pipe.last_d2h_bytes
+        assert n2 == info.nbytes and torch.equal(h_out[:n2], full_t), "host pipeline container differs"
+        assert torch.equal(h_y.view(torch.int32), y.cpu().view(torch.int32)), "host pipeline grid differs"
         et = torch.tensor([sum(e_ms) / len(e_ms), sum(ed_ms) / len(ed_ms)], dtype=torch.float64, device=dev)
         if sharded:
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
         e2e_c = {"value": bytes_all / (float(et[0]) / 1e3) / 1e9, "unit": "GB/s", "ms_per_step": float(et[0]),
-                 "h2d_bytes_per_step": int(x.numel() * 4), "d2h_bytes_per_step": int(info.nbytes),
-                 "api": "Codec.compress_staged from a pinned host field, container copied to pinned host memory"}
+                 "h2d_bytes_per_step": int(bi), "d2h_bytes_per_step": int(bo),
+                 "api": "HostPipeline.compress: pinned host field -> pinned host container, slabs of whole "
+                        "block-rows, copies overlapped with the kernels; container identical to the device call"}
         e2e_d = {"value": bytes_all / (float(et[1]) / 1e3) / 1e9, "unit": "GB/s", "ms_per_step": float(et[1]),
-                 "h2d_bytes_per_step": int(info.nbytes), "d2h_bytes_per_step": int(x.numel() * 4),
-                 "api": "Codec.index_blocks + decompress_device from a pinned host container, grid to pinned host"}
+                 "h2d_bytes_per_step": int(di), "d2h_bytes_per_step": int(do_),
+                 "api": "HostPipeline.decompress: pinned host container -> pinned host grid (block index walk "
+                        "on the host, slabs, copies overlapped); grid identical to the device call"}
+        del h_in, h_out, h_y
 
     # roofline: algorithmic bytes per element 4 + 4 CR
     # (compress reads the f32 field and writes the container; decompress the

@@ -8,7 +8,8 @@ from . import errors, transform
 from .errors import PermezError
 from .pipeline import (Codec, CompressConfig, CompressInfo, GraphedCompressor, PipelinedCompressor,
                        PipelinedDecompressor, compress, decompress)
+from .hostpipe import HostPipeline
 from .predictor import PerceptronModel, init_model, lorenzo_coefficients
 
-__all__ = ["compress", "decompress", "Codec", "GraphedCompressor", "PipelinedCompressor", "PipelinedDecompressor", "CompressConfig", "CompressInfo", "PerceptronModel", "init_model",
+__all__ = ["compress", "decompress", "Codec", "HostPipeline", "GraphedCompressor", "PipelinedCompressor", "PipelinedDecompressor", "CompressConfig", "CompressInfo", "PerceptronModel", "init_model",
            "lorenzo_coefficients", "errors", "transform", "PermezError"]

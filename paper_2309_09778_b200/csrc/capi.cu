@@ -432,15 +432,46 @@ int pmz_compress_analyze(const float *d_in, const pmz_geom *g, const pmz_params 
 }
 
 namespace {
+// Small stream-ordered device -> host read (status words, fix-up lists) that
+// does not queue behind bulk copies on the DMA engines: a one-CTA kernel stores
+// into mapped pinned memory, the stream is synchronised, the bytes are copied
+// out.  (A cudaMemcpyAsync of a few bytes waits for every device->host slab
+// copy already queued on the copy engine: the slab pipeline of hostpipe.py
+// synchronises per slab and would serialise on that.)
+__global__ void k_read_small(const unsigned char *src, unsigned char *dst, int n) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+  __threadfence_system();
+}
+constexpr size_t kBounceBytes = 4096;
+int read_small(void *h_dst, const void *d_src, size_t bytes, cudaStream_t st) {
+  thread_local void *bounce = nullptr;
+  if (bytes <= kBounceBytes) {
+    if (!bounce && cudaHostAlloc(&bounce, kBounceBytes, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
+      bounce = nullptr;
+      cudaGetLastError();
+    }
+    if (bounce) {
+      void *dptr = nullptr;
+      if (cudaHostGetDevicePointer(&dptr, bounce, 0) == cudaSuccess) {
+        k_read_small<<<1, 256, 0, st>>>(static_cast<const unsigned char *>(d_src), static_cast<unsigned char *>(dptr),
+                                        (int)bytes);
+        if (cudaStreamSynchronize(st) != cudaSuccess) return PMZ_ERR_CUDA;
+        memcpy(h_dst, bounce, bytes);
+        return PMZ_OK;
+      }
+      cudaGetLastError();
+    }
+  }
+  if (cudaMemcpyAsync(h_dst, d_src, bytes, cudaMemcpyDeviceToHost, st) != cudaSuccess) return PMZ_ERR_CUDA;
+  if (cudaStreamSynchronize(st) != cudaSuccess) return PMZ_ERR_CUDA;
+  return PMZ_OK;
+}
 int64_t read_np_fixups(WsStatus *d_status, const pmz_np_fix *d_fix, cudaStream_t st, pmz_np_fix *h, int64_t cap) {
   unsigned long long n = 0;
-  if (cudaMemcpyAsync(&n, &d_status->nfix, sizeof(n), cudaMemcpyDeviceToHost, st) != cudaSuccess) return PMZ_ERR_CUDA;
-  if (cudaStreamSynchronize(st) != cudaSuccess) return PMZ_ERR_CUDA;
+  if (read_small(&n, &d_status->nfix, sizeof(n), st) != PMZ_OK) return PMZ_ERR_CUDA;
   const int64_t k = (int64_t)n < cap ? (int64_t)n : cap;
   if (k > 0 && h) {
-    if (cudaMemcpyAsync(h, d_fix, sizeof(pmz_np_fix) * (size_t)k, cudaMemcpyDeviceToHost, st) != cudaSuccess)
-      return PMZ_ERR_CUDA;
-    if (cudaStreamSynchronize(st) != cudaSuccess) return PMZ_ERR_CUDA;
+    if (read_small(h, d_fix, sizeof(pmz_np_fix) * (size_t)k, st) != PMZ_OK) return PMZ_ERR_CUDA;
   }
   return (int64_t)n;
 }
@@ -611,8 +642,7 @@ int pmz_compress_result(const pmz_geom *g, const pmz_params *p, int wrote_output
   // status and coverage are adjacent at the front of the workspace: one copy
   static_assert(sizeof(WsStatus) <= 256, "status slot");
   alignas(8) uint8_t front[256 + 18 * 8];
-  CK(cudaMemcpyAsync(front, d_ws, L.cov + 18 * 8, cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
+  if (read_small(front, d_ws, L.cov + 18 * 8, st) != PMZ_OK) return PMZ_ERR_CUDA;
   WsStatus hs;
   memcpy(&hs, front, sizeof(WsStatus));
   if (res) {
@@ -1006,8 +1036,7 @@ int pmz_decompress_result(const pmz_header *hdr, void *d_ws, uint64_t ws_bytes, 
   if (ws_bytes < L.total) return PMZ_ERR_WORKSPACE;
   cudaStream_t st = (cudaStream_t)stream;
   WsStatus hs;
-  CK(cudaMemcpyAsync(&hs, at<WsStatus>(d_ws, L.status), sizeof(WsStatus), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
+  if (read_small(&hs, at<WsStatus>(d_ws, L.status), sizeof(WsStatus), st) != PMZ_OK) return PMZ_ERR_CUDA;
   const int s = err_from_bits(hs.err_bits);
   if (s && getenv("PMZ_DEBUG"))
     fprintf(stderr, "pmz_decompress: status %d bits 0x%x first site %d part %d\n", s, hs.err_bits, hs.err_site,
@@ -1023,8 +1052,7 @@ int pmz_decompress_status(const pmz_header *hdr, void *d_ws, uint64_t ws_bytes, 
   if (ws_bytes < L.total) return PMZ_ERR_WORKSPACE;
   cudaStream_t st = (cudaStream_t)stream;
   WsStatus hs;
-  CK(cudaMemcpyAsync(&hs, at<WsStatus>(d_ws, L.status), sizeof(WsStatus), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
+  if (read_small(&hs, at<WsStatus>(d_ws, L.status), sizeof(WsStatus), st) != PMZ_OK) return PMZ_ERR_CUDA;
   if (res) {
     memset(res, 0, sizeof(*res));
     res->nblocks = (uint64_t)G.nblocks;
@@ -1076,8 +1104,7 @@ int pmz_transform_params(const float *d_in, const pmz_geom *g, const pmz_params 
   s = launch_check();
   if (s) return s;
   WsStatus hs;
-  CK(cudaMemcpyAsync(&hs, at<WsStatus>(d_ws, L.status), sizeof(WsStatus), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
+  if (read_small(&hs, at<WsStatus>(d_ws, L.status), sizeof(WsStatus), st) != PMZ_OK) return PMZ_ERR_CUDA;
   return err_from_bits(hs.err_bits);
 }
 
@@ -1244,6 +1271,22 @@ int pmz_log2_f32_batch(const float *d_x, uint64_t n, double *d_out, uint32_t *d_
 }
 
 
+// Host pipeline helper (hostpipe.py): gather n blocks of br x bc floats out of
+// a pinned row-major host field (row length `cols`) into a dense device array,
+// block i at d_dst + i * br * bc, by strided DMA copies on `stream`.
+extern "C" PMZ_API int pmz_copy_blocks_h2d(const float *h_field, int64_t cols, int32_t br, int32_t bc,
+                                           const int64_t *h_r0, const int64_t *h_c0, int64_t n, float *d_dst,
+                                           void *stream) {
+  if (!h_field || !d_dst || !h_r0 || !h_c0 || cols <= 0 || br <= 0 || bc <= 0 || n < 0) return PMZ_ERR_CONFIG;
+  for (int64_t i = 0; i < n; i++) {
+    const float *src = h_field + h_r0[i] * cols + h_c0[i];
+    if (cudaMemcpy2DAsync(d_dst + i * (int64_t)br * bc, (size_t)bc * 4, src, (size_t)cols * 4, (size_t)bc * 4,
+                          (size_t)br, cudaMemcpyHostToDevice, (cudaStream_t)stream) != cudaSuccess)
+      return PMZ_ERR_CUDA;
+  }
+  return PMZ_OK;
+}
+
 #ifdef PMZ_CSTATS
 extern "C" PMZ_API int pmz_cstats_read(void *host) {
   return cudaMemcpyFromSymbol(host, pmz::g_cstats, sizeof(pmz::g_cstats)) == cudaSuccess ? 0 : -1;
@@ -1295,8 +1338,7 @@ int pmz_train_gradient(const float *d_in, const pmz_geom *g, const pmz_params *p
   s = launch_check();
   if (s) return s;
   WsStatus hs;
-  CK(cudaMemcpyAsync(&hs, at<WsStatus>(d_ws, L.status), sizeof(WsStatus), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
+  if (read_small(&hs, at<WsStatus>(d_ws, L.status), sizeof(WsStatus), st) != PMZ_OK) return PMZ_ERR_CUDA;
   return err_from_bits(hs.err_bits);
 }
 

@@ -1,0 +1,358 @@
+"""Host-to-host compress / decompress of ONE field with the PCIe copies
+overlapped with the kernels (the e2e path of bench.py).
+
+A field that lives in pinned host memory is cut along its slowest axis into
+slabs of whole block-rows -- the same cut as the multi-GPU sharding
+(sharding.py): blocks are independent given the model, m and
+the codebook -- and the slabs stream through the GPU on
+three CUDA streams: host->device copy of slab i+1, the kernels of slab i and
+the device->host copy of slab i-1 run concurrently, so the call is bound by
+the larger of the two PCIe directions instead of their sum.
+
+compress: m and the codebook depend on the validation blocks of the whole
+field (select_m SPEC.md:362-370, estimate_codebook SPEC.md:389-397), so those
+blocks (sample_blocks / split_validation) are uploaded first
+by strided DMA copies (pmz_copy_blocks_h2d) into a dense column of blocks;
+their coverage and final-code histograms are computed once and handed to every
+slab exactly where the multi-GPU path all-reduces them.  The container is
+byte-identical to the single-call one (tests/test_hostpipe.py).
+
+decompress: the host walks the block records (pmz_index_blocks), each slab's
+records go to the device behind a copy of the header (the code lengths), the
+slab is decoded into a device buffer and copied into the pinned output grid.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .errors import ConfigError, check
+from .pipeline import Codec, CompressConfig, CompressInfo, _ptr, grid_view_shape, host_b_a, make_params
+from .trainer import validation_blocks
+
+
+def _sp(stream: torch.cuda.Stream):
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+class HostPipeline:
+    """Reusable slab pipeline on one device.  ``slab_bytes`` is the target size
+    of a slab of the float32 field (whole block-rows); device buffers are kept
+    between calls."""
+
+    DEPTH = 3  # slab buffers in flight per direction
+
+    def __init__(self, codec: Codec | None = None, device=None, slab_bytes: int = 128 << 20):
+        self.codec = codec or Codec(device)
+        self.device = self.codec.device
+        self.lib = self.codec.lib
+        self.slab_bytes = int(slab_bytes)
+        self.s_in = torch.cuda.Stream(self.device)
+        self.s_c = torch.cuda.Stream(self.device)
+        self.s_out = torch.cuda.Stream(self.device)
+        self._bufs: dict = {}
+        self.last_h2d_bytes = 0
+        self.last_d2h_bytes = 0
+
+    def _buf(self, name: str, nbytes: int) -> torch.Tensor:
+        cur = self._bufs.get(name)
+        if cur is None or cur.numel() < nbytes:
+            cur = torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=self.device)
+            self._bufs[name] = cur
+        return cur
+
+    def _pinned(self, name: str, n: int, dtype) -> torch.Tensor:
+        cur = self._bufs.get(name)
+        if cur is None or cur.numel() < n or cur.dtype != dtype:
+            cur = torch.empty(max(int(n), 1), dtype=dtype, pin_memory=True)
+            self._bufs[name] = cur
+        return cur
+
+    def _slabs(self, nbr: int, br: int, cols: int):
+        per = max(1, self.slab_bytes // max(1, br * cols * 4))
+        return [(b0, min(nbr, b0 + per)) for b0 in range(0, nbr, per)]
+
+    # ------------------------------------------------------------------ compress
+    def compress(self, h_field: torch.Tensor, cfg: CompressConfig, h_out: torch.Tensor, *, block_row0: int = 0,
+                 global_rows: int | None = None, allreduce=None, write_header: bool = True):
+        """Compress a pinned float32 CPU tensor into the pinned uint8 tensor
+        ``h_out``; returns (container bytes, CompressInfo).  Raises
+        ConfigError when ``h_out`` is too small.
+
+        Multi-GPU: ``h_field`` is this rank's shard (whole
+        block-rows from global block-row ``block_row0`` of a field of
+        ``global_rows`` rows), ``allreduce(tensor)`` sums a device int64
+        tensor across the ranks (the coverage and validation-code histograms
+        of the shard's validation blocks) and only rank 0 writes the header."""
+        if h_field.dtype != torch.float32 or h_field.is_cuda or not h_field.is_pinned():
+            raise ConfigError("HostPipeline.compress expects a pinned float32 CPU tensor")
+        if h_out.dtype != torch.uint8 or not h_out.is_pinned():
+            raise ConfigError("HostPipeline.compress expects a pinned uint8 output tensor")
+        h_field = h_field.contiguous()
+        (rows, cols), S = grid_view_shape(tuple(h_field.shape))
+        x2 = h_field.view(rows, cols)
+        br, bc = cfg.block_rows, cfg.block_cols
+        nbr, nbc = (rows + br - 1) // br, (cols + bc - 1) // bc
+        grows = rows if global_rows is None else int(global_rows)
+        gnb = ((grows + br - 1) // br) * nbc
+        val = np.asarray(validation_blocks(gnb, cfg.sample_rate, cfg.seed), dtype=np.int64)
+        lo_b = block_row0 * nbc
+        val = val[(val >= lo_b) & (val < lo_b + nbr * nbc)] - lo_b  # this shard's validation blocks, local ids
+        vr, vc = val // max(nbc, 1), val % max(nbc, 1)
+        ragged = bool(len(val)) and bool(((vr + 1) * br > rows).any() or ((vc + 1) * bc > cols).any())
+        slabs = self._slabs(nbr, br, cols)
+        if (ragged or len(slabs) < 2 or rows == 1 or br == 1) and allreduce is None and block_row0 == 0 \
+                and grows == rows and write_header:
+            return self._compress_whole(x2, h_field.shape, cfg, h_out)
+        if ragged:
+            raise ConfigError("HostPipeline.compress: sharded fields need full-size validation blocks")
+        lib, codec = self.lib, self.codec
+        p = make_params(cfg, S)
+        self.last_h2d_bytes = self.last_d2h_bytes = 0
+
+        # ---- prologue: the validation blocks as a dense column of blocks
+        nval = len(val)
+        gv = N.Geom(max(nval, 1) * br, bc, 0, max(nval, 1) * br)
+        xv = self._buf("xv", nval * br * bc * 4).view(torch.float32)
+        h_r0 = np.ascontiguousarray(vr * br)
+        h_c0 = np.ascontiguousarray(vc * bc)
+        check(lib.pmz_copy_blocks_h2d(ctypes.c_void_p(x2.data_ptr()), cols, br, bc,
+                                      h_r0.ctypes.data_as(ctypes.c_void_p), h_c0.ctypes.data_as(ctypes.c_void_p),
+                                      nval, _ptr(xv), _sp(self.s_in)), "copy_blocks_h2d")
+        self.last_h2d_bytes += nval * br * bc * 4
+        ev_val = torch.cuda.Event()
+        ev_val.record(self.s_in)
+        wsz = ctypes.c_uint64(0)
+        check(lib.pmz_workspace_size(ctypes.byref(p), ctypes.byref(gv), ctypes.byref(wsz)), "workspace_size")
+        wsv = self._buf("wsv", wsz.value)
+        d_valv = torch.arange(nval, dtype=torch.int64, device=self.device)
+        d_none = torch.empty(0, dtype=torch.int64, device=self.device)
+
+        # slab geometry and buffers
+        geoms = []
+        ws_need = cap_need = 0
+        for (b0, b1) in slabs:
+            r0, r1 = b0 * br, min(b1 * br, rows)
+            g = N.Geom(r1 - r0, cols, block_row0 + b0, grows)
+            check(lib.pmz_workspace_size(ctypes.byref(p), ctypes.byref(g), ctypes.byref(wsz)), "workspace_size")
+            ws_need = max(ws_need, int(wsz.value))
+            cap = ctypes.c_uint64(0)
+            check(lib.pmz_max_container_size(ctypes.byref(p), ctypes.byref(g), ctypes.byref(cap)), "max_size")
+            cap_need = max(cap_need, int(cap.value))
+            geoms.append((g, r0, r1))
+        ws = self._buf("ws", ws_need)
+        slab_elems = max(g.rows for g, _, _ in geoms) * cols
+        xin = [self._buf(f"xin{i}", slab_elems * 4).view(torch.float32) for i in range(self.DEPTH)]
+        outs = [self._buf(f"out{i}", cap_need) for i in range(2)]
+        ev_in = [torch.cuda.Event() for _ in slabs]
+        ev_cdone = [torch.cuda.Event() for _ in slabs]
+        ev_out = [torch.cuda.Event() for _ in slabs]
+
+        def enqueue_h2d(i):
+            g, r0, r1 = geoms[i]
+            if i >= self.DEPTH:
+                self.s_in.wait_event(ev_cdone[i - self.DEPTH])  # the buffer's previous slab has been encoded
+            with torch.cuda.stream(self.s_in):
+                xin[i % self.DEPTH][: (r1 - r0) * cols].copy_(x2[r0:r1].reshape(-1), non_blocking=True)
+            ev_in[i].record(self.s_in)
+            self.last_h2d_bytes += (r1 - r0) * cols * 4
+
+        for i in range(min(self.DEPTH, len(slabs))):
+            enqueue_h2d(i)
+
+        with torch.cuda.stream(self.s_c):
+            sc = _sp(self.s_c)
+            self.s_c.wait_event(ev_val)
+            # coverage and final-code histograms of the validation blocks (all-reduced
+            # across the ranks of a sharded field, exactly where compress_staged does)
+            n_cov, n_hist = 18 * 8, (65536 + 1) * 8
+            if nval:
+                codec.analyze(xv, p, gv, d_valv, wsv, sc)
+                off = lib.pmz_ws_coverage(_ptr(wsv), ctypes.byref(p), ctypes.byref(gv)) - wsv.data_ptr()
+                cov = wsv[off: off + n_cov]
+            else:  # a shard without validation blocks contributes zeros
+                cov = torch.zeros(n_cov, dtype=torch.uint8, device=self.device)
+            if allreduce is not None:
+                allreduce(cov.view(torch.int64))
+            cov = cov.clone()
+            if nval:
+                check(lib.pmz_compress_codes(_ptr(xv), ctypes.byref(gv), ctypes.byref(p), _ptr(d_valv), nval,
+                                             _ptr(wsv), wsv.numel(), sc), "compress_codes")
+                off = lib.pmz_ws_histogram(_ptr(wsv), ctypes.byref(p), ctypes.byref(gv)) - wsv.data_ptr()
+                hist = wsv[off: off + n_hist]
+            else:
+                hist = torch.zeros(n_hist, dtype=torch.uint8, device=self.device)
+            if allreduce is not None:
+                allreduce(hist.view(torch.int64))
+            hist = hist.clone()
+
+            pos = 0
+            tot = dict(nblocks=0, ntrivial=0, nbal=0, nrepair=0, ncodes=0, launches=0)
+            res = N.Result()
+            header_bytes = 0
+            for i, (g, r0, r1) in enumerate(geoms):
+                xs = xin[i % self.DEPTH][: (r1 - r0) * cols]
+                self.s_c.wait_event(ev_in[i])
+                if i >= 2:
+                    self.s_c.wait_event(ev_out[i - 2])  # the output buffer has been copied out
+                codec.analyze(xs, p, g, d_none, ws, sc)
+                off = lib.pmz_ws_coverage(_ptr(ws), ctypes.byref(p), ctypes.byref(g)) - ws.data_ptr()
+                ws[off: off + 18 * 8].copy_(cov)
+                check(lib.pmz_compress_codes(_ptr(xs), ctypes.byref(g), ctypes.byref(p), _ptr(d_none), 0, _ptr(ws),
+                                             ws.numel(), sc), "compress_codes")
+                off = lib.pmz_ws_histogram(_ptr(ws), ctypes.byref(p), ctypes.byref(g)) - ws.data_ptr()
+                ws[off: off + (65536 + 1) * 8].copy_(hist)
+                check(lib.pmz_compress_encode(_ptr(xs), ctypes.byref(g), ctypes.byref(p), _ptr(ws), ws.numel(), sc),
+                      "compress_encode")
+                out = outs[i % 2]
+                check(codec._write(p, g, write_header and i == 0, out, None, ws, sc, res),
+                      "compress_finish")  # synchronises s_c
+                ev_cdone[i].record(self.s_c)
+                n = int(res.header_bytes + res.record_bytes)
+                if i == 0:
+                    header_bytes = int(res.header_bytes)
+                if pos + n > h_out.numel():
+                    torch.cuda.synchronize(self.device)
+                    raise ConfigError(f"output buffer too small ({h_out.numel()} bytes)")
+                self.s_out.wait_event(ev_cdone[i])
+                with torch.cuda.stream(self.s_out):
+                    h_out[pos: pos + n].copy_(out[:n], non_blocking=True)
+                ev_out[i].record(self.s_out)
+                self.last_d2h_bytes += n
+                pos += n
+                if i + self.DEPTH < len(slabs):
+                    enqueue_h2d(i + self.DEPTH)
+                tot["nblocks"] += int(res.nblocks)
+                tot["ntrivial"] += int(res.ntrivial)
+                tot["nbal"] += int(res.nbal)
+                tot["nrepair"] += int(res.nrepair)
+                tot["ncodes"] += int(res.ncodes)
+                tot["launches"] += int(res.launches)
+        self.s_out.synchronize()
+        info = CompressInfo(pos, header_bytes, tot["nblocks"], tot["ntrivial"], tot["nbal"], tot["nrepair"],
+                            tot["ncodes"], int(res.m), int(res.max_code_len), [int(v) for v in cov.view(torch.int64).cpu()],
+                            tuple(h_field.shape), val, tot["launches"])
+        return pos, info
+
+    def _compress_whole(self, x2, shape, cfg, h_out):
+        """Fields the slab pipeline does not cover (one slab, ragged validation
+        blocks, one-row partitions): one upload, one compress, one copy-out."""
+        xd = self._buf("xwhole", x2.numel() * 4).view(torch.float32)[: x2.numel()].view(x2.shape)
+        xd.copy_(x2, non_blocking=True)
+        buf, info = self.codec.compress_device(xd, cfg)
+        if info.nbytes > h_out.numel():
+            raise ConfigError(f"output buffer too small ({h_out.numel()} bytes)")
+        h_out[: info.nbytes].copy_(buf, non_blocking=True)
+        torch.cuda.synchronize(self.device)
+        self.last_h2d_bytes, self.last_d2h_bytes = x2.numel() * 4, int(info.nbytes)
+        info.shape = tuple(shape)
+        return int(info.nbytes), info
+
+    # ---------------------------------------------------------------- decompress
+    def decompress(self, h_container: torch.Tensor, h_out: torch.Tensor | None = None,
+                   shard_rows: int | None = None) -> torch.Tensor:
+        """Decompress a pinned uint8 CPU tensor holding one container into the
+        pinned float32 grid ``h_out`` (rows x cols of the header; allocated
+        when absent).  ``shard_rows``: the container holds the header and the
+        records of one shard of that many rows (multi-GPU)."""
+        if h_container.dtype != torch.uint8 or h_container.is_cuda or not h_container.is_pinned():
+            raise ConfigError("HostPipeline.decompress expects a pinned uint8 CPU tensor")
+        lib, codec = self.lib, self.codec
+        cont = h_container.numpy()
+        h = Codec.parse_header(cont)
+        if shard_rows is not None:
+            h.rows = int(shard_rows)
+            h.nblocks = ((int(shard_rows) + int(h.block_rows) - 1) // int(h.block_rows)) * \
+                ((int(h.cols) + int(h.block_cols) - 1) // int(h.block_cols))
+        rows, cols = int(h.rows), int(h.cols)
+        if h_out is None:
+            h_out = torch.empty((rows, cols), dtype=torch.float32, pin_memory=True)
+        if h_out.numel() != rows * cols or h_out.dtype != torch.float32 or not h_out.is_pinned():
+            raise ConfigError("HostPipeline.decompress: output must be a pinned float32 tensor of the header's size")
+        y2 = h_out.view(rows, cols)
+        self.last_h2d_bytes = self.last_d2h_bytes = 0
+        if rows == 0 or cols == 0:
+            return h_out
+        offs = Codec.index_blocks(cont, h).view(np.int64)
+        br, bc = int(h.block_rows), int(h.block_cols)
+        nbr, nbc = (rows + br - 1) // br, (cols + bc - 1) // bc
+        slabs = self._slabs(nbr, br, cols)
+        hb = int(h.header_bytes)
+        b_a = host_b_a(h.b_r)
+        # per-slab headers, record ranges, offsets relative to [header | slab records]
+        plan = []
+        rel = self._pinned("rel", int(h.nblocks) + len(slabs), torch.int64)
+        rel_np = rel.numpy()
+        k = 0
+        ws_need = rec_need = 0
+        wsz = ctypes.c_uint64(0)
+        for (b0, b1) in slabs:
+            r0, r1 = b0 * br, min(b1 * br, rows)
+            hs = N.Header.from_buffer_copy(h)
+            hs.rows = r1 - r0
+            hs.nblocks = (b1 - b0) * nbc
+            lo, hi = int(offs[b0 * nbc]), int(offs[b1 * nbc])
+            nb1 = int(hs.nblocks) + 1
+            rel_np[k: k + nb1] = offs[b0 * nbc: b1 * nbc + 1] - lo + hb
+            check(lib.pmz_decompress_workspace_size(ctypes.byref(hs), ctypes.byref(wsz)), "workspace")
+            ws_need = max(ws_need, int(wsz.value))
+            rec_need = max(rec_need, hi - lo)
+            plan.append((hs, r0, r1, lo, hi, k, nb1))
+            k += nb1
+        ws = self._buf("dws", ws_need)
+        din = [self._buf(f"din{i}", hb + rec_need + 64) for i in range(self.DEPTH)]
+        doff = [self._buf(f"doff{i}", 8 * (max(q[6] for q in plan))).view(torch.int64) for i in range(self.DEPTH)]
+        slab_elems = max(q[2] - q[1] for q in plan) * cols
+        dout = [self._buf(f"dout{i}", slab_elems * 4).view(torch.float32) for i in range(2)]
+        ev_in = [torch.cuda.Event() for _ in plan]
+        ev_cdone = [torch.cuda.Event() for _ in plan]
+        ev_out = [torch.cuda.Event() for _ in plan]
+        hdr_bytes = h_container[:hb]
+
+        def enqueue_h2d(i):
+            hs, r0, r1, lo, hi, k0, nb1 = plan[i]
+            if i >= self.DEPTH:
+                self.s_in.wait_event(ev_cdone[i - self.DEPTH])
+            with torch.cuda.stream(self.s_in):
+                d = din[i % self.DEPTH]
+                d[:hb].copy_(hdr_bytes, non_blocking=True)
+                d[hb: hb + hi - lo].copy_(h_container[lo:hi], non_blocking=True)
+                doff[i % self.DEPTH][:nb1].copy_(rel[k0: k0 + nb1], non_blocking=True)
+            ev_in[i].record(self.s_in)
+            self.last_h2d_bytes += hb + hi - lo + 8 * nb1
+
+        for i in range(min(self.DEPTH, len(plan))):
+            enqueue_h2d(i)
+        launches = 0
+        res = N.Result()
+        with torch.cuda.stream(self.s_c):
+            sc = _sp(self.s_c)
+            for i, (hs, r0, r1, lo, hi, k0, nb1) in enumerate(plan):
+                d, o = din[i % self.DEPTH], doff[i % self.DEPTH]
+                n = hb + hi - lo
+                y = dout[i % 2]
+                self.s_c.wait_event(ev_in[i])
+                if i >= 2:
+                    self.s_c.wait_event(ev_out[i - 2])
+                check(lib.pmz_decompress_prepare(_ptr(d), n, ctypes.byref(hs), b_a, _ptr(o), _ptr(ws), ws.numel(), sc),
+                      "decompress")
+                check(min(codec.np_fix_decompress(hs, ws, sc), 0), "np_fixups")
+                check(lib.pmz_decompress_run(_ptr(d), n, ctypes.byref(hs), b_a, _ptr(o), _ptr(y), _ptr(ws),
+                                             ws.numel(), sc), "decompress")
+                check(lib.pmz_decompress_status(ctypes.byref(hs), _ptr(ws), ws.numel(), sc, ctypes.byref(res)),
+                      "decompress")  # synchronises s_c
+                launches += int(res.launches)
+                ev_cdone[i].record(self.s_c)
+                self.s_out.wait_event(ev_cdone[i])
+                with torch.cuda.stream(self.s_out):
+                    y2[r0:r1].reshape(-1).copy_(y[: (r1 - r0) * cols], non_blocking=True)
+                ev_out[i].record(self.s_out)
+                self.last_d2h_bytes += (r1 - r0) * cols * 4
+                if i + self.DEPTH < len(plan):
+                    enqueue_h2d(i + self.DEPTH)
+        self.s_out.synchronize()
+        self.last_decompress_launches = launches
+        return h_out
