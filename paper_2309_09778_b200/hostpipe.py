@@ -60,7 +60,7 @@ class HostPipeline:
     def _buf(self, name: str, nbytes: int) -> torch.Tensor:
         cur = self._bufs.get(name)
         if cur is None or cur.numel() < nbytes:
-            cur = torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=self.device)
+            cur = torch.empty((max(int(nbytes), 16) + 15) & ~15, dtype=torch.uint8, device=self.device)
             self._bufs[name] = cur
         return cur
 
