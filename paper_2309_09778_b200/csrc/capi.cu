@@ -250,9 +250,6 @@ void launch_cmain(const float *x, const Geom &G, const KParams &k, const int64_t
   CMainOut o = cmain_out(d_ws, L);
   if (MODE == kCMain) {
     o.dump = reinterpret_cast<uint16_t *>(k.code_dump);
-    // the rows add their bit / balance counts to their partition's totals
-    cudaMemsetAsync(o.part_bits, 0, (size_t)G.nparts * sizeof(unsigned long long), st);
-    cudaMemsetAsync(o.part_zeros, 0, (size_t)G.nparts * sizeof(unsigned long long), st);
   }
   // m is selected on the device: size for the largest shared-memory table;
   // alphabets above 2^12 take the launch whose codewords come from global memory
@@ -272,6 +269,8 @@ void launch_cmain(const float *x, const Geom &G, const KParams &k, const int64_t
     cudaFuncSetAttribute(fb, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2);
     fb<<<grid, kCW * 32, smem2, st>>>(x, G, k, at<BlkP>(d_ws, L.blkp), at<WsStatus>(d_ws, L.status), d_val, n_val,
                                       o, chain);
+    k_c_part_totals<<<(unsigned)((G.nparts + 7) / 8), 256, 0, st>>>(G, at<BlkP>(d_ws, L.blkp), o.rowinfo, o.part_bits,
+                                                                    o.part_zeros, at<WsStatus>(d_ws, L.status));
   }
 }
 template <int MODE>

@@ -364,12 +364,11 @@ __global__ void __launch_bounds__(kCW * 32, 2)
     const double lgp = P.lg_pos, lgn = P.lg_neg, zcode = P.zero_code;
     unsigned *amb = &st->unresolved;
     const bool lane0 = lane == 0;
-    bool lane_in = lane < min(g.prow, rows_left);
-    int c = -lane;     // column in the lane's current partition (< 0: not started)
-    int qleft = cnt;   // partitions of the chain this lane has not finished
+    // > 0: the lane has a row in its current partition (lanes >= partition_rows never do)
+    int rleft = lane < g.prow ? min(rows_left, cnt * g.prow) - lane : -(1 << 28);
+    int cb = -lane;  // column in the lane's current partition = t + cb (< 0: not started)
     double vW = 0.0, pnt = 0.0;  // TRUE: own previous value (W), lane - 1's one column back (NW)
     double hl = 0.0, pn = 0.0;   // RECONSTRUCTED (exact): same
-    double nvt = 0.0, nhl = 0.0;  // N of the coming step: lane - 1's values, shuffled at the end of the step before
     unsigned long long acc = 0;  // row encoder: pending bits, left-aligned
     int na = 0;
     unsigned nb = 0, repairs = 0, tz = 0;
@@ -397,7 +396,12 @@ __global__ void __launch_bounds__(kCW * 32, 2)
       auto step = [&](const int t, auto swc) {
         constexpr bool SW = decltype(swc)::value;
         const int gc = t - lane;  // column of the chain's sweep: the ring slot
+        const int c = t + cb;     // column in the lane's current partition
         const bool started = gc >= 0;
+        const bool lane_in = rleft > 0;
+        // first column of a row (SW copy only: rows start right after a row end): W and NW are
+        // 0, partition-local neighbours (D2); the registers still hold the previous row's tail
+        const bool first = SW && c == 0;
         const bool active = lane_in & ((unsigned)c < (unsigned)C);
         const bool anchor = lane0 & (c == 0);
         // zero_sub_floor_magnitudes + class from the bits (transform.py:205-210; D8 classes)
@@ -422,8 +426,9 @@ __global__ void __launch_bounds__(kCW * 32, 2)
           va = u == 0 ? zcode : va;
         }
         // TRUE-surface residual from approximate surfaces, certified rounding
+        const double nvt = __shfl_up_sync(0xffffffffu, vW, 1);
         bool hamb;
-        const double at = c_pred_approx<PK>(k, vW, nvt, pnt, lane0, hamb);
+        const double at = c_pred_approx<PK>(k, first ? 0.0 : vW, nvt, first ? 0.0 : pnt, lane0, hamb);
         pnt = nvt;
         vW = started ? va : vW;
         const double q = __dmul_rn(__dsub_rn(va, at), inv);
@@ -458,15 +463,17 @@ __global__ void __launch_bounds__(kCW * 32, 2)
         } else {
           const bool out = qbig | (abs(rq) >= center);
           // decoder simulation on the RECONSTRUCTED surface (exact FP64, D3 order)
+          const double nhl = __shfl_up_sync(0xffffffffu, hl, 1);
+          const double hW = first ? 0.0 : hl, hNW = first ? 0.0 : pn;
           double ar;
           if (PK == 3) {  // predict_init (D3): a w2_0 + a w2_1 with w2 = 1/2, exactly as written
-            double h = __dsub_rn(__dadd_rn(hl, nhl), pn);
-            h = lane0 ? hl : h;
+            double h = __dsub_rn(__dadd_rn(hW, nhl), hNW);
+            h = lane0 ? hW : h;
             ar = h < 0.0 ? __dmul_rn(slope, h) : h;
             const double a2 = __dmul_rn(ar, 0.5);
             ar = __dadd_rn(a2, a2);
           } else {
-            ar = predict_steady<PK>(k, hl, nhl, pn, lane0);
+            ar = predict_steady<PK>(k, hW, nhl, hNW, lane0);
           }
           const double dq = __dmul_rn(qi, two_ba);
           const double vhat = __dadd_rn(ar, dq);
@@ -498,10 +505,10 @@ __global__ void __launch_bounds__(kCW * 32, 2)
               const float xz = __uint_as_float(u | (neg ? 0x80000000u : 0u));
               bool rep = false;
               double hr;  // (addressed only here: the common path keeps hnew in registers)
-              fin = c_rare<PK>(k, Pp, lane, xz, v, w, n, nw, hl, nhl, pn, anchor, center, amb, &hr, &rep);
+              fin = c_rare<PK>(k, Pp, lane, xz, v, w, n, nw, hW, nhl, hNW, anchor, center, amb, &hr, &rep);
               hnew = hr;
               repairs += rep ? 1u : 0u;
-              if (MODE == kCMain && anchor) o.anchors[p + (cnt - qleft)] = v;  // forced anchor, D1
+              if (MODE == kCMain && anchor) o.anchors[p + (-cb) / Cp] = v;  // forced anchor, D1
               if (fin == 0 && !anchor) {
                 if (MODE == kCMain) brow[nb] = v;
                 nb++;
@@ -537,9 +544,7 @@ __global__ void __launch_bounds__(kCW * 32, 2)
               na -= 32;
             }
           }
-          nhl = __shfl_up_sync(0xffffffffu, hl, 1);
         }
-        nvt = __shfl_up_sync(0xffffffffu, vW, 1);
         // end of the lane's row: close it and move to the same row of the chain's next
         // partition (surfaces restart from 0: partition-local neighbours, D2)
         if (SW && c == Cp - 1) {
@@ -547,32 +552,23 @@ __global__ void __launch_bounds__(kCW * 32, 2)
             if (lane_in) {
               const unsigned bits = 32u * (unsigned)(wp - (o.rowbits + row * (int64_t)g.bc)) + (unsigned)na;
               if (na) *wp = (unsigned)(acc >> 32);
-              o.rowinfo[row] = make_uint2(bits, nb);
-              const int64_t pc = p + (cnt - qleft);
-              atomicAdd(&o.part_bits[pc], (unsigned long long)bits);  // zeroed before the launch
-              if (nb) atomicAdd(&o.part_zeros[pc], (unsigned long long)nb);
+              o.rowinfo[row] = make_uint2(bits, nb);  // (partition totals: k_c_part_totals)
               tz += nb;
             }
             row += g.prow;
             wp = o.rowbits + row * (int64_t)g.bc;
             brow = o.balrow + row * (int64_t)g.bc;
-            if (dump != nullptr) dump = o.dump + tcode_base(g, p + (cnt - qleft) + 1) + (int64_t)lane * C;
+            if (dump != nullptr) dump += (int64_t)g.prow * g.bc;  // tcode_base of the next partition
           }
-          qleft--;
-          lane_in = qleft > 0 && lane < min(g.prow, rows_left - (cnt - qleft) * g.prow);
+          cb -= Cp;
+          rleft -= g.prow;
           acc = 0;
           na = 0;
           nb = 0;
-          vW = 0.0;
-          pnt = 0.0;
-          hl = 0.0;
-          pn = 0.0;
-          c = qleft > 0 ? 0 : -(1 << 30);
-        } else {
-          c++;
         }
       };
-      if (__any_sync(0xffffffffu, (unsigned)(Cp - 1 - c) < 8u)) {
+      const int cs = t0 + cb;  // a row ends within these 8 steps, or starts at the first of them
+      if (__any_sync(0xffffffffu, ((unsigned)(Cp - 1 - cs) < 8u) | (cs == 0))) {
 #pragma unroll 1
         for (int t = t0; t < t1; t++) step(t, std::true_type{});
       } else {
@@ -608,6 +604,39 @@ __global__ void __launch_bounds__(kCW * 32, 2)
     __syncthreads();
     for (int i = threadIdx.x; i < nalpha; i += blockDim.x)
       if (s_hist[i]) atomicAdd(&o.hist[i], (unsigned long long)s_hist[i]);
+  }
+}
+
+// Per-partition bit and balance-point totals from the rows' {bits, count}
+// (a warp per partition; trivial blocks have none).  The sweep closes rows one
+// lane at a time, so the sums are taken here in one coalesced pass.
+__global__ void __launch_bounds__(256) k_c_part_totals(Geom g, const BlkP *__restrict__ blkp,
+                                                       const uint2 *__restrict__ rowinfo,
+                                                       unsigned long long *part_bits,
+                                                       unsigned long long *part_zeros, WsStatus *st) {
+  count_launch(st);
+  const int lane = threadIdx.x & 31;
+  const int64_t p = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (p >= g.nparts) return;
+  int64_t b;
+  int pi;
+  part_of(g, p, b, pi);
+  unsigned tb = 0, tz = 0;
+  if (!blkp[b].trivial) {
+    const BlockBox bb = block_box(g, b);
+    if (lane < min(g.prow, bb.br - pi * g.prow)) {
+      const uint2 ri = rowinfo[p * g.prow + lane];
+      tb = ri.x;
+      tz = ri.y;
+    }
+  }
+  for (int s = 16; s; s >>= 1) {
+    tb += __shfl_xor_sync(0xffffffffu, tb, s);
+    tz += __shfl_xor_sync(0xffffffffu, tz, s);
+  }
+  if (lane == 0) {
+    part_bits[p] = tb;
+    part_zeros[p] = tz;
   }
 }
 

@@ -135,10 +135,10 @@ __global__ void __launch_bounds__(kCW * 32, 2)
     const float dpm = (float)k.dpos - mu, dnm = (float)k.dneg + mu, dpp = (float)k.dpos + mu, dnp = (float)k.dneg - mu;
     unsigned *amb = &st->unresolved;
     const bool lane0 = lane == 0;
-    bool lane_in = lane < min(g.prow, rows_left);
-    int c = -lane, qleft = cnt;
+    // > 0: the lane has a row in its current partition (lanes >= partition_rows never do)
+    int rleft = lane < g.prow ? min(rows_left, cnt * g.prow) - lane : -(1 << 28);
+    int cb = -lane;  // column in the lane's current partition = t + cb
     float vW = 0.0f, pnt = 0.0f, hl = 0.0f, pn = 0.0f;
-    float nvt = 0.0f, nhl = 0.0f;  // N of the coming step (shuffled at the end of the step before)
     unsigned long long acc = 0;
     int na = 0;
     unsigned nb = 0, repairs = 0, tz = 0;
@@ -160,8 +160,13 @@ __global__ void __launch_bounds__(kCW * 32, 2)
       // row-end branch is compiled only into that copy of the body)
       auto step = [&](const int t, auto swc) {
         constexpr bool SW = decltype(swc)::value;
-        const int gc = t - lane;
+        const int gc = t - lane;  // column of the chain's sweep: the ring slot
+        const int c = t + cb;     // column in the lane's current partition
         const bool started = gc >= 0;
+        const bool lane_in = rleft > 0;
+        // first column of a row (SW copy only: rows start right after a row end): W and NW are
+        // 0, partition-local neighbours (D2); the registers still hold the previous row's tail
+        const bool first = SW && c == 0;
         const bool active = lane_in & ((unsigned)c < (unsigned)C);
         const bool anchor = lane0 & (c == 0);
         const unsigned u0 = lds_u32(ring_s + ((unsigned)(gc & (kCRing - 1)) << 2));
@@ -172,7 +177,8 @@ __global__ void __launch_bounds__(kCW * 32, 2)
         float v = __fadd_rn(__log2f(__uint_as_float(u | (u == 0 ? 0x3f800000u : 0u))), neg ? lgn : lgp);
         v = u == 0 ? zc : v;
         // TRUE-surface residual and quantization in float32
-        const float at = c_pred32<PK>(k, vW, nvt, pnt, lane0);
+        const float nvt = __shfl_up_sync(0xffffffffu, vW, 1);
+        const float at = c_pred32<PK>(k, first ? 0.0f : vW, nvt, first ? 0.0f : pnt, lane0);
         pnt = nvt;
         vW = started ? v : vW;
         const float qr = rhaz32(__fmul_rn(__fsub_rn(v, at), inv));
@@ -186,7 +192,8 @@ __global__ void __launch_bounds__(kCW * 32, 2)
         } else {
           const bool out = big | (abs(rq) >= center);
           // decoder simulation (float32, the mirror of k_d_recon32)
-          const float ar = c_pred32<PK>(k, hl, nhl, pn, lane0);
+          const float nhl = __shfl_up_sync(0xffffffffu, hl, 1);
+          const float ar = c_pred32<PK>(k, first ? 0.0f : hl, nhl, first ? 0.0f : pn, lane0);
           const float vhat = __fadd_rn(ar, __fmul_rn(out ? 0.0f : qr, two_ba));
           const float d = __fsub_rn(vhat, v);
           const bool normal = (u - (kClsLo + 1u)) < (kClsHi - kClsLo - 1u);
@@ -220,7 +227,7 @@ __global__ void __launch_bounds__(kCW * 32, 2)
               brow[nb] = (double)v;  // the row's balance list (D9): the encoder's float32 value, exactly
               nb++;
             }
-            if (active & anchor) o.anchors[p + (cnt - qleft)] = (double)v;  // forced anchor, D1
+            if (active & anchor) o.anchors[p + (-cb) / Cp] = (double)v;  // forced anchor, D1
             if (dump != nullptr && active) dump[c] = anchor ? kAnc : (uint16_t)fin;
             if (STAB) {
               const uint2 e = lds_v2(tab_s + ((unsigned)(enc ? fin : nalpha) << 3));
@@ -238,41 +245,30 @@ __global__ void __launch_bounds__(kCW * 32, 2)
               na -= 32;
             }
           }
-          nhl = __shfl_up_sync(0xffffffffu, hl, 1);
         }
-        nvt = __shfl_up_sync(0xffffffffu, vW, 1);
         // end of the lane's row: close it, move to the same row of the chain's next partition
         if (SW && c == Cp - 1) {
           if (MODE == kCMain) {
             if (lane_in) {
               const unsigned bits = 32u * (unsigned)(wp - (o.rowbits + row * (int64_t)g.bc)) + (unsigned)na;
               if (na) *wp = (unsigned)(acc >> 32);
-              o.rowinfo[row] = make_uint2(bits, nb);
-              const int64_t pc = p + (cnt - qleft);
-              atomicAdd(&o.part_bits[pc], (unsigned long long)bits);  // zeroed before the launch
-              if (nb) atomicAdd(&o.part_zeros[pc], (unsigned long long)nb);
+              o.rowinfo[row] = make_uint2(bits, nb);  // (partition totals: k_c_part_totals)
               tz += nb;
             }
             row += g.prow;
             wp = o.rowbits + row * (int64_t)g.bc;
             brow = o.balrow + row * (int64_t)g.bc;
-            if (dump != nullptr) dump = o.dump + tcode_base(g, p + (cnt - qleft) + 1) + (int64_t)lane * C;
+            if (dump != nullptr) dump += (int64_t)g.prow * g.bc;  // tcode_base of the next partition
           }
-          qleft--;
-          lane_in = qleft > 0 && lane < min(g.prow, rows_left - (cnt - qleft) * g.prow);
+          cb -= Cp;
+          rleft -= g.prow;
           acc = 0;
           na = 0;
           nb = 0;
-          vW = 0.0f;
-          pnt = 0.0f;
-          hl = 0.0f;
-          pn = 0.0f;
-          c = qleft > 0 ? 0 : -(1 << 30);
-        } else {
-          c++;
         }
       };
-      if (__any_sync(0xffffffffu, (unsigned)(Cp - 1 - c) < 8u)) {
+      const int cs = t0 + cb;  // a row ends within these 8 steps, or starts at the first of them
+      if (__any_sync(0xffffffffu, ((unsigned)(Cp - 1 - cs) < 8u) | (cs == 0))) {
 #pragma unroll 1
         for (int t = t0; t < t1; t++) step(t, std::true_type{});
       } else {
