@@ -155,13 +155,17 @@ bool one_row_parts(const Geom &G) { return G.br == 1 || G.rows == 1; }
 // the throughput kernels need partition-level parallelism only, the latency
 // kernels also split each partition's work across a CTA.  PMZ_PATH=latency |
 // throughput overrides the size rule (tests exercise both on small fields).
-bool use_tpath(const Geom &G) {
+// The size rule is per direction (tools/path_cross.py, C2-like fields of 1024
+// columns): the throughput compress wins from ~9 K partitions on, the
+// thread-per-substream throughput decoder from ~6 K (C4, 3136 partitions:
+// compress 1.88 -> 1.06 ms, decompress 4.94 -> 1.63 ms on the latency path).
+bool use_tpath(const Geom &G, bool decomp = false) {
   if (G.fp32 || G.force_tpath) return true;  // the FP32 perf mode and the code dump: throughput path only
   if (one_row_parts(G)) return false;
   const char *e = getenv("PMZ_PATH");
   if (e && e[0] == 'l') return false;
   if (e && e[0] == 't') return true;
-  return G.nparts >= kTputMinParts;
+  return G.nparts >= (decomp ? kTputMinPartsD : kTputMinPartsC);
 }
 
 WsLayout compress_layout(const Geom &g) {
@@ -833,7 +837,7 @@ DecLayout dec_layout(const Geom &g) {
   L.lut = take(4ull * ((1u << kLutBits) + kLut2Max));            // first + second level
   L.lut1 = take(kDLutBytes + 16);                                 // k_d_decode's tables + subtable counter
   L.npfix = take(sizeof(pmz_np_fix) * (size_t)(g.nblocks + 1));
-  L.tpath = use_tpath(g);
+  L.tpath = use_tpath(g, true);
   if (L.tpath) {
     L.codes = take(2 * (size_t)g.nparts * (size_t)g.prow * (size_t)g.bc);  // raster per partition (tcode_base)
     L.rowz = take(4 * (size_t)g.nparts * (size_t)g.prow + 4);  // code-0 count per row

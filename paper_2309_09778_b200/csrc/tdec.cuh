@@ -25,8 +25,9 @@
 
 namespace pmz {
 
-// throughput path from this many partitions on (capi.cu use_tpath)
-constexpr int64_t kTputMinParts = 2048;
+// throughput path from this many partitions on (capi.cu use_tpath): compress / decompress
+constexpr int64_t kTputMinPartsC = 9216;
+constexpr int64_t kTputMinPartsD = 6144;
 
 // raster-contiguous per-partition code layout (index r * C + c), capacity prow x bc
 __host__ __device__ __forceinline__ int64_t tcode_base(const Geom &g, int64_t p) {
