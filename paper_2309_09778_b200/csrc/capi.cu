@@ -6,6 +6,7 @@
 #include <cstring>
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
 
 #include "common.cuh"
 #include "compress.cuh"
@@ -245,7 +246,18 @@ void launch_cmain(const float *x, const Geom &G, const KParams &k, const int64_t
                   const WsLayout &L, cudaStream_t st) {
   // kCMain: a warp sweeps a chain of up to `chain` consecutive partitions of a
   // block as one wavefront (PMZ_CHAIN overrides the default for experiments)
-  int chain = 8;
+  // Longer chains save more ramps but leave fewer, longer work items: keep at
+  // least ~6 rounds of chains over the GPU's resident warps (2 CTAs of kCW
+  // warps per SM), so a shard of a multi-GPU run (1/8 of C5: 32768 partitions)
+  // still balances.
+  static int sm_count = 0;
+  if (!sm_count) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sm_count <= 0)
+      sm_count = 148;
+  }
+  int chain = (int)std::min<int64_t>(8, std::max<int64_t>(1, G.nparts / ((int64_t)sm_count * 2 * kCW * 6)));
   if (const char *e = getenv("PMZ_CHAIN")) chain = atoi(e) > 0 ? atoi(e) : chain;
   unsigned grid;
   if (MODE == kCMain) grid = (unsigned)((c_nchains(G, chain) + kCW - 1) / kCW);

@@ -19,4 +19,7 @@ timeout 1200 ncu --set full --clock-control none --import-source on --kernel-nam
   -k regex:"k_c_mainILi3ELi0ELb1|k_c_write|k_stats|k_d_decode|k_d_reconILi3" -c 5 -o gpurun_out/full_c5 \
   python tools/scale_prof.py C5 > gpurun_out/ncu_full.log 2>&1
 echo "full rc=$?"
+# the e2e path against the box's PCIe ceiling, and the other BASELINE configs
+{ python tools/pcie_duplex.py 4.41 8.59; python tools/e2e_check.py --check --steps 2; } > gpurun_out/e2e.txt 2>&1
+{ for c in C1 C2 C3 C4; do python tools/scale_check.py $c | tail -3; done; python tools/path_cross.py; GEN=C4 python tools/path_cross.py 50000x500; } > gpurun_out/configs.txt 2>&1
 ls -la gpurun_out
