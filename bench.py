@@ -463,6 +463,24 @@ def main():
     roof_d["traffic_kernel"] = tr.get("decompress_dominant_kernel")
     roof_d["pipeline"] = roof(d_step, "whole decompress")
 
+    # what actually bounds the dominant kernels: instruction
+    # issue.  Executed warp instructions per launch from the committed ncu
+    # capture, divided by the live stage time, against SMs x 4 schedulers x
+    # the SM clock sampled during the timed region.
+    def issue(roofd, key, ms):
+        wi = tr.get(key)
+        mhz = sampler.summary().get("sm_mhz")
+        if not wi or not mhz:
+            return
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        peak = sms * 4 * mhz * 1e6
+        roofd["issue"] = {"warp_inst_per_launch": wi, "achieved_warp_inst_per_s": wi / (ms / 1e3),
+                          "peak_warp_inst_per_s": peak, "frac": wi / (ms / 1e3) / peak,
+                          "note": "instruction-issue bound (ncu instruction count of the dominant kernel / live "
+                                  "stage time); the HBM fraction above is the contract's figure"}
+    issue(roof_c, "compress_dominant_warp_inst_per_launch", float(cs[ic]))
+    issue(roof_d, "decompress_dominant_warp_inst_per_launch", float(ds[id_]))
+
     # CPU baseline + parity on the same sample (rank 0, N = 1): the oracle
     # restatement of the reference path on all host cores, and the CUDA path
     # on the identical sample -- containers must be byte-identical

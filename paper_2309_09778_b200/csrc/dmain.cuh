@@ -30,8 +30,17 @@
 
 namespace pmz {
 
-constexpr int kDDT = 512;          // decoder threads (partitions) per CTA
-constexpr int kDRB = 8;            // 16-byte stream blocks in each thread's shared ring
+#ifndef PMZ_DDT
+#define PMZ_DDT 512
+#endif
+#ifndef PMZ_DRB
+#define PMZ_DRB 8
+#endif
+#ifndef PMZ_DMINB
+#define PMZ_DMINB 1
+#endif
+constexpr int kDDT = PMZ_DDT;      // decoder threads (partitions) per CTA
+constexpr int kDRB = PMZ_DRB;      // 16-byte stream blocks in each thread's shared ring
 
 // First-level decode table over the top LB stream bits (built once per
 // container by k_d_lut): entry = symbol | length << SB for a codeword of at
@@ -116,7 +125,7 @@ __host__ __device__ constexpr size_t d_dec_smem() {
 }
 
 template <typename E>
-__global__ void __launch_bounds__(kDDT) k_d_decode(const uint8_t *__restrict__ buf, unsigned long long buf_n, Geom g,
+__global__ void __launch_bounds__(kDDT, PMZ_DMINB) k_d_decode(const uint8_t *__restrict__ buf, unsigned long long buf_n, Geom g,
                                                    const BlkP *__restrict__ blkp, const DecTab *__restrict__ tab,
                                                    const uint16_t *__restrict__ sym, int nalpha,
                                                    const E *__restrict__ lut1,
@@ -197,7 +206,9 @@ __global__ void __launch_bounds__(kDDT) k_d_decode(const uint8_t *__restrict__ b
     const unsigned lim = (wi >> 2) + (kDRB - 1u);
     while (nexti <= lim) issue(nexti++);
     cp_async_commit();
-    if (wide) cp_async_wait<1>();
+    // (a 4-block ring holds only the blocks of the coming eight codes: wait for this call's copies)
+    if (kDRB < 8) cp_async_wait<0>();
+    else if (wide) cp_async_wait<1>();
     else cp_async_wait<2>();
   };
   unsigned long long bits = 0;  // left-justified, zeros below the nb valid bits

@@ -38,6 +38,13 @@ def _sp(stream: torch.cuda.Stream):
     return ctypes.c_void_p(stream.cuda_stream)
 
 
+def plan_slabs(nbr: int, block_rows: int, cols: int, slab_bytes: int):
+    """Slabs of whole block-rows of about ``slab_bytes`` of float32 field:
+    [(first block-row, one past the last)], contiguous, covering [0, nbr)."""
+    per = max(1, int(slab_bytes) // max(1, block_rows * cols * 4))
+    return [(b0, min(nbr, b0 + per)) for b0 in range(0, nbr, per)]
+
+
 class HostPipeline:
     """Reusable slab pipeline on one device.  ``slab_bytes`` is the target size
     of a slab of the float32 field (whole block-rows); device buffers are kept
@@ -72,8 +79,7 @@ class HostPipeline:
         return cur
 
     def _slabs(self, nbr: int, br: int, cols: int):
-        per = max(1, self.slab_bytes // max(1, br * cols * 4))
-        return [(b0, min(nbr, b0 + per)) for b0 in range(0, nbr, per)]
+        return plan_slabs(nbr, br, cols, self.slab_bytes)
 
     # ------------------------------------------------------------------ compress
     def compress(self, h_field: torch.Tensor, cfg: CompressConfig, h_out: torch.Tensor, *, block_row0: int = 0,

@@ -127,3 +127,16 @@ def test_no_cpu_fallback_without_cuda():
     from paper_2309_09778_b200 import errors as E
     with pytest.raises(E.DeviceError):
         P.compress(np.ones((4, 4), np.float32))
+
+
+def test_hostpipe_slab_plan():
+    """hostpipe.plan_slabs: contiguous slabs of whole block-rows covering the field."""
+    from paper_2309_09778_b200.hostpipe import plan_slabs
+    for nbr, br, cols, sb in [(4096, 256, 2048, 128 << 20), (8, 256, 3600, 1 << 20), (1, 256, 500, 1 << 30),
+                              (196, 256, 500, 10 << 20), (0, 256, 512, 1 << 20)]:
+        sl = plan_slabs(nbr, br, cols, sb)
+        assert [a for a, _ in sl] == ([0] + [b for _, b in sl[:-1]] if sl else [])
+        assert (sl[-1][1] if sl else 0) == nbr and all(b > a for a, b in sl)
+        per = max(1, sb // (br * cols * 4))
+        assert all(b - a == per for a, b in sl[:-1]) and (not sl or sl[-1][1] - sl[-1][0] <= per)
+    assert len(plan_slabs(4096, 256, 2048, 128 << 20)) == 64  # C5: 64 slabs of 64 block-rows

@@ -36,7 +36,7 @@ def stalls(rep, kernel):
 
 def main():
     dst, reps = sys.argv[1], sys.argv[2:]
-    lines, traffic = [], {}
+    lines, traffic, insts = [], {}, {}
     for rep in reps:
         for k in raw(rep):
             name = k.get("Kernel Name", ("?", ""))[0]
@@ -46,7 +46,12 @@ def main():
                 if key in k:
                     v, u = k[key]
                     lines.append(f"   {key:62s} {v} {u}")
-            lines.append("   " + stalls(rep, short.replace("void ", "").split("::")[-1].split("<")[0]).replace("\n", "\n   "))
+            st = stalls(rep, short.replace("void ", "").split("::")[-1].split("<")[0])
+            lines.append("   " + st.replace("\n", "\n   "))
+            for ln in st.splitlines():  # "samples N instructions M": executed warp instructions of the launch
+                w = ln.split()
+                if len(w) >= 4 and w[0] == "samples" and w[2] == "instructions":
+                    insts[short] = int(w[3])
             try:
                 rd = float(k["dram__bytes_read.sum"][0].replace(",", ""))
                 wr = float(k["dram__bytes_write.sum"][0].replace(",", ""))
@@ -61,9 +66,13 @@ def main():
         if "k_c_main<3, 0, 1>" in name:  # the dominant compress kernel (bench roofline.traffic)
             tr["compress_dominant_bytes_per_launch"] = b
             tr["compress_dominant_kernel"] = name
+            tr["compress_dominant_warp_inst_per_launch"] = insts.get(name)
         if "k_d_recon" in name:  # the dominant decompress kernel
             tr["decompress_dominant_bytes_per_launch"] = b
             tr["decompress_dominant_kernel"] = name
+            # the bench's dominant decompress stage runs the decoder and the reconstruct kernel
+            dec = sum(v for k2, v in insts.items() if "k_d_decode" in k2)
+            tr["decompress_dominant_warp_inst_per_launch"] = (insts.get(name) or 0) + dec
     if tr:
         tr["source"] = os.path.basename(dst)
         path = os.path.join(os.path.dirname(__file__), "..", "profiles", "traffic_latest.json")
