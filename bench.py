@@ -120,6 +120,13 @@ def cpu_sample(x2d):
     return x2d[: min(rows, take)]
 
 
+def bench_config(args, world: int) -> dict:
+    """`config` of the JSON line, identical in both arms (--impl ours / reference)."""
+    return {"workload": workload(args.config, args.eps),
+            "l2": "input 8 GiB >> 126 MB L2 (no flush needed), one field at a time",
+            "parallelism": f"shard{world} (whole block-rows)" if world > 1 else "single"}
+
+
 def oracle_compress_time(xs: np.ndarray, eps: float, reps: int, threads: int):
     from oracle import oracle as O
     cfg = O.OracleConfig(b_r=eps, repair_factor=1.0)
@@ -154,9 +161,9 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": gbs, "unit": "GB/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload(args.config, args.eps),
-                   "path": "oracle/permez_oracle.c (C restatement of the reference path: the reference ships "
-                           "no compress code) + numpy split, OpenMP over blocks"},
+        "config": bench_config(args, args.gpus),  # the same dict as the CUDA arm's line
+        "reference_path": "oracle/permez_oracle.c (C restatement of the reference path: the reference ships "
+                          "no compress code) + numpy split, OpenMP over blocks",
         "compression_ratio": len(buf) / xs.nbytes,
         "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": threads, "kind": "port", "sample": sample},
         "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -511,9 +518,7 @@ def main():
             "metric": METRIC, "value": comp_gbs, "unit": "GB/s", "n_gpus": world, "steps": K,
             "warmup": args.warmup, "ms_per_step": c_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload(args.config, args.eps),
-                       "l2": "input 8 GiB >> 126 MB L2 (no flush needed), one field at a time",
-                       "parallelism": f"shard{world} (whole block-rows)" if world > 1 else "single"},
+            "config": bench_config(args, world),
             "compression_ratio": cr, "max_rel_err": max_rel, "m": info.m,
             "decompress": {"value": dec_gbs, "unit": "GB/s", "ms_per_step": d_step, "roofline": roof_d,
                            "e2e": e2e_d},
