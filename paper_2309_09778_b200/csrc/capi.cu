@@ -157,9 +157,10 @@ bool one_row_parts(const Geom &G) { return G.br == 1 || G.rows == 1; }
 // kernels also split each partition's work across a CTA.  PMZ_PATH=latency |
 // throughput overrides the size rule (tests exercise both on small fields).
 // The size rule is per direction (tools/path_cross.py, C2-like fields of 1024
-// columns): the throughput compress wins from ~9 K partitions on, the
+// columns; profiles/r2_configs.txt): the throughput compress wins from ~5 K
+// partitions on (with chains sized to the partition count), the
 // thread-per-substream throughput decoder from ~6 K (C4, 3136 partitions:
-// compress 1.88 -> 1.06 ms, decompress 4.94 -> 1.63 ms on the latency path).
+// decompress 4.84 ms on the throughput path, 1.72 ms on the latency path).
 bool use_tpath(const Geom &G, bool decomp = false) {
   if (G.fp32 || G.force_tpath) return true;  // the FP32 perf mode and the code dump: throughput path only
   if (one_row_parts(G)) return false;

@@ -26,7 +26,7 @@
 namespace pmz {
 
 // throughput path from this many partitions on (capi.cu use_tpath): compress / decompress
-constexpr int64_t kTputMinPartsC = 9216;
+constexpr int64_t kTputMinPartsC = 5120;
 constexpr int64_t kTputMinPartsD = 6144;
 
 // raster-contiguous per-partition code layout (index r * C + c), capacity prow x bc

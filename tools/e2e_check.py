@@ -14,7 +14,7 @@ import paper_2309_09778_b200 as P  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="C5")
 ap.add_argument("--steps", type=int, default=3)
-ap.add_argument("--slab-mb", type=int, default=256)
+ap.add_argument("--slab-mb", type=int, default=128)
 ap.add_argument("--check", action="store_true")
 a = ap.parse_args()
 dev = torch.device("cuda", 0)
