@@ -118,3 +118,30 @@ def test_two_ranks_slab_pipeline_container_identical(tmp_path, oracle):
     out = str(tmp_path / "shard")
     mp.spawn(_worker, args=(2, _free_port(), out), nprocs=2, join=True)
     assert open(f"{out}.0", "rb").read() + open(f"{out}.1", "rb").read() == ref
+
+
+@pytest.mark.slow
+def test_slab_pipeline_c3_full_size():
+    """C3 at full size (512 MiB, 16384 partitions) in 8 slabs of 64 MiB: the
+    slab container equals the single-call one (which tests/test_gpu_fullsize.py
+    pins to the oracle byte for byte); slab decode equals the device decode."""
+    import paper_2309_09778_b200 as P
+    from paper_2309_09778_b200 import synthetic
+    from paper_2309_09778_b200.pipeline import grid_view_shape
+    x = synthetic.generate("C3", device="cuda")
+    (r, c), _ = grid_view_shape(tuple(x.shape))
+    x = x.reshape(r, c).contiguous()
+    cfg = P.CompressConfig(rel_error=1e-2, repair_factor=1.0)
+    codec = P.Codec("cuda:0")
+    ref, rinfo = codec.compress_device(x, cfg)
+    ref = ref.cpu()
+    h = P.Codec.parse_header(ref.numpy())
+    offs = torch.from_numpy(P.Codec.index_blocks(ref.numpy(), h).view(np.int64)).cuda()
+    y_ref = codec.decompress_device(ref.cuda(), h, offs).cpu()
+    pipe = P.HostPipeline(codec, slab_bytes=64 << 20)
+    h_out = torch.empty(ref.numel() + (1 << 16), dtype=torch.uint8, pin_memory=True)
+    n, info = pipe.compress(_pin(x.cpu()), cfg, h_out)
+    assert n == ref.numel() and torch.equal(h_out[:n], ref)
+    assert (info.m, info.nbal, info.nrepair, info.ncodes) == (rinfo.m, rinfo.nbal, rinfo.nrepair, rinfo.ncodes)
+    y = pipe.decompress(h_out[:n])
+    assert torch.equal(y.view(torch.int32), y_ref.view(torch.int32))
