@@ -227,7 +227,9 @@ __global__ void __launch_bounds__(kCW * 32, 2)
               brow[nb] = (double)v;  // the row's balance list (D9): the encoder's float32 value, exactly
               nb++;
             }
-            if (active & anchor) o.anchors[p + (-cb) / Cp] = (double)v;  // forced anchor, D1
+            if (__builtin_expect(anchor, 0)) {  // forced anchor, D1 (lane 0, once per partition)
+              if (active) o.anchors[p + (-cb) / Cp] = (double)v;
+            }
             if (dump != nullptr && active) dump[c] = anchor ? kAnc : (uint16_t)fin;
             if (STAB) {
               const uint2 e = lds_v2(tab_s + ((unsigned)(enc ? fin : nalpha) << 3));

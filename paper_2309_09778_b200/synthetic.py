@@ -10,6 +10,7 @@ from __future__ import annotations
 
 import math
 
+import numpy as np
 import torch
 
 # name -> (shape, rel error bounds, seed, description)
@@ -31,7 +32,11 @@ def _gen(seed: int, device) -> torch.Generator:
 def grf(shape, beta: float, gen: torch.Generator, device) -> torch.Tensor:
     """Gaussian random field with power spectrum |k|^-beta (k=0 zeroed), standardized."""
     noise = torch.randn(shape, generator=gen, device=device, dtype=torch.float32)
-    f = torch.fft.rfftn(noise)
+    # CPU: numpy's pocketfft (float32 in, complex64 out).  torch's CPU FFT corrupts the heap
+    # now and then on this image ("free(): corrupted unsorted chunks" inside irfftn of a
+    # 20x500x500 field, with no other native code loaded), which would abort a test run.
+    cpu = torch.device(device).type == "cpu"
+    f = torch.from_numpy(np.fft.rfftn(noise.numpy())) if cpu else torch.fft.rfftn(noise)
     del noise
     k2 = None
     for ax, n in enumerate(shape):
@@ -46,7 +51,8 @@ def grf(shape, beta: float, gen: torch.Generator, device) -> torch.Tensor:
     amp = torch.where(k2 > 0, k2.clamp_min(1e-30) ** (-beta / 4.0), torch.zeros_like(k2))
     f.mul_(amp)
     del amp, k2
-    out = torch.fft.irfftn(f, s=shape)
+    out = torch.from_numpy(np.ascontiguousarray(np.fft.irfftn(f.numpy(), s=shape, axes=tuple(range(len(shape)))))) if cpu \
+        else torch.fft.irfftn(f, s=shape)
     del f
     out -= out.mean()
     out /= out.std()
