@@ -979,17 +979,33 @@ int pmz_decompress_run(const uint8_t *d_buf, uint64_t n, const pmz_header *hdr, 
   WsStatus *S = at<WsStatus>(d_ws, L.status);
   if (G.nblocks > 0 && L.tpath) {
     const int center = 1 << ((int)hdr->m - 1);
-#define PMZ_T_DECODE(E)                                                                                             \
+    // a thread per partition substream: big CTAs when the partitions fill every SM
+    // twice over, small ones otherwise so that they spread over all SMs (C3: 16384
+    // partitions are 32 CTAs of 512 threads, or 128 CTAs of 128)
+    int sms = 148;
+    {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
+    }
+    const bool big = G.nparts >= (int64_t)sms * 2 * kDDT;
+#define PMZ_T_DECODE(E, T)                                                                                          \
   do {                                                                                                              \
-    CK(cudaFuncSetAttribute(k_d_decode<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d_dec_smem<E>()));     \
-    k_d_decode<E><<<(unsigned)((G.nparts + kDDT - 1) / kDDT), kDDT, d_dec_smem<E>(), st>>>(                         \
+    CK(cudaFuncSetAttribute(k_d_decode<E, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,                          \
+                            (int)d_dec_smem<E, T>()));                                                              \
+    k_d_decode<E, T><<<(unsigned)((G.nparts + T - 1) / T), T, d_dec_smem<E, T>(), st>>>(                            \
         d_buf, n, G, at<BlkP>(d_ws, L.blkp), at<DecTab>(d_ws, L.tab), at<uint16_t>(d_ws, L.sym), 1 << (int)hdr->m, \
         at<E>(d_ws, L.lut1), at<unsigned long long>(d_ws, L.part_bits), at<unsigned long long>(d_ws, L.part_off),  \
         at<unsigned long long>(d_ws, L.pay_off), at<uint16_t>(d_ws, L.codes), at<unsigned>(d_ws, L.zflag),         \
         at<unsigned>(d_ws, L.rowz), S);                                                                             \
   } while (0)
-    if (d_lut16((int)hdr->m)) PMZ_T_DECODE(uint16_t);
-    else PMZ_T_DECODE(unsigned);
+    if (d_lut16((int)hdr->m)) {
+      if (big) PMZ_T_DECODE(uint16_t, kDDT);
+      else PMZ_T_DECODE(uint16_t, kDDTSmall);
+    } else {
+      if (big) PMZ_T_DECODE(unsigned, kDDT);
+      else PMZ_T_DECODE(unsigned, kDDTSmall);
+    }
 #undef PMZ_T_DECODE
     const unsigned grid = (unsigned)((G.nparts + kDRW - 1) / kDRW);
 #define PMZ_T_RECON(PKV)                                                                                            \

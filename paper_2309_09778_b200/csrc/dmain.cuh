@@ -119,13 +119,14 @@ __global__ void k_d_lut(const DecTab *__restrict__ tab, const uint16_t *__restri
 }
 
 // k_d_decode: dynamic shared memory = the tables + the per-thread stream rings
-template <typename E>
+constexpr int kDDTSmall = 128;     // CTA size when the partitions do not fill the GPU at kDDT (spread over all SMs)
+template <typename E, int T>
 __host__ __device__ constexpr size_t d_dec_smem() {
-  return d_lut_bytes<E>() + (size_t)kDDT * kDRB * 16;
+  return d_lut_bytes<E>() + (size_t)T * kDRB * 16;
 }
 
-template <typename E>
-__global__ void __launch_bounds__(kDDT, PMZ_DMINB) k_d_decode(const uint8_t *__restrict__ buf, unsigned long long buf_n, Geom g,
+template <typename E, int T>
+__global__ void __launch_bounds__(T, PMZ_DMINB) k_d_decode(const uint8_t *__restrict__ buf, unsigned long long buf_n, Geom g,
                                                    const BlkP *__restrict__ blkp, const DecTab *__restrict__ tab,
                                                    const uint16_t *__restrict__ sym, int nalpha,
                                                    const E *__restrict__ lut1,
@@ -149,12 +150,12 @@ __global__ void __launch_bounds__(kDDT, PMZ_DMINB) k_d_decode(const uint8_t *__r
   {
     const uint4 *src = reinterpret_cast<const uint4 *>(lut1);
     uint4 *dst = reinterpret_cast<uint4 *>(s_lut);
-    for (int i = threadIdx.x; i < (int)(d_lut_bytes<E>() / 16); i += kDDT) dst[i] = src[i];
+    for (int i = threadIdx.x; i < (int)(d_lut_bytes<E>() / 16); i += T) dst[i] = src[i];
   }
   const int maxl = tab->maxl;
   const int k2 = d_l2_bits<E>(maxl);
   __syncthreads();
-  const int64_t p = (int64_t)blockIdx.x * kDDT + threadIdx.x;
+  const int64_t p = (int64_t)blockIdx.x * T + threadIdx.x;
   if (p >= g.nparts) return;
   int64_t b;
   int pi;
