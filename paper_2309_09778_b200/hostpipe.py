@@ -110,11 +110,12 @@ class HostPipeline:
         vr, vc = val // max(nbc, 1), val % max(nbc, 1)
         ragged = bool(len(val)) and bool(((vr + 1) * br > rows).any() or ((vc + 1) * bc > cols).any())
         slabs = self._slabs(nbr, br, cols)
-        if (ragged or len(slabs) < 2 or rows == 1 or br == 1) and allreduce is None and block_row0 == 0 \
-                and grows == rows and write_header:
+        whole = ragged or len(slabs) < 2 or rows == 1 or br == 1 or cfg.code_dump is not None
+        if whole and allreduce is None and block_row0 == 0 and grows == rows and write_header:
             return self._compress_whole(x2, h_field.shape, cfg, h_out)
-        if ragged:
-            raise ConfigError("HostPipeline.compress: sharded fields need full-size validation blocks")
+        if ragged or cfg.code_dump is not None:
+            raise ConfigError("HostPipeline.compress: sharded fields need full-size validation blocks "
+                              "(and no code dump: its layout is per field, not per slab)")
         lib, codec = self.lib, self.codec
         p = make_params(cfg, S)
         self.last_h2d_bytes = self.last_d2h_bytes = 0
