@@ -249,6 +249,13 @@ PMZ_API int pmz_parse_header(const uint8_t *h_buf, uint64_t n, pmz_header *hdr);
 /* Walk the block records (host memory) and emit the byte offset of each
  * block record (nblocks entries).  Corrupt / TruncatedStream on bad framing. */
 PMZ_API int pmz_index_blocks(const uint8_t *h_buf, uint64_t n, const pmz_header *hdr, uint64_t *h_block_offsets);
+/* The same walk over the blocks [b0, b1) only, starting at byte pos0 (the
+ * end offset of block b0 - 1, or hdr->header_bytes for b0 = 0): fills
+ * h_block_offsets[0 .. b1 - b0] (the last entry is the end of block b1 - 1).
+ * The host pipeline walks one slab of block-rows at a time while the earlier
+ * slabs are already uploading. */
+PMZ_API int pmz_index_blocks_range(const uint8_t *h_buf, uint64_t n, const pmz_header *hdr, uint64_t b0, uint64_t b1,
+                                   uint64_t pos0, uint64_t *h_block_offsets);
 
 /* --- decompression --------------------------------------------------------- */
 

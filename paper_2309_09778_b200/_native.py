@@ -84,6 +84,7 @@ _SIGS = {
                                c_uint64, VP, ctypes.POINTER(Result)]),
     "pmz_parse_header": (c_int32, [VP, c_uint64, ctypes.POINTER(Header)]),
     "pmz_index_blocks": (c_int32, [VP, c_uint64, ctypes.POINTER(Header), VP]),
+    "pmz_index_blocks_range": (c_int32, [VP, c_uint64, ctypes.POINTER(Header), c_uint64, c_uint64, c_uint64, VP]),
     "pmz_decompress_workspace_size": (c_int32, [ctypes.POINTER(Header), ctypes.POINTER(c_uint64)]),
     "pmz_decompress": (c_int32, [VP, c_uint64, ctypes.POINTER(Header), c_double, VP, VP, VP, c_uint64, VP]),
     "pmz_decompress_enqueue": (c_int32, [VP, c_uint64, ctypes.POINTER(Header), c_double, VP, VP, VP, c_uint64, VP]),

@@ -786,13 +786,15 @@ int pmz_parse_header(const uint8_t *h, uint64_t n, pmz_header *hd) {
   return PMZ_OK;
 }
 
-int pmz_index_blocks(const uint8_t *h, uint64_t n, const pmz_header *hd, uint64_t *offs) {
+int pmz_index_blocks_range(const uint8_t *h, uint64_t n, const pmz_header *hd, uint64_t b0, uint64_t b1,
+                           uint64_t pos0, uint64_t *offs) {
   Geom G = make_geom((int64_t)hd->rows, (int64_t)hd->cols, (int)hd->block_rows, (int)hd->block_cols,
                      (int)hd->partition_rows, 0);
-  uint64_t pos = hd->header_bytes;
-  for (int64_t b = 0; b < G.nblocks; b++) {
+  if (b0 > b1 || b1 > (uint64_t)G.nblocks || !offs) return PMZ_ERR_CONFIG;
+  uint64_t pos = pos0;
+  for (int64_t b = (int64_t)b0; b < (int64_t)b1; b++) {
     if (pos >= n) return PMZ_ERR_TRUNCATED;
-    offs[b] = pos;
+    offs[b - (int64_t)b0] = pos;
     uint8_t t = h[pos];
     if (t == 1) { pos += 1; continue; }
     if (t != 0) return PMZ_ERR_CORRUPT;
@@ -814,9 +816,15 @@ int pmz_index_blocks(const uint8_t *h, uint64_t n, const pmz_header *hd, uint64_
     pos += head + 8 * nb + pay;
     if (pos > n) return PMZ_ERR_TRUNCATED;
   }
-  if (pos != n) return PMZ_ERR_CORRUPT;
-  if (G.nblocks >= 0) offs[G.nblocks] = pos;
+  if (b1 == (uint64_t)G.nblocks && pos != n) return PMZ_ERR_CORRUPT;  // the last record ends the container
+  offs[b1 - b0] = pos;
   return PMZ_OK;
+}
+
+int pmz_index_blocks(const uint8_t *h, uint64_t n, const pmz_header *hd, uint64_t *offs) {
+  Geom G = make_geom((int64_t)hd->rows, (int64_t)hd->cols, (int)hd->block_rows, (int)hd->block_cols,
+                     (int)hd->partition_rows, 0);
+  return pmz_index_blocks_range(h, n, hd, 0, (uint64_t)G.nblocks, hd->header_bytes, offs);
 }
 
 // ---------------------------------------------------------------------------
