@@ -140,3 +140,41 @@ def test_hostpipe_slab_plan():
         per = max(1, sb // (br * cols * 4))
         assert all(b - a == per for a, b in sl[:-1]) and (not sl or sl[-1][1] - sl[-1][0] <= per)
     assert len(plan_slabs(4096, 256, 2048, 128 << 20)) == 64  # C5: 64 slabs of 64 block-rows
+
+
+def test_index_blocks_range_matches_full_walk(oracle):
+    """pmz_index_blocks_range over consecutive block ranges reproduces the
+    whole-container walk (the host pipeline indexes one slab at a time), keeps
+    its framing checks and only the range that ends the container checks the
+    container's end."""
+    import ctypes
+    from paper_2309_09778_b200 import _native as N
+    from paper_2309_09778_b200 import errors as E
+    from paper_2309_09778_b200.pipeline import Codec
+    _, buf, _ = _container(oracle, shape=(1100, 900), b_r=1e-2)  # 5 x 4 blocks, ragged edges
+    a = np.frombuffer(buf, np.uint8).copy()
+    h = Codec.parse_header(a)
+    full = Codec.index_blocks(a, h)
+    lib = N.load()
+
+    def rng(arr, b0, b1, pos0):
+        out = np.zeros(b1 - b0 + 1, np.uint64)
+        s = lib.pmz_index_blocks_range(arr.ctypes.data_as(ctypes.c_void_p), arr.size, ctypes.byref(h), b0, b1, pos0,
+                                       out.ctypes.data_as(ctypes.c_void_p))
+        return s, out
+
+    nb = int(h.nblocks)
+    pos, got = int(h.header_bytes), []
+    for b0 in range(0, nb, 4):  # one block-row at a time
+        s, out = rng(a, b0, min(nb, b0 + 4), pos)
+        assert s == 0
+        got.extend(out[:-1].tolist())
+        pos = int(out[-1])
+    got.append(pos)
+    assert got == full.tolist()
+    assert rng(a, 3, 2, 0)[0] == -1 and rng(a, 0, nb + 1, int(h.header_bytes))[0] == -1  # ConfigError
+    # an inner range does not see trailing bytes, the final one does; truncation is seen where it bites
+    longer = np.concatenate([a, np.zeros(3, np.uint8)])
+    assert rng(longer, 0, 4, int(h.header_bytes))[0] == 0
+    assert isinstance(E.status_error(rng(longer, nb - 4, nb, int(full[nb - 4]))[0]), E.Corrupt)
+    assert rng(a[: int(full[2])].copy(), 0, 4, int(h.header_bytes))[0] in (-10, -14)
