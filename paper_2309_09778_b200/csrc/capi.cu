@@ -455,30 +455,56 @@ namespace {
 // copy already queued on the copy engine: the slab pipeline of hostpipe.py
 // synchronises per slab and would serialise on that.)
 __global__ void k_read_small(const unsigned char *src, unsigned char *dst, int n) {
-  for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+  if ((((uintptr_t)src | (uintptr_t)dst | (uintptr_t)n) & 3) == 0) {
+    for (int i = threadIdx.x; i < (n >> 2); i += blockDim.x)
+      reinterpret_cast<unsigned *>(dst)[i] = reinterpret_cast<const unsigned *>(src)[i];
+  } else {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+  }
   __threadfence_system();
 }
-constexpr size_t kBounceBytes = 4096;
-int read_small(void *h_dst, const void *d_src, size_t bytes, cudaStream_t st) {
+// (a full fix-up list: 4096 entries of 40 bytes)
+constexpr size_t kBounceBytes = 192 * 1024;
+void *small_bounce(void **dptr) {
   thread_local void *bounce = nullptr;
-  if (bytes <= kBounceBytes) {
-    if (!bounce && cudaHostAlloc(&bounce, kBounceBytes, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
-      bounce = nullptr;
-      cudaGetLastError();
-    }
-    if (bounce) {
-      void *dptr = nullptr;
-      if (cudaHostGetDevicePointer(&dptr, bounce, 0) == cudaSuccess) {
-        k_read_small<<<1, 256, 0, st>>>(static_cast<const unsigned char *>(d_src), static_cast<unsigned char *>(dptr),
-                                        (int)bytes);
-        if (cudaStreamSynchronize(st) != cudaSuccess) return PMZ_ERR_CUDA;
-        memcpy(h_dst, bounce, bytes);
-        return PMZ_OK;
-      }
-      cudaGetLastError();
-    }
+  if (!bounce && cudaHostAlloc(&bounce, kBounceBytes, cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) {
+    bounce = nullptr;
+    cudaGetLastError();
+  }
+  if (bounce && cudaHostGetDevicePointer(dptr, bounce, 0) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return bounce;
+}
+int read_small(void *h_dst, const void *d_src, size_t bytes, cudaStream_t st) {
+  void *dptr = nullptr;
+  void *bounce = bytes <= kBounceBytes ? small_bounce(&dptr) : nullptr;
+  if (bounce) {
+    k_read_small<<<1, 256, 0, st>>>(static_cast<const unsigned char *>(d_src), static_cast<unsigned char *>(dptr),
+                                    (int)bytes);
+    if (cudaStreamSynchronize(st) != cudaSuccess) return PMZ_ERR_CUDA;
+    memcpy(h_dst, bounce, bytes);
+    return PMZ_OK;
   }
   if (cudaMemcpyAsync(h_dst, d_src, bytes, cudaMemcpyDeviceToHost, st) != cudaSuccess) return PMZ_ERR_CUDA;
+  if (cudaStreamSynchronize(st) != cudaSuccess) return PMZ_ERR_CUDA;
+  return PMZ_OK;
+}
+// The mirror: a small stream-ordered host -> device write that does not queue
+// behind the slab uploads (the kernel reads the mapped bounce buffer).
+// Synchronises the stream (the bounce buffer is reused by the next call).
+int write_small(void *d_dst, const void *h_src, size_t bytes, cudaStream_t st) {
+  void *dptr = nullptr;
+  void *bounce = bytes <= kBounceBytes ? small_bounce(&dptr) : nullptr;
+  if (bounce) {
+    memcpy(bounce, h_src, bytes);
+    k_read_small<<<1, 256, 0, st>>>(static_cast<const unsigned char *>(dptr), static_cast<unsigned char *>(d_dst),
+                                    (int)bytes);
+    if (cudaStreamSynchronize(st) != cudaSuccess) return PMZ_ERR_CUDA;
+    return PMZ_OK;
+  }
+  if (cudaMemcpyAsync(d_dst, h_src, bytes, cudaMemcpyHostToDevice, st) != cudaSuccess) return PMZ_ERR_CUDA;
   if (cudaStreamSynchronize(st) != cudaSuccess) return PMZ_ERR_CUDA;
   return PMZ_OK;
 }
@@ -497,7 +523,7 @@ int apply_np_fixups(pmz_np_fix *d_fix, BlkP *d_blkp, WsStatus *d_status, int64_t
   if (n > nmax) return PMZ_ERR_CONFIG;
   for (int64_t i = 0; i < n; i++)
     if (h[i].block < 0 || h[i].block >= nmax) return PMZ_ERR_CONFIG;
-  CK(cudaMemcpyAsync(d_fix, h, sizeof(pmz_np_fix) * (size_t)n, cudaMemcpyHostToDevice, st));
+  if (write_small(d_fix, h, sizeof(pmz_np_fix) * (size_t)n, st) != PMZ_OK) return PMZ_ERR_CUDA;
   k_np_apply<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(d_fix, n, eps0, b_a, d_blkp, d_status);
   CK(cudaStreamSynchronize(st));  // h may be released by the caller
   return launch_check();
