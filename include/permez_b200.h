@@ -358,15 +358,16 @@ PMZ_API int pmz_log2_f32_batch(const float *d_x, uint64_t n, double *d_out, uint
 
 /* --- host pipeline helper ---------------------------------------------------- */
 
-/* Gather n blocks of br x bc floats out of a PINNED row-major host field (row
- * length `cols`; block i starts at row h_r0[i], column h_c0[i]) into a dense
- * device array, block i at d_dst + i * br * bc, by strided DMA copies on
- * `stream`.  The host-to-host pipeline (hostpipe.py) uploads the validation
- * blocks of sample_blocks / split_validation this way, so m
- * and the codebook exist before the field's slabs stream through the GPU.
- * Replaces nothing in the reference (numpy fancy indexing on the host). */
-PMZ_API int pmz_copy_blocks_h2d(const float *h_field, int64_t cols, int32_t br, int32_t bc, const int64_t *h_r0,
-                                const int64_t *h_c0, int64_t n, float *d_dst, void *stream);
+/* Pack n blocks of br x bc floats out of a row-major host field (row length
+ * `cols`; block i starts at row h_r0[i], column h_c0[i]) into a dense host
+ * array, block i at h_dst + i * br * bc, on `nthreads` host threads.  The
+ * host-to-host pipeline (hostpipe.py) packs the validation blocks of
+ * sample_blocks / split_validation this way into pinned
+ * memory and uploads them as one copy, so m and the codebook exist before the
+ * field's slabs are encoded.  Replaces nothing in the reference (numpy fancy
+ * indexing on the host). */
+PMZ_API int pmz_pack_blocks_host(const float *h_field, int64_t cols, int32_t br, int32_t bc, const int64_t *h_r0,
+                                 const int64_t *h_c0, int64_t n, float *h_dst, int32_t nthreads);
 
 #ifdef __cplusplus
 }

@@ -110,7 +110,7 @@ _SIGS = {
     "pmz_decompress_run": (c_int32, [VP, c_uint64, ctypes.POINTER(Header), c_double, VP, VP, VP, c_uint64, VP]),
     "pmz_decompress_np_fixups": (c_int64, [ctypes.POINTER(Header), VP, c_uint64, VP, VP, c_int64]),
     "pmz_decompress_np_apply": (c_int32, [ctypes.POINTER(Header), c_double, VP, c_uint64, VP, VP, c_int64]),
-    "pmz_copy_blocks_h2d": (c_int32, [VP, c_int64, c_int32, c_int32, VP, VP, c_int64, VP, VP]),
+    "pmz_pack_blocks_host": (c_int32, [VP, c_int64, c_int32, c_int32, VP, VP, c_int64, VP, c_int32]),
 }
 
 EXPORTS = tuple(_SIGS)

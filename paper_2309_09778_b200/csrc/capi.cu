@@ -7,6 +7,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <algorithm>
+#include <thread>
+#include <vector>
 
 #include "common.cuh"
 #include "compress.cuh"
@@ -1337,19 +1339,31 @@ int pmz_log2_f32_batch(const float *d_x, uint64_t n, double *d_out, uint32_t *d_
 }
 
 
-// Host pipeline helper (hostpipe.py): gather n blocks of br x bc floats out of
-// a pinned row-major host field (row length `cols`) into a dense device array,
-// block i at d_dst + i * br * bc, by strided DMA copies on `stream`.
-extern "C" PMZ_API int pmz_copy_blocks_h2d(const float *h_field, int64_t cols, int32_t br, int32_t bc,
-                                           const int64_t *h_r0, const int64_t *h_c0, int64_t n, float *d_dst,
-                                           void *stream) {
-  if (!h_field || !d_dst || !h_r0 || !h_c0 || cols <= 0 || br <= 0 || bc <= 0 || n < 0) return PMZ_ERR_CONFIG;
-  for (int64_t i = 0; i < n; i++) {
-    const float *src = h_field + h_r0[i] * cols + h_c0[i];
-    if (cudaMemcpy2DAsync(d_dst + i * (int64_t)br * bc, (size_t)bc * 4, src, (size_t)cols * 4, (size_t)bc * 4,
-                          (size_t)br, cudaMemcpyHostToDevice, (cudaStream_t)stream) != cudaSuccess)
-      return PMZ_ERR_CUDA;
+// Host pipeline helper (hostpipe.py): pack n blocks of br x bc floats out of a
+// row-major host field (row length `cols`) into a dense host array, block i at
+// h_dst + i * br * bc, on `nthreads` host threads.  (Strided DMA copies of the
+// same blocks run at ~22 GB/s: 1 KiB rows; packed, the blocks upload as one
+// contiguous copy while the CPU packing overlaps the first slab uploads.)
+extern "C" PMZ_API int pmz_pack_blocks_host(const float *h_field, int64_t cols, int32_t br, int32_t bc,
+                                            const int64_t *h_r0, const int64_t *h_c0, int64_t n, float *h_dst,
+                                            int32_t nthreads) {
+  if (!h_field || !h_dst || !h_r0 || !h_c0 || cols <= 0 || br <= 0 || bc <= 0 || n < 0) return PMZ_ERR_CONFIG;
+  const int T = (int)std::max<int64_t>(1, std::min<int64_t>(nthreads > 0 ? nthreads : 1, n));
+  auto work = [&](int tid) {
+    for (int64_t i = tid; i < n; i += T) {
+      const float *src = h_field + h_r0[i] * cols + h_c0[i];
+      float *dst = h_dst + i * (int64_t)br * bc;
+      for (int r = 0; r < br; r++) memcpy(dst + (int64_t)r * bc, src + (int64_t)r * cols, (size_t)bc * 4);
+    }
+  };
+  if (T == 1) {
+    work(0);
+    return PMZ_OK;
   }
+  std::vector<std::thread> th;
+  th.reserve(T);
+  for (int t = 0; t < T; t++) th.emplace_back(work, t);
+  for (auto &t : th) t.join();
   return PMZ_OK;
 }
 

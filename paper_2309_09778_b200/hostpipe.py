@@ -11,8 +11,9 @@ the larger of the two PCIe directions instead of their sum.
 
 compress: m and the codebook depend on the validation blocks of the whole
 field (select_m SPEC.md:362-370, estimate_codebook SPEC.md:389-397), so those
-blocks (sample_blocks / split_validation) are uploaded first
-by strided DMA copies (pmz_copy_blocks_h2d) into a dense column of blocks;
+blocks (sample_blocks / split_validation) are packed into
+pinned memory by host threads (pmz_pack_blocks_host) while the first slabs
+upload, and go up as one copy into a dense column of blocks;
 their coverage and final-code histograms are computed once and handed to every
 slab exactly where the multi-GPU path all-reduces them.  The container is
 byte-identical to the single-call one (tests/test_hostpipe.py).
@@ -24,6 +25,7 @@ slab is decoded into a device buffer and copied into the pinned output grid.
 from __future__ import annotations
 
 import ctypes
+import os
 
 import numpy as np
 import torch
@@ -50,7 +52,8 @@ class HostPipeline:
     of a slab of the float32 field (whole block-rows); device buffers are kept
     between calls."""
 
-    DEPTH = 3  # input slab buffers in flight (16 or 64 change nothing measurable: the copies already run back to back)
+    DEPTH = 3    # decompress: input slab buffers in flight (16 or 64 change nothing measurable)
+    DEPTH_C = 6  # compress: input slab buffers (uploads continue while the validation prologue runs)
 
     def __init__(self, codec: Codec | None = None, device=None, slab_bytes: int = 128 << 20):
         self.codec = codec or Codec(device)
@@ -126,12 +129,8 @@ class HostPipeline:
         xv = self._buf("xv", nval * br * bc * 4).view(torch.float32)
         h_r0 = np.ascontiguousarray(vr * br)
         h_c0 = np.ascontiguousarray(vc * bc)
-        check(lib.pmz_copy_blocks_h2d(ctypes.c_void_p(x2.data_ptr()), cols, br, bc,
-                                      h_r0.ctypes.data_as(ctypes.c_void_p), h_c0.ctypes.data_as(ctypes.c_void_p),
-                                      nval, _ptr(xv), _sp(self.s_in)), "copy_blocks_h2d")
-        self.last_h2d_bytes += nval * br * bc * 4
+        hv = self._pinned("hv", max(nval, 1) * br * bc, torch.float32)
         ev_val = torch.cuda.Event()
-        ev_val.record(self.s_in)
         wsz = ctypes.c_uint64(0)
         check(lib.pmz_workspace_size(ctypes.byref(p), ctypes.byref(gv), ctypes.byref(wsz)), "workspace_size")
         wsv = self._buf("wsv", wsz.value)
@@ -152,7 +151,8 @@ class HostPipeline:
             geoms.append((g, r0, r1))
         ws = self._buf("ws", ws_need)
         slab_elems = max(g.rows for g, _, _ in geoms) * cols
-        xin = [self._buf(f"xin{i}", slab_elems * 4).view(torch.float32) for i in range(self.DEPTH)]
+        depth = self.DEPTH_C
+        xin = [self._buf(f"xin{i}", slab_elems * 4).view(torch.float32) for i in range(depth)]
         outs = [self._buf(f"out{i}", cap_need) for i in range(2)]
         ev_in = [torch.cuda.Event() for _ in slabs]
         ev_cdone = [torch.cuda.Event() for _ in slabs]
@@ -160,14 +160,28 @@ class HostPipeline:
 
         def enqueue_h2d(i):
             g, r0, r1 = geoms[i]
-            if i >= self.DEPTH:
-                self.s_in.wait_event(ev_cdone[i - self.DEPTH])  # the buffer's previous slab has been encoded
+            if i >= depth:
+                self.s_in.wait_event(ev_cdone[i - depth])  # the buffer's previous slab has been encoded
             with torch.cuda.stream(self.s_in):
-                xin[i % self.DEPTH][: (r1 - r0) * cols].copy_(x2[r0:r1].reshape(-1), non_blocking=True)
+                xin[i % depth][: (r1 - r0) * cols].copy_(x2[r0:r1].reshape(-1), non_blocking=True)
             ev_in[i].record(self.s_in)
             self.last_h2d_bytes += (r1 - r0) * cols * 4
 
-        for i in range(min(self.DEPTH, len(slabs))):
+        # the first slabs start uploading; meanwhile the host packs the validation blocks into
+        # pinned memory (threads), then their one contiguous upload joins the copy queue
+        pre = min(3, len(slabs))
+        for i in range(pre):
+            enqueue_h2d(i)
+        check(lib.pmz_pack_blocks_host(ctypes.c_void_p(x2.data_ptr()), cols, br, bc,
+                                       h_r0.ctypes.data_as(ctypes.c_void_p), h_c0.ctypes.data_as(ctypes.c_void_p),
+                                       nval, ctypes.c_void_p(hv.data_ptr()), min(8, os.cpu_count() or 1)),
+              "pack_blocks_host")
+        with torch.cuda.stream(self.s_in):
+            if nval:
+                xv[: nval * br * bc].copy_(hv[: nval * br * bc], non_blocking=True)
+        ev_val.record(self.s_in)
+        self.last_h2d_bytes += nval * br * bc * 4
+        for i in range(pre, min(depth, len(slabs))):
             enqueue_h2d(i)
 
         with torch.cuda.stream(self.s_c):
@@ -201,7 +215,7 @@ class HostPipeline:
             res = N.Result()
             header_bytes = 0
             for i, (g, r0, r1) in enumerate(geoms):
-                xs = xin[i % self.DEPTH][: (r1 - r0) * cols]
+                xs = xin[i % depth][: (r1 - r0) * cols]
                 self.s_c.wait_event(ev_in[i])
                 if i >= 2:
                     self.s_c.wait_event(ev_out[i - 2])  # the output buffer has been copied out
@@ -230,8 +244,8 @@ class HostPipeline:
                 ev_out[i].record(self.s_out)
                 self.last_d2h_bytes += n
                 pos += n
-                if i + self.DEPTH < len(slabs):
-                    enqueue_h2d(i + self.DEPTH)
+                if i + depth < len(slabs):
+                    enqueue_h2d(i + depth)
                 tot["nblocks"] += int(res.nblocks)
                 tot["ntrivial"] += int(res.ntrivial)
                 tot["nbal"] += int(res.nbal)
