@@ -362,15 +362,22 @@ class HostPipeline:
             ev_in[i].record(self.s_in)
             self.last_h2d_bytes += hb + hi - lo + 8 * nb1
 
-        for i in range(len(geo)):
-            walk(i)
-            if i < self.DEPTH:
-                enqueue_h2d(i)
+        def fetch(i):  # walk slab i's records just before its upload is queued
+            try:
+                walk(i)
+            except Exception:
+                torch.cuda.synchronize(self.device)
+                raise
+            enqueue_h2d(i)
+
+        for i in range(min(self.DEPTH, len(geo))):
+            fetch(i)
         launches = 0
         res = N.Result()
         with torch.cuda.stream(self.s_c):
             sc = _sp(self.s_c)
-            for i, (hs, r0, r1, lo, hi, k0, nb1) in enumerate(plan):
+            for i in range(len(geo)):
+                hs, r0, r1, lo, hi, k0, nb1 = plan[i]
                 d, o = din[i % self.DEPTH], doff[i % self.DEPTH]
                 n = hb + hi - lo
                 y = dout[i % 2]
@@ -391,8 +398,8 @@ class HostPipeline:
                     y2[r0:r1].reshape(-1).copy_(y[: (r1 - r0) * cols], non_blocking=True)
                 ev_out[i].record(self.s_out)
                 self.last_d2h_bytes += (r1 - r0) * cols * 4
-                if i + self.DEPTH < len(plan):
-                    enqueue_h2d(i + self.DEPTH)
+                if i + self.DEPTH < len(geo):
+                    fetch(i + self.DEPTH)
         self.s_out.synchronize()
         self.last_decompress_launches = launches
         return h_out
