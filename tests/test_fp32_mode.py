@@ -55,3 +55,32 @@ def test_fp32_roundtrip_bound_and_mismatch_counts(name, shape, b_r):
     assert cm["codes"] == infos["fp64"].ncodes == infos["fp32"].ncodes
     assert cm["code_mismatches"] / cm["codes"] < 0.05, cm
     assert abs(len(bufs["fp32"]) - len(bufs["fp64"])) / len(bufs["fp64"]) < 0.05
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shape,br,bc,pr", [((2048, 1536), 256, 256, 32), ((1100, 900), 256, 256, 32),
+                                           ((700, 330), 64, 128, 16)])
+def test_fp32_container_independent_of_chain_length(shape, br, bc, pr):
+    """The FP32 sweep gives the same container whether a warp takes one
+    partition or a chain of consecutive partitions of a block (PMZ_CHAIN; the
+    size rule gives small fields 1, C5 8), and the code dump agrees too."""
+    import os
+    from paper_2309_09778_b200 import synthetic
+    codec = P.Codec("cuda:0")
+    xd = synthetic.generate("C2", shape=shape).cuda()
+    got = {}
+    for chain in ("1", "3", "8"):
+        os.environ["PMZ_CHAIN"] = chain
+        try:
+            n = codec.code_dump_numel(xd.shape, CompressConfig(block_rows=br, block_cols=bc, partition_rows=pr))
+            d = torch.full((n,), 0xFFFE, dtype=torch.int32, device="cuda").to(torch.uint16)
+            cfg = CompressConfig(rel_error=1e-2, repair_factor=1.0, block_rows=br, block_cols=bc, partition_rows=pr,
+                                 precision="fp32", code_dump=d)
+            buf, info = codec.compress_device(xd, cfg)
+            got[chain] = (buf.cpu().numpy().tobytes(), d.cpu(), info.nbal, info.nrepair)
+        finally:
+            os.environ.pop("PMZ_CHAIN", None)
+    for chain in ("3", "8"):
+        assert got[chain][0] == got["1"][0], chain
+        assert torch.equal(got[chain][1].view(torch.int16), got["1"][1].view(torch.int16)), chain
+        assert got[chain][2:] == got["1"][2:], chain

@@ -33,22 +33,29 @@ def _check_bound(x, y, bound):
 
 
 class _path:
-    """PMZ_PATH override (the library reads it at every call)."""
+    """PMZ_PATH (and PMZ_CHAIN: partitions per warp of the throughput sweep)
+    overrides; the library reads them at every call."""
 
-    def __init__(self, path):
-        self.path, self.old = path, None
+    def __init__(self, path, chain=None):
+        self.env = {"PMZ_PATH": path, "PMZ_CHAIN": chain}
+        self.old = {}
 
     def __enter__(self):
         import os
-        self.old = os.environ.get("PMZ_PATH")
-        os.environ["PMZ_PATH"] = self.path
+        for k, v in self.env.items():
+            self.old[k] = os.environ.get(k)
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
 
     def __exit__(self, *a):
         import os
-        if self.old is None:
-            os.environ.pop("PMZ_PATH", None)
-        else:
-            os.environ["PMZ_PATH"] = self.old
+        for k, v in self.old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
 
 
 def _parity(codec, oracle, x, **kw):
@@ -59,9 +66,13 @@ def _parity(codec, oracle, x, **kw):
                             partition_rows=kw.get("partition_rows", 32), m=kw.get("m", 0))
     ref, rinfo = oracle.compress(x, ocfg)
     xd = torch.from_numpy(np.ascontiguousarray(x)).cuda()
-    for path in ("latency", "throughput"):  # both compress paths (PMZ_PATH overrides the size rule)
-        with _path(path):
+    # both compress paths (PMZ_PATH overrides the size rule); the throughput sweep with one
+    # partition per warp (what the size rule gives small fields) and with chains of 3 and 8
+    # consecutive partitions per warp (what it gives C5)
+    for path, chain in (("latency", None), ("throughput", None), ("throughput", "3"), ("throughput", "8")):
+        with _path(path, chain):
             dbuf, info = codec.compress_device(xd, pcfg)
+        path = f"{path} chain={chain}"
         gpu = dbuf.cpu().numpy().tobytes()
         assert info.m == rinfo["m"], path
         assert info.nbal == rinfo["nbal"] and info.nrepair == rinfo["nrepair"], path
