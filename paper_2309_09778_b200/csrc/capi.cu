@@ -1024,7 +1024,8 @@ int pmz_decompress_run(const uint8_t *d_buf, uint64_t n, const pmz_header *hdr, 
       cudaGetDevice(&dev);
       if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
     }
-    const bool big = G.nparts >= (int64_t)sms * 2 * kDDT;
+    bool big = G.nparts >= (int64_t)sms * 2 * kDDT;
+    if (const char *e = getenv("PMZ_DEC_CTA")) big = e[0] == 'b' ? true : (e[0] == 's' ? false : big);  // tests
 #define PMZ_T_DECODE(E, T)                                                                                          \
   do {                                                                                                              \
     CK(cudaFuncSetAttribute(k_d_decode<E, T>, cudaFuncAttributeMaxDynamicSharedMemorySize,                          \

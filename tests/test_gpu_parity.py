@@ -82,10 +82,18 @@ def _parity(codec, oracle, x, **kw):
             d = np.nonzero(a[:n] != b[:n])[0]
             pytest.fail(f"{path}: container mismatch: len {a.size} vs {b.size}, first diff {d[:5]}")
     yo = oracle.decompress(ref)
-    for path in ("latency", "throughput"):  # both decoders (PMZ_PATH overrides the size rule)
-        with _path(path):
-            y = P.decompress(gpu, device="cuda:0")
-        assert np.array_equal(y.reshape(-1).view(np.uint32), yo.reshape(-1).view(np.uint32)), path
+    # both decoders (PMZ_PATH overrides the size rule); the throughput decoder with the small
+    # CTAs the size rule gives these fields and with the 512-thread CTAs it gives C5
+    import os
+    for path, cta in (("latency", None), ("throughput", "small"), ("throughput", "big")):
+        if cta:
+            os.environ["PMZ_DEC_CTA"] = cta
+        try:
+            with _path(path):
+                y = P.decompress(gpu, device="cuda:0")
+        finally:
+            os.environ.pop("PMZ_DEC_CTA", None)
+        assert np.array_equal(y.reshape(-1).view(np.uint32), yo.reshape(-1).view(np.uint32)), (path, cta)
     bound = kw.get("b_r", 1e-2) * kw.get("repair_factor", 1.5)
     _check_bound(x, y, bound)
     return info, len(gpu)
