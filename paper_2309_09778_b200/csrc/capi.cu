@@ -457,14 +457,17 @@ namespace {
 // copy already queued on the copy engine: the slab pipeline of hostpipe.py
 // synchronises per slab and would serialise on that.)
 __global__ void k_read_small(const unsigned char *src, unsigned char *dst, int n) {
-  if ((((uintptr_t)src | (uintptr_t)dst | (uintptr_t)n) & 3) == 0) {
-    for (int i = threadIdx.x; i < (n >> 2); i += blockDim.x)
-      reinterpret_cast<unsigned *>(dst)[i] = reinterpret_cast<const unsigned *>(src)[i];
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
+  if ((((uintptr_t)src | (uintptr_t)dst) & 15) == 0) {  // 16-byte words, then the tail
+    const int nq = n >> 4;
+    for (int i = tid; i < nq; i += nt) reinterpret_cast<uint4 *>(dst)[i] = reinterpret_cast<const uint4 *>(src)[i];
+    for (int i = (nq << 4) + tid; i < n; i += nt) dst[i] = src[i];
   } else {
-    for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+    for (int i = tid; i < n; i += nt) dst[i] = src[i];
   }
   __threadfence_system();
 }
+__host__ inline unsigned small_grid(size_t bytes) { return (unsigned)std::min<size_t>(32, (bytes + 4095) / 4096 + 0); }
 // (a full fix-up list: 4096 entries of 40 bytes)
 constexpr size_t kBounceBytes = 192 * 1024;
 void *small_bounce(void **dptr) {
@@ -483,8 +486,8 @@ int read_small(void *h_dst, const void *d_src, size_t bytes, cudaStream_t st) {
   void *dptr = nullptr;
   void *bounce = bytes <= kBounceBytes ? small_bounce(&dptr) : nullptr;
   if (bounce) {
-    k_read_small<<<1, 256, 0, st>>>(static_cast<const unsigned char *>(d_src), static_cast<unsigned char *>(dptr),
-                                    (int)bytes);
+    k_read_small<<<std::max(1u, small_grid(bytes)), 256, 0, st>>>(static_cast<const unsigned char *>(d_src),
+                                                                  static_cast<unsigned char *>(dptr), (int)bytes);
     if (cudaStreamSynchronize(st) != cudaSuccess) return PMZ_ERR_CUDA;
     memcpy(h_dst, bounce, bytes);
     return PMZ_OK;
@@ -501,8 +504,8 @@ int write_small(void *d_dst, const void *h_src, size_t bytes, cudaStream_t st) {
   void *bounce = bytes <= kBounceBytes ? small_bounce(&dptr) : nullptr;
   if (bounce) {
     memcpy(bounce, h_src, bytes);
-    k_read_small<<<1, 256, 0, st>>>(static_cast<const unsigned char *>(dptr), static_cast<unsigned char *>(d_dst),
-                                    (int)bytes);
+    k_read_small<<<std::max(1u, small_grid(bytes)), 256, 0, st>>>(static_cast<const unsigned char *>(dptr),
+                                                                  static_cast<unsigned char *>(d_dst), (int)bytes);
     if (cudaStreamSynchronize(st) != cudaSuccess) return PMZ_ERR_CUDA;
     return PMZ_OK;
   }

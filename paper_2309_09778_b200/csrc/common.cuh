@@ -2,12 +2,20 @@
 // quantizer, workspace layout.
 #pragma once
 #include <cstdint>
+#ifndef PMZ_UNR_C
+#define PMZ_UNR_C 2
+#endif
+#ifndef PMZ_UNR_D
+#define PMZ_UNR_D 1
+#endif
 #include <type_traits>
 #include <cuda_runtime.h>
 #include "../../include/permez_b200.h"
 #include "dmath.cuh"
 
 namespace pmz {
+constexpr int kUnrC = PMZ_UNR_C, kUnrD = PMZ_UNR_D;  // unroll factors of the sweep bodies (A/B builds)
+
 
 constexpr int kMaxAlpha = 1 << 16;
 constexpr int kWarps = 4;  // warps per CTA for per-partition kernels

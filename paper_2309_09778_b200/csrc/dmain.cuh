@@ -481,7 +481,7 @@ __global__ void __launch_bounds__(kDRW * 32, 3)
     cnext = ld_codes((t0 >> 3) + 1);
     __syncwarp();
     const int t1 = min(nsteps, t0 + 8);
-#pragma unroll 2
+#pragma unroll kUnrD
     for (int t = t0; t < t1; t++) {
       const int c = t - lane;
       const bool started = c >= 0;
@@ -654,7 +654,7 @@ __global__ void __launch_bounds__(kDRW * 32, 3)
     cnext = ld_codes((t0 >> 3) + 1);
     __syncwarp();
     const int t1 = min(nsteps, t0 + 8);
-#pragma unroll 2
+#pragma unroll kUnrD
     for (int t = t0; t < t1; t++) {
       const int c = t - lane;
       const bool started = c >= 0;
