@@ -425,11 +425,11 @@ def main():
         if sharded:
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
         e2e_c = {"value": bytes_all / (float(et[0]) / 1e3) / 1e9, "unit": "GB/s", "ms_per_step": float(et[0]),
-                 "h2d_bytes_per_step": int(bi), "d2h_bytes_per_step": int(bo),
+                 "ms_each": [round(v, 2) for v in e_ms], "h2d_bytes_per_step": int(bi), "d2h_bytes_per_step": int(bo),
                  "api": "HostPipeline.compress: pinned host field -> pinned host container, slabs of whole "
                         "block-rows, copies overlapped with the kernels; container identical to the device call"}
         e2e_d = {"value": bytes_all / (float(et[1]) / 1e3) / 1e9, "unit": "GB/s", "ms_per_step": float(et[1]),
-                 "h2d_bytes_per_step": int(di), "d2h_bytes_per_step": int(do_),
+                 "ms_each": [round(v, 2) for v in ed_ms], "h2d_bytes_per_step": int(di), "d2h_bytes_per_step": int(do_),
                  "api": "HostPipeline.decompress: pinned host container -> pinned host grid (block index walk "
                         "on the host, slabs, copies overlapped); grid identical to the device call"}
         del h_in, h_out, h_y

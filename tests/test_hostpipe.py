@@ -145,3 +145,24 @@ def test_slab_pipeline_c3_full_size():
     assert (info.m, info.nbal, info.nrepair, info.ncodes) == (rinfo.m, rinfo.nbal, rinfo.nrepair, rinfo.ncodes)
     y = pipe.decompress(h_out[:n])
     assert torch.equal(y.view(torch.int32), y_ref.view(torch.int32))
+
+
+def test_decompress_shard_of_a_container():
+    """HostPipeline.decompress(shard_rows=...): header + the records of one
+    shard of whole block-rows (what a rank of a sharded run holds) decode to
+    that shard's rows of the full decode."""
+    import paper_2309_09778_b200 as P
+    from paper_2309_09778_b200 import synthetic
+    x = synthetic.generate("C2", shape=(2048, 1024)).contiguous()
+    codec = P.Codec("cuda:0")
+    buf, _ = codec.compress_device(x.cuda(), P.CompressConfig(rel_error=1e-2, repair_factor=1.0))
+    full = buf.cpu().numpy()
+    h = P.Codec.parse_header(full)
+    offs = P.Codec.index_blocks(full, h)
+    y_full = P.decompress(full.tobytes(), device="cuda:0")
+    nbc, hb = 4, int(h.header_bytes)
+    pipe = P.HostPipeline(codec, slab_bytes=256 * 1024 * 4)  # slabs of one block-row
+    for br0, br1 in ((0, 3), (3, 8)):  # two shards: block-rows [0, 3) and [3, 8)
+        part = np.concatenate([full[:hb], full[int(offs[br0 * nbc]): int(offs[br1 * nbc])]])
+        y = pipe.decompress(_pin(torch.from_numpy(part)), shard_rows=(br1 - br0) * 256)
+        assert np.array_equal(y.numpy().view(np.uint32), y_full[br0 * 256: br1 * 256].view(np.uint32))
