@@ -5,6 +5,9 @@
 #ifndef PMZ_UNR_C
 #define PMZ_UNR_C 2
 #endif
+#ifndef PMZ_DREC_MINB
+#define PMZ_DREC_MINB 3
+#endif
 #ifndef PMZ_UNR_D
 #define PMZ_UNR_D 1
 #endif

@@ -368,7 +368,7 @@ __device__ __forceinline__ float d_exp2_f32(double y, unsigned tab_s, unsigned *
 }
 
 template <int PK>
-__global__ void __launch_bounds__(kDRW * 32, 3)
+__global__ void __launch_bounds__(kDRW * 32, PMZ_DREC_MINB)
     k_d_recon(const uint8_t *__restrict__ buf, unsigned long long buf_n, Geom g, const __grid_constant__ KParams k,
               const BlkP *__restrict__ blkp, const uint16_t *__restrict__ codes, const unsigned *__restrict__ part_z,
               const unsigned *__restrict__ rowz, const double *__restrict__ anchors,
@@ -541,7 +541,7 @@ __global__ void __launch_bounds__(kDRW * 32, 3)
 // and anchors are the encoder's float32 values stored as doubles; the output
 // is inverse_map((double)vhat) exactly as the encoder's bound check saw it.
 template <int PK>
-__global__ void __launch_bounds__(kDRW * 32, 3)
+__global__ void __launch_bounds__(kDRW * 32, PMZ_DREC_MINB)
     k_d_recon32(const uint8_t *__restrict__ buf, unsigned long long buf_n, Geom g, const __grid_constant__ KParams k,
               const BlkP *__restrict__ blkp, const uint16_t *__restrict__ codes, const unsigned *__restrict__ part_z,
               const unsigned *__restrict__ rowz, const double *__restrict__ anchors,
