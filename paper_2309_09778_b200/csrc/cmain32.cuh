@@ -274,7 +274,7 @@ __global__ void __launch_bounds__(kCW * 32, 2)
 #pragma unroll 1
         for (int t = t0; t < t1; t++) step(t, std::true_type{});
       } else {
-#pragma unroll kUnrC
+#pragma unroll kUnrC32
         for (int t = t0; t < t1; t++) step(t, std::false_type{});
       }
     }

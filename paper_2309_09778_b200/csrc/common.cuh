@@ -8,6 +8,9 @@
 #ifndef PMZ_DREC_MINB
 #define PMZ_DREC_MINB 3
 #endif
+#ifndef PMZ_UNR_C32
+#define PMZ_UNR_C32 4
+#endif
 #ifndef PMZ_UNR_D
 #define PMZ_UNR_D 1
 #endif
@@ -17,7 +20,7 @@
 #include "dmath.cuh"
 
 namespace pmz {
-constexpr int kUnrC = PMZ_UNR_C, kUnrD = PMZ_UNR_D;  // unroll factors of the sweep bodies (A/B builds)
+constexpr int kUnrC = PMZ_UNR_C, kUnrC32 = PMZ_UNR_C32, kUnrD = PMZ_UNR_D;  // unroll factors of the sweep bodies (A/B builds)
 
 
 constexpr int kMaxAlpha = 1 << 16;
